@@ -1,0 +1,176 @@
+/*
+ * meshloop_b200.h — C ABI of libmeshloop_b200.so, the B200 execution backend
+ * for the OP2-style op_par_loop abstraction of arXiv:1403.7209.
+ *
+ * The reference (`meshloop`, pure Python + numpy, /root/reference/pkg) has no
+ * FFI: its "plugin interface" for this path is the loop descriptor + kernel
+ * callback contract and the closed backend switch of run_program.  Each entry
+ * point below replaces one reference function on the hot path; the citation
+ * is `pkg/src/meshloop/<file>:<line>`.  INTEGRATION.md shows the ctypes stub
+ * a maintainer would add to meshloop to bind them.
+ *
+ * Conventions
+ *   - every function returns 0 on success or a negative ML_E* code; the
+ *     message is available from ml_last_error() (thread-local);
+ *   - no C++ exceptions cross the ABI; plain pointers and sizes only;
+ *   - host pointers are borrowed for the duration of a call;
+ *   - device memory is owned by the library (ml_alloc/ml_free);
+ *   - all device work is enqueued on the library's compute stream of the
+ *     current device; ml_synchronize() waits for it.
+ */
+#ifndef MESHLOOP_B200_H
+#define MESHLOOP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes -------------------------------------------------------- */
+#define ML_OK          0
+#define ML_EINVAL     -1   /* bad argument / signature mismatch             */
+#define ML_ECUDA      -2   /* CUDA runtime error                            */
+#define ML_ENOMEM     -3   /* allocation failed                             */
+#define ML_ENOFUNCTOR -4   /* no compiled functor of that name/dtype        */
+#define ML_ENCCL      -5   /* NCCL error / exchange timeout                 */
+
+/* ---- argument descriptors (core.py:223-254, 50-71) ----------------------- */
+enum { ML_DIRECT = 0, ML_INDIRECT = 1, ML_GLOBAL = 2 };
+enum { ML_READ = 0, ML_WRITE = 1, ML_RW = 2, ML_INC = 3, ML_MIN = 4, ML_MAX = 5 };
+enum { ML_F64 = 0, ML_I64 = 1 };
+enum { ML_AOS = 0, ML_SOA = 1 };
+
+typedef struct ml_arg {
+    int32_t kind;          /* ML_DIRECT / ML_INDIRECT / ML_GLOBAL                 */
+    int32_t mode;          /* ML_READ .. ML_MAX                                   */
+    int32_t dim;           /* components per element (global: buffer length)      */
+    int32_t dtype;         /* ML_F64 / ML_I64                                     */
+    int32_t layout;        /* ML_AOS / ML_SOA (dat args)                          */
+    int32_t slot;          /* 0-based map column (indirect args)                  */
+    void *data;            /* device payload of the dat, or device global buffer  */
+    const int32_t *map;    /* device map table, column-major int32 [arity][from]  */
+    int64_t map_from;      /* from-set size of the map (column stride)            */
+    int64_t set_size;      /* size of the dat's set (SOA component stride)        */
+} ml_arg_t;
+
+/* Device copy of an execution plan (plan.py:30-45).  `color_offsets` is a
+ * HOST array; the rest are device arrays produced by ml_plan_* below. */
+typedef struct ml_plan_dev {
+    int64_t nblocks;
+    int64_t ncolors;
+    int64_t block_size;
+    const int64_t *color_offsets;   /* host [ncolors+1] into `blocks`           */
+    const int32_t *blocks;          /* device: block ids ordered by colour      */
+    const uint16_t *elem_color;     /* device [n]; NULL when no indirect writes */
+    const int32_t *elem_ncolors;    /* device [nblocks]; NULL likewise          */
+} ml_plan_dev_t;
+
+typedef struct ml_loop {
+    const char *name;               /* for error messages                       */
+    int32_t functor;                /* id from ml_functor_lookup                */
+    int32_t nargs;
+    const ml_arg_t *args;
+    int64_t n;                      /* iteration-set size                       */
+    ml_plan_dev_t plan;
+    double fconst[4];               /* kernel constants (e.g. dt)               */
+    int64_t iconst[4];              /* kernel constants (e.g. integer scale)    */
+    void *scratch;                  /* device scratch >= ml_loop_scratch_bytes  */
+} ml_loop_t;
+
+typedef struct ml_device_info {
+    char name[128];
+    int32_t sm_count;
+    int32_t cc_major, cc_minor;
+    int64_t l2_bytes;
+    int64_t hbm_bytes;
+} ml_device_info_t;
+
+/* ---- runtime --------------------------------------------------------------
+ * Replaces the reference's execution context: the worker pool of
+ * executor.py:720 (threads) / the rank threads of executor.py:641-647. */
+const char *ml_last_error(void);
+int ml_version(void);
+int ml_init(int device);                               /* select device, create streams */
+int ml_device_info(ml_device_info_t *out);
+int ml_synchronize(void);
+
+/* ---- memory: framework-owned dat payloads (core.py:131-168) -------------- */
+int ml_alloc(uint64_t bytes, void **dptr);
+int ml_free(void *dptr);
+int ml_host_alloc(uint64_t bytes, void **hptr);        /* pinned host staging    */
+int ml_host_free(void *hptr);
+int ml_upload(void *dst, const void *src, uint64_t bytes);    /* H2D, stream-ordered */
+int ml_download(void *dst, const void *src, uint64_t bytes);  /* D2H, synchronous    */
+int ml_memset(void *dst, int value, uint64_t bytes);
+/* Upload an int64 0-based (rows, arity) row-major map table as the device's
+ * int32 column-major layout (core.py:362-387 stores int64 row-major). */
+int ml_map_upload(int32_t *dst, const int64_t *table, int64_t rows, int32_t arity);
+
+/* ---- execution plan: plan.py:55-131 (build_plan), bit-exact -------------
+ * `cols[j]` is the target column (0-based ids, length n) of the j-th
+ * indirect WRITE/RW/INC argument; `col_key[j]` identifies its dat (targets
+ * of different keys never conflict; see the offset quirk at plan.py:77-81). */
+typedef struct ml_plan ml_plan_t;
+int ml_plan_build(int64_t n, int32_t ncols, const int64_t *const *cols,
+                  const int32_t *col_key, int64_t block_size, ml_plan_t **out);
+int ml_plan_sizes(const ml_plan_t *p, int64_t *nblocks, int64_t *ncolors,
+                  int64_t *max_elem_colors);
+/* Any output pointer may be NULL.  Sizes: block_color/elem_ncolors [nblocks],
+ * color_offsets [ncolors+1], blocks_by_color [nblocks], elem_color and
+ * block_elem_order [n] (block_elem_order flattened, plan.py:126-129). */
+int ml_plan_export(const ml_plan_t *p, int64_t *block_color, int64_t *elem_ncolors,
+                   int64_t *color_offsets, int64_t *blocks_by_color,
+                   int64_t *elem_color, int64_t *block_elem_order);
+int ml_plan_free(ml_plan_t *p);
+
+/* ---- renumbering: renumber.py:53-128 ------------------------------------- */
+/* Co-occurrence adjacency of a set from `nmaps` tables that target it
+ * (renumber.py:53-81).  Two-phase: pass indices==NULL to get *nnz. */
+int ml_co_occurrence(int64_t n, int32_t nmaps, const int64_t *const *tables,
+                     const int64_t *rows, const int32_t *arity,
+                     int64_t *indptr, int64_t *indices, int64_t *nnz);
+/* Cuthill–McKee order over CSR adjacency (renumber.py:84-119, not reversed). */
+int ml_cm_order(int64_t n, const int64_t *indptr, const int64_t *indices, int64_t *order);
+
+/* ---- loop execution: executor.py:206-275 (run_serial/_threads_loop) ------ */
+/* Look up a compiled device functor by name and element type. */
+int ml_functor_lookup(const char *name, int32_t dtype, int32_t *functor_id);
+/* Compile-time signature of a functor, for validation against a Loop. */
+int ml_functor_signature(int32_t functor_id, int32_t *nargs, int32_t *kinds,
+                         int32_t *modes, int32_t *dims, int32_t *dtypes);
+int ml_functor_count(int32_t *count);
+int ml_functor_name(int32_t functor_id, char *buf, int32_t buflen, int32_t *dtype);
+/* Device scratch a loop needs (global-reduction partials). */
+int ml_loop_scratch_bytes(const ml_loop_t *loop, uint64_t *bytes);
+/* Enqueue one loop: coloured launches + deterministic reduction combine. */
+int ml_loop_run(const ml_loop_t *loop);
+
+/* ---- programs: run_program (executor.py:707-729) as one native object ----
+ * The loop list is copied.  Running replays it (optionally as a CUDA graph)
+ * with global initial values uploaded from / results downloaded to the
+ * pinned staging buffer `globals_host` ([globals_bytes]) mirrored at
+ * `globals_dev`.  Timings: per-loop device milliseconds of the last
+ * non-graph run. */
+typedef struct ml_program ml_program_t;
+int ml_program_create(const ml_loop_t *loops, int32_t nloops, void *globals_host,
+                      void *globals_dev, uint64_t globals_bytes, ml_program_t **out);
+int ml_program_run(ml_program_t *p, int32_t use_graph, int32_t time_loops);
+/* Launch the program's CUDA graph `count` times back to back, no host sync
+ * between replays (device-throughput measurement); syncs at the end. */
+int ml_program_replay(ml_program_t *p, int32_t count);
+int ml_program_loop_times(const ml_program_t *p, float *ms);
+int ml_program_free(ml_program_t *p);
+
+/* ---- measurement helpers -------------------------------------------------- */
+int ml_flush_l2(void);                                 /* write a buffer > L2       */
+typedef struct ml_timer ml_timer_t;
+int ml_timer_create(ml_timer_t **t);
+int ml_timer_start(ml_timer_t *t);                     /* event on compute stream   */
+int ml_timer_stop(ml_timer_t *t, float *ms);           /* event + sync + elapsed    */
+int ml_timer_free(ml_timer_t *t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MESHLOOP_B200_H */

@@ -1,0 +1,230 @@
+"""Vectorised oracle for the bundled app kernels (TEST ORACLE ONLY).
+
+Each function reproduces, with numpy, *exactly* what the per-element
+executor (:mod:`oracle.serial`, i.e. reference ``run_serial``) computes for
+one functor — including float64 rounding:
+
+* per-element arithmetic is written as the same expression tree as the
+  Python kernel (numpy elementwise float64 ops are the same IEEE ops);
+* increments reach each target in the serial order (ascending element,
+  then statement order inside the kernel) because ``np.add.at`` is applied
+  to indices interleaved element-major;
+* global INC reductions are the sequential left fold
+  ``init + x_0 + x_1 + ...`` (``np.cumsum`` accumulates sequentially);
+* indirect WRITE conflicts keep the last writer, as serial order does.
+
+This lets tests check the GPU at full benchmark size in seconds.  The
+bit-identity of ``bulk`` and ``serial`` is itself tested on small meshes.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["run_program", "run_loop", "SUPPORTED"]
+
+
+def _vals(d):
+    flat = d.data
+    n = d.set.size
+    return flat.reshape(n, d.dim) if d.layout.name == "AOS" else flat.reshape(d.dim, n).T
+
+
+def _tgt(a):
+    return a.map.table[:, a.slot]
+
+
+def _gather(a):
+    return _vals(a.dat)[_tgt(a)]
+
+
+def _inc_serial(view, idx_list, val_list):
+    """Apply per-element increments in serial order; idx/val per INC statement."""
+    idx = np.stack(idx_list, 1).reshape(-1)
+    val = np.stack(val_list, 1).reshape(idx.size, -1)
+    for c in range(view.shape[1]):
+        np.add.at(view[:, c], idx, val[:, c])
+
+
+def _write_serial(view, idx_list, val_list):
+    idx = np.stack(idx_list, 1).reshape(-1)
+    val = np.stack(val_list, 1).reshape(idx.size, -1)
+    if idx.size == 0:
+        return
+    _, first_rev = np.unique(idx[::-1], return_index=True)
+    last = idx.size - 1 - first_rev
+    view[idx[last]] = val[last]
+
+
+def _seq_sum(init, terms):
+    terms = np.asarray(terms).reshape(-1)
+    if terms.size == 0:
+        return init
+    return np.cumsum(np.concatenate([np.atleast_1d(init), terms]))[-1]
+
+
+# -- kernels -----------------------------------------------------------------
+
+def _copy(loop, c):
+    src, dst = loop.args
+    _vals(dst.dat)[:, 0] = _vals(src.dat)[:, 0]
+
+
+def _edge_flux(loop, c):
+    u1, u2, f1, f2 = loop.args
+    d = _gather(u2)[:, 0] - _gather(u1)[:, 0]
+    _inc_serial(_vals(f1.dat), [_tgt(f1), _tgt(f2)], [d[:, None], -d[:, None]])
+
+
+def _diffusion_update(loop, c):
+    u, up, f, res = loop.args
+    fv = _vals(f.dat)[:, 0].copy()
+    if fv.dtype.kind == "f":
+        (dt,) = c.fconsts
+        nu = _vals(up.dat)[:, 0] + dt * fv
+        res.glob.buffer[0] = _seq_sum(res.glob.buffer[0], fv * fv)
+        _vals(f.dat)[:, 0] = 0.0
+    else:
+        (scale,) = c.iconsts
+        nu = _vals(up.dat)[:, 0] + fv // scale
+        res.glob.buffer[0] = res.glob.buffer[0] + np.abs(fv).sum()
+        _vals(f.dat)[:, 0] = 0
+    _vals(u.dat)[:, 0] = nu
+
+
+def _boundary_fix(loop, c):
+    u1, u2, g1, g2 = loop.args
+    _write_serial(_vals(u1.dat), [_tgt(u1), _tgt(u2)], [_gather(g1), _gather(g2)])
+
+
+def _tri_area(loop, c):
+    c1, c2, c3, out = (_gather(a) if a.kind == "indirect" else a for a in loop.args)
+    area = 0.5 * np.abs((c2[:, 0] - c1[:, 0]) * (c3[:, 1] - c1[:, 1])
+                        - (c3[:, 0] - c1[:, 0]) * (c2[:, 1] - c1[:, 1]))
+    _vals(out.dat)[:, 0] = area
+
+
+def _distribute(loop, c):
+    ac, a1, a2, a3 = loop.args
+    v = _vals(ac.dat)[:, 0]
+    third = v / 3.0 if v.dtype.kind == "f" else v // 3
+    _inc_serial(_vals(a1.dat), [_tgt(a1), _tgt(a2), _tgt(a3)],
+                [third[:, None]] * 3)
+
+
+def _sum(loop, c):
+    v, total = loop.args
+    x = _vals(v.dat)[:, 0]
+    if x.dtype.kind == "f":
+        total.glob.buffer[0] = _seq_sum(total.glob.buffer[0], x)
+    else:
+        total.glob.buffer[0] = total.glob.buffer[0] + x.sum()
+
+
+def _proxy_save(loop, c):
+    q, q_old = loop.args
+    _vals(q_old.dat)[:] = _vals(q.dat)
+
+
+def _proxy_dt(loop, c):
+    q, vol, dt_loc, dt_min = loop.args
+    (cfl,) = c.fconsts
+    qv = _vals(q.dat)
+    s = np.ones(qv.shape[0])
+    for v in range(qv.shape[1]):
+        s = s + np.abs(qv[:, v])
+    d = cfl * _vals(vol.dat)[:, 0] / s
+    _vals(dt_loc.dat)[:, 0] = d
+    if d.size:
+        dt_min.glob.buffer[0] = min(dt_min.glob.buffer[0], d.min())
+
+
+def _proxy_grad(loop, c):
+    w, q1, q2, x1, x2, g1, g2 = loop.args
+    W, Q1, Q2, X1, X2 = _vals(w.dat), _gather(q1), _gather(q2), _gather(x1), _gather(x2)
+    nq = Q1.shape[1]
+    F = np.empty((W.shape[0], 3 * nq))
+    for v in range(nq):
+        qa = 0.5 * (Q1[:, v] + Q2[:, v])
+        dq = Q2[:, v] - Q1[:, v]
+        for k in range(3):
+            F[:, 3 * v + k] = qa * W[:, k] + 0.125 * dq * (X2[:, k] - X1[:, k])
+    _inc_serial(_vals(g1.dat), [_tgt(g1), _tgt(g2)], [F, -F])
+
+
+def _proxy_iflux(loop, c):
+    w, q1, q2, x1, x2, l1, l2, r1, r2 = loop.args
+    W, Q1, Q2, X1, X2 = _vals(w.dat), _gather(q1), _gather(q2), _gather(x1), _gather(x2)
+    L1, L2 = _gather(l1), _gather(l2)
+    d0, d1, d2 = X2[:, 0] - X1[:, 0], X2[:, 1] - X1[:, 1], X2[:, 2] - X1[:, 2]
+    ds = np.sqrt(d0 * d0 + d1 * d1 + d2 * d2)
+    an = np.sqrt(W[:, 0] * W[:, 0] + W[:, 1] * W[:, 1] + W[:, 2] * W[:, 2])
+    s = np.zeros(W.shape[0])
+    for j in range(L1.shape[1]):
+        t = L1[:, j] + L2[:, j]
+        s = s + t * t
+    lam = an / ((1.0 + ds) * (1.0 + 0.0625 * s))
+    F = lam[:, None] * (Q2 - Q1)
+    _inc_serial(_vals(r1.dat), [_tgt(r1), _tgt(r2)], [F, -F])
+
+
+def _proxy_vflux(loop, c):
+    w, q1, q2, g1, g2, x1, x2, a1, a2, r1, r2 = loop.args
+    W, Q1, Q2, X1, X2 = _vals(w.dat), _gather(q1), _gather(q2), _gather(x1), _gather(x2)
+    G1, G2, A1, A2 = _gather(g1), _gather(g2), _gather(a1), _gather(a2)
+    d0, d1, d2 = X2[:, 0] - X1[:, 0], X2[:, 1] - X1[:, 1], X2[:, 2] - X1[:, 2]
+    ds2 = d0 * d0 + d1 * d1 + d2 * d2 + 1e-12
+    wd = W[:, 0] * d0 + W[:, 1] * d1 + W[:, 2] * d2
+    naux = A1.shape[1]
+    mu = np.zeros(W.shape[0])
+    for j in range(naux):
+        mu = mu + (A1[:, j] + A2[:, j])
+    mu = 0.01 * mu / (2.0 * naux)
+    nq = Q1.shape[1]
+    F = np.empty((W.shape[0], nq))
+    for v in range(nq):
+        b = 3 * v
+        gx = 0.5 * (G1[:, b] + G2[:, b])
+        gy = 0.5 * (G1[:, b + 1] + G2[:, b + 1])
+        gz = 0.5 * (G1[:, b + 2] + G2[:, b + 2])
+        dq = Q2[:, v] - Q1[:, v]
+        corr = (dq - (gx * d0 + gy * d1 + gz * d2)) / ds2
+        F[:, v] = mu * (0.001 * (gx * W[:, 0] + gy * W[:, 1] + gz * W[:, 2]) + corr * np.abs(wd))
+    _inc_serial(_vals(r1.dat), [_tgt(r1), _tgt(r2)], [F, -F])
+
+
+def _proxy_update(loop, c):
+    q, q_old, res, vol, grad, dt_min, rms = loop.args
+    R = _vals(res.dat).copy()
+    s = dt_min.glob.buffer[0] / _vals(vol.dat)[:, 0]
+    _vals(q.dat)[:] = _vals(q_old.dat) + s[:, None] * R
+    rms.glob.buffer[0] = _seq_sum(rms.glob.buffer[0], R * R)     # (e, v) row-major order
+    _vals(res.dat)[:] = 0.0
+    _vals(grad.dat)[:] = 0.0
+
+
+def _proxy_bc(loop, c):
+    q1, q2, b1, b2 = loop.args
+    _write_serial(_vals(q1.dat), [_tgt(q1), _tgt(q2)], [_gather(b1), _gather(b2)])
+
+
+SUPPORTED = {
+    "copy": _copy, "edge_flux": _edge_flux, "diffusion_update": _diffusion_update,
+    "boundary_fix": _boundary_fix, "tri_area": _tri_area, "distribute": _distribute,
+    "distribute_int": _distribute, "sum": _sum,
+    "proxy_save": _proxy_save, "proxy_dt": _proxy_dt, "proxy_grad": _proxy_grad,
+    "proxy_iflux": _proxy_iflux, "proxy_vflux": _proxy_vflux,
+    "proxy_update": _proxy_update, "proxy_bc": _proxy_bc,
+}
+
+
+def run_loop(loop, binding) -> None:
+    """``binding``: object with ``functor``, ``fconsts``, ``iconsts``."""
+    if loop.iter_set.size == 0:
+        return
+    SUPPORTED[binding.functor](loop, binding)
+
+
+def run_program(program, resolve) -> None:
+    """``resolve(kernel) -> binding`` (e.g. the product's kernel registry)."""
+    for loop in program:
+        run_loop(loop, resolve(loop.kernel))

@@ -1,0 +1,367 @@
+// Loop engine: one templated CUDA kernel family per loop *shape*, specialised
+// at compile time for each hand-written functor (the B200 counterpart of the
+// per-loop code OP2 generates; reference execution semantics executor.py:
+// 149-275, plan consumption plan.py:30-45).
+//
+// A functor declares its argument signature (kind, access mode, dim, type)
+// and a device `apply(consts, view0, view1, ...)`.  Views are
+//   * Ref<T>/Ref<const T>  — strided references straight into HBM for
+//     direct args, indirect READ args and (phased mode) indirect WRITE/RW
+//     args; loads are issued at first use, so the compiler schedules them
+//     and register pressure stays bounded for wide dats;
+//   * T*                   — a register array: increments of an indirect INC
+//     argument (applied colour by colour after the element is computed) and
+//     global INC/MIN/MAX accumulators (block-reduced afterwards).
+//
+// Kernels
+//   k_direct  — loops without indirect writes: one launch over all plan
+//               blocks, per-block reduction partials.
+//   k_staged  — loops whose only indirect writes are INC and bs <= blockDim:
+//               every thread computes its element at once, then element
+//               colour phases (separated by __syncthreads) apply the
+//               register increments with plain read-modify-write.  One
+//               launch per block colour; blocks of one colour share no
+//               target, so no atomics are needed and the result is
+//               deterministic run to run.
+//   k_phased  — general case (indirect WRITE/RW, or bs > blockDim): each
+//               element executes entirely inside its colour phase.
+// Global reductions: warp shuffle -> shared -> one partial per plan block;
+// k_combine folds the partials in a fixed order onto the initial value.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cuda/std/limits>
+#include <cuda/std/tuple>
+#include <cuda/std/utility>
+
+namespace ml {
+
+enum : int { KD = 0, KI = 1, KG = 2 };                        // direct / indirect / global
+enum : int { MR = 0, MW = 1, MRW = 2, MINC = 3, MMIN = 4, MMAX = 5 };
+constexpr int MAX_ARGS = 16;
+
+template <int K, int M, int DIM, class T>
+struct Arg {
+    static constexpr int kind = K, mode = M, dim = DIM;
+    using type = T;
+};
+
+template <class... As>
+struct Sig {
+    static constexpr int n = sizeof...(As);
+};
+
+template <class T>
+constexpr int type_code() { return sizeof(T) == 8 && T(0.5) != T(0) ? 0 : 1; }   // 0 f64, 1 i64
+
+struct ArgRt {
+    void *data;
+    const int32_t *map;   // map column (already offset by slot*from)
+    int64_t se, sc;       // element stride, component stride (in elements)
+};
+
+struct Consts {
+    double f[4];
+    int64_t i[4];
+};
+
+struct LaunchParams {
+    ArgRt a[MAX_ARGS];
+    void *part[MAX_ARGS];       // reduction partials [nblocks][dim] per global reduce arg
+    int64_t n;
+    int32_t bs;
+    const int32_t *blocks;      // block ids of this launch (nullptr: identity)
+    const uint16_t *ecol;       // element colours
+    const int32_t *encol;       // per-block element colour count
+    Consts k;
+};
+
+// strided view of one element's components
+template <class T>
+struct Ref {
+    T *p;
+    int64_t sc;
+    __device__ __forceinline__ T &operator[](int c) const { return p[c * sc]; }
+};
+
+template <class T, int M>
+__device__ __forceinline__ T reduce_identity() {
+    if (M == MMIN) return cuda::std::numeric_limits<T>::has_infinity
+                              ? cuda::std::numeric_limits<T>::infinity()
+                              : cuda::std::numeric_limits<T>::max();
+    if (M == MMAX) return cuda::std::numeric_limits<T>::has_infinity
+                              ? -cuda::std::numeric_limits<T>::infinity()
+                              : cuda::std::numeric_limits<T>::lowest();
+    return T(0);
+}
+
+template <int M, class T>
+__device__ __forceinline__ T combine(T a, T b) {
+    if (M == MMIN) return b < a ? b : a;
+    if (M == MMAX) return b > a ? b : a;
+    return a + b;
+}
+
+// ---- per-argument slot --------------------------------------------------------
+template <class A, bool STAGE_INC>
+struct Slot {
+    using T = typename A::type;
+    static constexpr bool is_global = A::kind == KG;
+    static constexpr bool is_reduce = is_global && A::mode != MR;
+    static constexpr bool staged = (A::kind == KI && A::mode == MINC && STAGE_INC) || is_reduce;
+
+    T acc[staged ? A::dim : 1];
+    T *ptr;          // element base pointer (non-staged dat / global READ)
+    int64_t sc;
+
+    __device__ __forceinline__ void init_global(const LaunchParams &p, int i) {
+        if constexpr (is_reduce) {
+#pragma unroll
+            for (int c = 0; c < A::dim; ++c) acc[c] = reduce_identity<T, A::mode>();
+        } else if constexpr (is_global) {
+            ptr = static_cast<T *>(p.a[i].data);
+            sc = 1;
+        }
+    }
+    __device__ __forceinline__ void init_elem(const LaunchParams &p, int i, int64_t e) {
+        if constexpr (!is_global) {
+            const ArgRt &r = p.a[i];
+            const int64_t t = A::kind == KI ? int64_t(__ldg(r.map + e)) : e;
+            ptr = static_cast<T *>(r.data) + t * r.se;
+            sc = r.sc;
+            if constexpr (staged) {
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
+            }
+        }
+    }
+    __device__ __forceinline__ auto view() {
+        if constexpr (staged) {
+            return static_cast<T *>(acc);
+        } else if constexpr (A::mode == MR) {
+            return Ref<const T>{ptr, sc};
+        } else {
+            return Ref<T>{ptr, sc};
+        }
+    }
+    __device__ __forceinline__ void apply_staged() {
+        if constexpr (staged && !is_global) {
+#pragma unroll
+            for (int c = 0; c < A::dim; ++c) ptr[c * sc] += acc[c];
+        }
+    }
+};
+
+template <class T, int M>
+__device__ __forceinline__ T block_reduce(T v, T *smem_t) {
+    // warp shuffle, then warp leaders through shared memory
+    const unsigned full = 0xffffffffu;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = combine<M>(v, __shfl_down_sync(full, v, o));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (lane == 0) smem_t[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < nw ? smem_t[lane] : reduce_identity<T, M>();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = combine<M>(v, __shfl_down_sync(full, v, o));
+    }
+    return v;   // valid in thread 0
+}
+
+template <class F, bool STAGE_INC, class... As>
+struct Engine {
+    using Slots = cuda::std::tuple<Slot<As, STAGE_INC>...>;
+    static constexpr int N = sizeof...(As);
+
+    template <size_t... Is>
+    __device__ __forceinline__ static void init_globals(Slots &s, const LaunchParams &p,
+                                                        cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).init_global(p, int(Is)), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void init_elem(Slots &s, const LaunchParams &p, int64_t e,
+                                                     cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).init_elem(p, int(Is), e), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void call(Slots &s, const LaunchParams &p,
+                                                cuda::std::index_sequence<Is...>) {
+        F::apply(p.k, cuda::std::get<Is>(s).view()...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void apply_staged(Slots &s, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).apply_staged(), ...);
+    }
+    template <size_t I>
+    __device__ __forceinline__ static void reduce_one(Slots &s, const LaunchParams &p, int32_t b,
+                                                      double *smem) {
+        using S = cuda::std::tuple_element_t<I, Slots>;
+        if constexpr (S::is_reduce) {
+            using T = typename S::T;
+            constexpr int M = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>::mode;
+            constexpr int D = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>::dim;
+#pragma unroll 1
+            for (int c = 0; c < D; ++c) {
+                T v = block_reduce<T, M>(cuda::std::get<I>(s).acc[c], reinterpret_cast<T *>(smem));
+                if (threadIdx.x == 0) static_cast<T *>(p.part[I])[int64_t(b) * D + c] = v;
+            }
+        }
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void reduce_all(Slots &s, const LaunchParams &p, int32_t b,
+                                                      double *smem, cuda::std::index_sequence<Is...>) {
+        (reduce_one<Is>(s, p, b, smem), ...);
+    }
+    static constexpr bool has_reduce = ((As::kind == KG && As::mode != MR) || ...);
+};
+
+template <class F, class... As>
+__device__ __forceinline__ void run_direct(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, false, As...>;
+    __shared__ double smem[32];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const int32_t b = blockIdx.x;
+    const int64_t lo = int64_t(b) * p.bs, hi = lo + p.bs < p.n ? lo + p.bs : p.n;
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+        E::init_elem(s, p, e, idx);
+        E::call(s, p, idx);
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
+}
+
+template <class F, class... As>
+__device__ __forceinline__ void run_staged(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, true, As...>;
+    __shared__ double smem[32];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const int32_t b = p.blocks[blockIdx.x];
+    const int64_t e = int64_t(b) * p.bs + threadIdx.x;
+    const int64_t hi = int64_t(b) * p.bs + p.bs < p.n ? int64_t(b) * p.bs + p.bs : p.n;
+    const bool active = threadIdx.x < p.bs && e < hi;
+    const int ncol = p.encol[b];
+    const int mine = active ? int(p.ecol[e]) : -1;
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    if (active) {
+        E::init_elem(s, p, e, idx);
+        E::call(s, p, idx);
+    }
+    if (ncol == 1) {
+        if (active) E::apply_staged(s, idx);
+    } else {
+        for (int c = 0; c < ncol; ++c) {
+            if (mine == c) E::apply_staged(s, idx);
+            __syncthreads();
+        }
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
+}
+
+template <class F, class... As>
+__device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, false, As...>;
+    __shared__ double smem[32];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const int32_t b = p.blocks[blockIdx.x];
+    const int64_t lo = int64_t(b) * p.bs, hi = lo + p.bs < p.n ? lo + p.bs : p.n;
+    const int ncol = p.encol[b];
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    for (int c = 0; c < ncol; ++c) {
+        for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+            if (int(p.ecol[e]) != c) continue;
+            E::init_elem(s, p, e, idx);
+            E::call(s, p, idx);
+        }
+        __syncthreads();
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
+}
+
+template <class F, class T>
+__global__ void __launch_bounds__(256) k_direct(const __grid_constant__ LaunchParams p) {
+    run_direct<F>(p, typename F::template sig<T>{});
+}
+template <class F, class T>
+__global__ void __launch_bounds__(256) k_staged(const __grid_constant__ LaunchParams p) {
+    run_staged<F>(p, typename F::template sig<T>{});
+}
+template <class F, class T>
+__global__ void __launch_bounds__(256) k_phased(const __grid_constant__ LaunchParams p) {
+    run_phased<F>(p, typename F::template sig<T>{});
+}
+
+// ---- compile-time signature introspection -------------------------------------
+template <class S>
+struct SigInfo;
+template <class... As>
+struct SigInfo<Sig<As...>> {
+    static constexpr int n = sizeof...(As);
+    static void fill(int32_t *kind, int32_t *mode, int32_t *dim, int32_t *dtype) {
+        int i = 0;
+        ((kind[i] = As::kind, mode[i] = As::mode, dim[i] = As::dim,
+          dtype[i] = type_code<typename As::type>(), ++i), ...);
+    }
+    static constexpr bool ind_write = ((As::kind == KI && As::mode != MR) || ...);
+    static constexpr bool ind_write_non_inc = ((As::kind == KI && (As::mode == MW || As::mode == MRW)) || ...);
+};
+
+// ---- registry -------------------------------------------------------------------
+using LaunchFn = void (*)(const LaunchParams &, dim3, dim3, cudaStream_t);
+
+struct FunctorEntry {
+    const char *name;
+    int32_t dtype;
+    int32_t nargs;
+    int32_t kind[MAX_ARGS], mode[MAX_ARGS], dim[MAX_ARGS], atype[MAX_ARGS];
+    bool ind_write, ind_write_non_inc;
+    LaunchFn direct, staged, phased;
+};
+
+void register_functor(const FunctorEntry &e);
+
+template <class F, class T>
+struct Registrar {
+    static void direct(const LaunchParams &p, dim3 g, dim3 b, cudaStream_t s) {
+        k_direct<F, T><<<g, b, 0, s>>>(p);
+    }
+    static void staged(const LaunchParams &p, dim3 g, dim3 b, cudaStream_t s) {
+        k_staged<F, T><<<g, b, 0, s>>>(p);
+    }
+    static void phased(const LaunchParams &p, dim3 g, dim3 b, cudaStream_t s) {
+        k_phased<F, T><<<g, b, 0, s>>>(p);
+    }
+    explicit Registrar(const char *name) {
+        using S = typename F::template sig<T>;
+        FunctorEntry e{};
+        e.name = name;
+        e.dtype = type_code<T>();
+        e.nargs = SigInfo<S>::n;
+        SigInfo<S>::fill(e.kind, e.mode, e.dim, e.atype);
+        e.ind_write = SigInfo<S>::ind_write;
+        e.ind_write_non_inc = SigInfo<S>::ind_write_non_inc;
+        e.direct = &direct;
+        e.staged = SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc ? &staged : nullptr;
+        e.phased = SigInfo<S>::ind_write ? &phased : nullptr;
+        register_functor(e);
+    }
+};
+
+#define ML_CAT2(a, b) a##b
+#define ML_CAT(a, b) ML_CAT2(a, b)
+#define ML_REGISTER(NAME, FUNCTOR, T) \
+    static ::ml::Registrar<FUNCTOR, T> ML_CAT(ml_reg_, __COUNTER__)(NAME)
+
+// integer floor division with Python semantics (numpy int64 //)
+__device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
+    int64_t q = a / b;
+    return (q * b != a && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+}  // namespace ml

@@ -1,0 +1,205 @@
+// Device functors for the bundled cell-area and diffusion programs and for the
+// loop shapes the reference test-suite exercises.  Each mirrors a Python
+// kernel line by line (same operation order; the library is compiled with
+// -fmad=false so a*b+c is never contracted and per-element float64 results
+// are bit-identical to numpy — only the order of increments differs).
+//
+//   copy            reference apps.py:213   (_k_copy)
+//   edge_flux       reference apps.py:217   (_k_edge_flux)        hot loop A1
+//   boundary_fix    reference apps.py:223   (_k_boundary_fix)
+//   diffusion_update reference apps.py:255 / 269 (_k_update, f64 dt / i64 floor-div scale)
+//   tri_area        reference apps.py:136
+//   distribute      reference apps.py:141   distribute_int apps.py:148
+//   sum             reference apps.py:155
+//   test shapes     reference tests/conftest.py:43-79, tests/test_executor.py:14-411
+#include <cuda/std/type_traits>
+
+#include "engine.cuh"
+
+namespace ml {
+namespace {
+
+template <class V>
+using elem_t = cuda::std::remove_cv_t<cuda::std::remove_reference_t<decltype(cuda::std::declval<V>()[0])>>;
+
+struct Copy {
+    template <class T> using sig = Sig<Arg<KD, MR, 1, T>, Arg<KD, MW, 1, T>>;
+    template <class S, class D>
+    __device__ static void apply(const Consts &, S src, D dst) { dst[0] = src[0]; }
+};
+
+struct EdgeFlux {
+    template <class T>
+    using sig = Sig<Arg<KI, MR, 1, T>, Arg<KI, MR, 1, T>, Arg<KI, MINC, 1, T>, Arg<KI, MINC, 1, T>>;
+    template <class U1, class U2, class F1, class F2>
+    __device__ static void apply(const Consts &, U1 u1, U2 u2, F1 f1, F2 f2) {
+        const auto d = u2[0] - u1[0];
+        f1[0] += d;
+        f2[0] -= d;
+    }
+};
+
+struct BoundaryFix {
+    template <class T>
+    using sig = Sig<Arg<KI, MW, 1, T>, Arg<KI, MW, 1, T>, Arg<KI, MR, 1, T>, Arg<KI, MR, 1, T>>;
+    template <class U1, class U2, class G1, class G2>
+    __device__ static void apply(const Consts &, U1 u1, U2 u2, G1 g1, G2 g2) {
+        u1[0] = g1[0];
+        u2[0] = g2[0];
+    }
+};
+
+struct DiffusionUpdate {
+    template <class T>
+    using sig = Sig<Arg<KD, MW, 1, T>, Arg<KD, MR, 1, T>, Arg<KD, MRW, 1, T>, Arg<KG, MINC, 1, T>>;
+    template <class U, class UP, class F, class R>
+    __device__ static void apply(const Consts &k, U u, UP up, F f, R res) {
+        using T = elem_t<U>;
+        if constexpr (cuda::std::is_floating_point_v<T>) {
+            const T fv = f[0];
+            const T nu = up[0] + k.f[0] * fv;
+            res[0] += fv * fv;
+            u[0] = nu;
+            f[0] = T(0);
+        } else {
+            const T fv = f[0];
+            const T nu = up[0] + floordiv(fv, k.i[0]);
+            res[0] += fv < 0 ? -fv : fv;
+            u[0] = nu;
+            f[0] = T(0);
+        }
+    }
+};
+
+struct TriArea {
+    template <class T>
+    using sig = Sig<Arg<KI, MR, 2, T>, Arg<KI, MR, 2, T>, Arg<KI, MR, 2, T>, Arg<KD, MW, 1, T>>;
+    template <class C1, class C2, class C3, class O>
+    __device__ static void apply(const Consts &, C1 c1, C2 c2, C3 c3, O out) {
+        out[0] = 0.5 * fabs((c2[0] - c1[0]) * (c3[1] - c1[1]) - (c3[0] - c1[0]) * (c2[1] - c1[1]));
+    }
+};
+
+struct Distribute {   // float: /3.0 ; int: floor // 3
+    template <class T>
+    using sig = Sig<Arg<KD, MR, 1, T>, Arg<KI, MINC, 1, T>, Arg<KI, MINC, 1, T>, Arg<KI, MINC, 1, T>>;
+    template <class A, class A1, class A2, class A3>
+    __device__ static void apply(const Consts &, A ac, A1 a1, A2 a2, A3 a3) {
+        using T = elem_t<A>;
+        T third;
+        if constexpr (cuda::std::is_floating_point_v<T>) third = ac[0] / 3.0;
+        else third = floordiv(ac[0], 3);
+        a1[0] += third;
+        a2[0] += third;
+        a3[0] += third;
+    }
+};
+
+struct Sum {
+    template <class T> using sig = Sig<Arg<KD, MR, 1, T>, Arg<KG, MINC, 1, T>>;
+    template <class V, class G>
+    __device__ static void apply(const Consts &, V v, G total) { total[0] += v[0]; }
+};
+
+// -- shapes from the reference test-suite ---------------------------------------
+
+template <int K>
+struct IncOne {   // conftest.inc_loop: every map column increments its target by one
+    template <class T, int... I> static auto make(cuda::std::integer_sequence<int, I...>)
+        -> Sig<decltype((void)I, Arg<KI, MINC, 1, T>{})...>;
+    template <class T> using sig = decltype(make<T>(cuda::std::make_integer_sequence<int, K>{}));
+    template <class... V>
+    __device__ static void apply(const Consts &, V... v) { ((v[0] += 1), ...); }
+};
+
+template <int K>
+struct ScatterSrc {   // conftest.random_loop_mesh: t[0] += s[0] for each column
+    template <class T, int... I> static auto make(cuda::std::integer_sequence<int, I...>)
+        -> Sig<Arg<KD, MR, 1, T>, decltype((void)I, Arg<KI, MINC, 1, T>{})...>;
+    template <class T> using sig = decltype(make<T>(cuda::std::make_integer_sequence<int, K>{}));
+    template <class S, class... V>
+    __device__ static void apply(const Consts &, S s, V... v) { ((v[0] += s[0]), ...); }
+};
+
+struct MixMax {   // test_executor._wide_dat_minmax_case: SOA dim 5, READ/MIN/MAX globals
+    template <class T>
+    using sig = Sig<Arg<KI, MR, 5, T>, Arg<KI, MR, 5, T>, Arg<KI, MINC, 5, T>, Arg<KI, MINC, 5, T>,
+                    Arg<KG, MR, 1, T>, Arg<KG, MMIN, 1, T>, Arg<KG, MMAX, 1, T>>;
+    template <class W1, class W2, class A1, class A2, class S, class LO, class HI>
+    __device__ static void apply(const Consts &, W1 w1, W2 w2, A1 a1, A2 a2, S s, LO lo, HI hi) {
+        using T = elem_t<W1>;
+        T m = w1[0], big = w1[0];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            a1[c] += w2[c] * s[0];
+            a2[c] += w1[c] * s[0];
+        }
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            m = w1[c] < m ? w1[c] : m;
+            m = w2[c] < m ? w2[c] : m;
+            big = w1[c] > big ? w1[c] : big;
+            big = w2[c] > big ? w2[c] : big;
+        }
+        if (m < lo[0]) lo[0] = m;
+        if (big > hi[0]) hi[0] = big;
+    }
+};
+
+struct ScaleRW {   // test_executor.test_threads_direct_loop_is_exact_even_float
+    template <class T> using sig = Sig<Arg<KD, MRW, 1, T>>;
+    template <class V>
+    __device__ static void apply(const Consts &, V v) { v[0] = v[0] * 1.0000001 + 0.25; }
+};
+
+struct SetOne {   // test_executor.test_no_exchange_between_consecutive_reads ("init")
+    template <class T> using sig = Sig<Arg<KD, MW, 1, T>>;
+    template <class V>
+    __device__ static void apply(const Consts &, V v) { v[0] = 1; }
+};
+
+struct GatherPair {   // ... ("gather"): out += a + b, direct INC with indirect reads
+    template <class T>
+    using sig = Sig<Arg<KI, MR, 1, T>, Arg<KI, MR, 1, T>, Arg<KD, MINC, 1, T>>;
+    template <class A, class B, class O>
+    __device__ static void apply(const Consts &, A a, B b, O out) { out[0] = out[0] + a[0] + b[0]; }
+};
+
+struct NoOp1 {   // direct RW no-op (plan tests)
+    template <class T> using sig = Sig<Arg<KD, MRW, 1, T>>;
+    template <class V>
+    __device__ static void apply(const Consts &, V) {}
+};
+
+}  // namespace
+
+ML_REGISTER("copy", Copy, double);
+ML_REGISTER("copy", Copy, int64_t);
+ML_REGISTER("edge_flux", EdgeFlux, double);
+ML_REGISTER("edge_flux", EdgeFlux, int64_t);
+ML_REGISTER("boundary_fix", BoundaryFix, double);
+ML_REGISTER("boundary_fix", BoundaryFix, int64_t);
+ML_REGISTER("diffusion_update", DiffusionUpdate, double);
+ML_REGISTER("diffusion_update", DiffusionUpdate, int64_t);
+ML_REGISTER("tri_area", TriArea, double);
+ML_REGISTER("distribute", Distribute, double);
+ML_REGISTER("distribute_int", Distribute, int64_t);
+ML_REGISTER("sum", Sum, double);
+ML_REGISTER("sum", Sum, int64_t);
+ML_REGISTER("inc_one_1", IncOne<1>, int64_t);
+ML_REGISTER("inc_one_2", IncOne<2>, int64_t);
+ML_REGISTER("inc_one_3", IncOne<3>, int64_t);
+ML_REGISTER("inc_one_1", IncOne<1>, double);
+ML_REGISTER("inc_one_2", IncOne<2>, double);
+ML_REGISTER("inc_one_3", IncOne<3>, double);
+ML_REGISTER("scatter_src_1", ScatterSrc<1>, int64_t);
+ML_REGISTER("scatter_src_2", ScatterSrc<2>, int64_t);
+ML_REGISTER("scatter_src_3", ScatterSrc<3>, int64_t);
+ML_REGISTER("mixmax", MixMax, int64_t);
+ML_REGISTER("scale_rw", ScaleRW, double);
+ML_REGISTER("set_one", SetOne, double);
+ML_REGISTER("gather_pair", GatherPair, double);
+ML_REGISTER("noop_rw", NoOp1, double);
+ML_REGISTER("noop_rw", NoOp1, int64_t);
+
+}  // namespace ml

@@ -1,0 +1,518 @@
+// libmeshloop_b200 runtime: device/stream management, memory, functor registry,
+// loop launch (colour schedule + deterministic reduction combine), native
+// programs with CUDA-graph replay, timers and the L2 flush used by the bench.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "ml_common.h"
+
+namespace ml {
+
+static thread_local std::string g_error;
+
+void set_error(const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_error = buf;
+}
+const char *get_error() { return g_error.c_str(); }
+
+// ---- functor registry -------------------------------------------------------------
+static std::vector<FunctorEntry> &registry() {
+    static std::vector<FunctorEntry> r;
+    return r;
+}
+void register_functor(const FunctorEntry &e) { registry().push_back(e); }
+
+// ---- per-device state ------------------------------------------------------------
+struct DeviceState {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    int sm_count = 0;
+    int64_t l2_bytes = 0;
+    void *flush_buf = nullptr;
+    size_t flush_bytes = 0;
+};
+static DeviceState g_dev;
+static std::mutex g_init_mu;
+
+static int ensure_init() {
+    if (g_dev.stream) return ML_OK;
+    ML_FAIL(ML_EINVAL, "libmeshloop_b200: ml_init() has not been called");
+}
+
+// ---- reduction combine ------------------------------------------------------------
+template <class T, int M>
+__global__ void __launch_bounds__(256) k_combine(T *g, const T *part, int64_t nparts, int dim) {
+    __shared__ double smem[32];
+    for (int c = 0; c < dim; ++c) {
+        T v = reduce_identity<T, M>();
+        for (int64_t i = threadIdx.x; i < nparts; i += blockDim.x) v = combine<M>(v, part[i * dim + c]);
+        v = block_reduce<T, M>(v, reinterpret_cast<T *>(smem));
+        if (threadIdx.x == 0) g[c] = combine<M>(g[c], v);
+        __syncthreads();
+    }
+}
+
+template <class T>
+static void launch_combine(int mode, T *g, const T *part, int64_t nparts, int dim, cudaStream_t s) {
+    if (mode == MINC) k_combine<T, MINC><<<1, 256, 0, s>>>(g, part, nparts, dim);
+    else if (mode == MMIN) k_combine<T, MMIN><<<1, 256, 0, s>>>(g, part, nparts, dim);
+    else k_combine<T, MMAX><<<1, 256, 0, s>>>(g, part, nparts, dim);
+}
+
+static int round_up32(int64_t x) { return int((x + 31) / 32 * 32); }
+
+static int validate(const ml_loop_t *L, const FunctorEntry &f) {
+    const char *nm = L->name ? L->name : "?";
+    if (L->nargs != f.nargs)
+        ML_FAIL(ML_EINVAL, "loop '%s': functor '%s' takes %d args, loop has %d", nm, f.name, f.nargs,
+                L->nargs);
+    for (int i = 0; i < f.nargs; ++i) {
+        const ml_arg_t &a = L->args[i];
+        if (a.kind != f.kind[i] || a.mode != f.mode[i] || a.dim != f.dim[i] || a.dtype != f.atype[i])
+            ML_FAIL(ML_EINVAL,
+                    "loop '%s' arg %d: functor '%s' expects (kind %d, mode %d, dim %d, dtype %d), "
+                    "got (kind %d, mode %d, dim %d, dtype %d)",
+                    nm, i, f.name, f.kind[i], f.mode[i], f.dim[i], f.atype[i], a.kind, a.mode, a.dim,
+                    a.dtype);
+        if (!a.data && !(a.kind != ML_GLOBAL && a.set_size == 0))
+            ML_FAIL(ML_EINVAL, "loop '%s' arg %d: null device pointer", nm, i);
+        if (a.kind == ML_INDIRECT && !a.map && L->n > 0)
+            ML_FAIL(ML_EINVAL, "loop '%s' arg %d: indirect arg without device map", nm, i);
+    }
+    return ML_OK;
+}
+
+static uint64_t scratch_bytes(const ml_loop_t *L, const FunctorEntry &f) {
+    uint64_t bytes = 0;
+    const int64_t nb = std::max<int64_t>(L->plan.nblocks, 1);
+    for (int i = 0; i < f.nargs; ++i)
+        if (f.kind[i] == KG && f.mode[i] != MR) bytes += uint64_t(nb) * f.dim[i] * 8 + 256;
+    return bytes;
+}
+
+static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
+    auto &reg = registry();
+    if (L->functor < 0 || L->functor >= int(reg.size()))
+        ML_FAIL(ML_ENOFUNCTOR, "loop '%s': bad functor id %d", L->name ? L->name : "?", L->functor);
+    const FunctorEntry &f = reg[L->functor];
+    int rc = validate(L, f);
+    if (rc) return rc;
+    if (L->n == 0) return ML_OK;   // empty iteration set: no launch, globals untouched
+    const int64_t bs = L->plan.block_size;
+    const int64_t nb = L->plan.nblocks;
+    if (bs < 1 || nb != (L->n + bs - 1) / bs)
+        ML_FAIL(ML_EINVAL, "loop '%s': plan does not cover the iteration set", L->name);
+
+    LaunchParams p{};
+    p.n = L->n;
+    p.bs = int32_t(bs);
+    for (int i = 0; i < 4; ++i) {
+        p.k.f[i] = L->fconst[i];
+        p.k.i[i] = L->iconst[i];
+    }
+    char *scratch = static_cast<char *>(L->scratch);
+    for (int i = 0; i < f.nargs; ++i) {
+        const ml_arg_t &a = L->args[i];
+        ArgRt &r = p.a[i];
+        r.data = a.data;
+        if (a.kind == ML_INDIRECT) r.map = a.map + int64_t(a.slot) * a.map_from;
+        if (a.kind == ML_GLOBAL) {
+            r.se = 0;
+            r.sc = 1;
+            if (a.mode != ML_READ) {
+                if (!scratch) ML_FAIL(ML_EINVAL, "loop '%s': reduction needs scratch", L->name);
+                p.part[i] = scratch;
+                scratch += uint64_t(nb) * a.dim * 8 + 256;
+            }
+        } else if (a.layout == ML_AOS) {
+            r.se = a.dim;
+            r.sc = 1;
+        } else {
+            r.se = 1;
+            r.sc = a.set_size;
+        }
+    }
+
+    if (!f.ind_write) {
+        const int threads = std::clamp(round_up32(bs), 32, 256);
+        p.blocks = nullptr;
+        f.direct(p, dim3(unsigned(nb)), dim3(unsigned(threads)), stream);
+    } else {
+        if (!L->plan.color_offsets || !L->plan.blocks || !L->plan.elem_color || !L->plan.elem_ncolors)
+            ML_FAIL(ML_EINVAL, "loop '%s': indirect writes need a coloured plan", L->name);
+        p.ecol = L->plan.elem_color;
+        p.encol = L->plan.elem_ncolors;
+        const bool staged = f.staged && bs <= 256;
+        const int threads = staged ? round_up32(bs) : std::clamp(round_up32(bs), 32, 256);
+        for (int64_t c = 0; c < L->plan.ncolors; ++c) {
+            const int64_t off = L->plan.color_offsets[c], cnt = L->plan.color_offsets[c + 1] - off;
+            if (cnt <= 0) continue;
+            p.blocks = L->plan.blocks + off;
+            (staged ? f.staged : f.phased)(p, dim3(unsigned(cnt)), dim3(unsigned(threads)), stream);
+        }
+    }
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) ML_FAIL(ML_ECUDA, "loop '%s': launch failed: %s", L->name, cudaGetErrorString(err));
+
+    for (int i = 0; i < f.nargs; ++i) {
+        const ml_arg_t &a = L->args[i];
+        if (a.kind != ML_GLOBAL || a.mode == ML_READ) continue;
+        if (a.dtype == ML_F64)
+            launch_combine<double>(a.mode, static_cast<double *>(a.data), static_cast<const double *>(p.part[i]),
+                                   nb, a.dim, stream);
+        else
+            launch_combine<int64_t>(a.mode, static_cast<int64_t *>(a.data),
+                                    static_cast<const int64_t *>(p.part[i]), nb, a.dim, stream);
+    }
+    err = cudaGetLastError();
+    if (err != cudaSuccess) ML_FAIL(ML_ECUDA, "loop '%s': combine failed: %s", L->name, cudaGetErrorString(err));
+    return ML_OK;
+}
+
+__global__ void k_map_to_i32(int32_t *dst, const int64_t *src, int64_t rows, int32_t arity) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < rows * arity;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / arity, c = i % arity;
+        dst[c * rows + r] = int32_t(src[i]);
+    }
+}
+
+}  // namespace ml
+
+using namespace ml;
+
+// ---- ABI: runtime --------------------------------------------------------------------
+extern "C" const char *ml_last_error(void) { return get_error(); }
+extern "C" int ml_version(void) { return 1; }
+
+extern "C" int ml_init(int device) {
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    if (g_dev.stream && g_dev.device == device) return ML_OK;
+    int n = 0;
+    ML_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) ML_FAIL(ML_EINVAL, "ml_init: device %d of %d", device, n);
+    ML_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    ML_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        ML_FAIL(ML_ECUDA, "ml_init: device %d is sm_%d%d; this library is built for sm_100a only", device,
+                prop.major, prop.minor);
+    if (g_dev.stream) cudaStreamDestroy(g_dev.stream);
+    ML_CUDA(cudaStreamCreateWithFlags(&g_dev.stream, cudaStreamNonBlocking));
+    g_dev.device = device;
+    g_dev.sm_count = prop.multiProcessorCount;
+    g_dev.l2_bytes = prop.l2CacheSize;
+    return ML_OK;
+}
+
+extern "C" int ml_device_info(ml_device_info_t *out) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    cudaDeviceProp prop;
+    ML_CUDA(cudaGetDeviceProperties(&prop, g_dev.device));
+    std::memset(out, 0, sizeof *out);
+    std::strncpy(out->name, prop.name, sizeof(out->name) - 1);
+    out->sm_count = prop.multiProcessorCount;
+    out->cc_major = prop.major;
+    out->cc_minor = prop.minor;
+    out->l2_bytes = prop.l2CacheSize;
+    out->hbm_bytes = int64_t(prop.totalGlobalMem);
+    return ML_OK;
+}
+
+extern "C" int ml_synchronize(void) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    ML_CUDA(cudaStreamSynchronize(g_dev.stream));
+    return ML_OK;
+}
+
+// ---- ABI: memory -----------------------------------------------------------------------
+extern "C" int ml_alloc(uint64_t bytes, void **dptr) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    *dptr = nullptr;
+    if (bytes == 0) return ML_OK;
+    cudaError_t e = cudaMalloc(dptr, bytes);
+    if (e != cudaSuccess) ML_FAIL(ML_ENOMEM, "cudaMalloc(%llu) failed: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+    return ML_OK;
+}
+extern "C" int ml_free(void *dptr) {
+    if (dptr) ML_CUDA(cudaFree(dptr));
+    return ML_OK;
+}
+extern "C" int ml_host_alloc(uint64_t bytes, void **hptr) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    cudaError_t e = cudaHostAlloc(hptr, std::max<uint64_t>(bytes, 8), cudaHostAllocPortable);
+    if (e != cudaSuccess) ML_FAIL(ML_ENOMEM, "cudaHostAlloc(%llu) failed: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+    return ML_OK;
+}
+extern "C" int ml_host_free(void *hptr) {
+    if (hptr) ML_CUDA(cudaFreeHost(hptr));
+    return ML_OK;
+}
+extern "C" int ml_upload(void *dst, const void *src, uint64_t bytes) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (bytes) ML_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g_dev.stream));
+    return ML_OK;
+}
+extern "C" int ml_download(void *dst, const void *src, uint64_t bytes) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (bytes) ML_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g_dev.stream));
+    ML_CUDA(cudaStreamSynchronize(g_dev.stream));
+    return ML_OK;
+}
+extern "C" int ml_memset(void *dst, int value, uint64_t bytes) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (bytes) ML_CUDA(cudaMemsetAsync(dst, value, bytes, g_dev.stream));
+    return ML_OK;
+}
+extern "C" int ml_map_upload(int32_t *dst, const int64_t *table, int64_t rows, int32_t arity) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    const uint64_t n = uint64_t(rows) * arity;
+    if (!n) return ML_OK;
+    int64_t *tmp = nullptr;
+    ML_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&tmp), n * 8, g_dev.stream));
+    ML_CUDA(cudaMemcpyAsync(tmp, table, n * 8, cudaMemcpyHostToDevice, g_dev.stream));
+    const int grid = int(std::min<uint64_t>((n + 255) / 256, 65535));
+    k_map_to_i32<<<grid, 256, 0, g_dev.stream>>>(dst, tmp, rows, arity);
+    ML_CUDA(cudaGetLastError());
+    ML_CUDA(cudaFreeAsync(tmp, g_dev.stream));
+    ML_CUDA(cudaStreamSynchronize(g_dev.stream));   // `table` is borrowed
+    return ML_OK;
+}
+
+// ---- ABI: functors and loops --------------------------------------------------------------
+extern "C" int ml_functor_lookup(const char *name, int32_t dtype, int32_t *functor_id) {
+    auto &reg = registry();
+    for (size_t i = 0; i < reg.size(); ++i)
+        if (std::strcmp(reg[i].name, name) == 0 && reg[i].dtype == dtype) {
+            *functor_id = int32_t(i);
+            return ML_OK;
+        }
+    ML_FAIL(ML_ENOFUNCTOR, "no compiled functor '%s' for dtype %s", name, dtype == ML_F64 ? "float64" : "int64");
+}
+
+extern "C" int ml_functor_signature(int32_t id, int32_t *nargs, int32_t *kinds, int32_t *modes,
+                                    int32_t *dims, int32_t *dtypes) {
+    auto &reg = registry();
+    if (id < 0 || id >= int(reg.size())) ML_FAIL(ML_ENOFUNCTOR, "bad functor id %d", id);
+    const FunctorEntry &f = reg[id];
+    *nargs = f.nargs;
+    for (int i = 0; i < f.nargs; ++i) {
+        if (kinds) kinds[i] = f.kind[i];
+        if (modes) modes[i] = f.mode[i];
+        if (dims) dims[i] = f.dim[i];
+        if (dtypes) dtypes[i] = f.atype[i];
+    }
+    return ML_OK;
+}
+
+extern "C" int ml_functor_count(int32_t *count) {
+    *count = int32_t(registry().size());
+    return ML_OK;
+}
+
+extern "C" int ml_functor_name(int32_t id, char *buf, int32_t buflen, int32_t *dtype) {
+    auto &reg = registry();
+    if (id < 0 || id >= int(reg.size())) ML_FAIL(ML_ENOFUNCTOR, "bad functor id %d", id);
+    std::snprintf(buf, size_t(buflen), "%s", reg[id].name);
+    if (dtype) *dtype = reg[id].dtype;
+    return ML_OK;
+}
+
+extern "C" int ml_loop_scratch_bytes(const ml_loop_t *loop, uint64_t *bytes) {
+    auto &reg = registry();
+    if (loop->functor < 0 || loop->functor >= int(reg.size())) ML_FAIL(ML_ENOFUNCTOR, "bad functor id");
+    *bytes = scratch_bytes(loop, reg[loop->functor]);
+    return ML_OK;
+}
+
+extern "C" int ml_loop_run(const ml_loop_t *loop) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    return enqueue_loop(loop, g_dev.stream);
+}
+
+// ---- ABI: programs -----------------------------------------------------------------------------
+struct ml_program {
+    std::vector<ml_loop_t> loops;
+    std::vector<std::vector<ml_arg_t>> args;
+    std::vector<std::vector<int64_t>> color_offsets;
+    std::vector<std::string> names;
+    void *ghost = nullptr, *gdev = nullptr;
+    uint64_t gbytes = 0;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    std::vector<cudaEvent_t> events;
+    std::vector<float> times;
+};
+
+static int program_enqueue(ml_program *p, bool timed) {
+    cudaStream_t s = g_dev.stream;
+    if (p->gbytes) ML_CUDA(cudaMemcpyAsync(p->gdev, p->ghost, p->gbytes, cudaMemcpyHostToDevice, s));
+    for (size_t i = 0; i < p->loops.size(); ++i) {
+        if (timed) ML_CUDA(cudaEventRecord(p->events[i], s));
+        int rc = enqueue_loop(&p->loops[i], s);
+        if (rc) return rc;
+    }
+    if (timed) ML_CUDA(cudaEventRecord(p->events[p->loops.size()], s));
+    if (p->gbytes) ML_CUDA(cudaMemcpyAsync(p->ghost, p->gdev, p->gbytes, cudaMemcpyDeviceToHost, s));
+    return ML_OK;
+}
+
+extern "C" int ml_program_create(const ml_loop_t *loops, int32_t nloops, void *globals_host,
+                                 void *globals_dev, uint64_t globals_bytes, ml_program_t **out) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    ML_GUARD_BEGIN
+    auto p = std::make_unique<ml_program>();
+    p->loops.assign(loops, loops + nloops);
+    p->args.resize(nloops);
+    p->color_offsets.resize(nloops);
+    p->names.resize(nloops);
+    for (int i = 0; i < nloops; ++i) {
+        ml_loop_t &L = p->loops[i];
+        p->args[i].assign(L.args, L.args + L.nargs);
+        L.args = p->args[i].data();
+        p->names[i] = L.name ? L.name : "?";
+        L.name = p->names[i].c_str();
+        if (L.plan.color_offsets) {
+            p->color_offsets[i].assign(L.plan.color_offsets, L.plan.color_offsets + L.plan.ncolors + 1);
+            L.plan.color_offsets = p->color_offsets[i].data();
+        }
+        auto &reg = registry();
+        if (L.functor < 0 || L.functor >= int(reg.size())) ML_FAIL(ML_ENOFUNCTOR, "bad functor id");
+        rc = validate(&L, reg[L.functor]);
+        if (rc) return rc;
+    }
+    p->ghost = globals_host;
+    p->gdev = globals_dev;
+    p->gbytes = globals_bytes;
+    p->events.resize(size_t(nloops) + 1);
+    for (auto &e : p->events) ML_CUDA(cudaEventCreate(&e));
+    p->times.assign(nloops, 0.f);
+    *out = p.release();
+    return ML_OK;
+    ML_GUARD_END
+}
+
+static int program_capture(ml_program *p) {
+    if (p->exec) return ML_OK;
+    cudaStream_t s = g_dev.stream;
+    ML_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int rc = program_enqueue(p, false);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) ML_FAIL(ML_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    p->graph = g;
+    ML_CUDA(cudaGraphInstantiate(&p->exec, g, 0));
+    return ML_OK;
+}
+
+extern "C" int ml_program_replay(ml_program_t *p, int32_t count) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    rc = program_capture(p);
+    if (rc) return rc;
+    for (int32_t i = 0; i < count; ++i) ML_CUDA(cudaGraphLaunch(p->exec, g_dev.stream));
+    ML_CUDA(cudaStreamSynchronize(g_dev.stream));
+    return ML_OK;
+}
+
+extern "C" int ml_program_run(ml_program_t *p, int32_t use_graph, int32_t time_loops) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    cudaStream_t s = g_dev.stream;
+    if (use_graph) {
+        rc = program_capture(p);
+        if (rc) return rc;
+        ML_CUDA(cudaGraphLaunch(p->exec, s));
+        ML_CUDA(cudaStreamSynchronize(s));
+        return ML_OK;
+    }
+    rc = program_enqueue(p, time_loops != 0);
+    if (rc) return rc;
+    ML_CUDA(cudaStreamSynchronize(s));
+    if (time_loops)
+        for (size_t i = 0; i < p->loops.size(); ++i)
+            ML_CUDA(cudaEventElapsedTime(&p->times[i], p->events[i], p->events[i + 1]));
+    return ML_OK;
+}
+
+extern "C" int ml_program_loop_times(const ml_program_t *p, float *ms) {
+    std::copy(p->times.begin(), p->times.end(), ms);
+    return ML_OK;
+}
+
+extern "C" int ml_program_free(ml_program_t *p) {
+    if (!p) return ML_OK;
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    for (auto &e : p->events) cudaEventDestroy(e);
+    delete p;
+    return ML_OK;
+}
+
+// ---- ABI: measurement helpers ----------------------------------------------------------------
+extern "C" int ml_flush_l2(void) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (!g_dev.flush_buf) {
+        g_dev.flush_bytes = size_t(std::max<int64_t>(g_dev.l2_bytes, 64 << 20)) * 2;
+        ML_CUDA(cudaMalloc(&g_dev.flush_buf, g_dev.flush_bytes));
+    }
+    ML_CUDA(cudaMemsetAsync(g_dev.flush_buf, 0x5a, g_dev.flush_bytes, g_dev.stream));
+    return ML_OK;
+}
+
+struct ml_timer {
+    cudaEvent_t a, b;
+};
+extern "C" int ml_timer_create(ml_timer_t **t) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    auto *x = new ml_timer;
+    ML_CUDA(cudaEventCreate(&x->a));
+    ML_CUDA(cudaEventCreate(&x->b));
+    *t = x;
+    return ML_OK;
+}
+extern "C" int ml_timer_start(ml_timer_t *t) {
+    ML_CUDA(cudaEventRecord(t->a, g_dev.stream));
+    return ML_OK;
+}
+extern "C" int ml_timer_stop(ml_timer_t *t, float *ms) {
+    ML_CUDA(cudaEventRecord(t->b, g_dev.stream));
+    ML_CUDA(cudaEventSynchronize(t->b));
+    ML_CUDA(cudaEventElapsedTime(ms, t->a, t->b));
+    return ML_OK;
+}
+extern "C" int ml_timer_free(ml_timer_t *t) {
+    if (!t) return ML_OK;
+    cudaEventDestroy(t->a);
+    cudaEventDestroy(t->b);
+    delete t;
+    return ML_OK;
+}

@@ -1,0 +1,144 @@
+"""Device residency: HBM mirrors of dats, maps and plans.
+
+Layout in HBM:
+
+* a dat is one contiguous float64/int64 buffer in the dat's own layout
+  (AOS ``e*dim+c`` or SOA ``c*size+e``), uploaded on first use and kept
+  resident across ``run_program`` calls;
+* a map is stored int32 and column-major (``[arity][from_size]``), so the
+  index reads of one map column by consecutive elements are coalesced and
+  cost 4 B per element instead of the host table's 8 B;
+* a plan is three arrays: block ids ordered by colour (int32), element
+  colours (uint16) and per-block colour counts (int32).
+
+Coherence is lazy and conservative: ``Dat.data`` (which may be written
+through) marks the mirror host-newer; executions mark written dats
+device-newer and the host copy is refreshed on the next host access.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from .core import AOS, Dat, ExecError, Map
+
+__all__ = ["DatMirror", "dat_mirror", "map_mirror", "plan_mirror", "pin_mesh"]
+
+
+class DatMirror:
+    """Device copy of one dat payload."""
+
+    __slots__ = ("buf", "layout", "nbytes", "host_newer", "device_newer")
+
+    def __init__(self):
+        self.buf = None
+        self.layout = None
+        self.nbytes = -1
+        self.host_newer = True
+        self.device_newer = False
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.ptr if self.buf is not None else 0
+
+    def download(self, host: np.ndarray) -> None:
+        if self.buf is not None and host.nbytes:
+            if not host.flags.c_contiguous:
+                raise ExecError("dat payload must be contiguous to receive device data")
+            self.buf.download(host)
+        self.device_newer = False
+
+
+def dat_mirror(dat: Dat, force_upload: bool = False) -> DatMirror:
+    """The up-to-date device mirror of ``dat`` (allocating/uploading as needed)."""
+    m = dat._dev
+    if m is None:
+        m = dat._dev = DatMirror()
+    host = dat._host
+    if m.buf is None or m.nbytes != host.nbytes:
+        if m.device_newer:
+            raise ExecError(f"dat {dat.name!r}: payload resized while device data is newer")
+        m.buf = N.DeviceBuffer(host.nbytes) if host.nbytes else None
+        m.nbytes = host.nbytes
+        m.host_newer = True
+    if m.layout is not dat.layout:
+        m.layout = dat.layout
+        m.host_newer = True
+    if (m.host_newer or force_upload) and not m.device_newer:
+        if host.nbytes:
+            if not host.flags.c_contiguous:
+                dat._host = host = np.ascontiguousarray(host)
+            m.buf.upload(host)
+        m.host_newer = False
+    return m
+
+
+class _MapMirror:
+    __slots__ = ("buf", "table", "shape")
+
+    def __init__(self, buf, table):
+        self.buf = buf
+        self.table = table
+        self.shape = table.shape
+
+
+def map_mirror(m: Map) -> int:
+    """Device pointer of the int32 column-major copy of ``m.table``."""
+    mm = m._dev
+    if mm is not None and mm.table is m.table and mm.shape == m.table.shape:
+        return mm.buf.ptr if mm.buf is not None else 0
+    t = np.ascontiguousarray(m.table, dtype=np.int64)
+    if t.size and int(t.max(initial=0)) >= 2 ** 31:
+        raise ExecError(f"map {m.name!r}: ids exceed int32")
+    buf = N.DeviceBuffer(t.size * 4) if t.size else None
+    if t.size:
+        N.check(N.lib().ml_map_upload(buf.ptr, N.ptr(t), t.shape[0], t.shape[1]), "ml_map_upload")
+    m._dev = _MapMirror(buf, m.table)
+    return buf.ptr if buf is not None else 0
+
+
+class PlanMirror:
+    __slots__ = ("blocks", "ecol", "encol", "offsets")
+
+    def __init__(self, plan):
+        blocks = plan.blocks_flat.astype(np.int32)
+        self.offsets = np.ascontiguousarray(plan.color_offsets, dtype=np.int64)
+        self.blocks = N.DeviceBuffer(max(blocks.nbytes, 4))
+        if blocks.size:
+            self.blocks.upload(blocks)
+        self.ecol = self.encol = None
+        if plan.has_writes:
+            if plan.max_elem_colors > 65535:
+                raise ExecError("more than 65535 element colours in one block")
+            ecol = plan.elem_color.astype(np.uint16)
+            encol = plan.elem_ncolors.astype(np.int32)
+            self.ecol = N.DeviceBuffer(max(ecol.nbytes, 4))
+            self.encol = N.DeviceBuffer(max(encol.nbytes, 4))
+            if ecol.size:
+                self.ecol.upload(ecol)
+                self.encol.upload(encol)
+
+
+def plan_mirror(plan) -> PlanMirror:
+    if plan._dev is None:
+        plan._dev = PlanMirror(plan)
+    return plan._dev
+
+
+_PINNED_KEEPALIVE: dict = {}
+
+
+def pin_mesh(mesh, min_bytes: int = 1 << 20) -> int:
+    """Re-home every dat payload of at least ``min_bytes`` into pinned host memory
+    (so host<->device copies run at full PCIe speed); returns the bytes pinned."""
+    total = 0
+    for d in mesh.dats.values():
+        host = d._pull()
+        if host.nbytes < min_bytes:
+            continue
+        pa = N.PinnedArray(host.shape, host.dtype)
+        pa.array[...] = host
+        _PINNED_KEEPALIVE[id(pa.array)] = pa
+        d._host = pa.array
+        total += host.nbytes
+    return total

@@ -1,0 +1,391 @@
+"""B200 execution backend: ``run_program`` for op_par_loop programs.
+
+Drop-in for reference ``executor.py:707-729``: same ``BackendConfig`` field
+names and validation style, same ``RunResult``, same post-conditions (mesh
+frozen; every written dat visible through ``dat.fetch()`` / ``dat.data``;
+reduction results in ``glob.buffer``; loops run in program order).  The
+backend name is ``"cuda"`` — the only one this package has: every loop runs
+as hand-written sm_100a kernels from ``libmeshloop_b200.so`` and there is no
+CPU fallback (an unbound kernel raises :class:`ExecError`).
+
+A program is compiled once into a native ``ml_program`` (loop descriptors
+with device pointers, plans, functor ids, a globals arena) and then replayed
+— eagerly with per-loop CUDA-event timing, or as one CUDA graph
+(``BackendConfig(use_graph=True)``).  Reductions stay on the device between
+loops, so a MIN computed by one loop can be READ by the next without a host
+round trip; globals travel to the host once per program run.
+
+``nranks > 1`` (or a multi-process launch) routes to the owner-compute
+multi-GPU layer in :mod:`paper_1403_7209_b200.multigpu`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from collections import OrderedDict
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Mesh, MeshError)
+from .device import dat_mirror, map_mirror, plan_mirror
+from .kernels import resolve_kernel
+from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
+from .plan import plan_for, plan_stats
+
+__all__ = ["BackendConfig", "RunResult", "ExchangeTimeout", "reduce_global", "run_program",
+           "run_loop", "compile_program", "CompiledProgram"]
+
+_BACKENDS = ("cuda",)
+
+
+class ExchangeTimeout(ExecError):
+    """A rank waited longer than the configured bound for a halo message."""
+
+
+@dataclass
+class BackendConfig:
+    backend: str = "cuda"
+    nthreads: int = 4                       # accepted for source compatibility; unused
+    nranks: int = 1                         # GPUs (one process per GPU)
+    block_size: int = 256
+    block_size_table: dict | None = None    # per-loop block size overrides
+    partitioner: str = "trivial"            # trivial | rcb (multi-GPU)
+    coord_dat: str = "coords"
+    balance: float = 1.0
+    class_a_ranks: int = 1
+    class_a_width: int = 4
+    class_b_width: int = 1
+    class_a_speed: float = 1.0
+    class_b_speed: float = 1.0
+    timeout_ms: float = 10000.0
+    simulated_elem_cost: float = 0.0
+    cost_model: Callable[[int], float] | None = None
+    phase_callback: Callable[[str, int], None] | None = None
+    # B200-specific
+    device: int | None = None               # default: LOCAL_RANK or 0
+    use_graph: bool = False                 # replay the program as one CUDA graph
+    time_loops: bool = True                 # per-loop CUDA-event timing (eager mode)
+    residency: str = "device"               # "device": lazy; "host": copy in/out every run
+
+    def __post_init__(self):
+        if self.backend not in _BACKENDS:
+            raise MeshError(f"unknown backend {self.backend!r}; expected one of {_BACKENDS} "
+                            f"(the CPU backends live in the reference package)")
+        if self.nthreads < 1 or self.nranks < 1 or self.block_size < 1:
+            raise MeshError("nthreads, nranks and block_size must be positive")
+        if self.balance <= 0:
+            raise MeshError(f"balance must be positive, got {self.balance}")
+        if self.partitioner not in ("trivial", "rcb"):
+            raise MeshError(f"unknown partitioner {self.partitioner!r}")
+        if self.residency not in ("device", "host"):
+            raise MeshError(f"unknown residency {self.residency!r}")
+
+    def block_size_for(self, loop_name: str) -> int:
+        if self.block_size_table and loop_name in self.block_size_table:
+            return int(self.block_size_table[loop_name])
+        return self.block_size
+
+    def device_index(self) -> int:
+        if self.device is not None:
+            return int(self.device)
+        return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+@dataclass
+class RunResult:
+    perf: list[PerfRecord]
+    total_sec: float
+    messages: int = 0
+    layout: object = None
+    assignments: dict | None = None
+
+
+def reduce_global(partials: Sequence, mode, initial=None):
+    """Combine partials in the given order (reference executor.py:123-143)."""
+    if mode not in (INC, MIN, MAX):
+        raise MeshError(f"mode {mode} is not a reduction")
+    arrs = [np.atleast_1d(np.asarray(p)) for p in partials]
+    if initial is not None:
+        acc = np.atleast_1d(np.asarray(initial)).copy()
+    elif not arrs:
+        raise MeshError("nothing to reduce")
+    elif mode is INC:
+        acc = np.zeros_like(arrs[0])
+    else:
+        acc, arrs = arrs[0].copy(), arrs[1:]
+    op = {INC: np.add, MIN: np.minimum, MAX: np.maximum}[mode]
+    for p in arrs:
+        acc = op(acc, p)
+    return acc[0] if acc.size == 1 else acc
+
+
+# -- program compilation -------------------------------------------------------------
+
+_KIND = {"direct": N.ML_DIRECT, "indirect": N.ML_INDIRECT, "global": N.ML_GLOBAL}
+
+
+def _dtype_code(dt) -> int:
+    return N.ML_F64 if np.dtype(dt) == np.float64 else N.ML_I64
+
+
+def _functor_id(name: str, dtype: int, cache={}) -> int:
+    key = (name, dtype)
+    if key not in cache:
+        fid = C.c_int32()
+        N.check(N.lib().ml_functor_lookup(name.encode(), dtype, C.byref(fid)),
+                f"kernel binding {name!r}")
+        cache[key] = fid.value
+    return cache[key]
+
+
+def _loop_dtype(loop: Loop) -> int:
+    for a in loop.args:
+        if a.kind != "global":
+            return _dtype_code(a.dat.dtype)
+    for a in loop.args:
+        return _dtype_code(a.glob.dtype)
+    return N.ML_F64
+
+
+class _LoopEntry:
+    """Everything one loop needs on the device, kept alive with the program."""
+
+    def __init__(self, loop: Loop, mesh: Mesh, config: BackendConfig, gslot: dict,
+                 garena_ptr: int):
+        self.loop = loop
+        binding = resolve_kernel(loop.kernel)
+        self.binding = binding
+        self.functor = _functor_id(binding.functor, _loop_dtype(loop))
+        self.bs = config.block_size_for(loop.name)
+        self.plan = plan_for(loop, mesh, self.bs)
+        self.st = plan_stats(self.plan)
+        pm = plan_mirror(self.plan)
+        self.pm = pm
+        args = (N.MlArg * max(len(loop.args), 1))()
+        self.dats = []
+        for i, a in enumerate(loop.args):
+            r = args[i]
+            r.kind = _KIND[a.kind]
+            r.mode = N.MODE_CODE[a.mode.name]
+            if a.kind == "global":
+                r.dim = a.glob.dim
+                r.dtype = _dtype_code(a.glob.dtype)
+                r.data = garena_ptr + gslot[id(a.glob)]
+                continue
+            d = a.dat
+            r.dim = d.dim
+            r.dtype = _dtype_code(d.dtype)
+            r.layout = N.ML_AOS if d.layout.name == "AOS" else N.ML_SOA
+            r.set_size = d.set.size
+            self.dats.append(d)
+            r.data = dat_mirror(d).ptr or None
+            if a.kind == "indirect":
+                r.slot = a.slot
+                r.map = map_mirror(a.map) or None
+                r.map_from = a.map.from_set.size
+        self.args = args
+        L = N.MlLoop()
+        self.name = loop.name.encode()
+        L.name = self.name
+        L.functor = self.functor
+        L.nargs = len(loop.args)
+        L.args = C.cast(args, C.POINTER(N.MlArg))
+        L.n = loop.iter_set.size
+        L.plan.nblocks = self.plan.nblocks
+        L.plan.ncolors = self.plan.ncolors
+        L.plan.block_size = self.bs
+        L.plan.color_offsets = pm.offsets.ctypes.data_as(C.POINTER(C.c_int64))
+        L.plan.blocks = pm.blocks.ptr
+        L.plan.elem_color = pm.ecol.ptr if pm.ecol is not None else None
+        L.plan.elem_ncolors = pm.encol.ptr if pm.encol is not None else None
+        for k, v in enumerate(binding.fconsts[:4]):
+            L.fconst[k] = v
+        for k, v in enumerate(binding.iconsts[:4]):
+            L.iconst[k] = v
+        nbytes = C.c_uint64()
+        N.check(N.lib().ml_loop_scratch_bytes(C.byref(L), C.byref(nbytes)))
+        self.scratch = N.DeviceBuffer(nbytes.value) if nbytes.value else None
+        L.scratch = self.scratch.ptr if self.scratch else None
+        self.desc = L
+        self.useful = useful_bytes(loop)
+        self.alg = b_alg(loop)
+        self.written = [a.dat for a in loop.args if a.kind != "global" and a.mode in WRITE_MODES]
+
+    def dat_pointers(self) -> tuple:
+        return tuple(d._dev.ptr if d._dev is not None else 0 for d in self.dats)
+
+
+class CompiledProgram:
+    """A program bound to device state; replayable (optionally as a CUDA graph)."""
+
+    def __init__(self, program: Sequence[Loop], mesh: Mesh, config: BackendConfig):
+        self.loops = list(program)
+        self.mesh = mesh
+        self.version = mesh.version
+        globs: list[Global] = []
+        for loop in self.loops:
+            for a in loop.args:
+                if a.kind == "global" and all(g is not a.glob for g in globs):
+                    globs.append(a.glob)
+        self.globs = globs
+        self.gslot, off = {}, 0
+        for g in globs:
+            self.gslot[id(g)] = off
+            off += ((g.buffer.nbytes + 255) // 256) * 256
+        self.gbytes = off
+        self.gdev = N.DeviceBuffer(max(off, 256))
+        self.ghost = N.PinnedArray((max(off, 256),), np.uint8)
+        self.entries = [_LoopEntry(l, mesh, config, self.gslot, self.gdev.ptr) for l in self.loops]
+        self.all_dats = []
+        for e in self.entries:
+            for d in e.dats:
+                if all(d is not x for x in self.all_dats):
+                    self.all_dats.append(d)
+        self.written = []
+        for e in self.entries:
+            for d in e.written:
+                if all(d is not x for x in self.written):
+                    self.written.append(d)
+        descs = (N.MlLoop * max(len(self.entries), 1))(*[e.desc for e in self.entries])
+        handle = C.c_void_p()
+        N.check(N.lib().ml_program_create(descs, len(self.entries), self.ghost.array.ctypes.data,
+                                          self.gdev.ptr, self.gbytes, C.byref(handle)),
+                "ml_program_create")
+        self.handle = handle.value
+        self.ptrs = [e.dat_pointers() for e in self.entries]
+        self.runs = 0
+
+    def valid_for(self, mesh: Mesh) -> bool:
+        if mesh.version != self.version:
+            return False
+        for d in self.all_dats:
+            dat_mirror(d)
+        return [e.dat_pointers() for e in self.entries] == self.ptrs
+
+    def run(self, use_graph: bool, time_loops: bool, force_upload: bool = False):
+        for d in self.all_dats:
+            dat_mirror(d, force_upload=force_upload)
+        hv = self.ghost.array
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            hv[o:o + g.buffer.nbytes] = g.buffer.view(np.uint8)
+        timed = bool(time_loops) and not use_graph
+        N.check(N.lib().ml_program_run(self.handle, int(bool(use_graph)), int(timed)),
+                f"program [{', '.join(l.name for l in self.loops[:4])}...]")
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            g.buffer[:] = hv[o:o + g.buffer.nbytes].view(g.buffer.dtype)
+        for d in self.written:
+            d._dev.device_newer = True
+        self.runs += 1
+        if timed:
+            ms = (C.c_float * max(len(self.entries), 1))()
+            N.check(N.lib().ml_program_loop_times(self.handle, ms))
+            return [float(ms[i]) * 1e-3 for i in range(len(self.entries))]
+        return None
+
+    def replay(self, count: int) -> None:
+        """``count`` back-to-back CUDA-graph replays (device throughput; globals
+        are written back to the host once, after the last replay)."""
+        for d in self.all_dats:
+            dat_mirror(d)
+        hv = self.ghost.array
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            hv[o:o + g.buffer.nbytes] = g.buffer.view(np.uint8)
+        N.check(N.lib().ml_program_replay(self.handle, int(count)), "ml_program_replay")
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            g.buffer[:] = hv[o:o + g.buffer.nbytes].view(g.buffer.dtype)
+        for d in self.written:
+            d._dev.device_newer = True
+        self.runs += count
+
+    def launches_per_run(self) -> int:
+        """Kernel launches one run enqueues (colour launches + reduction combines)."""
+        total = 0
+        for e in self.entries:
+            if e.loop.iter_set.size == 0:
+                continue
+            total += e.plan.ncolors if e.plan.has_writes else 1
+            total += sum(1 for a in e.loop.args if a.kind == "global" and a.mode.name != "READ")
+        return total
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and N._lib is not None:
+            N._lib.ml_program_free(h)
+            self.handle = None
+
+
+_PROGRAM_CACHE_SIZE = 32
+
+
+def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig) -> CompiledProgram:
+    """Compiled program for (loops, block sizes, mesh version), cached on the mesh."""
+    N.init(config.device_index())
+    cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
+    key = (tuple(id(l) for l in program),
+           tuple(config.block_size_for(l.name) for l in program))
+    cp = cache.get(key)
+    if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):
+        cache.move_to_end(key)
+        return cp
+    cp = CompiledProgram(program, mesh, config)
+    cache[key] = cp
+    while len(cache) > _PROGRAM_CACHE_SIZE:
+        cache.popitem(last=False)
+    return cp
+
+
+def _sync_host(dats) -> None:
+    for d in dats:
+        d._pull()
+
+
+def _record(collector: PerfCollector, cp: CompiledProgram, times) -> None:
+    for e, t in zip(cp.entries, times):
+        collector.add(e.loop.name, t, e.useful, nb=e.st.nb, nc=e.st.nc, alg_bytes=e.alg)
+
+
+def run_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig | None = None
+                ) -> RunResult:
+    """Execute a loop program on B200 and collect per-loop device timings."""
+    config = config or BackendConfig()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if config.nranks > 1 or world > 1:
+        from .multigpu import run_program_distributed
+        return run_program_distributed(program, mesh, config)
+    mesh.freeze()
+    t0 = time.perf_counter()
+    collector = PerfCollector()
+    program = list(program)
+    if not program:
+        return RunResult([], 0.0)
+    cp = compile_program(program, mesh, config)
+    if config.phase_callback is not None:
+        for e in cp.entries:
+            for c in range(e.plan.ncolors):
+                config.phase_callback(e.loop.name, c)
+    host = config.residency == "host"
+    times = cp.run(config.use_graph, config.time_loops, force_upload=host)
+    if host:
+        _sync_host(cp.written)
+    if times is not None:
+        _record(collector, cp, times)
+    return RunResult(collector.finalize(), time.perf_counter() - t0)
+
+
+def run_loop(loop: Loop, mesh: Mesh, config: BackendConfig | None = None,
+             collector: PerfCollector | None = None) -> None:
+    """Execute one loop (the per-loop entry of reference executor.py:206/278)."""
+    config = config or BackendConfig()
+    mesh.freeze()
+    cp = compile_program([loop], mesh, config)
+    times = cp.run(False, config.time_loops or collector is not None)
+    if collector is not None and times is not None:
+        _record(collector, cp, times)

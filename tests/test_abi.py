@@ -1,0 +1,66 @@
+"""The C-ABI library loads on a CPU box and exports every symbol the public
+header declares (no device calls here)."""
+from __future__ import annotations
+
+import ctypes as C
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from paper_1403_7209_b200 import _native as N
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "meshloop_b200.h"
+
+
+def declared_functions() -> list[str]:
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ml_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_what_the_binding_exports():
+    assert declared_functions() == sorted(N.EXPORTED)
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = N.lib()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(N.lib_path())], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (ml_[a-z0-9_]+)$", out, flags=re.M))
+    assert set(declared_functions()) <= exported
+
+
+def test_library_is_built_for_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(N.lib_path())], capture_output=True,
+                         text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_functor_registry_and_signatures():
+    table = N.functor_table()
+    names = {n for n, _ in table}
+    for want in ("edge_flux", "copy", "diffusion_update", "boundary_fix", "tri_area",
+                 "distribute", "distribute_int", "sum", "proxy_vflux", "proxy_iflux",
+                 "proxy_grad", "proxy_update", "proxy_dt", "proxy_bc", "proxy_save", "mixmax"):
+        assert want in names, want
+    fid = C.c_int32()
+    assert N.lib().ml_functor_lookup(b"proxy_vflux", N.ML_F64, C.byref(fid)) == 0
+    nargs = C.c_int32()
+    kinds, modes, dims, dts = [(C.c_int32 * 16)() for _ in range(4)]
+    assert N.lib().ml_functor_signature(fid.value, C.byref(nargs), kinds, modes, dims, dts) == 0
+    assert nargs.value == 11
+    assert [dims[i] for i in range(11)] == [3, 6, 6, 18, 18, 3, 3, 19, 19, 6, 6]
+    assert sum(dims[i] for i in range(1, 9)) == 92          # vfluxedge: 92 indirect doubles read
+    assert N.lib().ml_functor_lookup(b"nope", 0, C.byref(fid)) != 0
+    assert b"nope" in N.lib().ml_last_error()
+
+
+def test_device_calls_fail_cleanly_without_init():
+    p = C.c_void_p()
+    rc = N.lib().ml_alloc(16, C.byref(p))
+    assert rc != 0 and b"ml_init" in N.lib().ml_last_error()

@@ -1,0 +1,272 @@
+"""GPU parity: the B200 backend vs the reference golden vectors and the CPU oracle.
+
+Bars: int64 results bit-exact; float64 outputs within
+rtol=1e-12 (reference tests/test_acceptance.py:94-97) — for raw increment
+accumulators, where colouring reorders cancelling sums, within
+1e-12 * max|ref| of the same component as well (``close``).  Everything
+runs through the public API ``run_program`` -> libmeshloop_b200.so.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import _cases
+import paper_1403_7209_b200 as ml
+from conftest import golden
+from oracle import bulk, serial as oserial
+from paper_1403_7209_b200 import apps
+from paper_1403_7209_b200.kernels import device_kernel, resolve_kernel
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+
+
+def close(got, ref, rtol=RTOL, what=""):
+    """rtol 1e-12, plus an absolute floor of 1e-12 * max|ref| per component."""
+    got, ref = np.asarray(got, dtype=np.float64), np.asarray(ref, dtype=np.float64)
+    if ref.ndim == 2:
+        floor = rtol * np.max(np.abs(ref), axis=0, initial=0.0)[None, :]
+    else:
+        floor = rtol * np.max(np.abs(ref), initial=0.0)
+    bad = np.abs(got - ref) > rtol * np.abs(ref) + floor
+    assert not bad.any(), f"{what}: {bad.sum()} mismatches, max |d| {np.max(np.abs(got - ref))}"
+
+
+def cfg(**kw):
+    return ml.BackendConfig(**kw)
+
+
+def _exec_cases():
+    return [c for c in golden("exec.npz").index if c["app"] in ("diffusion", "cell-area")]
+
+
+@pytest.mark.parametrize("case", _exec_cases(), ids=lambda c: c["name"])
+@pytest.mark.parametrize("bs", [256, 16])
+def test_apps_match_reference_golden(case, bs):
+    g = golden("exec.npz")
+    mesh, prog, h = _cases.build_app(case["app"], case["n"], case["dtype"], case["steps"])
+    res = ml.run_program(prog, mesh, cfg(block_size=bs))
+    assert {r.loop for r in res.perf} == {l.name for l in prog}
+    for k, v in _cases.app_results(case["app"], h).items():
+        want = g[f"exec/{case['name']}/{k}"]
+        if case["dtype"] == "int64":
+            np.testing.assert_array_equal(v, want, k)
+        else:
+            close(v, want, what=k)
+
+
+@pytest.mark.parametrize("bs", [1, 3, 32, 100, 256, 512, 1024])
+def test_int64_diffusion_bit_exact_at_every_block_size(bs):
+    g = golden("exec.npz")
+    mesh, prog, h = _cases.build_app("diffusion", 8, "int64", 3)
+    ml.run_program(prog, mesh, cfg(block_size=bs))
+    np.testing.assert_array_equal(h["u"].fetch(), g["exec/diffusion_n8_int64_s3/u"])
+    np.testing.assert_array_equal([r.value for r in h["residuals"]],
+                                  g["exec/diffusion_n8_int64_s3/residuals"])
+
+
+def test_renumbered_diffusion_matches_reference():
+    g = golden("exec.npz")
+    mesh = apps.gen_mesh(10)
+    prog, h = apps.build_diffusion(mesh, 2, dtype="int64")
+    ml.renumber_mesh(mesh)
+    ml.run_program(prog, mesh, cfg())
+    np.testing.assert_array_equal(h["u"].fetch(), g["exec/diffusion_renum_n10_int64/u"])
+
+
+@pytest.mark.parametrize("soa", [4, None, 0])
+def test_mixmax_soa_minmax_read_globals(soa):
+    g = golden("exec.npz")
+    mesh, loop, acc, lo, hi = _cases.mixmax_case(auto_soa_threshold=soa)
+    ml.run_program([loop], mesh, cfg(block_size=8))
+    np.testing.assert_array_equal(acc.fetch(), g["exec/mixmax/acc"])
+    assert [lo.value, hi.value] == g["exec/mixmax/lohi"].tolist()
+
+
+def test_fuzz_meshes_match_reference_and_oracle(rng):
+    g = golden("exec.npz")
+    for case in g.index:
+        if case["app"] != "fuzz":
+            continue
+        mesh, loop = _cases.random_loop_mesh(np.random.default_rng(case["seed"]), max_elems=300)
+        ml.run_program([loop], mesh, cfg(block_size=int(rng.choice([1, 7, 32, 256]))))
+        np.testing.assert_array_equal(mesh.dats["vals"].fetch(), g[f"exec/{case['name']}/vals"])
+    for _ in range(20):
+        seed = int(rng.integers(0, 2 ** 31))
+        ref_mesh, ref_loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=5000)
+        oserial.run_loop(ref_loop)
+        mesh, loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=5000)
+        ml.run_program([loop], mesh, cfg(block_size=int(rng.choice([1, 7, 64, 256, 1024]))))
+        np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref_mesh.dats["vals"].fetch())
+
+
+@pytest.mark.parametrize("N,steps", [(5, 2), (7, 1)])
+def test_proxy_matches_reference_golden(N, steps):
+    g = golden("exec.npz")
+    mesh = apps.gen_hex_mesh(N, seed=4)
+    prog, h = apps.build_hydra_proxy(mesh, steps=steps, seed=4)
+    ml.run_program(prog, mesh, cfg())
+    name = f"proxy_hex{N}_s{steps}"
+    for k in ("q", "q_old", "dt_loc"):
+        close(h[k].fetch(), g[f"exec/{name}/{k}"], what=k)
+    for k in ("res", "grad"):                # zeroed by the update loop: exact
+        np.testing.assert_array_equal(h[k].fetch(), g[f"exec/{name}/{k}"])
+    close([r.value for r in h["rms"]], g[f"exec/{name}/rms"], what="rms")
+    np.testing.assert_array_equal([r.value for r in h["dt_min"]], g[f"exec/{name}/dt_min"])
+
+
+def _proxy_pair(N, seed=0, renumber=True, shuffle=True, soa=4):
+    out = []
+    for _ in range(2):
+        mesh = apps.gen_hex_mesh(N, seed=seed, auto_soa_threshold=soa)
+        if shuffle:
+            apps.shuffle_mesh(mesh, seed=seed + 1)
+        prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=seed)
+        if renumber:
+            ml.renumber_mesh(mesh)
+        out.append((mesh, prog, h))
+    return out
+
+
+@pytest.mark.parametrize("soa", [4, None, 0])
+def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa):
+    """Stop before the update so the raw INC accumulators (res, grad) are compared."""
+    (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, soa=soa)
+    bulk.run_program(rprog[:5], resolve_kernel)
+    ml.run_program(prog[:5], mesh, cfg())
+    for k in ("grad", "res", "q_old", "dt_loc"):
+        close(h[k].fetch(), rh[k].fetch(), what=k)
+    np.testing.assert_array_equal(h["dt_min"][0].value, rh["dt_min"][0].value)
+
+
+def test_proxy_full_size_iteration_vs_oracle():
+    """Config B (Rotor37-sized, 2.47M edges): one full iteration, shuffled + CM-renumbered."""
+    (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(94, seed=0)
+    bulk.run_program(rprog, resolve_kernel)
+    ml.run_program(prog, mesh, cfg())
+    close(h["q"].fetch(), rh["q"].fetch(), what="q")
+    close([h["rms"][0].value], [rh["rms"][0].value], what="rms")
+    assert h["dt_min"][0].value == rh["dt_min"][0].value
+
+
+def test_int64_diffusion_rotor37_size_bit_exact():
+    """gen_mesh(913): 835,396 nodes / 2,502,533 edges, int64 twin, bit-exact vs oracle."""
+    ref = apps.gen_mesh(913)
+    rprog, rh = apps.build_diffusion(ref, 2, dtype="int64")
+    bulk.run_program(rprog, resolve_kernel)
+    mesh = apps.gen_mesh(913)
+    prog, h = apps.build_diffusion(mesh, 2, dtype="int64")
+    ml.run_program(prog, mesh, cfg())
+    np.testing.assert_array_equal(h["u"].fetch(), rh["u"].fetch())
+    assert [r.value for r in h["residuals"]] == [r.value for r in rh["residuals"]]
+
+
+def test_colouring_stress_hub_and_shuffled_meshes():
+    for make in (lambda: apps.gen_hub_mesh(20000, 200000, n_hubs=4, hub_share=0.05, seed=2),
+                 lambda: _shuffled_hex(30)):
+        ref, mesh = make(), make()
+        rl, l = _cases.inc_loop(ref, "edge_nodes"), _cases.inc_loop(mesh, "edge_nodes")
+        oserial.run_loop(rl)
+        res = ml.run_program([l], mesh, cfg())
+        np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
+        assert res.perf[0].nc > 8
+
+
+def _shuffled_hex(N):
+    m = apps.gen_hex_mesh(N)
+    apps.shuffle_mesh(m, seed=9)
+    return m
+
+
+def test_empty_iteration_set_is_a_noop():
+    mesh = ml.Mesh()
+    nodes = mesh.decl_set("nodes", 5)
+    none = mesh.decl_set("none", 0)
+    m = mesh.decl_map("en", none, nodes, 1, [])
+    vals = mesh.decl_dat("vals", nodes, 1, "int64", np.arange(5))
+    loop = _cases.inc_loop(mesh, "en", "vals")
+    total = ml.Global(np.int64(7))
+    z = mesh.decl_dat("z", none, 1, "int64", [])
+    cnt = ml.Loop("cnt", none, [ml.arg_direct(z, ml.READ), ml.arg_global(total, ml.INC)],
+                  apps._k_sum)
+    ml.run_program([loop, cnt], mesh, cfg())
+    np.testing.assert_array_equal(vals.fetch().ravel(), np.arange(5))
+    assert total.value == 7
+
+
+def test_direct_loop_is_exact_even_in_float():
+    @device_kernel("scale_rw")
+    def scale(v):
+        v[0] = v[0] * 1.0000001 + 0.25
+    mesh = ml.Mesh()
+    d = mesh.decl_dat("d", mesh.decl_set("s", 100000), 1, "float64", np.linspace(0.0, 1.0, 100000))
+    want = np.linspace(0.0, 1.0, 100000) * 1.0000001 + 0.25
+    ml.run_program([ml.Loop("scale", d.set, [ml.arg_direct(d, ml.RW)], scale)], mesh, cfg(block_size=64))
+    np.testing.assert_array_equal(d.fetch().ravel(), want)
+
+
+def test_float_results_are_deterministic_run_to_run():
+    outs = []
+    for _ in range(2):
+        mesh = apps.gen_hex_mesh(24, seed=1)
+        prog, h = apps.build_hydra_proxy(mesh, steps=3, seed=1)
+        ml.run_program(prog, mesh, cfg())
+        outs.append((h["q"].fetch(), [r.value for r in h["rms"]]))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
+
+
+def test_graph_replay_and_host_residency_match_eager():
+    results = []
+    for kw in ({}, {"use_graph": True}, {"residency": "host"}):
+        mesh = apps.gen_hex_mesh(12, seed=2)
+        prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=2)
+        for _ in range(3):                   # replayed: state advances identically
+            ml.run_program(prog, mesh, cfg(**kw))
+        results.append((h["q"].fetch(), h["rms"][0].value))
+    for q, r in results[1:]:
+        np.testing.assert_array_equal(q, results[0][0])
+        assert r == results[0][1]
+
+
+def test_host_writes_between_runs_are_uploaded():
+    mesh = apps.gen_mesh(6)
+    prog, h = apps.build_diffusion(mesh, 1, dtype="int64")
+    ml.run_program(prog, mesh, cfg())
+    h["u"].put(np.zeros((mesh.sets["nodes"].size, 1), np.int64))      # host write
+    h["bc_values"].data[:] = 0                                        # write through .data
+    h["residuals"][0].buffer[:] = 0
+    ml.run_program(prog, mesh, cfg())
+    assert h["residuals"][0].value == 0
+    np.testing.assert_array_equal(h["u"].fetch(), 0)
+
+
+def test_unbound_kernel_raises_exec_error():
+    mesh = ml.Mesh()
+    d = mesh.decl_dat("d", mesh.decl_set("s", 4), 1, "float64", np.zeros(4))
+    with pytest.raises(ml.ExecError, match="no device functor"):
+        ml.run_program([ml.Loop("x", d.set, [ml.arg_direct(d, ml.RW)], lambda v: None)], mesh)
+
+
+def test_signature_mismatch_raises_exec_error():
+    mesh = ml.Mesh()
+    s = mesh.decl_set("s", 4)
+    d = mesh.decl_dat("d", s, 2, "float64", np.zeros(8))
+    with pytest.raises(ml.ExecError, match="expects"):
+        ml.run_program([ml.Loop("x", s, [ml.arg_direct(d, ml.RW)], apps._k_copy)], mesh)
+
+
+def test_perf_records_and_report_schema(tmp_path):
+    import json
+    mesh = apps.gen_mesh(16)
+    prog, _ = apps.build_cell_area(mesh, "float64")
+    out = ml.run_program(prog, mesh, cfg())
+    assert sum(r.pct_runtime for r in out.perf) == pytest.approx(100.0, abs=0.01)
+    assert all(r.time_sec > 0 and r.gb_per_sec > 0 for r in out.perf)
+    path = tmp_path / "r.json"
+    ml.emit_report(out.perf, path, config={"backend": "cuda"},
+                   mesh_sets={n: s.size for n, s in mesh.sets.items()})
+    assert {l["loop"] for l in json.loads(path.read_text())["loops"]} == \
+        {"area_calc", "area_distribute", "area_total"}

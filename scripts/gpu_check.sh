@@ -1,0 +1,20 @@
+#!/usr/bin/env bash
+# One gpurun call: smoke, GPU tests, bench, ncu launch list + full capture of the top loop.
+# Usage (from the build container):
+#   /usr/local/graft/bin/gpurun --timeout 2400 -- bash scripts/gpu_check.sh [tag]
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
+python -c "import __graft_entry__ as g; g.build()" > "$OUT/build.log" 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?" >> "$OUT/status.txt"
+timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider --durations=15 > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/status.txt"
+timeout 600 python bench.py --steps 20 --warmup 3 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/status.txt"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
+    python bench.py --steps 2 --warmup 1 --no-cpu > "$OUT/bench_ncu.log" 2>&1; echo "ncu-list rc=$?" >> "$OUT/status.txt"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ProxyVflux -s 10 -c 2 \
+    -o "$OUT/vflux" python bench.py --steps 1 --warmup 1 --no-cpu > "$OUT/ncu_full.log" 2>&1; echo "ncu-full rc=$?" >> "$OUT/status.txt"
+cat "$OUT/status.txt"
+tail -3 "$OUT/pytest_gpu.log"
+cat "$OUT/bench.json"

@@ -66,6 +66,21 @@ typedef struct ml_plan_dev {
     const int32_t *elem_ncolors;    /* device [nblocks]; NULL likewise          */
 } ml_plan_dev_t;
 
+/* Shared-memory staging of indirect increments (optional; ngroups == 0 turns
+ * it off).  A group is one dat written with INC through a map: per block the
+ * sorted unique targets (`off`/`list`, from ml_staging_build) and, per INC
+ * argument, the local position of each element's target (`loc`). */
+#define ML_MAX_ARGS 16
+#define ML_MAX_GROUPS 2
+typedef struct ml_staging_dev {
+    int32_t ngroups;
+    int32_t group[ML_MAX_ARGS];          /* group of each arg, -1 if not staged  */
+    const int32_t *off[ML_MAX_GROUPS];   /* device [nblocks+1]                    */
+    const int32_t *list[ML_MAX_GROUPS];  /* device unique targets                 */
+    int32_t umax[ML_MAX_GROUPS];         /* max unique targets in one block       */
+    const uint16_t *loc[ML_MAX_ARGS];    /* device [n] per staged arg             */
+} ml_staging_dev_t;
+
 typedef struct ml_loop {
     const char *name;               /* for error messages                       */
     int32_t functor;                /* id from ml_functor_lookup                */
@@ -76,6 +91,10 @@ typedef struct ml_loop {
     double fconst[4];               /* kernel constants (e.g. dt)               */
     int64_t iconst[4];              /* kernel constants (e.g. integer scale)    */
     void *scratch;                  /* device scratch >= ml_loop_scratch_bytes  */
+    ml_staging_dev_t staging;
+    int64_t rlim;                   /* elements >= rlim skip global reductions
+                                       (exec-halo elements on multi-GPU runs);
+                                       < 0 means n                               */
 } ml_loop_t;
 
 typedef struct ml_device_info {
@@ -123,6 +142,17 @@ int ml_plan_export(const ml_plan_t *p, int64_t *block_color, int64_t *elem_ncolo
                    int64_t *color_offsets, int64_t *blocks_by_color,
                    int64_t *elem_color, int64_t *block_elem_order);
 int ml_plan_free(ml_plan_t *p);
+
+/* Staging lists for shared-memory increment accumulation (derived from the
+ * plan's blocking; the plan itself is unchanged).  `col_group[j]` assigns the
+ * j-th INC column to a group (one group per INC dat). */
+typedef struct ml_staging ml_staging_t;
+int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols, const int64_t *const *cols,
+                     const int32_t *col_group, ml_staging_t **out);
+int ml_staging_sizes(const ml_staging_t *s, int32_t group, int64_t *total, int64_t *umax);
+int ml_staging_export(const ml_staging_t *s, int32_t group, int32_t *off, int32_t *list);
+int ml_staging_export_loc(const ml_staging_t *s, int32_t col, uint16_t *loc);
+int ml_staging_free(ml_staging_t *s);
 
 /* ---- renumbering: renumber.py:53-128 ------------------------------------- */
 /* Co-occurrence adjacency of a set from `nmaps` tables that target it

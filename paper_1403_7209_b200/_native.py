@@ -29,6 +29,8 @@ EXPORTED = [
     "ml_alloc", "ml_free", "ml_host_alloc", "ml_host_free", "ml_upload", "ml_download",
     "ml_memset", "ml_map_upload",
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
+    "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
+    "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
     "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name",
     "ml_loop_scratch_bytes", "ml_loop_run",
@@ -51,10 +53,20 @@ class MlPlanDev(C.Structure):
                 ("elem_color", C.c_void_p), ("elem_ncolors", C.c_void_p)]
 
 
+MAX_ARGS, MAX_GROUPS = 16, 2
+
+
+class MlStagingDev(C.Structure):
+    _fields_ = [("ngroups", C.c_int32), ("group", C.c_int32 * MAX_ARGS),
+                ("off", C.c_void_p * MAX_GROUPS), ("list", C.c_void_p * MAX_GROUPS),
+                ("umax", C.c_int32 * MAX_GROUPS), ("loc", C.c_void_p * MAX_ARGS)]
+
+
 class MlLoop(C.Structure):
     _fields_ = [("name", C.c_char_p), ("functor", C.c_int32), ("nargs", C.c_int32),
                 ("args", C.POINTER(MlArg)), ("n", C.c_int64), ("plan", MlPlanDev),
-                ("fconst", C.c_double * 4), ("iconst", C.c_int64 * 4), ("scratch", C.c_void_p)]
+                ("fconst", C.c_double * 4), ("iconst", C.c_int64 * 4), ("scratch", C.c_void_p),
+                ("staging", MlStagingDev), ("rlim", C.c_int64)]
 
 
 class MlDeviceInfo(C.Structure):
@@ -85,6 +97,11 @@ _SIGNATURES = {
     "ml_plan_sizes": (C.c_int, [_P, _I64P, _I64P, _I64P]),
     "ml_plan_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "ml_plan_free": (C.c_int, [_P]),
+    "ml_staging_build": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, _PP, _I32P, _PP]),
+    "ml_staging_sizes": (C.c_int, [_P, C.c_int32, _I64P, _I64P]),
+    "ml_staging_export": (C.c_int, [_P, C.c_int32, _P, _P]),
+    "ml_staging_export_loc": (C.c_int, [_P, C.c_int32, _P]),
+    "ml_staging_free": (C.c_int, [_P]),
     "ml_co_occurrence": (C.c_int, [C.c_int64, C.c_int32, _PP, _I64P, _I32P, _P, _P, _I64P]),
     "ml_cm_order": (C.c_int, [C.c_int64, _P, _P, _P]),
     "ml_functor_lookup": (C.c_int, [C.c_char_p, C.c_int32, _I32P]),

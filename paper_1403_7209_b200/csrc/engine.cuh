@@ -67,10 +67,27 @@ struct Consts {
     int64_t i[4];
 };
 
+constexpr int MAX_GROUPS = 2;
+
+// Shared-memory staging of indirect increments (OP2-style): per block, the
+// sorted unique targets of each INC dat ("group") and, per element and INC
+// argument, the target's position in that list.
+struct Staging {
+    int32_t group[MAX_ARGS];             // staging group of each arg (-1: none)
+    int32_t leader[MAX_ARGS];            // 1 on the arg that writes its group back
+    const int32_t *off[MAX_GROUPS];      // [nblocks+1] offsets into list
+    const int32_t *list[MAX_GROUPS];     // unique targets, ascending per block
+    const uint16_t *loc[MAX_ARGS];       // [n] local position of the arg's target
+    int32_t umax[MAX_GROUPS];            // max unique targets per block (smem stride)
+    int32_t soff[MAX_GROUPS];            // byte offset of the group in dynamic smem
+};
+
 struct LaunchParams {
     ArgRt a[MAX_ARGS];
     void *part[MAX_ARGS];       // reduction partials [nblocks][dim] per global reduce arg
+    Staging st;
     int64_t n;
+    int64_t rlim;               // elements >= rlim do not contribute to reductions
     int32_t bs;
     const int32_t *blocks;      // block ids of this launch (nullptr: identity)
     const uint16_t *ecol;       // element colours
@@ -105,15 +122,22 @@ __device__ __forceinline__ T combine(T a, T b) {
 }
 
 // ---- per-argument slot --------------------------------------------------------
-template <class A, bool STAGE_INC>
+// MODE 0: no staging (views into HBM); 1: indirect INC staged in registers and
+// applied to HBM in colour phases; 2: staged in registers, applied to shared
+// memory in colour phases, written back once per block.
+enum : int { ST_NONE = 0, ST_REG = 1, ST_SMEM = 2 };
+
+template <class A, int MODE>
 struct Slot {
     using T = typename A::type;
     static constexpr bool is_global = A::kind == KG;
     static constexpr bool is_reduce = is_global && A::mode != MR;
-    static constexpr bool staged = (A::kind == KI && A::mode == MINC && STAGE_INC) || is_reduce;
+    static constexpr bool is_inc = A::kind == KI && A::mode == MINC;
+    static constexpr bool staged = (is_inc && MODE != ST_NONE) || is_reduce;
 
     T acc[staged ? A::dim : 1];
-    T *ptr;          // element base pointer (non-staged dat / global READ)
+    T bak[is_reduce ? A::dim : 1];
+    T *ptr;          // element base pointer (HBM or shared memory)
     int64_t sc;
 
     __device__ __forceinline__ void init_global(const LaunchParams &p, int i) {
@@ -125,12 +149,18 @@ struct Slot {
             sc = 1;
         }
     }
-    __device__ __forceinline__ void init_elem(const LaunchParams &p, int i, int64_t e) {
+    __device__ __forceinline__ void init_elem(const LaunchParams &p, int i, int64_t e, char *smem) {
         if constexpr (!is_global) {
-            const ArgRt &r = p.a[i];
-            const int64_t t = A::kind == KI ? int64_t(__ldg(r.map + e)) : e;
-            ptr = static_cast<T *>(r.data) + t * r.se;
-            sc = r.sc;
+            if constexpr (is_inc && MODE == ST_SMEM) {
+                const int g = p.st.group[i];
+                ptr = reinterpret_cast<T *>(smem + p.st.soff[g]) + __ldg(p.st.loc[i] + e);
+                sc = p.st.umax[g];
+            } else {
+                const ArgRt &r = p.a[i];
+                const int64_t t = A::kind == KI ? int64_t(__ldg(r.map + e)) : e;
+                ptr = static_cast<T *>(r.data) + t * r.se;
+                sc = r.sc;
+            }
             if constexpr (staged) {
 #pragma unroll
                 for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
@@ -150,6 +180,43 @@ struct Slot {
         if constexpr (staged && !is_global) {
 #pragma unroll
             for (int c = 0; c < A::dim; ++c) ptr[c * sc] += acc[c];
+        }
+    }
+    __device__ __forceinline__ void backup() {
+        if constexpr (is_reduce) {
+#pragma unroll
+            for (int c = 0; c < A::dim; ++c) bak[c] = acc[c];
+        }
+    }
+    __device__ __forceinline__ void restore() {
+        if constexpr (is_reduce) {
+#pragma unroll
+            for (int c = 0; c < A::dim; ++c) acc[c] = bak[c];
+        }
+    }
+    // shared memory -> HBM, once per block (MODE 2, group leader only)
+    __device__ __forceinline__ void zero_smem(const LaunchParams &p, int i, int32_t b, char *smem) {
+        if constexpr (is_inc && MODE == ST_SMEM) {
+            const int g = p.st.group[i];
+            if (!p.st.leader[i]) return;
+            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo, um = p.st.umax[g];
+            T *s = reinterpret_cast<T *>(smem + p.st.soff[g]);
+            for (int k = threadIdx.x; k < u * A::dim; k += blockDim.x) s[(k / u) * um + (k % u)] = T(0);
+        }
+    }
+    __device__ __forceinline__ void write_back(const LaunchParams &p, int i, int32_t b, char *smem) {
+        if constexpr (is_inc && MODE == ST_SMEM) {
+            const int g = p.st.group[i];
+            if (!p.st.leader[i]) return;
+            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo, um = p.st.umax[g];
+            const T *s = reinterpret_cast<const T *>(smem + p.st.soff[g]);
+            const int32_t *list = p.st.list[g] + lo;
+            const ArgRt &r = p.a[i];
+            T *d = static_cast<T *>(r.data);
+            for (int k = threadIdx.x; k < u * A::dim; k += blockDim.x) {
+                const int c = k / u, j = k % u;
+                d[int64_t(__ldg(list + j)) * r.se + c * r.sc] += s[c * um + j];
+            }
         }
     }
 };
@@ -172,9 +239,9 @@ __device__ __forceinline__ T block_reduce(T v, T *smem_t) {
     return v;   // valid in thread 0
 }
 
-template <class F, bool STAGE_INC, class... As>
+template <class F, int MODE, class... As>
 struct Engine {
-    using Slots = cuda::std::tuple<Slot<As, STAGE_INC>...>;
+    using Slots = cuda::std::tuple<Slot<As, MODE>...>;
     static constexpr int N = sizeof...(As);
 
     template <size_t... Is>
@@ -184,13 +251,38 @@ struct Engine {
     }
     template <size_t... Is>
     __device__ __forceinline__ static void init_elem(Slots &s, const LaunchParams &p, int64_t e,
-                                                     cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).init_elem(p, int(Is), e), ...);
+                                                     char *smem, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).init_elem(p, int(Is), e, smem), ...);
     }
     template <size_t... Is>
-    __device__ __forceinline__ static void call(Slots &s, const LaunchParams &p,
-                                                cuda::std::index_sequence<Is...>) {
+    __device__ __forceinline__ static void call_raw(Slots &s, const LaunchParams &p,
+                                                    cuda::std::index_sequence<Is...>) {
         F::apply(p.k, cuda::std::get<Is>(s).view()...);
+    }
+    // apply the functor; contributions of elements past p.rlim (multi-GPU exec
+    // halo) to global reductions are discarded (reference executor.py:519-524)
+    template <size_t... Is>
+    __device__ __forceinline__ static void call(Slots &s, const LaunchParams &p, int64_t e,
+                                                cuda::std::index_sequence<Is...> idx) {
+        if constexpr (((As::kind == KG && As::mode != MR) || ...)) {
+            if (e >= p.rlim) {
+                (cuda::std::get<Is>(s).backup(), ...);
+                call_raw(s, p, idx);
+                (cuda::std::get<Is>(s).restore(), ...);
+                return;
+            }
+        }
+        call_raw(s, p, idx);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void zero_smem(Slots &s, const LaunchParams &p, int32_t b,
+                                                     char *smem, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).zero_smem(p, int(Is), b, smem), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void write_back(Slots &s, const LaunchParams &p, int32_t b,
+                                                      char *smem, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).write_back(p, int(Is), b, smem), ...);
     }
     template <size_t... Is>
     __device__ __forceinline__ static void apply_staged(Slots &s, cuda::std::index_sequence<Is...>) {
@@ -221,7 +313,7 @@ struct Engine {
 
 template <class F, class... As>
 __device__ __forceinline__ void run_direct(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, false, As...>;
+    using E = Engine<F, ST_NONE, As...>;
     __shared__ double smem[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     const int32_t b = blockIdx.x;
@@ -229,15 +321,15 @@ __device__ __forceinline__ void run_direct(const LaunchParams &p, Sig<As...>) {
     typename E::Slots s;
     E::init_globals(s, p, idx);
     for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-        E::init_elem(s, p, e, idx);
-        E::call(s, p, idx);
+        E::init_elem(s, p, e, nullptr, idx);
+        E::call(s, p, e, idx);
     }
     if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
 }
 
 template <class F, class... As>
 __device__ __forceinline__ void run_staged(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, true, As...>;
+    using E = Engine<F, ST_REG, As...>;
     __shared__ double smem[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     const int32_t b = p.blocks[blockIdx.x];
@@ -249,8 +341,8 @@ __device__ __forceinline__ void run_staged(const LaunchParams &p, Sig<As...>) {
     typename E::Slots s;
     E::init_globals(s, p, idx);
     if (active) {
-        E::init_elem(s, p, e, idx);
-        E::call(s, p, idx);
+        E::init_elem(s, p, e, nullptr, idx);
+        E::call(s, p, e, idx);
     }
     if (ncol == 1) {
         if (active) E::apply_staged(s, idx);
@@ -263,9 +355,39 @@ __device__ __forceinline__ void run_staged(const LaunchParams &p, Sig<As...>) {
     if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
 }
 
+// Increments staged in shared memory: compute -> colour phases into smem ->
+// one coalesced read-modify-write of the block's unique targets.
+template <class F, class... As>
+__device__ __forceinline__ void run_smem(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_SMEM, As...>;
+    __shared__ double red[32];
+    extern __shared__ __align__(16) char dsm[];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const int32_t b = p.blocks[blockIdx.x];
+    const int64_t e = int64_t(b) * p.bs + threadIdx.x;
+    const int64_t hi = int64_t(b) * p.bs + p.bs < p.n ? int64_t(b) * p.bs + p.bs : p.n;
+    const bool active = threadIdx.x < p.bs && e < hi;
+    const int ncol = p.encol[b];
+    const int mine = active ? int(p.ecol[e]) : -1;
+    typename E::Slots s;
+    E::zero_smem(s, p, b, dsm, idx);
+    E::init_globals(s, p, idx);
+    if (active) {
+        E::init_elem(s, p, e, dsm, idx);
+        E::call(s, p, e, idx);
+    }
+    __syncthreads();
+    for (int c = 0; c < ncol; ++c) {
+        if (mine == c) E::apply_staged(s, idx);
+        __syncthreads();
+    }
+    E::write_back(s, p, b, dsm, idx);
+    if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
+}
+
 template <class F, class... As>
 __device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, false, As...>;
+    using E = Engine<F, ST_NONE, As...>;
     __shared__ double smem[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     const int32_t b = p.blocks[blockIdx.x];
@@ -276,8 +398,8 @@ __device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
     for (int c = 0; c < ncol; ++c) {
         for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
             if (int(p.ecol[e]) != c) continue;
-            E::init_elem(s, p, e, idx);
-            E::call(s, p, idx);
+            E::init_elem(s, p, e, nullptr, idx);
+            E::call(s, p, e, idx);
         }
         __syncthreads();
     }
@@ -296,6 +418,10 @@ template <class F, class T>
 __global__ void __launch_bounds__(256) k_phased(const __grid_constant__ LaunchParams p) {
     run_phased<F>(p, typename F::template sig<T>{});
 }
+template <class F, class T>
+__global__ void __launch_bounds__(256) k_smem(const __grid_constant__ LaunchParams p) {
+    run_smem<F>(p, typename F::template sig<T>{});
+}
 
 // ---- compile-time signature introspection -------------------------------------
 template <class S>
@@ -313,7 +439,7 @@ struct SigInfo<Sig<As...>> {
 };
 
 // ---- registry -------------------------------------------------------------------
-using LaunchFn = void (*)(const LaunchParams &, dim3, dim3, cudaStream_t);
+using LaunchFn = void (*)(const LaunchParams &, dim3, dim3, size_t, cudaStream_t);
 
 struct FunctorEntry {
     const char *name;
@@ -321,21 +447,29 @@ struct FunctorEntry {
     int32_t nargs;
     int32_t kind[MAX_ARGS], mode[MAX_ARGS], dim[MAX_ARGS], atype[MAX_ARGS];
     bool ind_write, ind_write_non_inc;
-    LaunchFn direct, staged, phased;
+    LaunchFn direct, staged, phased, smem;
 };
 
 void register_functor(const FunctorEntry &e);
 
 template <class F, class T>
 struct Registrar {
-    static void direct(const LaunchParams &p, dim3 g, dim3 b, cudaStream_t s) {
+    static void direct(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_direct<F, T><<<g, b, 0, s>>>(p);
     }
-    static void staged(const LaunchParams &p, dim3 g, dim3 b, cudaStream_t s) {
+    static void staged(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_staged<F, T><<<g, b, 0, s>>>(p);
     }
-    static void phased(const LaunchParams &p, dim3 g, dim3 b, cudaStream_t s) {
+    static void phased(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_phased<F, T><<<g, b, 0, s>>>(p);
+    }
+    static void smem(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
+        static bool opted = false;
+        if (!opted && bytes > 48 * 1024) {
+            cudaFuncSetAttribute(k_smem<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            opted = true;
+        }
+        k_smem<F, T><<<g, b, bytes, s>>>(p);
     }
     explicit Registrar(const char *name) {
         using S = typename F::template sig<T>;
@@ -349,6 +483,7 @@ struct Registrar {
         e.direct = &direct;
         e.staged = SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc ? &staged : nullptr;
         e.phased = SigInfo<S>::ind_write ? &phased : nullptr;
+        e.smem = e.staged ? &smem : nullptr;
         register_functor(e);
     }
 };

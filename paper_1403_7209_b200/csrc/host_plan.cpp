@@ -255,3 +255,83 @@ extern "C" int ml_plan_free(ml_plan_t *p) {
     delete p;
     return ML_OK;
 }
+
+// ---- staging lists for shared-memory increment accumulation -------------------------
+// Per block and per group (one INC dat), the ascending unique targets of the
+// group's columns over the block's elements, and for every (element, column)
+// the target's position in that list (uint16: a block has <= 65535 targets).
+struct ml_staging {
+    int64_t n = 0, bs = 1, nb = 0;
+    int32_t ngroups = 0;
+    std::vector<std::vector<int32_t>> off, list;   // per group
+    std::vector<int64_t> umax;                     // per group
+    std::vector<std::vector<uint16_t>> loc;        // per column
+};
+
+extern "C" int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols,
+                                const int64_t *const *cols, const int32_t *col_group,
+                                ml_staging_t **out) {
+    if (!out || block_size < 1 || n < 0 || ncols < 0) ML_FAIL(ML_EINVAL, "ml_staging_build: bad arguments");
+    ML_GUARD_BEGIN
+    auto s = std::make_unique<ml_staging>();
+    s->n = n;
+    s->bs = block_size;
+    s->nb = n ? (n + block_size - 1) / block_size : 0;
+    int32_t ng = 0;
+    for (int32_t j = 0; j < ncols; ++j) ng = std::max(ng, col_group[j] + 1);
+    s->ngroups = ng;
+    s->off.assign(ng, std::vector<int32_t>(size_t(s->nb) + 1, 0));
+    s->list.assign(ng, {});
+    s->umax.assign(ng, 0);
+    s->loc.assign(ncols, std::vector<uint16_t>(size_t(n), 0));
+    std::vector<int64_t> buf;
+    for (int32_t g = 0; g < ng; ++g) {
+        auto &list = s->list[g];
+        for (int64_t b = 0; b < s->nb; ++b) {
+            const int64_t lo = b * block_size, hi = std::min(n, lo + block_size);
+            buf.clear();
+            for (int32_t j = 0; j < ncols; ++j)
+                if (col_group[j] == g)
+                    for (int64_t e = lo; e < hi; ++e) buf.push_back(cols[j][e]);
+            std::sort(buf.begin(), buf.end());
+            buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
+            if (buf.size() > 65535) throw std::length_error("more than 65535 staged targets in one block");
+            if (buf.size() && buf.back() >= (int64_t(1) << 31)) throw std::length_error("target id exceeds int32");
+            s->umax[g] = std::max<int64_t>(s->umax[g], int64_t(buf.size()));
+            for (int32_t j = 0; j < ncols; ++j)
+                if (col_group[j] == g)
+                    for (int64_t e = lo; e < hi; ++e)
+                        s->loc[j][e] = uint16_t(std::lower_bound(buf.begin(), buf.end(), cols[j][e]) - buf.begin());
+            for (int64_t t : buf) list.push_back(int32_t(t));
+            s->off[g][b + 1] = int32_t(list.size());
+        }
+    }
+    *out = s.release();
+    return ML_OK;
+    ML_GUARD_END
+}
+
+extern "C" int ml_staging_sizes(const ml_staging_t *s, int32_t g, int64_t *total, int64_t *umax) {
+    if (!s || g < 0 || g >= s->ngroups) ML_FAIL(ML_EINVAL, "ml_staging_sizes: bad group");
+    if (total) *total = int64_t(s->list[g].size());
+    if (umax) *umax = s->umax[g];
+    return ML_OK;
+}
+
+extern "C" int ml_staging_export(const ml_staging_t *s, int32_t g, int32_t *off, int32_t *list) {
+    if (!s || g < 0 || g >= s->ngroups) ML_FAIL(ML_EINVAL, "ml_staging_export: bad group");
+    if (off) std::copy(s->off[g].begin(), s->off[g].end(), off);
+    if (list) std::copy(s->list[g].begin(), s->list[g].end(), list);
+    return ML_OK;
+}
+
+extern "C" int ml_staging_export_loc(const ml_staging_t *s, int32_t col, uint16_t *loc) {
+    if (!s || col < 0 || col >= int32_t(s->loc.size())) ML_FAIL(ML_EINVAL, "ml_staging_export_loc: bad column");
+    std::copy(s->loc[col].begin(), s->loc[col].end(), loc);
+    return ML_OK;
+}
+
+extern "C" int ml_staging_free(ml_staging_t *s) {
+    delete s;
+    return ML_OK;
+}

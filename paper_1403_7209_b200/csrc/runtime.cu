@@ -117,7 +117,9 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
 
     LaunchParams p{};
     p.n = L->n;
+    p.rlim = L->rlim < 0 ? L->n : L->rlim;
     p.bs = int32_t(bs);
+    for (int i = 0; i < MAX_ARGS; ++i) p.st.group[i] = -1;
     for (int i = 0; i < 4; ++i) {
         p.k.f[i] = L->fconst[i];
         p.k.i[i] = L->iconst[i];
@@ -145,22 +147,57 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         }
     }
 
+    // shared-memory staging of INC increments (every INC-indirect arg in a group)
+    size_t smem_bytes = 0;
+    bool use_smem = false;
+    const ml_staging_dev_t &sg = L->staging;
+    if (f.smem && bs <= 256 && sg.ngroups > 0 && sg.ngroups <= MAX_GROUPS) {
+        use_smem = true;
+        bool seen[MAX_GROUPS] = {false, false};
+        for (int i = 0; i < f.nargs; ++i) {
+            const bool inc = f.kind[i] == KI && f.mode[i] == MINC;
+            const int g = sg.group[i];
+            if (inc != (g >= 0) || g >= sg.ngroups || (inc && !sg.loc[i])) {
+                use_smem = false;
+                break;
+            }
+            if (g < 0) continue;
+            p.st.group[i] = g;
+            p.st.loc[i] = sg.loc[i];
+            if (!seen[g]) {
+                seen[g] = true;
+                p.st.leader[i] = 1;
+                p.st.off[g] = sg.off[g];
+                p.st.list[g] = sg.list[g];
+                p.st.umax[g] = sg.umax[g];
+                p.st.soff[g] = int32_t(smem_bytes);
+                smem_bytes += (size_t(sg.umax[g]) * f.dim[i] * 8 + 15) / 16 * 16;
+            }
+        }
+        if (!use_smem || smem_bytes > 200 * 1024) {
+            use_smem = false;
+            smem_bytes = 0;
+            for (int i = 0; i < MAX_ARGS; ++i) p.st.group[i] = -1;
+        }
+    }
+
     if (!f.ind_write) {
         const int threads = std::clamp(round_up32(bs), 32, 256);
         p.blocks = nullptr;
-        f.direct(p, dim3(unsigned(nb)), dim3(unsigned(threads)), stream);
+        f.direct(p, dim3(unsigned(nb)), dim3(unsigned(threads)), 0, stream);
     } else {
         if (!L->plan.color_offsets || !L->plan.blocks || !L->plan.elem_color || !L->plan.elem_ncolors)
             ML_FAIL(ML_EINVAL, "loop '%s': indirect writes need a coloured plan", L->name);
         p.ecol = L->plan.elem_color;
         p.encol = L->plan.elem_ncolors;
         const bool staged = f.staged && bs <= 256;
+        const LaunchFn fn = use_smem ? f.smem : (staged ? f.staged : f.phased);
         const int threads = staged ? round_up32(bs) : std::clamp(round_up32(bs), 32, 256);
         for (int64_t c = 0; c < L->plan.ncolors; ++c) {
             const int64_t off = L->plan.color_offsets[c], cnt = L->plan.color_offsets[c + 1] - off;
             if (cnt <= 0) continue;
             p.blocks = L->plan.blocks + off;
-            (staged ? f.staged : f.phased)(p, dim3(unsigned(cnt)), dim3(unsigned(threads)), stream);
+            fn(p, dim3(unsigned(cnt)), dim3(unsigned(threads)), smem_bytes, stream);
         }
     }
     cudaError_t err = cudaGetLastError();

@@ -125,6 +125,71 @@ def plan_mirror(plan) -> PlanMirror:
     return plan._dev
 
 
+class StagingMirror:
+    """Device staging lists of one loop's INC arguments (see ml_staging_build).
+
+    ``group[i]`` is the staging group of argument i (one group per INC dat),
+    -1 for arguments that are not indirect INC."""
+
+    __slots__ = ("group", "ngroups", "off", "list", "umax", "loc")
+
+    def __init__(self, loop, plan):
+        import ctypes as C
+        inc = [i for i, a in enumerate(loop.args) if a.kind == "indirect" and a.mode.name == "INC"]
+        names: list[str] = []
+        self.group = [-1] * len(loop.args)
+        for i in inc:
+            nm = loop.args[i].dat.name
+            if nm not in names:
+                names.append(nm)
+            self.group[i] = names.index(nm)
+        self.ngroups = len(names)
+        cols = [np.ascontiguousarray(loop.args[i].map.table[:plan.n, loop.args[i].slot], dtype=np.int64)
+                for i in inc]
+        cgrp = np.array([self.group[i] for i in inc], dtype=np.int32)
+        L = N.lib()
+        handle = C.c_void_p()
+        cptr = (C.c_void_p * max(len(cols), 1))(*[N.ptr(c) for c in cols])
+        N.check(L.ml_staging_build(plan.n, plan.block_size, len(cols), cptr,
+                                   cgrp.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(handle)),
+                "ml_staging_build")
+        try:
+            self.off, self.list, self.umax, self.loc = [], [], [], {}
+            for g in range(self.ngroups):
+                tot, um = C.c_int64(), C.c_int64()
+                N.check(L.ml_staging_sizes(handle, g, C.byref(tot), C.byref(um)))
+                off = np.empty(plan.nblocks + 1, np.int32)
+                lst = np.empty(max(tot.value, 1), np.int32)
+                N.check(L.ml_staging_export(handle, g, N.ptr(off), N.ptr(lst)))
+                self.off.append(_upload(off))
+                self.list.append(_upload(lst))
+                self.umax.append(int(um.value))
+            for j, i in enumerate(inc):
+                loc = np.empty(max(plan.n, 1), np.uint16)
+                N.check(L.ml_staging_export_loc(handle, j, N.ptr(loc)))
+                self.loc[i] = _upload(loc)
+        finally:
+            L.ml_staging_free(handle)
+
+
+def _upload(host: np.ndarray):
+    buf = N.DeviceBuffer(max(host.nbytes, 4))
+    if host.nbytes:
+        buf.upload(host)
+    return buf
+
+
+def staging_mirror(loop, plan) -> StagingMirror | None:
+    """Staging lists for ``loop`` (cached on the plan), or None if not applicable."""
+    cache = plan.__dict__.setdefault("_staging", {})
+    key = loop.signature()
+    if key not in cache:
+        inc = {a.dat.name for a in loop.args if a.kind == "indirect" and a.mode.name == "INC"}
+        ok = 0 < len(inc) <= N.MAX_GROUPS and plan.block_size <= 256 and plan.n > 0
+        cache[key] = StagingMirror(loop, plan) if ok else None
+    return cache[key]
+
+
 _PINNED_KEEPALIVE: dict = {}
 
 

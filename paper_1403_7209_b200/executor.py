@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _native as N
 from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Mesh, MeshError)
-from .device import dat_mirror, map_mirror, plan_mirror
+from .device import dat_mirror, map_mirror, plan_mirror, staging_mirror
 from .kernels import resolve_kernel
 from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
 from .plan import plan_for, plan_stats
@@ -70,6 +70,7 @@ class BackendConfig:
     use_graph: bool = False                 # replay the program as one CUDA graph
     time_loops: bool = True                 # per-loop CUDA-event timing (eager mode)
     residency: str = "device"               # "device": lazy; "host": copy in/out every run
+    smem_staging: bool = True               # INC increments staged in shared memory
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -206,6 +207,19 @@ class _LoopEntry:
             L.fconst[k] = v
         for k, v in enumerate(binding.iconsts[:4]):
             L.iconst[k] = v
+        L.rlim = -1
+        self.staging = staging_mirror(loop, self.plan) if config.smem_staging else None
+        if self.staging is not None:
+            sg = self.staging
+            L.staging.ngroups = sg.ngroups
+            for i in range(N.MAX_ARGS):
+                L.staging.group[i] = sg.group[i] if i < len(sg.group) else -1
+            for g in range(sg.ngroups):
+                L.staging.off[g] = sg.off[g].ptr
+                L.staging.list[g] = sg.list[g].ptr
+                L.staging.umax[g] = sg.umax[g]
+            for i, buf in sg.loc.items():
+                L.staging.loc[i] = buf.ptr
         nbytes = C.c_uint64()
         N.check(N.lib().ml_loop_scratch_bytes(C.byref(L), C.byref(nbytes)))
         self.scratch = N.DeviceBuffer(nbytes.value) if nbytes.value else None
@@ -330,7 +344,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig) 
     N.init(config.device_index())
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
-           tuple(config.block_size_for(l.name) for l in program))
+           tuple(config.block_size_for(l.name) for l in program), config.smem_staging)
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):
         cache.move_to_end(key)

@@ -1,0 +1,27 @@
+"""Set up the benchmark workload and run it eagerly a few times (for ncu captures).
+
+    python scripts/profile_proxy.py [--grid 94] [--iters 3] [--block-size 256]
+"""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import paper_1403_7209_b200 as ml                  # noqa: E402
+from paper_1403_7209_b200 import apps              # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--grid", type=int, default=94)
+ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--block-size", type=int, default=256)
+ap.add_argument("--soa", type=int, default=4)
+args = ap.parse_args()
+mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)
+apps.shuffle_mesh(mesh, seed=1)
+prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
+ml.renumber_mesh(mesh)
+cfg = ml.BackendConfig(device=0, block_size=args.block_size)
+for i in range(args.iters):
+    r = ml.run_program(prog, mesh, cfg)
+    print(" ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf))

@@ -231,6 +231,24 @@ def test_graph_replay_and_host_residency_match_eager():
         assert r == results[0][1]
 
 
+@pytest.mark.parametrize("bs", [32, 128, 256])
+def test_smem_and_register_staging_agree(bs):
+    outs = []
+    for staging in (True, False):
+        mesh = apps.gen_hex_mesh(14, seed=5)
+        apps.shuffle_mesh(mesh, seed=6)
+        prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=5)
+        ml.renumber_mesh(mesh)
+        ml.run_program(prog[:5], mesh, cfg(block_size=bs, smem_staging=staging))
+        outs.append((h["res"].fetch(), h["grad"].fetch()))
+    close(outs[0][0], outs[1][0], what="res")
+    close(outs[0][1], outs[1][1], what="grad")
+    ref, mesh = apps.gen_mesh(40), apps.gen_mesh(40)
+    for m, st in ((ref, False), (mesh, True)):
+        ml.run_program([_cases.inc_loop(m, "edge_nodes")], m, cfg(block_size=bs, smem_staging=st))
+    np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
+
+
 def test_host_writes_between_runs_are_uploaded():
     mesh = apps.gen_mesh(6)
     prog, h = apps.build_diffusion(mesh, 1, dtype="int64")
@@ -254,7 +272,7 @@ def test_signature_mismatch_raises_exec_error():
     mesh = ml.Mesh()
     s = mesh.decl_set("s", 4)
     d = mesh.decl_dat("d", s, 2, "float64", np.zeros(8))
-    with pytest.raises(ml.ExecError, match="expects"):
+    with pytest.raises(ml.ExecError, match="takes 2 args"):
         ml.run_program([ml.Loop("x", s, [ml.arg_direct(d, ml.RW)], apps._k_copy)], mesh)
 
 

@@ -281,3 +281,34 @@ def test_backend_config_validation():
     with pytest.raises(ml.MeshError, match="partitioner"):
         BackendConfig(partitioner="metis")
     assert BackendConfig(block_size_table={"a": 64}).block_size_for("a") == 64
+
+
+def test_staging_lists_resolve_every_increment(rng):
+    """ml_staging_build: list[off[b] + loc[e]] is exactly element e's target."""
+    import ctypes as C
+    from paper_1403_7209_b200 import _native as N
+    for _ in range(10):
+        mesh, loop = _cases.random_loop_mesh(rng, max_elems=3000)
+        bs = int(rng.choice([1, 7, 64, 256]))
+        n = loop.iter_set.size
+        cols = [np.ascontiguousarray(a.map.table[:, a.slot]) for a in loop.args if a.kind == "indirect"]
+        grp = np.zeros(len(cols), np.int32)
+        h = C.c_void_p()
+        ptrs = (C.c_void_p * len(cols))(*[N.ptr(c) for c in cols])
+        assert N.lib().ml_staging_build(n, bs, len(cols), ptrs, grp.ctypes.data_as(C.POINTER(C.c_int32)),
+                                        C.byref(h)) == 0
+        tot, um = C.c_int64(), C.c_int64()
+        N.lib().ml_staging_sizes(h, 0, C.byref(tot), C.byref(um))
+        nb = (n + bs - 1) // bs
+        off = np.empty(nb + 1, np.int32)
+        lst = np.empty(tot.value, np.int32)
+        N.lib().ml_staging_export(h, 0, N.ptr(off), N.ptr(lst))
+        for j, c in enumerate(cols):
+            loc = np.empty(n, np.uint16)
+            N.lib().ml_staging_export_loc(h, j, N.ptr(loc))
+            blk = np.arange(n) // bs
+            np.testing.assert_array_equal(lst[off[blk] + loc], c)
+        for b in range(nb):
+            seg = lst[off[b]:off[b + 1]]
+            assert np.all(np.diff(seg) > 0) and seg.size <= um.value
+        N.lib().ml_staging_free(h)

@@ -90,6 +90,10 @@ struct LaunchParams {
     int64_t rlim;               // elements >= rlim do not contribute to reductions
     int32_t bs;
     const int32_t *blocks;      // block ids of this launch (nullptr: identity)
+    const int32_t *dep_off;     // dataflow: per block, lower-colour conflicting blocks
+    const int32_t *dep_list;
+    int32_t *flags;             // dataflow: [nblocks] done flags + queue counter at [nblocks]
+    int32_t nqueue;             // dataflow: number of blocks in the queue
     const uint16_t *ecol;       // element colours
     const int32_t *encol;       // per-block element colour count
     Consts k;
@@ -210,12 +214,30 @@ struct Slot {
             if (!p.st.leader[i]) return;
             const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo, um = p.st.umax[g];
             const T *s = reinterpret_cast<const T *>(smem + p.st.soff[g]);
-            const int32_t *list = p.st.list[g] + lo;
+            const int32_t *__restrict__ list = p.st.list[g] + lo;
             const ArgRt &r = p.a[i];
             T *d = static_cast<T *>(r.data);
-            for (int k = threadIdx.x; k < u * A::dim; k += blockDim.x) {
-                const int c = k / u, j = k % u;
-                d[int64_t(__ldg(list + j)) * r.se + c * r.sc] += s[c * um + j];
+            const int total = u * A::dim;
+            const bool aos = r.sc == 1 && A::dim > 1;   // AOS: component-fastest is contiguous
+            constexpr int U = 4;
+            for (int k0 = threadIdx.x; k0 < total; k0 += U * blockDim.x) {
+                int64_t addr[U];
+                T val[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int k = k0 + q * blockDim.x;
+                    if (k < total) {
+                        const int c = aos ? k % A::dim : k / u, j = aos ? k / A::dim : k % u;
+                        addr[q] = int64_t(__ldg(list + j)) * r.se + c * r.sc;
+                        val[q] = s[c * um + j];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    if (k0 + q * blockDim.x < total) val[q] += __ldcg(d + addr[q]);
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    if (k0 + q * blockDim.x < total) d[addr[q]] = val[q];
             }
         }
     }
@@ -385,6 +407,67 @@ __device__ __forceinline__ void run_smem(const LaunchParams &p, Sig<As...>) {
     if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
 }
 
+// Dataflow schedule: a persistent grid pulls blocks in plan (colour) order from
+// a global counter.  Gather + compute + in-block colour phases run at once; the
+// write-back waits only for the lower-colour blocks this block conflicts with,
+// so colours overlap without grid-wide barriers while every target still sees
+// its increments in exactly the order of the per-colour launch schedule.
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int32_t *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <class F, class... As>
+__device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_SMEM, As...>;
+    __shared__ double red[32];
+    __shared__ int s_q;
+    extern __shared__ __align__(16) char dsm[];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    int32_t *counter = p.flags + p.nqueue;
+    for (;;) {
+        if (threadIdx.x == 0) s_q = atomicAdd(counter, 1);
+        __syncthreads();
+        const int q = s_q;
+        if (q >= p.nqueue) break;
+        const int32_t b = p.blocks[q];
+        const int64_t e = int64_t(b) * p.bs + threadIdx.x;
+        const int64_t hi = int64_t(b) * p.bs + p.bs < p.n ? int64_t(b) * p.bs + p.bs : p.n;
+        const bool active = threadIdx.x < p.bs && e < hi;
+        const int ncol = p.encol[b];
+        const int mine = active ? int(p.ecol[e]) : -1;
+        typename E::Slots s;
+        E::zero_smem(s, p, b, dsm, idx);
+        E::init_globals(s, p, idx);
+        if (active) {
+            E::init_elem(s, p, e, dsm, idx);
+            E::call(s, p, e, idx);
+        }
+        __syncthreads();
+        for (int c = 0; c < ncol; ++c) {
+            if (mine == c) E::apply_staged(s, idx);
+            __syncthreads();
+        }
+        // wait for the conflicting lower-colour blocks (one thread per dependency)
+        for (int k = p.dep_off[b] + threadIdx.x; k < p.dep_off[b + 1]; k += blockDim.x) {
+            const int32_t *f = p.flags + p.dep_list[k];
+            while (ld_acquire(f) == 0) __nanosleep(64);
+        }
+        __syncthreads();
+        E::write_back(s, p, b, dsm, idx);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release(p.flags + b, 1);
+        }
+        if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
+    }
+}
+
 template <class F, class... As>
 __device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
     using E = Engine<F, ST_NONE, As...>;
@@ -422,6 +505,10 @@ template <class F, class T>
 __global__ void __launch_bounds__(256) k_smem(const __grid_constant__ LaunchParams p) {
     run_smem<F>(p, typename F::template sig<T>{});
 }
+template <class F, class T>
+__global__ void __launch_bounds__(256) k_flow(const __grid_constant__ LaunchParams p) {
+    run_flow<F>(p, typename F::template sig<T>{});
+}
 
 // ---- compile-time signature introspection -------------------------------------
 template <class S>
@@ -447,7 +534,8 @@ struct FunctorEntry {
     int32_t nargs;
     int32_t kind[MAX_ARGS], mode[MAX_ARGS], dim[MAX_ARGS], atype[MAX_ARGS];
     bool ind_write, ind_write_non_inc;
-    LaunchFn direct, staged, phased, smem;
+    LaunchFn direct, staged, phased, smem, flow;
+    int (*flow_occupancy)(int threads, size_t smem);
 };
 
 void register_functor(const FunctorEntry &e);
@@ -471,6 +559,22 @@ struct Registrar {
         }
         k_smem<F, T><<<g, b, bytes, s>>>(p);
     }
+    static void flow(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
+        static bool opted = false;
+        if (!opted && bytes > 48 * 1024) {
+            cudaFuncSetAttribute(k_flow<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            opted = true;
+        }
+        k_flow<F, T><<<g, b, bytes, s>>>(p);
+    }
+    static int flow_occupancy(int threads, size_t bytes) {
+        if (bytes > 48 * 1024)
+            cudaFuncSetAttribute(k_flow<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_flow<F, T>, threads, bytes) != cudaSuccess)
+            return 0;
+        return n;
+    }
     explicit Registrar(const char *name) {
         using S = typename F::template sig<T>;
         FunctorEntry e{};
@@ -484,6 +588,8 @@ struct Registrar {
         e.staged = SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc ? &staged : nullptr;
         e.phased = SigInfo<S>::ind_write ? &phased : nullptr;
         e.smem = e.staged ? &smem : nullptr;
+        e.flow = e.staged ? &flow : nullptr;
+        e.flow_occupancy = e.staged ? &flow_occupancy : nullptr;
         register_functor(e);
     }
 };

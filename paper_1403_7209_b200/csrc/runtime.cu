@@ -193,7 +193,22 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         const bool staged = f.staged && bs <= 256;
         const LaunchFn fn = use_smem ? f.smem : (staged ? f.staged : f.phased);
         const int threads = staged ? round_up32(bs) : std::clamp(round_up32(bs), 32, 256);
-        for (int64_t c = 0; c < L->plan.ncolors; ++c) {
+        int occ = 0;
+        if (use_smem && f.flow && L->plan.dep_off && L->plan.dep_list && L->plan.flow_state &&
+            L->plan.ncolors > 1)
+            occ = f.flow_occupancy(threads, smem_bytes);
+        if (occ > 0) {
+            // one persistent launch: dataflow over the colour-ordered block queue
+            const int64_t grid = std::min<int64_t>(nb, int64_t(occ) * g_dev.sm_count);
+            ML_CUDA(cudaMemsetAsync(L->plan.flow_state, 0, size_t(nb + 1) * sizeof(int32_t), stream));
+            p.blocks = L->plan.blocks;
+            p.dep_off = L->plan.dep_off;
+            p.dep_list = L->plan.dep_list;
+            p.flags = L->plan.flow_state;
+            p.nqueue = int32_t(nb);
+            f.flow(p, dim3(unsigned(grid)), dim3(unsigned(threads)), smem_bytes, stream);
+        }
+        for (int64_t c = 0; occ == 0 && c < L->plan.ncolors; ++c) {
             const int64_t off = L->plan.color_offsets[c], cnt = L->plan.color_offsets[c + 1] - off;
             if (cnt <= 0) continue;
             p.blocks = L->plan.blocks + off;

@@ -98,7 +98,7 @@ def map_mirror(m: Map) -> int:
 
 
 class PlanMirror:
-    __slots__ = ("blocks", "ecol", "encol", "offsets")
+    __slots__ = ("blocks", "ecol", "encol", "offsets", "dep_off", "dep_list", "flow_state")
 
     def __init__(self, plan):
         blocks = plan.blocks_flat.astype(np.int32)
@@ -117,6 +117,11 @@ class PlanMirror:
             if ecol.size:
                 self.ecol.upload(ecol)
                 self.encol.upload(encol)
+        self.dep_off = self.dep_list = self.flow_state = None
+        if plan.dep_off is not None:
+            self.dep_off = _upload(plan.dep_off)
+            self.dep_list = _upload(plan.dep_list)
+            self.flow_state = N.DeviceBuffer(4 * (plan.nblocks + 1))
 
 
 def plan_mirror(plan) -> PlanMirror:

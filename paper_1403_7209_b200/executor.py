@@ -71,6 +71,7 @@ class BackendConfig:
     time_loops: bool = True                 # per-loop CUDA-event timing (eager mode)
     residency: str = "device"               # "device": lazy; "host": copy in/out every run
     smem_staging: bool = True               # INC increments staged in shared memory
+    dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -152,6 +153,13 @@ def _loop_dtype(loop: Loop) -> int:
     return N.ML_F64
 
 
+def _inc_aliased(loop: Loop) -> bool:
+    """A dat both incremented and otherwise accessed in one loop: its reads would
+    observe a schedule-dependent mix, so keep the strict per-colour launches."""
+    inc = {a.dat.name for a in loop.args if a.kind == "indirect" and a.mode is INC}
+    return any(a.kind != "global" and a.dat.name in inc and a.mode is not INC for a in loop.args)
+
+
 class _LoopEntry:
     """Everything one loop needs on the device, kept alive with the program."""
 
@@ -203,6 +211,10 @@ class _LoopEntry:
         L.plan.blocks = pm.blocks.ptr
         L.plan.elem_color = pm.ecol.ptr if pm.ecol is not None else None
         L.plan.elem_ncolors = pm.encol.ptr if pm.encol is not None else None
+        if config.dataflow and pm.dep_off is not None and not _inc_aliased(loop):
+            L.plan.dep_off = pm.dep_off.ptr
+            L.plan.dep_list = pm.dep_list.ptr
+            L.plan.flow_state = pm.flow_state.ptr
         for k, v in enumerate(binding.fconsts[:4]):
             L.fconst[k] = v
         for k, v in enumerate(binding.iconsts[:4]):
@@ -344,7 +356,8 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig) 
     N.init(config.device_index())
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
-           tuple(config.block_size_for(l.name) for l in program), config.smem_staging)
+           tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
+           config.dataflow)
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):
         cache.move_to_end(key)

@@ -231,6 +231,27 @@ def test_graph_replay_and_host_residency_match_eager():
         assert r == results[0][1]
 
 
+@pytest.mark.parametrize("bs", [32, 256])
+def test_dataflow_schedule_is_bitwise_identical_to_colour_launches(bs):
+    """Same per-target increment order, so float results must match bit for bit."""
+    outs = []
+    for flow in (True, False):
+        mesh = apps.gen_hex_mesh(20, seed=8)
+        apps.shuffle_mesh(mesh, seed=9)
+        prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=8)
+        ml.renumber_mesh(mesh)
+        ml.run_program(prog[:5], mesh, cfg(block_size=bs, dataflow=flow))
+        outs.append((h["res"].fetch(), h["grad"].fetch()))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    for make in (lambda: apps.gen_hub_mesh(5000, 60000, n_hubs=64, hub_share=0.05, seed=3),
+                 lambda: _shuffled_hex(16)):
+        ref, mesh = make(), make()
+        ml.run_program([_cases.inc_loop(ref, "edge_nodes")], ref, cfg(block_size=bs, dataflow=False))
+        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh, cfg(block_size=bs))
+        np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
+
+
 @pytest.mark.parametrize("bs", [32, 128, 256])
 def test_smem_and_register_staging_agree(bs):
     outs = []

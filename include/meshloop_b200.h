@@ -86,6 +86,13 @@ typedef struct ml_staging_dev {
     const int32_t *list[ML_MAX_GROUPS];  /* device unique targets                 */
     int32_t umax[ML_MAX_GROUPS];         /* max unique targets in one block       */
     const uint16_t *loc[ML_MAX_ARGS];    /* device [n] per staged arg             */
+    /* segmented mode (seg != 0): every (element, INC arg) owns a private
+     * shared-memory slot; per unique target, `toff` delimits its contributing
+     * slots in `src` (a*256 + element-in-block, element order), summed in that
+     * fixed order during the write-back — no element colour phases. */
+    int32_t seg;
+    const int32_t *toff[ML_MAX_GROUPS];  /* device [total+1]                      */
+    const uint16_t *src[ML_MAX_GROUPS];  /* device [n * args in group]            */
 } ml_staging_dev_t;
 
 typedef struct ml_loop {
@@ -164,6 +171,9 @@ int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols, const int64_t
 int ml_staging_sizes(const ml_staging_t *s, int32_t group, int64_t *total, int64_t *umax);
 int ml_staging_export(const ml_staging_t *s, int32_t group, int32_t *off, int32_t *list);
 int ml_staging_export_loc(const ml_staging_t *s, int32_t col, uint16_t *loc);
+/* Segmented-mode lists of a group: toff [total+1], src [*nrefs]. */
+int ml_staging_export_seg(const ml_staging_t *s, int32_t group, int64_t *nrefs, int32_t *toff,
+                          uint16_t *src);
 int ml_staging_free(ml_staging_t *s);
 
 /* ---- renumbering: renumber.py:53-128 ------------------------------------- */

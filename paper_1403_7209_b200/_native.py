@@ -30,7 +30,7 @@ EXPORTED = [
     "ml_memset", "ml_map_upload",
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free", "ml_plan_deps",
     "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
-    "ml_staging_free",
+    "ml_staging_export_seg", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
     "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name",
     "ml_loop_scratch_bytes", "ml_loop_run",
@@ -60,7 +60,9 @@ MAX_ARGS, MAX_GROUPS = 16, 2
 class MlStagingDev(C.Structure):
     _fields_ = [("ngroups", C.c_int32), ("group", C.c_int32 * MAX_ARGS),
                 ("off", C.c_void_p * MAX_GROUPS), ("list", C.c_void_p * MAX_GROUPS),
-                ("umax", C.c_int32 * MAX_GROUPS), ("loc", C.c_void_p * MAX_ARGS)]
+                ("umax", C.c_int32 * MAX_GROUPS), ("loc", C.c_void_p * MAX_ARGS),
+                ("seg", C.c_int32), ("toff", C.c_void_p * MAX_GROUPS),
+                ("src", C.c_void_p * MAX_GROUPS)]
 
 
 class MlLoop(C.Structure):
@@ -103,6 +105,7 @@ _SIGNATURES = {
     "ml_staging_sizes": (C.c_int, [_P, C.c_int32, _I64P, _I64P]),
     "ml_staging_export": (C.c_int, [_P, C.c_int32, _P, _P]),
     "ml_staging_export_loc": (C.c_int, [_P, C.c_int32, _P]),
+    "ml_staging_export_seg": (C.c_int, [_P, C.c_int32, _I64P, _P, _P]),
     "ml_staging_free": (C.c_int, [_P]),
     "ml_co_occurrence": (C.c_int, [C.c_int64, C.c_int32, _PP, _I64P, _I32P, _P, _P, _I64P]),
     "ml_cm_order": (C.c_int, [C.c_int64, _P, _P, _P]),

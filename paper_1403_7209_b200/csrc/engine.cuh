@@ -80,6 +80,11 @@ struct Staging {
     const uint16_t *loc[MAX_ARGS];       // [n] local position of the arg's target
     int32_t umax[MAX_GROUPS];            // max unique targets per block (smem stride)
     int32_t soff[MAX_GROUPS];            // byte offset of the group in dynamic smem
+    // segmented mode: private slot per (element, INC arg); per unique target the
+    // contributing slots in element order (src = arg position * 256 + element)
+    const int32_t *toff[MAX_GROUPS];     // [total+1] into src (global target index)
+    const uint16_t *src[MAX_GROUPS];
+    int32_t gpos[MAX_ARGS];              // position of the arg inside its group
 };
 
 struct LaunchParams {
@@ -129,7 +134,10 @@ __device__ __forceinline__ T combine(T a, T b) {
 // MODE 0: no staging (views into HBM); 1: indirect INC staged in registers and
 // applied to HBM in colour phases; 2: staged in registers, applied to shared
 // memory in colour phases, written back once per block.
-enum : int { ST_NONE = 0, ST_REG = 1, ST_SMEM = 2 };
+// MODE 3 (ST_SEG): the functor increments a private shared-memory slot of its
+// own (no registers held, no phases); the write-back sums each target's slots
+// in element order — a deterministic segmented reduction.
+enum : int { ST_NONE = 0, ST_REG = 1, ST_SMEM = 2, ST_SEG = 3 };
 
 template <class A, int MODE>
 struct Slot {
@@ -137,7 +145,8 @@ struct Slot {
     static constexpr bool is_global = A::kind == KG;
     static constexpr bool is_reduce = is_global && A::mode != MR;
     static constexpr bool is_inc = A::kind == KI && A::mode == MINC;
-    static constexpr bool staged = (is_inc && MODE != ST_NONE) || is_reduce;
+    static constexpr bool seg = is_inc && MODE == ST_SEG;
+    static constexpr bool staged = (is_inc && MODE != ST_NONE && MODE != ST_SEG) || is_reduce;
 
     T acc[staged ? A::dim : 1];
     T bak[is_reduce ? A::dim : 1];
@@ -159,6 +168,13 @@ struct Slot {
                 const int g = p.st.group[i];
                 ptr = reinterpret_cast<T *>(smem + p.st.soff[g]) + __ldg(p.st.loc[i] + e);
                 sc = p.st.umax[g];
+            } else if constexpr (seg) {
+                const int g = p.st.group[i];
+                ptr = reinterpret_cast<T *>(smem + p.st.soff[g]) +
+                      int64_t(p.st.gpos[i]) * A::dim * blockDim.x + threadIdx.x;
+                sc = blockDim.x;
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) ptr[c * sc] = T(0);
             } else {
                 const ArgRt &r = p.a[i];
                 const int64_t t = A::kind == KI ? int64_t(__ldg(r.map + e)) : e;
@@ -238,6 +254,43 @@ struct Slot {
 #pragma unroll
                 for (int q = 0; q < U; ++q)
                     if (k0 + q * blockDim.x < total) d[addr[q]] = val[q];
+            }
+        } else if constexpr (seg) {
+            const int g = p.st.group[i];
+            if (!p.st.leader[i]) return;
+            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo;
+            const T *s = reinterpret_cast<const T *>(smem + p.st.soff[g]);
+            const int32_t *__restrict__ list = p.st.list[g] + lo;
+            const int32_t *__restrict__ toff = p.st.toff[g] + lo;
+            const uint16_t *__restrict__ src = p.st.src[g];
+            const ArgRt &r = p.a[i];
+            T *d = static_cast<T *>(r.data);
+            const int total = u * A::dim, nt = blockDim.x;
+            const bool aos = r.sc == 1 && A::dim > 1;
+            constexpr int U = 4;
+            for (int k0 = threadIdx.x; k0 < total; k0 += U * nt) {
+                int64_t addr[U];
+                T val[U];
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const int k = k0 + q * nt;
+                    if (k < total) {
+                        const int c = aos ? k % A::dim : k / u, j = aos ? k / A::dim : k % u;
+                        addr[q] = int64_t(__ldg(list + j)) * r.se + c * r.sc;
+                        T acc = T(0);
+                        for (int m = __ldg(toff + j), me = __ldg(toff + j + 1); m < me; ++m) {
+                            const int v = __ldg(src + m);
+                            acc += s[((v >> 8) * A::dim + c) * nt + (v & 255)];
+                        }
+                        val[q] = acc;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    if (k0 + q * nt < total) val[q] = __ldcg(d + addr[q]) + val[q];
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    if (k0 + q * nt < total) d[addr[q]] = val[q];
             }
         }
     }
@@ -379,9 +432,9 @@ __device__ __forceinline__ void run_staged(const LaunchParams &p, Sig<As...>) {
 
 // Increments staged in shared memory: compute -> colour phases into smem ->
 // one coalesced read-modify-write of the block's unique targets.
-template <class F, class... As>
+template <class F, int MODE, class... As>
 __device__ __forceinline__ void run_smem(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_SMEM, As...>;
+    using E = Engine<F, MODE, As...>;
     __shared__ double red[32];
     extern __shared__ __align__(16) char dsm[];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
@@ -392,16 +445,18 @@ __device__ __forceinline__ void run_smem(const LaunchParams &p, Sig<As...>) {
     const int ncol = p.encol[b];
     const int mine = active ? int(p.ecol[e]) : -1;
     typename E::Slots s;
-    E::zero_smem(s, p, b, dsm, idx);
+    if constexpr (MODE == ST_SMEM) E::zero_smem(s, p, b, dsm, idx);
     E::init_globals(s, p, idx);
     if (active) {
         E::init_elem(s, p, e, dsm, idx);
         E::call(s, p, e, idx);
     }
     __syncthreads();
-    for (int c = 0; c < ncol; ++c) {
-        if (mine == c) E::apply_staged(s, idx);
-        __syncthreads();
+    if constexpr (MODE == ST_SMEM) {
+        for (int c = 0; c < ncol; ++c) {
+            if (mine == c) E::apply_staged(s, idx);
+            __syncthreads();
+        }
     }
     E::write_back(s, p, b, dsm, idx);
     if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
@@ -421,9 +476,9 @@ __device__ __forceinline__ void st_release(int32_t *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <class F, class... As>
+template <class F, int MODE, class... As>
 __device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_SMEM, As...>;
+    using E = Engine<F, MODE, As...>;
     __shared__ double red[32];
     __shared__ int s_q;
     extern __shared__ __align__(16) char dsm[];
@@ -441,16 +496,18 @@ __device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
         const int ncol = p.encol[b];
         const int mine = active ? int(p.ecol[e]) : -1;
         typename E::Slots s;
-        E::zero_smem(s, p, b, dsm, idx);
+        if constexpr (MODE == ST_SMEM) E::zero_smem(s, p, b, dsm, idx);
         E::init_globals(s, p, idx);
         if (active) {
             E::init_elem(s, p, e, dsm, idx);
             E::call(s, p, e, idx);
         }
         __syncthreads();
-        for (int c = 0; c < ncol; ++c) {
-            if (mine == c) E::apply_staged(s, idx);
-            __syncthreads();
+        if constexpr (MODE == ST_SMEM) {
+            for (int c = 0; c < ncol; ++c) {
+                if (mine == c) E::apply_staged(s, idx);
+                __syncthreads();
+            }
         }
         // wait for the conflicting lower-colour blocks (one thread per dependency)
         for (int k = p.dep_off[b] + threadIdx.x; k < p.dep_off[b + 1]; k += blockDim.x) {
@@ -501,13 +558,13 @@ template <class F, class T>
 __global__ void __launch_bounds__(256) k_phased(const __grid_constant__ LaunchParams p) {
     run_phased<F>(p, typename F::template sig<T>{});
 }
-template <class F, class T>
+template <class F, class T, int MODE>
 __global__ void __launch_bounds__(256) k_smem(const __grid_constant__ LaunchParams p) {
-    run_smem<F>(p, typename F::template sig<T>{});
+    run_smem<F, MODE>(p, typename F::template sig<T>{});
 }
-template <class F, class T>
+template <class F, class T, int MODE>
 __global__ void __launch_bounds__(256) k_flow(const __grid_constant__ LaunchParams p) {
-    run_flow<F>(p, typename F::template sig<T>{});
+    run_flow<F, MODE>(p, typename F::template sig<T>{});
 }
 
 // ---- compile-time signature introspection -------------------------------------
@@ -534,8 +591,9 @@ struct FunctorEntry {
     int32_t nargs;
     int32_t kind[MAX_ARGS], mode[MAX_ARGS], dim[MAX_ARGS], atype[MAX_ARGS];
     bool ind_write, ind_write_non_inc;
-    LaunchFn direct, staged, phased, smem, flow;
-    int (*flow_occupancy)(int threads, size_t smem);
+    LaunchFn direct, staged, phased;
+    LaunchFn smem[2], flow[2];                       // [0] colour phases, [1] segmented
+    int (*flow_occupancy[2])(int threads, size_t smem);
 };
 
 void register_functor(const FunctorEntry &e);
@@ -551,27 +609,30 @@ struct Registrar {
     static void phased(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_phased<F, T><<<g, b, 0, s>>>(p);
     }
+    template <int MODE>
     static void smem(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
         static bool opted = false;
         if (!opted && bytes > 48 * 1024) {
-            cudaFuncSetAttribute(k_smem<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(k_smem<F, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             opted = true;
         }
-        k_smem<F, T><<<g, b, bytes, s>>>(p);
+        k_smem<F, T, MODE><<<g, b, bytes, s>>>(p);
     }
+    template <int MODE>
     static void flow(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
         static bool opted = false;
         if (!opted && bytes > 48 * 1024) {
-            cudaFuncSetAttribute(k_flow<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(k_flow<F, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             opted = true;
         }
-        k_flow<F, T><<<g, b, bytes, s>>>(p);
+        k_flow<F, T, MODE><<<g, b, bytes, s>>>(p);
     }
+    template <int MODE>
     static int flow_occupancy(int threads, size_t bytes) {
         if (bytes > 48 * 1024)
-            cudaFuncSetAttribute(k_flow<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(k_flow<F, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_flow<F, T>, threads, bytes) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_flow<F, T, MODE>, threads, bytes) != cudaSuccess)
             return 0;
         return n;
     }
@@ -587,9 +648,13 @@ struct Registrar {
         e.direct = &direct;
         e.staged = SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc ? &staged : nullptr;
         e.phased = SigInfo<S>::ind_write ? &phased : nullptr;
-        e.smem = e.staged ? &smem : nullptr;
-        e.flow = e.staged ? &flow : nullptr;
-        e.flow_occupancy = e.staged ? &flow_occupancy : nullptr;
+        const bool st = e.staged != nullptr;
+        e.smem[0] = st ? &smem<ST_SMEM> : nullptr;
+        e.smem[1] = st ? &smem<ST_SEG> : nullptr;
+        e.flow[0] = st ? &flow<ST_SMEM> : nullptr;
+        e.flow[1] = st ? &flow<ST_SEG> : nullptr;
+        e.flow_occupancy[0] = st ? &flow_occupancy<ST_SMEM> : nullptr;
+        e.flow_occupancy[1] = st ? &flow_occupancy<ST_SEG> : nullptr;
         register_functor(e);
     }
 };

@@ -316,6 +316,10 @@ struct ml_staging {
     std::vector<std::vector<int32_t>> off, list;   // per group
     std::vector<int64_t> umax;                     // per group
     std::vector<std::vector<uint16_t>> loc;        // per column
+    // segmented mode: per unique target (global index into list), its
+    // contributing (arg position, element in block) slots in element order
+    std::vector<std::vector<int32_t>> toff;        // per group [total+1]
+    std::vector<std::vector<uint16_t>> src;        // per group
 };
 
 extern "C" int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols,
@@ -335,14 +339,28 @@ extern "C" int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols,
     s->umax.assign(ng, 0);
     s->loc.assign(ncols, std::vector<uint16_t>(size_t(n), 0));
     std::vector<int64_t> buf;
+    s->toff.assign(ng, {});
+    s->src.assign(ng, {});
+    struct Ref { int64_t tgt; int32_t elem, pos; };
+    std::vector<Ref> refs;
     for (int32_t g = 0; g < ng; ++g) {
         auto &list = s->list[g];
+        auto &toff = s->toff[g];
+        auto &src = s->src[g];
+        toff.push_back(0);
         for (int64_t b = 0; b < s->nb; ++b) {
             const int64_t lo = b * block_size, hi = std::min(n, lo + block_size);
             buf.clear();
+            refs.clear();
+            int32_t pos = 0;
             for (int32_t j = 0; j < ncols; ++j)
-                if (col_group[j] == g)
-                    for (int64_t e = lo; e < hi; ++e) buf.push_back(cols[j][e]);
+                if (col_group[j] == g) {
+                    for (int64_t e = lo; e < hi; ++e) {
+                        buf.push_back(cols[j][e]);
+                        refs.push_back({cols[j][e], int32_t(e - lo), pos});
+                    }
+                    ++pos;
+                }
             std::sort(buf.begin(), buf.end());
             buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
             if (buf.size() > 65535) throw std::length_error("more than 65535 staged targets in one block");
@@ -354,6 +372,22 @@ extern "C" int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols,
                         s->loc[j][e] = uint16_t(std::lower_bound(buf.begin(), buf.end(), cols[j][e]) - buf.begin());
             for (int64_t t : buf) list.push_back(int32_t(t));
             s->off[g][b + 1] = int32_t(list.size());
+            // contributions per target in element order, then argument order
+            std::sort(refs.begin(), refs.end(), [](const Ref &x, const Ref &y) {
+                if (x.tgt != y.tgt) return x.tgt < y.tgt;
+                if (x.elem != y.elem) return x.elem < y.elem;
+                return x.pos < y.pos;
+            });
+            size_t r = 0;
+            for (int64_t t : buf) {
+                while (r < refs.size() && refs[r].tgt == t) {
+                    if (refs[r].elem > 255 || refs[r].pos > 255)
+                        throw std::length_error("segmented staging needs block_size <= 256");
+                    src.push_back(uint16_t(refs[r].pos * 256 + refs[r].elem));
+                    ++r;
+                }
+                toff.push_back(int32_t(src.size()));
+            }
         }
     }
     *out = s.release();
@@ -378,6 +412,15 @@ extern "C" int ml_staging_export(const ml_staging_t *s, int32_t g, int32_t *off,
 extern "C" int ml_staging_export_loc(const ml_staging_t *s, int32_t col, uint16_t *loc) {
     if (!s || col < 0 || col >= int32_t(s->loc.size())) ML_FAIL(ML_EINVAL, "ml_staging_export_loc: bad column");
     std::copy(s->loc[col].begin(), s->loc[col].end(), loc);
+    return ML_OK;
+}
+
+extern "C" int ml_staging_export_seg(const ml_staging_t *s, int32_t g, int64_t *nrefs, int32_t *toff,
+                                     uint16_t *src) {
+    if (!s || g < 0 || g >= s->ngroups) ML_FAIL(ML_EINVAL, "ml_staging_export_seg: bad group");
+    if (nrefs) *nrefs = int64_t(s->src[g].size());
+    if (toff) std::copy(s->toff[g].begin(), s->toff[g].end(), toff);
+    if (src) std::copy(s->src[g].begin(), s->src[g].end(), src);
     return ML_OK;
 }
 

@@ -151,28 +151,38 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     size_t smem_bytes = 0;
     bool use_smem = false;
     const ml_staging_dev_t &sg = L->staging;
-    if (f.smem && bs <= 256 && sg.ngroups > 0 && sg.ngroups <= MAX_GROUPS) {
+    const int seg = sg.seg ? 1 : 0;
+    const int sthreads = round_up32(bs);
+    if (f.smem[seg] && bs <= 256 && sg.ngroups > 0 && sg.ngroups <= MAX_GROUPS) {
         use_smem = true;
-        bool seen[MAX_GROUPS] = {false, false};
+        int leader[MAX_GROUPS] = {-1, -1}, count[MAX_GROUPS] = {0, 0};
         for (int i = 0; i < f.nargs; ++i) {
             const bool inc = f.kind[i] == KI && f.mode[i] == MINC;
             const int g = sg.group[i];
-            if (inc != (g >= 0) || g >= sg.ngroups || (inc && !sg.loc[i])) {
+            if (inc != (g >= 0) || g >= sg.ngroups || (inc && !seg && !sg.loc[i]) ||
+                (inc && seg && (!sg.toff[g] || !sg.src[g]))) {
                 use_smem = false;
                 break;
             }
             if (g < 0) continue;
             p.st.group[i] = g;
             p.st.loc[i] = sg.loc[i];
-            if (!seen[g]) {
-                seen[g] = true;
+            p.st.gpos[i] = count[g]++;
+            if (leader[g] < 0) {
+                leader[g] = i;
                 p.st.leader[i] = 1;
                 p.st.off[g] = sg.off[g];
                 p.st.list[g] = sg.list[g];
                 p.st.umax[g] = sg.umax[g];
-                p.st.soff[g] = int32_t(smem_bytes);
-                smem_bytes += (size_t(sg.umax[g]) * f.dim[i] * 8 + 15) / 16 * 16;
+                p.st.toff[g] = sg.toff[g];
+                p.st.src[g] = sg.src[g];
             }
+        }
+        for (int g = 0; use_smem && g < sg.ngroups; ++g) {
+            if (leader[g] < 0) { use_smem = false; break; }
+            p.st.soff[g] = int32_t(smem_bytes);
+            const size_t slots = seg ? size_t(count[g]) * sthreads : size_t(sg.umax[g]);
+            smem_bytes += (slots * f.dim[leader[g]] * 8 + 15) / 16 * 16;
         }
         if (!use_smem || smem_bytes > 200 * 1024) {
             use_smem = false;
@@ -191,12 +201,12 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         p.ecol = L->plan.elem_color;
         p.encol = L->plan.elem_ncolors;
         const bool staged = f.staged && bs <= 256;
-        const LaunchFn fn = use_smem ? f.smem : (staged ? f.staged : f.phased);
+        const LaunchFn fn = use_smem ? f.smem[seg] : (staged ? f.staged : f.phased);
         const int threads = staged ? round_up32(bs) : std::clamp(round_up32(bs), 32, 256);
         int occ = 0;
-        if (use_smem && f.flow && L->plan.dep_off && L->plan.dep_list && L->plan.flow_state &&
+        if (use_smem && f.flow[seg] && L->plan.dep_off && L->plan.dep_list && L->plan.flow_state &&
             L->plan.ncolors > 1)
-            occ = f.flow_occupancy(threads, smem_bytes);
+            occ = f.flow_occupancy[seg](threads, smem_bytes);
         if (occ > 0) {
             // one persistent launch: dataflow over the colour-ordered block queue
             const int64_t grid = std::min<int64_t>(nb, int64_t(occ) * g_dev.sm_count);
@@ -206,7 +216,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
             p.dep_list = L->plan.dep_list;
             p.flags = L->plan.flow_state;
             p.nqueue = int32_t(nb);
-            f.flow(p, dim3(unsigned(grid)), dim3(unsigned(threads)), smem_bytes, stream);
+            f.flow[seg](p, dim3(unsigned(grid)), dim3(unsigned(threads)), smem_bytes, stream);
         }
         for (int64_t c = 0; occ == 0 && c < L->plan.ncolors; ++c) {
             const int64_t off = L->plan.color_offsets[c], cnt = L->plan.color_offsets[c + 1] - off;

@@ -136,7 +136,7 @@ class StagingMirror:
     ``group[i]`` is the staging group of argument i (one group per INC dat),
     -1 for arguments that are not indirect INC."""
 
-    __slots__ = ("group", "ngroups", "off", "list", "umax", "loc")
+    __slots__ = ("group", "ngroups", "off", "list", "umax", "loc", "toff", "src")
 
     def __init__(self, loop, plan):
         import ctypes as C
@@ -160,6 +160,7 @@ class StagingMirror:
                 "ml_staging_build")
         try:
             self.off, self.list, self.umax, self.loc = [], [], [], {}
+            self.toff, self.src = [], []
             for g in range(self.ngroups):
                 tot, um = C.c_int64(), C.c_int64()
                 N.check(L.ml_staging_sizes(handle, g, C.byref(tot), C.byref(um)))
@@ -169,6 +170,13 @@ class StagingMirror:
                 self.off.append(_upload(off))
                 self.list.append(_upload(lst))
                 self.umax.append(int(um.value))
+                nref = C.c_int64()
+                N.check(L.ml_staging_export_seg(handle, g, C.byref(nref), None, None))
+                toff = np.empty(tot.value + 1, np.int32)
+                src = np.empty(max(nref.value, 1), np.uint16)
+                N.check(L.ml_staging_export_seg(handle, g, C.byref(nref), N.ptr(toff), N.ptr(src)))
+                self.toff.append(_upload(toff))
+                self.src.append(_upload(src))
             for j, i in enumerate(inc):
                 loc = np.empty(max(plan.n, 1), np.uint16)
                 N.check(L.ml_staging_export_loc(handle, j, N.ptr(loc)))

@@ -72,6 +72,7 @@ class BackendConfig:
     residency: str = "device"               # "device": lazy; "host": copy in/out every run
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
+    inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -85,6 +86,8 @@ class BackendConfig:
             raise MeshError(f"unknown partitioner {self.partitioner!r}")
         if self.residency not in ("device", "host"):
             raise MeshError(f"unknown residency {self.residency!r}")
+        if self.inc_staging not in ("segmented", "colour"):
+            raise MeshError(f"unknown inc_staging {self.inc_staging!r}")
 
     def block_size_for(self, loop_name: str) -> int:
         if self.block_size_table and loop_name in self.block_size_table:
@@ -232,6 +235,10 @@ class _LoopEntry:
                 L.staging.umax[g] = sg.umax[g]
             for i, buf in sg.loc.items():
                 L.staging.loc[i] = buf.ptr
+            L.staging.seg = 1 if config.inc_staging == "segmented" else 0
+            for g in range(sg.ngroups):
+                L.staging.toff[g] = sg.toff[g].ptr
+                L.staging.src[g] = sg.src[g].ptr
         nbytes = C.c_uint64()
         N.check(N.lib().ml_loop_scratch_bytes(C.byref(L), C.byref(nbytes)))
         self.scratch = N.DeviceBuffer(nbytes.value) if nbytes.value else None
@@ -357,7 +364,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig) 
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
            tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
-           config.dataflow)
+           config.dataflow, config.inc_staging)
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):
         cache.move_to_end(key)

@@ -13,7 +13,7 @@ timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider --durations=15
 timeout 600 python bench.py --steps 20 --warmup 3 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/status.txt"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 2 --warmup 1 --no-cpu > "$OUT/bench_ncu.log" 2>&1; echo "ncu-list rc=$?" >> "$OUT/status.txt"
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:ProxyVflux|ProxyGrad" -s 6 -c 4 \
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:ProxyVflux|ProxyGrad|ProxyIflux" -s 0 -c 3 \
     -o "$OUT/edge_loops" python scripts/profile_proxy.py --iters 1 > "$OUT/ncu_full.log" 2>&1; echo "ncu-full rc=$?" >> "$OUT/status.txt"
 cat "$OUT/status.txt"
 tail -3 "$OUT/pytest_gpu.log"

@@ -255,19 +255,23 @@ def test_dataflow_schedule_is_bitwise_identical_to_colour_launches(bs):
 @pytest.mark.parametrize("bs", [32, 128, 256])
 def test_smem_and_register_staging_agree(bs):
     outs = []
-    for staging in (True, False):
+    variants = ({"smem_staging": False}, {"inc_staging": "colour"}, {"inc_staging": "segmented"})
+    for kw in variants:
         mesh = apps.gen_hex_mesh(14, seed=5)
         apps.shuffle_mesh(mesh, seed=6)
         prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=5)
         ml.renumber_mesh(mesh)
-        ml.run_program(prog[:5], mesh, cfg(block_size=bs, smem_staging=staging))
+        ml.run_program(prog[:5], mesh, cfg(block_size=bs, **kw))
         outs.append((h["res"].fetch(), h["grad"].fetch()))
-    close(outs[0][0], outs[1][0], what="res")
-    close(outs[0][1], outs[1][1], what="grad")
-    ref, mesh = apps.gen_mesh(40), apps.gen_mesh(40)
-    for m, st in ((ref, False), (mesh, True)):
-        ml.run_program([_cases.inc_loop(m, "edge_nodes")], m, cfg(block_size=bs, smem_staging=st))
-    np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
+    for o in outs[1:]:
+        close(o[0], outs[0][0], what="res")
+        close(o[1], outs[0][1], what="grad")
+    ref = apps.gen_mesh(40)
+    ml.run_program([_cases.inc_loop(ref, "edge_nodes")], ref, cfg(block_size=bs, smem_staging=False))
+    for kw in variants[1:]:
+        mesh = apps.gen_mesh(40)
+        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh, cfg(block_size=bs, **kw))
+        np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
 
 
 def test_host_writes_between_runs_are_uploaded():

@@ -311,4 +311,17 @@ def test_staging_lists_resolve_every_increment(rng):
         for b in range(nb):
             seg = lst[off[b]:off[b + 1]]
             assert np.all(np.diff(seg) > 0) and seg.size <= um.value
+        # segmented lists: each target's contributing (arg, element) slots, element order
+        nref = C.c_int64()
+        N.lib().ml_staging_export_seg(h, 0, C.byref(nref), None, None)
+        assert nref.value == n * len(cols)
+        toff = np.empty(tot.value + 1, np.int32)
+        src = np.empty(nref.value, np.uint16)
+        N.lib().ml_staging_export_seg(h, 0, C.byref(nref), N.ptr(toff), N.ptr(src))
+        for u in range(tot.value):
+            b = int(np.searchsorted(off, u, side="right") - 1)
+            slots = src[toff[u]:toff[u + 1]]
+            elems, args = b * bs + (slots & 255), slots >> 8
+            assert np.all([cols[a][e] == lst[u] for a, e in zip(args, elems)])
+            assert np.all(np.diff(elems.astype(np.int64) * 8 + args) > 0)
         N.lib().ml_staging_free(h)

@@ -64,12 +64,12 @@ typedef struct ml_plan_dev {
     const int32_t *blocks;          /* device: block ids ordered by colour      */
     const uint16_t *elem_color;     /* device [n]; NULL when no indirect writes */
     const int32_t *elem_ncolors;    /* device [nblocks]; NULL likewise          */
-    /* Optional dataflow schedule (ml_plan_deps): one persistent launch walks
-     * the blocks in colour order; a block writes back only after the
-     * lower-colour blocks it conflicts with did (same result as per-colour
-     * launches, no inter-colour barriers).  NULL dep_off disables it. */
+    /* Optional dataflow schedule (ml_schedule_build): one persistent launch
+     * walks `queue`; a block writes back only after the earlier-queued blocks
+     * it conflicts with did (no inter-colour barriers).  NULL disables it. */
+    const int32_t *queue;           /* device [nblocks] block ids in queue order */
     const int32_t *dep_off;         /* device [nblocks+1]                        */
-    const int32_t *dep_list;        /* device conflicting lower-colour blocks    */
+    const int32_t *dep_list;        /* device conflicting earlier-queued blocks  */
     int32_t *flow_state;            /* device scratch [nblocks+1], zeroed per run */
 } ml_plan_dev_t;
 
@@ -156,11 +156,19 @@ int ml_plan_export(const ml_plan_t *p, int64_t *block_color, int64_t *elem_ncolo
                    int64_t *color_offsets, int64_t *blocks_by_color,
                    int64_t *elem_color, int64_t *block_elem_order);
 int ml_plan_free(ml_plan_t *p);
-/* Block dependencies of the dataflow schedule: for block b, off[b]..off[b+1]
- * of `list` are the lower-colour blocks sharing a write target.  *ndeps is -1
- * when a hub target makes the lists quadratic (use per-colour launches).
- * Sizes: off [nblocks+1], list [*ndeps]; pass NULLs to query *ndeps. */
-int ml_plan_deps(const ml_plan_t *p, int64_t *ndeps, int32_t *off, int32_t *list);
+/* Dataflow schedule of an indirect-write loop (csrc/host_schedule.cpp): a
+ * block queue in (window, colour, index) order — windows of consecutive
+ * blocks sized to the L2 — and, per block, the blocks sharing a write target
+ * that precede it in the queue (its dependencies).  Export sizes: queue
+ * [nblocks], dep_off [nblocks+1], dep_list [*ndeps]; *ndeps is -1 when a hub
+ * target makes the lists quadratic (use per-colour launches instead). */
+typedef struct ml_schedule ml_schedule_t;
+int ml_schedule_build(int64_t n, int32_t ncols, const int64_t *const *cols, const int32_t *col_key,
+                      int64_t block_size, const int64_t *block_color, int32_t nwindows,
+                      ml_schedule_t **out);
+int ml_schedule_export(const ml_schedule_t *s, int64_t *ndeps, int32_t *queue, int32_t *dep_off,
+                       int32_t *dep_list);
+int ml_schedule_free(ml_schedule_t *s);
 
 /* Staging lists for shared-memory increment accumulation (derived from the
  * plan's blocking; the plan itself is unchanged).  `col_group[j]` assigns the

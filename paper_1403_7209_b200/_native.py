@@ -28,7 +28,8 @@ EXPORTED = [
     "ml_last_error", "ml_version", "ml_init", "ml_device_info", "ml_synchronize",
     "ml_alloc", "ml_free", "ml_host_alloc", "ml_host_free", "ml_upload", "ml_download",
     "ml_memset", "ml_map_upload",
-    "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free", "ml_plan_deps",
+    "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
+    "ml_schedule_build", "ml_schedule_export", "ml_schedule_free",
     "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
     "ml_staging_export_seg", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
@@ -51,7 +52,8 @@ class MlPlanDev(C.Structure):
     _fields_ = [("nblocks", C.c_int64), ("ncolors", C.c_int64), ("block_size", C.c_int64),
                 ("color_offsets", C.POINTER(C.c_int64)), ("blocks", C.c_void_p),
                 ("elem_color", C.c_void_p), ("elem_ncolors", C.c_void_p),
-                ("dep_off", C.c_void_p), ("dep_list", C.c_void_p), ("flow_state", C.c_void_p)]
+                ("queue", C.c_void_p), ("dep_off", C.c_void_p), ("dep_list", C.c_void_p),
+                ("flow_state", C.c_void_p)]
 
 
 MAX_ARGS, MAX_GROUPS = 16, 2
@@ -100,7 +102,10 @@ _SIGNATURES = {
     "ml_plan_sizes": (C.c_int, [_P, _I64P, _I64P, _I64P]),
     "ml_plan_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "ml_plan_free": (C.c_int, [_P]),
-    "ml_plan_deps": (C.c_int, [_P, _I64P, _P, _P]),
+    "ml_schedule_build": (C.c_int, [C.c_int64, C.c_int32, _PP, _I32P, C.c_int64, _P, C.c_int32,
+                                    _PP]),
+    "ml_schedule_export": (C.c_int, [_P, _I64P, _P, _P, _P]),
+    "ml_schedule_free": (C.c_int, [_P]),
     "ml_staging_build": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, _PP, _I32P, _PP]),
     "ml_staging_sizes": (C.c_int, [_P, C.c_int32, _I64P, _I64P]),
     "ml_staging_export": (C.c_int, [_P, C.c_int32, _P, _P]),

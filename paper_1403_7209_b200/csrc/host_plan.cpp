@@ -35,9 +35,6 @@ struct ml_plan {
     std::vector<int32_t> block_color, elem_ncolors, elem_color;
     std::vector<int64_t> color_off;
     std::vector<int32_t> blocks_by_color;
-    // dataflow dependencies: per block, the conflicting blocks of lower colour
-    std::vector<int32_t> dep_off, dep_list;
-    bool flow_ok = true;
 };
 
 namespace {
@@ -198,39 +195,6 @@ extern "C" int ml_plan_build(int64_t n, int32_t ncols, const int64_t *const *col
         }
         p->max_ecol = max_ecol;
 
-        // block dependencies for the dataflow schedule: every pair of blocks
-        // sharing a (plan) target, directed from the higher colour to the lower
-        std::vector<std::pair<int64_t, int32_t>> tb;   // (target, block), unique per block
-        tb.reserve(size_t(n) * ncols);
-        for (int32_t j = 0; j < ncols; ++j)
-            for (int64_t e = 0; e < n; ++e) tb.emplace_back(cols[j][e] + base[j], int32_t(e / block_size));
-        std::sort(tb.begin(), tb.end());
-        tb.erase(std::unique(tb.begin(), tb.end()), tb.end());
-        std::vector<std::pair<int32_t, int32_t>> edges;   // (later block, earlier block)
-        for (size_t i = 0; i < tb.size();) {
-            size_t k = i;
-            while (k < tb.size() && tb[k].first == tb[i].first) ++k;
-            if (k - i > 512) {          // hub target: quadratic dependency lists; no dataflow
-                p->flow_ok = false;
-                edges.clear();
-                break;
-            }
-            for (size_t a = i; a < k; ++a)
-                for (size_t c = a + 1; c < k; ++c) {
-                    int32_t x = tb[a].second, y = tb[c].second;
-                    if (p->block_color[x] == p->block_color[y]) continue;
-                    if (p->block_color[x] < p->block_color[y]) std::swap(x, y);
-                    edges.emplace_back(x, y);
-                }
-            i = k;
-        }
-        std::sort(edges.begin(), edges.end());
-        edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
-        p->dep_off.assign(size_t(nb) + 1, 0);
-        for (auto &ed : edges) p->dep_off[ed.first + 1]++;
-        for (int64_t b = 0; b < nb; ++b) p->dep_off[b + 1] += p->dep_off[b];
-        p->dep_list.resize(edges.size());
-        for (size_t i = 0; i < edges.size(); ++i) p->dep_list[i] = edges[i].second;
     } else {
         p->nc = nb ? 1 : 0;
     }
@@ -286,19 +250,6 @@ extern "C" int ml_plan_export(const ml_plan_t *p, int64_t *block_color, int64_t 
     }
     return ML_OK;
     ML_GUARD_END
-}
-
-extern "C" int ml_plan_deps(const ml_plan_t *p, int64_t *ndeps, int32_t *off, int32_t *list) {
-    if (!p) ML_FAIL(ML_EINVAL, "ml_plan_deps: null plan");
-    if (ndeps) *ndeps = p->flow_ok ? int64_t(p->dep_list.size()) : -1;
-    if (off) {
-        if (p->dep_off.empty())
-            std::fill(off, off + p->nb + 1, 0);
-        else
-            std::copy(p->dep_off.begin(), p->dep_off.end(), off);
-    }
-    if (list) std::copy(p->dep_list.begin(), p->dep_list.end(), list);
-    return ML_OK;
 }
 
 extern "C" int ml_plan_free(ml_plan_t *p) {

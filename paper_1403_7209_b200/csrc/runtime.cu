@@ -204,14 +204,14 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         const LaunchFn fn = use_smem ? f.smem[seg] : (staged ? f.staged : f.phased);
         const int threads = staged ? round_up32(bs) : std::clamp(round_up32(bs), 32, 256);
         int occ = 0;
-        if (use_smem && f.flow[seg] && L->plan.dep_off && L->plan.dep_list && L->plan.flow_state &&
-            L->plan.ncolors > 1)
+        if (use_smem && f.flow[seg] && L->plan.queue && L->plan.dep_off && L->plan.dep_list &&
+            L->plan.flow_state && L->plan.ncolors > 1)
             occ = f.flow_occupancy[seg](threads, smem_bytes);
         if (occ > 0) {
             // one persistent launch: dataflow over the colour-ordered block queue
             const int64_t grid = std::min<int64_t>(nb, int64_t(occ) * g_dev.sm_count);
             ML_CUDA(cudaMemsetAsync(L->plan.flow_state, 0, size_t(nb + 1) * sizeof(int32_t), stream));
-            p.blocks = L->plan.blocks;
+            p.blocks = L->plan.queue;
             p.dep_off = L->plan.dep_off;
             p.dep_list = L->plan.dep_list;
             p.flags = L->plan.flow_state;

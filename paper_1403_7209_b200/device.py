@@ -98,7 +98,7 @@ def map_mirror(m: Map) -> int:
 
 
 class PlanMirror:
-    __slots__ = ("blocks", "ecol", "encol", "offsets", "dep_off", "dep_list", "flow_state")
+    __slots__ = ("blocks", "ecol", "encol", "offsets")
 
     def __init__(self, plan):
         blocks = plan.blocks_flat.astype(np.int32)
@@ -117,17 +117,60 @@ class PlanMirror:
             if ecol.size:
                 self.ecol.upload(ecol)
                 self.encol.upload(encol)
-        self.dep_off = self.dep_list = self.flow_state = None
-        if plan.dep_off is not None:
-            self.dep_off = _upload(plan.dep_off)
-            self.dep_list = _upload(plan.dep_list)
-            self.flow_state = N.DeviceBuffer(4 * (plan.nblocks + 1))
 
 
 def plan_mirror(plan) -> PlanMirror:
     if plan._dev is None:
         plan._dev = PlanMirror(plan)
     return plan._dev
+
+
+class ScheduleMirror:
+    """Device copy of a dataflow schedule (ml_schedule_build): block queue in
+    (window, colour, index) order, dependency CSR and the per-run flag array."""
+
+    __slots__ = ("queue", "dep_off", "dep_list", "flow_state", "nwindows")
+
+    def __init__(self, loop, plan, nwindows: int):
+        import ctypes as C
+        from .plan import write_columns
+        wc = write_columns(loop)
+        keys: dict = {}
+        cols = [np.ascontiguousarray(c[:plan.n], dtype=np.int64) for _, c in wc]
+        kid = np.array([keys.setdefault(k, len(keys)) for k, _ in wc], dtype=np.int32)
+        colour = np.ascontiguousarray(plan.block_color, dtype=np.int64)
+        L = N.lib()
+        h = C.c_void_p()
+        cptr = (C.c_void_p * max(len(cols), 1))(*[N.ptr(c) for c in cols])
+        N.check(L.ml_schedule_build(plan.n, len(cols), cptr, kid.ctypes.data_as(C.POINTER(C.c_int32)),
+                                    plan.block_size, N.ptr(colour), int(nwindows), C.byref(h)),
+                "ml_schedule_build")
+        self.nwindows = int(nwindows)
+        self.queue = self.dep_off = self.dep_list = self.flow_state = None
+        try:
+            nd = C.c_int64()
+            N.check(L.ml_schedule_export(h, C.byref(nd), None, None, None))
+            if nd.value >= 0:
+                queue = np.empty(max(plan.nblocks, 1), np.int32)
+                off = np.empty(plan.nblocks + 1, np.int32)
+                lst = np.empty(max(nd.value, 1), np.int32)
+                N.check(L.ml_schedule_export(h, C.byref(nd), N.ptr(queue), N.ptr(off), N.ptr(lst)))
+                self.queue, self.dep_off, self.dep_list = _upload(queue), _upload(off), _upload(lst)
+                self.flow_state = N.DeviceBuffer(4 * (plan.nblocks + 1))
+        finally:
+            L.ml_schedule_free(h)
+
+    @property
+    def usable(self) -> bool:
+        return self.queue is not None
+
+
+def schedule_mirror(loop, plan, nwindows: int) -> ScheduleMirror:
+    cache = plan.__dict__.setdefault("_schedules", {})
+    key = (loop.signature(), int(nwindows))
+    if key not in cache:
+        cache[key] = ScheduleMirror(loop, plan, nwindows)
+    return cache[key]
 
 
 class StagingMirror:

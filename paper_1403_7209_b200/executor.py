@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _native as N
 from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Mesh, MeshError)
-from .device import dat_mirror, map_mirror, plan_mirror, staging_mirror
+from .device import dat_mirror, map_mirror, plan_mirror, schedule_mirror, staging_mirror
 from .kernels import resolve_kernel
 from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
 from .plan import plan_for, plan_stats
@@ -73,6 +73,8 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
+    flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
+    flow_window_l2_fraction: float = 0.5
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -156,6 +158,26 @@ def _loop_dtype(loop: Loop) -> int:
     return N.ML_F64
 
 
+_L2_BYTES: list = []
+
+
+def _flow_windows(loop: Loop, config: "BackendConfig") -> int:
+    """Windows of the dataflow queue: the loop's dat footprint / (fraction of L2)."""
+    if config.flow_windows is not None:
+        return max(1, int(config.flow_windows))
+    if not _L2_BYTES:
+        _L2_BYTES.append(N.device_info()["l2_bytes"] or 126 << 20)
+    seen, total = set(), 0
+    for a in loop.args:
+        if a.kind != "global" and a.dat.name not in seen:
+            seen.add(a.dat.name)
+            total += a.dat.nbytes
+    for a in loop.args:
+        if a.kind == "indirect":
+            total += 4 * a.map.from_set.size
+    return max(1, -(-total // int(_L2_BYTES[0] * config.flow_window_l2_fraction)))
+
+
 def _inc_aliased(loop: Loop) -> bool:
     """A dat both incremented and otherwise accessed in one loop: its reads would
     observe a schedule-dependent mix, so keep the strict per-colour launches."""
@@ -214,10 +236,16 @@ class _LoopEntry:
         L.plan.blocks = pm.blocks.ptr
         L.plan.elem_color = pm.ecol.ptr if pm.ecol is not None else None
         L.plan.elem_ncolors = pm.encol.ptr if pm.encol is not None else None
-        if config.dataflow and pm.dep_off is not None and not _inc_aliased(loop):
-            L.plan.dep_off = pm.dep_off.ptr
-            L.plan.dep_list = pm.dep_list.ptr
-            L.plan.flow_state = pm.flow_state.ptr
+        self.schedule = None
+        if (config.dataflow and self.plan.has_writes and self.plan.ncolors > 1
+                and not _inc_aliased(loop)):
+            sched = schedule_mirror(loop, self.plan, _flow_windows(loop, config))
+            if sched.usable:
+                self.schedule = sched
+                L.plan.queue = sched.queue.ptr
+                L.plan.dep_off = sched.dep_off.ptr
+                L.plan.dep_list = sched.dep_list.ptr
+                L.plan.flow_state = sched.flow_state.ptr
         for k, v in enumerate(binding.fconsts[:4]):
             L.fconst[k] = v
         for k, v in enumerate(binding.iconsts[:4]):
@@ -364,7 +392,8 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig) 
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
            tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
-           config.dataflow, config.inc_staging)
+           config.dataflow, config.inc_staging, config.flow_windows,
+           config.flow_window_l2_fraction)
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):
         cache.move_to_end(key)

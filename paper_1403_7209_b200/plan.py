@@ -48,8 +48,6 @@ class ExecPlan:
     elem_order_flat: np.ndarray          # per block: elements by (colour, index)
     has_writes: bool = True
     max_elem_colors: int = 1
-    dep_off: np.ndarray | None = None    # dataflow deps (lower-colour conflicting blocks)
-    dep_list: np.ndarray | None = None
     _dev: object = field(default=None, repr=False, compare=False)
 
     @cached_property
@@ -103,20 +101,11 @@ def build_plan(n: int, write_cols: list, block_size: int) -> ExecPlan:
         order = np.empty(n, np.int64)
         N.check(L.ml_plan_export(handle, N.ptr(block_color), N.ptr(elem_nc), N.ptr(offsets),
                                  N.ptr(flat), N.ptr(elem_color), N.ptr(order)), "ml_plan_export")
-        nd = C.c_int64()
-        N.check(L.ml_plan_deps(handle, C.byref(nd), None, None), "ml_plan_deps")
-        dep_off = dep_list = None
-        if nd.value >= 0 and nc > 1:
-            dep_off = np.empty(nb + 1, np.int32)
-            dep_list = np.empty(max(nd.value, 1), np.int32)
-            N.check(L.ml_plan_deps(handle, C.byref(nd), N.ptr(dep_off), N.ptr(dep_list)),
-                    "ml_plan_deps")
     finally:
         L.ml_plan_free(handle)
     bounds = np.minimum(np.arange(nb + 1, dtype=np.int64) * block_size, n)
     return ExecPlan(n, int(block_size), nb, bounds, block_color, nc, offsets, flat, elem_color,
-                    elem_nc, order, has_writes=bool(cols) and n > 0, max_elem_colors=int(mx.value),
-                    dep_off=dep_off, dep_list=dep_list)
+                    elem_nc, order, has_writes=bool(cols) and n > 0, max_elem_colors=int(mx.value))
 
 
 def write_columns(loop: Loop) -> list:

@@ -232,18 +232,21 @@ def test_graph_replay_and_host_residency_match_eager():
 
 
 @pytest.mark.parametrize("bs", [32, 256])
-def test_dataflow_schedule_is_bitwise_identical_to_colour_launches(bs):
-    """Same per-target increment order, so float results must match bit for bit."""
+def test_dataflow_schedule_matches_colour_launches(bs):
+    """One window: same per-target increment order as per-colour launches, so float
+    results match bit for bit; several windows reorder increments (tolerance)."""
     outs = []
-    for flow in (True, False):
+    for kw in ({"dataflow": False}, {"flow_windows": 1}, {"flow_windows": 7}):
         mesh = apps.gen_hex_mesh(20, seed=8)
         apps.shuffle_mesh(mesh, seed=9)
         prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=8)
         ml.renumber_mesh(mesh)
-        ml.run_program(prog[:5], mesh, cfg(block_size=bs, dataflow=flow))
+        ml.run_program(prog[:5], mesh, cfg(block_size=bs, **kw))
         outs.append((h["res"].fetch(), h["grad"].fetch()))
-    np.testing.assert_array_equal(outs[0][0], outs[1][0])
-    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(outs[1][0], outs[0][0])
+    np.testing.assert_array_equal(outs[1][1], outs[0][1])
+    close(outs[2][0], outs[0][0], what="res")
+    close(outs[2][1], outs[0][1], what="grad")
     for make in (lambda: apps.gen_hub_mesh(5000, 60000, n_hubs=64, hub_share=0.05, seed=3),
                  lambda: _shuffled_hex(16)):
         ref, mesh = make(), make()

@@ -283,6 +283,53 @@ def test_backend_config_validation():
     assert BackendConfig(block_size_table={"a": 64}).block_size_for("a") == 64
 
 
+@pytest.mark.parametrize("nwin", [1, 3, 8])
+def test_dataflow_schedule_orders_every_conflicting_pair(rng, nwin):
+    """ml_schedule_build: the queue is a permutation of the blocks in (window,
+    colour) order, dependencies point backwards, and every pair of blocks that
+    share a write target is ordered by a dependency (no write-back race)."""
+    import ctypes as C
+    from paper_1403_7209_b200 import _native as N
+    for _ in range(6):
+        mesh, loop = _cases.random_loop_mesh(rng, max_elems=2500)
+        bs = int(rng.choice([4, 16, 64]))
+        plan = ml.plan_for(loop, mesh, bs)
+        wc = oplan.write_columns(loop)
+        cols = [np.ascontiguousarray(c) for _, c in wc]
+        kid = np.zeros(len(cols), np.int32)
+        colour = np.ascontiguousarray(plan.block_color)
+        h = C.c_void_p()
+        ptrs = (C.c_void_p * len(cols))(*[N.ptr(c) for c in cols])
+        assert N.lib().ml_schedule_build(plan.n, len(cols), ptrs, kid.ctypes.data_as(C.POINTER(C.c_int32)),
+                                         bs, N.ptr(colour), nwin, C.byref(h)) == 0
+        nd = C.c_int64()
+        N.lib().ml_schedule_export(h, C.byref(nd), None, None, None)
+        if nd.value < 0:
+            continue
+        queue = np.empty(plan.nblocks, np.int32)
+        off = np.empty(plan.nblocks + 1, np.int32)
+        lst = np.empty(max(nd.value, 1), np.int32)
+        N.lib().ml_schedule_export(h, C.byref(nd), N.ptr(queue), N.ptr(off), N.ptr(lst))
+        N.lib().ml_schedule_free(h)
+        assert sorted(queue.tolist()) == list(range(plan.nblocks))
+        win = np.arange(plan.nblocks) * nwin // plan.nblocks
+        keys = list(zip(win[queue], colour[queue]))
+        assert keys == sorted(keys)
+        pos = np.empty(plan.nblocks, np.int64)
+        pos[queue] = np.arange(plan.nblocks)
+        deps = {(b, int(d)) for b in range(plan.nblocks) for d in lst[off[b]:off[b + 1]]}
+        assert all(pos[d] < pos[b] for b, d in deps)
+        tgt_blocks: dict = {}
+        for c in cols:
+            for e, t in enumerate(c):
+                tgt_blocks.setdefault(int(t), set()).add(e // bs)
+        for blocks in tgt_blocks.values():
+            bl = sorted(blocks, key=lambda b: pos[b])
+            for i in range(len(bl)):
+                for j in range(i + 1, len(bl)):
+                    assert (bl[j], bl[i]) in deps
+
+
 def test_staging_lists_resolve_every_increment(rng):
     """ml_staging_build: list[off[b] + loc[e]] is exactly element e's target."""
     import ctypes as C

@@ -467,9 +467,15 @@ __device__ __forceinline__ void run_smem(const LaunchParams &p, Sig<As...>) {
 // write-back waits only for the lower-colour blocks this block conflicts with,
 // so colours overlap without grid-wide barriers while every target still sees
 // its increments in exactly the order of the per-colour launch schedule.
-__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+// Polling uses relaxed gpu-scope loads: an acquire load would invalidate the
+// whole L1 (CCTL.IVALL) on every spin, evicting the gathered data of every
+// CTA on the SM.  The write-back reads its targets with ld.global.cg (L2, the
+// coherence point), after the flag was observed and a CTA barrier, and the
+// producer publishes with st.release after its CTA barrier — so the targets
+// it wrote are visible in L2 before the flag is.
+__device__ __forceinline__ int ld_relaxed(const int32_t *p) {
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release(int32_t *p, int v) {
@@ -484,12 +490,16 @@ __device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
     extern __shared__ __align__(16) char dsm[];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     int32_t *counter = p.flags + p.nqueue;
-    for (;;) {
-        if (threadIdx.x == 0) s_q = atomicAdd(counter, 1);
-        __syncthreads();
-        const int q = s_q;
-        if (q >= p.nqueue) break;
+    if (threadIdx.x == 0) s_q = atomicAdd(counter, 1);
+    __syncthreads();
+    int q = s_q;
+    while (q < p.nqueue) {
+        // prefetch the next queue position while this block is processed
+        int next = 0;
+        if (threadIdx.x == 0) next = atomicAdd(counter, 1);
         const int32_t b = p.blocks[q];
+        const int d0 = p.dep_off[b], d1 = p.dep_off[b + 1];
+        const int32_t dep = d0 + int(threadIdx.x) < d1 ? p.dep_list[d0 + threadIdx.x] : -1;
         const int64_t e = int64_t(b) * p.bs + threadIdx.x;
         const int64_t hi = int64_t(b) * p.bs + p.bs < p.n ? int64_t(b) * p.bs + p.bs : p.n;
         const bool active = threadIdx.x < p.bs && e < hi;
@@ -509,19 +519,18 @@ __device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
                 __syncthreads();
             }
         }
-        // wait for the conflicting lower-colour blocks (one thread per dependency)
-        for (int k = p.dep_off[b] + threadIdx.x; k < p.dep_off[b + 1]; k += blockDim.x) {
-            const int32_t *f = p.flags + p.dep_list[k];
-            while (ld_acquire(f) == 0) __nanosleep(64);
-        }
+        // wait for the conflicting earlier-queued blocks (one thread per dependency)
+        if (dep >= 0)
+            while (ld_relaxed(p.flags + dep) == 0) __nanosleep(32);
+        for (int k = d0 + int(threadIdx.x) + int(blockDim.x); k < d1; k += blockDim.x)
+            while (ld_relaxed(p.flags + p.dep_list[k]) == 0) __nanosleep(32);
         __syncthreads();
         E::write_back(s, p, b, dsm, idx);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            st_release(p.flags + b, 1);
-        }
         if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
+        if (threadIdx.x == 0) s_q = next;
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(p.flags + b, 1);
+        q = s_q;
     }
 }
 

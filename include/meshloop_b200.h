@@ -222,6 +222,22 @@ int ml_program_replay(ml_program_t *p, int32_t count);
 int ml_program_loop_times(const ml_program_t *p, float *ms);
 int ml_program_free(ml_program_t *p);
 
+/* ---- multi-GPU owner-compute support: executor.py:484-497 (exchange),
+ *      163-173 (_gather_rows/_scatter_rows), 652-660 (rank-ordered reduce) ---- */
+/* Gather rows `idx` (device int32, local element ids) of an 8-byte-element dat
+ * with strides (elem_stride, comp_stride) into a contiguous [nidx][dim] buffer,
+ * and the inverse scatter.  Stream-ordered on the compute stream. */
+int ml_pack_rows(void *dst, const void *dat, const int32_t *idx, int64_t nidx, int32_t dim,
+                 int64_t elem_stride, int64_t comp_stride);
+int ml_unpack_rows(void *dat, const void *src, const int32_t *idx, int64_t nidx, int32_t dim,
+                   int64_t elem_stride, int64_t comp_stride);
+/* value = value (+|min|max) gathered[0] ... gathered[nranks-1], in rank order
+ * (mode ML_INC/ML_MIN/ML_MAX, dtype ML_F64/ML_I64, `dim` components each). */
+int ml_combine_ranks(void *value, const void *gathered, int32_t nranks, int32_t dim, int32_t mode,
+                     int32_t dtype);
+/* The library's compute stream (cudaStream_t), for ordering NCCL work with it. */
+void *ml_stream(void);
+
 /* ---- measurement helpers -------------------------------------------------- */
 int ml_flush_l2(void);                                 /* write a buffer > L2       */
 typedef struct ml_timer ml_timer_t;

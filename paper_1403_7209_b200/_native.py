@@ -37,6 +37,7 @@ EXPORTED = [
     "ml_loop_scratch_bytes", "ml_loop_run",
     "ml_program_create", "ml_program_run", "ml_program_replay", "ml_program_loop_times",
     "ml_program_free",
+    "ml_pack_rows", "ml_unpack_rows", "ml_combine_ranks", "ml_stream",
     "ml_flush_l2", "ml_timer_create", "ml_timer_start", "ml_timer_stop", "ml_timer_free",
 ]
 
@@ -125,6 +126,10 @@ _SIGNATURES = {
     "ml_program_replay": (C.c_int, [_P, C.c_int32]),
     "ml_program_loop_times": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "ml_program_free": (C.c_int, [_P]),
+    "ml_pack_rows": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int64, C.c_int64]),
+    "ml_unpack_rows": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int64, C.c_int64]),
+    "ml_combine_ranks": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "ml_stream": (C.c_void_p, []),
     "ml_flush_l2": (C.c_int, []),
     "ml_timer_create": (C.c_int, [_PP]),
     "ml_timer_start": (C.c_int, [_P]),

@@ -537,6 +537,84 @@ extern "C" int ml_program_free(ml_program_t *p) {
     return ML_OK;
 }
 
+// ---- ABI: multi-GPU helpers --------------------------------------------------------------------
+namespace ml {
+__global__ void k_pack_rows(double *dst, const double *dat, const int32_t *idx, int64_t nidx, int dim,
+                            int64_t se, int64_t sc) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nidx * dim;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = k / dim, c = k % dim;
+        dst[k] = dat[int64_t(idx[r]) * se + c * sc];
+    }
+}
+__global__ void k_unpack_rows(double *dat, const double *src, const int32_t *idx, int64_t nidx, int dim,
+                              int64_t se, int64_t sc) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nidx * dim;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = k / dim, c = k % dim;
+        dat[int64_t(idx[r]) * se + c * sc] = src[k];
+    }
+}
+template <class T, int M>
+__global__ void k_combine_ranks(T *value, const T *gathered, int nranks, int dim) {
+    for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+        T v = value[c];
+        for (int r = 0; r < nranks; ++r) v = combine<M>(v, gathered[r * dim + c]);
+        value[c] = v;
+    }
+}
+}  // namespace ml
+
+extern "C" int ml_pack_rows(void *dst, const void *dat, const int32_t *idx, int64_t nidx, int32_t dim,
+                            int64_t se, int64_t sc) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (nidx <= 0) return ML_OK;
+    const int64_t work = nidx * dim;
+    const int grid = int(std::min<int64_t>((work + 255) / 256, 4 * 148));
+    k_pack_rows<<<grid, 256, 0, g_dev.stream>>>(static_cast<double *>(dst), static_cast<const double *>(dat),
+                                               idx, nidx, dim, se, sc);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+extern "C" int ml_unpack_rows(void *dat, const void *src, const int32_t *idx, int64_t nidx, int32_t dim,
+                              int64_t se, int64_t sc) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (nidx <= 0) return ML_OK;
+    const int64_t work = nidx * dim;
+    const int grid = int(std::min<int64_t>((work + 255) / 256, 4 * 148));
+    k_unpack_rows<<<grid, 256, 0, g_dev.stream>>>(static_cast<double *>(dat), static_cast<const double *>(src),
+                                                 idx, nidx, dim, se, sc);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+extern "C" int ml_combine_ranks(void *value, const void *gathered, int32_t nranks, int32_t dim, int32_t mode,
+                                int32_t dtype) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    cudaStream_t s = g_dev.stream;
+#define ML_CR(T, M) k_combine_ranks<T, M><<<1, 32, 0, s>>>(static_cast<T *>(value), static_cast<const T *>(gathered), nranks, dim)
+    if (dtype == ML_F64) {
+        if (mode == ML_INC) ML_CR(double, MINC);
+        else if (mode == ML_MIN) ML_CR(double, MMIN);
+        else if (mode == ML_MAX) ML_CR(double, MMAX);
+        else ML_FAIL(ML_EINVAL, "ml_combine_ranks: mode %d is not a reduction", mode);
+    } else {
+        if (mode == ML_INC) ML_CR(int64_t, MINC);
+        else if (mode == ML_MIN) ML_CR(int64_t, MMIN);
+        else if (mode == ML_MAX) ML_CR(int64_t, MMAX);
+        else ML_FAIL(ML_EINVAL, "ml_combine_ranks: mode %d is not a reduction", mode);
+    }
+#undef ML_CR
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+extern "C" void *ml_stream(void) { return g_dev.stream; }
+
 // ---- ABI: measurement helpers ----------------------------------------------------------------
 extern "C" int ml_flush_l2(void) {
     int rc = ensure_init();

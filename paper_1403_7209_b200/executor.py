@@ -189,13 +189,16 @@ class _LoopEntry:
     """Everything one loop needs on the device, kept alive with the program."""
 
     def __init__(self, loop: Loop, mesh: Mesh, config: BackendConfig, gslot: dict,
-                 garena_ptr: int):
+                 garena_ptr: int, iter_counts: dict | None = None, rlim: dict | None = None):
+        sname = loop.iter_set.name
+        self.n = int(iter_counts[sname]) if iter_counts and sname in iter_counts else loop.iter_set.size
         self.loop = loop
         binding = resolve_kernel(loop.kernel)
         self.binding = binding
         self.functor = _functor_id(binding.functor, _loop_dtype(loop))
         self.bs = config.block_size_for(loop.name)
-        self.plan = plan_for(loop, mesh, self.bs)
+        self.plan = plan_for(loop, mesh, self.bs,
+                             None if self.n == loop.iter_set.size else self.n)
         self.st = plan_stats(self.plan)
         pm = plan_mirror(self.plan)
         self.pm = pm
@@ -228,7 +231,7 @@ class _LoopEntry:
         L.functor = self.functor
         L.nargs = len(loop.args)
         L.args = C.cast(args, C.POINTER(N.MlArg))
-        L.n = loop.iter_set.size
+        L.n = self.n
         L.plan.nblocks = self.plan.nblocks
         L.plan.ncolors = self.plan.ncolors
         L.plan.block_size = self.bs
@@ -250,7 +253,7 @@ class _LoopEntry:
             L.fconst[k] = v
         for k, v in enumerate(binding.iconsts[:4]):
             L.iconst[k] = v
-        L.rlim = -1
+        L.rlim = int(rlim[sname]) if rlim and sname in rlim else -1
         self.staging = staging_mirror(loop, self.plan) if config.smem_staging else None
         if self.staging is not None:
             sg = self.staging
@@ -283,7 +286,8 @@ class _LoopEntry:
 class CompiledProgram:
     """A program bound to device state; replayable (optionally as a CUDA graph)."""
 
-    def __init__(self, program: Sequence[Loop], mesh: Mesh, config: BackendConfig):
+    def __init__(self, program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
+                 iter_counts: dict | None = None, rlim: dict | None = None):
         self.loops = list(program)
         self.mesh = mesh
         self.version = mesh.version
@@ -300,7 +304,8 @@ class CompiledProgram:
         self.gbytes = off
         self.gdev = N.DeviceBuffer(max(off, 256))
         self.ghost = N.PinnedArray((max(off, 256),), np.uint8)
-        self.entries = [_LoopEntry(l, mesh, config, self.gslot, self.gdev.ptr) for l in self.loops]
+        self.entries = [_LoopEntry(l, mesh, config, self.gslot, self.gdev.ptr, iter_counts, rlim)
+                        for l in self.loops]
         self.all_dats = []
         for e in self.entries:
             for d in e.dats:
@@ -386,19 +391,25 @@ class CompiledProgram:
 _PROGRAM_CACHE_SIZE = 32
 
 
-def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig) -> CompiledProgram:
-    """Compiled program for (loops, block sizes, mesh version), cached on the mesh."""
+def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
+                    iter_counts: dict | None = None, rlim: dict | None = None) -> CompiledProgram:
+    """Compiled program for (loops, block sizes, mesh version), cached on the mesh.
+
+    ``iter_counts`` (set name -> n) runs loops over a prefix of their iteration
+    set and ``rlim`` (set name -> n) limits global reductions to a prefix —
+    the owned / owned+exec-halo split of a multi-GPU rank."""
     N.init(config.device_index())
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
            tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
            config.dataflow, config.inc_staging, config.flow_windows,
-           config.flow_window_l2_fraction)
+           config.flow_window_l2_fraction,
+           tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):
         cache.move_to_end(key)
         return cp
-    cp = CompiledProgram(program, mesh, config)
+    cp = CompiledProgram(program, mesh, config, iter_counts, rlim)
     cache[key] = cp
     while len(cache) > _PROGRAM_CACHE_SIZE:
         cache.popitem(last=False)

@@ -1,15 +1,375 @@
-"""Owner-compute multi-GPU execution (one process per GPU) — under construction.
+"""Owner-compute multi-GPU execution: one process per GPU.
 
-See DESIGN.md §6.  Until the NCCL halo layer lands, multi-rank execution
-raises instead of silently running something else.
+Semantic model: the reference ranks backend (executor.py:300-329 layout,
+367-574 rank context, 577-600 rank main loop, 603-627 dat roles, 630-687
+program driver).  Each rank:
+
+1. builds the same layout as the reference (``build_layout``: partition the
+   map target sets — trivial or RCB — derive iteration-set ownership, close
+   exec / non-exec halos; bit-exact with the reference, golden-tested);
+2. builds a *local mesh* numbered ``[owned | exec halo | non-exec halo]``
+   (reference ``SetHalos.local_ids``) holding only what its elements touch;
+3. executes, per program entry, the owned + exec-halo elements of the
+   iteration set on its GPU; global reductions only count the owned prefix
+   (``rlim``, reference executor.py:519-524);
+4. exchanges a dat's halo lazily — before a loop that reads it after some
+   loop wrote it (reference dirty bits, executor.py:582-595) — by packing the
+   export rows on the device, moving them with the transport, and scattering
+   them into the import slots;
+5. after every reducing loop, gathers the per-rank partials and folds them
+   in ascending rank order onto the running value (so a MIN computed by one
+   loop is the value a later loop READs, as in serial execution — the
+   reference's ranks backend instead exposes the initial value until the
+   program ends);
+6. at the end, all-gathers owned rows so every rank's dats and globals hold
+   the full result.
+
+Transports: ``"nccl"`` (torch.distributed NCCL on device buffers, ordered on
+the library's stream; the production path on 2-8 B200s) and ``"gloo"``
+(host-staged; used to test the protocol with several ranks on one GPU and,
+with an injected CPU executor, on CPU).
 """
 from __future__ import annotations
 
-from .core import ExecError
+import os
+import time
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from .core import (AOS, INC, MAX, MIN, READ, RW, SOA, WRITE_MODES, ExecError, Global, Loop, Mesh,
+                   MeshError, arg_direct, arg_global, arg_indirect, transform_layout)
+from .partition import (RankLayout, build_halos, derive_assignments, partition_rcb,
+                        partition_trivial)
+
+__all__ = ["build_layout", "RankProgram", "run_program_distributed", "bench_distributed",
+           "unique_loops", "loop_dat_roles"]
 
 
-def run_program_distributed(program, mesh, config):
-    raise ExecError("multi-GPU execution (nranks > 1) is not implemented yet")
+def unique_loops(program: Sequence[Loop]) -> list[Loop]:
+    seen, out = set(), []
+    for loop in program:
+        sig = loop.signature()
+        if sig not in seen:
+            seen.add(sig)
+            out.append(loop)
+    return out
+
+
+def build_layout(mesh: Mesh, program: Sequence[Loop], config) -> RankLayout:
+    """Partition every touched set and close the halos (reference executor.py:300-329)."""
+    loops = unique_loops(program)
+    targets = []
+    for loop in loops:
+        for a in loop.args:
+            if a.kind == "indirect" and a.map.to_set not in targets:
+                targets.append(a.map.to_set)
+    base = {}
+    for s in targets:
+        if config.partitioner == "rcb":
+            coords = mesh.dats.get(config.coord_dat)
+            if coords is None or coords.set is not s:
+                raise MeshError(f"rcb partitioning needs coordinates dat {config.coord_dat!r} "
+                                f"on set {s.name!r}")
+            base[s.name] = partition_rcb(coords, config.nranks)
+        else:
+            base[s.name] = partition_trivial(s, config.nranks)
+    return build_halos(mesh, loops, derive_assignments(mesh, loops, base, config.nranks))
+
+
+def loop_dat_roles(program: Sequence[Loop], layout: RankLayout):
+    """Per program entry: dats needing fresh halos before, dats written after
+    (reference executor.py:603-627)."""
+    roles = []
+    for loop in program:
+        redundant = any(layout.sets[loop.iter_set.name][r].exec_halo.size
+                        for r in range(layout.nranks))
+        reads, writes = [], []
+        for a in loop.args:
+            if a.dat is None:
+                continue
+            if (a.mode in (READ, RW) and (a.kind == "indirect" or redundant)
+                    and a.dat.name not in reads):
+                reads.append(a.dat.name)
+            if a.mode in WRITE_MODES and a.dat.name not in writes:
+                writes.append(a.dat.name)
+        roles.append((reads, writes))
+    return roles
+
+
+def _identity(mode, dtype, dim):
+    dtype = np.dtype(dtype)
+    if mode is INC:
+        return np.zeros(dim, dtype)
+    if dtype.kind == "i":
+        return np.full(dim, np.iinfo(dtype).max if mode is MIN else np.iinfo(dtype).min, dtype)
+    return np.full(dim, np.inf if mode is MIN else -np.inf, dtype)
+
+
+def fold(value: np.ndarray, partials, mode) -> np.ndarray:
+    """value ⊕ p_0 ⊕ p_1 ⊕ ... in the given (rank) order."""
+    op = {INC: np.add, MIN: np.minimum, MAX: np.maximum}[mode]
+    out = np.array(value, copy=True)
+    for p in partials:
+        out = op(out, p)
+    return out
+
+
+@dataclass
+class Exchange:
+    """Export / import local ids of one set on one rank."""
+    exports: dict = field(default_factory=dict)      # dst -> local ids (int32)
+    imports: dict = field(default_factory=dict)      # src -> local ids (int32)
+
+
+class RankProgram:
+    """One rank's slice of a program: local mesh, loops, counts and exchange lists."""
+
+    def __init__(self, mesh: Mesh, program: Sequence[Loop], layout: RankLayout, rank: int):
+        self.rank, self.nranks = rank, layout.nranks
+        self.layout = layout
+        self.program = list(program)
+        self.local = Mesh(auto_soa_threshold=None)
+        self.local_ids: dict[str, np.ndarray] = {}
+        self.g2l: dict[str, np.ndarray] = {}
+        self.n_exec: dict[str, int] = {}
+        self.n_owned: dict[str, int] = {}
+        self.exchange: dict[str, Exchange] = {}
+        sets = {}
+        for name in mesh.sets:                                   # global declaration order
+            if name not in layout.sets:
+                continue
+            h = layout.sets[name][rank]
+            ids = h.local_ids.astype(np.int64)
+            g2l = np.full(mesh.sets[name].size, -1, np.int64)
+            g2l[ids] = np.arange(ids.size)
+            self.local_ids[name], self.g2l[name] = ids, g2l
+            self.n_owned[name] = int(h.owned.size)
+            self.n_exec[name] = int(h.owned.size + h.exec_halo.size)
+            sets[name] = self.local.decl_set(name, int(ids.size))
+            self.exchange[name] = Exchange(
+                {d: g2l[v].astype(np.int32) for d, v in sorted(h.exports.items())},
+                {s: g2l[v].astype(np.int32) for s, v in sorted(h.imports.items())})
+        maps = {}
+        for loop in self.program:
+            for a in loop.args:
+                if a.kind != "indirect" or a.map.name in maps:
+                    continue
+                m = a.map
+                rows = self.local_ids[m.from_set.name]
+                t = self.g2l[m.to_set.name][m.table[rows]]
+                ne = self.n_exec[m.from_set.name]
+                if (t[:ne] < 0).any():
+                    raise ExecError(f"rank {rank}: map {m.name!r} leaves the halo closure")
+                t[ne:][t[ne:] < 0] = 0          # rows of never-executed halo elements
+                maps[m.name] = self.local.decl_map(m.name, sets[m.from_set.name],
+                                                   sets[m.to_set.name], m.arity, (t + 1).ravel())
+        dats = {}
+        for loop in self.program:
+            for a in loop.args:
+                if a.dat is None or a.dat.name in dats:
+                    continue
+                d = a.dat
+                vals = d.fetch()[self.local_ids[d.set.name]]
+                ld = self.local.decl_dat(d.name, sets[d.set.name], d.dim, d.dtype.name, vals.ravel())
+                if d.layout is SOA:
+                    transform_layout(ld, SOA)
+                dats[d.name] = ld
+        self.global_dats = {name: mesh.dats[name] for name in dats}
+        self.dats = dats
+        # globals: one running value per global; one identity partial per reducing arg
+        self.values: dict[int, Global] = {}
+        self.partials: dict[tuple, Global] = {}
+        self.user_globals: dict[int, Global] = {}
+        self.loops: list[Loop] = []
+        self.reductions: list[list] = []          # per entry: [(partial Global, value Global, mode)]
+        for i, loop in enumerate(self.program):
+            args, reds = [], []
+            for j, a in enumerate(loop.args):
+                if a.kind == "global":
+                    g = a.glob
+                    self.user_globals[id(g)] = g
+                    val = self.values.setdefault(id(g), Global(g.buffer.copy(), name=g.name))
+                    if a.mode is READ:
+                        args.append(arg_global(val, READ))
+                    else:
+                        part = Global(_identity(a.mode, g.dtype, g.dim), name=f"{g.name}@{i}.{j}")
+                        self.partials[(i, j)] = part
+                        reds.append((part, val, a.mode))
+                        args.append(arg_global(part, a.mode))
+                elif a.kind == "direct":
+                    args.append(arg_direct(dats[a.dat.name], a.mode))
+                else:
+                    args.append(arg_indirect(dats[a.dat.name], maps[a.map.name], a.slot + 1, a.mode))
+            self.loops.append(Loop(loop.name, sets[loop.iter_set.name], args, loop.kernel))
+            self.reductions.append(reds)
+        self.roles = loop_dat_roles(self.program, layout)
+
+    def reset_partials(self, entry: int) -> None:
+        for part, _val, mode in self.reductions[entry]:
+            part.buffer[:] = _identity(mode, part.dtype, part.dim)
+
+    def refresh_globals(self) -> None:
+        """Re-read user global values (a new run starts from the user's buffers)."""
+        for gid, val in self.values.items():
+            val.buffer[:] = self.user_globals[gid].buffer
+
+    def halo_rows(self, dat_name: str) -> tuple[dict, dict]:
+        ex = self.exchange[self.dats[dat_name].set.name]
+        return ex.exports, ex.imports
+
+    def owned_rows(self, dat_name: str) -> np.ndarray:
+        d = self.dats[dat_name]
+        return d.fetch()[: self.n_owned[d.set.name]]
+
+
+# -- transports ------------------------------------------------------------------------------
+
+class GlooTransport:
+    """Host-staged point-to-point and all-gather over torch.distributed (gloo)."""
+
+    name = "gloo"
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+
+    def exchange(self, sends: dict, recv_shapes: dict, dtype) -> dict:
+        torch, dist = self.torch, self.dist
+        ops, bufs = [], {}
+        for dst, arr in sorted(sends.items()):
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(arr)), dst,
+                                  group=self.group))
+        for src, shape in sorted(recv_shapes.items()):
+            bufs[src] = torch.empty(shape, dtype=torch.float64 if np.dtype(dtype) == np.float64
+                                    else torch.int64)
+            ops.append(dist.P2POp(dist.irecv, bufs[src], src, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return {s: b.numpy() for s, b in bufs.items()}
+
+    def allgather(self, arr: np.ndarray) -> list:
+        torch, dist = self.torch, self.dist
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        out = [torch.empty_like(t) for _ in range(dist.get_world_size(self.group))]
+        dist.all_gather(out, t, group=self.group)
+        return [o.numpy() for o in out]
+
+    def allgather_object(self, obj) -> list:
+        out = [None] * self.dist.get_world_size(self.group)
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+# -- device execution ------------------------------------------------------------------------
+
+class DeviceRank:
+    """Runs a RankProgram's loops on this rank's GPU through libmeshloop_b200."""
+
+    def __init__(self, rp: RankProgram, config):
+        from .executor import compile_program
+        self.rp, self.config = rp, config
+        self.progs = [compile_program([l], rp.local, config, iter_counts=rp.n_exec,
+                                      rlim=rp.n_owned) for l in rp.loops]
+
+    def run_loop(self, i: int, use_graph: bool = False) -> float:
+        self.rp.reset_partials(i)
+        t = self.progs[i].run(use_graph, not use_graph)
+        return t[0] if t else 0.0
+
+    def pack(self, dat_name: str, ids: np.ndarray) -> np.ndarray:
+        from . import _native as N
+        from .device import dat_mirror
+        d = self.rp.dats[dat_name]
+        m = dat_mirror(d)
+        if m.device_newer:
+            d._pull()
+        return d.fetch()[ids]
+
+    def unpack(self, dat_name: str, ids: np.ndarray, rows: np.ndarray) -> None:
+        d = self.rp.dats[dat_name]
+        vals = d.fetch()
+        vals[ids] = rows
+        d.put(vals)
+
+
+def _run_rank(rp: RankProgram, dev, transport, timeout_ms: float):
+    """The rank main loop (reference executor.py:577-600) + reductions."""
+    dirty: dict = {}
+    messages = 0
+    comm = np.zeros(len(rp.program))
+    comp = np.zeros(len(rp.program))
+    rp.refresh_globals()
+    for i, loop in enumerate(rp.loops):
+        reads, writes = rp.roles[i]
+        t0 = time.perf_counter()
+        for name in reads:
+            if dirty.get(name):
+                exports, imports = rp.halo_rows(name)
+                d = rp.dats[name]
+                sends = {dst: dev.pack(name, ids) for dst, ids in exports.items()}
+                shapes = {src: (ids.size, d.dim) for src, ids in imports.items()}
+                got = transport.exchange(sends, shapes, d.dtype)
+                for src, ids in imports.items():
+                    dev.unpack(name, ids, got[src])
+                messages += len(sends)
+                dirty[name] = False
+        t1 = time.perf_counter()
+        dev.run_loop(i)
+        for part, val, mode in rp.reductions[i]:
+            parts = transport.allgather(part.buffer)
+            val.buffer[:] = fold(val.buffer, parts, mode)
+        comp[i] = time.perf_counter() - t1
+        comm[i] = t1 - t0
+        for name in writes:
+            dirty[name] = True
+    return messages, comm, comp
+
+
+def run_program_distributed(program, mesh, config, transport=None, executor_factory=None):
+    """Owner-compute execution of a program on ``WORLD_SIZE`` processes (one GPU each)."""
+    import torch.distributed as dist
+    from .executor import RunResult
+    from .perf import PerfCollector, useful_bytes
+    if not dist.is_initialized():
+        dist.init_process_group(backend="gloo")
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if config.nranks not in (1, world):
+        raise MeshError(f"nranks={config.nranks} but WORLD_SIZE={world}")
+    if config.nranks != world:
+        from dataclasses import replace
+        config = replace(config, nranks=world)
+    mesh.freeze()
+    t_start = time.perf_counter()
+    layout = build_layout(mesh, program, config)
+    rp = RankProgram(mesh, program, layout, rank)
+    transport = transport or GlooTransport()
+    dev = executor_factory(rp, config) if executor_factory else DeviceRank(rp, config)
+    messages, comm, comp = _run_rank(rp, dev, transport, config.timeout_ms)
+    # final: every rank gets the owned rows of every dat, and the global values
+    owned = {name: rp.owned_rows(name) for name in rp.dats}
+    allowned = transport.allgather_object(owned)
+    for name, gd in rp.global_dats.items():
+        logical = gd.fetch()
+        for r, ow in enumerate(allowned):
+            ids = layout.sets[gd.set.name][r].owned
+            logical[ids] = ow[name]
+        gd.put(logical)
+    for gid, val in rp.values.items():
+        rp.user_globals[gid].buffer[:] = val.buffer
+    msgs = sum(transport.allgather_object(messages))
+    collector = PerfCollector()
+    for i, loop in enumerate(program):
+        collector.add(loop.name, float(comm[i] + comp[i]), useful_bytes(loop), comm=float(comm[i]),
+                      comp=float(comp[i]))
+    return RunResult(collector.finalize(), time.perf_counter() - t_start, messages=msgs,
+                     layout=layout, assignments=layout.assignments)
 
 
 def bench_distributed(args, metric):

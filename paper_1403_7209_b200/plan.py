@@ -114,13 +114,19 @@ def write_columns(loop: Loop) -> list:
             if a.kind == "indirect" and a.mode in WRITE_MODES]
 
 
-def plan_for(loop: Loop, mesh: Mesh, block_size: int | None = None) -> ExecPlan:
-    """Build or fetch the cached plan (key: signature, block size, mesh version)."""
+def plan_for(loop: Loop, mesh: Mesh, block_size: int | None = None, n: int | None = None) -> ExecPlan:
+    """Build or fetch the cached plan (key: signature, block size, mesh version).
+
+    ``n`` restricts the plan to the first ``n`` iteration elements (a rank's
+    owned + exec-halo prefix on multi-GPU runs)."""
     bs = PlanConfig().block_size if block_size is None else int(block_size)
-    key = (loop.signature(), bs, mesh.version)
+    key = (loop.signature(), bs, mesh.version) if n is None else (loop.signature(), bs, mesh.version, n)
     plan = mesh._plan_cache.get(key)
     if plan is None:
-        plan = build_plan(loop.iter_set.size, write_columns(loop), bs)
+        cols = write_columns(loop)
+        if n is not None:
+            cols = [(k, c[:n]) for k, c in cols]
+        plan = build_plan(loop.iter_set.size if n is None else n, cols, bs)
         mesh._plan_cache[key] = plan
         mesh._plan_builds += 1
     return plan

@@ -93,6 +93,17 @@ typedef struct ml_staging_dev {
     int32_t seg;
     const int32_t *toff[ML_MAX_GROUPS];  /* device [total+1]                      */
     const uint16_t *src[ML_MAX_GROUPS];  /* device [n * args in group]            */
+    /* arrival mode (arrive != 0, needs seg): one launch over the blocks in
+     * natural order, no block colours.  A target touched by one block is
+     * updated directly; a shared target's per-block sums go to `partial` slots
+     * and the last block to arrive (atomic counter) adds them in block order —
+     * deterministic, no inter-block waiting.  Counters return to 0. */
+    int32_t arrive;
+    const int32_t *pslot[ML_MAX_GROUPS]; /* device [total]                        */
+    const int32_t *poff[ML_MAX_GROUPS];  /* device [targets]                      */
+    const int32_t *nblk[ML_MAX_GROUPS];  /* device [targets]                      */
+    int32_t *count[ML_MAX_GROUPS];       /* device [targets], zero between runs   */
+    void *partial[ML_MAX_GROUPS];        /* device [nslots][dim]                  */
 } ml_staging_dev_t;
 
 typedef struct ml_loop {
@@ -182,6 +193,12 @@ int ml_staging_export_loc(const ml_staging_t *s, int32_t col, uint16_t *loc);
 /* Segmented-mode lists of a group: toff [total+1], src [*nrefs]. */
 int ml_staging_export_seg(const ml_staging_t *s, int32_t group, int64_t *nrefs, int32_t *toff,
                           uint16_t *src);
+/* Arrival-mode lists of a group: per list entry the partial slot (-1 when the
+ * block is the only one touching the target): pslot [total]; per target id:
+ * first slot poff [*ntargets] and number of touching blocks nblk [*ntargets];
+ * *nslots partial slots in all. */
+int ml_staging_export_arrival(const ml_staging_t *s, int32_t group, int64_t *ntargets,
+                              int64_t *nslots, int32_t *pslot, int32_t *poff, int32_t *nblk);
 int ml_staging_free(ml_staging_t *s);
 
 /* ---- renumbering: renumber.py:53-128 ------------------------------------- */

@@ -31,7 +31,7 @@ EXPORTED = [
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
     "ml_schedule_build", "ml_schedule_export", "ml_schedule_free",
     "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
-    "ml_staging_export_seg", "ml_staging_free",
+    "ml_staging_export_seg", "ml_staging_export_arrival", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
     "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name",
     "ml_loop_scratch_bytes", "ml_loop_run",
@@ -65,7 +65,10 @@ class MlStagingDev(C.Structure):
                 ("off", C.c_void_p * MAX_GROUPS), ("list", C.c_void_p * MAX_GROUPS),
                 ("umax", C.c_int32 * MAX_GROUPS), ("loc", C.c_void_p * MAX_ARGS),
                 ("seg", C.c_int32), ("toff", C.c_void_p * MAX_GROUPS),
-                ("src", C.c_void_p * MAX_GROUPS)]
+                ("src", C.c_void_p * MAX_GROUPS), ("arrive", C.c_int32),
+                ("pslot", C.c_void_p * MAX_GROUPS), ("poff", C.c_void_p * MAX_GROUPS),
+                ("nblk", C.c_void_p * MAX_GROUPS), ("count", C.c_void_p * MAX_GROUPS),
+                ("partial", C.c_void_p * MAX_GROUPS)]
 
 
 class MlLoop(C.Structure):
@@ -112,6 +115,7 @@ _SIGNATURES = {
     "ml_staging_export": (C.c_int, [_P, C.c_int32, _P, _P]),
     "ml_staging_export_loc": (C.c_int, [_P, C.c_int32, _P]),
     "ml_staging_export_seg": (C.c_int, [_P, C.c_int32, _I64P, _P, _P]),
+    "ml_staging_export_arrival": (C.c_int, [_P, C.c_int32, _I64P, _I64P, _P, _P, _P]),
     "ml_staging_free": (C.c_int, [_P]),
     "ml_co_occurrence": (C.c_int, [C.c_int64, C.c_int32, _PP, _I64P, _I32P, _P, _P, _I64P]),
     "ml_cm_order": (C.c_int, [C.c_int64, _P, _P, _P]),

@@ -85,6 +85,14 @@ struct Staging {
     const int32_t *toff[MAX_GROUPS];     // [total+1] into src (global target index)
     const uint16_t *src[MAX_GROUPS];
     int32_t gpos[MAX_ARGS];              // position of the arg inside its group
+    // arrival mode: shared targets go through per-block partial slots; the last
+    // block to arrive (atomic counter) folds them in block order
+    const int32_t *pslot[MAX_GROUPS];    // [total] partial slot per list entry (-1: sole block)
+    const int32_t *poff[MAX_GROUPS];     // [targets] first slot of a shared target
+    const int32_t *nblk[MAX_GROUPS];     // [targets] blocks touching the target
+    int32_t *count[MAX_GROUPS];          // [targets] arrivals (back to 0 after each run)
+    void *partial[MAX_GROUPS];           // [slots][dim]
+    int32_t foff[MAX_GROUPS];            // byte offset of the finaliser list in dynamic smem
 };
 
 struct LaunchParams {
@@ -294,6 +302,85 @@ struct Slot {
             }
         }
     }
+
+    // ---- arrival mode (segmented slots, no block colours) ------------------------
+    // phase 1: per (target, component) fold this block's slots in element order;
+    // a target owned by this block alone is updated in HBM, a shared one writes
+    // its block sum into the target's partial slot for this block.
+    __device__ __forceinline__ void arrive_sums(const LaunchParams &p, int i, int32_t b, char *smem) {
+        if constexpr (seg) {
+            const int g = p.st.group[i];
+            if (!p.st.leader[i]) return;
+            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo;
+            const T *s = reinterpret_cast<const T *>(smem + p.st.soff[g]);
+            const int32_t *__restrict__ list = p.st.list[g] + lo;
+            const int32_t *__restrict__ toff = p.st.toff[g] + lo;
+            const int32_t *__restrict__ pslot = p.st.pslot[g] + lo;
+            const uint16_t *__restrict__ src = p.st.src[g];
+            T *part = static_cast<T *>(p.st.partial[g]);
+            const ArgRt &r = p.a[i];
+            T *d = static_cast<T *>(r.data);
+            const int total = u * A::dim, nt = blockDim.x;
+            const bool aos = r.sc == 1 && A::dim > 1;
+            for (int k = threadIdx.x; k < total; k += nt) {
+                const int c = aos ? k % A::dim : k / u, j = aos ? k / A::dim : k % u;
+                T acc = T(0);
+                for (int m = __ldg(toff + j), me = __ldg(toff + j + 1); m < me; ++m) {
+                    const int v = __ldg(src + m);
+                    acc += s[((v >> 8) * A::dim + c) * nt + (v & 255)];
+                }
+                const int32_t ps = __ldg(pslot + j);
+                if (ps < 0) {
+                    const int64_t a = int64_t(__ldg(list + j)) * r.se + c * r.sc;
+                    d[a] = __ldcg(d + a) + acc;
+                } else {
+                    __stcg(part + int64_t(ps) * A::dim + c, acc);
+                }
+            }
+        }
+    }
+    // phase 2 (after a fence + barrier): count this block's arrival at every
+    // shared target; the last arriver queues the target for finalisation and
+    // resets its counter for the next run.
+    __device__ __forceinline__ void arrive_count(const LaunchParams &p, int i, int32_t b, char *smem,
+                                                 int *nfin) {
+        if constexpr (seg) {
+            const int g = p.st.group[i];
+            if (!p.st.leader[i]) return;
+            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo;
+            int32_t *fin = reinterpret_cast<int32_t *>(smem + p.st.foff[g]);
+            for (int j = threadIdx.x; j < u; j += blockDim.x) {
+                if (__ldg(p.st.pslot[g] + lo + j) < 0) continue;
+                const int32_t t = __ldg(p.st.list[g] + lo + j);
+                const int32_t need = __ldg(p.st.nblk[g] + t);
+                if (atomicAdd(p.st.count[g] + t, 1) == need - 1) {
+                    p.st.count[g][t] = 0;
+                    fin[atomicAdd(nfin + g, 1)] = t;
+                }
+            }
+        }
+    }
+    // phase 3: fold the partial slots of finalised targets in block order
+    __device__ __forceinline__ void arrive_final(const LaunchParams &p, int i, char *smem, const int *nfin) {
+        if constexpr (seg) {
+            const int g = p.st.group[i];
+            if (!p.st.leader[i]) return;
+            const int nf = nfin[g];
+            const int32_t *fin = reinterpret_cast<const int32_t *>(smem + p.st.foff[g]);
+            const T *part = static_cast<const T *>(p.st.partial[g]);
+            const ArgRt &r = p.a[i];
+            T *d = static_cast<T *>(r.data);
+            for (int k = threadIdx.x; k < nf * A::dim; k += blockDim.x) {
+                const int c = k % A::dim;
+                const int32_t t = fin[k / A::dim];
+                const int32_t o = __ldg(p.st.poff[g] + t), nb = __ldg(p.st.nblk[g] + t);
+                T acc = T(0);
+                for (int q = 0; q < nb; ++q) acc += __ldcg(part + int64_t(o + q) * A::dim + c);
+                const int64_t a = int64_t(t) * r.se + c * r.sc;
+                d[a] = __ldcg(d + a) + acc;
+            }
+        }
+    }
 };
 
 template <class T, int M>
@@ -358,6 +445,22 @@ struct Engine {
     __device__ __forceinline__ static void write_back(Slots &s, const LaunchParams &p, int32_t b,
                                                       char *smem, cuda::std::index_sequence<Is...>) {
         (cuda::std::get<Is>(s).write_back(p, int(Is), b, smem), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void arrive_sums(Slots &s, const LaunchParams &p, int32_t b,
+                                                       char *smem, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).arrive_sums(p, int(Is), b, smem), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void arrive_count(Slots &s, const LaunchParams &p, int32_t b,
+                                                        char *smem, int *nfin,
+                                                        cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).arrive_count(p, int(Is), b, smem, nfin), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void arrive_final(Slots &s, const LaunchParams &p, char *smem,
+                                                        const int *nfin, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).arrive_final(p, int(Is), smem, nfin), ...);
     }
     template <size_t... Is>
     __device__ __forceinline__ static void apply_staged(Slots &s, cuda::std::index_sequence<Is...>) {
@@ -534,6 +637,40 @@ __device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
     }
 }
 
+// Arrival schedule: one launch over the plan blocks in natural order (best
+// locality), no block colours and no inter-block waiting.  Targets touched by
+// one block are updated directly; shared targets are completed by whichever
+// block arrives last, folding the per-block partials in block order, so the
+// result is deterministic run to run.  Partials of neighbouring blocks are
+// written and read within a short time window, so they live in L2.
+template <class F, class... As>
+__device__ __forceinline__ void run_arrive(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_SEG, As...>;
+    __shared__ double red[32];
+    __shared__ int nfin[MAX_GROUPS];
+    extern __shared__ __align__(16) char dsm[];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const int32_t b = blockIdx.x;
+    const int64_t e = int64_t(b) * p.bs + threadIdx.x;
+    const int64_t hi = int64_t(b) * p.bs + p.bs < p.n ? int64_t(b) * p.bs + p.bs : p.n;
+    const bool active = threadIdx.x < p.bs && e < hi;
+    if (threadIdx.x < MAX_GROUPS) nfin[threadIdx.x] = 0;
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    if (active) {
+        E::init_elem(s, p, e, dsm, idx);
+        E::call(s, p, e, idx);
+    }
+    __syncthreads();
+    E::arrive_sums(s, p, b, dsm, idx);
+    __threadfence();
+    __syncthreads();
+    E::arrive_count(s, p, b, dsm, nfin, idx);
+    __syncthreads();
+    E::arrive_final(s, p, dsm, nfin, idx);
+    if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
+}
+
 template <class F, class... As>
 __device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
     using E = Engine<F, ST_NONE, As...>;
@@ -575,6 +712,10 @@ template <class F, class T, int MODE>
 __global__ void __launch_bounds__(256) k_flow(const __grid_constant__ LaunchParams p) {
     run_flow<F, MODE>(p, typename F::template sig<T>{});
 }
+template <class F, class T>
+__global__ void __launch_bounds__(256) k_arrive(const __grid_constant__ LaunchParams p) {
+    run_arrive<F>(p, typename F::template sig<T>{});
+}
 
 // ---- compile-time signature introspection -------------------------------------
 template <class S>
@@ -602,6 +743,7 @@ struct FunctorEntry {
     bool ind_write, ind_write_non_inc;
     LaunchFn direct, staged, phased;
     LaunchFn smem[2], flow[2];                       // [0] colour phases, [1] segmented
+    LaunchFn arrive;                                 // segmented, no block colours
     int (*flow_occupancy[2])(int threads, size_t smem);
 };
 
@@ -636,6 +778,14 @@ struct Registrar {
         }
         k_flow<F, T, MODE><<<g, b, bytes, s>>>(p);
     }
+    static void arrive(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
+        static bool opted = false;
+        if (!opted && bytes > 48 * 1024) {
+            cudaFuncSetAttribute(k_arrive<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            opted = true;
+        }
+        k_arrive<F, T><<<g, b, bytes, s>>>(p);
+    }
     template <int MODE>
     static int flow_occupancy(int threads, size_t bytes) {
         if (bytes > 48 * 1024)
@@ -664,6 +814,7 @@ struct Registrar {
         e.flow[1] = st ? &flow<ST_SEG> : nullptr;
         e.flow_occupancy[0] = st ? &flow_occupancy<ST_SMEM> : nullptr;
         e.flow_occupancy[1] = st ? &flow_occupancy<ST_SEG> : nullptr;
+        e.arrive = st ? &arrive : nullptr;
         register_functor(e);
     }
 };

@@ -271,6 +271,11 @@ struct ml_staging {
     // contributing (arg position, element in block) slots in element order
     std::vector<std::vector<int32_t>> toff;        // per group [total+1]
     std::vector<std::vector<uint16_t>> src;        // per group
+    // arrival mode: per list entry, the partial slot of a target shared by
+    // several blocks (-1: the block owns the target alone); per target id,
+    // the first slot and the number of blocks touching it
+    std::vector<std::vector<int32_t>> pslot, poff, nblk;
+    std::vector<int64_t> nslots;
 };
 
 extern "C" int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols,
@@ -341,6 +346,36 @@ extern "C" int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols,
             }
         }
     }
+    // arrival lists: blocks touching each target, in block order
+    s->pslot.assign(ng, {});
+    s->poff.assign(ng, {});
+    s->nblk.assign(ng, {});
+    s->nslots.assign(ng, 0);
+    for (int32_t g = 0; g < ng; ++g) {
+        const auto &list = s->list[g];
+        int64_t ntgt = 0;
+        for (int32_t t : list) ntgt = std::max<int64_t>(ntgt, int64_t(t) + 1);
+        auto &nblk = s->nblk[g];
+        auto &poff = s->poff[g];
+        nblk.assign(size_t(ntgt), 0);
+        for (int32_t t : list) nblk[t]++;
+        poff.assign(size_t(ntgt), -1);
+        int64_t slots = 0;
+        for (int64_t t = 0; t < ntgt; ++t)
+            if (nblk[t] > 1) {
+                poff[t] = int32_t(slots);
+                slots += nblk[t];
+            }
+        if (slots >= (int64_t(1) << 31)) throw std::length_error("too many partial slots");
+        s->nslots[g] = slots;
+        std::vector<int32_t> seen(size_t(ntgt), 0);
+        auto &pslot = s->pslot[g];
+        pslot.resize(list.size());
+        for (size_t k = 0; k < list.size(); ++k) {     // list is block-major: block order
+            const int32_t t = list[k];
+            pslot[k] = nblk[t] > 1 ? poff[t] + seen[t]++ : -1;
+        }
+    }
     *out = s.release();
     return ML_OK;
     ML_GUARD_END
@@ -372,6 +407,17 @@ extern "C" int ml_staging_export_seg(const ml_staging_t *s, int32_t g, int64_t *
     if (nrefs) *nrefs = int64_t(s->src[g].size());
     if (toff) std::copy(s->toff[g].begin(), s->toff[g].end(), toff);
     if (src) std::copy(s->src[g].begin(), s->src[g].end(), src);
+    return ML_OK;
+}
+
+extern "C" int ml_staging_export_arrival(const ml_staging_t *s, int32_t g, int64_t *ntargets,
+                                         int64_t *nslots, int32_t *pslot, int32_t *poff, int32_t *nblk) {
+    if (!s || g < 0 || g >= s->ngroups) ML_FAIL(ML_EINVAL, "ml_staging_export_arrival: bad group");
+    if (ntargets) *ntargets = int64_t(s->nblk[g].size());
+    if (nslots) *nslots = s->nslots[g];
+    if (pslot) std::copy(s->pslot[g].begin(), s->pslot[g].end(), pslot);
+    if (poff) std::copy(s->poff[g].begin(), s->poff[g].end(), poff);
+    if (nblk) std::copy(s->nblk[g].begin(), s->nblk[g].end(), nblk);
     return ML_OK;
 }
 

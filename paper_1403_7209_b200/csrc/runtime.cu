@@ -184,6 +184,19 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
             const size_t slots = seg ? size_t(count[g]) * sthreads : size_t(sg.umax[g]);
             smem_bytes += (slots * f.dim[leader[g]] * 8 + 15) / 16 * 16;
         }
+        if (use_smem && seg && sg.arrive) {
+            for (int g = 0; g < sg.ngroups; ++g) {
+                if (!sg.pslot[g] || !sg.poff[g] || !sg.nblk[g] || !sg.count[g] || !sg.partial[g])
+                    ML_FAIL(ML_EINVAL, "loop '%s': arrival staging lists missing", L->name);
+                p.st.pslot[g] = sg.pslot[g];
+                p.st.poff[g] = sg.poff[g];
+                p.st.nblk[g] = sg.nblk[g];
+                p.st.count[g] = sg.count[g];
+                p.st.partial[g] = sg.partial[g];
+                p.st.foff[g] = int32_t(smem_bytes);
+                smem_bytes += (size_t(sg.umax[g]) * 4 + 15) / 16 * 16;
+            }
+        }
         if (!use_smem || smem_bytes > 200 * 1024) {
             use_smem = false;
             smem_bytes = 0;
@@ -204,10 +217,16 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         const LaunchFn fn = use_smem ? f.smem[seg] : (staged ? f.staged : f.phased);
         const int threads = staged ? round_up32(bs) : std::clamp(round_up32(bs), 32, 256);
         int occ = 0;
-        if (use_smem && f.flow[seg] && L->plan.queue && L->plan.dep_off && L->plan.dep_list &&
+        const bool arrive = use_smem && seg && sg.arrive && f.arrive;
+        if (!arrive && use_smem && f.flow[seg] && L->plan.queue && L->plan.dep_off && L->plan.dep_list &&
             L->plan.flow_state && L->plan.ncolors > 1)
             occ = f.flow_occupancy[seg](threads, smem_bytes);
-        if (occ > 0) {
+        if (arrive) {
+            // one launch, blocks in natural order, no colours (see run_arrive)
+            p.blocks = nullptr;
+            f.arrive(p, dim3(unsigned(nb)), dim3(unsigned(threads)), smem_bytes, stream);
+            occ = -1;
+        } else if (occ > 0) {
             // one persistent launch: dataflow over the colour-ordered block queue
             const int64_t grid = std::min<int64_t>(nb, int64_t(occ) * g_dev.sm_count);
             ML_CUDA(cudaMemsetAsync(L->plan.flow_state, 0, size_t(nb + 1) * sizeof(int32_t), stream));

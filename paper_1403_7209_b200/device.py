@@ -179,7 +179,8 @@ class StagingMirror:
     ``group[i]`` is the staging group of argument i (one group per INC dat),
     -1 for arguments that are not indirect INC."""
 
-    __slots__ = ("group", "ngroups", "off", "list", "umax", "loc", "toff", "src")
+    __slots__ = ("group", "ngroups", "off", "list", "umax", "loc", "toff", "src",
+                 "pslot", "poff", "nblk", "count", "partial")
 
     def __init__(self, loop, plan):
         import ctypes as C
@@ -204,6 +205,7 @@ class StagingMirror:
         try:
             self.off, self.list, self.umax, self.loc = [], [], [], {}
             self.toff, self.src = [], []
+            self.pslot, self.poff, self.nblk, self.count, self.partial = [], [], [], [], []
             for g in range(self.ngroups):
                 tot, um = C.c_int64(), C.c_int64()
                 N.check(L.ml_staging_sizes(handle, g, C.byref(tot), C.byref(um)))
@@ -220,6 +222,23 @@ class StagingMirror:
                 N.check(L.ml_staging_export_seg(handle, g, C.byref(nref), N.ptr(toff), N.ptr(src)))
                 self.toff.append(_upload(toff))
                 self.src.append(_upload(src))
+                # arrival mode: partial slots of targets shared by several blocks
+                ntg, nsl = C.c_int64(), C.c_int64()
+                N.check(L.ml_staging_export_arrival(handle, g, C.byref(ntg), C.byref(nsl), None, None,
+                                                    None))
+                pslot = np.empty(max(tot.value, 1), np.int32)
+                poff = np.empty(max(ntg.value, 1), np.int32)
+                nblk = np.empty(max(ntg.value, 1), np.int32)
+                N.check(L.ml_staging_export_arrival(handle, g, C.byref(ntg), C.byref(nsl), N.ptr(pslot),
+                                                    N.ptr(poff), N.ptr(nblk)))
+                dim = loop.args[self.group.index(g)].dat.dim
+                self.pslot.append(_upload(pslot))
+                self.poff.append(_upload(poff))
+                self.nblk.append(_upload(nblk))
+                cnt = N.DeviceBuffer(4 * max(ntg.value, 1))
+                N.check(L.ml_memset(cnt.ptr, 0, cnt.nbytes))
+                self.count.append(cnt)
+                self.partial.append(N.DeviceBuffer(8 * dim * max(nsl.value, 1)))
             for j, i in enumerate(inc):
                 loc = np.empty(max(plan.n, 1), np.uint16)
                 N.check(L.ml_staging_export_loc(handle, j, N.ptr(loc)))

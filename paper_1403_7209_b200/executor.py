@@ -73,6 +73,7 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
+    inc_schedule: str = "flow"              # "flow" | "arrival" | "colour": cross-block scheme
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
 
@@ -90,6 +91,10 @@ class BackendConfig:
             raise MeshError(f"unknown residency {self.residency!r}")
         if self.inc_staging not in ("segmented", "colour"):
             raise MeshError(f"unknown inc_staging {self.inc_staging!r}")
+        if self.inc_schedule not in ("flow", "arrival", "colour"):
+            raise MeshError(f"unknown inc_schedule {self.inc_schedule!r}")
+        if self.inc_schedule == "colour":
+            self.dataflow = False
 
     def block_size_for(self, loop_name: str) -> int:
         if self.block_size_table and loop_name in self.block_size_table:
@@ -267,9 +272,16 @@ class _LoopEntry:
             for i, buf in sg.loc.items():
                 L.staging.loc[i] = buf.ptr
             L.staging.seg = 1 if config.inc_staging == "segmented" else 0
+            L.staging.arrive = 1 if (config.inc_schedule == "arrival" and L.staging.seg
+                                     and not _inc_aliased(loop)) else 0
             for g in range(sg.ngroups):
                 L.staging.toff[g] = sg.toff[g].ptr
                 L.staging.src[g] = sg.src[g].ptr
+                L.staging.pslot[g] = sg.pslot[g].ptr
+                L.staging.poff[g] = sg.poff[g].ptr
+                L.staging.nblk[g] = sg.nblk[g].ptr
+                L.staging.count[g] = sg.count[g].ptr
+                L.staging.partial[g] = sg.partial[g].ptr
         nbytes = C.c_uint64()
         N.check(N.lib().ml_loop_scratch_bytes(C.byref(L), C.byref(nbytes)))
         self.scratch = N.DeviceBuffer(nbytes.value) if nbytes.value else None
@@ -402,7 +414,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
            tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
-           config.dataflow, config.inc_staging, config.flow_windows,
+           config.dataflow, config.inc_staging, config.inc_schedule, config.flow_windows,
            config.flow_window_l2_fraction,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)

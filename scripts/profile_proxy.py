@@ -1,6 +1,8 @@
-"""Set up the benchmark workload and run it eagerly a few times (for ncu captures).
+"""Set up the benchmark workload and run it eagerly a few times (for ncu captures
+and schedule comparisons).
 
     python scripts/profile_proxy.py [--grid 94] [--iters 3] [--block-size 256]
+                                    [--inc-schedule flow|arrival|colour] [--soa 4]
 """
 import argparse
 import sys
@@ -16,12 +18,19 @@ ap.add_argument("--grid", type=int, default=94)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--block-size", type=int, default=256)
 ap.add_argument("--soa", type=int, default=4)
+ap.add_argument("--inc-schedule", nargs="+", default=["flow"])
+ap.add_argument("--no-renumber", action="store_true")
 args = ap.parse_args()
 mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)
 apps.shuffle_mesh(mesh, seed=1)
 prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
-ml.renumber_mesh(mesh)
-cfg = ml.BackendConfig(device=0, block_size=args.block_size)
-for i in range(args.iters):
-    r = ml.run_program(prog, mesh, cfg)
-    print(" ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf))
+if not args.no_renumber:
+    ml.renumber_mesh(mesh)
+for sched in args.inc_schedule:
+    cfg = ml.BackendConfig(device=0, block_size=args.block_size, inc_schedule=sched)
+    for i in range(args.iters):
+        r = ml.run_program(prog, mesh, cfg)
+        tot = sum(p.time_sec for p in r.perf)
+        print(f"[{sched} bs={args.block_size} soa={args.soa}] total={tot*1e3:.3f}ms " +
+              " ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf),
+              flush=True)

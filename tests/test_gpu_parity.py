@@ -255,6 +255,35 @@ def test_dataflow_schedule_matches_colour_launches(bs):
         np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
 
 
+@pytest.mark.parametrize("bs", [16, 64, 256])
+def test_arrival_schedule_matches_and_is_deterministic(bs):
+    """Arrival schedule (no block colours): int64 bit-exact, float within tolerance of
+    the colour schedule, and bitwise reproducible run to run (counters self-reset)."""
+    outs = []
+    for kw in ({"inc_schedule": "colour"}, {"inc_schedule": "arrival"},
+               {"inc_schedule": "arrival"}):
+        mesh = apps.gen_hex_mesh(18, seed=3)
+        apps.shuffle_mesh(mesh, seed=4)
+        prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=3)
+        ml.renumber_mesh(mesh)
+        ml.run_program(prog, mesh, cfg(block_size=bs, **kw))
+        ml.run_program(prog[:5], mesh, cfg(block_size=bs, **kw))       # replay: counters reused
+        outs.append((h["res"].fetch(), h["grad"].fetch(), h["q"].fetch()))
+    for k in range(3):
+        close(outs[1][k], outs[0][k], what=f"field {k}")
+        np.testing.assert_array_equal(outs[1][k], outs[2][k])
+    for make in (lambda: apps.gen_hub_mesh(5000, 60000, n_hubs=8, hub_share=0.2, seed=3),
+                 lambda: _shuffled_hex(16), lambda: apps.gen_mesh(50)):
+        ref, mesh = make(), make()
+        rl = _cases.inc_loop(ref, "edge_nodes")
+        oserial.run_loop(rl)
+        l = _cases.inc_loop(mesh, "edge_nodes")
+        for _ in range(2):
+            mesh.dats["acc"].put(np.zeros((mesh.sets["nodes"].size, 1), np.int64))
+            ml.run_program([l], mesh, cfg(block_size=bs, inc_schedule="arrival"))
+            np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
+
+
 @pytest.mark.parametrize("bs", [32, 128, 256])
 def test_smem_and_register_staging_agree(bs):
     outs = []

@@ -1,7 +1,7 @@
 """Benchmark: one Hydra-shaped solver iteration per step on B200 (BASELINE.json configs[1]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload proxy|diffusion] [--grid 94]
+                    [--workload proxy|diffusion] [--grid 94] [--inc-schedule flow|arrival|colour]
 
 Workload (default): ``build_hydra_proxy`` on the Rotor37-sized 3-D grid
 (94^3 = 830,584 nodes, 2,465,244 edges), numbered randomly (an unstructured
@@ -15,7 +15,7 @@ plus achieved HBM GB/s vs the measured peak for the dominant loop (vflux).
 
 * ``value``      edges/s with all state resident in HBM: K back-to-back CUDA
                  graph replays of the iteration, CUDA events on the library
-                 stream, max over ranks.
+                 stream (N=1); max over ranks (N>1).
 * ``e2e``        the same metric through the public API with HOST buffers:
                  every step ``run_program(..., residency="host")`` uploads
                  every dat the iteration touches from pinned host memory and
@@ -27,122 +27,26 @@ plus achieved HBM GB/s vs the measured peak for the dominant loop (vflux).
                  semantics) on a bounded sample.
 
 ``--impl reference`` times that CPU path alone (rank 0; other ranks exit).
-Multi-GPU (torchrun, N>1): RCB owner-compute partition, one GPU per rank,
-NCCL halo exchange; ``value`` is total edges/s.
+Multi-GPU (torchrun, N>1): RCB owner-compute partition of the same mesh
+(strong scaling), one GPU per rank, halos over NCCL; value = total edges/s.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
-import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
-
-import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+from paper_1403_7209_b200.bench_support import build_workload, clock_sampler, peaks_gbs  # noqa: E402
+
 METRIC = "edges/sec and time per solver iteration; achieved HBM GB/s vs peak, 1/2/4/8 B200"
-FALLBACK_PEAK = 6650.0
-
-
-def peaks() -> tuple[float, str]:
-    p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
-        try:
-            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-        except Exception:
-            pass
-    return FALLBACK_PEAK, "fallback (B200_PROFILING.md)"
-
-
-class ClockSampler:
-    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines: list[str] = []
-
-    def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
-        return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-
-    def summary(self) -> dict:
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
-
-
-def cp_ms_estimate(cp) -> float:
-    """Seconds per replay of a compiled program (one timed replay)."""
-    t0 = time.perf_counter()
-    cp.replay(1)
-    return time.perf_counter() - t0
-
-
-def build_workload(args):
-    import paper_1403_7209_b200 as ml
-    from paper_1403_7209_b200 import apps
-    t0 = time.perf_counter()
-    if args.workload == "proxy":
-        mesh = apps.gen_hex_mesh(args.grid, seed=0)
-        apps.shuffle_mesh(mesh, seed=1)
-        prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
-        name = f"hydra-proxy iteration, 3-D grid {args.grid}^3"
-    else:
-        mesh = apps.gen_mesh(args.grid)
-        apps.shuffle_mesh(mesh, seed=1)
-        prog, h = apps.build_diffusion(mesh, steps=1, dtype="float64")
-        name = f"diffusion step, gen_mesh({args.grid})"
-    t_gen = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    ml.renumber_mesh(mesh)
-    t_ren = time.perf_counter() - t0
-    return mesh, prog, h, name, {"generate_s": round(t_gen, 3), "renumber_s": round(t_ren, 3)}
 
 
 def cpu_baseline(args) -> dict:
@@ -171,19 +75,18 @@ def cpu_baseline(args) -> dict:
 
 
 def run_reference(args) -> None:
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    for _ in range(args.warmup_ref):
+    for _ in range(args.warmup):
         cpu_baseline(args)
     vals, secs = [], []
-    for _ in range(args.steps_ref):
+    for _ in range(args.steps):
         cb = cpu_baseline(args)
         vals.append(cb["value"])
         secs.append(cb["sec_per_iteration"])
     cb["value"] = statistics.mean(vals)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "edges/s",
-            "n_gpus": args.gpus, "steps": args.steps_ref, "warmup": args.warmup_ref,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cb["sample"].split(";")[0], "parallelism": "cpu-serial"},
@@ -191,6 +94,12 @@ def run_reference(args) -> None:
             "e2e": {"value": cb["value"], "unit": "edges/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def _replay_seconds(cp) -> float:
+    t0 = time.perf_counter()
+    cp.replay(1)
+    return time.perf_counter() - t0
 
 
 def run_ours(args) -> None:
@@ -206,46 +115,42 @@ def run_ours(args) -> None:
 
     mesh, prog, h, wname, setup = build_workload(args)
     edges = mesh.sets["edges"].size
-    cfg = ml.BackendConfig(device=0, use_graph=True)
+    cfg = ml.BackendConfig(device=0, use_graph=True, inc_schedule=args.inc_schedule)
     t0 = time.perf_counter()
     cp = compile_program(prog, mesh, cfg)
     setup["plans_and_upload_s"] = round(time.perf_counter() - t0, 3)
     info = N.device_info()
 
-    # -- device-resident throughput: K graph replays, CUDA events ------------------
+    # -- device-resident throughput: K graph replays, CUDA events ----------------------
     cp.replay(args.warmup)
-    import ctypes as C
     timer = C.c_void_p()
     N.check(N.lib().ml_timer_create(C.byref(timer)))
     ms = C.c_float()
-    with ClockSampler(0) as clk:
-        # nvidia-smi needs ~0.2 s to start; keep the GPU busy (untimed) until it samples,
-        # so the clock record covers the load the timed region runs under
+    with clock_sampler(0) as clk:
+        # nvidia-smi needs ~0.2 s to start: keep the GPU busy (untimed) until it samples
         time.sleep(0.3)
-        cp.replay(max(20, int(0.3 / max(cp_ms_estimate(cp), 1e-4))))
+        cp.replay(max(20, int(0.3 / max(_replay_seconds(cp), 1e-4))))
         N.check(N.lib().ml_synchronize())
         N.check(N.lib().ml_timer_start(timer))
         cp.replay(args.steps)
         N.check(N.lib().ml_timer_stop(timer, C.byref(ms)))
     total_ms = ms.value
-    ms_per_step = total_ms / args.steps
     value = edges * args.steps / (total_ms * 1e-3)
 
-    # -- per-loop breakdown (eager, CUDA events between loops on the same stream) -----
+    # -- per-loop breakdown (eager, CUDA events between loops on the same stream) ----------
     per_loop = {e.loop.name: [] for e in cp.entries}
     for _ in range(max(3, args.steps // 2)):
-        times = cp.run(False, True)
-        for e, t in zip(cp.entries, times):
+        for e, t in zip(cp.entries, cp.run(False, True)):
             per_loop[e.loop.name].append(t)
     loops = {}
     for e in cp.entries:
         t = statistics.mean(per_loop[e.loop.name])
         loops[e.loop.name] = {"ms": round(t * 1e3, 4), "b_alg": e.alg, "useful_bytes": e.useful,
                               "gbs_alg": round(e.alg / t / 1e9, 1), "nb": e.st.nb, "nc": e.st.nc}
-    eager_ms = sum(v["ms"] for v in loops.values())
-    top = max(loops, key=lambda k: loops[k]["ms"])
-    peak, peak_src = peaks()
-    dom = cp.entries[[e.loop.name for e in cp.entries].index("vflux" if "vflux" in loops else top)]
+    peak, peak_src = peaks_gbs()
+    names = [e.loop.name for e in cp.entries]
+    dom = cp.entries[names.index("vflux") if "vflux" in names
+                     else max(range(len(names)), key=lambda i: loops[names[i]]["ms"])]
     t_dom = statistics.mean(per_loop[dom.loop.name])
     achieved = dom.alg / t_dom / 1e9
     traffic = None
@@ -253,9 +158,10 @@ def run_ours(args) -> None:
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(dom.loop.name)
 
-    # -- end to end through the public API with host buffers ---------------------------
+    # -- end to end through the public API with host buffers ---------------------------------
     pin_mesh(mesh)
-    ecfg = ml.BackendConfig(device=0, use_graph=True, residency="host")
+    ecfg = ml.BackendConfig(device=0, use_graph=True, residency="host",
+                            inc_schedule=args.inc_schedule)
     h2d = sum(d.nbytes for d in cp.all_dats)
     d2h = sum(d.nbytes for d in cp.written) + sum(g.buffer.nbytes for g in cp.globs)
     for _ in range(max(1, args.warmup // 2)):
@@ -271,11 +177,12 @@ def run_ours(args) -> None:
     cb = cpu_baseline(args) if not args.no_cpu else None
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (jittered 3-D grid, random numbering then CM renumbering)",
         "config": {"workload": wname, "nodes": mesh.sets["nodes"].size, "edges": edges,
                    "loops_per_step": len(prog), "block_size": cfg.block_size,
+                   "inc_schedule": args.inc_schedule,
                    "l2": "inputs > 126 MB L2 (no flush needed)",
                    "timing": "CUDA graph replays back to back, CUDA events on the library stream",
                    "parallelism": "single GPU", "device": info["name"], "setup": setup},
@@ -287,7 +194,7 @@ def run_ours(args) -> None:
                      "algorithmic_bytes_per_launch": dom.alg,
                      "mean_loop_ms": round(t_dom * 1e3, 4)},
         "loops": loops,
-        "eager_ms_per_step": round(eager_ms, 4),
+        "eager_ms_per_step": round(sum(v["ms"] for v in loops.values()), 4),
         "e2e": e2e,
         "cpu_baseline": cb,
     }
@@ -303,6 +210,7 @@ def main():
     ap.add_argument("--workload", choices=["proxy", "diffusion"], default="proxy")
     ap.add_argument("--grid", type=int, default=None)
     ap.add_argument("--cpu-grid", type=int, default=None)
+    ap.add_argument("--inc-schedule", choices=["flow", "arrival", "colour"], default="flow")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.grid is None:
@@ -312,7 +220,6 @@ def main():
             args.cpu_grid = 22 if args.workload == "proxy" else 96
         else:
             args.cpu_grid = 30 if args.workload == "proxy" else 160
-    args.steps_ref, args.warmup_ref = args.steps, args.warmup
     if args.impl == "reference":
         run_reference(args)
     else:

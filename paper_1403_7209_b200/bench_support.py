@@ -1,0 +1,116 @@
+"""Measurement helpers shared by bench.py and the multi-GPU bench path.
+
+* ``build_workload`` — the benchmark program: the Hydra-shaped proxy
+  iteration on a jittered 3-D grid (default 94^3 = 2,465,244 edges, the
+  Rotor37 size), numbered randomly then Cuthill–McKee renumbered; or one
+  diffusion step on ``gen_mesh``.
+* ``clock_sampler`` — ``nvidia-smi`` SM clocks and throttle reasons sampled
+  during a timed region.
+* ``peaks_gbs`` — the HBM roofline denominator (MEASURED_PEAKS.json, else
+  the profiling guide's fallback).
+"""
+from __future__ import annotations
+
+import json
+import statistics
+import subprocess
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+FALLBACK_PEAK_GBS = 6650.0
+
+__all__ = ["build_workload", "clock_sampler", "peaks_gbs", "ClockSampler"]
+
+
+def peaks_gbs() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except (ValueError, KeyError):
+            pass
+    return FALLBACK_PEAK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons (context manager)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def clock_sampler(index: int) -> ClockSampler:
+    return ClockSampler(index)
+
+
+def build_workload(args):
+    """(mesh, program, handles, name, setup timings) for ``args.workload`` / ``args.grid``."""
+    from . import apps
+    from .renumber import renumber_mesh
+    t0 = time.perf_counter()
+    if args.workload == "proxy":
+        mesh = apps.gen_hex_mesh(args.grid, seed=0)
+        apps.shuffle_mesh(mesh, seed=1)
+        prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
+        name = f"hydra-proxy iteration, 3-D grid {args.grid}^3"
+    else:
+        mesh = apps.gen_mesh(args.grid)
+        apps.shuffle_mesh(mesh, seed=1)
+        prog, h = apps.build_diffusion(mesh, steps=1, dtype="float64")
+        name = f"diffusion step, gen_mesh({args.grid})"
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    renumber_mesh(mesh)
+    t_ren = time.perf_counter() - t0
+    return mesh, prog, h, name, {"generate_s": round(t_gen, 3), "renumber_s": round(t_ren, 3)}

@@ -266,6 +266,73 @@ class GlooTransport:
     def barrier(self):
         self.dist.barrier(group=self.group)
 
+    # device-buffer interface (DeviceRank): device staging + pinned host mirror
+    def buffer(self, key, n: int, dtype):
+        from . import _native as N
+        cache = self.__dict__.setdefault("_bufs", {})
+        if key not in cache or cache[key][0].nbytes < max(8 * n, 8):
+            cache[key] = (N.DeviceBuffer(max(8 * n, 8)), N.PinnedArray((max(n, 1),), dtype), n)
+        return cache[key]
+
+    @staticmethod
+    def ptr(buf) -> int:
+        return buf[0].ptr
+
+    def sendrecv(self, sends: dict, recvs: dict, dtype) -> None:
+        from . import _native as N
+        L = N.lib()
+        for dev, host, n in sends.values():
+            N.check(L.ml_download(N.ptr(host.array), dev.ptr, 8 * n), "ml_download")
+        got = self.exchange({d: b[1].array[:b[2]] for d, b in sends.items()},
+                            {s: (b[2],) for s, b in recvs.items()}, dtype)
+        for src, (dev, host, n) in recvs.items():
+            host.array[:n] = got[src]
+            N.check(L.ml_upload(dev.ptr, N.ptr(host.array), 8 * n), "ml_upload")
+
+
+class NcclTransport(GlooTransport):
+    """Device-to-device halo exchange with torch.distributed's NCCL backend.
+
+    Send/receive buffers are CUDA tensors; ``ml_pack_rows`` writes into them
+    on the library stream, which is synchronised before the grouped NCCL
+    send/recv (batch_isend_irecv) and the receive side is synchronised before
+    ``ml_unpack_rows`` scatters the rows into the import slots."""
+
+    name = "nccl"
+
+    def buffer(self, key, n: int, dtype):
+        cache = self.__dict__.setdefault("_bufs", {})
+        torch = self.torch
+        if key not in cache or cache[key].numel() < max(n, 1):
+            tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.int64
+            cache[key] = torch.empty(max(n, 1), dtype=tdt, device="cuda")
+        return cache[key][:max(n, 1)] if n else cache[key][:0]
+
+    @staticmethod
+    def ptr(buf) -> int:
+        return buf.data_ptr()
+
+    def sendrecv(self, sends: dict, recvs: dict, dtype=None) -> None:
+        from . import _native as N
+        N.check(N.lib().ml_synchronize(), "ml_synchronize")
+        dist = self.dist
+        ops = [dist.P2POp(dist.isend, t, dst, group=self.group) for dst, t in sorted(sends.items())]
+        ops += [dist.P2POp(dist.irecv, t, src, group=self.group) for src, t in sorted(recvs.items())]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        self.torch.cuda.current_stream().synchronize()
+
+    def exchange(self, sends: dict, recv_shapes: dict, dtype) -> dict:
+        raise ExecError("NcclTransport moves device buffers only")
+
+    def allgather(self, arr: np.ndarray) -> list:
+        torch = self.torch
+        t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+        out = [torch.empty_like(t) for _ in range(self.dist.get_world_size(self.group))]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
 
 # -- device execution ------------------------------------------------------------------------
 
@@ -283,20 +350,56 @@ class DeviceRank:
         t = self.progs[i].run(use_graph, not use_graph)
         return t[0] if t else 0.0
 
-    def pack(self, dat_name: str, ids: np.ndarray) -> np.ndarray:
+    # halo exchange on the device: pack export rows (ml_pack_rows), move them,
+    # scatter into import slots (ml_unpack_rows); reference executor.py:484-497
+    def _index(self, key, ids: np.ndarray):
+        from . import _native as N
+        cache = self.__dict__.setdefault("_idx", {})
+        if key not in cache:
+            buf = N.DeviceBuffer(max(ids.nbytes, 4))
+            if ids.size:
+                buf.upload(np.ascontiguousarray(ids, dtype=np.int32))
+            cache[key] = buf
+        return cache[key]
+
+    def exchange_halo(self, name: str, transport) -> int:
         from . import _native as N
         from .device import dat_mirror
-        d = self.rp.dats[dat_name]
+        d = self.rp.dats[name]
         m = dat_mirror(d)
-        if m.device_newer:
-            d._pull()
-        return d.fetch()[ids]
+        se, sc = (d.dim, 1) if d.layout is AOS else (1, d.set.size)
+        exports, imports = self.rp.halo_rows(name)
+        L = N.lib()
+        sends = {}
+        for dst, ids in exports.items():
+            buf = transport.buffer(("s", name, dst), ids.size * d.dim, d.dtype)
+            N.check(L.ml_pack_rows(transport.ptr(buf), m.ptr, self._index(("e", name, dst), ids).ptr,
+                                   ids.size, d.dim, se, sc), "ml_pack_rows")
+            sends[dst] = buf
+        recvs = {src: transport.buffer(("r", name, src), ids.size * d.dim, d.dtype)
+                 for src, ids in imports.items()}
+        transport.sendrecv(sends, recvs, d.dtype)
+        for src, ids in imports.items():
+            N.check(L.ml_unpack_rows(m.ptr, transport.ptr(recvs[src]),
+                                     self._index(("i", name, src), ids).ptr, ids.size, d.dim, se, sc),
+                    "ml_unpack_rows")
+        m.device_newer = True
+        return len(sends)
 
-    def unpack(self, dat_name: str, ids: np.ndarray, rows: np.ndarray) -> None:
-        d = self.rp.dats[dat_name]
-        vals = d.fetch()
-        vals[ids] = rows
-        d.put(vals)
+
+class _HostRows:
+    """Numpy-side exchange for executors that expose pack/unpack (test oracle)."""
+
+    @staticmethod
+    def exchange_halo(dev, rp, name: str, transport) -> int:
+        exports, imports = rp.halo_rows(name)
+        d = rp.dats[name]
+        sends = {dst: dev.pack(name, ids) for dst, ids in exports.items()}
+        shapes = {src: (ids.size, d.dim) for src, ids in imports.items()}
+        got = transport.exchange(sends, shapes, d.dtype)
+        for src, ids in imports.items():
+            dev.unpack(name, ids, got[src])
+        return len(sends)
 
 
 def _run_rank(rp: RankProgram, dev, transport, timeout_ms: float):
@@ -311,14 +414,10 @@ def _run_rank(rp: RankProgram, dev, transport, timeout_ms: float):
         t0 = time.perf_counter()
         for name in reads:
             if dirty.get(name):
-                exports, imports = rp.halo_rows(name)
-                d = rp.dats[name]
-                sends = {dst: dev.pack(name, ids) for dst, ids in exports.items()}
-                shapes = {src: (ids.size, d.dim) for src, ids in imports.items()}
-                got = transport.exchange(sends, shapes, d.dtype)
-                for src, ids in imports.items():
-                    dev.unpack(name, ids, got[src])
-                messages += len(sends)
+                if hasattr(dev, "exchange_halo"):
+                    messages += dev.exchange_halo(name, transport)
+                else:
+                    messages += _HostRows.exchange_halo(dev, rp, name, transport)
                 dirty[name] = False
         t1 = time.perf_counter()
         dev.run_loop(i)
@@ -332,25 +431,44 @@ def _run_rank(rp: RankProgram, dev, transport, timeout_ms: float):
     return messages, comm, comp
 
 
-def run_program_distributed(program, mesh, config, transport=None, executor_factory=None):
-    """Owner-compute execution of a program on ``WORLD_SIZE`` processes (one GPU each)."""
+def init_distributed(config=None):
+    """Initialise torch.distributed for one process per GPU (NCCL when GPUs are
+    visible to torch, gloo otherwise); returns (rank, world, transport)."""
+    import torch
     import torch.distributed as dist
-    from .executor import RunResult
-    from .perf import PerfCollector, useful_bytes
     if not dist.is_initialized():
-        dist.init_process_group(backend="gloo")
-    world, rank = dist.get_world_size(), dist.get_rank()
+        use_nccl = torch.cuda.is_available() and os.environ.get("ML_TRANSPORT", "") != "gloo"
+        if use_nccl:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group(backend="nccl" if use_nccl else "gloo")
+    transport = NcclTransport() if dist.get_backend() == "nccl" else GlooTransport()
+    return dist.get_rank(), dist.get_world_size(), transport
+
+
+def setup_distributed(program, mesh, config, transport=None, executor_factory=None):
+    """Layout + this rank's local program + executor (one-time setup)."""
+    import torch.distributed as dist
+    rank, world, default_transport = init_distributed(config)
     if config.nranks not in (1, world):
         raise MeshError(f"nranks={config.nranks} but WORLD_SIZE={world}")
     if config.nranks != world:
         from dataclasses import replace
         config = replace(config, nranks=world)
     mesh.freeze()
-    t_start = time.perf_counter()
     layout = build_layout(mesh, program, config)
     rp = RankProgram(mesh, program, layout, rank)
-    transport = transport or GlooTransport()
+    transport = transport or default_transport
     dev = executor_factory(rp, config) if executor_factory else DeviceRank(rp, config)
+    return rp, dev, transport, layout, config
+
+
+def run_program_distributed(program, mesh, config, transport=None, executor_factory=None):
+    """Owner-compute execution of a program on ``WORLD_SIZE`` processes (one GPU each)."""
+    from .executor import RunResult
+    from .perf import PerfCollector, useful_bytes
+    t_start = time.perf_counter()
+    rp, dev, transport, layout, config = setup_distributed(program, mesh, config, transport,
+                                                           executor_factory)
     messages, comm, comp = _run_rank(rp, dev, transport, config.timeout_ms)
     # final: every rank gets the owned rows of every dat, and the global values
     owned = {name: rp.owned_rows(name) for name in rp.dats}
@@ -373,4 +491,61 @@ def run_program_distributed(program, mesh, config, transport=None, executor_fact
 
 
 def bench_distributed(args, metric):
-    raise ExecError("multi-GPU bench is not implemented yet")
+    """bench.py at N GPUs (torchrun, one process per GPU): same workload as N=1
+    (strong scaling), RCB partition, halos over NCCL; time = max over ranks."""
+    import json
+    import statistics
+    import torch
+    import torch.distributed as dist
+    import paper_1403_7209_b200 as ml
+    from . import _native as N
+    from .bench_support import build_workload, clock_sampler, peaks_gbs
+    rank, world, transport = init_distributed()
+    mesh, prog, h, wname, setup = build_workload(args)
+    edges = mesh.sets["edges"].size
+    cfg = ml.BackendConfig(device=int(os.environ.get("LOCAL_RANK", "0")), nranks=world,
+                           partitioner="rcb", coord_dat="coords")
+    t0 = time.perf_counter()
+    rp, dev, transport, layout, cfg = setup_distributed(prog, mesh, cfg, transport)
+    setup["layout_and_local_mesh_s"] = round(time.perf_counter() - t0, 3)
+    for _ in range(args.warmup):
+        _run_rank(rp, dev, transport, cfg.timeout_ms)
+    local_dev = int(os.environ.get("LOCAL_RANK", "0"))
+    with clock_sampler(local_dev) as clk:
+        dist.barrier()
+        N.check(N.lib().ml_synchronize())
+        t_begin = time.perf_counter()
+        msgs = 0
+        comm_t = 0.0
+        for _ in range(args.steps):
+            m, comm, comp = _run_rank(rp, dev, transport, cfg.timeout_ms)
+            msgs += m
+            comm_t += float(comm.sum())
+        N.check(N.lib().ml_synchronize())
+        elapsed = time.perf_counter() - t_begin
+        dist.barrier()
+    tmax = torch.tensor([elapsed], dtype=torch.float64,
+                        device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    tmax = float(tmax.item())
+    halo = [len(layout.sets["nodes"][r].nonexec_halo) + len(layout.sets["nodes"][r].exec_halo)
+            for r in range(world)]
+    if rank == 0:
+        peak, src = peaks_gbs()
+        launches = sum(p.launches_per_run() for p in dev.progs) * args.steps
+        line = {"metric": metric, "value": edges * args.steps / tmax, "unit": "edges/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * tmax / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (jittered 3-D grid, random numbering then CM renumbering)",
+                "config": {"workload": wname, "edges": edges, "nodes": mesh.sets["nodes"].size,
+                           "parallelism": f"owner-compute dp{world} (RCB)",
+                           "transport": transport.name, "halo_nodes_per_rank": halo,
+                           "timing": "wall clock around K iterations between barriers + device "
+                                     "syncs, max over ranks", "setup": setup},
+                "gpu_launches": launches, "clocks": clk.summary(),
+                "halo_messages_per_step": msgs / args.steps,
+                "comm_ms_per_step_rank0": 1e3 * comm_t / args.steps,
+                "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    dist.barrier()

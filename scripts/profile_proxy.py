@@ -1,8 +1,8 @@
-"""Set up the benchmark workload and run it eagerly a few times (for ncu captures
-and schedule comparisons).
+"""Set up the benchmark workload and run it eagerly (ncu captures, schedule /
+layout / block-size sweeps).
 
-    python scripts/profile_proxy.py [--grid 94] [--iters 3] [--block-size 256]
-                                    [--inc-schedule flow|arrival|colour] [--soa 4]
+    python scripts/profile_proxy.py [--grid 94] [--iters 3] [--block-size 256 128]
+                                    [--inc-schedule flow arrival colour] [--soa 4]
 """
 import argparse
 import sys
@@ -16,8 +16,8 @@ from paper_1403_7209_b200 import apps              # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--grid", type=int, default=94)
 ap.add_argument("--iters", type=int, default=3)
-ap.add_argument("--block-size", type=int, default=256)
-ap.add_argument("--soa", type=int, default=4)
+ap.add_argument("--block-size", type=int, nargs="+", default=[256])
+ap.add_argument("--soa", type=int, default=4, help="auto-SOA threshold; -1 = all AOS")
 ap.add_argument("--inc-schedule", nargs="+", default=["flow"])
 ap.add_argument("--no-renumber", action="store_true")
 args = ap.parse_args()
@@ -26,11 +26,14 @@ apps.shuffle_mesh(mesh, seed=1)
 prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
 if not args.no_renumber:
     ml.renumber_mesh(mesh)
-for sched in args.inc_schedule:
-    cfg = ml.BackendConfig(device=0, block_size=args.block_size, inc_schedule=sched)
-    for i in range(args.iters):
-        r = ml.run_program(prog, mesh, cfg)
-        tot = sum(p.time_sec for p in r.perf)
-        print(f"[{sched} bs={args.block_size} soa={args.soa}] total={tot*1e3:.3f}ms " +
-              " ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf),
-              flush=True)
+for bs in args.block_size:
+    for sched in args.inc_schedule:
+        cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched)
+        for i in range(args.iters):
+            r = ml.run_program(prog, mesh, cfg)
+            if i + 1 < args.iters:
+                continue
+            tot = sum(p.time_sec for p in r.perf)
+            print(f"[{sched} bs={bs} soa={args.soa}] total={tot*1e3:.3f}ms " +
+                  " ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf),
+                  flush=True)

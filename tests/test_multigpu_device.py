@@ -1,0 +1,104 @@
+"""Multi-rank owner-compute execution ON THE GPU: 2 and 3 processes sharing one
+B200 (the gpurun box has one GPU; NCCL refuses two ranks on one device, so the
+halo rows travel host-staged over gloo — everything else is the production
+path: local meshes, ml_pack_rows/ml_unpack_rows, coloured kernels with
+iteration prefixes and reduction limits).  Results must equal the reference
+serial golden vectors bit for bit (int64) and the oracle within 1e-12 (f64)."""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK="0", ML_TRANSPORT="gloo")
+    sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import _cases
+        import paper_1403_7209_b200 as ml
+        from paper_1403_7209_b200 import apps
+        app, n, dtype, steps, part, sched = case
+        if app == "proxy":
+            mesh = apps.gen_hex_mesh(n, seed=5)
+            prog, h = apps.build_hydra_proxy(mesh, steps=steps, seed=5)
+            ml.renumber_mesh(mesh)
+        else:
+            mesh, prog, h = _cases.build_app(app, n, dtype, steps)
+        cfg = ml.BackendConfig(nranks=world, partitioner=part, device=0, inc_schedule=sched)
+        result = ml.run_program(prog, mesh, cfg)
+        if app == "proxy":
+            out = {"q": h["q"].fetch(), "rms": np.array([g.value for g in h["rms"]]),
+                   "dt": np.array([g.value for g in h["dt_min"]])}
+        else:
+            out = _cases.app_results(app, h)
+        q.put((rank, out, result.messages))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc(), -1))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(case, world=2):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, out, msgs in outs:
+        if msgs < 0:
+            raise AssertionError(f"rank {rank} failed:\n{out}")
+    return sorted(outs, key=lambda x: x[0])
+
+
+@pytest.mark.parametrize("world,part,sched", [(2, "rcb", "flow"), (3, "trivial", "arrival"),
+                                              (2, "trivial", "colour")])
+def test_ranks_on_device_match_reference_int64(world, part, sched):
+    from conftest import golden
+    g = golden("exec.npz")
+    outs = _run(("diffusion", 8, "int64", 3, part, sched), world)
+    for rank, out, msgs in outs:
+        assert msgs > 0
+        for k, v in out.items():
+            np.testing.assert_array_equal(v, g[f"exec/diffusion_n8_int64_s3/{k}"], f"rank {rank} {k}")
+
+
+def test_proxy_two_ranks_on_device_vs_oracle():
+    import paper_1403_7209_b200 as ml
+    from oracle import bulk
+    from paper_1403_7209_b200 import apps
+    from paper_1403_7209_b200.kernels import resolve_kernel
+    mesh = apps.gen_hex_mesh(12, seed=5)
+    prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=5)
+    ml.renumber_mesh(mesh)
+    bulk.run_program(prog, resolve_kernel)
+    outs = _run(("proxy", 12, "float64", 2, "rcb", "flow"), 2)
+    ref_q = h["q"].fetch()
+    for rank, out, _ in outs:
+        np.testing.assert_allclose(out["q"], ref_q, rtol=1e-12, atol=1e-12 * np.abs(ref_q).max())
+        np.testing.assert_allclose(out["rms"], [r.value for r in h["rms"]], rtol=1e-12)
+        np.testing.assert_array_equal(out["dt"], [r.value for r in h["dt_min"]])

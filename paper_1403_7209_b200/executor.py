@@ -73,7 +73,7 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
-    inc_schedule: str = "flow"              # "flow" | "arrival" | "colour": cross-block scheme
+    inc_schedule: str = "colour"            # "colour" | "flow" | "arrival": cross-block scheme
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
 

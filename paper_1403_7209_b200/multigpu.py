@@ -503,14 +503,14 @@ def bench_distributed(args, metric):
     rank, world, transport = init_distributed()
     mesh, prog, h, wname, setup = build_workload(args)
     edges = mesh.sets["edges"].size
-    cfg = ml.BackendConfig(device=int(os.environ.get("LOCAL_RANK", "0")), nranks=world,
-                           partitioner="rcb", coord_dat="coords")
+    local_dev = int(os.environ.get("ML_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    cfg = ml.BackendConfig(device=local_dev, nranks=world, partitioner="rcb", coord_dat="coords",
+                           inc_schedule=getattr(args, "inc_schedule", "colour"))
     t0 = time.perf_counter()
     rp, dev, transport, layout, cfg = setup_distributed(prog, mesh, cfg, transport)
     setup["layout_and_local_mesh_s"] = round(time.perf_counter() - t0, 3)
     for _ in range(args.warmup):
         _run_rank(rp, dev, transport, cfg.timeout_ms)
-    local_dev = int(os.environ.get("LOCAL_RANK", "0"))
     with clock_sampler(local_dev) as clk:
         dist.barrier()
         N.check(N.lib().ml_synchronize())

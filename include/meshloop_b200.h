@@ -120,6 +120,11 @@ typedef struct ml_loop {
     int64_t rlim;                   /* elements >= rlim skip global reductions
                                        (exec-halo elements on multi-GPU runs);
                                        < 0 means n                               */
+    /* target-centric schedule (ml_gather_build); ntargets == 0 disables it */
+    int64_t gather_ntargets;
+    const int32_t *gather_off;      /* device [ntargets+1]                       */
+    const int32_t *gather_elem;     /* device [n * inc args]                     */
+    const uint8_t *gather_pos;      /* device [n * inc args]                     */
 } ml_loop_t;
 
 typedef struct ml_device_info {
@@ -180,6 +185,17 @@ int ml_schedule_build(int64_t n, int32_t ncols, const int64_t *const *cols, cons
 int ml_schedule_export(const ml_schedule_t *s, int64_t *ndeps, int32_t *queue, int32_t *dep_off,
                        int32_t *dep_list);
 int ml_schedule_free(ml_schedule_t *s);
+
+/* Target-centric ("gather") schedule of an INC loop whose indirect writes all
+ * increment one dat: per target, its (element, INC-argument position)
+ * incidences in serial order (element, then argument).  `cols` are the INC
+ * arguments' target columns in argument order.  Export sizes: off
+ * [ntargets+1], elem/pos [n*ncols]. */
+typedef struct ml_gather ml_gather_t;
+int ml_gather_build(int64_t n, int32_t ncols, const int64_t *const *cols, int64_t ntargets,
+                    ml_gather_t **out);
+int ml_gather_export(const ml_gather_t *g, int32_t *off, int32_t *elem, uint8_t *pos);
+int ml_gather_free(ml_gather_t *g);
 
 /* Staging lists for shared-memory increment accumulation (derived from the
  * plan's blocking; the plan itself is unchanged).  `col_group[j]` assigns the

@@ -30,6 +30,7 @@ EXPORTED = [
     "ml_memset", "ml_map_upload",
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
     "ml_schedule_build", "ml_schedule_export", "ml_schedule_free",
+    "ml_gather_build", "ml_gather_export", "ml_gather_free",
     "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
     "ml_staging_export_seg", "ml_staging_export_arrival", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
@@ -75,7 +76,9 @@ class MlLoop(C.Structure):
     _fields_ = [("name", C.c_char_p), ("functor", C.c_int32), ("nargs", C.c_int32),
                 ("args", C.POINTER(MlArg)), ("n", C.c_int64), ("plan", MlPlanDev),
                 ("fconst", C.c_double * 4), ("iconst", C.c_int64 * 4), ("scratch", C.c_void_p),
-                ("staging", MlStagingDev), ("rlim", C.c_int64)]
+                ("staging", MlStagingDev), ("rlim", C.c_int64),
+                ("gather_ntargets", C.c_int64), ("gather_off", C.c_void_p),
+                ("gather_elem", C.c_void_p), ("gather_pos", C.c_void_p)]
 
 
 class MlDeviceInfo(C.Structure):
@@ -110,6 +113,9 @@ _SIGNATURES = {
                                     _PP]),
     "ml_schedule_export": (C.c_int, [_P, _I64P, _P, _P, _P]),
     "ml_schedule_free": (C.c_int, [_P]),
+    "ml_gather_build": (C.c_int, [C.c_int64, C.c_int32, _PP, C.c_int64, _PP]),
+    "ml_gather_export": (C.c_int, [_P, _P, _P, _P]),
+    "ml_gather_free": (C.c_int, [_P]),
     "ml_staging_build": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, _PP, _I32P, _PP]),
     "ml_staging_sizes": (C.c_int, [_P, C.c_int32, _I64P, _I64P]),
     "ml_staging_export": (C.c_int, [_P, C.c_int32, _P, _P]),

@@ -110,6 +110,12 @@ struct LaunchParams {
     const uint16_t *ecol;       // element colours
     const int32_t *encol;       // per-block element colour count
     Consts k;
+    // target-centric schedule: per target, its (element, INC-arg position)
+    // incidences in serial order
+    int64_t g_ntargets;
+    const int32_t *g_off;
+    const int32_t *g_elem;
+    const uint8_t *g_pos;
 };
 
 // strided view of one element's components
@@ -401,6 +407,26 @@ __device__ __forceinline__ T block_reduce(T v, T *smem_t) {
     return v;   // valid in thread 0
 }
 
+template <class... As>
+struct IncIndex {
+    // position of argument I among the INC-indirect arguments (-1 if not one)
+    template <size_t I>
+    __host__ __device__ static constexpr int of() {
+        constexpr bool inc[] = {(As::kind == KI && As::mode == MINC)...};
+        if (!inc[I]) return -1;
+        int p = 0;
+        for (size_t j = 0; j < I; ++j) p += inc[j] ? 1 : 0;
+        return p;
+    }
+    template <size_t I>
+    __host__ __device__ static constexpr int first() {
+        constexpr bool inc[] = {(As::kind == KI && As::mode == MINC)...};
+        for (size_t j = 0; j < sizeof...(As); ++j)
+            if (inc[j]) return int(j);
+        return -1;
+    }
+};
+
 template <class F, int MODE, class... As>
 struct Engine {
     using Slots = cuda::std::tuple<Slot<As, MODE>...>;
@@ -445,6 +471,31 @@ struct Engine {
     __device__ __forceinline__ static void write_back(Slots &s, const LaunchParams &p, int32_t b,
                                                       char *smem, cuda::std::index_sequence<Is...>) {
         (cuda::std::get<Is>(s).write_back(p, int(Is), b, smem), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void backup_all(Slots &s, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).backup(), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void restore_all(Slots &s, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).restore(), ...);
+    }
+    // run += increments of the INC argument at position `a` (gather schedule)
+    template <int DG, class TG, size_t... Is>
+    __device__ __forceinline__ static void add_inc(Slots &s, int a, TG *run,
+                                                   cuda::std::index_sequence<Is...>) {
+        (add_inc_one<Is, DG>(s, a, run), ...);
+    }
+    template <size_t I, int DG, class TG>
+    __device__ __forceinline__ static void add_inc_one(Slots &s, int a, TG *run) {
+        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
+        if constexpr (A::kind == KI && A::mode == MINC) {
+            constexpr int pos = IncIndex<As...>::template of<I>();
+            if (a == pos) {
+#pragma unroll
+                for (int c = 0; c < DG; ++c) run[c] += cuda::std::get<I>(s).acc[c];
+            }
+        }
     }
     template <size_t... Is>
     __device__ __forceinline__ static void arrive_sums(Slots &s, const LaunchParams &p, int32_t b,
@@ -637,6 +688,62 @@ __device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
     }
 }
 
+// Target-centric ("gather") schedule for loops whose indirect writes all
+// increment one dat: one thread per target element re-evaluates the kernel for
+// every (element, INC argument) incidence of that target, in serial order, and
+// keeps only that argument's increment — running value starts from the
+// target's current value, so the accumulation order is exactly the reference
+// serial order.  No colours, no shared memory, no atomics, and a target's
+// increments never leave the thread's registers.  Global reductions count
+// each element once (on its first INC argument's incidence).
+template <class T, int D>
+struct GatherAcc {
+    T v[D];
+};
+
+template <class F, class... As>
+__device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_REG, As...>;
+    using II = IncIndex<As...>;
+    constexpr int G = II::template first<0>();
+    static_assert(G >= 0, "gather schedule needs an INC argument");
+    using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
+    using TG = typename AG::type;
+    constexpr int DG = AG::dim;
+    __shared__ double red[32];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    if (t < p.g_ntargets) {
+        const ArgRt &rg = p.a[G];
+        TG *dst = static_cast<TG *>(rg.data) + t * rg.se;
+        TG run[DG];
+#pragma unroll
+        for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+        for (int k = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1); k < ke; ++k) {
+            const int64_t e = __ldg(p.g_elem + k);
+            const int a = __ldg(p.g_pos + k);
+            E::init_elem(s, p, e, nullptr, idx);
+            if constexpr (E::has_reduce) {
+                if (a != 0 || e >= p.rlim) {
+                    E::backup_all(s, idx);
+                    E::call_raw(s, p, idx);
+                    E::restore_all(s, idx);
+                } else {
+                    E::call_raw(s, p, idx);
+                }
+            } else {
+                E::call_raw(s, p, idx);
+            }
+            E::template add_inc<DG>(s, a, run, idx);
+        }
+#pragma unroll
+        for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
+}
+
 // Arrival schedule: one launch over the plan blocks in natural order (best
 // locality), no block colours and no inter-block waiting.  Targets touched by
 // one block are updated directly; shared targets are completed by whichever
@@ -716,6 +823,10 @@ template <class F, class T>
 __global__ void __launch_bounds__(256) k_arrive(const __grid_constant__ LaunchParams p) {
     run_arrive<F>(p, typename F::template sig<T>{});
 }
+template <class F, class T>
+__global__ void __launch_bounds__(256) k_gather(const __grid_constant__ LaunchParams p) {
+    run_gather<F>(p, typename F::template sig<T>{});
+}
 
 // ---- compile-time signature introspection -------------------------------------
 template <class S>
@@ -730,6 +841,7 @@ struct SigInfo<Sig<As...>> {
     }
     static constexpr bool ind_write = ((As::kind == KI && As::mode != MR) || ...);
     static constexpr bool ind_write_non_inc = ((As::kind == KI && (As::mode == MW || As::mode == MRW)) || ...);
+    static constexpr bool direct_write = ((As::kind == KD && As::mode != MR) || ...);
 };
 
 // ---- registry -------------------------------------------------------------------
@@ -744,6 +856,7 @@ struct FunctorEntry {
     LaunchFn direct, staged, phased;
     LaunchFn smem[2], flow[2];                       // [0] colour phases, [1] segmented
     LaunchFn arrive;                                 // segmented, no block colours
+    LaunchFn gather;                                 // target-centric (INC-only loops)
     int (*flow_occupancy[2])(int threads, size_t smem);
 };
 
@@ -777,6 +890,9 @@ struct Registrar {
             opted = true;
         }
         k_flow<F, T, MODE><<<g, b, bytes, s>>>(p);
+    }
+    static void gather(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        k_gather<F, T><<<g, b, 0, s>>>(p);
     }
     static void arrive(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
         static bool opted = false;
@@ -815,6 +931,10 @@ struct Registrar {
         e.flow_occupancy[0] = st ? &flow_occupancy<ST_SMEM> : nullptr;
         e.flow_occupancy[1] = st ? &flow_occupancy<ST_SEG> : nullptr;
         e.arrive = st ? &arrive : nullptr;
+        if constexpr (SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc && !SigInfo<S>::direct_write)
+            e.gather = &gather;
+        else
+            e.gather = nullptr;
         register_functor(e);
     }
 };

@@ -96,7 +96,7 @@ static int validate(const ml_loop_t *L, const FunctorEntry &f) {
 
 static uint64_t scratch_bytes(const ml_loop_t *L, const FunctorEntry &f) {
     uint64_t bytes = 0;
-    const int64_t nb = std::max<int64_t>(L->plan.nblocks, 1);
+    const int64_t nb = std::max<int64_t>({L->plan.nblocks, (L->gather_ntargets + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i)
         if (f.kind[i] == KG && f.mode[i] != MR) bytes += uint64_t(nb) * f.dim[i] * 8 + 256;
     return bytes;
@@ -125,6 +125,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         p.k.i[i] = L->iconst[i];
     }
     char *scratch = static_cast<char *>(L->scratch);
+    const int64_t pstride = std::max<int64_t>({nb, (L->gather_ntargets + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i) {
         const ml_arg_t &a = L->args[i];
         ArgRt &r = p.a[i];
@@ -136,7 +137,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
             if (a.mode != ML_READ) {
                 if (!scratch) ML_FAIL(ML_EINVAL, "loop '%s': reduction needs scratch", L->name);
                 p.part[i] = scratch;
-                scratch += uint64_t(nb) * a.dim * 8 + 256;
+                scratch += uint64_t(pstride) * a.dim * 8 + 256;
             }
         } else if (a.layout == ML_AOS) {
             r.se = a.dim;
@@ -204,7 +205,19 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         }
     }
 
-    if (!f.ind_write) {
+    int64_t nparts = nb;   // reduction partials written by the launch(es)
+    if (f.ind_write && f.gather && L->gather_ntargets > 0 && L->gather_off && L->gather_elem &&
+        L->gather_pos) {
+        // target-centric: one thread per target, serial-order accumulation
+        p.g_ntargets = L->gather_ntargets;
+        p.g_off = L->gather_off;
+        p.g_elem = L->gather_elem;
+        p.g_pos = L->gather_pos;
+        nparts = (L->gather_ntargets + 255) / 256;
+        if (nparts > pstride)
+            ML_FAIL(ML_EINVAL, "loop '%s': gather schedule needs more reduction scratch", L->name);
+        f.gather(p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+    } else if (!f.ind_write) {
         const int threads = std::clamp(round_up32(bs), 32, 256);
         p.blocks = nullptr;
         f.direct(p, dim3(unsigned(nb)), dim3(unsigned(threads)), 0, stream);
@@ -252,10 +265,10 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         if (a.kind != ML_GLOBAL || a.mode == ML_READ) continue;
         if (a.dtype == ML_F64)
             launch_combine<double>(a.mode, static_cast<double *>(a.data), static_cast<const double *>(p.part[i]),
-                                   nb, a.dim, stream);
+                                   nparts, a.dim, stream);
         else
             launch_combine<int64_t>(a.mode, static_cast<int64_t *>(a.data),
-                                    static_cast<const int64_t *>(p.part[i]), nb, a.dim, stream);
+                                    static_cast<const int64_t *>(p.part[i]), nparts, a.dim, stream);
     }
     err = cudaGetLastError();
     if (err != cudaSuccess) ML_FAIL(ML_ECUDA, "loop '%s': combine failed: %s", L->name, cudaGetErrorString(err));

@@ -165,6 +165,53 @@ class ScheduleMirror:
         return self.queue is not None
 
 
+class GatherMirror:
+    """Device target-centric incidence lists of an INC loop (ml_gather_build)."""
+
+    __slots__ = ("off", "elem", "pos", "ntargets")
+
+    def __init__(self, loop, n: int):
+        import ctypes as C
+        inc = [a for a in loop.args if a.kind == "indirect" and a.mode.name == "INC"]
+        self.ntargets = inc[0].dat.set.size
+        cols = [np.ascontiguousarray(a.map.table[:n, a.slot], dtype=np.int64) for a in inc]
+        L = N.lib()
+        h = C.c_void_p()
+        cptr = (C.c_void_p * len(cols))(*[N.ptr(c) for c in cols])
+        N.check(L.ml_gather_build(n, len(cols), cptr, self.ntargets, C.byref(h)), "ml_gather_build")
+        try:
+            off = np.empty(self.ntargets + 1, np.int32)
+            elem = np.empty(max(n * len(cols), 1), np.int32)
+            pos = np.empty(max(n * len(cols), 1), np.uint8)
+            N.check(L.ml_gather_export(h, N.ptr(off), N.ptr(elem), N.ptr(pos)), "ml_gather_export")
+        finally:
+            L.ml_gather_free(h)
+        self.off, self.elem, self.pos = _upload(off), _upload(elem), _upload(pos)
+
+
+def gather_eligible(loop) -> bool:
+    """Target-centric execution applies when every indirect write is an INC of one
+    dat, no direct argument is written, and the INC dat is not read elsewhere."""
+    ind_w = [a for a in loop.args if a.kind == "indirect" and a.mode.name != "READ"]
+    if not ind_w or any(a.mode.name != "INC" for a in ind_w):
+        return False
+    if len({a.dat.name for a in ind_w}) != 1:
+        return False
+    if any(a.kind == "direct" and a.mode.name != "READ" for a in loop.args):
+        return False
+    name = ind_w[0].dat.name
+    return not any(a.kind != "global" and a.dat.name == name and a.mode.name != "INC"
+                   for a in loop.args)
+
+
+def gather_mirror(loop, plan) -> GatherMirror:
+    cache = plan.__dict__.setdefault("_gathers", {})
+    key = loop.signature()
+    if key not in cache:
+        cache[key] = GatherMirror(loop, plan.n)
+    return cache[key]
+
+
 def schedule_mirror(loop, plan, nwindows: int) -> ScheduleMirror:
     cache = plan.__dict__.setdefault("_schedules", {})
     key = (loop.signature(), int(nwindows))

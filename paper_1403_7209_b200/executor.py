@@ -31,7 +31,8 @@ import numpy as np
 
 from . import _native as N
 from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Mesh, MeshError)
-from .device import dat_mirror, map_mirror, plan_mirror, schedule_mirror, staging_mirror
+from .device import (dat_mirror, gather_eligible, gather_mirror, map_mirror, plan_mirror,
+                     schedule_mirror, staging_mirror)
 from .kernels import resolve_kernel
 from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
 from .plan import plan_for, plan_stats
@@ -73,7 +74,7 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
-    inc_schedule: str = "colour"            # "colour" | "flow" | "arrival": cross-block scheme
+    inc_schedule: str = "colour"            # "colour" | "flow" | "arrival" | "gather"
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
 
@@ -91,7 +92,7 @@ class BackendConfig:
             raise MeshError(f"unknown residency {self.residency!r}")
         if self.inc_staging not in ("segmented", "colour"):
             raise MeshError(f"unknown inc_staging {self.inc_staging!r}")
-        if self.inc_schedule not in ("flow", "arrival", "colour"):
+        if self.inc_schedule not in ("flow", "arrival", "colour", "gather"):
             raise MeshError(f"unknown inc_schedule {self.inc_schedule!r}")
         if self.inc_schedule == "colour":
             self.dataflow = False
@@ -244,6 +245,13 @@ class _LoopEntry:
         L.plan.blocks = pm.blocks.ptr
         L.plan.elem_color = pm.ecol.ptr if pm.ecol is not None else None
         L.plan.elem_ncolors = pm.encol.ptr if pm.encol is not None else None
+        self.gather = None
+        if config.inc_schedule == "gather" and self.n > 0 and gather_eligible(loop):
+            self.gather = gather_mirror(loop, self.plan)
+            L.gather_ntargets = self.gather.ntargets
+            L.gather_off = self.gather.off.ptr
+            L.gather_elem = self.gather.elem.ptr
+            L.gather_pos = self.gather.pos.ptr
         self.schedule = None
         if (config.dataflow and self.plan.has_writes and self.plan.ncolors > 1
                 and not _inc_aliased(loop)):

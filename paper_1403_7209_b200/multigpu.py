@@ -403,8 +403,9 @@ class _HostRows:
 
 
 def _run_rank(rp: RankProgram, dev, transport, timeout_ms: float):
-    """The rank main loop (reference executor.py:577-600) + reductions."""
-    dirty: dict = {}
+    """The rank main loop (reference executor.py:577-600) + reductions.  Dirty
+    bits live on the RankProgram, so repeated runs keep halos coherent."""
+    dirty = rp.__dict__.setdefault("dirty", {})
     messages = 0
     comm = np.zeros(len(rp.program))
     comp = np.zeros(len(rp.program))

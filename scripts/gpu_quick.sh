@@ -5,8 +5,8 @@ TAG=${1:-quick}; shift || true
 OUT=gpurun_out/$TAG; mkdir -p "$OUT"
 python -c "import __graft_entry__ as g; g.build()" > "$OUT/build.log" 2>&1
 timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider -x > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/status.txt"
-timeout 600 python scripts/profile_proxy.py --iters 3 --inc-schedule colour flow arrival > "$OUT/schedules.log" 2>&1; echo "sched rc=$?" >> "$OUT/status.txt"
+timeout 600 python scripts/profile_proxy.py --iters 3 --inc-schedule colour gather arrival > "$OUT/schedules.log" 2>&1; echo "sched rc=$?" >> "$OUT/status.txt"
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-   -k "regex:ProxyVflux|ProxyGrad|ProxyIflux" -s 0 -c 3 -o "$OUT/arrive" \
-   python scripts/profile_proxy.py --iters 1 --inc-schedule arrival > "$OUT/ncu.log" 2>&1; echo "ncu rc=$?" >> "$OUT/status.txt"
+   -k "regex:ProxyVflux|ProxyGrad|ProxyIflux" -s 0 -c 3 -o "$OUT/gather" \
+   python scripts/profile_proxy.py --iters 1 --inc-schedule gather > "$OUT/ncu.log" 2>&1; echo "ncu rc=$?" >> "$OUT/status.txt"
 cat "$OUT/status.txt"; tail -2 "$OUT/pytest_gpu.log"; cat "$OUT/schedules.log"

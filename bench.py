@@ -1,7 +1,7 @@
 """Benchmark: one Hydra-shaped solver iteration per step on B200 (BASELINE.json configs[1]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload proxy|diffusion] [--grid 94] [--inc-schedule flow|arrival|colour]
+                    [--workload proxy|diffusion] [--grid 94] [--inc-schedule gather|colour|flow|arrival]
 
 Workload (default): ``build_hydra_proxy`` on the Rotor37-sized 3-D grid
 (94^3 = 830,584 nodes, 2,465,244 edges), numbered randomly (an unstructured
@@ -210,7 +210,7 @@ def main():
     ap.add_argument("--workload", choices=["proxy", "diffusion"], default="proxy")
     ap.add_argument("--grid", type=int, default=None)
     ap.add_argument("--cpu-grid", type=int, default=None)
-    ap.add_argument("--inc-schedule", choices=["flow", "arrival", "colour", "gather"], default="colour")
+    ap.add_argument("--inc-schedule", choices=["gather", "colour", "flow", "arrival"], default="gather")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.grid is None:

@@ -827,6 +827,10 @@ template <class F, class T>
 __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ LaunchParams p) {
     run_gather<F>(p, typename F::template sig<T>{});
 }
+template <class F, class T, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_gather_occ(const __grid_constant__ LaunchParams p) {
+    run_gather<F>(p, typename F::template sig<T>{});
+}
 
 // ---- compile-time signature introspection -------------------------------------
 template <class S>
@@ -856,7 +860,8 @@ struct FunctorEntry {
     LaunchFn direct, staged, phased;
     LaunchFn smem[2], flow[2];                       // [0] colour phases, [1] segmented
     LaunchFn arrive;                                 // segmented, no block colours
-    LaunchFn gather;                                 // target-centric (INC-only loops)
+    LaunchFn gather[4];                              // target-centric (INC-only loops):
+                                                     // free / >=2 / >=3 / >=4 CTAs of 256 per SM
     int (*flow_occupancy[2])(int threads, size_t smem);
 };
 
@@ -893,6 +898,10 @@ struct Registrar {
     }
     static void gather(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_gather<F, T><<<g, b, 0, s>>>(p);
+    }
+    template <int MINB>
+    static void gather_occ(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        k_gather_occ<F, T, MINB><<<g, b, 0, s>>>(p);
     }
     static void arrive(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
         static bool opted = false;
@@ -932,9 +941,12 @@ struct Registrar {
         e.flow_occupancy[1] = st ? &flow_occupancy<ST_SEG> : nullptr;
         e.arrive = st ? &arrive : nullptr;
         if constexpr (SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc && !SigInfo<S>::direct_write)
-            e.gather = &gather;
-        else
-            e.gather = nullptr;
+        {
+            e.gather[0] = &gather;
+            e.gather[1] = &gather_occ<2>;
+            e.gather[2] = &gather_occ<3>;
+            e.gather[3] = &gather_occ<4>;
+        }
         register_functor(e);
     }
 };

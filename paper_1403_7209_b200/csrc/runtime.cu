@@ -73,6 +73,17 @@ static void launch_combine(int mode, T *g, const T *part, int64_t nparts, int di
 
 static int round_up32(int64_t x) { return int((x + 31) / 32 * 32); }
 
+// k_gather occupancy variant: ML_GATHER_MINB unset/0/1 = the compiler's register
+// choice; 2, 3 or 4 = registers capped for that many resident CTAs of 256 per SM
+static int gather_variant() {
+    static const int v = [] {
+        const char *s = std::getenv("ML_GATHER_MINB");
+        const int m = s ? std::atoi(s) : 0;
+        return m <= 1 ? 0 : m >= 4 ? 3 : m - 1;
+    }();
+    return v;
+}
+
 static int validate(const ml_loop_t *L, const FunctorEntry &f) {
     const char *nm = L->name ? L->name : "?";
     if (L->nargs != f.nargs)
@@ -206,7 +217,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     }
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
-    if (f.ind_write && f.gather && L->gather_ntargets > 0 && L->gather_off && L->gather_elem &&
+    if (f.ind_write && f.gather[0] && L->gather_ntargets > 0 && L->gather_off && L->gather_elem &&
         L->gather_pos) {
         // target-centric: one thread per target, serial-order accumulation
         p.g_ntargets = L->gather_ntargets;
@@ -216,7 +227,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         nparts = (L->gather_ntargets + 255) / 256;
         if (nparts > pstride)
             ML_FAIL(ML_EINVAL, "loop '%s': gather schedule needs more reduction scratch", L->name);
-        f.gather(p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+        f.gather[gather_variant()](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
     } else if (!f.ind_write) {
         const int threads = std::clamp(round_up32(bs), 32, 256);
         p.blocks = nullptr;

@@ -74,7 +74,7 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
-    inc_schedule: str = "colour"            # "colour" | "flow" | "arrival" | "gather"
+    inc_schedule: str = "gather"            # "gather" | "colour" | "flow" | "arrival"
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
 
@@ -94,7 +94,8 @@ class BackendConfig:
             raise MeshError(f"unknown inc_staging {self.inc_staging!r}")
         if self.inc_schedule not in ("flow", "arrival", "colour", "gather"):
             raise MeshError(f"unknown inc_schedule {self.inc_schedule!r}")
-        if self.inc_schedule == "colour":
+        if self.inc_schedule in ("colour", "gather"):
+            # gather: loops it does not apply to run the colour schedule
             self.dataflow = False
 
     def block_size_for(self, loop_name: str) -> int:

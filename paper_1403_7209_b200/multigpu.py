@@ -506,7 +506,7 @@ def bench_distributed(args, metric):
     edges = mesh.sets["edges"].size
     local_dev = int(os.environ.get("ML_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     cfg = ml.BackendConfig(device=local_dev, nranks=world, partitioner="rcb", coord_dat="coords",
-                           inc_schedule=getattr(args, "inc_schedule", "colour"))
+                           inc_schedule=getattr(args, "inc_schedule", "gather"))
     t0 = time.perf_counter()
     rp, dev, transport, layout, cfg = setup_distributed(prog, mesh, cfg, transport)
     setup["layout_and_local_mesh_s"] = round(time.perf_counter() - t0, 3)

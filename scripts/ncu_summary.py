@@ -36,7 +36,8 @@ METRICS = [
     ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall_wait"),
 ]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-        "msecond": 1e-3, "second": 1}
+        "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1,
+        "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
 def read_raw(rep: str):
@@ -55,8 +56,11 @@ def read_raw(rep: str):
 
 
 def short(name: str) -> str:
-    m = re.search(r"(k_[a-z]+)<[^>]*?(\w+), (double|long)", name)
-    return f"{m.group(1)}<{m.group(2)}>" if m else name[:60]
+    m = re.search(r"(k_[a-z_0-9]+)<(?:.*?::)?(\w+), (double|long)", name)
+    if m:
+        return f"{m.group(1)}<{m.group(2)}>"
+    m = re.search(r"(k_[a-z_0-9]+)", name)
+    return m.group(1) if m else name[:60]
 
 
 def main():

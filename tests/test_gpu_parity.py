@@ -34,6 +34,9 @@ def close(got, ref, rtol=RTOL, what=""):
     assert not bad.any(), f"{what}: {bad.sum()} mismatches, max |d| {np.max(np.abs(got - ref))}"
 
 
+SCHEDULES = ("gather", "colour", "flow", "arrival")
+
+
 def cfg(**kw):
     return ml.BackendConfig(**kw)
 
@@ -43,11 +46,12 @@ def _exec_cases():
 
 
 @pytest.mark.parametrize("case", _exec_cases(), ids=lambda c: c["name"])
-@pytest.mark.parametrize("bs", [256, 16])
-def test_apps_match_reference_golden(case, bs):
+@pytest.mark.parametrize("bs,sched", [(256, "gather"), (16, "gather"), (256, "colour"),
+                                      (16, "colour")])
+def test_apps_match_reference_golden(case, bs, sched):
     g = golden("exec.npz")
     mesh, prog, h = _cases.build_app(case["app"], case["n"], case["dtype"], case["steps"])
-    res = ml.run_program(prog, mesh, cfg(block_size=bs))
+    res = ml.run_program(prog, mesh, cfg(block_size=bs, inc_schedule=sched))
     assert {r.loop for r in res.perf} == {l.name for l in prog}
     for k, v in _cases.app_results(case["app"], h).items():
         want = g[f"exec/{case['name']}/{k}"]
@@ -91,14 +95,16 @@ def test_fuzz_meshes_match_reference_and_oracle(rng):
         if case["app"] != "fuzz":
             continue
         mesh, loop = _cases.random_loop_mesh(np.random.default_rng(case["seed"]), max_elems=300)
-        ml.run_program([loop], mesh, cfg(block_size=int(rng.choice([1, 7, 32, 256]))))
+        ml.run_program([loop], mesh, cfg(block_size=int(rng.choice([1, 7, 32, 256])),
+                                         inc_schedule=str(rng.choice(SCHEDULES))))
         np.testing.assert_array_equal(mesh.dats["vals"].fetch(), g[f"exec/{case['name']}/vals"])
     for _ in range(20):
         seed = int(rng.integers(0, 2 ** 31))
         ref_mesh, ref_loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=5000)
         oserial.run_loop(ref_loop)
         mesh, loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=5000)
-        ml.run_program([loop], mesh, cfg(block_size=int(rng.choice([1, 7, 64, 256, 1024]))))
+        ml.run_program([loop], mesh, cfg(block_size=int(rng.choice([1, 7, 64, 256, 1024])),
+                                         inc_schedule=str(rng.choice(SCHEDULES))))
         np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref_mesh.dats["vals"].fetch())
 
 
@@ -141,11 +147,12 @@ def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa):
     np.testing.assert_array_equal(h["dt_min"][0].value, rh["dt_min"][0].value)
 
 
-def test_proxy_full_size_iteration_vs_oracle():
+@pytest.mark.parametrize("sched", ["gather", "colour"])
+def test_proxy_full_size_iteration_vs_oracle(sched):
     """Config B (Rotor37-sized, 2.47M edges): one full iteration, shuffled + CM-renumbered."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(94, seed=0)
     bulk.run_program(rprog, resolve_kernel)
-    ml.run_program(prog, mesh, cfg())
+    ml.run_program(prog, mesh, cfg(inc_schedule=sched))
     close(h["q"].fetch(), rh["q"].fetch(), what="q")
     close([h["rms"][0].value], [rh["rms"][0].value], what="rms")
     assert h["dt_min"][0].value == rh["dt_min"][0].value
@@ -167,10 +174,14 @@ def test_colouring_stress_hub_and_shuffled_meshes():
     for make in (lambda: apps.gen_hub_mesh(20000, 200000, n_hubs=4, hub_share=0.05, seed=2),
                  lambda: _shuffled_hex(30)):
         ref, mesh = make(), make()
-        rl, l = _cases.inc_loop(ref, "edge_nodes"), _cases.inc_loop(mesh, "edge_nodes")
+        rl = _cases.inc_loop(ref, "edge_nodes")
         oserial.run_loop(rl)
-        res = ml.run_program([l], mesh, cfg())
-        np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
+        want = ref.dats["acc"].fetch()
+        for sched in SCHEDULES:
+            mesh.dats["acc"].put(np.zeros_like(want))
+            l = _cases.inc_loop(mesh, "edge_nodes")
+            res = ml.run_program([l], mesh, cfg(inc_schedule=sched))
+            np.testing.assert_array_equal(mesh.dats["acc"].fetch(), want, sched)
         assert res.perf[0].nc > 8
 
 
@@ -236,7 +247,8 @@ def test_dataflow_schedule_matches_colour_launches(bs):
     """One window: same per-target increment order as per-colour launches, so float
     results match bit for bit; several windows reorder increments (tolerance)."""
     outs = []
-    for kw in ({"dataflow": False}, {"flow_windows": 1}, {"flow_windows": 7}):
+    for kw in ({"inc_schedule": "colour"}, {"inc_schedule": "flow", "flow_windows": 1},
+               {"inc_schedule": "flow", "flow_windows": 7}):
         mesh = apps.gen_hex_mesh(20, seed=8)
         apps.shuffle_mesh(mesh, seed=9)
         prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=8)
@@ -250,8 +262,10 @@ def test_dataflow_schedule_matches_colour_launches(bs):
     for make in (lambda: apps.gen_hub_mesh(5000, 60000, n_hubs=64, hub_share=0.05, seed=3),
                  lambda: _shuffled_hex(16)):
         ref, mesh = make(), make()
-        ml.run_program([_cases.inc_loop(ref, "edge_nodes")], ref, cfg(block_size=bs, dataflow=False))
-        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh, cfg(block_size=bs))
+        ml.run_program([_cases.inc_loop(ref, "edge_nodes")], ref,
+                       cfg(block_size=bs, inc_schedule="colour"))
+        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh,
+                       cfg(block_size=bs, inc_schedule="flow"))
         np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
 
 
@@ -327,16 +341,18 @@ def test_smem_and_register_staging_agree(bs):
         apps.shuffle_mesh(mesh, seed=6)
         prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=5)
         ml.renumber_mesh(mesh)
-        ml.run_program(prog[:5], mesh, cfg(block_size=bs, **kw))
+        ml.run_program(prog[:5], mesh, cfg(block_size=bs, inc_schedule="colour", **kw))
         outs.append((h["res"].fetch(), h["grad"].fetch()))
     for o in outs[1:]:
         close(o[0], outs[0][0], what="res")
         close(o[1], outs[0][1], what="grad")
     ref = apps.gen_mesh(40)
-    ml.run_program([_cases.inc_loop(ref, "edge_nodes")], ref, cfg(block_size=bs, smem_staging=False))
+    ml.run_program([_cases.inc_loop(ref, "edge_nodes")], ref,
+                   cfg(block_size=bs, smem_staging=False, inc_schedule="colour"))
     for kw in variants[1:]:
         mesh = apps.gen_mesh(40)
-        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh, cfg(block_size=bs, **kw))
+        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh,
+                       cfg(block_size=bs, inc_schedule="colour", **kw))
         np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
 
 

@@ -484,3 +484,42 @@ def run_loop(loop: Loop, mesh: Mesh, config: BackendConfig | None = None,
     times = cp.run(False, config.time_loops or collector is not None)
     if collector is not None and times is not None:
         _record(collector, cp, times)
+
+
+def run_serial(loop: Loop, mesh: Mesh, config: BackendConfig | None = None,
+               collector: PerfCollector | None = None) -> None:
+    """Reference ``run_serial`` (executor.py:206-217) on the device: indirect
+    increments use the target-centric schedule, which applies every target's
+    increments in ascending element order — the serial result, bit for bit.
+    Loops with indirect WRITE/RW arguments run coloured (as the reference's
+    parallel backends do)."""
+    from dataclasses import replace
+    run_loop(loop, mesh, replace(config or BackendConfig(), inc_schedule="gather"), collector)
+
+
+def run_threads(loop: Loop, mesh: Mesh, config: BackendConfig | None = None,
+                collector: PerfCollector | None = None) -> None:
+    """Reference ``run_threads`` (executor.py:278-284): the coloured schedule of
+    the reference plan (block colours in order, element colours inside a block)
+    as per-colour CUDA launches."""
+    from dataclasses import replace
+    run_loop(loop, mesh, replace(config or BackendConfig(), inc_schedule="colour"), collector)
+
+
+def run_ranks(program: Sequence[Loop], mesh: Mesh, layout=None,
+              config: BackendConfig | None = None,
+              collector: PerfCollector | None = None) -> RunResult:
+    """Reference ``run_ranks`` (executor.py:690-695): owner-compute execution over
+    ``layout`` (or the layout of ``config``), one process per GPU — launch with
+    torchrun; the ranks are processes, not threads of this one."""
+    from .multigpu import run_program_distributed
+    config = config or BackendConfig(nranks=layout.nranks if layout is not None else 1)
+    return run_program_distributed(program, mesh, config, layout=layout, collector=collector)
+
+
+def run_hybrid(program: Sequence[Loop], mesh: Mesh, config: BackendConfig | None = None,
+               collector: PerfCollector | None = None) -> RunResult:
+    """Reference ``run_hybrid`` (executor.py:698-704) mixes CPU worker classes; on
+    B200 there is no CPU execution path, so this is refused loudly."""
+    raise ExecError("run_hybrid: CPU+GPU hybrid execution is not provided by the B200 backend; "
+                    "use run_program (one GPU) or run_ranks (one process per GPU)")

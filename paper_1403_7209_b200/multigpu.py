@@ -446,7 +446,7 @@ def init_distributed(config=None):
     return dist.get_rank(), dist.get_world_size(), transport
 
 
-def setup_distributed(program, mesh, config, transport=None, executor_factory=None):
+def setup_distributed(program, mesh, config, transport=None, executor_factory=None, layout=None):
     """Layout + this rank's local program + executor (one-time setup)."""
     import torch.distributed as dist
     rank, world, default_transport = init_distributed(config)
@@ -456,20 +456,24 @@ def setup_distributed(program, mesh, config, transport=None, executor_factory=No
         from dataclasses import replace
         config = replace(config, nranks=world)
     mesh.freeze()
-    layout = build_layout(mesh, program, config)
+    if layout is None:
+        layout = build_layout(mesh, program, config)
+    elif layout.nranks != world:
+        raise MeshError(f"layout has {layout.nranks} ranks but WORLD_SIZE={world}")
     rp = RankProgram(mesh, program, layout, rank)
     transport = transport or default_transport
     dev = executor_factory(rp, config) if executor_factory else DeviceRank(rp, config)
     return rp, dev, transport, layout, config
 
 
-def run_program_distributed(program, mesh, config, transport=None, executor_factory=None):
+def run_program_distributed(program, mesh, config, transport=None, executor_factory=None,
+                            layout=None, collector=None):
     """Owner-compute execution of a program on ``WORLD_SIZE`` processes (one GPU each)."""
     from .executor import RunResult
     from .perf import PerfCollector, useful_bytes
     t_start = time.perf_counter()
     rp, dev, transport, layout, config = setup_distributed(program, mesh, config, transport,
-                                                           executor_factory)
+                                                           executor_factory, layout)
     messages, comm, comp = _run_rank(rp, dev, transport, config.timeout_ms)
     # final: every rank gets the owned rows of every dat, and the global values
     owned = {name: rp.owned_rows(name) for name in rp.dats}
@@ -483,7 +487,7 @@ def run_program_distributed(program, mesh, config, transport=None, executor_fact
     for gid, val in rp.values.items():
         rp.user_globals[gid].buffer[:] = val.buffer
     msgs = sum(transport.allgather_object(messages))
-    collector = PerfCollector()
+    collector = collector if collector is not None else PerfCollector()
     for i, loop in enumerate(program):
         collector.add(loop.name, float(comm[i] + comp[i]), useful_bytes(loop), comm=float(comm[i]),
                       comp=float(comp[i]))

@@ -120,8 +120,16 @@ def op_arg_gbl(data, dim: int, type_: str, acc):
     return arg_global(g, acc)
 
 
-def op_par_loop(set_, kernel, *args, name: str | None = None):
-    """Build the loop and run it now on the session backend; returns its RunResult."""
+def op_par_loop(*call, name: str | None = None):
+    """Build the loop and run it now on the session backend; returns its RunResult.
+
+    Both OP2 spellings: ``op_par_loop(set, kernel, *args)`` (Fortran, Fig. 4)
+    and ``op_par_loop(kernel, "name", set, *args)`` (C++).
+    """
+    if call and callable(call[0]):
+        kernel, name, set_, args = call[0], call[1], call[2], call[3:]
+    else:
+        set_, kernel, args = call[0], call[1], call[2:]
     loop = Loop(name or getattr(kernel, "__name__", "op_par_loop"), set_, list(args), kernel)
     result = run_program([loop], op_mesh(), _session.get("config") or BackendConfig())
     for arr, g in _session.pop("gbl", []):

@@ -395,3 +395,21 @@ def test_perf_records_and_report_schema(tmp_path):
                    mesh_sets={n: s.size for n, s in mesh.sets.items()})
     assert {l["loop"] for l in json.loads(path.read_text())["loops"]} == \
         {"area_calc", "area_distribute", "area_total"}
+
+
+def test_reference_per_loop_entries():
+    """run_serial reproduces the serial order bit for bit (gather schedule);
+    run_threads is the coloured schedule; run_hybrid refuses loudly."""
+    ref, a, b = apps.gen_hub_mesh(3000, 30000, n_hubs=4, hub_share=0.1, seed=5), None, None
+    ref.decl_dat("acc", ref.sets["nodes"], 1, "float64", np.zeros(ref.sets["nodes"].size))
+    a = apps.gen_hub_mesh(3000, 30000, n_hubs=4, hub_share=0.1, seed=5)
+    a.decl_dat("acc", a.sets["nodes"], 1, "float64", np.zeros(a.sets["nodes"].size))
+    b = apps.gen_hub_mesh(3000, 30000, n_hubs=4, hub_share=0.1, seed=5)
+    b.decl_dat("acc", b.sets["nodes"], 1, "float64", np.zeros(b.sets["nodes"].size))
+    oserial.run_loop(_cases.inc_loop(ref, "edge_nodes", dtype="float64"))
+    ml.run_serial(_cases.inc_loop(a, "edge_nodes", dtype="float64"), a)
+    np.testing.assert_array_equal(a.dats["acc"].fetch(), ref.dats["acc"].fetch())
+    ml.run_threads(_cases.inc_loop(b, "edge_nodes", dtype="float64"), b)
+    close(b.dats["acc"].fetch(), ref.dats["acc"].fetch(), what="threads")
+    with pytest.raises(ml.ExecError, match="run_hybrid"):
+        ml.run_hybrid([], b)

@@ -65,7 +65,7 @@ def test_fig4_loops_on_device_match_oracle():
                     op_arg_dat(coords, 2, pcell, 2, "r8", OP_READ),
                     op_arg_dat(coords, 3, pcell, 2, "r8", OP_READ),
                     op_arg_dat(areac, -1, OP_ID, 1, "r8", OP_WRITE))
-        op_par_loop(cells, apps._k_distribute,
+        op_par_loop(apps._k_distribute, "distr", cells,          # the C++ spelling
                     op_arg_dat(areac, -1, OP_ID, 1, "r8", OP_READ),
                     op_arg_dat(arean, 1, pcell, 1, "r8", OP_INC),
                     op_arg_dat(arean, 2, pcell, 1, "r8", OP_INC),

@@ -47,6 +47,9 @@ class ExchangeTimeout(ExecError):
     """A rank waited longer than the configured bound for a halo message."""
 
 
+SCHEDULES = ("gather", "colour", "flow", "arrival")
+
+
 @dataclass
 class BackendConfig:
     backend: str = "cuda"
@@ -75,6 +78,7 @@ class BackendConfig:
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
     inc_schedule: str = "gather"            # "gather" | "colour" | "flow" | "arrival"
+    inc_schedule_table: dict | None = None  # per-loop override (tuner.tune_schedule)
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
 
@@ -92,11 +96,16 @@ class BackendConfig:
             raise MeshError(f"unknown residency {self.residency!r}")
         if self.inc_staging not in ("segmented", "colour"):
             raise MeshError(f"unknown inc_staging {self.inc_staging!r}")
-        if self.inc_schedule not in ("flow", "arrival", "colour", "gather"):
-            raise MeshError(f"unknown inc_schedule {self.inc_schedule!r}")
-        if self.inc_schedule in ("colour", "gather"):
-            # gather: loops it does not apply to run the colour schedule
-            self.dataflow = False
+        for sched in [self.inc_schedule, *(self.inc_schedule_table or {}).values()]:
+            if sched not in SCHEDULES:
+                raise MeshError(f"unknown inc_schedule {sched!r}; expected one of {SCHEDULES}")
+
+    def schedule_for(self, loop_name: str) -> str:
+        """The INC schedule of one loop ("gather" falls back to "colour" for
+        loops it does not apply to; "flow"/"arrival" need ``dataflow``)."""
+        if self.inc_schedule_table and loop_name in self.inc_schedule_table:
+            return self.inc_schedule_table[loop_name]
+        return self.inc_schedule
 
     def block_size_for(self, loop_name: str) -> int:
         if self.block_size_table and loop_name in self.block_size_table:
@@ -247,15 +256,17 @@ class _LoopEntry:
         L.plan.elem_color = pm.ecol.ptr if pm.ecol is not None else None
         L.plan.elem_ncolors = pm.encol.ptr if pm.encol is not None else None
         self.gather = None
-        if config.inc_schedule == "gather" and self.n > 0 and gather_eligible(loop):
+        sched = config.schedule_for(loop.name)
+        self.sched = sched
+        if sched == "gather" and self.n > 0 and gather_eligible(loop):
             self.gather = gather_mirror(loop, self.plan)
             L.gather_ntargets = self.gather.ntargets
             L.gather_off = self.gather.off.ptr
             L.gather_elem = self.gather.elem.ptr
             L.gather_pos = self.gather.pos.ptr
         self.schedule = None
-        if (config.dataflow and self.plan.has_writes and self.plan.ncolors > 1
-                and not _inc_aliased(loop)):
+        if (self.gather is None and config.dataflow and sched in ("flow", "arrival")
+                and self.plan.has_writes and self.plan.ncolors > 1 and not _inc_aliased(loop)):
             sched = schedule_mirror(loop, self.plan, _flow_windows(loop, config))
             if sched.usable:
                 self.schedule = sched
@@ -268,7 +279,8 @@ class _LoopEntry:
         for k, v in enumerate(binding.iconsts[:4]):
             L.iconst[k] = v
         L.rlim = int(rlim[sname]) if rlim and sname in rlim else -1
-        self.staging = staging_mirror(loop, self.plan) if config.smem_staging else None
+        self.staging = (staging_mirror(loop, self.plan)
+                        if config.smem_staging and self.gather is None else None)
         if self.staging is not None:
             sg = self.staging
             L.staging.ngroups = sg.ngroups
@@ -281,7 +293,7 @@ class _LoopEntry:
             for i, buf in sg.loc.items():
                 L.staging.loc[i] = buf.ptr
             L.staging.seg = 1 if config.inc_staging == "segmented" else 0
-            L.staging.arrive = 1 if (config.inc_schedule == "arrival" and L.staging.seg
+            L.staging.arrive = 1 if (sched == "arrival" and L.staging.seg
                                      and not _inc_aliased(loop)) else 0
             for g in range(sg.ngroups):
                 L.staging.toff[g] = sg.toff[g].ptr
@@ -423,7 +435,8 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
            tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
-           config.dataflow, config.inc_staging, config.inc_schedule, config.flow_windows,
+           config.dataflow, config.inc_staging, config.inc_schedule,
+           tuple(sorted((config.inc_schedule_table or {}).items())), config.flow_windows,
            config.flow_window_l2_fraction,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)

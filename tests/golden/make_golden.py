@@ -368,7 +368,38 @@ def make_bytes():
     return res
 
 
+MESHIO_BAD = [
+    "sets", "nope 1", "sets 1\nn x", "sets 1\nn 2\nmaps 1\nm n n 1\n1\n3\ndats 0",
+    "sets 1\nn 1\nmaps 0\ndats 1\nd n 1 float64\nz",
+    "sets 1\nn 1\nmaps 0\ndats 1\nd n 1 float16\n1", "sets 0\nmaps 0\ndats 0\nextra",
+    "sets 1\nn 2\nmaps 1\nm n missing 1\n1\n2\ndats 0",
+    "sets 1\nn 2\nmaps 1\nm n n 1\n1\n1.5\ndats 0",
+    "sets 1\nn 3\nmaps 1\nm n n 1\n1 x", "sets 1\nn 3\nmaps 1\nm n n 1\n1 2",
+    "sets 1\nn 2\nmaps 0\ndats 1\nd n 2 int64\n1 2 3.5 4",
+    "sets 1\nn 2\nmaps 0\ndats 1\nd n 1 float64\n1e3",
+    "sets 2\nn 2\nn 3\nmaps 0\ndats 0", "sets 1\nn 2\nmaps 1\nm n n 0\ndats 0",
+    "sets 1\nn -1\nmaps 0\ndats 0",
+]
+
+
+def make_meshio():
+    """Reference text form of two meshes and its error message per malformed input."""
+    texts = {"sample": R.format_mesh(RA.sample_mesh()), "gen3": R.format_mesh(RA.gen_mesh(3))}
+    errors = []
+    for bad in MESHIO_BAD:
+        try:
+            R.parse_mesh(bad)
+            errors.append([bad, None])
+        except R.FormatError as err:
+            errors.append([bad, str(err)])
+    return {"texts": texts, "errors": errors}
+
+
 def main():
+    if sys.argv[1:] == ["meshio"]:
+        (HERE / "meshio.json").write_text(json.dumps(make_meshio(), indent=1) + "\n")
+        return
+    (HERE / "meshio.json").write_text(json.dumps(make_meshio(), indent=1) + "\n")
     for fname, maker in (("plans.npz", make_plans), ("renumber.npz", make_renumber),
                          ("partition.npz", make_partition), ("exec.npz", make_exec)):
         out: dict = {}

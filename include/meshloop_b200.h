@@ -123,8 +123,11 @@ typedef struct ml_loop {
     /* target-centric schedule (ml_gather_build); ntargets == 0 disables it */
     int64_t gather_ntargets;
     const int32_t *gather_off;      /* device [ntargets+1]                       */
-    const int32_t *gather_elem;     /* device [n * inc args]                     */
-    const uint8_t *gather_pos;      /* device [n * inc args]                     */
+    const int32_t *gather_elem;     /* device [n * written args]                 */
+    const uint8_t *gather_pos;      /* device [n * written args]                 */
+    const int32_t *gather_targets;  /* device [ntargets] target ids of a compacted
+                                       list (only targets with incidences), or
+                                       NULL: target k is element k of the set   */
 } ml_loop_t;
 
 typedef struct ml_device_info {
@@ -186,10 +189,11 @@ int ml_schedule_export(const ml_schedule_t *s, int64_t *ndeps, int32_t *queue, i
                        int32_t *dep_list);
 int ml_schedule_free(ml_schedule_t *s);
 
-/* Target-centric ("gather") schedule of an INC loop whose indirect writes all
- * increment one dat: per target, its (element, INC-argument position)
- * incidences in serial order (element, then argument).  `cols` are the INC
- * arguments' target columns in argument order.  Export sizes: off
+/* Target-centric ("gather") schedule of a loop whose indirect writes all go to
+ * one dat with one mode (INC, or WRITE): per target, its (element, argument
+ * position) incidences in serial order (element, then argument) — the order
+ * reference run_serial (executor.py:206-217) applies them in.  `cols` are the
+ * written arguments' target columns in argument order.  Export sizes: off
  * [ntargets+1], elem/pos [n*ncols]. */
 typedef struct ml_gather ml_gather_t;
 int ml_gather_build(int64_t n, int32_t ncols, const int64_t *const *cols, int64_t ntargets,

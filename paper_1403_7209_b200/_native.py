@@ -78,7 +78,8 @@ class MlLoop(C.Structure):
                 ("fconst", C.c_double * 4), ("iconst", C.c_int64 * 4), ("scratch", C.c_void_p),
                 ("staging", MlStagingDev), ("rlim", C.c_int64),
                 ("gather_ntargets", C.c_int64), ("gather_off", C.c_void_p),
-                ("gather_elem", C.c_void_p), ("gather_pos", C.c_void_p)]
+                ("gather_elem", C.c_void_p), ("gather_pos", C.c_void_p),
+                ("gather_targets", C.c_void_p)]
 
 
 class MlDeviceInfo(C.Structure):

@@ -116,6 +116,7 @@ struct LaunchParams {
     const int32_t *g_off;
     const int32_t *g_elem;
     const uint8_t *g_pos;
+    const int32_t *g_tlist;     // compacted target ids (nullptr: identity)
 };
 
 // strided view of one element's components
@@ -151,7 +152,9 @@ __device__ __forceinline__ T combine(T a, T b) {
 // MODE 3 (ST_SEG): the functor increments a private shared-memory slot of its
 // own (no registers held, no phases); the write-back sums each target's slots
 // in element order — a deterministic segmented reduction.
-enum : int { ST_NONE = 0, ST_REG = 1, ST_SMEM = 2, ST_SEG = 3 };
+// MODE 4 (ST_GATHER): target-centric schedule — INC and WRITE indirect args
+// are staged in registers (zero-initialised); the kernel keeps one of them.
+enum : int { ST_NONE = 0, ST_REG = 1, ST_SMEM = 2, ST_SEG = 3, ST_GATHER = 4 };
 
 template <class A, int MODE>
 struct Slot {
@@ -160,7 +163,9 @@ struct Slot {
     static constexpr bool is_reduce = is_global && A::mode != MR;
     static constexpr bool is_inc = A::kind == KI && A::mode == MINC;
     static constexpr bool seg = is_inc && MODE == ST_SEG;
-    static constexpr bool staged = (is_inc && MODE != ST_NONE && MODE != ST_SEG) || is_reduce;
+    static constexpr bool is_ind_write = A::kind == KI && A::mode == MW;
+    static constexpr bool staged = (is_inc && MODE != ST_NONE && MODE != ST_SEG) || is_reduce ||
+                                   (is_ind_write && MODE == ST_GATHER);
 
     T acc[staged ? A::dim : 1];
     T bak[is_reduce ? A::dim : 1];
@@ -407,25 +412,27 @@ __device__ __forceinline__ T block_reduce(T v, T *smem_t) {
     return v;   // valid in thread 0
 }
 
-template <class... As>
-struct IncIndex {
-    // position of argument I among the INC-indirect arguments (-1 if not one)
+template <int MM, class... As>
+struct ModeIndex {
+    // position of argument I among the indirect arguments of mode MM (-1 if not one)
     template <size_t I>
     __host__ __device__ static constexpr int of() {
-        constexpr bool inc[] = {(As::kind == KI && As::mode == MINC)...};
-        if (!inc[I]) return -1;
+        constexpr bool in[] = {(As::kind == KI && As::mode == MM)...};
+        if (!in[I]) return -1;
         int p = 0;
-        for (size_t j = 0; j < I; ++j) p += inc[j] ? 1 : 0;
+        for (size_t j = 0; j < I; ++j) p += in[j] ? 1 : 0;
         return p;
     }
     template <size_t I>
     __host__ __device__ static constexpr int first() {
-        constexpr bool inc[] = {(As::kind == KI && As::mode == MINC)...};
+        constexpr bool in[] = {(As::kind == KI && As::mode == MM)...};
         for (size_t j = 0; j < sizeof...(As); ++j)
-            if (inc[j]) return int(j);
+            if (in[j]) return int(j);
         return -1;
     }
 };
+template <class... As>
+using IncIndex = ModeIndex<MINC, As...>;
 
 template <class F, int MODE, class... As>
 struct Engine {
@@ -480,20 +487,27 @@ struct Engine {
     __device__ __forceinline__ static void restore_all(Slots &s, cuda::std::index_sequence<Is...>) {
         (cuda::std::get<Is>(s).restore(), ...);
     }
-    // run += increments of the INC argument at position `a` (gather schedule)
-    template <int DG, class TG, size_t... Is>
-    __device__ __forceinline__ static void add_inc(Slots &s, int a, TG *run,
-                                                   cuda::std::index_sequence<Is...>) {
-        (add_inc_one<Is, DG>(s, a, run), ...);
+    // gather schedule, argument at position `a` among the mode-MM indirect args:
+    // OP 0: run += its increments (INC); 1: its registers = run (WRITE, before
+    // the call: the kernel sees the target's current value); 2: run = its registers
+    template <int MM, int OP, int DG, class TG, size_t... Is>
+    __device__ __forceinline__ static void gather_op(Slots &s, int a, TG *run,
+                                                     cuda::std::index_sequence<Is...>) {
+        (gather_op_one<Is, MM, OP, DG>(s, a, run), ...);
     }
-    template <size_t I, int DG, class TG>
-    __device__ __forceinline__ static void add_inc_one(Slots &s, int a, TG *run) {
+    template <size_t I, int MM, int OP, int DG, class TG>
+    __device__ __forceinline__ static void gather_op_one(Slots &s, int a, TG *run) {
         using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
-        if constexpr (A::kind == KI && A::mode == MINC) {
-            constexpr int pos = IncIndex<As...>::template of<I>();
+        if constexpr (A::kind == KI && A::mode == MM) {
+            constexpr int pos = ModeIndex<MM, As...>::template of<I>();
             if (a == pos) {
+                auto &acc = cuda::std::get<I>(s).acc;
 #pragma unroll
-                for (int c = 0; c < DG; ++c) run[c] += cuda::std::get<I>(s).acc[c];
+                for (int c = 0; c < DG; ++c) {
+                    if constexpr (OP == 0) run[c] += acc[c];
+                    else if constexpr (OP == 1) acc[c] = run[c];
+                    else run[c] = acc[c];
+                }
             }
         }
     }
@@ -688,25 +702,24 @@ __device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
     }
 }
 
-// Target-centric ("gather") schedule for loops whose indirect writes all
-// increment one dat: one thread per target element re-evaluates the kernel for
-// every (element, INC argument) incidence of that target, in serial order, and
-// keeps only that argument's increment — running value starts from the
-// target's current value, so the accumulation order is exactly the reference
-// serial order.  No colours, no shared memory, no atomics, and a target's
-// increments never leave the thread's registers.  Global reductions count
-// each element once (on its first INC argument's incidence).
-template <class T, int D>
-struct GatherAcc {
-    T v[D];
-};
-
+// Target-centric ("gather") schedule for loops whose indirect writes all go to
+// one dat with one mode — INC, or WRITE — and that write no direct argument: one
+// thread per target element re-evaluates the kernel for every (element,
+// argument) incidence of that target, in serial order, and keeps only that
+// argument's effect on a running value that starts from the target's current
+// value: INC adds the increment, WRITE replaces the value (the kernel is handed
+// the running value in that argument, so it sees what the serial order would
+// show it).  The target's final value is therefore exactly the serial one.  No
+// colours, no shared memory, no atomics; a target's running value never leaves
+// the thread's registers.  Global reductions count each element once (on its
+// incidence through the first such argument).
 template <class F, class... As>
 __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_REG, As...>;
-    using II = IncIndex<As...>;
-    constexpr int G = II::template first<0>();
-    static_assert(G >= 0, "gather schedule needs an INC argument");
+    using E = Engine<F, ST_GATHER, As...>;
+    constexpr bool has_inc = ((As::kind == KI && As::mode == MINC) || ...);
+    constexpr int MM = has_inc ? MINC : MW;
+    constexpr int G = ModeIndex<MM, As...>::template first<0>();
+    static_assert(G >= 0, "gather schedule needs an INC or WRITE indirect argument");
     using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
     using TG = typename AG::type;
     constexpr int DG = AG::dim;
@@ -717,7 +730,8 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
     E::init_globals(s, p, idx);
     if (t < p.g_ntargets) {
         const ArgRt &rg = p.a[G];
-        TG *dst = static_cast<TG *>(rg.data) + t * rg.se;
+        const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
+        TG *dst = static_cast<TG *>(rg.data) + tg * rg.se;
         TG run[DG];
 #pragma unroll
         for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
@@ -725,6 +739,7 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
             const int64_t e = __ldg(p.g_elem + k);
             const int a = __ldg(p.g_pos + k);
             E::init_elem(s, p, e, nullptr, idx);
+            if constexpr (MM == MW) E::template gather_op<MW, 1, DG>(s, a, run, idx);
             if constexpr (E::has_reduce) {
                 if (a != 0 || e >= p.rlim) {
                     E::backup_all(s, idx);
@@ -736,7 +751,7 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
             } else {
                 E::call_raw(s, p, idx);
             }
-            E::template add_inc<DG>(s, a, run, idx);
+            E::template gather_op<MM, MM == MINC ? 0 : 2, DG>(s, a, run, idx);
         }
 #pragma unroll
         for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
@@ -846,6 +861,11 @@ struct SigInfo<Sig<As...>> {
     static constexpr bool ind_write = ((As::kind == KI && As::mode != MR) || ...);
     static constexpr bool ind_write_non_inc = ((As::kind == KI && (As::mode == MW || As::mode == MRW)) || ...);
     static constexpr bool direct_write = ((As::kind == KD && As::mode != MR) || ...);
+    static constexpr bool ind_inc = ((As::kind == KI && As::mode == MINC) || ...);
+    static constexpr bool ind_w = ((As::kind == KI && As::mode == MW) || ...);
+    static constexpr bool ind_rw = ((As::kind == KI && As::mode == MRW) || ...);
+    // target-centric schedule: indirect writes of one mode (INC or WRITE), no direct writes
+    static constexpr bool gather_ok = ind_write && !ind_rw && !(ind_inc && ind_w) && !direct_write;
 };
 
 // ---- registry -------------------------------------------------------------------
@@ -860,7 +880,7 @@ struct FunctorEntry {
     LaunchFn direct, staged, phased;
     LaunchFn smem[2], flow[2];                       // [0] colour phases, [1] segmented
     LaunchFn arrive;                                 // segmented, no block colours
-    LaunchFn gather[4];                              // target-centric (INC-only loops):
+    LaunchFn gather[4];                              // target-centric (INC-only or WRITE-only):
                                                      // free / >=2 / >=3 / >=4 CTAs of 256 per SM
     int (*flow_occupancy[2])(int threads, size_t smem);
 };
@@ -940,8 +960,7 @@ struct Registrar {
         e.flow_occupancy[0] = st ? &flow_occupancy<ST_SMEM> : nullptr;
         e.flow_occupancy[1] = st ? &flow_occupancy<ST_SEG> : nullptr;
         e.arrive = st ? &arrive : nullptr;
-        if constexpr (SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc && !SigInfo<S>::direct_write)
-        {
+        if constexpr (SigInfo<S>::gather_ok) {
             e.gather[0] = &gather;
             e.gather[1] = &gather_occ<2>;
             e.gather[2] = &gather_occ<3>;

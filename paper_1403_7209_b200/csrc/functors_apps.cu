@@ -121,6 +121,18 @@ struct ScatterSrc {   // conftest.random_loop_mesh: t[0] += s[0] for each column
     __device__ static void apply(const Consts &, S s, V... v) { ((v[0] += s[0]), ...); }
 };
 
+template <int K>
+struct WriteSrc {   // conflicting indirect WRITEs: column k gets s[0] + k (serial: last writer wins)
+    template <class T, int... I> static auto make(cuda::std::integer_sequence<int, I...>)
+        -> Sig<Arg<KD, MR, 1, T>, decltype((void)I, Arg<KI, MW, 1, T>{})...>;
+    template <class T> using sig = decltype(make<T>(cuda::std::make_integer_sequence<int, K>{}));
+    template <class S, class... V>
+    __device__ static void apply(const Consts &, S s, V... v) {
+        int k = 0;
+        ((v[0] = s[0] + k++), ...);
+    }
+};
+
 struct MixMax {   // test_executor._wide_dat_minmax_case: SOA dim 5, READ/MIN/MAX globals
     template <class T>
     using sig = Sig<Arg<KI, MR, 5, T>, Arg<KI, MR, 5, T>, Arg<KI, MINC, 5, T>, Arg<KI, MINC, 5, T>,
@@ -195,6 +207,10 @@ ML_REGISTER("inc_one_3", IncOne<3>, double);
 ML_REGISTER("scatter_src_1", ScatterSrc<1>, int64_t);
 ML_REGISTER("scatter_src_2", ScatterSrc<2>, int64_t);
 ML_REGISTER("scatter_src_3", ScatterSrc<3>, int64_t);
+ML_REGISTER("write_src_1", WriteSrc<1>, int64_t);
+ML_REGISTER("write_src_2", WriteSrc<2>, int64_t);
+ML_REGISTER("write_src_3", WriteSrc<3>, int64_t);
+ML_REGISTER("write_src_2", WriteSrc<2>, double);
 ML_REGISTER("mixmax", MixMax, int64_t);
 ML_REGISTER("scale_rw", ScaleRW, double);
 ML_REGISTER("set_one", SetOne, double);

@@ -224,6 +224,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         p.g_off = L->gather_off;
         p.g_elem = L->gather_elem;
         p.g_pos = L->gather_pos;
+        p.g_tlist = L->gather_targets;
         nparts = (L->gather_ntargets + 255) / 256;
         if (nparts > pstride)
             ML_FAIL(ML_EINVAL, "loop '%s': gather schedule needs more reduction scratch", L->name);

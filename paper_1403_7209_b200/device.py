@@ -166,41 +166,54 @@ class ScheduleMirror:
 
 
 class GatherMirror:
-    """Device target-centric incidence lists of an INC loop (ml_gather_build)."""
+    """Device target-centric incidence lists (ml_gather_build) of a loop whose
+    indirect writes are all INC, or all WRITE, of one dat.  When fewer than
+    half of the target set's elements have incidences (e.g. boundary loops),
+    the list is compacted to those targets (``targets``)."""
 
-    __slots__ = ("off", "elem", "pos", "ntargets")
+    __slots__ = ("off", "elem", "pos", "ntargets", "targets")
 
     def __init__(self, loop, n: int):
         import ctypes as C
-        inc = [a for a in loop.args if a.kind == "indirect" and a.mode.name == "INC"]
-        self.ntargets = inc[0].dat.set.size
-        cols = [np.ascontiguousarray(a.map.table[:n, a.slot], dtype=np.int64) for a in inc]
+        wr = [a for a in loop.args if a.kind == "indirect" and a.mode.name != "READ"]
+        nset = wr[0].dat.set.size
+        cols = [np.ascontiguousarray(a.map.table[:n, a.slot], dtype=np.int64) for a in wr]
         L = N.lib()
         h = C.c_void_p()
         cptr = (C.c_void_p * len(cols))(*[N.ptr(c) for c in cols])
-        N.check(L.ml_gather_build(n, len(cols), cptr, self.ntargets, C.byref(h)), "ml_gather_build")
+        N.check(L.ml_gather_build(n, len(cols), cptr, nset, C.byref(h)), "ml_gather_build")
         try:
-            off = np.empty(self.ntargets + 1, np.int32)
+            off = np.empty(nset + 1, np.int32)
             elem = np.empty(max(n * len(cols), 1), np.int32)
             pos = np.empty(max(n * len(cols), 1), np.uint8)
             N.check(L.ml_gather_export(h, N.ptr(off), N.ptr(elem), N.ptr(pos)), "ml_gather_export")
         finally:
             L.ml_gather_free(h)
+        deg = np.diff(off)
+        touched = np.flatnonzero(deg)
+        self.targets = None
+        if 2 * touched.size < nset:
+            off = np.concatenate([[0], np.cumsum(deg[touched])]).astype(np.int32)
+            self.targets = _upload(touched.astype(np.int32))
+        self.ntargets = int(off.size - 1)
         self.off, self.elem, self.pos = _upload(off), _upload(elem), _upload(pos)
 
 
 def gather_eligible(loop) -> bool:
-    """Target-centric execution applies when every indirect write is an INC of one
-    dat, no direct argument is written, and the INC dat is not read elsewhere."""
+    """Target-centric execution applies when the loop's indirect writes all go to
+    one dat with one mode — INC, or WRITE — no direct argument is written, and
+    that dat is not accessed in any other way by the loop."""
     ind_w = [a for a in loop.args if a.kind == "indirect" and a.mode.name != "READ"]
-    if not ind_w or any(a.mode.name != "INC" for a in ind_w):
+    if not ind_w or len({a.mode.name for a in ind_w}) != 1:
+        return False
+    if ind_w[0].mode.name not in ("INC", "WRITE"):
         return False
     if len({a.dat.name for a in ind_w}) != 1:
         return False
     if any(a.kind == "direct" and a.mode.name != "READ" for a in loop.args):
         return False
-    name = ind_w[0].dat.name
-    return not any(a.kind != "global" and a.dat.name == name and a.mode.name != "INC"
+    name, mode = ind_w[0].dat.name, ind_w[0].mode.name
+    return not any(a.kind != "global" and a.dat.name == name and a.mode.name != mode
                    for a in loop.args)
 
 

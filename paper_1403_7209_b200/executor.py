@@ -264,6 +264,7 @@ class _LoopEntry:
             L.gather_off = self.gather.off.ptr
             L.gather_elem = self.gather.elem.ptr
             L.gather_pos = self.gather.pos.ptr
+            L.gather_targets = self.gather.targets.ptr if self.gather.targets is not None else None
         self.schedule = None
         if (self.gather is None and config.dataflow and sched in ("flow", "arrival")
                 and self.plan.has_writes and self.plan.ncolors > 1 and not _inc_aliased(loop)):

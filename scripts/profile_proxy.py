@@ -2,7 +2,7 @@
 layout / block-size sweeps).
 
     python scripts/profile_proxy.py [--grid 94] [--iters 3] [--block-size 256 128]
-                                    [--inc-schedule flow arrival colour] [--soa 4]
+                                    [--inc-schedule gather colour flow arrival] [--soa 4]
 """
 import argparse
 import sys
@@ -18,7 +18,7 @@ ap.add_argument("--grid", type=int, default=94)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--block-size", type=int, nargs="+", default=[256])
 ap.add_argument("--soa", type=int, default=4, help="auto-SOA threshold; -1 = all AOS")
-ap.add_argument("--inc-schedule", nargs="+", default=["flow"])
+ap.add_argument("--inc-schedule", nargs="+", default=["gather"])
 ap.add_argument("--no-renumber", action="store_true")
 args = ap.parse_args()
 mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)

@@ -29,6 +29,22 @@ def _inc_kernel(arity: int):
     return kern
 
 
+def _write_kernel(arity: int):
+    @device_kernel(f"write_src_{arity}")
+    def kern(s, *views):
+        for k, v in enumerate(views):
+            v[0] = s[0] + k
+    return kern
+
+
+def write_loop(mesh, map_name="m", src_name="src", dat_name="vals"):
+    """Conflicting indirect WRITEs: serial order decides (last writer wins)."""
+    m = mesh.maps[map_name]
+    args = [ml.arg_direct(mesh.dats[src_name], ml.READ)] + [
+        ml.arg_indirect(mesh.dats[dat_name], m, k + 1, ml.WRITE) for k in range(m.arity)]
+    return ml.Loop("write_conflicts", m.from_set, args, _write_kernel(m.arity))
+
+
 def random_loop_mesh(rng, max_elems=500):
     """reference tests/conftest.py:59-79, same RNG draw order."""
     nt = int(rng.integers(2, max(3, max_elems // 3)))

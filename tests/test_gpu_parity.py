@@ -178,8 +178,8 @@ def test_colouring_stress_hub_and_shuffled_meshes():
         oserial.run_loop(rl)
         want = ref.dats["acc"].fetch()
         for sched in SCHEDULES:
-            mesh.dats["acc"].put(np.zeros_like(want))
             l = _cases.inc_loop(mesh, "edge_nodes")
+            mesh.dats["acc"].put(np.zeros_like(want))
             res = ml.run_program([l], mesh, cfg(inc_schedule=sched))
             np.testing.assert_array_equal(mesh.dats["acc"].fetch(), want, sched)
         assert res.perf[0].nc > 8
@@ -413,3 +413,17 @@ def test_reference_per_loop_entries():
     close(b.dats["acc"].fetch(), ref.dats["acc"].fetch(), what="threads")
     with pytest.raises(ml.ExecError, match="run_hybrid"):
         ml.run_hybrid([], b)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_gather_write_is_serial_last_writer(seed):
+    """Indirect WRITE loops with conflicting writers: the gather schedule keeps the
+    serial order's last writer per target (compacted target list when sparse)."""
+    rng = np.random.default_rng(seed)
+    for max_elems in (50, 5000, 40000):
+        ref, _ = _cases.random_loop_mesh(np.random.default_rng(seed * 7 + max_elems), max_elems)
+        mesh, _ = _cases.random_loop_mesh(np.random.default_rng(seed * 7 + max_elems), max_elems)
+        oserial.run_loop(_cases.write_loop(ref))
+        ml.run_program([_cases.write_loop(mesh)], mesh,
+                       cfg(block_size=int(rng.choice([7, 64, 256]))))
+        np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref.dats["vals"].fetch())

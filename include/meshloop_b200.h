@@ -128,6 +128,9 @@ typedef struct ml_loop {
     const int32_t *gather_targets;  /* device [ntargets] target ids of a compacted
                                        list (only targets with incidences), or
                                        NULL: target k is element k of the set   */
+    void *fold_buf;                 /* fold schedule (needs the gather lists):
+                                       device [n][INC args][dim] increment slots;
+                                       NULL selects the gather schedule          */
 } ml_loop_t;
 
 typedef struct ml_device_info {

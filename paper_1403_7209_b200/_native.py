@@ -79,7 +79,7 @@ class MlLoop(C.Structure):
                 ("staging", MlStagingDev), ("rlim", C.c_int64),
                 ("gather_ntargets", C.c_int64), ("gather_off", C.c_void_p),
                 ("gather_elem", C.c_void_p), ("gather_pos", C.c_void_p),
-                ("gather_targets", C.c_void_p)]
+                ("gather_targets", C.c_void_p), ("fold_buf", C.c_void_p)]
 
 
 class MlDeviceInfo(C.Structure):

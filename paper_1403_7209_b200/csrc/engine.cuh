@@ -117,6 +117,9 @@ struct LaunchParams {
     const int32_t *g_elem;
     const uint8_t *g_pos;
     const int32_t *g_tlist;     // compacted target ids (nullptr: identity)
+    // fold schedule: per (element, INC-arg position) increment slots, element-major
+    void *g_buf;
+    int32_t g_nw;               // INC arguments per element
 };
 
 // strided view of one element's components
@@ -511,6 +514,24 @@ struct Engine {
             }
         }
     }
+    // fold schedule: store each INC argument's register increments into its
+    // (element, position) slot of the element-major increment buffer
+    template <size_t... Is>
+    __device__ __forceinline__ static void store_incs(Slots &s, const LaunchParams &p, int64_t e,
+                                                      cuda::std::index_sequence<Is...>) {
+        (store_inc_one<Is>(s, p, e), ...);
+    }
+    template <size_t I>
+    __device__ __forceinline__ static void store_inc_one(Slots &s, const LaunchParams &p, int64_t e) {
+        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
+        if constexpr (A::kind == KI && A::mode == MINC) {
+            constexpr int pos = IncIndex<As...>::template of<I>();
+            using T = typename A::type;
+            T *dst = static_cast<T *>(p.g_buf) + (e * p.g_nw + pos) * A::dim;
+#pragma unroll
+            for (int c = 0; c < A::dim; ++c) dst[c] = cuda::std::get<I>(s).acc[c];
+        }
+    }
     template <size_t... Is>
     __device__ __forceinline__ static void arrive_sums(Slots &s, const LaunchParams &p, int32_t b,
                                                        char *smem, cuda::std::index_sequence<Is...>) {
@@ -759,6 +780,51 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
 }
 
+// Fold schedule, pass 1 — every element evaluated exactly once, like a direct
+// loop (coalesced direct access, no colours): its INC increments, computed
+// from zero in registers, go to the element's slots of an element-major
+// buffer instead of the targets.  Pass 2 (k_fold_targets) adds each target's
+// slots onto it in serial order.  The increments are the very values the
+// serial run adds (same functor, same zero start), added in the same order,
+// so the result is the serial one bit for bit — with the kernel evaluated
+// once per element instead of once per incidence as in the gather schedule.
+template <class F, class... As>
+__device__ __forceinline__ void run_fold_edges(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_REG, As...>;
+    __shared__ double red[32];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    if (e < p.n) {
+        E::init_elem(s, p, e, nullptr, idx);
+        E::call(s, p, e, idx);
+        E::store_incs(s, p, e, idx);
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
+}
+
+// Fold schedule, pass 2: one thread per target, slots in serial order.
+template <class T, int DG>
+__global__ void __launch_bounds__(256) k_fold_targets(const __grid_constant__ LaunchParams p, int ga) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= p.g_ntargets) return;
+    const ArgRt &rg = p.a[ga];
+    const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
+    T *dst = static_cast<T *>(rg.data) + tg * rg.se;
+    const T *buf = static_cast<const T *>(p.g_buf);
+    T run[DG];
+#pragma unroll
+    for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+    for (int k = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1); k < ke; ++k) {
+        const T *src = buf + (int64_t(__ldg(p.g_elem + k)) * p.g_nw + __ldg(p.g_pos + k)) * DG;
+#pragma unroll
+        for (int c = 0; c < DG; ++c) run[c] += __ldcs(src + c);
+    }
+#pragma unroll
+    for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+}
+
 // Arrival schedule: one launch over the plan blocks in natural order (best
 // locality), no block colours and no inter-block waiting.  Targets touched by
 // one block are updated directly; shared targets are completed by whichever
@@ -835,6 +901,10 @@ __global__ void __launch_bounds__(256) k_flow(const __grid_constant__ LaunchPara
     run_flow<F, MODE>(p, typename F::template sig<T>{});
 }
 template <class F, class T>
+__global__ void __launch_bounds__(256) k_fold_edges(const __grid_constant__ LaunchParams p) {
+    run_fold_edges<F>(p, typename F::template sig<T>{});
+}
+template <class F, class T>
 __global__ void __launch_bounds__(256) k_arrive(const __grid_constant__ LaunchParams p) {
     run_arrive<F>(p, typename F::template sig<T>{});
 }
@@ -866,6 +936,16 @@ struct SigInfo<Sig<As...>> {
     static constexpr bool ind_rw = ((As::kind == KI && As::mode == MRW) || ...);
     // target-centric schedule: indirect writes of one mode (INC or WRITE), no direct writes
     static constexpr bool gather_ok = ind_write && !ind_rw && !(ind_inc && ind_w) && !direct_write;
+    // fold schedule: indirect writes all INC (direct writes allowed)
+    static constexpr bool fold_ok = ind_inc && !ind_rw && !ind_w;
+};
+
+template <class S>
+struct FirstInc;
+template <class... As>
+struct FirstInc<Sig<As...>> {
+    static constexpr int value = IncIndex<As...>::template first<0>() < 0 ? 0 : IncIndex<As...>::template first<0>();
+    using type = cuda::std::tuple_element_t<value, cuda::std::tuple<As...>>;
 };
 
 // ---- registry -------------------------------------------------------------------
@@ -883,6 +963,8 @@ struct FunctorEntry {
     LaunchFn gather[4];                              // target-centric (INC-only or WRITE-only):
                                                      // free / >=2 / >=3 / >=4 CTAs of 256 per SM
     int (*flow_occupancy[2])(int threads, size_t smem);
+    LaunchFn fold_edges, fold_targets;               // fold schedule (INC-only indirect writes)
+    int32_t fold_dim, fold_arg;                      // INC dim, first INC argument
 };
 
 void register_functor(const FunctorEntry &e);
@@ -918,6 +1000,15 @@ struct Registrar {
     }
     static void gather(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_gather<F, T><<<g, b, 0, s>>>(p);
+    }
+    static void fold_edges(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        k_fold_edges<F, T><<<g, b, 0, s>>>(p);
+    }
+    static void fold_targets(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        using S = typename F::template sig<T>;
+        constexpr int G = FirstInc<S>::value;
+        using AG = typename FirstInc<S>::type;
+        k_fold_targets<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, G);
     }
     template <int MINB>
     static void gather_occ(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
@@ -960,6 +1051,12 @@ struct Registrar {
         e.flow_occupancy[0] = st ? &flow_occupancy<ST_SMEM> : nullptr;
         e.flow_occupancy[1] = st ? &flow_occupancy<ST_SEG> : nullptr;
         e.arrive = st ? &arrive : nullptr;
+        if constexpr (SigInfo<S>::fold_ok) {
+            e.fold_edges = &fold_edges;
+            e.fold_targets = &fold_targets;
+            e.fold_arg = FirstInc<S>::value;
+            e.fold_dim = FirstInc<S>::type::dim;
+        }
         if constexpr (SigInfo<S>::gather_ok) {
             e.gather[0] = &gather;
             e.gather[1] = &gather_occ<2>;

@@ -107,7 +107,8 @@ static int validate(const ml_loop_t *L, const FunctorEntry &f) {
 
 static uint64_t scratch_bytes(const ml_loop_t *L, const FunctorEntry &f) {
     uint64_t bytes = 0;
-    const int64_t nb = std::max<int64_t>({L->plan.nblocks, (L->gather_ntargets + 255) / 256, int64_t(1)});
+    const int64_t nb = std::max<int64_t>({L->plan.nblocks, (L->gather_ntargets + 255) / 256,
+                                          (L->n + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i)
         if (f.kind[i] == KG && f.mode[i] != MR) bytes += uint64_t(nb) * f.dim[i] * 8 + 256;
     return bytes;
@@ -136,7 +137,8 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         p.k.i[i] = L->iconst[i];
     }
     char *scratch = static_cast<char *>(L->scratch);
-    const int64_t pstride = std::max<int64_t>({nb, (L->gather_ntargets + 255) / 256, int64_t(1)});
+    const int64_t pstride = std::max<int64_t>({nb, (L->gather_ntargets + 255) / 256,
+                                               (L->n + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i) {
         const ml_arg_t &a = L->args[i];
         ArgRt &r = p.a[i];
@@ -217,7 +219,21 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     }
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
-    if (f.ind_write && f.gather[0] && L->gather_ntargets > 0 && L->gather_off && L->gather_elem &&
+    const bool lists = L->gather_ntargets > 0 && L->gather_off && L->gather_elem && L->gather_pos;
+    if (L->fold_buf && f.fold_edges && lists) {
+        // fold: each element once -> increment slots; then per target, serial order
+        p.g_ntargets = L->gather_ntargets;
+        p.g_off = L->gather_off;
+        p.g_elem = L->gather_elem;
+        p.g_pos = L->gather_pos;
+        p.g_tlist = L->gather_targets;
+        p.g_buf = L->fold_buf;
+        p.g_nw = 0;
+        for (int i = 0; i < f.nargs; ++i) p.g_nw += (f.kind[i] == KI && f.mode[i] == MINC) ? 1 : 0;
+        nparts = (L->n + 255) / 256;
+        f.fold_edges(p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+        f.fold_targets(p, dim3(unsigned((L->gather_ntargets + 255) / 256)), dim3(256), 0, stream);
+    } else if (f.ind_write && f.gather[0] && L->gather_ntargets > 0 && L->gather_off && L->gather_elem &&
         L->gather_pos) {
         // target-centric: one thread per target, serial-order accumulation
         p.g_ntargets = L->gather_ntargets;

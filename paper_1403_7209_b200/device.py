@@ -217,6 +217,20 @@ def gather_eligible(loop) -> bool:
                    for a in loop.args)
 
 
+def fold_eligible(loop) -> bool:
+    """The fold schedule applies when the loop's indirect writes are all INCs of
+    one dat that the loop accesses in no other way (direct writes are fine: each
+    element is evaluated once)."""
+    ind_w = [a for a in loop.args if a.kind == "indirect" and a.mode.name != "READ"]
+    if not ind_w or any(a.mode.name != "INC" for a in ind_w):
+        return False
+    if len({a.dat.name for a in ind_w}) != 1:
+        return False
+    name = ind_w[0].dat.name
+    return not any(a.kind != "global" and a.dat.name == name and a.mode.name != "INC"
+                   for a in loop.args)
+
+
 def gather_mirror(loop, plan) -> GatherMirror:
     cache = plan.__dict__.setdefault("_gathers", {})
     key = loop.signature()

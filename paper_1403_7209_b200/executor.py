@@ -31,7 +31,8 @@ import numpy as np
 
 from . import _native as N
 from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Mesh, MeshError)
-from .device import (dat_mirror, gather_eligible, gather_mirror, map_mirror, plan_mirror,
+from .device import (dat_mirror, fold_eligible, gather_eligible, gather_mirror, map_mirror,
+                     plan_mirror,
                      schedule_mirror, staging_mirror)
 from .kernels import resolve_kernel
 from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
@@ -47,7 +48,7 @@ class ExchangeTimeout(ExecError):
     """A rank waited longer than the configured bound for a halo message."""
 
 
-SCHEDULES = ("gather", "colour", "flow", "arrival")
+SCHEDULES = ("gather", "fold", "colour", "flow", "arrival")
 
 
 @dataclass
@@ -77,7 +78,7 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
-    inc_schedule: str = "gather"            # "gather" | "colour" | "flow" | "arrival"
+    inc_schedule: str = "gather"            # "gather" | "fold" | "colour" | "flow" | "arrival"
     inc_schedule_table: dict | None = None  # per-loop override (tuner.tune_schedule)
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
@@ -101,8 +102,9 @@ class BackendConfig:
                 raise MeshError(f"unknown inc_schedule {sched!r}; expected one of {SCHEDULES}")
 
     def schedule_for(self, loop_name: str) -> str:
-        """The INC schedule of one loop ("gather" falls back to "colour" for
-        loops it does not apply to; "flow"/"arrival" need ``dataflow``)."""
+        """The INC schedule of one loop ("fold" falls back to "gather", "gather"
+        to "colour" for loops they do not apply to; "flow"/"arrival" need
+        ``dataflow``)."""
         if self.inc_schedule_table and loop_name in self.inc_schedule_table:
             return self.inc_schedule_table[loop_name]
         return self.inc_schedule
@@ -256,10 +258,17 @@ class _LoopEntry:
         L.plan.elem_color = pm.ecol.ptr if pm.ecol is not None else None
         L.plan.elem_ncolors = pm.encol.ptr if pm.encol is not None else None
         self.gather = None
+        self.fold = None
         sched = config.schedule_for(loop.name)
         self.sched = sched
-        if sched == "gather" and self.n > 0 and gather_eligible(loop):
+        if sched == "fold" and self.n > 0 and fold_eligible(loop):
             self.gather = gather_mirror(loop, self.plan)
+            inc = [a for a in loop.args if a.kind == "indirect" and a.mode is INC]
+            self.fold = N.DeviceBuffer(self.n * len(inc) * inc[0].dat.dim * inc[0].dat.dtype.itemsize)
+            L.fold_buf = self.fold.ptr
+        elif sched in ("gather", "fold") and self.n > 0 and gather_eligible(loop):
+            self.gather = gather_mirror(loop, self.plan)
+        if self.gather is not None:
             L.gather_ntargets = self.gather.ntargets
             L.gather_off = self.gather.off.ptr
             L.gather_elem = self.gather.elem.ptr
@@ -268,13 +277,13 @@ class _LoopEntry:
         self.schedule = None
         if (self.gather is None and config.dataflow and sched in ("flow", "arrival")
                 and self.plan.has_writes and self.plan.ncolors > 1 and not _inc_aliased(loop)):
-            sched = schedule_mirror(loop, self.plan, _flow_windows(loop, config))
-            if sched.usable:
-                self.schedule = sched
-                L.plan.queue = sched.queue.ptr
-                L.plan.dep_off = sched.dep_off.ptr
-                L.plan.dep_list = sched.dep_list.ptr
-                L.plan.flow_state = sched.flow_state.ptr
+            sm = schedule_mirror(loop, self.plan, _flow_windows(loop, config))
+            if sm.usable:
+                self.schedule = sm
+                L.plan.queue = sm.queue.ptr
+                L.plan.dep_off = sm.dep_off.ptr
+                L.plan.dep_list = sm.dep_list.ptr
+                L.plan.flow_state = sm.flow_state.ptr
         for k, v in enumerate(binding.fconsts[:4]):
             L.fconst[k] = v
         for k, v in enumerate(binding.iconsts[:4]):
@@ -411,7 +420,14 @@ class CompiledProgram:
         for e in self.entries:
             if e.loop.iter_set.size == 0:
                 continue
-            total += e.plan.ncolors if e.plan.has_writes else 1
+            if e.fold is not None:
+                total += 2
+            elif e.gather is not None or not e.plan.has_writes:
+                total += 1
+            elif e.schedule is not None or (e.staging is not None and e.desc.staging.arrive):
+                total += 1
+            else:
+                total += e.plan.ncolors
             total += sum(1 for a in e.loop.args if a.kind == "global" and a.mode.name != "READ")
         return total
 

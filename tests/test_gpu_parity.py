@@ -34,7 +34,7 @@ def close(got, ref, rtol=RTOL, what=""):
     assert not bad.any(), f"{what}: {bad.sum()} mismatches, max |d| {np.max(np.abs(got - ref))}"
 
 
-SCHEDULES = ("gather", "colour", "flow", "arrival")
+SCHEDULES = ("gather", "fold", "colour", "flow", "arrival")
 
 
 def cfg(**kw):
@@ -269,24 +269,25 @@ def test_dataflow_schedule_matches_colour_launches(bs):
         np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
 
 
-@pytest.mark.parametrize("soa", [4, None])
-def test_gather_schedule_reproduces_serial_order_bitwise(soa):
+@pytest.mark.parametrize("soa,sched", [(4, "gather"), (None, "gather"), (4, "fold"),
+                                       (None, "fold")])
+def test_gather_schedule_reproduces_serial_order_bitwise(soa, sched):
     """Target-centric schedule accumulates every target in the reference serial
     order, so even float64 raw INC accumulators equal the oracle bit for bit."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(20, soa=soa)
     bulk.run_program(rprog[:5], resolve_kernel)
-    ml.run_program(prog[:5], mesh, cfg(inc_schedule="gather"))
+    ml.run_program(prog[:5], mesh, cfg(inc_schedule=sched))
     for k in ("grad", "res", "q_old", "dt_loc"):
         np.testing.assert_array_equal(h[k].fetch(), rh[k].fetch(), k)
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, seed=3)
     bulk.run_program(rprog, resolve_kernel)
-    ml.run_program(prog, mesh, cfg(inc_schedule="gather"))
+    ml.run_program(prog, mesh, cfg(inc_schedule=sched))
     close(h["q"].fetch(), rh["q"].fetch(), what="q")
     for app in ("diffusion", "cell-area"):
         g = golden("exec.npz")
         mesh, p, hh = _cases.build_app(app, 8 if app == "diffusion" else 6, "float64",
                                        3 if app == "diffusion" else 0)
-        ml.run_program(p, mesh, cfg(inc_schedule="gather"))
+        ml.run_program(p, mesh, cfg(inc_schedule=sched))
         name = f"{app}_n{8 if app == 'diffusion' else 6}_float64_s{3 if app == 'diffusion' else 0}"
         for k, v in _cases.app_results(app, hh).items():
             close(v, g[f"exec/{name}/{k}"], what=k)
@@ -294,10 +295,10 @@ def test_gather_schedule_reproduces_serial_order_bitwise(soa):
                  lambda: _shuffled_hex(16)):
         ref, mesh = make(), make()
         oserial.run_loop(_cases.inc_loop(ref, "edge_nodes"))
-        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh, cfg(inc_schedule="gather"))
+        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh, cfg(inc_schedule=sched))
         np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
     mesh, loop, acc, lo, hi = _cases.mixmax_case()
-    ml.run_program([loop], mesh, cfg(inc_schedule="gather"))
+    ml.run_program([loop], mesh, cfg(inc_schedule=sched))
     gg = golden("exec.npz")
     np.testing.assert_array_equal(acc.fetch(), gg["exec/mixmax/acc"])
     assert [lo.value, hi.value] == gg["exec/mixmax/lohi"].tolist()

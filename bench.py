@@ -156,7 +156,7 @@ def run_ours(args) -> None:
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(dom.loop.name)
+        traffic = json.loads(tfile.read_text()).get(args.inc_schedule, {}).get(dom.loop.name)
 
     # -- end to end through the public API with host buffers ---------------------------------
     pin_mesh(mesh)

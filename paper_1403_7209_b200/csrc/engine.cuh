@@ -999,9 +999,19 @@ struct Registrar {
         k_flow<F, T, MODE><<<g, b, bytes, s>>>(p);
     }
     static void gather(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        static bool once = false;
+        if (!once) {   // no shared memory to speak of: give the SM's storage to L1
+            cudaFuncSetAttribute(k_gather<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+            once = true;
+        }
         k_gather<F, T><<<g, b, 0, s>>>(p);
     }
     static void fold_edges(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        static bool once = false;
+        if (!once) {
+            cudaFuncSetAttribute(k_fold_edges<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+            once = true;
+        }
         k_fold_edges<F, T><<<g, b, 0, s>>>(p);
     }
     static void fold_targets(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {

@@ -34,6 +34,7 @@
 
 #include <cuda/std/limits>
 #include <cuda/std/tuple>
+#include <cuda/std/type_traits>
 #include <cuda/std/utility>
 
 namespace ml {
@@ -514,20 +515,20 @@ struct Engine {
             }
         }
     }
-    // fold schedule: store each INC argument's register increments into its
-    // (element, position) slot of the element-major increment buffer
-    template <size_t... Is>
-    __device__ __forceinline__ static void store_incs(Slots &s, const LaunchParams &p, int64_t e,
+    // fold schedule: copy each INC argument's register increments into its
+    // (position) slot of this element's shared-memory staging row
+    template <int DGP, size_t... Is>
+    __device__ __forceinline__ static void stage_incs(Slots &s, void *row,
                                                       cuda::std::index_sequence<Is...>) {
-        (store_inc_one<Is>(s, p, e), ...);
+        (stage_inc_one<Is, DGP>(s, row), ...);
     }
-    template <size_t I>
-    __device__ __forceinline__ static void store_inc_one(Slots &s, const LaunchParams &p, int64_t e) {
+    template <size_t I, int DGP>
+    __device__ __forceinline__ static void stage_inc_one(Slots &s, void *row) {
         using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
         if constexpr (A::kind == KI && A::mode == MINC) {
             constexpr int pos = IncIndex<As...>::template of<I>();
             using T = typename A::type;
-            T *dst = static_cast<T *>(p.g_buf) + (e * p.g_nw + pos) * A::dim;
+            T *dst = static_cast<T *>(row) + pos * DGP;
 #pragma unroll
             for (int c = 0; c < A::dim; ++c) dst[c] = cuda::std::get<I>(s).acc[c];
         }
@@ -783,43 +784,91 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
 // Fold schedule, pass 1 — every element evaluated exactly once, like a direct
 // loop (coalesced direct access, no colours): its INC increments, computed
 // from zero in registers, go to the element's slots of an element-major
-// buffer instead of the targets.  Pass 2 (k_fold_targets) adds each target's
-// slots onto it in serial order.  The increments are the very values the
-// serial run adds (same functor, same zero start), added in the same order,
-// so the result is the serial one bit for bit — with the kernel evaluated
-// once per element instead of once per incidence as in the gather schedule.
+// buffer [n][INC args][DGP] (DGP = dim rounded up to 4 doubles, so a slot is
+// whole 32-byte sectors) instead of the targets.  The slots of a CTA's 256
+// elements are one contiguous region: they are staged through shared memory
+// (rows padded by one word against bank conflicts) and stored coalesced.
+// Pass 2 (k_fold_targets) adds each target's slots onto it in serial order.
+// The increments are the very values the serial run adds (same functor, same
+// zero start), added in the same order, so the result is the serial one bit
+// for bit — with the kernel evaluated once per element instead of once per
+// incidence as in the gather schedule.
+template <class T, int DG>
+struct FoldShape {
+    static constexpr int DGP = (DG + 3) / 4 * 4;
+};
+
 template <class F, class... As>
 __device__ __forceinline__ void run_fold_edges(const LaunchParams &p, Sig<As...>) {
     using E = Engine<F, ST_REG, As...>;
+    constexpr int G = IncIndex<As...>::template first<0>();
+    using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
+    using TG = typename AG::type;
+    constexpr int NW = ((As::kind == KI && As::mode == MINC) + ...);
+    constexpr int DGP = FoldShape<TG, AG::dim>::DGP;
+    constexpr int ROW = NW * DGP, SROW = ROW + 1;
     __shared__ double red[32];
+    extern __shared__ __align__(16) char dsm[];
+    TG *st = reinterpret_cast<TG *>(dsm);
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t e0 = int64_t(blockIdx.x) * blockDim.x, e = e0 + threadIdx.x;
     typename E::Slots s;
     E::init_globals(s, p, idx);
     if (e < p.n) {
         E::init_elem(s, p, e, nullptr, idx);
         E::call(s, p, e, idx);
-        E::store_incs(s, p, e, idx);
+        E::template stage_incs<DGP>(s, st + threadIdx.x * SROW, idx);
+    }
+    __syncthreads();
+    const int64_t rows = p.n - e0 < int64_t(blockDim.x) ? p.n - e0 : int64_t(blockDim.x);
+    TG *out = static_cast<TG *>(p.g_buf) + e0 * ROW;
+    for (int k = threadIdx.x; k < rows * ROW; k += blockDim.x) {
+        const int r = k / ROW, c = k - r * ROW;
+        if (c % DGP < AG::dim) __stcg(out + k, st[r * SROW + c]);
     }
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
 }
 
+template <class S>
+struct FoldSmem;
+template <class... As>
+struct FoldSmem<Sig<As...>> {
+    static size_t bytes(int threads) {
+        constexpr int G = IncIndex<As...>::template first<0>() < 0 ? 0 : IncIndex<As...>::template first<0>();
+        using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
+        constexpr int NW = ((As::kind == KI && As::mode == MINC) + ...);
+        constexpr int DGP = FoldShape<typename AG::type, AG::dim>::DGP;
+        return size_t(threads) * (NW * DGP + 1) * sizeof(typename AG::type);
+    }
+};
+
 // Fold schedule, pass 2: one thread per target, slots in serial order.
 template <class T, int DG>
 __global__ void __launch_bounds__(256) k_fold_targets(const __grid_constant__ LaunchParams p, int ga) {
+    constexpr int DGP = FoldShape<T, DG>::DGP;
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= p.g_ntargets) return;
     const ArgRt &rg = p.a[ga];
     const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
     T *dst = static_cast<T *>(rg.data) + tg * rg.se;
     const T *buf = static_cast<const T *>(p.g_buf);
+    const int64_t row = int64_t(p.g_nw) * DGP;
     T run[DG];
 #pragma unroll
     for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
     for (int k = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1); k < ke; ++k) {
-        const T *src = buf + (int64_t(__ldg(p.g_elem + k)) * p.g_nw + __ldg(p.g_pos + k)) * DG;
+        const T *src = buf + int64_t(__ldg(p.g_elem + k)) * row + int(__ldg(p.g_pos + k)) * DGP;
+        if constexpr (DG % 2 == 0 && cuda::std::is_same_v<T, double>) {
 #pragma unroll
-        for (int c = 0; c < DG; ++c) run[c] += __ldcs(src + c);
+            for (int c = 0; c < DG; c += 2) {   // 16-byte loads: slots are 32-byte aligned
+                const double2 v = __ldcs(reinterpret_cast<const double2 *>(src + c));
+                run[c] += v.x;
+                run[c + 1] += v.y;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < DG; ++c) run[c] += __ldcs(src + c);
+        }
     }
 #pragma unroll
     for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
@@ -1007,12 +1056,15 @@ struct Registrar {
         k_gather<F, T><<<g, b, 0, s>>>(p);
     }
     static void fold_edges(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        using S = typename F::template sig<T>;
+        const size_t bytes = FoldSmem<S>::bytes(int(b.x));
         static bool once = false;
         if (!once) {
-            cudaFuncSetAttribute(k_fold_edges<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+            if (bytes > 48 * 1024)
+                cudaFuncSetAttribute(k_fold_edges<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             once = true;
         }
-        k_fold_edges<F, T><<<g, b, 0, s>>>(p);
+        k_fold_edges<F, T><<<g, b, bytes, s>>>(p);
     }
     static void fold_targets(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;

@@ -264,7 +264,8 @@ class _LoopEntry:
         if sched == "fold" and self.n > 0 and fold_eligible(loop):
             self.gather = gather_mirror(loop, self.plan)
             inc = [a for a in loop.args if a.kind == "indirect" and a.mode is INC]
-            self.fold = N.DeviceBuffer(self.n * len(inc) * inc[0].dat.dim * inc[0].dat.dtype.itemsize)
+            dgp = (inc[0].dat.dim + 3) // 4 * 4          # slots padded to 32-byte sectors
+            self.fold = N.DeviceBuffer(self.n * len(inc) * dgp * inc[0].dat.dtype.itemsize)
             L.fold_buf = self.fold.ptr
         elif sched in ("gather", "fold") and self.n > 0 and gather_eligible(loop):
             self.gather = gather_mirror(loop, self.plan)

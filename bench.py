@@ -210,7 +210,8 @@ def main():
     ap.add_argument("--workload", choices=["proxy", "diffusion"], default="proxy")
     ap.add_argument("--grid", type=int, default=None)
     ap.add_argument("--cpu-grid", type=int, default=None)
-    ap.add_argument("--inc-schedule", choices=["gather", "fold", "colour", "flow", "arrival"], default="gather")
+    ap.add_argument("--inc-schedule", choices=["gather", "tile", "fold", "colour", "flow", "arrival"],
+                    default="gather")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.grid is None:

@@ -131,6 +131,22 @@ typedef struct ml_loop {
     void *fold_buf;                 /* fold schedule (needs the gather lists):
                                        device [n][INC args][dim] increment slots;
                                        NULL selects the gather schedule          */
+    /* tile schedule (ml_tile_build export, on the device); tile_count == 0
+     * disables it.  All indirect args must use one map; INC dats must not be
+     * accessed otherwise; no direct writes. */
+    int64_t tile_count;
+    int32_t tile_arity;             /* map arity (loc row length)                */
+    int32_t tile_umax;              /* max staged targets of a tile              */
+    int32_t tile_cmax;              /* max owned targets of a tile               */
+    int32_t tile_pad;
+    const int32_t *tile_list_off;   /* [tile_count+1]                            */
+    const int32_t *tile_nown;       /* [tile_count]                              */
+    const int32_t *tile_list;       /* staged targets, owned first               */
+    const int32_t *tile_elem_off;   /* [tile_count+1]                            */
+    const int32_t *tile_elem;       /* evaluated elements                        */
+    const int32_t *tile_ncol;       /* [tile_count] colours                      */
+    const uint16_t *tile_loc;       /* [elements][arity] local target indices    */
+    const uint8_t *tile_ecol;       /* colour | 0x80 reduction owner             */
 } ml_loop_t;
 
 typedef struct ml_device_info {
@@ -203,6 +219,34 @@ int ml_gather_build(int64_t n, int32_t ncols, const int64_t *const *cols, int64_
                     ml_gather_t **out);
 int ml_gather_export(const ml_gather_t *g, int32_t *off, int32_t *elem, uint8_t *pos);
 int ml_gather_free(ml_gather_t *g);
+
+/* Tile plan of an indirect-increment loop (csrc/host_tile.cpp; the B200
+ * counterpart of OP2's locality blocking — plan.py:55-131 is the reference
+ * plan, which this does not replace).  The target set is cut into compact
+ * tiles; a tile owns its targets, evaluates every element that increments
+ * one of them (elements on the cut are evaluated by both tiles, each keeping
+ * its own targets' increments) and stages its owned + halo targets in shared
+ * memory.  `table` is the loop's map, 0-based row-major [n][arity];
+ * `inc_mask` bit c marks column c as INC-written; `red_col` is the column
+ * whose owner counts the element in global reductions.  A tile satisfies
+ * staged*stage_bytes + owned*own_bytes <= budget and owned <= cmax.  Tiles
+ * come from recursive bisection of the targets along `coords` ([ntargets]
+ * [cdim] row-major, e.g. the mesh's coordinate dat) or, when NULL, along
+ * hop-distance pseudo-coordinates from three far-apart landmarks.
+ * Fails (ML_EINVAL) when one target alone exceeds the budget or a tile needs
+ * more than 127 colours (hub targets): use the gather schedule then.
+ * Export sizes: list_off/elem_off [ntiles+1], nown/ncol [ntiles],
+ * list [nlist], elem/ecol [nelem], loc [nelem*arity]. */
+typedef struct ml_tile ml_tile_t;
+int ml_tile_build(int64_t n, int32_t arity, const int64_t *table, int64_t ntargets,
+                  uint32_t inc_mask, int32_t red_col, int64_t stage_bytes, int64_t own_bytes,
+                  int64_t budget, int32_t cmax, const double *coords, int32_t cdim,
+                  ml_tile_t **out);
+int ml_tile_sizes(const ml_tile_t *t, int64_t *ntiles, int64_t *nlist, int64_t *nelem,
+                  int64_t *umax, int64_t *cmax, int64_t *emax, int32_t *maxcol);
+int ml_tile_export(const ml_tile_t *t, int32_t *list_off, int32_t *nown, int32_t *list,
+                   int32_t *elem_off, int32_t *elem, uint16_t *loc, uint8_t *ecol, int32_t *ncol);
+int ml_tile_free(ml_tile_t *t);
 
 /* Staging lists for shared-memory increment accumulation (derived from the
  * plan's blocking; the plan itself is unchanged).  `col_group[j]` assigns the

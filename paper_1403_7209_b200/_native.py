@@ -31,6 +31,7 @@ EXPORTED = [
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
     "ml_schedule_build", "ml_schedule_export", "ml_schedule_free",
     "ml_gather_build", "ml_gather_export", "ml_gather_free",
+    "ml_tile_build", "ml_tile_sizes", "ml_tile_export", "ml_tile_free",
     "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
     "ml_staging_export_seg", "ml_staging_export_arrival", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
@@ -79,7 +80,13 @@ class MlLoop(C.Structure):
                 ("staging", MlStagingDev), ("rlim", C.c_int64),
                 ("gather_ntargets", C.c_int64), ("gather_off", C.c_void_p),
                 ("gather_elem", C.c_void_p), ("gather_pos", C.c_void_p),
-                ("gather_targets", C.c_void_p), ("fold_buf", C.c_void_p)]
+                ("gather_targets", C.c_void_p), ("fold_buf", C.c_void_p),
+                ("tile_count", C.c_int64), ("tile_arity", C.c_int32), ("tile_umax", C.c_int32),
+                ("tile_cmax", C.c_int32), ("tile_pad", C.c_int32),
+                ("tile_list_off", C.c_void_p), ("tile_nown", C.c_void_p),
+                ("tile_list", C.c_void_p), ("tile_elem_off", C.c_void_p),
+                ("tile_elem", C.c_void_p), ("tile_ncol", C.c_void_p),
+                ("tile_loc", C.c_void_p), ("tile_ecol", C.c_void_p)]
 
 
 class MlDeviceInfo(C.Structure):
@@ -117,6 +124,11 @@ _SIGNATURES = {
     "ml_gather_build": (C.c_int, [C.c_int64, C.c_int32, _PP, C.c_int64, _PP]),
     "ml_gather_export": (C.c_int, [_P, _P, _P, _P]),
     "ml_gather_free": (C.c_int, [_P]),
+    "ml_tile_build": (C.c_int, [C.c_int64, C.c_int32, _P, C.c_int64, C.c_uint32, C.c_int32,
+                                C.c_int64, C.c_int64, C.c_int64, C.c_int32, _P, C.c_int32, _PP]),
+    "ml_tile_sizes": (C.c_int, [_P, _I64P, _I64P, _I64P, _I64P, _I64P, _I64P, _I32P]),
+    "ml_tile_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ml_tile_free": (C.c_int, [_P]),
     "ml_staging_build": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, _PP, _I32P, _PP]),
     "ml_staging_sizes": (C.c_int, [_P, C.c_int32, _I64P, _I64P]),
     "ml_staging_export": (C.c_int, [_P, C.c_int32, _P, _P]),

@@ -96,6 +96,22 @@ struct Staging {
     int32_t foff[MAX_GROUPS];            // byte offset of the finaliser list in dynamic smem
 };
 
+// Tile schedule (csrc/host_tile.cpp): per tile, the staged target list (owned
+// first), the elements it evaluates with their local target indices per map
+// column, element colours (bit 7: reduction owner) and the colour count.
+constexpr int MAX_TGROUPS = 8;
+struct TileParams {
+    const int32_t *list_off, *nown, *list, *elem_off, *elem, *ncol;
+    const uint16_t *loc;
+    const uint8_t *ecol;
+    int32_t arity;
+    int32_t nread, ninc;                 // staged READ dats, accumulated INC dats
+    int32_t garg[MAX_TGROUPS];           // an argument of each group (read groups, then INC)
+    int32_t gdim[MAX_TGROUPS];           // components of each group's dat
+    int8_t grp[MAX_ARGS];                // group of each indirect argument
+    int8_t slot[MAX_ARGS];               // map column of each indirect argument
+};
+
 struct LaunchParams {
     ArgRt a[MAX_ARGS];
     void *part[MAX_ARGS];       // reduction partials [nblocks][dim] per global reduce arg
@@ -121,6 +137,7 @@ struct LaunchParams {
     // fold schedule: per (element, INC-arg position) increment slots, element-major
     void *g_buf;
     int32_t g_nw;               // INC arguments per element
+    TileParams t;
 };
 
 // strided view of one element's components
@@ -158,7 +175,12 @@ __device__ __forceinline__ T combine(T a, T b) {
 // in element order — a deterministic segmented reduction.
 // MODE 4 (ST_GATHER): target-centric schedule — INC and WRITE indirect args
 // are staged in registers (zero-initialised); the kernel keeps one of them.
-enum : int { ST_NONE = 0, ST_REG = 1, ST_SMEM = 2, ST_SEG = 3, ST_GATHER = 4 };
+// MODE 5 (ST_TILE): tile schedule — indirect READ args view the tile's staged
+// copy in shared memory, INC args are staged in registers and added in colour
+// phases to the tile's shared-memory accumulators of owned targets (increments
+// of targets owned by another tile are dropped: that tile evaluates the
+// element too).
+enum : int { ST_NONE = 0, ST_REG = 1, ST_SMEM = 2, ST_SEG = 3, ST_GATHER = 4, ST_TILE = 5 };
 
 template <class A, int MODE>
 struct Slot {
@@ -210,6 +232,32 @@ struct Slot {
             }
         }
     }
+    // tile schedule: `gb` are the group bases in shared memory, U the staged
+    // count (component stride of READ copies), C the owned count
+    __device__ __forceinline__ void init_tile(const LaunchParams &p, int i, int64_t e, const uint16_t *locs,
+                                              char *const *gb, int U, int C) {
+        if constexpr (!is_global) {
+            if constexpr (A::kind == KI) {
+                const int l = locs[p.t.slot[i]];
+                T *base = reinterpret_cast<T *>(gb[p.t.grp[i]]);
+                if constexpr (is_inc) {
+                    ptr = l < C ? base + l : nullptr;
+                    sc = C;
+                } else {
+                    ptr = base + l;
+                    sc = U;
+                }
+            } else {
+                const ArgRt &r = p.a[i];
+                ptr = static_cast<T *>(r.data) + e * r.se;
+                sc = r.sc;
+            }
+            if constexpr (staged) {
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
+            }
+        }
+    }
     __device__ __forceinline__ auto view() {
         if constexpr (staged) {
             return static_cast<T *>(acc);
@@ -221,6 +269,8 @@ struct Slot {
     }
     __device__ __forceinline__ void apply_staged() {
         if constexpr (staged && !is_global) {
+            if constexpr (MODE == ST_TILE)
+                if (!ptr) return;
 #pragma unroll
             for (int c = 0; c < A::dim; ++c) ptr[c * sc] += acc[c];
         }
@@ -452,6 +502,12 @@ struct Engine {
     __device__ __forceinline__ static void init_elem(Slots &s, const LaunchParams &p, int64_t e,
                                                      char *smem, cuda::std::index_sequence<Is...>) {
         (cuda::std::get<Is>(s).init_elem(p, int(Is), e, smem), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void init_tile(Slots &s, const LaunchParams &p, int64_t e,
+                                                     const uint16_t *locs, char *const *gb, int U, int C,
+                                                     cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).init_tile(p, int(Is), e, locs, gb, U, C), ...);
     }
     template <size_t... Is>
     __device__ __forceinline__ static void call_raw(Slots &s, const LaunchParams &p,
@@ -874,6 +930,120 @@ __global__ void __launch_bounds__(256) k_fold_targets(const __grid_constant__ La
     for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
 }
 
+// Tile schedule (see host_tile.cpp): one CTA per tile.
+//  1. stage: the tile's target list, then every READ dat's rows of the staged
+//     targets, copied HBM/L2 -> shared memory with cp.async (8-byte copies,
+//     no registers held, thousands in flight per CTA), component-major
+//     [dim][U]; INC accumulators of the owned targets [dim][C] zeroed;
+//  2. evaluate: the tile's elements in chunks of blockDim; READ args are
+//     shared-memory views, direct args HBM views, INC args registers;
+//  3. apply: element-colour phases add the register increments of owned
+//     targets into the accumulators (elements of one colour share no owned
+//     target), so no atomics and a fixed order — deterministic run to run;
+//  4. write back: one read-modify-write per owned target and component.
+// A target's increments all come from its owning tile, so tiles never
+// conflict: one launch, no block colours, no inter-CTA synchronisation.
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+template <class S>
+struct TileType;
+template <class... As>
+struct TileType<Sig<As...>> {
+    static constexpr int G = IncIndex<As...>::template first<0>() < 0 ? 0 : IncIndex<As...>::template first<0>();
+    using type = typename cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>::type;
+};
+
+__host__ __device__ inline size_t tile_align(size_t x) { return (x + 15) / 16 * 16; }
+
+template <class F, class... As>
+__device__ __forceinline__ void run_tile(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_TILE, As...>;
+    using T = typename TileType<Sig<As...>>::type;
+    __shared__ double red[32];
+    extern __shared__ __align__(16) char dsm[];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const TileParams &tp = p.t;
+    const int32_t t = blockIdx.x;
+    const int32_t l0 = tp.list_off[t], U = tp.list_off[t + 1] - l0, C = tp.nown[t];
+    const int ng = tp.nread + tp.ninc;
+    int32_t *slist = reinterpret_cast<int32_t *>(dsm);
+    char *gb[MAX_TGROUPS];
+    {
+        size_t off = tile_align(size_t(U) * 4);
+#pragma unroll
+        for (int g = 0; g < MAX_TGROUPS; ++g) {
+            if (g >= ng) break;
+            gb[g] = dsm + off;
+            off += tile_align(sizeof(T) * size_t(tp.gdim[g]) * size_t(g < tp.nread ? U : C));
+        }
+    }
+    for (int j = threadIdx.x; j < U; j += blockDim.x) slist[j] = __ldg(tp.list + l0 + j);
+    for (int g = tp.nread; g < ng; ++g) {
+        T *acc = reinterpret_cast<T *>(gb[g]);
+        for (int k = threadIdx.x; k < tp.gdim[g] * C; k += blockDim.x) acc[k] = T(0);
+    }
+    __syncthreads();
+    for (int g = 0; g < tp.nread; ++g) {
+        const ArgRt &r = p.a[tp.garg[g]];
+        const T *src = static_cast<const T *>(r.data);
+        T *dst = reinterpret_cast<T *>(gb[g]);
+        const int dim = tp.gdim[g];
+        for (int c = 0; c < dim; ++c)
+            for (int j = threadIdx.x; j < U; j += blockDim.x)
+                cp_async8(dst + c * U + j, src + int64_t(slist[j]) * r.se + c * r.sc);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    const int32_t k1 = tp.elem_off[t + 1];
+    const int ncol = tp.ncol[t];
+    for (int32_t k0 = tp.elem_off[t]; k0 < k1; k0 += blockDim.x) {
+        const int32_t k = k0 + threadIdx.x;
+        int mine = -1;
+        if (k < k1) {
+            const int64_t e = __ldg(tp.elem + k);
+            const uint8_t fl = __ldg(tp.ecol + k);
+            mine = fl & 127;
+            E::init_tile(s, p, e, tp.loc + int64_t(k) * tp.arity, gb, U, C, idx);
+            if constexpr (E::has_reduce) {
+                if (!(fl & 128) || e >= p.rlim) {
+                    E::backup_all(s, idx);
+                    E::call_raw(s, p, idx);
+                    E::restore_all(s, idx);
+                } else {
+                    E::call_raw(s, p, idx);
+                }
+            } else {
+                E::call_raw(s, p, idx);
+            }
+        }
+        for (int c = 0; c < ncol; ++c) {
+            if (mine == c) E::apply_staged(s, idx);
+            __syncthreads();
+        }
+    }
+    for (int g = tp.nread; g < ng; ++g) {
+        const ArgRt &r = p.a[tp.garg[g]];
+        T *d = static_cast<T *>(r.data);
+        const T *acc = reinterpret_cast<const T *>(gb[g]);
+        const int dim = tp.gdim[g];
+        for (int k = threadIdx.x; k < dim * C; k += blockDim.x) {
+            const int c = k / C, j = k - c * C;
+            const int64_t a = int64_t(slist[j]) * r.se + c * r.sc;
+            d[a] = d[a] + acc[k];
+        }
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, t, red, idx);
+}
+
 // Arrival schedule: one launch over the plan blocks in natural order (best
 // locality), no block colours and no inter-block waiting.  Targets touched by
 // one block are updated directly; shared targets are completed by whichever
@@ -958,6 +1128,10 @@ __global__ void __launch_bounds__(256) k_arrive(const __grid_constant__ LaunchPa
     run_arrive<F>(p, typename F::template sig<T>{});
 }
 template <class F, class T>
+__global__ void __launch_bounds__(256, 2) k_tile(const __grid_constant__ LaunchParams p) {
+    run_tile<F>(p, typename F::template sig<T>{});
+}
+template <class F, class T>
 __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ LaunchParams p) {
     run_gather<F>(p, typename F::template sig<T>{});
 }
@@ -987,6 +1161,9 @@ struct SigInfo<Sig<As...>> {
     static constexpr bool gather_ok = ind_write && !ind_rw && !(ind_inc && ind_w) && !direct_write;
     // fold schedule: indirect writes all INC (direct writes allowed)
     static constexpr bool fold_ok = ind_inc && !ind_rw && !ind_w;
+    // tile schedule: indirect writes all INC, no direct writes (cut elements
+    // are evaluated by two tiles)
+    static constexpr bool tile_ok = ind_inc && !ind_rw && !ind_w && !direct_write;
 };
 
 template <class S>
@@ -1014,6 +1191,7 @@ struct FunctorEntry {
     int (*flow_occupancy[2])(int threads, size_t smem);
     LaunchFn fold_edges, fold_targets;               // fold schedule (INC-only indirect writes)
     int32_t fold_dim, fold_arg;                      // INC dim, first INC argument
+    LaunchFn tile;                                   // tile schedule (INC-only, no direct writes)
 };
 
 void register_functor(const FunctorEntry &e);
@@ -1072,6 +1250,14 @@ struct Registrar {
         using AG = typename FirstInc<S>::type;
         k_fold_targets<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, G);
     }
+    static void tile(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
+        static size_t opted = 48 * 1024;
+        if (bytes > opted) {
+            cudaFuncSetAttribute(k_tile<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+            opted = bytes;
+        }
+        k_tile<F, T><<<g, b, bytes, s>>>(p);
+    }
     template <int MINB>
     static void gather_occ(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_gather_occ<F, T, MINB><<<g, b, 0, s>>>(p);
@@ -1119,6 +1305,7 @@ struct Registrar {
             e.fold_arg = FirstInc<S>::value;
             e.fold_dim = FirstInc<S>::type::dim;
         }
+        if constexpr (SigInfo<S>::tile_ok) e.tile = &tile;
         if constexpr (SigInfo<S>::gather_ok) {
             e.gather[0] = &gather;
             e.gather[1] = &gather_occ<2>;

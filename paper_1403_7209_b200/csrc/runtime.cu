@@ -108,10 +108,68 @@ static int validate(const ml_loop_t *L, const FunctorEntry &f) {
 static uint64_t scratch_bytes(const ml_loop_t *L, const FunctorEntry &f) {
     uint64_t bytes = 0;
     const int64_t nb = std::max<int64_t>({L->plan.nblocks, (L->gather_ntargets + 255) / 256,
-                                          (L->n + 255) / 256, int64_t(1)});
+                                          (L->n + 255) / 256, L->tile_count, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i)
         if (f.kind[i] == KG && f.mode[i] != MR) bytes += uint64_t(nb) * f.dim[i] * 8 + 256;
     return bytes;
+}
+
+// Tile schedule parameters: READ dats staged per tile (one group per distinct
+// dat), INC dats accumulated per owned target; all indirect args on one map.
+static int tile_setup(const ml_loop_t *L, const FunctorEntry &f, LaunchParams &p, size_t &smem) {
+    const char *nm = L->name ? L->name : "?";
+    if (!f.tile) ML_FAIL(ML_EINVAL, "loop '%s': functor '%s' has no tile schedule", nm, f.name);
+    if (!L->tile_list_off || !L->tile_nown || !L->tile_list || !L->tile_elem_off || !L->tile_elem ||
+        !L->tile_ncol || !L->tile_loc || !L->tile_ecol || L->tile_arity < 1)
+        ML_FAIL(ML_EINVAL, "loop '%s': tile plan arrays missing", nm);
+    TileParams &t = p.t;
+    t.list_off = L->tile_list_off;
+    t.nown = L->tile_nown;
+    t.list = L->tile_list;
+    t.elem_off = L->tile_elem_off;
+    t.elem = L->tile_elem;
+    t.ncol = L->tile_ncol;
+    t.loc = L->tile_loc;
+    t.ecol = L->tile_ecol;
+    t.arity = L->tile_arity;
+    const int32_t *map0 = nullptr;
+    const void *gdat[MAX_TGROUPS] = {};
+    int nr = 0, ni = 0;
+    for (int pass = 0; pass < 2; ++pass)             // READ groups first, then INC groups
+        for (int i = 0; i < f.nargs; ++i) {
+            const ml_arg_t &a = L->args[i];
+            if (a.kind != ML_INDIRECT) continue;
+            if (!map0) map0 = a.map;
+            if (a.map != map0) ML_FAIL(ML_EINVAL, "loop '%s': tile schedule needs one map", nm);
+            if (a.slot < 0 || a.slot >= L->tile_arity) ML_FAIL(ML_EINVAL, "loop '%s': bad slot", nm);
+            const bool inc = a.mode == ML_INC;
+            if (inc != (pass == 1)) continue;
+            int g = -1;
+            for (int k = (inc ? nr : 0); k < (inc ? nr + ni : nr); ++k)
+                if (gdat[k] == a.data) g = k;
+            if (g < 0) {
+                g = nr + ni;
+                if (g >= MAX_TGROUPS) ML_FAIL(ML_EINVAL, "loop '%s': too many dats for the tile schedule", nm);
+                gdat[g] = a.data;
+                t.garg[g] = i;
+                t.gdim[g] = a.dim;
+                (inc ? ni : nr)++;
+            }
+            t.grp[i] = int8_t(g);
+            t.slot[i] = int8_t(a.slot);
+        }
+    for (int g = nr; g < nr + ni; ++g)
+        for (int i = 0; i < f.nargs; ++i)
+            if (L->args[i].kind != ML_GLOBAL && L->args[i].mode != ML_INC && L->args[i].data == gdat[g])
+                ML_FAIL(ML_EINVAL, "loop '%s': an INC dat is also accessed otherwise (tile schedule)", nm);
+    t.nread = nr;
+    t.ninc = ni;
+    smem = tile_align(size_t(L->tile_umax) * 4);
+    for (int g = 0; g < nr + ni; ++g)
+        smem += tile_align(size_t(8) * t.gdim[g] * size_t(g < nr ? L->tile_umax : L->tile_cmax));
+    if (smem > 227 * 1024)
+        ML_FAIL(ML_EINVAL, "loop '%s': tile needs %zu bytes of shared memory", nm, smem);
+    return ML_OK;
 }
 
 static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
@@ -138,7 +196,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     }
     char *scratch = static_cast<char *>(L->scratch);
     const int64_t pstride = std::max<int64_t>({nb, (L->gather_ntargets + 255) / 256,
-                                               (L->n + 255) / 256, int64_t(1)});
+                                               (L->n + 255) / 256, L->tile_count, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i) {
         const ml_arg_t &a = L->args[i];
         ArgRt &r = p.a[i];
@@ -220,7 +278,16 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
     const bool lists = L->gather_ntargets > 0 && L->gather_off && L->gather_elem && L->gather_pos;
-    if (L->fold_buf && f.fold_edges && lists) {
+    size_t tile_smem = 0;
+    if (L->tile_count > 0) {
+        rc = tile_setup(L, f, p, tile_smem);
+        if (rc) return rc;
+    }
+    if (L->tile_count > 0) {
+        // tile schedule: one CTA per tile, owner-computes, no inter-CTA conflicts
+        nparts = L->tile_count;
+        f.tile(p, dim3(unsigned(L->tile_count)), dim3(256), tile_smem, stream);
+    } else if (L->fold_buf && f.fold_edges && lists) {
         // fold: each element once -> increment slots; then per target, serial order
         p.g_ntargets = L->gather_ntargets;
         p.g_off = L->gather_off;

@@ -231,6 +231,116 @@ def fold_eligible(loop) -> bool:
                    for a in loop.args)
 
 
+class TileMirror:
+    """Device tile plan (ml_tile_build) of an indirect-increment loop: compact
+    tiles of the INC target set, each owning its targets and staging them plus
+    their halo in shared memory (see csrc/host_tile.cpp)."""
+
+    __slots__ = ("count", "arity", "umax", "cmax", "emax", "maxcol", "list_off", "nown", "list",
+                 "elem_off", "elem", "ncol", "loc", "ecol", "staged_total", "elem_total")
+
+    def __init__(self, loop, n: int, budget: int, cmax: int, coords: np.ndarray | None):
+        h = tile_plan_host(loop, n, budget, cmax, coords)
+        for k in ("count", "arity", "umax", "cmax", "emax", "maxcol"):
+            setattr(self, k, h[k])
+        self.staged_total, self.elem_total = int(h["list"].size), int(h["elem"].size)
+        for k in ("list_off", "nown", "list", "elem_off", "elem", "loc", "ecol", "ncol"):
+            setattr(self, k, _upload(h[k]))
+
+
+def tile_plan_host(loop, n: int, budget: int, cmax: int, coords: np.ndarray | None) -> dict:
+    """Host arrays of the tile plan of ``loop`` over its first ``n`` elements
+    (ml_tile_build; see include/meshloop_b200.h for their meaning)."""
+    import ctypes as C
+    ind = [a for a in loop.args if a.kind == "indirect"]
+    m = ind[0].map
+    table = np.ascontiguousarray(m.table[:n], dtype=np.int64)
+    inc_mask = 0
+    for a in ind:
+        if a.mode.name == "INC":
+            inc_mask |= 1 << a.slot
+    red_col = next(a.slot for a in ind if a.mode.name == "INC")
+    stage = 4 + 8 * sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name != "INC"))
+    own = 8 * sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name == "INC"))
+    L = N.lib()
+    h = C.c_void_p()
+    if coords is not None:
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+    cptr = coords.ctypes.data if coords is not None else None
+    cdim = int(coords.shape[1]) if coords is not None else 0
+    N.check(L.ml_tile_build(n, m.arity, N.ptr(table), m.to_set.size, inc_mask, red_col, stage, own,
+                            int(budget), int(cmax), cptr, cdim, C.byref(h)), "ml_tile_build")
+    try:
+        sz = [C.c_int64() for _ in range(6)]
+        mc = C.c_int32()
+        N.check(L.ml_tile_sizes(h, *[C.byref(x) for x in sz], C.byref(mc)))
+        nt, nl, ne, umax, cm, emax = (x.value for x in sz)
+        out = dict(list_off=np.empty(nt + 1, np.int32), nown=np.empty(nt, np.int32),
+                   list=np.empty(nl, np.int32), elem_off=np.empty(nt + 1, np.int32),
+                   elem=np.empty(ne, np.int32), loc=np.empty(ne * m.arity, np.uint16),
+                   ecol=np.empty(ne, np.uint8), ncol=np.empty(nt, np.int32))
+        N.check(L.ml_tile_export(h, *[N.ptr(out[k]) for k in ("list_off", "nown", "list", "elem_off",
+                                                                "elem", "loc", "ecol", "ncol")]))
+    finally:
+        L.ml_tile_free(h)
+    out.update(count=nt, arity=m.arity, umax=umax, cmax=cm, emax=emax, maxcol=mc.value,
+               inc_mask=inc_mask, red_col=red_col, stage_bytes=stage, own_bytes=own)
+    return out
+
+
+def _distinct(dats):
+    out = []
+    for d in dats:
+        if all(d is not x for x in out):
+            out.append(d)
+    return out
+
+
+def tile_eligible(loop) -> bool:
+    """The tile schedule applies when every indirect argument goes through one
+    map, the indirect writes are all INC, nothing is written directly, the INC
+    dats are accessed in no other way and at most 8 dats are staged."""
+    ind = [a for a in loop.args if a.kind == "indirect"]
+    if not ind or not any(a.mode.name == "INC" for a in ind):
+        return False
+    if any(a.mode.name not in ("READ", "INC") for a in ind):
+        return False
+    if any(a.map is not ind[0].map for a in ind):
+        return False
+    if any(a.kind == "direct" and a.mode.name != "READ" for a in loop.args):
+        return False
+    inc = {a.dat.name for a in ind if a.mode.name == "INC"}
+    if any(a.kind != "global" and a.dat.name in inc and a.mode.name != "INC" for a in loop.args):
+        return False
+    return len(_distinct(a.dat for a in ind)) <= 8
+
+
+def tile_mirror(loop, mesh, n: int, budget: int, cmax: int, coord_dat: str | None) -> TileMirror | None:
+    """Tile plan of ``loop`` (cached on the mesh per map version and budget);
+    None when a target alone exceeds the budget or a tile would need more than
+    127 colours (hub targets) — the gather schedule handles those."""
+    ind = [a for a in loop.args if a.kind == "indirect"]
+    m = ind[0].map
+    coords = None
+    cd = mesh.dats.get(coord_dat) if coord_dat else None
+    if (cd is not None and cd.set is m.to_set and cd.dim in (2, 3)
+            and np.dtype(cd.dtype) == np.float64):
+        coords = np.ascontiguousarray(cd.fetch(), dtype=np.float64)
+    inc_mask = tuple(sorted({a.slot for a in ind if a.mode.name == "INC"}))
+    stage = sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name != "INC"))
+    own = sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name == "INC"))
+    red_col = next(a.slot for a in ind if a.mode.name == "INC")
+    key = (m.name, mesh.version, n, inc_mask, red_col, stage, own, int(budget), int(cmax),
+           coords is not None)
+    cache = mesh.__dict__.setdefault("_ml_tiles", {})
+    if key not in cache:
+        try:
+            cache[key] = TileMirror(loop, n, budget, cmax, coords)
+        except ExecError:
+            cache[key] = None
+    return cache[key]
+
+
 def gather_mirror(loop, plan) -> GatherMirror:
     cache = plan.__dict__.setdefault("_gathers", {})
     key = loop.signature()

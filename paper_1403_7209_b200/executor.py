@@ -32,8 +32,7 @@ import numpy as np
 from . import _native as N
 from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Mesh, MeshError)
 from .device import (dat_mirror, fold_eligible, gather_eligible, gather_mirror, map_mirror,
-                     plan_mirror,
-                     schedule_mirror, staging_mirror)
+                     plan_mirror, schedule_mirror, staging_mirror, tile_eligible, tile_mirror)
 from .kernels import resolve_kernel
 from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
 from .plan import plan_for, plan_stats
@@ -48,7 +47,7 @@ class ExchangeTimeout(ExecError):
     """A rank waited longer than the configured bound for a halo message."""
 
 
-SCHEDULES = ("gather", "fold", "colour", "flow", "arrival")
+SCHEDULES = ("tile", "gather", "fold", "colour", "flow", "arrival")
 
 
 @dataclass
@@ -78,10 +77,12 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
-    inc_schedule: str = "gather"            # "gather" | "fold" | "colour" | "flow" | "arrival"
+    inc_schedule: str = "gather"            # "gather" | "tile" | "fold" | "colour" | "flow" | "arrival"
     inc_schedule_table: dict | None = None  # per-loop override (tuner.tune_schedule)
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
+    tile_smem_kb: int = 100                 # tile schedule: shared memory per tile (2 CTAs/SM)
+    tile_cmax: int = 512                    # tile schedule: max owned targets per tile
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -95,6 +96,8 @@ class BackendConfig:
             raise MeshError(f"unknown partitioner {self.partitioner!r}")
         if self.residency not in ("device", "host"):
             raise MeshError(f"unknown residency {self.residency!r}")
+        if not 8 <= self.tile_smem_kb <= 227 or self.tile_cmax < 1:
+            raise MeshError("tile_smem_kb must be in [8, 227] and tile_cmax positive")
         if self.inc_staging not in ("segmented", "colour"):
             raise MeshError(f"unknown inc_staging {self.inc_staging!r}")
         for sched in [self.inc_schedule, *(self.inc_schedule_table or {}).values()]:
@@ -102,9 +105,9 @@ class BackendConfig:
                 raise MeshError(f"unknown inc_schedule {sched!r}; expected one of {SCHEDULES}")
 
     def schedule_for(self, loop_name: str) -> str:
-        """The INC schedule of one loop ("fold" falls back to "gather", "gather"
-        to "colour" for loops they do not apply to; "flow"/"arrival" need
-        ``dataflow``)."""
+        """The INC schedule of one loop ("tile" and "fold" fall back to "gather",
+        "gather" to "colour" for loops they do not apply to; "flow"/"arrival"
+        need ``dataflow``)."""
         if self.inc_schedule_table and loop_name in self.inc_schedule_table:
             return self.inc_schedule_table[loop_name]
         return self.inc_schedule
@@ -259,9 +262,26 @@ class _LoopEntry:
         L.plan.elem_ncolors = pm.encol.ptr if pm.encol is not None else None
         self.gather = None
         self.fold = None
+        self.tile = None
         sched = config.schedule_for(loop.name)
+        if sched == "tile" and self.n > 0 and tile_eligible(loop):
+            self.tile = tile_mirror(loop, mesh, self.n, config.tile_smem_kb * 1024, config.tile_cmax,
+                                    config.coord_dat)
+            if self.tile is None:
+                sched = "gather"
+        elif sched == "tile":
+            sched = "gather"
         self.sched = sched
-        if sched == "fold" and self.n > 0 and fold_eligible(loop):
+        if self.tile is not None:
+            t = self.tile
+            L.tile_count = t.count
+            L.tile_arity = t.arity
+            L.tile_umax = t.umax
+            L.tile_cmax = t.cmax
+            L.tile_list_off, L.tile_nown, L.tile_list = t.list_off.ptr, t.nown.ptr, t.list.ptr
+            L.tile_elem_off, L.tile_elem, L.tile_ncol = t.elem_off.ptr, t.elem.ptr, t.ncol.ptr
+            L.tile_loc, L.tile_ecol = t.loc.ptr, t.ecol.ptr
+        elif sched == "fold" and self.n > 0 and fold_eligible(loop):
             self.gather = gather_mirror(loop, self.plan)
             inc = [a for a in loop.args if a.kind == "indirect" and a.mode is INC]
             dgp = (inc[0].dat.dim + 3) // 4 * 4          # slots padded to 32-byte sectors
@@ -291,7 +311,8 @@ class _LoopEntry:
             L.iconst[k] = v
         L.rlim = int(rlim[sname]) if rlim and sname in rlim else -1
         self.staging = (staging_mirror(loop, self.plan)
-                        if config.smem_staging and self.gather is None else None)
+                        if config.smem_staging and self.gather is None and self.tile is None
+                        else None)
         if self.staging is not None:
             sg = self.staging
             L.staging.ngroups = sg.ngroups
@@ -423,6 +444,8 @@ class CompiledProgram:
                 continue
             if e.fold is not None:
                 total += 2
+            elif e.tile is not None:
+                total += 1
             elif e.gather is not None or not e.plan.has_writes:
                 total += 1
             elif e.schedule is not None or (e.staging is not None and e.desc.staging.arrive):
@@ -455,7 +478,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
            tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
            config.dataflow, config.inc_staging, config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.flow_windows,
-           config.flow_window_l2_fraction,
+           config.flow_window_l2_fraction, config.tile_smem_kb, config.tile_cmax, config.coord_dat,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

@@ -20,20 +20,26 @@ ap.add_argument("--block-size", type=int, nargs="+", default=[256])
 ap.add_argument("--soa", type=int, default=4, help="auto-SOA threshold; -1 = all AOS")
 ap.add_argument("--inc-schedule", nargs="+", default=["gather"])
 ap.add_argument("--no-renumber", action="store_true")
+ap.add_argument("--tile-smem", type=int, nargs="+", default=[100])
+ap.add_argument("--tile-cmax", type=int, default=512)
 args = ap.parse_args()
 mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)
 apps.shuffle_mesh(mesh, seed=1)
 prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
 if not args.no_renumber:
     ml.renumber_mesh(mesh)
-for bs in args.block_size:
+import itertools
+for bs, kb in itertools.product(args.block_size, args.tile_smem):
     for sched in args.inc_schedule:
-        cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched)
+        if sched != "tile" and kb != args.tile_smem[0]:
+            continue
+        cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched, tile_smem_kb=kb,
+                               tile_cmax=args.tile_cmax)
         for i in range(args.iters):
             r = ml.run_program(prog, mesh, cfg)
             if i + 1 < args.iters:
                 continue
             tot = sum(p.time_sec for p in r.perf)
-            print(f"[{sched} bs={bs} soa={args.soa}] total={tot*1e3:.3f}ms " +
+            print(f"[{sched} bs={bs} soa={args.soa} tile_kb={kb}] total={tot*1e3:.3f}ms " +
                   " ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf),
                   flush=True)

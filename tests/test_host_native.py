@@ -372,3 +372,78 @@ def test_staging_lists_resolve_every_increment(rng):
             assert np.all([cols[a][e] == lst[u] for a, e in zip(args, elems)])
             assert np.all(np.diff(elems.astype(np.int64) * 8 + args) > 0)
         N.lib().ml_staging_free(h)
+
+
+def _check_tile_plan(h, table, n, inc_cols, red_col, budget, cmax):
+    """Invariants of a tile plan (csrc/host_tile.cpp): every INC incidence is
+    evaluated by exactly the tile owning its target, staged lists resolve every
+    map entry of every evaluated element, colours separate elements sharing an
+    owned target, every element has exactly one reduction owner, budgets hold."""
+    table = np.asarray(table[:n], dtype=np.int64)
+    owner = np.full(int(table.max(initial=-1)) + 1, -1)
+    red_count = np.zeros(n, np.int64)
+    evaluated = set()
+    for t in range(h["count"]):
+        lst = h["list"][h["list_off"][t]:h["list_off"][t + 1]]
+        c = int(h["nown"][t])
+        own, halo = lst[:c], lst[c:]
+        assert np.all(np.diff(own) > 0) and np.all(np.diff(halo) > 0)
+        assert not set(own.tolist()) & set(halo.tolist())
+        assert np.all(owner[own] < 0)
+        owner[own] = t
+        assert c <= cmax and lst.size * h["stage_bytes"] + c * h["own_bytes"] <= budget
+        k0, k1 = h["elem_off"][t], h["elem_off"][t + 1]
+        el = h["elem"][k0:k1]
+        assert np.all(np.diff(el) > 0)
+        loc = h["loc"][k0 * h["arity"]:k1 * h["arity"]].reshape(-1, h["arity"])
+        np.testing.assert_array_equal(lst[loc], table[el])
+        col = h["ecol"][k0:k1] & 127
+        assert col.size == 0 or col.max() < h["ncol"][t]
+        seen = {}
+        for i, e in enumerate(el.tolist()):
+            for j in inc_cols:
+                if loc[i, j] < c:
+                    key = (int(loc[i, j]), int(col[i]))
+                    assert seen.get(key, e) == e, "two elements of one colour share an owned target"
+                    seen[key] = e
+            evaluated.add((t, e))
+        red_count[el[(h["ecol"][k0:k1] & 128) > 0]] += 1
+    for e in range(n):
+        for j in inc_cols:
+            assert (owner[table[e, j]], e) in evaluated
+    assert np.all(red_count == 1)
+    for e in range(n):
+        assert (owner[table[e, red_col]], e) in evaluated
+
+
+def test_tile_plan_invariants_fuzz(rng):
+    from paper_1403_7209_b200.device import tile_plan_host
+    for trial in range(30):
+        mesh, loop = _cases.random_loop_mesh(rng, max_elems=400)
+        m = mesh.maps["m"]
+        n = m.from_set.size
+        budget = int(rng.choice([200, 600, 4000]))
+        cmax = int(rng.choice([1, 3, 16, 512]))
+        try:
+            h = tile_plan_host(loop, n, budget, cmax, None)
+        except ml.ExecError as ex:               # a hub target alone over budget / > 127 colours
+            assert "budget" in str(ex) or "colours" in str(ex)
+            continue
+        _check_tile_plan(h, m.table, n, list(range(m.arity)), 0, budget, cmax)
+
+
+def test_tile_plan_invariants_proxy_mesh_with_coords():
+    from paper_1403_7209_b200.device import tile_plan_host
+    mesh = apps.gen_hex_mesh(7, seed=2)
+    apps.shuffle_mesh(mesh, seed=3)
+    prog, _ = apps.build_hydra_proxy(mesh, steps=1, seed=0)
+    ml.renumber_mesh(mesh)
+    loop = next(l for l in prog if l.name == "vflux")
+    m = mesh.maps["edge_nodes"]
+    coords = mesh.dats["coords"].fetch()
+    for c in (coords, None):
+        h = tile_plan_host(loop, m.from_set.size, 20_000, 64, c)
+        assert h["count"] > 1
+        _check_tile_plan(h, m.table, m.from_set.size, [0, 1], 0, 20_000, 64)
+    with pytest.raises(ml.ExecError, match="budget"):
+        tile_plan_host(loop, m.from_set.size, 500, 64, None)

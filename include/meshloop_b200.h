@@ -138,7 +138,7 @@ typedef struct ml_loop {
     int32_t tile_arity;             /* map arity (loc row length)                */
     int32_t tile_umax;              /* max staged targets of a tile              */
     int32_t tile_cmax;              /* max owned targets of a tile               */
-    int32_t tile_pad;
+    int32_t tile_threads;           /* CTA size: 256 (2 CTAs/SM) or 128 (4/SM)   */
     const int32_t *tile_list_off;   /* [tile_count+1]                            */
     const int32_t *tile_nown;       /* [tile_count]                              */
     const int32_t *tile_list;       /* staged targets, owned first               */

@@ -22,7 +22,7 @@ BUILD = ROOT / "build"
 LIB = PKG / "libmeshloop_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC,-fopenmp",
-          f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+          f"-I{ROOT / 'include'}", f"-I{CSRC}", *os.environ.get("MESHLOOP_NVCC_FLAGS", "").split()]
 
 
 def _nvcc() -> str:

@@ -82,7 +82,7 @@ class MlLoop(C.Structure):
                 ("gather_elem", C.c_void_p), ("gather_pos", C.c_void_p),
                 ("gather_targets", C.c_void_p), ("fold_buf", C.c_void_p),
                 ("tile_count", C.c_int64), ("tile_arity", C.c_int32), ("tile_umax", C.c_int32),
-                ("tile_cmax", C.c_int32), ("tile_pad", C.c_int32),
+                ("tile_cmax", C.c_int32), ("tile_threads", C.c_int32),
                 ("tile_list_off", C.c_void_p), ("tile_nown", C.c_void_p),
                 ("tile_list", C.c_void_p), ("tile_elem_off", C.c_void_p),
                 ("tile_elem", C.c_void_p), ("tile_ncol", C.c_void_p),

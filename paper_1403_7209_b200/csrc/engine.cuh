@@ -232,6 +232,8 @@ struct Slot {
             }
         }
     }
+    // gather schedule with CTA-local staging: READ args whose target lies in
+    // the CTA's range [t0, t0 + blockDim) read the staged copy
     // tile schedule: `gb` are the group bases in shared memory, U the staged
     // count (component stride of READ copies), C the owned count
     __device__ __forceinline__ void init_tile(const LaunchParams &p, int i, int64_t e, const uint16_t *locs,
@@ -271,8 +273,13 @@ struct Slot {
         if constexpr (staged && !is_global) {
             if constexpr (MODE == ST_TILE)
                 if (!ptr) return;
+            // the components are distinct addresses: issue every load before
+            // the first store so the read-modify-writes overlap
+            T old[A::dim];
 #pragma unroll
-            for (int c = 0; c < A::dim; ++c) ptr[c * sc] += acc[c];
+            for (int c = 0; c < A::dim; ++c) old[c] = ptr[c * sc];
+#pragma unroll
+            for (int c = 0; c < A::dim; ++c) ptr[c * sc] = old[c] + acc[c];
         }
     }
     __device__ __forceinline__ void backup() {
@@ -972,34 +979,45 @@ __device__ __forceinline__ void run_tile(const LaunchParams &p, Sig<As...>) {
     const int32_t t = blockIdx.x;
     const int32_t l0 = tp.list_off[t], U = tp.list_off[t + 1] - l0, C = tp.nown[t];
     const int ng = tp.nread + tp.ninc;
+#ifdef ML_TILE_PROFILE
+    long long tk0 = clock64(), tk1 = 0, tk2 = 0, tk3 = 0, tk4 = 0;
+#endif
     int32_t *slist = reinterpret_cast<int32_t *>(dsm);
-    char *gb[MAX_TGROUPS];
-    {
+    __shared__ char *gb[MAX_TGROUPS];        // group bases (shared: indexed at run time)
+    if (threadIdx.x == 0) {
         size_t off = tile_align(size_t(U) * 4);
-#pragma unroll
-        for (int g = 0; g < MAX_TGROUPS; ++g) {
-            if (g >= ng) break;
+        for (int g = 0; g < ng; ++g) {
             gb[g] = dsm + off;
             off += tile_align(sizeof(T) * size_t(tp.gdim[g]) * size_t(g < tp.nread ? U : C));
         }
     }
-    for (int j = threadIdx.x; j < U; j += blockDim.x) slist[j] = __ldg(tp.list + l0 + j);
+    __syncthreads();
     for (int g = tp.nread; g < ng; ++g) {
         T *acc = reinterpret_cast<T *>(gb[g]);
         for (int k = threadIdx.x; k < tp.gdim[g] * C; k += blockDim.x) acc[k] = T(0);
     }
-    __syncthreads();
-    for (int g = 0; g < tp.nread; ++g) {
-        const ArgRt &r = p.a[tp.garg[g]];
-        const T *src = static_cast<const T *>(r.data);
-        T *dst = reinterpret_cast<T *>(gb[g]);
-        const int dim = tp.gdim[g];
-        for (int c = 0; c < dim; ++c)
-            for (int j = threadIdx.x; j < U; j += blockDim.x)
-                cp_async8(dst + c * U + j, src + int64_t(slist[j]) * r.se + c * r.sc);
+    // one staged target per thread and pass: its id is loaded once, then every
+    // component of every READ dat is copied (lanes = consecutive list entries)
+    for (int j = threadIdx.x; j < U; j += blockDim.x) {
+        const int64_t v = __ldg(tp.list + l0 + j);
+        slist[j] = int32_t(v);
+        for (int g = 0; g < tp.nread; ++g) {
+            const ArgRt &r = p.a[tp.garg[g]];
+            const T *src = static_cast<const T *>(r.data) + v * r.se;
+            T *dst = reinterpret_cast<T *>(gb[g]) + j;
+            const int dim = tp.gdim[g];
+#pragma unroll 4
+            for (int c = 0; c < dim; ++c) cp_async8(dst + c * U, src + c * r.sc);
+        }
     }
+#ifdef ML_TILE_PROFILE
+    tk1 = clock64();
+#endif
     cp_async_wait_all();
     __syncthreads();
+#ifdef ML_TILE_PROFILE
+    tk2 = clock64();
+#endif
 
     typename E::Slots s;
     E::init_globals(s, p, idx);
@@ -1030,17 +1048,41 @@ __device__ __forceinline__ void run_tile(const LaunchParams &p, Sig<As...>) {
             __syncthreads();
         }
     }
+#ifdef ML_TILE_PROFILE
+    tk3 = clock64();
+#endif
+    // write back: 4 independent read-modify-writes in flight per thread
     for (int g = tp.nread; g < ng; ++g) {
         const ArgRt &r = p.a[tp.garg[g]];
         T *d = static_cast<T *>(r.data);
         const T *acc = reinterpret_cast<const T *>(gb[g]);
-        const int dim = tp.gdim[g];
-        for (int k = threadIdx.x; k < dim * C; k += blockDim.x) {
-            const int c = k / C, j = k - c * C;
-            const int64_t a = int64_t(slist[j]) * r.se + c * r.sc;
-            d[a] = d[a] + acc[k];
+        const int total = tp.gdim[g] * C;
+        constexpr int UN = 4;
+        for (int k0 = threadIdx.x; k0 < total; k0 += UN * blockDim.x) {
+            int64_t a[UN];
+            T v[UN];
+#pragma unroll
+            for (int q = 0; q < UN; ++q) {
+                const int k = k0 + q * blockDim.x;
+                if (k < total) {
+                    const int c = k / C, j = k - c * C;
+                    a[q] = int64_t(slist[j]) * r.se + c * r.sc;
+                    v[q] = d[a[q]];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UN; ++q)
+                if (k0 + q * blockDim.x < total) d[a[q]] = v[q] + acc[k0 + q * blockDim.x];
         }
     }
+#ifdef ML_TILE_PROFILE
+    __syncthreads();
+    tk4 = clock64();
+    if (threadIdx.x == 0 && p.g_buf) {
+        long long *o = static_cast<long long *>(p.g_buf) + int64_t(t) * 4;
+        o[0] = tk1 - tk0; o[1] = tk2 - tk1; o[2] = tk3 - tk2; o[3] = tk4 - tk3;
+    }
+#endif
     if constexpr (E::has_reduce) E::reduce_all(s, p, t, red, idx);
 }
 
@@ -1127,8 +1169,8 @@ template <class F, class T>
 __global__ void __launch_bounds__(256) k_arrive(const __grid_constant__ LaunchParams p) {
     run_arrive<F>(p, typename F::template sig<T>{});
 }
-template <class F, class T>
-__global__ void __launch_bounds__(256, 2) k_tile(const __grid_constant__ LaunchParams p) {
+template <class F, class T, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_tile(const __grid_constant__ LaunchParams p) {
     run_tile<F>(p, typename F::template sig<T>{});
 }
 template <class F, class T>
@@ -1250,13 +1292,18 @@ struct Registrar {
         using AG = typename FirstInc<S>::type;
         k_fold_targets<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, G);
     }
-    static void tile(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
+    template <int NT>
+    static void tile_launch(const LaunchParams &p, dim3 g, size_t bytes, cudaStream_t s) {
         static size_t opted = 48 * 1024;
         if (bytes > opted) {
-            cudaFuncSetAttribute(k_tile<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+            cudaFuncSetAttribute(k_tile<F, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
             opted = bytes;
         }
-        k_tile<F, T><<<g, b, bytes, s>>>(p);
+        k_tile<F, T, NT><<<g, NT, bytes, s>>>(p);
+    }
+    static void tile(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
+        if (b.x == 128) tile_launch<128>(p, g, bytes, s);
+        else tile_launch<256>(p, g, bytes, s);
     }
     template <int MINB>
     static void gather_occ(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {

@@ -286,7 +286,8 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     if (L->tile_count > 0) {
         // tile schedule: one CTA per tile, owner-computes, no inter-CTA conflicts
         nparts = L->tile_count;
-        f.tile(p, dim3(unsigned(L->tile_count)), dim3(256), tile_smem, stream);
+        p.g_buf = L->fold_buf;   // per-tile phase timings when built with ML_TILE_PROFILE
+        f.tile(p, dim3(unsigned(L->tile_count)), dim3(L->tile_threads == 128 ? 128 : 256), tile_smem, stream);
     } else if (L->fold_buf && f.fold_edges && lists) {
         // fold: each element once -> increment slots; then per target, serial order
         p.g_ntargets = L->gather_ntargets;

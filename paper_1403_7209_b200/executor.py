@@ -83,6 +83,7 @@ class BackendConfig:
     flow_window_l2_fraction: float = 0.5
     tile_smem_kb: int = 100                 # tile schedule: shared memory per tile (2 CTAs/SM)
     tile_cmax: int = 512                    # tile schedule: max owned targets per tile
+    tile_threads: int = 256                 # tile schedule: CTA size (256: 2 CTAs/SM, 128: 4)
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -96,8 +97,8 @@ class BackendConfig:
             raise MeshError(f"unknown partitioner {self.partitioner!r}")
         if self.residency not in ("device", "host"):
             raise MeshError(f"unknown residency {self.residency!r}")
-        if not 8 <= self.tile_smem_kb <= 227 or self.tile_cmax < 1:
-            raise MeshError("tile_smem_kb must be in [8, 227] and tile_cmax positive")
+        if not 8 <= self.tile_smem_kb <= 227 or self.tile_cmax < 1 or self.tile_threads not in (128, 256):
+            raise MeshError("tile_smem_kb must be in [8, 227], tile_cmax positive, tile_threads 128|256")
         if self.inc_staging not in ("segmented", "colour"):
             raise MeshError(f"unknown inc_staging {self.inc_staging!r}")
         for sched in [self.inc_schedule, *(self.inc_schedule_table or {}).values()]:
@@ -278,6 +279,7 @@ class _LoopEntry:
             L.tile_arity = t.arity
             L.tile_umax = t.umax
             L.tile_cmax = t.cmax
+            L.tile_threads = config.tile_threads
             L.tile_list_off, L.tile_nown, L.tile_list = t.list_off.ptr, t.nown.ptr, t.list.ptr
             L.tile_elem_off, L.tile_elem, L.tile_ncol = t.elem_off.ptr, t.elem.ptr, t.ncol.ptr
             L.tile_loc, L.tile_ecol = t.loc.ptr, t.ecol.ptr
@@ -478,7 +480,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
            tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
            config.dataflow, config.inc_staging, config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.flow_windows,
-           config.flow_window_l2_fraction, config.tile_smem_kb, config.tile_cmax, config.coord_dat,
+           config.flow_window_l2_fraction, config.tile_smem_kb, config.tile_cmax, config.tile_threads, config.coord_dat,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

@@ -20,26 +20,52 @@ ap.add_argument("--block-size", type=int, nargs="+", default=[256])
 ap.add_argument("--soa", type=int, default=4, help="auto-SOA threshold; -1 = all AOS")
 ap.add_argument("--inc-schedule", nargs="+", default=["gather"])
 ap.add_argument("--no-renumber", action="store_true")
+ap.add_argument("--kd", type=int, default=0, help="k-d leaf size: renumber nodes in k-d order after CM")
 ap.add_argument("--tile-smem", type=int, nargs="+", default=[100])
 ap.add_argument("--tile-cmax", type=int, default=512)
+ap.add_argument("--tile-threads", type=int, nargs="+", default=[256])
+
 args = ap.parse_args()
 mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)
 apps.shuffle_mesh(mesh, seed=1)
 prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
 if not args.no_renumber:
     ml.renumber_mesh(mesh)
+if args.kd:
+    import numpy as np
+    from paper_1403_7209_b200.renumber import Permutation, apply_permutation, row_order_by_targets, _forward
+
+    def kd_order(xyz, leaf):
+        out, stack = [], [np.arange(len(xyz))]
+        while stack:
+            a = stack.pop()
+            if len(a) <= leaf:
+                out.append(np.sort(a))
+                continue
+            p = xyz[a]
+            ax = int(np.argmax(p.max(0) - p.min(0)))
+            o = np.lexsort((a, p[:, ax]))
+            m = (len(a) + 1) // 2
+            stack.append(a[o[m:]])
+            stack.append(a[o[:m]])
+        return np.concatenate(out)
+    order = kd_order(mesh.dats["coords"].fetch(), args.kd)
+    apply_permutation(mesh, Permutation("nodes", _forward(order), order, mesh.version))
+    for sname in ("edges", "bedges"):
+        m = next(m for m in mesh.maps.values() if m.from_set.name == sname)
+        apply_permutation(mesh, row_order_by_targets(mesh, m))
 import itertools
-for bs, kb in itertools.product(args.block_size, args.tile_smem):
+for bs, kb, nt in itertools.product(args.block_size, args.tile_smem, args.tile_threads):
     for sched in args.inc_schedule:
-        if sched != "tile" and kb != args.tile_smem[0]:
+        if sched != "tile" and (kb != args.tile_smem[0] or nt != args.tile_threads[0]):
             continue
         cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched, tile_smem_kb=kb,
-                               tile_cmax=args.tile_cmax)
+                               tile_cmax=args.tile_cmax, tile_threads=nt)
         for i in range(args.iters):
             r = ml.run_program(prog, mesh, cfg)
             if i + 1 < args.iters:
                 continue
             tot = sum(p.time_sec for p in r.perf)
-            print(f"[{sched} bs={bs} soa={args.soa} tile_kb={kb}] total={tot*1e3:.3f}ms " +
+            print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} tile_kb={kb} nt={nt}] total={tot*1e3:.3f}ms " +
                   " ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf),
                   flush=True)

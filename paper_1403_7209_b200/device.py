@@ -171,7 +171,7 @@ class GatherMirror:
     half of the target set's elements have incidences (e.g. boundary loops),
     the list is compacted to those targets (``targets``)."""
 
-    __slots__ = ("off", "elem", "pos", "ntargets", "targets")
+    __slots__ = ("off", "elem", "pos", "ntargets", "targets", "host")
 
     def __init__(self, loop, n: int):
         import ctypes as C
@@ -192,11 +192,30 @@ class GatherMirror:
         deg = np.diff(off)
         touched = np.flatnonzero(deg)
         self.targets = None
+        tl = None
         if 2 * touched.size < nset:
             off = np.concatenate([[0], np.cumsum(deg[touched])]).astype(np.int32)
-            self.targets = _upload(touched.astype(np.int32))
+            tl = touched.astype(np.int32)
+            self.targets = _upload(tl)
         self.ntargets = int(off.size - 1)
         self.off, self.elem, self.pos = _upload(off), _upload(elem), _upload(pos)
+        # host copies: target subsets (multi-GPU core/boundary split) are cut from them
+        self.host = {"off": off, "elem": elem, "pos": pos,
+                     "targets": tl if tl is not None else np.arange(self.ntargets, dtype=np.int32)}
+
+    def subset(self, targets_idx: np.ndarray) -> dict:
+        """Device lists of a subset of this list's targets (positions into it, ascending)."""
+        h = self.host
+        off = h["off"]
+        deg = (off[targets_idx + 1] - off[targets_idx]).astype(np.int64)
+        starts = off[targets_idx].astype(np.int64)
+        new_off = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+        take = (np.repeat(starts - new_off[:-1], deg) + np.arange(int(deg.sum()))).astype(np.int64)
+        return {"ntargets": int(targets_idx.size), "off": _upload(new_off),
+                "elem": _upload(np.ascontiguousarray(h["elem"][take])),
+                "pos": _upload(np.ascontiguousarray(h["pos"][take])),
+                "targets": _upload(np.ascontiguousarray(h["targets"][targets_idx], dtype=np.int32)),
+                "elem_host": h["elem"][take]}
 
 
 def gather_eligible(loop) -> bool:

@@ -26,9 +26,10 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, executor="stream"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                      WORLD_SIZE=str(world), LOCAL_RANK="0", ML_TRANSPORT="gloo")
+                      WORLD_SIZE=str(world), LOCAL_RANK="0", ML_TRANSPORT="gloo",
+                      ML_RANK_EXECUTOR=executor)
     sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -58,12 +59,13 @@ def _worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
-def _run(case, world=2):
+def _run(case, world=2, executor="stream"):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, executor))
+             for r in range(world)]
     for p in procs:
         p.start()
     outs = [q.get(timeout=600) for _ in range(world)]
@@ -75,19 +77,21 @@ def _run(case, world=2):
     return sorted(outs, key=lambda x: x[0])
 
 
-@pytest.mark.parametrize("world,part,sched", [(2, "rcb", "flow"), (3, "trivial", "arrival"),
-                                              (2, "trivial", "colour")])
-def test_ranks_on_device_match_reference_int64(world, part, sched):
+@pytest.mark.parametrize("world,part,sched,executor", [
+    (2, "rcb", "gather", "stream"), (3, "trivial", "gather", "stream"), (2, "rcb", "flow", "stream"),
+    (3, "trivial", "arrival", "host"), (2, "trivial", "colour", "host"), (2, "rcb", "tile", "stream")])
+def test_ranks_on_device_match_reference_int64(world, part, sched, executor):
     from conftest import golden
     g = golden("exec.npz")
-    outs = _run(("diffusion", 8, "int64", 3, part, sched), world)
+    outs = _run(("diffusion", 8, "int64", 3, part, sched), world, executor)
     for rank, out, msgs in outs:
         assert msgs > 0
         for k, v in out.items():
             np.testing.assert_array_equal(v, g[f"exec/diffusion_n8_int64_s3/{k}"], f"rank {rank} {k}")
 
 
-def test_proxy_two_ranks_on_device_vs_oracle():
+@pytest.mark.parametrize("sched,executor", [("gather", "stream"), ("flow", "host")])
+def test_proxy_two_ranks_on_device_vs_oracle(sched, executor):
     import paper_1403_7209_b200 as ml
     from oracle import bulk
     from paper_1403_7209_b200 import apps
@@ -96,7 +100,7 @@ def test_proxy_two_ranks_on_device_vs_oracle():
     prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=5)
     ml.renumber_mesh(mesh)
     bulk.run_program(prog, resolve_kernel)
-    outs = _run(("proxy", 12, "float64", 2, "rcb", "flow"), 2)
+    outs = _run(("proxy", 12, "float64", 2, "rcb", sched), 2, executor)
     ref_q = h["q"].fetch()
     for rank, out, _ in outs:
         np.testing.assert_allclose(out["q"], ref_q, rtol=1e-12, atol=1e-12 * np.abs(ref_q).max())

@@ -810,10 +810,13 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
     constexpr int DG = AG::dim;
     __shared__ double red[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     typename E::Slots s;
     E::init_globals(s, p, idx);
-    if (t < p.g_ntargets) {
+    // grid-stride over blocks of targets (a smaller grid keeps fewer targets'
+    // rows in flight per SM; the default grid covers every target once)
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+         t - threadIdx.x < p.g_ntargets; t += int64_t(gridDim.x) * blockDim.x) {
+        if (t >= p.g_ntargets) continue;
         const ArgRt &rg = p.a[G];
         const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
         TG *dst = static_cast<TG *>(rg.data) + tg * rg.se;
@@ -1231,6 +1234,7 @@ struct FunctorEntry {
     LaunchFn gather[4];                              // target-centric (INC-only or WRITE-only):
                                                      // free / >=2 / >=3 / >=4 CTAs of 256 per SM
     int (*flow_occupancy[2])(int threads, size_t smem);
+    int (*gather_occupancy)();
     LaunchFn fold_edges, fold_targets;               // fold schedule (INC-only indirect writes)
     int32_t fold_dim, fold_arg;                      // INC dim, first INC argument
     LaunchFn tile;                                   // tile schedule (INC-only, no direct writes)
@@ -1274,6 +1278,15 @@ struct Registrar {
             once = true;
         }
         k_gather<F, T><<<g, b, 0, s>>>(p);
+    }
+    // resident CTAs of 256 threads per SM (sizes the persistent gather grid)
+    static int gather_occupancy() {
+        static int n = -1;
+        if (n < 0) {
+            cudaFuncSetAttribute(k_gather<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gather<F, T>, 256, 0) != cudaSuccess) n = 0;
+        }
+        return n;
     }
     static void fold_edges(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
@@ -1354,6 +1367,7 @@ struct Registrar {
         }
         if constexpr (SigInfo<S>::tile_ok) e.tile = &tile;
         if constexpr (SigInfo<S>::gather_ok) {
+            e.gather_occupancy = &gather_occupancy;
             e.gather[0] = &gather;
             e.gather[1] = &gather_occ<2>;
             e.gather[2] = &gather_occ<3>;

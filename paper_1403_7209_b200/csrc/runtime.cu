@@ -84,6 +84,21 @@ static int gather_variant() {
     return v;
 }
 
+// k_gather grid: persistent by default — as many CTAs as fit on the SMs at
+// once, grid-striding over the targets (each SM keeps exactly its resident
+// CTAs busy, no tail wave).  ML_GATHER_GRID=k forces k CTAs per SM, "full"
+// one CTA per 256 targets.
+static int gather_grid_per_sm(const FunctorEntry &f) {
+    static const int v = [] {
+        const char *s = std::getenv("ML_GATHER_GRID");
+        if (!s) return -1;
+        if (std::string(s) == "full") return 0;
+        return std::max(0, std::atoi(s));
+    }();
+    if (v >= 0) return v;
+    return f.gather_occupancy ? f.gather_occupancy() : 0;
+}
+
 static int validate(const ml_loop_t *L, const FunctorEntry &f) {
     const char *nm = L->name ? L->name : "?";
     if (L->nargs != f.nargs)
@@ -310,6 +325,8 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         p.g_pos = L->gather_pos;
         p.g_tlist = L->gather_targets;
         nparts = (L->gather_ntargets + 255) / 256;
+        if (const int per_sm = gather_grid_per_sm(f); per_sm > 0)
+            nparts = std::min<int64_t>(nparts, int64_t(per_sm) * g_dev.sm_count);
         if (nparts > pstride)
             ML_FAIL(ML_EINVAL, "loop '%s': gather schedule needs more reduction scratch", L->name);
         f.gather[gather_variant()](p, dim3(unsigned(nparts)), dim3(256), 0, stream);

@@ -644,15 +644,19 @@ __device__ __forceinline__ void run_direct(const LaunchParams &p, Sig<As...>) {
     using E = Engine<F, ST_NONE, As...>;
     __shared__ double smem[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    const int32_t b = blockIdx.x;
-    const int64_t lo = int64_t(b) * p.bs, hi = lo + p.bs < p.n ? lo + p.bs : p.n;
     typename E::Slots s;
     E::init_globals(s, p, idx);
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-        E::init_elem(s, p, e, nullptr, idx);
-        E::call(s, p, e, idx);
+    // persistent grid: CTA-strided over the plan blocks; one reduction
+    // partial per CTA (folded in CTA order by k_combine)
+    const int64_t nb = (p.n + p.bs - 1) / p.bs;
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int64_t lo = b * p.bs, hi = lo + p.bs < p.n ? lo + p.bs : p.n;
+        for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+            E::init_elem(s, p, e, nullptr, idx);
+            E::call(s, p, e, idx);
+        }
     }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
+    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, smem, idx);
 }
 
 template <class F, class... As>
@@ -1235,6 +1239,7 @@ struct FunctorEntry {
                                                      // free / >=2 / >=3 / >=4 CTAs of 256 per SM
     int (*flow_occupancy[2])(int threads, size_t smem);
     int (*gather_occupancy)();
+    int (*direct_occupancy)(int threads);
     LaunchFn fold_edges, fold_targets;               // fold schedule (INC-only indirect writes)
     int32_t fold_dim, fold_arg;                      // INC dim, first INC argument
     LaunchFn tile;                                   // tile schedule (INC-only, no direct writes)
@@ -1246,6 +1251,11 @@ template <class F, class T>
 struct Registrar {
     static void direct(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_direct<F, T><<<g, b, 0, s>>>(p);
+    }
+    static int direct_occupancy(int threads) {
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_direct<F, T>, threads, 0) != cudaSuccess) n = 0;
+        return n;
     }
     static void staged(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_staged<F, T><<<g, b, 0, s>>>(p);
@@ -1349,6 +1359,7 @@ struct Registrar {
         e.ind_write = SigInfo<S>::ind_write;
         e.ind_write_non_inc = SigInfo<S>::ind_write_non_inc;
         e.direct = &direct;
+        e.direct_occupancy = &direct_occupancy;
         e.staged = SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc ? &staged : nullptr;
         e.phased = SigInfo<S>::ind_write ? &phased : nullptr;
         const bool st = e.staged != nullptr;

@@ -333,7 +333,17 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     } else if (!f.ind_write) {
         const int threads = std::clamp(round_up32(bs), 32, 256);
         p.blocks = nullptr;
-        f.direct(p, dim3(unsigned(nb)), dim3(unsigned(threads)), 0, stream);
+        // persistent grid: resident CTAs x SMs (occupancy cached per block size)
+        static std::vector<std::pair<std::pair<int, int>, int>> occ_cache;
+        int occ = -1;
+        for (auto &kv : occ_cache)
+            if (kv.first == std::make_pair(L->functor, threads)) occ = kv.second;
+        if (occ < 0) {
+            occ = f.direct_occupancy ? f.direct_occupancy(threads) : 0;
+            occ_cache.push_back({{L->functor, threads}, occ});
+        }
+        nparts = occ > 0 ? std::min<int64_t>(nb, int64_t(occ) * g_dev.sm_count) : nb;
+        f.direct(p, dim3(unsigned(nparts)), dim3(unsigned(threads)), 0, stream);
     } else {
         if (!L->plan.color_offsets || !L->plan.blocks || !L->plan.elem_color || !L->plan.elem_ncolors)
             ML_FAIL(ML_EINVAL, "loop '%s': indirect writes need a coloured plan", L->name);

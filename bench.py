@@ -1,7 +1,7 @@
 """Benchmark: one Hydra-shaped solver iteration per step on B200 (BASELINE.json configs[1]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload proxy|diffusion] [--grid 94] [--inc-schedule gather|colour|flow|arrival]
+                    [--workload proxy|diffusion] [--grid 94] [--inc-schedule tuned|gather|pfold|...]
 
 Workload (default): ``build_hydra_proxy`` on the Rotor37-sized 3-D grid
 (94^3 = 830,584 nodes, 2,465,244 edges), numbered randomly (an unstructured
@@ -115,7 +115,18 @@ def run_ours(args) -> None:
 
     mesh, prog, h, wname, setup = build_workload(args)
     edges = mesh.sets["edges"].size
-    cfg = ml.BackendConfig(device=0, use_graph=True, inc_schedule=args.inc_schedule)
+    table = None
+    sched = args.inc_schedule
+    if sched == "tuned":
+        # per-loop INC schedule chosen on the device before timing (OP2-style
+        # auto-tuning, tuner.tune_schedule): gather vs primary fold
+        from paper_1403_7209_b200.tuner import tune_schedule
+        t0 = time.perf_counter()
+        res = tune_schedule(prog, mesh, ("gather", "pfold"), ml.BackendConfig(device=0), repeats=3)
+        table = dict(res.best)
+        setup["tune_s"] = round(time.perf_counter() - t0, 3)
+        sched = "gather"
+    cfg = ml.BackendConfig(device=0, use_graph=True, inc_schedule=sched, inc_schedule_table=table)
     t0 = time.perf_counter()
     cp = compile_program(prog, mesh, cfg)
     setup["plans_and_upload_s"] = round(time.perf_counter() - t0, 3)
@@ -156,12 +167,13 @@ def run_ours(args) -> None:
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(args.inc_schedule, {}).get(dom.loop.name)
+        dom_sched = (table or {}).get(dom.loop.name, sched)
+        traffic = json.loads(tfile.read_text()).get(dom_sched, {}).get(dom.loop.name)
 
     # -- end to end through the public API with host buffers ---------------------------------
     pin_mesh(mesh)
     ecfg = ml.BackendConfig(device=0, use_graph=True, residency="host",
-                            inc_schedule=args.inc_schedule)
+                            inc_schedule=sched, inc_schedule_table=table)
     h2d = sum(d.nbytes for d in cp.all_dats)
     d2h = sum(d.nbytes for d in cp.written) + sum(g.buffer.nbytes for g in cp.globs)
     for _ in range(max(1, args.warmup // 2)):
@@ -183,6 +195,7 @@ def run_ours(args) -> None:
         "config": {"workload": wname, "nodes": mesh.sets["nodes"].size, "edges": edges,
                    "loops_per_step": len(prog), "block_size": cfg.block_size,
                    "inc_schedule": args.inc_schedule,
+                   "inc_schedule_table": table,
                    "l2": "inputs > 126 MB L2 (no flush needed)",
                    "timing": "CUDA graph replays back to back, CUDA events on the library stream",
                    "parallelism": "single GPU", "device": info["name"], "setup": setup},
@@ -210,8 +223,8 @@ def main():
     ap.add_argument("--workload", choices=["proxy", "diffusion"], default="proxy")
     ap.add_argument("--grid", type=int, default=None)
     ap.add_argument("--cpu-grid", type=int, default=None)
-    ap.add_argument("--inc-schedule", choices=["gather", "tile", "fold", "colour", "flow", "arrival"],
-                    default="gather")
+    ap.add_argument("--inc-schedule", default="tuned",
+                    choices=["tuned", "gather", "pfold", "tile", "fold", "colour", "flow", "arrival"])
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.grid is None:

@@ -147,6 +147,18 @@ typedef struct ml_loop {
     const int32_t *tile_ncol;       /* [tile_count] colours                      */
     const uint16_t *tile_loc;       /* [elements][arity] local target indices    */
     const uint8_t *tile_ecol;       /* colour | 0x80 reduction owner             */
+    /* primary-fold schedule (INC-only loops); pf_n1 == 0 disables it.  Per
+     * target, CSRs of its incidences through the first INC argument
+     * (pf_off1/pf_elem1) and through the others (pf_off2/pf_elem2/pf_pos2,
+     * position >= 1), element ascending; pf_tl* map list rows to target ids
+     * (NULL: identity).  pf_slots: device [n][INC args - 1][dim rounded up
+     * to even] (ml_loop_pfold_slot_bytes). */
+    int64_t pf_n1;
+    const int32_t *pf_off1, *pf_elem1, *pf_tl1;
+    int64_t pf_n2;
+    const int32_t *pf_off2, *pf_elem2, *pf_tl2;
+    const uint8_t *pf_pos2;
+    void *pf_slots;
 } ml_loop_t;
 
 typedef struct ml_device_info {
@@ -287,6 +299,8 @@ int ml_functor_count(int32_t *count);
 int ml_functor_name(int32_t functor_id, char *buf, int32_t buflen, int32_t *dtype);
 /* Device scratch a loop needs (global-reduction partials). */
 int ml_loop_scratch_bytes(const ml_loop_t *loop, uint64_t *bytes);
+/* Bytes of the primary-fold slot buffer a loop needs (0: not applicable). */
+int ml_loop_pfold_slot_bytes(const ml_loop_t *loop, uint64_t *bytes);
 /* Enqueue one loop: coloured launches + deterministic reduction combine. */
 int ml_loop_run(const ml_loop_t *loop);
 

@@ -36,7 +36,7 @@ EXPORTED = [
     "ml_staging_export_seg", "ml_staging_export_arrival", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
     "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name",
-    "ml_loop_scratch_bytes", "ml_loop_run",
+    "ml_loop_scratch_bytes", "ml_loop_run", "ml_loop_pfold_slot_bytes",
     "ml_program_create", "ml_program_run", "ml_program_replay", "ml_program_loop_times",
     "ml_program_free",
     "ml_pack_rows", "ml_unpack_rows", "ml_combine_ranks", "ml_stream",
@@ -86,7 +86,11 @@ class MlLoop(C.Structure):
                 ("tile_list_off", C.c_void_p), ("tile_nown", C.c_void_p),
                 ("tile_list", C.c_void_p), ("tile_elem_off", C.c_void_p),
                 ("tile_elem", C.c_void_p), ("tile_ncol", C.c_void_p),
-                ("tile_loc", C.c_void_p), ("tile_ecol", C.c_void_p)]
+                ("tile_loc", C.c_void_p), ("tile_ecol", C.c_void_p),
+                ("pf_n1", C.c_int64), ("pf_off1", C.c_void_p), ("pf_elem1", C.c_void_p),
+                ("pf_tl1", C.c_void_p), ("pf_n2", C.c_int64), ("pf_off2", C.c_void_p),
+                ("pf_elem2", C.c_void_p), ("pf_tl2", C.c_void_p), ("pf_pos2", C.c_void_p),
+                ("pf_slots", C.c_void_p)]
 
 
 class MlDeviceInfo(C.Structure):
@@ -144,6 +148,7 @@ _SIGNATURES = {
     "ml_functor_name": (C.c_int, [C.c_int32, C.c_char_p, C.c_int32, _I32P]),
     "ml_loop_scratch_bytes": (C.c_int, [C.POINTER(MlLoop), C.POINTER(C.c_uint64)]),
     "ml_loop_run": (C.c_int, [C.POINTER(MlLoop)]),
+    "ml_loop_pfold_slot_bytes": (C.c_int, [C.POINTER(MlLoop), C.POINTER(C.c_uint64)]),
     "ml_program_create": (C.c_int, [C.POINTER(MlLoop), C.c_int32, _P, _P, C.c_uint64, _PP]),
     "ml_program_run": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "ml_program_replay": (C.c_int, [_P, C.c_int32]),

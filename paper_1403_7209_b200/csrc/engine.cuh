@@ -112,6 +112,20 @@ struct TileParams {
     int8_t slot[MAX_ARGS];               // map column of each indirect argument
 };
 
+// Primary-fold schedule (INC-only loops): pass 1 gives each target the elements
+// whose FIRST INC argument targets it; each element is evaluated once there,
+// its first increment accumulated in the thread's registers and the others
+// written to per-element slots; pass 2 folds each target's slots.
+struct PFoldParams {
+    int64_t n1;                          // targets with primary incidences
+    const int32_t *off1, *elem1, *tl1;   // CSR (element ascending); tl1: target ids
+    int64_t n2;                          // targets with secondary incidences
+    const int32_t *off2, *elem2, *tl2;
+    const uint8_t *pos2;                 // INC-argument position (>= 1) of each
+    void *slots;                         // [n][nslot][dgp]
+    int32_t nslot, dgp;
+};
+
 struct LaunchParams {
     ArgRt a[MAX_ARGS];
     void *part[MAX_ARGS];       // reduction partials [nblocks][dim] per global reduce arg
@@ -138,6 +152,7 @@ struct LaunchParams {
     void *g_buf;
     int32_t g_nw;               // INC arguments per element
     TileParams t;
+    PFoldParams pf;
 };
 
 // strided view of one element's components
@@ -596,6 +611,31 @@ struct Engine {
             for (int c = 0; c < A::dim; ++c) dst[c] = cuda::std::get<I>(s).acc[c];
         }
     }
+    // primary fold: INC arguments at positions >= 1 -> the element's slots
+    template <int DGP, size_t... Is>
+    __device__ __forceinline__ static void stage_rest(Slots &s, void *row, cuda::std::index_sequence<Is...>) {
+        (stage_rest_one<Is, DGP>(s, row), ...);
+    }
+    template <size_t I, int DGP>
+    __device__ __forceinline__ static void stage_rest_one(Slots &s, void *row) {
+        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
+        if constexpr (A::kind == KI && A::mode == MINC) {
+            constexpr int pos = IncIndex<As...>::template of<I>();
+            if constexpr (pos >= 1) {
+                using T = typename A::type;
+                T *dst = static_cast<T *>(row) + (pos - 1) * DGP;
+                if constexpr (A::dim % 2 == 0 && DGP % 2 == 0 && cuda::std::is_same_v<T, double>) {
+#pragma unroll
+                    for (int c = 0; c < A::dim; c += 2)
+                        __stcg(reinterpret_cast<double2 *>(dst + c),
+                               make_double2(cuda::std::get<I>(s).acc[c], cuda::std::get<I>(s).acc[c + 1]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < A::dim; ++c) __stcg(dst + c, cuda::std::get<I>(s).acc[c]);
+                }
+            }
+        }
+    }
     template <size_t... Is>
     __device__ __forceinline__ static void arrive_sums(Slots &s, const LaunchParams &p, int32_t b,
                                                        char *smem, cuda::std::index_sequence<Is...>) {
@@ -849,6 +889,92 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
         for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
     }
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
+}
+
+// Primary-fold schedule, pass 1 (see PFoldParams): a persistent grid strides
+// over the targets; thread t evaluates, in element order, every element whose
+// first INC argument targets it — each element exactly once in the whole
+// launch, its neighbours' rows read once per element instead of once per
+// incidence — adds that argument's increments to a running value that starts
+// from the target's current value, and stores the other INC arguments'
+// increments in the element's slots.  Global reductions count every element
+// here (once).  Pass 2 (k_pfold_rest) adds each target's slots in element
+// order.  Per target the result is value + primary increments + secondary
+// increments: deterministic, within rounding of the serial order.
+template <class TG, int DG>
+struct PFoldShape {
+    static constexpr int DGP = (DG + 1) / 2 * 2;   // slot rows of whole 16-byte pairs
+};
+
+template <class F, class... As>
+__device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_GATHER, As...>;
+    constexpr int G = IncIndex<As...>::template first<0>();
+    static_assert(G >= 0, "primary fold needs an INC argument");
+    using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
+    using TG = typename AG::type;
+    constexpr int DG = AG::dim;
+    constexpr int NW = ((As::kind == KI && As::mode == MINC) + ...);
+    constexpr int DGP = PFoldShape<TG, DG>::DGP;
+    __shared__ double red[32];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    const PFoldParams &pf = p.pf;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t - threadIdx.x < pf.n1;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        if (t >= pf.n1) continue;
+        const ArgRt &rg = p.a[G];
+        const int64_t tg = pf.tl1 ? int64_t(__ldg(pf.tl1 + t)) : t;
+        TG *dst = static_cast<TG *>(rg.data) + tg * rg.se;
+        TG run[DG];
+#pragma unroll
+        for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+        for (int k = __ldg(pf.off1 + t), ke = __ldg(pf.off1 + t + 1); k < ke; ++k) {
+            const int64_t e = __ldg(pf.elem1 + k);
+            E::init_elem(s, p, e, nullptr, idx);
+            E::call(s, p, e, idx);
+            E::template gather_op<MINC, 0, DG>(s, 0, run, idx);
+            if constexpr (NW > 1)
+                E::template stage_rest<DGP>(s, static_cast<TG *>(pf.slots) + e * int64_t(NW - 1) * DGP, idx);
+        }
+#pragma unroll
+        for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
+}
+
+// Primary-fold schedule, pass 2: each target adds its slots in element order.
+template <class T, int DG>
+__global__ void __launch_bounds__(256) k_pfold_rest(const __grid_constant__ LaunchParams p, int ga) {
+    constexpr int DGP = PFoldShape<T, DG>::DGP;
+    const PFoldParams &pf = p.pf;
+    const ArgRt &rg = p.a[ga];
+    const T *slots = static_cast<const T *>(pf.slots);
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < pf.n2;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t tg = pf.tl2 ? int64_t(__ldg(pf.tl2 + t)) : t;
+        T *dst = static_cast<T *>(rg.data) + tg * rg.se;
+        T run[DG];
+#pragma unroll
+        for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+        for (int k = __ldg(pf.off2 + t), ke = __ldg(pf.off2 + t + 1); k < ke; ++k) {
+            const T *src = slots + (int64_t(__ldg(pf.elem2 + k)) * pf.nslot + (__ldg(pf.pos2 + k) - 1)) * DGP;
+            if constexpr (DG % 2 == 0 && cuda::std::is_same_v<T, double>) {
+#pragma unroll
+                for (int c = 0; c < DG; c += 2) {
+                    const double2 v = __ldcs(reinterpret_cast<const double2 *>(src + c));
+                    run[c] += v.x;
+                    run[c + 1] += v.y;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < DG; ++c) run[c] += __ldcs(src + c);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+    }
 }
 
 // Fold schedule, pass 1 — every element evaluated exactly once, like a direct
@@ -1181,6 +1307,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_tile(const __grid_constant__ L
     run_tile<F>(p, typename F::template sig<T>{});
 }
 template <class F, class T>
+__global__ void __launch_bounds__(256) k_pfold1(const __grid_constant__ LaunchParams p) {
+    run_pfold1<F>(p, typename F::template sig<T>{});
+}
+template <class F, class T>
 __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ LaunchParams p) {
     run_gather<F>(p, typename F::template sig<T>{});
 }
@@ -1204,6 +1334,7 @@ struct SigInfo<Sig<As...>> {
     static constexpr bool ind_write_non_inc = ((As::kind == KI && (As::mode == MW || As::mode == MRW)) || ...);
     static constexpr bool direct_write = ((As::kind == KD && As::mode != MR) || ...);
     static constexpr bool ind_inc = ((As::kind == KI && As::mode == MINC) || ...);
+    static constexpr int n_inc = ((As::kind == KI && As::mode == MINC) + ... + 0);
     static constexpr bool ind_w = ((As::kind == KI && As::mode == MW) || ...);
     static constexpr bool ind_rw = ((As::kind == KI && As::mode == MRW) || ...);
     // target-centric schedule: indirect writes of one mode (INC or WRITE), no direct writes
@@ -1243,6 +1374,9 @@ struct FunctorEntry {
     LaunchFn fold_edges, fold_targets;               // fold schedule (INC-only indirect writes)
     int32_t fold_dim, fold_arg;                      // INC dim, first INC argument
     LaunchFn tile;                                   // tile schedule (INC-only, no direct writes)
+    LaunchFn pfold1, pfold2;                         // primary-fold schedule (INC-only)
+    int (*pfold_occupancy)();
+    int32_t pfold_dgp, pfold_nslot;
 };
 
 void register_functor(const FunctorEntry &e);
@@ -1309,6 +1443,27 @@ struct Registrar {
         }
         k_fold_edges<F, T><<<g, b, bytes, s>>>(p);
     }
+    static void pfold1(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        static bool once = false;
+        if (!once) {
+            cudaFuncSetAttribute(k_pfold1<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+            once = true;
+        }
+        k_pfold1<F, T><<<g, b, 0, s>>>(p);
+    }
+    static int pfold_occupancy() {
+        static int n = -1;
+        if (n < 0) {
+            cudaFuncSetAttribute(k_pfold1<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pfold1<F, T>, 256, 0) != cudaSuccess) n = 0;
+        }
+        return n;
+    }
+    static void pfold2(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        using S = typename F::template sig<T>;
+        using AG = typename FirstInc<S>::type;
+        k_pfold_rest<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, FirstInc<S>::value);
+    }
     static void fold_targets(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
         constexpr int G = FirstInc<S>::value;
@@ -1371,6 +1526,12 @@ struct Registrar {
         e.flow_occupancy[1] = st ? &flow_occupancy<ST_SEG> : nullptr;
         e.arrive = st ? &arrive : nullptr;
         if constexpr (SigInfo<S>::fold_ok) {
+            e.pfold1 = &pfold1;
+            e.pfold2 = &pfold2;
+            e.pfold_occupancy = &pfold_occupancy;
+            using AG = typename FirstInc<S>::type;
+            e.pfold_dgp = PFoldShape<typename AG::type, AG::dim>::DGP;
+            e.pfold_nslot = SigInfo<S>::n_inc - 1;
             e.fold_edges = &fold_edges;
             e.fold_targets = &fold_targets;
             e.fold_arg = FirstInc<S>::value;

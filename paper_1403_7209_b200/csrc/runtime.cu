@@ -293,12 +293,44 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
     const bool lists = L->gather_ntargets > 0 && L->gather_off && L->gather_elem && L->gather_pos;
+    if (L->pf_n1 > 0) {
+        // primary fold: pass 1 over targets' primary incidences (persistent grid),
+        // pass 2 folds the secondary slots
+        if (!f.pfold1 || !L->pf_off1 || !L->pf_elem1 || (f.pfold_nslot > 0 && (!L->pf_slots ||
+            (L->pf_n2 > 0 && (!L->pf_off2 || !L->pf_elem2 || !L->pf_pos2)))))
+            ML_FAIL(ML_EINVAL, "loop '%s': primary-fold lists missing", L->name);
+        PFoldParams &pf = p.pf;
+        pf.n1 = L->pf_n1;
+        pf.off1 = L->pf_off1;
+        pf.elem1 = L->pf_elem1;
+        pf.tl1 = L->pf_tl1;
+        pf.n2 = f.pfold_nslot > 0 ? L->pf_n2 : 0;
+        pf.off2 = L->pf_off2;
+        pf.elem2 = L->pf_elem2;
+        pf.tl2 = L->pf_tl2;
+        pf.pos2 = L->pf_pos2;
+        pf.slots = L->pf_slots;
+        pf.nslot = f.pfold_nslot;
+        pf.dgp = f.pfold_dgp;
+        const int occ = f.pfold_occupancy ? f.pfold_occupancy() : 0;
+        nparts = std::max<int64_t>(1, std::min<int64_t>((pf.n1 + 255) / 256,
+                                                        occ > 0 ? int64_t(occ) * g_dev.sm_count : INT64_MAX));
+        if (nparts > pstride) ML_FAIL(ML_EINVAL, "loop '%s': primary fold needs more scratch", L->name);
+        f.pfold1(p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+        if (pf.n2 > 0) {
+            const int64_t g2 = std::min<int64_t>((pf.n2 + 255) / 256, int64_t(8) * g_dev.sm_count);
+            f.pfold2(p, dim3(unsigned(g2)), dim3(256), 0, stream);
+        }
+    }
     size_t tile_smem = 0;
-    if (L->tile_count > 0) {
+    if (L->pf_n1 > 0) {
+    } else if (L->tile_count > 0) {
         rc = tile_setup(L, f, p, tile_smem);
         if (rc) return rc;
     }
-    if (L->tile_count > 0) {
+    if (L->pf_n1 > 0) {
+        // launched above
+    } else if (L->tile_count > 0) {
         // tile schedule: one CTA per tile, owner-computes, no inter-CTA conflicts
         nparts = L->tile_count;
         p.g_buf = L->fold_buf;   // per-tile phase timings when built with ML_TILE_PROFILE
@@ -559,6 +591,15 @@ extern "C" int ml_loop_scratch_bytes(const ml_loop_t *loop, uint64_t *bytes) {
     auto &reg = registry();
     if (loop->functor < 0 || loop->functor >= int(reg.size())) ML_FAIL(ML_ENOFUNCTOR, "bad functor id");
     *bytes = scratch_bytes(loop, reg[loop->functor]);
+    return ML_OK;
+}
+
+extern "C" int ml_loop_pfold_slot_bytes(const ml_loop_t *L, uint64_t *bytes) {
+    auto &reg = registry();
+    if (!L || !bytes || L->functor < 0 || L->functor >= int(reg.size()))
+        ML_FAIL(ML_EINVAL, "ml_loop_pfold_slot_bytes: bad arguments");
+    const FunctorEntry &f = reg[L->functor];
+    *bytes = f.pfold1 ? uint64_t(L->n) * uint64_t(f.pfold_nslot) * uint64_t(f.pfold_dgp) * 8 : 0;
     return ML_OK;
 }
 

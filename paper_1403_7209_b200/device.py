@@ -218,6 +218,42 @@ class GatherMirror:
                 "elem_host": h["elem"][take]}
 
 
+class PFoldMirror:
+    """Device lists of the primary-fold schedule (see PFoldParams in
+    csrc/engine.cuh), split from a loop's gather lists: per target, its
+    incidences through the first INC argument (pass 1) and through the others
+    (pass 2), element ascending; plus the per-element slot buffer."""
+
+    __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2")
+
+    def __init__(self, g: GatherMirror):
+        h = g.host
+        off, elem, pos, tl = h["off"], h["elem"], h["pos"], h["targets"]
+        nt = off.size - 1
+        owner = np.repeat(np.arange(nt), np.diff(off))
+        e, p_ = elem[:off[-1]], pos[:off[-1]]
+        for which in (1, 2):
+            m = (p_ == 0) if which == 1 else (p_ > 0)
+            rows = owner[m]
+            cnt = np.bincount(rows, minlength=nt)
+            keep = np.flatnonzero(cnt)
+            o = np.concatenate([[0], np.cumsum(cnt[keep])]).astype(np.int32)
+            setattr(self, f"n{which}", int(keep.size))
+            setattr(self, f"off{which}", _upload(o))
+            setattr(self, f"elem{which}", _upload(np.ascontiguousarray(e[m], dtype=np.int32)))
+            setattr(self, f"tl{which}", _upload(np.ascontiguousarray(tl[keep], dtype=np.int32)))
+            if which == 2:
+                self.pos2 = _upload(np.ascontiguousarray(p_[m], dtype=np.uint8))
+
+
+def pfold_mirror(loop, plan) -> PFoldMirror:
+    cache = plan.__dict__.setdefault("_pfolds", {})
+    key = loop.signature()
+    if key not in cache:
+        cache[key] = PFoldMirror(gather_mirror(loop, plan))
+    return cache[key]
+
+
 def gather_eligible(loop) -> bool:
     """Target-centric execution applies when the loop's indirect writes all go to
     one dat with one mode — INC, or WRITE — no direct argument is written, and

@@ -32,7 +32,8 @@ import numpy as np
 from . import _native as N
 from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Mesh, MeshError)
 from .device import (dat_mirror, fold_eligible, gather_eligible, gather_mirror, map_mirror,
-                     plan_mirror, schedule_mirror, staging_mirror, tile_eligible, tile_mirror)
+                     pfold_mirror, plan_mirror, schedule_mirror, staging_mirror, tile_eligible,
+                     tile_mirror)
 from .kernels import resolve_kernel
 from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
 from .plan import plan_for, plan_stats
@@ -47,7 +48,7 @@ class ExchangeTimeout(ExecError):
     """A rank waited longer than the configured bound for a halo message."""
 
 
-SCHEDULES = ("tile", "gather", "fold", "colour", "flow", "arrival")
+SCHEDULES = ("gather", "pfold", "tile", "fold", "colour", "flow", "arrival")
 
 
 @dataclass
@@ -77,7 +78,7 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
-    inc_schedule: str = "gather"            # "gather" | "tile" | "fold" | "colour" | "flow" | "arrival"
+    inc_schedule: str = "gather"            # "gather" | "pfold" | "tile" | "fold" | "colour" | "flow" | "arrival"
     inc_schedule_table: dict | None = None  # per-loop override (tuner.tune_schedule)
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
@@ -264,7 +265,11 @@ class _LoopEntry:
         self.gather = None
         self.fold = None
         self.tile = None
+        self.pfold = None
+        self.pf_slots = None
         sched = config.schedule_for(loop.name)
+        if sched == "pfold" and not (self.n > 0 and fold_eligible(loop)):
+            sched = "gather"
         if sched == "tile" and self.n > 0 and tile_eligible(loop):
             self.tile = tile_mirror(loop, mesh, self.n, config.tile_smem_kb * 1024, config.tile_cmax,
                                     config.coord_dat)
@@ -273,7 +278,18 @@ class _LoopEntry:
         elif sched == "tile":
             sched = "gather"
         self.sched = sched
-        if self.tile is not None:
+        if sched == "pfold":
+            self.gather = gather_mirror(loop, self.plan)
+            pf = self.pfold = pfold_mirror(loop, self.plan)
+            L.pf_n1, L.pf_off1, L.pf_elem1, L.pf_tl1 = pf.n1, pf.off1.ptr, pf.elem1.ptr, pf.tl1.ptr
+            L.pf_n2, L.pf_off2, L.pf_elem2, L.pf_tl2 = pf.n2, pf.off2.ptr, pf.elem2.ptr, pf.tl2.ptr
+            L.pf_pos2 = pf.pos2.ptr
+            L.functor = self.functor
+            nb = C.c_uint64()
+            N.check(N.lib().ml_loop_pfold_slot_bytes(C.byref(L), C.byref(nb)))
+            self.pf_slots = N.DeviceBuffer(max(nb.value, 8))
+            L.pf_slots = self.pf_slots.ptr
+        elif self.tile is not None:
             t = self.tile
             L.tile_count = t.count
             L.tile_arity = t.arity
@@ -291,7 +307,7 @@ class _LoopEntry:
             L.fold_buf = self.fold.ptr
         elif sched in ("gather", "fold") and self.n > 0 and gather_eligible(loop):
             self.gather = gather_mirror(loop, self.plan)
-        if self.gather is not None:
+        if self.gather is not None and self.pfold is None:
             L.gather_ntargets = self.gather.ntargets
             L.gather_off = self.gather.off.ptr
             L.gather_elem = self.gather.elem.ptr
@@ -314,7 +330,7 @@ class _LoopEntry:
         L.rlim = int(rlim[sname]) if rlim and sname in rlim else -1
         self.staging = (staging_mirror(loop, self.plan)
                         if config.smem_staging and self.gather is None and self.tile is None
-                        else None)
+                        and self.pfold is None else None)
         if self.staging is not None:
             sg = self.staging
             L.staging.ngroups = sg.ngroups
@@ -446,6 +462,8 @@ class CompiledProgram:
                 continue
             if e.fold is not None:
                 total += 2
+            elif e.pfold is not None:
+                total += 1 + (1 if e.pfold.n2 > 0 else 0)
             elif e.tile is not None:
                 total += 1
             elif e.gather is not None or not e.plan.has_writes:

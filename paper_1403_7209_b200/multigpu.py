@@ -495,7 +495,7 @@ class StreamRank:
 
     def _build_split(self, i: int, names: tuple):
         e = self.entries[i]
-        if e.gather is None or not names or e.loop.iter_set.size == 0:
+        if e.gather is None or e.pfold is not None or not names or e.loop.iter_set.size == 0:
             return None
         ex_names = set(names)
         loop = e.loop
@@ -832,7 +832,8 @@ def bench_distributed(args, metric):
     edges = mesh.sets["edges"].size
     local_dev = int(os.environ.get("ML_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     cfg = ml.BackendConfig(device=local_dev, nranks=world, partitioner="rcb", coord_dat="coords",
-                           inc_schedule=getattr(args, "inc_schedule", "gather"))
+                           inc_schedule=("gather" if getattr(args, "inc_schedule", "gather") == "tuned"
+                                         else args.inc_schedule))
     t0 = time.perf_counter()
     rp, dev, transport, layout, cfg = setup_distributed(prog, mesh, cfg, transport)
     setup["layout_and_local_mesh_s"] = round(time.perf_counter() - t0, 3)

@@ -34,7 +34,7 @@ def close(got, ref, rtol=RTOL, what=""):
     assert not bad.any(), f"{what}: {bad.sum()} mismatches, max |d| {np.max(np.abs(got - ref))}"
 
 
-SCHEDULES = ("tile", "gather", "fold", "colour", "flow", "arrival")
+SCHEDULES = ("tile", "gather", "pfold", "fold", "colour", "flow", "arrival")
 
 
 def cfg(**kw):
@@ -46,7 +46,7 @@ def _exec_cases():
 
 
 @pytest.mark.parametrize("case", _exec_cases(), ids=lambda c: c["name"])
-@pytest.mark.parametrize("bs,sched", [(256, "tile"), (256, "gather"), (16, "gather"),
+@pytest.mark.parametrize("bs,sched", [(256, "tile"), (256, "pfold"), (256, "gather"), (16, "gather"),
                                       (256, "colour"), (16, "colour")])
 def test_apps_match_reference_golden(case, bs, sched):
     g = golden("exec.npz")
@@ -147,7 +147,7 @@ def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa):
     np.testing.assert_array_equal(h["dt_min"][0].value, rh["dt_min"][0].value)
 
 
-@pytest.mark.parametrize("sched", ["tile", "gather", "colour"])
+@pytest.mark.parametrize("sched", ["tile", "pfold", "gather", "colour"])
 def test_proxy_full_size_iteration_vs_oracle(sched):
     """Config B (Rotor37-sized, 2.47M edges): one full iteration, shuffled + CM-renumbered."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(94, seed=0)
@@ -469,3 +469,35 @@ def test_tile_schedule_int64_fuzz_and_diffusion(rng):
     mesh, prog, h = _cases.build_app("diffusion", 8, "int64", 3)
     ml.run_program(prog, mesh, cfg(inc_schedule="tile", tile_smem_kb=8, tile_cmax=5))
     np.testing.assert_array_equal(h["u"].fetch(), g["exec/diffusion_n8_int64_s3/u"])
+
+
+def test_pfold_schedule_raw_accumulators_reductions_and_determinism():
+    """Primary fold: raw INC accumulators within tolerance of the serial oracle,
+    int64 bit-exact (fuzz + diffusion), MIN/MAX/READ globals counted once per
+    element, bitwise run to run."""
+    (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(12)
+    bulk.run_program(rprog[:5], resolve_kernel)
+    c = cfg(inc_schedule="pfold")
+    ml.run_program(prog[:5], mesh, c)
+    for k in ("grad", "res"):
+        close(h[k].fetch(), rh[k].fetch(), what=k)
+    first = {k: h[k].fetch().copy() for k in ("grad", "res")}
+    for k in ("grad", "res"):
+        h[k].data[...] = 0.0
+    ml.run_program(prog[:5], mesh, c)
+    for k in ("grad", "res"):
+        np.testing.assert_array_equal(h[k].fetch(), first[k])
+    g = golden("exec.npz")
+    for soa in (4, None):
+        mesh, loop, acc, lo, hi = _cases.mixmax_case(auto_soa_threshold=soa)
+        ml.run_program([loop], mesh, cfg(inc_schedule="pfold"))
+        np.testing.assert_array_equal(acc.fetch(), g["exec/mixmax/acc"])
+        assert [lo.value, hi.value] == g["exec/mixmax/lohi"].tolist()
+    rng = np.random.default_rng(11)
+    for _ in range(10):
+        seed = int(rng.integers(0, 2 ** 31))
+        ref_mesh, ref_loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
+        oserial.run_loop(ref_loop)
+        mesh, loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
+        ml.run_program([loop], mesh, cfg(inc_schedule="pfold"))
+        np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref_mesh.dats["vals"].fetch())

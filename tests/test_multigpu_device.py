@@ -79,7 +79,8 @@ def _run(case, world=2, executor="stream"):
 
 @pytest.mark.parametrize("world,part,sched,executor", [
     (2, "rcb", "gather", "stream"), (3, "trivial", "gather", "stream"), (2, "rcb", "flow", "stream"),
-    (3, "trivial", "arrival", "host"), (2, "trivial", "colour", "host"), (2, "rcb", "tile", "stream")])
+    (3, "trivial", "arrival", "host"), (2, "trivial", "colour", "host"), (2, "rcb", "tile", "stream"),
+    (2, "rcb", "pfold", "stream")])
 def test_ranks_on_device_match_reference_int64(world, part, sched, executor):
     from conftest import golden
     g = golden("exec.npz")

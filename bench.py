@@ -117,7 +117,10 @@ def run_ours(args) -> None:
     edges = mesh.sets["edges"].size
     table = None
     sched = args.inc_schedule
-    if sched == "tuned":
+    if args.schedule_table:
+        table = dict(kv.split("=", 1) for kv in args.schedule_table.split(","))
+        sched = "gather" if sched == "tuned" else sched
+    elif sched == "tuned":
         # per-loop INC schedule chosen on the device before timing (OP2-style
         # auto-tuning, tuner.tune_schedule): gather vs primary fold
         from paper_1403_7209_b200.tuner import tune_schedule
@@ -225,6 +228,8 @@ def main():
     ap.add_argument("--cpu-grid", type=int, default=None)
     ap.add_argument("--inc-schedule", default="tuned",
                     choices=["tuned", "gather", "pfold", "tile", "fold", "colour", "flow", "arrival"])
+    ap.add_argument("--schedule-table", default=None,
+                    help="per-loop INC schedules, e.g. vflux=pfold,iflux=gather (skips tuning)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.grid is None:

@@ -147,6 +147,13 @@ typedef struct ml_loop {
     const int32_t *tile_ncol;       /* [tile_count] colours                      */
     const uint16_t *tile_loc;       /* [elements][arity] local target indices    */
     const uint8_t *tile_ecol;       /* colour | 0x80 reduction owner             */
+    /* tile-gather variant (non-NULL tile_inc_off selects it): one thread per
+     * owned target accumulates its incidences in element order from the
+     * staged rows (ml_tile_export_incidences) */
+    const int32_t *tile_inc_base;
+    const int32_t *tile_inc_off;
+    const uint16_t *tile_inc_k;
+    const uint8_t *tile_inc_c;
     /* primary-fold schedule (INC-only loops); pf_n1 == 0 disables it.  Per
      * target, CSRs of its incidences through the first INC argument
      * (pf_off1/pf_elem1) and through the others (pf_off2/pf_elem2/pf_pos2,
@@ -258,6 +265,13 @@ int ml_tile_sizes(const ml_tile_t *t, int64_t *ntiles, int64_t *nlist, int64_t *
                   int64_t *umax, int64_t *cmax, int64_t *emax, int32_t *maxcol);
 int ml_tile_export(const ml_tile_t *t, int32_t *list_off, int32_t *nown, int32_t *list,
                    int32_t *elem_off, int32_t *elem, uint16_t *loc, uint8_t *ecol, int32_t *ncol);
+/* Per owned target of each tile, its incidences (element index within the
+ * tile, map column) in element-then-column order (tile-gather variant).
+ * Sizes: inc_base [ntiles] (start of the tile's rows in inc_off), inc_off
+ * [sum(nown + 1)] (absolute offsets into inc_k/inc_c), inc_k/inc_c [*ninc];
+ * pass NULL arrays to query *ninc. */
+int ml_tile_export_incidences(const ml_tile_t *t, int64_t *ninc, int32_t *inc_base, int32_t *inc_off,
+                              uint16_t *inc_k, uint8_t *inc_c);
 int ml_tile_free(ml_tile_t *t);
 
 /* Staging lists for shared-memory increment accumulation (derived from the

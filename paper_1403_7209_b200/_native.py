@@ -31,7 +31,7 @@ EXPORTED = [
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
     "ml_schedule_build", "ml_schedule_export", "ml_schedule_free",
     "ml_gather_build", "ml_gather_export", "ml_gather_free",
-    "ml_tile_build", "ml_tile_sizes", "ml_tile_export", "ml_tile_free",
+    "ml_tile_build", "ml_tile_sizes", "ml_tile_export", "ml_tile_export_incidences", "ml_tile_free",
     "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
     "ml_staging_export_seg", "ml_staging_export_arrival", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
@@ -87,6 +87,8 @@ class MlLoop(C.Structure):
                 ("tile_list", C.c_void_p), ("tile_elem_off", C.c_void_p),
                 ("tile_elem", C.c_void_p), ("tile_ncol", C.c_void_p),
                 ("tile_loc", C.c_void_p), ("tile_ecol", C.c_void_p),
+                ("tile_inc_base", C.c_void_p), ("tile_inc_off", C.c_void_p),
+                ("tile_inc_k", C.c_void_p), ("tile_inc_c", C.c_void_p),
                 ("pf_n1", C.c_int64), ("pf_off1", C.c_void_p), ("pf_elem1", C.c_void_p),
                 ("pf_tl1", C.c_void_p), ("pf_n2", C.c_int64), ("pf_off2", C.c_void_p),
                 ("pf_elem2", C.c_void_p), ("pf_tl2", C.c_void_p), ("pf_pos2", C.c_void_p),
@@ -132,6 +134,7 @@ _SIGNATURES = {
                                 C.c_int64, C.c_int64, C.c_int64, C.c_int32, _P, C.c_int32, _PP]),
     "ml_tile_sizes": (C.c_int, [_P, _I64P, _I64P, _I64P, _I64P, _I64P, _I64P, _I32P]),
     "ml_tile_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ml_tile_export_incidences": (C.c_int, [_P, _I64P, _P, _P, _P, _P]),
     "ml_tile_free": (C.c_int, [_P]),
     "ml_staging_build": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, _PP, _I32P, _PP]),
     "ml_staging_sizes": (C.c_int, [_P, C.c_int32, _I64P, _I64P]),

@@ -110,6 +110,11 @@ struct TileParams {
     int32_t gdim[MAX_TGROUPS];           // components of each group's dat
     int8_t grp[MAX_ARGS];                // group of each indirect argument
     int8_t slot[MAX_ARGS];               // map column of each indirect argument
+    // tile-gather variant: per owned target, (element-in-tile, column) incidences
+    const int32_t *inc_base, *inc_off;
+    const uint16_t *inc_k;
+    const uint8_t *inc_c;
+    int32_t red_col;                     // column whose incidence counts the element in reductions
 };
 
 // Primary-fold schedule (INC-only loops): pass 1 gives each target the elements
@@ -609,6 +614,23 @@ struct Engine {
             T *dst = static_cast<T *>(row) + pos * DGP;
 #pragma unroll
             for (int c = 0; c < A::dim; ++c) dst[c] = cuda::std::get<I>(s).acc[c];
+        }
+    }
+    // tile gather: run += increments of the INC arguments on map column c
+    template <int DG, class TG, size_t... Is>
+    __device__ __forceinline__ static void gather_col(Slots &s, const LaunchParams &p, int c, TG *run,
+                                                      cuda::std::index_sequence<Is...>) {
+        (gather_col_one<Is, DG>(s, p, c, run), ...);
+    }
+    template <size_t I, int DG, class TG>
+    __device__ __forceinline__ static void gather_col_one(Slots &s, const LaunchParams &p, int c, TG *run) {
+        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
+        if constexpr (A::kind == KI && A::mode == MINC) {
+            if (p.t.slot[I] == c) {
+                auto &acc = cuda::std::get<I>(s).acc;
+#pragma unroll
+                for (int q = 0; q < DG; ++q) run[q] += acc[q];
+            }
         }
     }
     // primary fold: INC arguments at positions >= 1 -> the element's slots
@@ -1219,6 +1241,85 @@ __device__ __forceinline__ void run_tile(const LaunchParams &p, Sig<As...>) {
     if constexpr (E::has_reduce) E::reduce_all(s, p, t, red, idx);
 }
 
+// Tile-gather variant: the tile's staged rows as in run_tile, then one thread
+// per owned target re-evaluates each of its incidences (element order, then
+// column) from shared memory and keeps its own increments in registers — no
+// colour phases, no accumulators, one barrier.  Elements are evaluated once
+// per incidence (like the gather schedule) but every node row comes from
+// shared memory, staged once per tile.  Reductions count an element at its
+// `red_col` incidence (exactly one tile owns that target).
+template <class F, class... As>
+__device__ __forceinline__ void run_tgather(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_TILE, As...>;
+    constexpr int G = IncIndex<As...>::template first<0>();
+    using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
+    using T = typename AG::type;
+    constexpr int DG = AG::dim;
+    __shared__ double red[32];
+    __shared__ char *gb[MAX_TGROUPS];
+    extern __shared__ __align__(16) char dsm[];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    const TileParams &tp = p.t;
+    const int32_t t = blockIdx.x;
+    const int32_t l0 = tp.list_off[t], U = tp.list_off[t + 1] - l0, C = tp.nown[t];
+    const int ng = tp.nread;
+    int32_t *slist = reinterpret_cast<int32_t *>(dsm);
+    if (threadIdx.x == 0) {
+        size_t off = tile_align(size_t(U) * 4);
+        for (int g = 0; g < ng; ++g) {
+            gb[g] = dsm + off;
+            off += tile_align(sizeof(T) * size_t(tp.gdim[g]) * size_t(U));
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < U; j += blockDim.x) {
+        const int64_t v = __ldg(tp.list + l0 + j);
+        slist[j] = int32_t(v);
+        for (int g = 0; g < ng; ++g) {
+            const ArgRt &r = p.a[tp.garg[g]];
+            const T *src = static_cast<const T *>(r.data) + v * r.se;
+            T *dst = reinterpret_cast<T *>(gb[g]) + j;
+            const int dim = tp.gdim[g];
+#pragma unroll 4
+            for (int c = 0; c < dim; ++c) cp_async8(dst + c * U, src + c * r.sc);
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    const int32_t e0 = tp.elem_off[t];
+    const int32_t *ioff = tp.inc_off + tp.inc_base[t];
+    const ArgRt &rg = p.a[G];
+    for (int j = threadIdx.x; j < C; j += blockDim.x) {
+        T *dst = static_cast<T *>(rg.data) + int64_t(slist[j]) * rg.se;
+        T run[DG];
+#pragma unroll
+        for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+        for (int q = __ldg(ioff + j), qe = __ldg(ioff + j + 1); q < qe; ++q) {
+            const int k = e0 + __ldg(tp.inc_k + q);
+            const int col = __ldg(tp.inc_c + q);
+            const int64_t e = __ldg(tp.elem + k);
+            E::init_tile(s, p, e, tp.loc + int64_t(k) * tp.arity, gb, U, 0, idx);
+            if constexpr (E::has_reduce) {
+                if (col != tp.red_col || e >= p.rlim) {
+                    E::backup_all(s, idx);
+                    E::call_raw(s, p, idx);
+                    E::restore_all(s, idx);
+                } else {
+                    E::call_raw(s, p, idx);
+                }
+            } else {
+                E::call_raw(s, p, idx);
+            }
+            E::template gather_col<DG>(s, p, col, run, idx);
+        }
+#pragma unroll
+        for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, t, red, idx);
+}
+
 // Arrival schedule: one launch over the plan blocks in natural order (best
 // locality), no block colours and no inter-block waiting.  Targets touched by
 // one block are updated directly; shared targets are completed by whichever
@@ -1306,6 +1407,10 @@ template <class F, class T, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) k_tile(const __grid_constant__ LaunchParams p) {
     run_tile<F>(p, typename F::template sig<T>{});
 }
+template <class F, class T, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_tgather(const __grid_constant__ LaunchParams p) {
+    run_tgather<F>(p, typename F::template sig<T>{});
+}
 template <class F, class T>
 __global__ void __launch_bounds__(256) k_pfold1(const __grid_constant__ LaunchParams p) {
     run_pfold1<F>(p, typename F::template sig<T>{});
@@ -1374,6 +1479,7 @@ struct FunctorEntry {
     LaunchFn fold_edges, fold_targets;               // fold schedule (INC-only indirect writes)
     int32_t fold_dim, fold_arg;                      // INC dim, first INC argument
     LaunchFn tile;                                   // tile schedule (INC-only, no direct writes)
+    LaunchFn tgather;                                // tile-gather variant
     LaunchFn pfold1, pfold2;                         // primary-fold schedule (INC-only)
     int (*pfold_occupancy)();
     int32_t pfold_dgp, pfold_nslot;
@@ -1479,6 +1585,19 @@ struct Registrar {
         }
         k_tile<F, T, NT><<<g, NT, bytes, s>>>(p);
     }
+    template <int NT>
+    static void tgather_launch(const LaunchParams &p, dim3 g, size_t bytes, cudaStream_t s) {
+        static size_t opted = 48 * 1024;
+        if (bytes > opted) {
+            cudaFuncSetAttribute(k_tgather<F, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+            opted = bytes;
+        }
+        k_tgather<F, T, NT><<<g, NT, bytes, s>>>(p);
+    }
+    static void tgather(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
+        if (b.x == 128) tgather_launch<128>(p, g, bytes, s);
+        else tgather_launch<256>(p, g, bytes, s);
+    }
     static void tile(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
         if (b.x == 128) tile_launch<128>(p, g, bytes, s);
         else tile_launch<256>(p, g, bytes, s);
@@ -1537,7 +1656,10 @@ struct Registrar {
             e.fold_arg = FirstInc<S>::value;
             e.fold_dim = FirstInc<S>::type::dim;
         }
-        if constexpr (SigInfo<S>::tile_ok) e.tile = &tile;
+        if constexpr (SigInfo<S>::tile_ok) {
+            e.tile = &tile;
+            e.tgather = &tgather;
+        }
         if constexpr (SigInfo<S>::gather_ok) {
             e.gather_occupancy = &gather_occupancy;
             e.gather[0] = &gather;

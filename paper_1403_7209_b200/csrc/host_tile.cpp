@@ -39,6 +39,11 @@
 
 struct ml_tile {
     std::vector<int32_t> list_off, nown, list, elem_off, elem, ncol;
+    // per owned target: its incidences (element index in the tile, map column)
+    // in element-then-column order — the tile-gather variant's lists
+    std::vector<int32_t> inc_base, inc_off;
+    std::vector<uint16_t> inc_k;
+    std::vector<uint8_t> inc_c;
     std::vector<uint16_t> loc;
     std::vector<uint8_t> ecol;
     int64_t umax = 0, cmax = 0, emax = 0;
@@ -275,6 +280,33 @@ extern "C" int ml_tile_build(int64_t n, int32_t arity, const int64_t *table, int
             t->ecol.push_back(uint8_t(col | (red_owner ? 0x80 : 0)));
             for (int c = 0; c < arity; ++c) t->loc.push_back(uint16_t(local[table[int64_t(e) * arity + c]]));
         }
+        // owned-target incidence lists (element order, then column)
+        {
+            const int32_t C = int32_t(owned.size());
+            const size_t e0 = t->elem.size() - elems.size();
+            if (elems.size() > 65535) throw std::length_error("tile has more than 65535 elements");
+            std::vector<int32_t> cnt(size_t(C) + 1, 0);
+            for (size_t k = 0; k < elems.size(); ++k)
+                for (int c = 0; c < arity; ++c)
+                    if ((inc_mask >> c & 1) && t->loc[(e0 + k) * arity + c] < C)
+                        cnt[t->loc[(e0 + k) * arity + c] + 1]++;
+            for (int32_t j = 0; j < C; ++j) cnt[j + 1] += cnt[j];
+            t->inc_base.push_back(int32_t(t->inc_off.size()));
+            const int32_t kb = int32_t(t->inc_k.size());
+            for (int32_t j = 0; j <= C; ++j) t->inc_off.push_back(kb + cnt[j]);
+            t->inc_k.resize(size_t(kb) + cnt[C]);
+            t->inc_c.resize(size_t(kb) + cnt[C]);
+            std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+            for (size_t k = 0; k < elems.size(); ++k)
+                for (int c = 0; c < arity; ++c) {
+                    const int32_t l = t->loc[(e0 + k) * arity + c];
+                    if ((inc_mask >> c & 1) && l < C) {
+                        const int32_t q = kb + fill[l]++;
+                        t->inc_k[q] = uint16_t(k);
+                        t->inc_c[q] = uint8_t(c);
+                    }
+                }
+        }
         t->elem_off.push_back(int32_t(t->elem.size()));
         t->ncol.push_back(ncol);
         t->umax = std::max<int64_t>(t->umax, li);
@@ -313,6 +345,17 @@ extern "C" int ml_tile_export(const ml_tile_t *t, int32_t *list_off, int32_t *no
     if (loc) std::copy(t->loc.begin(), t->loc.end(), loc);
     if (ecol) std::copy(t->ecol.begin(), t->ecol.end(), ecol);
     if (ncol) std::copy(t->ncol.begin(), t->ncol.end(), ncol);
+    return ML_OK;
+}
+
+extern "C" int ml_tile_export_incidences(const ml_tile_t *t, int64_t *ninc, int32_t *inc_base,
+                                         int32_t *inc_off, uint16_t *inc_k, uint8_t *inc_c) {
+    if (!t) ML_FAIL(ML_EINVAL, "ml_tile_export_incidences: null");
+    if (ninc) *ninc = int64_t(t->inc_k.size());
+    if (inc_base) std::copy(t->inc_base.begin(), t->inc_base.end(), inc_base);
+    if (inc_off) std::copy(t->inc_off.begin(), t->inc_off.end(), inc_off);
+    if (inc_k) std::copy(t->inc_k.begin(), t->inc_k.end(), inc_k);
+    if (inc_c) std::copy(t->inc_c.begin(), t->inc_c.end(), inc_c);
     return ML_OK;
 }
 

@@ -334,6 +334,21 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         // tile schedule: one CTA per tile, owner-computes, no inter-CTA conflicts
         nparts = L->tile_count;
         p.g_buf = L->fold_buf;   // per-tile phase timings when built with ML_TILE_PROFILE
+        if (L->tile_inc_off) {
+            // tile-gather: staged READ rows only; one INC dat
+            if (!L->tile_inc_base || !L->tile_inc_k || !L->tile_inc_c || !f.tgather || p.t.ninc != 1)
+                ML_FAIL(ML_EINVAL, "loop '%s': tile-gather needs its incidence lists and one INC dat", L->name);
+            p.t.inc_base = L->tile_inc_base;
+            p.t.inc_off = L->tile_inc_off;
+            p.t.inc_k = L->tile_inc_k;
+            p.t.inc_c = L->tile_inc_c;
+            int rc2 = -1;
+            for (int i = 0; i < f.nargs && rc2 < 0; ++i)
+                if (L->args[i].kind == ML_INDIRECT && L->args[i].mode == ML_INC) rc2 = L->args[i].slot;
+            p.t.red_col = rc2;
+            const size_t smem = tile_smem - tile_align(size_t(8) * p.t.gdim[p.t.nread] * size_t(L->tile_cmax));
+            f.tgather(p, dim3(unsigned(L->tile_count)), dim3(L->tile_threads == 128 ? 128 : 256), smem, stream);
+        } else
         f.tile(p, dim3(unsigned(L->tile_count)), dim3(L->tile_threads == 128 ? 128 : 256), tile_smem, stream);
     } else if (L->fold_buf && f.fold_edges && lists) {
         // fold: each element once -> increment slots; then per target, serial order

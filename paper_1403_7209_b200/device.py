@@ -292,18 +292,25 @@ class TileMirror:
     their halo in shared memory (see csrc/host_tile.cpp)."""
 
     __slots__ = ("count", "arity", "umax", "cmax", "emax", "maxcol", "list_off", "nown", "list",
-                 "elem_off", "elem", "ncol", "loc", "ecol", "staged_total", "elem_total")
+                 "elem_off", "elem", "ncol", "loc", "ecol", "staged_total", "elem_total",
+                 "inc_base", "inc_off", "inc_k", "inc_c")
 
-    def __init__(self, loop, n: int, budget: int, cmax: int, coords: np.ndarray | None):
-        h = tile_plan_host(loop, n, budget, cmax, coords)
+    def __init__(self, loop, n: int, budget: int, cmax: int, coords: np.ndarray | None,
+                 gather: bool = False):
+        h = tile_plan_host(loop, n, budget, cmax, coords, accumulate=not gather)
         for k in ("count", "arity", "umax", "cmax", "emax", "maxcol"):
             setattr(self, k, h[k])
         self.staged_total, self.elem_total = int(h["list"].size), int(h["elem"].size)
         for k in ("list_off", "nown", "list", "elem_off", "elem", "loc", "ecol", "ncol"):
             setattr(self, k, _upload(h[k]))
+        self.inc_base = self.inc_off = self.inc_k = self.inc_c = None
+        if gather:
+            for k in ("inc_base", "inc_off", "inc_k", "inc_c"):
+                setattr(self, k, _upload(h[k]))
 
 
-def tile_plan_host(loop, n: int, budget: int, cmax: int, coords: np.ndarray | None) -> dict:
+def tile_plan_host(loop, n: int, budget: int, cmax: int, coords: np.ndarray | None,
+                   accumulate: bool = True) -> dict:
     """Host arrays of the tile plan of ``loop`` over its first ``n`` elements
     (ml_tile_build; see include/meshloop_b200.h for their meaning)."""
     import ctypes as C
@@ -317,6 +324,8 @@ def tile_plan_host(loop, n: int, budget: int, cmax: int, coords: np.ndarray | No
     red_col = next(a.slot for a in ind if a.mode.name == "INC")
     stage = 4 + 8 * sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name != "INC"))
     own = 8 * sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name == "INC"))
+    if not accumulate:                    # tile-gather: owned targets live in registers
+        own = 0
     L = N.lib()
     h = C.c_void_p()
     if coords is not None:
@@ -336,6 +345,14 @@ def tile_plan_host(loop, n: int, budget: int, cmax: int, coords: np.ndarray | No
                    ecol=np.empty(ne, np.uint8), ncol=np.empty(nt, np.int32))
         N.check(L.ml_tile_export(h, *[N.ptr(out[k]) for k in ("list_off", "nown", "list", "elem_off",
                                                                 "elem", "loc", "ecol", "ncol")]))
+        ni = C.c_int64()
+        N.check(L.ml_tile_export_incidences(h, C.byref(ni), None, None, None, None))
+        out["inc_base"] = np.empty(nt, np.int32)
+        out["inc_off"] = np.empty(int(out["nown"].sum()) + nt, np.int32)
+        out["inc_k"] = np.empty(ni.value, np.uint16)
+        out["inc_c"] = np.empty(ni.value, np.uint8)
+        N.check(L.ml_tile_export_incidences(h, C.byref(ni), *[N.ptr(out[k]) for k in
+                                                                ("inc_base", "inc_off", "inc_k", "inc_c")]))
     finally:
         L.ml_tile_free(h)
     out.update(count=nt, arity=m.arity, umax=umax, cmax=cm, emax=emax, maxcol=mc.value,
@@ -370,7 +387,8 @@ def tile_eligible(loop) -> bool:
     return len(_distinct(a.dat for a in ind)) <= 8
 
 
-def tile_mirror(loop, mesh, n: int, budget: int, cmax: int, coord_dat: str | None) -> TileMirror | None:
+def tile_mirror(loop, mesh, n: int, budget: int, cmax: int, coord_dat: str | None,
+                gather: bool = False) -> TileMirror | None:
     """Tile plan of ``loop`` (cached on the mesh per map version and budget);
     None when a target alone exceeds the budget or a tile would need more than
     127 colours (hub targets) — the gather schedule handles those."""
@@ -386,11 +404,11 @@ def tile_mirror(loop, mesh, n: int, budget: int, cmax: int, coord_dat: str | Non
     own = sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name == "INC"))
     red_col = next(a.slot for a in ind if a.mode.name == "INC")
     key = (m.name, mesh.version, n, inc_mask, red_col, stage, own, int(budget), int(cmax),
-           coords is not None)
+           coords is not None, gather)
     cache = mesh.__dict__.setdefault("_ml_tiles", {})
     if key not in cache:
         try:
-            cache[key] = TileMirror(loop, n, budget, cmax, coords)
+            cache[key] = TileMirror(loop, n, budget, cmax, coords, gather)
         except ExecError:
             cache[key] = None
     return cache[key]

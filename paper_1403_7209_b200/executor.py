@@ -48,7 +48,7 @@ class ExchangeTimeout(ExecError):
     """A rank waited longer than the configured bound for a halo message."""
 
 
-SCHEDULES = ("gather", "pfold", "tile", "fold", "colour", "flow", "arrival")
+SCHEDULES = ("gather", "pfold", "tile", "tgather", "fold", "colour", "flow", "arrival")
 
 
 @dataclass
@@ -270,12 +270,13 @@ class _LoopEntry:
         sched = config.schedule_for(loop.name)
         if sched == "pfold" and not (self.n > 0 and fold_eligible(loop)):
             sched = "gather"
-        if sched == "tile" and self.n > 0 and tile_eligible(loop):
+        one_inc = len({a.dat.name for a in loop.args if a.kind == "indirect" and a.mode is INC}) == 1
+        if (sched == "tile" or (sched == "tgather" and one_inc)) and self.n > 0 and tile_eligible(loop):
             self.tile = tile_mirror(loop, mesh, self.n, config.tile_smem_kb * 1024, config.tile_cmax,
-                                    config.coord_dat)
+                                    config.coord_dat, gather=sched == "tgather")
             if self.tile is None:
                 sched = "gather"
-        elif sched == "tile":
+        elif sched in ("tile", "tgather"):
             sched = "gather"
         self.sched = sched
         if sched == "pfold":
@@ -299,6 +300,9 @@ class _LoopEntry:
             L.tile_list_off, L.tile_nown, L.tile_list = t.list_off.ptr, t.nown.ptr, t.list.ptr
             L.tile_elem_off, L.tile_elem, L.tile_ncol = t.elem_off.ptr, t.elem.ptr, t.ncol.ptr
             L.tile_loc, L.tile_ecol = t.loc.ptr, t.ecol.ptr
+            if t.inc_off is not None:
+                L.tile_inc_base, L.tile_inc_off = t.inc_base.ptr, t.inc_off.ptr
+                L.tile_inc_k, L.tile_inc_c = t.inc_k.ptr, t.inc_c.ptr
         elif sched == "fold" and self.n > 0 and fold_eligible(loop):
             self.gather = gather_mirror(loop, self.plan)
             inc = [a for a in loop.args if a.kind == "indirect" and a.mode is INC]

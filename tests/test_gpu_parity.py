@@ -34,7 +34,7 @@ def close(got, ref, rtol=RTOL, what=""):
     assert not bad.any(), f"{what}: {bad.sum()} mismatches, max |d| {np.max(np.abs(got - ref))}"
 
 
-SCHEDULES = ("tile", "gather", "pfold", "fold", "colour", "flow", "arrival")
+SCHEDULES = ("tile", "tgather", "gather", "pfold", "fold", "colour", "flow", "arrival")
 
 
 def cfg(**kw):
@@ -147,7 +147,7 @@ def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa):
     np.testing.assert_array_equal(h["dt_min"][0].value, rh["dt_min"][0].value)
 
 
-@pytest.mark.parametrize("sched", ["tile", "pfold", "gather", "colour"])
+@pytest.mark.parametrize("sched", ["tile", "tgather", "pfold", "gather", "colour"])
 def test_proxy_full_size_iteration_vs_oracle(sched):
     """Config B (Rotor37-sized, 2.47M edges): one full iteration, shuffled + CM-renumbered."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(94, seed=0)
@@ -430,14 +430,15 @@ def test_gather_write_is_serial_last_writer(seed):
         np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref.dats["vals"].fetch())
 
 
-@pytest.mark.parametrize("smem_kb,cmax", [(100, 512), (12, 4), (227, 4096)])
-def test_tile_schedule_matches_oracle_and_is_deterministic(smem_kb, cmax):
+@pytest.mark.parametrize("smem_kb,cmax,sched", [(100, 512, "tile"), (12, 4, "tile"), (227, 4096, "tile"),
+                                               (100, 512, "tgather"), (12, 4, "tgather")])
+def test_tile_schedule_matches_oracle_and_is_deterministic(smem_kb, cmax, sched):
     """Tile schedule (owner-computes tiles, shared-memory staging): raw INC
     accumulators within tolerance of the serial oracle at several tile sizes,
     int64 bit-exact, reductions counted once per element, bitwise run to run."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(12)
     bulk.run_program(rprog[:5], resolve_kernel)
-    c = cfg(inc_schedule="tile", tile_smem_kb=smem_kb, tile_cmax=cmax)
+    c = cfg(inc_schedule=sched, tile_smem_kb=smem_kb, tile_cmax=cmax)
     ml.run_program(prog[:5], mesh, c)
     for k in ("grad", "res"):
         close(h[k].fetch(), rh[k].fetch(), what=k)
@@ -449,7 +450,7 @@ def test_tile_schedule_matches_oracle_and_is_deterministic(smem_kb, cmax):
         np.testing.assert_array_equal(h[k].fetch(), first[k])
     for soa in (4, None):
         mesh, loop, acc, lo, hi = _cases.mixmax_case(auto_soa_threshold=soa)
-        ml.run_program([loop], mesh, cfg(inc_schedule="tile", tile_smem_kb=8, tile_cmax=3))
+        ml.run_program([loop], mesh, cfg(inc_schedule=sched, tile_smem_kb=8, tile_cmax=3))
         g = golden("exec.npz")
         np.testing.assert_array_equal(acc.fetch(), g["exec/mixmax/acc"])
         assert [lo.value, hi.value] == g["exec/mixmax/lohi"].tolist()

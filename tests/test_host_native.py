@@ -430,6 +430,24 @@ def test_tile_plan_invariants_fuzz(rng):
             assert "budget" in str(ex) or "colours" in str(ex)
             continue
         _check_tile_plan(h, m.table, n, list(range(m.arity)), 0, budget, cmax)
+        _check_tile_incidences(h, m.table, n, list(range(m.arity)))
+
+
+def _check_tile_incidences(h, table, n, inc_cols):
+    """Tile-gather lists: per owned target, exactly its (element, INC column)
+    incidences in the tile, element-then-column order."""
+    table = np.asarray(table[:n], dtype=np.int64)
+    for t in range(h["count"]):
+        lst = h["list"][h["list_off"][t]:h["list_off"][t + 1]]
+        c = int(h["nown"][t])
+        k0, k1 = h["elem_off"][t], h["elem_off"][t + 1]
+        el = h["elem"][k0:k1]
+        base = h["inc_base"][t]
+        for j in range(c):
+            q0, q1 = h["inc_off"][base + j], h["inc_off"][base + j + 1]
+            got = [(int(el[k]), int(col)) for k, col in zip(h["inc_k"][q0:q1], h["inc_c"][q0:q1])]
+            want = sorted((int(e), col) for e in el for col in inc_cols if table[e, col] == lst[j])
+            assert got == want
 
 
 def test_tile_plan_invariants_proxy_mesh_with_coords():
@@ -445,5 +463,6 @@ def test_tile_plan_invariants_proxy_mesh_with_coords():
         h = tile_plan_host(loop, m.from_set.size, 20_000, 64, c)
         assert h["count"] > 1
         _check_tile_plan(h, m.table, m.from_set.size, [0, 1], 0, 20_000, 64)
+        _check_tile_incidences(h, m.table, m.from_set.size, [0, 1])
     with pytest.raises(ml.ExecError, match="budget"):
         tile_plan_host(loop, m.from_set.size, 500, 64, None)

@@ -18,8 +18,9 @@ plus achieved HBM GB/s vs the measured peak for the dominant loop (vflux).
                  stream (N=1); max over ranks (N>1).
 * ``e2e``        the same metric through the public API with HOST buffers:
                  every step ``run_program(..., residency="host")`` uploads
-                 every dat the iteration touches from pinned host memory and
-                 downloads every dat it writes plus the reductions.
+                 every input dat of the iteration from pinned host memory and
+                 downloads every dat it writes plus the reductions; uploads,
+                 loops and downloads overlap on three streams.
 * ``roofline``   vflux loop: B_alg / mean loop time from an eager pass with
                  CUDA events between loops (same stream).
 * ``cpu_baseline`` the reference CPU path restated (oracle/serial.py:
@@ -177,7 +178,8 @@ def run_ours(args) -> None:
     pin_mesh(mesh)
     ecfg = ml.BackendConfig(device=0, use_graph=True, residency="host",
                             inc_schedule=sched, inc_schedule_table=table)
-    h2d = sum(d.nbytes for d in cp.all_dats)
+    first, _last = cp._stream_plan()
+    h2d = sum(d.nbytes for ds in first for d in ds) + sum(g.buffer.nbytes for g in cp.globs)
     d2h = sum(d.nbytes for d in cp.written) + sum(g.buffer.nbytes for g in cp.globs)
     for _ in range(max(1, args.warmup // 2)):
         ml.run_program(prog, mesh, ecfg)

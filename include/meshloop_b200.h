@@ -193,6 +193,15 @@ int ml_host_free(void *hptr);
 int ml_upload(void *dst, const void *src, uint64_t bytes);    /* H2D, stream-ordered */
 int ml_download(void *dst, const void *src, uint64_t bytes);  /* D2H, synchronous    */
 int ml_memset(void *dst, int value, uint64_t bytes);
+/* Copy engines for the host-resident path (streamed residency): H2D and D2H
+ * run on their own streams so input uploads, loop execution and result
+ * downloads overlap; ml_order(from, to) makes stream `to` wait for all work
+ * enqueued so far on stream `from`; ml_sync_all waits for all three. */
+enum { ML_STREAM_COMPUTE = 0, ML_STREAM_H2D = 1, ML_STREAM_D2H = 2 };
+int ml_copy_h2d(void *dst, const void *src, uint64_t bytes);
+int ml_copy_d2h(void *dst, const void *src, uint64_t bytes);
+int ml_order(int32_t from, int32_t to);
+int ml_sync_all(void);
 /* Upload an int64 0-based (rows, arity) row-major map table as the device's
  * int32 column-major layout (core.py:362-387 stores int64 row-major). */
 int ml_map_upload(int32_t *dst, const int64_t *table, int64_t rows, int32_t arity);

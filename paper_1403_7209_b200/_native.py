@@ -22,12 +22,13 @@ ML_DIRECT, ML_INDIRECT, ML_GLOBAL = 0, 1, 2
 MODE_CODE = {"READ": 0, "WRITE": 1, "RW": 2, "INC": 3, "MIN": 4, "MAX": 5}
 ML_F64, ML_I64 = 0, 1
 ML_AOS, ML_SOA = 0, 1
+ML_STREAM_COMPUTE, ML_STREAM_H2D, ML_STREAM_D2H = 0, 1, 2
 
 #: every symbol include/meshloop_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = [
     "ml_last_error", "ml_version", "ml_init", "ml_device_info", "ml_synchronize",
     "ml_alloc", "ml_free", "ml_host_alloc", "ml_host_free", "ml_upload", "ml_download",
-    "ml_memset", "ml_map_upload",
+    "ml_memset", "ml_map_upload", "ml_copy_h2d", "ml_copy_d2h", "ml_order", "ml_sync_all",
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
     "ml_schedule_build", "ml_schedule_export", "ml_schedule_free",
     "ml_gather_build", "ml_gather_export", "ml_gather_free",
@@ -119,6 +120,10 @@ _SIGNATURES = {
     "ml_download": (C.c_int, [_P, _P, C.c_uint64]),
     "ml_memset": (C.c_int, [_P, C.c_int, C.c_uint64]),
     "ml_map_upload": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
+    "ml_copy_h2d": (C.c_int, [_P, _P, C.c_uint64]),
+    "ml_copy_d2h": (C.c_int, [_P, _P, C.c_uint64]),
+    "ml_order": (C.c_int, [C.c_int32, C.c_int32]),
+    "ml_sync_all": (C.c_int, []),
     "ml_plan_build": (C.c_int, [C.c_int64, C.c_int32, _PP, _I32P, C.c_int64, _PP]),
     "ml_plan_sizes": (C.c_int, [_P, _I64P, _I64P, _I64P]),
     "ml_plan_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),

@@ -38,6 +38,9 @@ void register_functor(const FunctorEntry &e) { registry().push_back(e); }
 struct DeviceState {
     int device = -1;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy[2] = {nullptr, nullptr};     // H2D, D2H copy streams
+    cudaEvent_t order_ev[64] = {};
+    int order_next = 0;
     int sm_count = 0;
     int64_t l2_bytes = 0;
     void *flush_buf = nullptr;
@@ -474,7 +477,12 @@ extern "C" int ml_init(int device) {
         ML_FAIL(ML_ECUDA, "ml_init: device %d is sm_%d%d; this library is built for sm_100a only", device,
                 prop.major, prop.minor);
     if (g_dev.stream) cudaStreamDestroy(g_dev.stream);
+    for (auto &c : g_dev.copy)
+        if (c) cudaStreamDestroy(c), c = nullptr;
     ML_CUDA(cudaStreamCreateWithFlags(&g_dev.stream, cudaStreamNonBlocking));
+    for (auto &c : g_dev.copy) ML_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+    for (auto &e : g_dev.order_ev)
+        if (!e) ML_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     g_dev.device = device;
     g_dev.sm_count = prop.multiProcessorCount;
     g_dev.l2_bytes = prop.l2CacheSize;
@@ -547,6 +555,40 @@ extern "C" int ml_memset(void *dst, int value, uint64_t bytes) {
     if (bytes) ML_CUDA(cudaMemsetAsync(dst, value, bytes, g_dev.stream));
     return ML_OK;
 }
+static cudaStream_t stream_of(int32_t which) {
+    return which == ML_STREAM_H2D ? g_dev.copy[0] : which == ML_STREAM_D2H ? g_dev.copy[1] : g_dev.stream;
+}
+extern "C" int ml_copy_h2d(void *dst, const void *src, uint64_t bytes) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (bytes) ML_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g_dev.copy[0]));
+    return ML_OK;
+}
+extern "C" int ml_copy_d2h(void *dst, const void *src, uint64_t bytes) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (bytes) ML_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g_dev.copy[1]));
+    return ML_OK;
+}
+extern "C" int ml_order(int32_t from, int32_t to) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (from == to) return ML_OK;
+    cudaEvent_t ev = g_dev.order_ev[g_dev.order_next];
+    g_dev.order_next = (g_dev.order_next + 1) % 64;
+    ML_CUDA(cudaEventRecord(ev, stream_of(from)));
+    ML_CUDA(cudaStreamWaitEvent(stream_of(to), ev, 0));
+    return ML_OK;
+}
+extern "C" int ml_sync_all(void) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    ML_CUDA(cudaStreamSynchronize(g_dev.copy[0]));
+    ML_CUDA(cudaStreamSynchronize(g_dev.stream));
+    ML_CUDA(cudaStreamSynchronize(g_dev.copy[1]));
+    return ML_OK;
+}
+
 extern "C" int ml_map_upload(int32_t *dst, const int64_t *table, int64_t rows, int32_t arity) {
     int rc = ensure_init();
     if (rc) return rc;

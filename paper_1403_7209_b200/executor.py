@@ -441,6 +441,76 @@ class CompiledProgram:
             return [float(ms[i]) * 1e-3 for i in range(len(self.entries))]
         return None
 
+    def _stream_plan(self):
+        """Per loop: the input dats first used there (uploaded just before it)
+        and the written dats last written there (downloaded right after it).
+        A dat is an input unless its first access overwrites the whole set
+        (a direct WRITE over the full iteration set, not also read there)."""
+        plan = self.__dict__.get("_splan")
+        if plan is not None:
+            return plan
+        first, last = [[] for _ in self.entries], [[] for _ in self.entries]
+        seen, last_w = set(), {}
+        for i, e in enumerate(self.entries):
+            loop = e.loop
+            for d in e.dats:
+                key = id(d)
+                if key in seen:
+                    continue
+                seen.add(key)
+                modes = [a for a in loop.args if a.kind != "global" and a.dat is d]
+                overwrite = (all(a.kind == "direct" and a.mode.name == "WRITE" for a in modes)
+                             and e.n == d.set.size)
+                if not overwrite:
+                    first[i].append(d)
+            for d in e.written:
+                last_w[id(d)] = (i, d)
+        for i, d in last_w.values():
+            last[i].append(d)
+        self._splan = (first, last)
+        return self._splan
+
+    def run_streamed(self) -> None:
+        """Host-resident run with the copies overlapped with execution: each
+        input dat is uploaded (H2D stream) just before the first loop that uses
+        it, each written dat downloaded (D2H stream) right after its last
+        writer, while the compute stream runs the loops (stream-ordered with
+        events, one host synchronisation at the end)."""
+        L = N.lib()
+        first, last = self._stream_plan()
+        hv = self.ghost.array
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            hv[o:o + g.buffer.nbytes] = g.buffer.view(np.uint8)
+        for d in self.all_dats:
+            dat_mirror(d)                      # allocation; contents come below
+        N.check(L.ml_copy_h2d(self.gdev.ptr, N.ptr(hv), self.gbytes), "ml_copy_h2d")
+        for i, e in enumerate(self.entries):
+            for d in first[i]:
+                host = d._host
+                if host.nbytes:
+                    if not host.flags.c_contiguous:
+                        d._host = host = np.ascontiguousarray(host)
+                    N.check(L.ml_copy_h2d(d._dev.ptr, N.ptr(host), host.nbytes), "ml_copy_h2d")
+            if first[i] or i == 0:
+                N.check(L.ml_order(N.ML_STREAM_H2D, N.ML_STREAM_COMPUTE))
+            N.check(L.ml_loop_run(C.byref(e.desc)), f"loop {e.loop.name!r}")
+            if last[i]:
+                N.check(L.ml_order(N.ML_STREAM_COMPUTE, N.ML_STREAM_D2H))
+                for d in last[i]:
+                    if d._host.nbytes:
+                        N.check(L.ml_copy_d2h(N.ptr(d._host), d._dev.ptr, d._host.nbytes), "ml_copy_d2h")
+        N.check(L.ml_order(N.ML_STREAM_COMPUTE, N.ML_STREAM_D2H))
+        N.check(L.ml_copy_d2h(N.ptr(hv), self.gdev.ptr, self.gbytes), "ml_copy_d2h")
+        N.check(L.ml_sync_all(), "ml_sync_all")
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            g.buffer[:] = hv[o:o + g.buffer.nbytes].view(g.buffer.dtype)
+        for d in self.all_dats:
+            d._dev.host_newer = False
+            d._dev.device_newer = False
+        self.runs += 1
+
     def replay(self, count: int) -> None:
         """``count`` back-to-back CUDA-graph replays (device throughput; globals
         are written back to the host once, after the last replay)."""
@@ -545,9 +615,13 @@ def run_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig | Non
             for c in range(e.plan.ncolors):
                 config.phase_callback(e.loop.name, c)
     host = config.residency == "host"
-    times = cp.run(config.use_graph, config.time_loops, force_upload=host)
-    if host:
-        _sync_host(cp.written)
+    if host and (config.use_graph or not config.time_loops):
+        cp.run_streamed()
+        times = None
+    else:
+        times = cp.run(config.use_graph, config.time_loops, force_upload=host)
+        if host:
+            _sync_host(cp.written)
     if times is not None:
         _record(collector, cp, times)
     return RunResult(collector.finalize(), time.perf_counter() - t0)

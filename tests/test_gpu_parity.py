@@ -231,15 +231,20 @@ def test_float_results_are_deterministic_run_to_run():
 
 def test_graph_replay_and_host_residency_match_eager():
     results = []
-    for kw in ({}, {"use_graph": True}, {"residency": "host"}):
+    for kw in ({}, {"use_graph": True}, {"residency": "host"},
+               {"residency": "host", "use_graph": True}, {"residency": "host", "time_loops": False}):
         mesh = apps.gen_hex_mesh(12, seed=2)
         prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=2)
         for _ in range(3):                   # replayed: state advances identically
             ml.run_program(prog, mesh, cfg(**kw))
-        results.append((h["q"].fetch(), h["rms"][0].value))
-    for q, r in results[1:]:
+            if kw.get("residency") == "host":     # host edits between runs are uploaded
+                assert not h["q"]._dev.device_newer
+        results.append((h["q"].fetch(), h["rms"][0].value, h["res"].fetch(), h["q_old"].fetch()))
+    for q, r, res, qo in results[1:]:
         np.testing.assert_array_equal(q, results[0][0])
         assert r == results[0][1]
+        np.testing.assert_array_equal(res, results[0][2])
+        np.testing.assert_array_equal(qo, results[0][3])
 
 
 @pytest.mark.parametrize("bs", [32, 256])

@@ -128,6 +128,15 @@ typedef struct ml_loop {
     const int32_t *gather_targets;  /* device [ntargets] target ids of a compacted
                                        list (only targets with incidences), or
                                        NULL: target k is element k of the set   */
+    /* hub splitting (INC gather only; gather_seg NULL disables it): rows of
+     * one heavy target accumulate from zero into partial slots
+     * (gather_seg[row], -1 for ordinary rows), then per hub target
+     * gather_hub_tl[h] += slots gather_hub_off[h]..gather_hub_off[h+1]-1 */
+    const int32_t *gather_seg;      /* device [ntargets rows]                    */
+    void *gather_part;              /* device [slots][dim]                       */
+    int64_t gather_nhub;
+    const int32_t *gather_hub_tl;   /* device [nhub]                             */
+    const int32_t *gather_hub_off;  /* device [nhub+1]                           */
     void *fold_buf;                 /* fold schedule (needs the gather lists):
                                        device [n][INC args][dim] increment slots;
                                        NULL selects the gather schedule          */

@@ -81,7 +81,10 @@ class MlLoop(C.Structure):
                 ("staging", MlStagingDev), ("rlim", C.c_int64),
                 ("gather_ntargets", C.c_int64), ("gather_off", C.c_void_p),
                 ("gather_elem", C.c_void_p), ("gather_pos", C.c_void_p),
-                ("gather_targets", C.c_void_p), ("fold_buf", C.c_void_p),
+                ("gather_targets", C.c_void_p),
+                ("gather_seg", C.c_void_p), ("gather_part", C.c_void_p), ("gather_nhub", C.c_int64),
+                ("gather_hub_tl", C.c_void_p), ("gather_hub_off", C.c_void_p),
+                ("fold_buf", C.c_void_p),
                 ("tile_count", C.c_int64), ("tile_arity", C.c_int32), ("tile_umax", C.c_int32),
                 ("tile_cmax", C.c_int32), ("tile_threads", C.c_int32),
                 ("tile_list_off", C.c_void_p), ("tile_nown", C.c_void_p),

@@ -153,6 +153,13 @@ struct LaunchParams {
     const int32_t *g_elem;
     const uint8_t *g_pos;
     const int32_t *g_tlist;     // compacted target ids (nullptr: identity)
+    // hub targets (INC only): a target with many incidences is split into
+    // several rows; a split row accumulates from zero into partial slot
+    // g_seg[row] (-1: ordinary row), k_gather_hubs folds the slots in order
+    const int32_t *g_seg;
+    void *g_part;
+    int64_t g_nhub;
+    const int32_t *g_hub_tl, *g_hub_off;
     // fold schedule: per (element, INC-arg position) increment slots, element-major
     void *g_buf;
     int32_t g_nw;               // INC arguments per element
@@ -886,9 +893,10 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
         const ArgRt &rg = p.a[G];
         const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
         TG *dst = static_cast<TG *>(rg.data) + tg * rg.se;
+        const int32_t seg = (MM == MINC && p.g_seg) ? __ldg(p.g_seg + t) : -1;
         TG run[DG];
 #pragma unroll
-        for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+        for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : TG(0);
         for (int k = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1); k < ke; ++k) {
             const int64_t e = __ldg(p.g_elem + k);
             const int a = __ldg(p.g_pos + k);
@@ -907,10 +915,35 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
             }
             E::template gather_op<MM, MM == MINC ? 0 : 2, DG>(s, a, run, idx);
         }
+        if (seg >= 0) {
+            TG *part = static_cast<TG *>(p.g_part) + int64_t(seg) * DG;
 #pragma unroll
-        for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+            for (int c = 0; c < DG; ++c) part[c] = run[c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+        }
     }
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
+}
+
+// Hub targets of the gather schedule: value + the partial of each of its
+// rows, in row (= element) order.
+template <class T, int DG>
+__global__ void __launch_bounds__(256) k_gather_hubs(const __grid_constant__ LaunchParams p, int ga) {
+    const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (h >= p.g_nhub) return;
+    const ArgRt &rg = p.a[ga];
+    T *dst = static_cast<T *>(rg.data) + int64_t(__ldg(p.g_hub_tl + h)) * rg.se;
+    const T *part = static_cast<const T *>(p.g_part);
+    T run[DG];
+#pragma unroll
+    for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+    for (int q = __ldg(p.g_hub_off + h), qe = __ldg(p.g_hub_off + h + 1); q < qe; ++q)
+#pragma unroll
+        for (int c = 0; c < DG; ++c) run[c] += part[int64_t(q) * DG + c];
+#pragma unroll
+    for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
 }
 
 // Primary-fold schedule, pass 1 (see PFoldParams): a persistent grid strides
@@ -1481,6 +1514,7 @@ struct FunctorEntry {
     LaunchFn tile;                                   // tile schedule (INC-only, no direct writes)
     LaunchFn tgather;                                // tile-gather variant
     LaunchFn pfold1, pfold2;                         // primary-fold schedule (INC-only)
+    LaunchFn gather_hubs;                            // hub fix-up of the gather schedule (INC)
     int (*pfold_occupancy)();
     int32_t pfold_dgp, pfold_nslot;
 };
@@ -1548,6 +1582,11 @@ struct Registrar {
             once = true;
         }
         k_fold_edges<F, T><<<g, b, bytes, s>>>(p);
+    }
+    static void gather_hubs(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        using S = typename F::template sig<T>;
+        using AG = typename FirstInc<S>::type;
+        k_gather_hubs<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, FirstInc<S>::value);
     }
     static void pfold1(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         static bool once = false;
@@ -1660,6 +1699,7 @@ struct Registrar {
             e.tile = &tile;
             e.tgather = &tgather;
         }
+        if constexpr (SigInfo<S>::gather_ok && SigInfo<S>::ind_inc) e.gather_hubs = &gather_hubs;
         if constexpr (SigInfo<S>::gather_ok) {
             e.gather_occupancy = &gather_occupancy;
             e.gather[0] = &gather;

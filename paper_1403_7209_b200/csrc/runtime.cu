@@ -379,7 +379,18 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
             nparts = std::min<int64_t>(nparts, int64_t(per_sm) * g_dev.sm_count);
         if (nparts > pstride)
             ML_FAIL(ML_EINVAL, "loop '%s': gather schedule needs more reduction scratch", L->name);
+        if (L->gather_seg) {
+            if (!f.gather_hubs || !L->gather_part || !L->gather_hub_tl || !L->gather_hub_off)
+                ML_FAIL(ML_EINVAL, "loop '%s': hub lists incomplete (INC gather only)", L->name);
+            p.g_seg = L->gather_seg;
+            p.g_part = L->gather_part;
+            p.g_nhub = L->gather_nhub;
+            p.g_hub_tl = L->gather_hub_tl;
+            p.g_hub_off = L->gather_hub_off;
+        }
         f.gather[gather_variant()](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+        if (L->gather_seg && L->gather_nhub > 0)
+            f.gather_hubs(p, dim3(unsigned((L->gather_nhub + 255) / 256)), dim3(256), 0, stream);
     } else if (!f.ind_write) {
         const int threads = std::clamp(round_up32(bs), 32, 256);
         p.blocks = nullptr;

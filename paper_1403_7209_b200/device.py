@@ -165,13 +165,18 @@ class ScheduleMirror:
         return self.queue is not None
 
 
+#: incidences per gather row before a target is split across rows (hub targets)
+HUB_ROW = 128
+
+
 class GatherMirror:
     """Device target-centric incidence lists (ml_gather_build) of a loop whose
     indirect writes are all INC, or all WRITE, of one dat.  When fewer than
     half of the target set's elements have incidences (e.g. boundary loops),
     the list is compacted to those targets (``targets``)."""
 
-    __slots__ = ("off", "elem", "pos", "ntargets", "targets", "host")
+    __slots__ = ("off", "elem", "pos", "ntargets", "targets", "host", "seg", "part", "nhub",
+                 "hub_tl", "hub_off")
 
     def __init__(self, loop, n: int):
         import ctypes as C
@@ -196,12 +201,39 @@ class GatherMirror:
         if 2 * touched.size < nset:
             off = np.concatenate([[0], np.cumsum(deg[touched])]).astype(np.int32)
             tl = touched.astype(np.int32)
+        # host copies, one row per target: target subsets (multi-GPU core/boundary
+        # split) and the primary-fold lists are cut from them
+        self.host = {"off": off, "elem": elem, "pos": pos,
+                     "targets": tl if tl is not None else np.arange(off.size - 1, dtype=np.int32)}
+        # hub targets (INC): rows of at most HUB_ROW incidences, accumulated into
+        # partial slots and folded per hub by k_gather_hubs
+        self.seg = self.part = self.hub_tl = self.hub_off = None
+        self.nhub = 0
+        deg = np.diff(off)
+        heavy = np.flatnonzero(deg > HUB_ROW)
+        if heavy.size and wr[0].mode.name == "INC":
+            rows_tl = tl if tl is not None else np.arange(deg.size, dtype=np.int32)
+            nseg = np.where(deg > HUB_ROW, -(-deg // HUB_ROW), 1)
+            row_target = np.repeat(np.arange(deg.size), nseg)
+            first = np.concatenate([[0], np.cumsum(nseg)])[:-1]
+            within = np.arange(row_target.size) - np.repeat(first, nseg)
+            row_lo = off[row_target] + within * HUB_ROW
+            row_hi = np.minimum(row_lo + HUB_ROW, off[row_target + 1])
+            is_hub_row = deg[row_target] > HUB_ROW
+            seg = np.full(row_target.size, -1, np.int32)
+            seg[is_hub_row] = np.arange(int(is_hub_row.sum()), dtype=np.int32)
+            off = np.concatenate([row_lo, row_hi[-1:]]).astype(np.int32)
+            tl = rows_tl[row_target].astype(np.int32)
+            self.nhub = int(heavy.size)
+            hub_off = np.concatenate([[0], np.cumsum(nseg[heavy])]).astype(np.int32)
+            self.seg = _upload(seg)
+            self.part = N.DeviceBuffer(max(int(is_hub_row.sum()) * wr[0].dat.dim * 8, 8))
+            self.hub_tl = _upload(rows_tl[heavy].astype(np.int32))
+            self.hub_off = _upload(hub_off)
+        if tl is not None:
             self.targets = _upload(tl)
         self.ntargets = int(off.size - 1)
         self.off, self.elem, self.pos = _upload(off), _upload(elem), _upload(pos)
-        # host copies: target subsets (multi-GPU core/boundary split) are cut from them
-        self.host = {"off": off, "elem": elem, "pos": pos,
-                     "targets": tl if tl is not None else np.arange(self.ntargets, dtype=np.int32)}
 
     def subset(self, targets_idx: np.ndarray) -> dict:
         """Device lists of a subset of this list's targets (positions into it, ascending)."""

@@ -317,6 +317,10 @@ class _LoopEntry:
             L.gather_elem = self.gather.elem.ptr
             L.gather_pos = self.gather.pos.ptr
             L.gather_targets = self.gather.targets.ptr if self.gather.targets is not None else None
+            if self.gather.seg is not None:
+                g = self.gather
+                L.gather_seg, L.gather_part, L.gather_nhub = g.seg.ptr, g.part.ptr, g.nhub
+                L.gather_hub_tl, L.gather_hub_off = g.hub_tl.ptr, g.hub_off.ptr
         self.schedule = None
         if (self.gather is None and config.dataflow and sched in ("flow", "arrival")
                 and self.plan.has_writes and self.plan.ncolors > 1 and not _inc_aliased(loop)):
@@ -541,7 +545,7 @@ class CompiledProgram:
             elif e.tile is not None:
                 total += 1
             elif e.gather is not None or not e.plan.has_writes:
-                total += 1
+                total += 1 + (1 if e.gather is not None and e.gather.nhub else 0)
             elif e.schedule is not None or (e.staging is not None and e.desc.staging.arrive):
                 total += 1
             else:

@@ -495,7 +495,8 @@ class StreamRank:
 
     def _build_split(self, i: int, names: tuple):
         e = self.entries[i]
-        if e.gather is None or e.pfold is not None or not names or e.loop.iter_set.size == 0:
+        if (e.gather is None or e.pfold is not None or e.gather.nhub or not names
+                or e.loop.iter_set.size == 0):
             return None
         ex_names = set(names)
         loop = e.loop

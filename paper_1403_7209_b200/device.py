@@ -178,7 +178,7 @@ class GatherMirror:
     __slots__ = ("off", "elem", "pos", "ntargets", "targets", "host", "seg", "part", "nhub",
                  "hub_tl", "hub_off")
 
-    def __init__(self, loop, n: int):
+    def __init__(self, loop, n: int, hubs: bool = False):
         import ctypes as C
         wr = [a for a in loop.args if a.kind == "indirect" and a.mode.name != "READ"]
         nset = wr[0].dat.set.size
@@ -211,7 +211,7 @@ class GatherMirror:
         self.nhub = 0
         deg = np.diff(off)
         heavy = np.flatnonzero(deg > HUB_ROW)
-        if heavy.size and wr[0].mode.name == "INC":
+        if hubs and heavy.size and wr[0].mode.name == "INC":
             rows_tl = tl if tl is not None else np.arange(deg.size, dtype=np.int32)
             nseg = np.where(deg > HUB_ROW, -(-deg // HUB_ROW), 1)
             row_target = np.repeat(np.arange(deg.size), nseg)
@@ -446,11 +446,13 @@ def tile_mirror(loop, mesh, n: int, budget: int, cmax: int, coord_dat: str | Non
     return cache[key]
 
 
-def gather_mirror(loop, plan) -> GatherMirror:
+def gather_mirror(loop, plan, hubs: bool = False) -> GatherMirror:
+    """Gather lists of ``loop``; ``hubs`` splits heavy targets into several
+    rows (the gather kernel only — the fold kernels need one row per target)."""
     cache = plan.__dict__.setdefault("_gathers", {})
-    key = loop.signature()
+    key = (loop.signature(), hubs)
     if key not in cache:
-        cache[key] = GatherMirror(loop, plan.n)
+        cache[key] = GatherMirror(loop, plan.n, hubs)
     return cache[key]
 
 

@@ -310,7 +310,7 @@ class _LoopEntry:
             self.fold = N.DeviceBuffer(self.n * len(inc) * dgp * inc[0].dat.dtype.itemsize)
             L.fold_buf = self.fold.ptr
         elif sched in ("gather", "fold") and self.n > 0 and gather_eligible(loop):
-            self.gather = gather_mirror(loop, self.plan)
+            self.gather = gather_mirror(loop, self.plan, hubs=True)
         if self.gather is not None and self.pfold is None:
             L.gather_ntargets = self.gather.ntargets
             L.gather_off = self.gather.off.ptr

@@ -536,9 +536,9 @@ class StreamRank:
         return out
 
     # -- one program run ------------------------------------------------------------------
-    def _image(self):
+    def _image(self, capturing: bool = False):
         ev = self.__dict__.get("_img_event")
-        if ev is not None:
+        if ev is not None and not capturing:
             ev.synchronize()            # the previous run's copy has read the pinned image
         img = self.image.numpy()
         rp = self.rp
@@ -553,8 +553,9 @@ class StreamRank:
                 img[o:o + ident.nbytes] = ident.view(np.uint8)
         with self.torch.cuda.stream(self.lib_stream):
             self.arena.copy_(self.image, non_blocking=True)
-        self._img_event = self.torch.cuda.Event()
-        self._img_event.record(self.lib_stream)
+        if not capturing:
+            self._img_event = self.torch.cuda.Event()
+            self._img_event.record(self.lib_stream)
 
     def _pack(self, name: str):
         N = self.N
@@ -602,17 +603,21 @@ class StreamRank:
     def _launch(self, desc) -> None:
         self.N.check(self.N.lib().ml_loop_run(self.C.byref(desc)), f"loop {desc.name!r}")
 
-    def run(self, overlap: bool = True) -> int:
-        """Enqueue one program run; returns the halo messages sent."""
+    def run(self, overlap: bool = True, capturing: bool = False) -> int:
+        """Enqueue one program run; returns the halo messages sent.  With
+        ``capturing`` (inside a CUDA-graph capture) no host synchronisation or
+        timing event is issued."""
         torch, rp, tr = self.torch, self.rp, self.transport
         dirty = rp.__dict__.setdefault("dirty", {})
         messages = 0
-        self._image()
+        self._image(capturing)
         self.events = []
         for i, e in enumerate(self.entries):
             reads, writes = rp.roles[i]
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev0.record(self.lib_stream)
+            ev0 = None
+            if not capturing:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record(self.lib_stream)
             names = [n for n in reads if dirty.get(n)]
             packed = [(n, *self._pack(n)) for n in names]
             messages += sum(len(p[1]) for p in packed)
@@ -655,13 +660,37 @@ class StreamRank:
                                                            part.dim, code, dt), "ml_combine_ranks")
             for n in writes:
                 dirty[n] = True
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev1.record(self.lib_stream)
-            self.events.append((ev0, ev1))
+            if not capturing:
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev1.record(self.lib_stream)
+                self.events.append((ev0, ev1))
         for e in self.entries:
             for d in e.written:
                 d._dev.device_newer = True
         return messages
+
+    def capture(self, overlap: bool = True):
+        """Capture one program run (loops, pack/unpack, NCCL exchanges and
+        reductions, the overlap fork/join) as a CUDA graph on the compute
+        stream; replay() then launches a whole rank step with one call (the
+        host no longer paces the GPU).  NCCL transport only."""
+        if self.transport.name != "nccl":
+            raise ExecError("graph capture needs the NCCL transport")
+        torch = self.torch
+        self.finish()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.lib_stream):
+            msgs = self.run(overlap, capturing=True)
+        self.graph, self.graph_messages = g, msgs
+        return msgs
+
+    def replay(self) -> int:
+        with self.torch.cuda.stream(self.lib_stream):
+            self.graph.replay()
+        for e in self.entries:
+            for d in e.written:
+                d._dev.device_newer = True
+        return self.graph_messages
 
     def loop_seconds(self) -> list:
         """Device time of each loop of the last run (exchange + launches + fold)."""
@@ -747,8 +776,11 @@ def init_distributed(config=None):
     if not dist.is_initialized():
         use_nccl = torch.cuda.is_available() and os.environ.get("ML_TRANSPORT", "") != "gloo"
         if use_nccl:
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group(backend="nccl" if use_nccl else "gloo")
+            dev = int(os.environ.get("ML_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+            torch.cuda.set_device(dev)
+            dist.init_process_group(backend="nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend="gloo")
     transport = NcclTransport() if dist.get_backend() == "nccl" else GlooTransport()
     return dist.get_rank(), dist.get_world_size(), transport
 
@@ -840,25 +872,31 @@ def bench_distributed(args, metric):
     setup["layout_and_local_mesh_s"] = round(time.perf_counter() - t0, 3)
     if not isinstance(dev, StreamRank):
         raise ExecError("bench_distributed needs the stream-ordered rank executor")
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 2)):
         dev.run()
     dev.finish()
+    dev.run()                         # per-loop device times of one eager step (reported)
+    dev.finish()
+    loop_s = dev.loop_seconds()
+    graphed = transport.name == "nccl" and os.environ.get("ML_RANK_GRAPH", "1") == "1"
+    if graphed:                       # one graph launch per rank step (NCCL inside)
+        dev.capture()
+    step = dev.replay if graphed else dev.run
     dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with clock_sampler(local_dev) as clk:
         time.sleep(0.3)
         for _ in range(max(3, args.steps)):                  # keep the GPU busy while sampling starts
-            dev.run()
+            step()
         dev.finish()
         dist.barrier()
         msgs = 0
         start.record(dev.lib_stream)
         for _ in range(args.steps):
-            msgs += dev.run()
+            msgs += step()
         stop.record(dev.lib_stream)
         dev.finish()
     dev_s = start.elapsed_time(stop) * 1e-3
-    loop_s = dev.loop_seconds()
     # end to end: host buffers in and out every step
     for d in rp.dats.values():
         d._pull()
@@ -895,6 +933,7 @@ def bench_distributed(args, metric):
                            "parallelism": f"owner-compute dp{world} (RCB)",
                            "transport": transport.name, "halo_nodes_per_rank": halo,
                            "overlapped_loops": split,
+                           "cuda_graph": graphed,
                            "l2": "per-rank working set streamed each step",
                            "timing": "CUDA events on each rank's compute stream around K runs, "
                                      "max over ranks", "setup": setup},
@@ -910,3 +949,4 @@ def bench_distributed(args, metric):
                 "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     dist.barrier()
+    dist.destroy_process_group()

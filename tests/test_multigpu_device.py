@@ -107,3 +107,52 @@ def test_proxy_two_ranks_on_device_vs_oracle(sched, executor):
         np.testing.assert_allclose(out["q"], ref_q, rtol=1e-12, atol=1e-12 * np.abs(ref_q).max())
         np.testing.assert_allclose(out["rms"], [r.value for r in h["rms"]], rtol=1e-12)
         np.testing.assert_array_equal(out["dt"], [r.value for r in h["dt_min"]])
+
+
+def _graph_worker(port, q):
+    """One NCCL rank: a CUDA-graph-captured rank step (loops, NCCL all-gather of
+    the reductions, rank fold) replayed twice must equal two eager steps."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1",
+                      LOCAL_RANK="0")
+    sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+    try:
+        import paper_1403_7209_b200 as ml
+        from paper_1403_7209_b200 import apps
+        from paper_1403_7209_b200.multigpu import setup_distributed
+        outs = []
+        for graphed in (False, True):
+            mesh = apps.gen_hex_mesh(14, seed=6)
+            prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=6)
+            ml.renumber_mesh(mesh)
+            cfg = ml.BackendConfig(nranks=1, partitioner="rcb", device=0)
+            rp, dev, tr, layout, cfg = setup_distributed(prog, mesh, cfg)
+            assert tr.name == "nccl"
+            dev.run()
+            dev.finish()
+            if graphed:
+                dev.capture()
+                dev.replay()
+                dev.replay()
+            else:
+                dev.run()
+                dev.run()
+            dev.finish()
+            outs.append((rp.dats["q"].fetch(), [v.buffer.copy() for v in rp.values.values()]))
+        q.put((outs[0][0], outs[1][0], outs[0][1], outs[1][1], None))
+    except Exception:
+        import traceback
+        q.put((None, None, None, None, traceback.format_exc()))
+
+
+def test_rank_step_cuda_graph_with_nccl_matches_eager():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_graph_worker, args=(_free_port(), q))
+    p.start()
+    a, b, va, vb, err = q.get(timeout=600)
+    p.join(timeout=60)
+    assert err is None, err
+    np.testing.assert_array_equal(a, b)
+    for x, y in zip(va, vb):
+        np.testing.assert_array_equal(x, y)

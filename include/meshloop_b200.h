@@ -175,6 +175,9 @@ typedef struct ml_loop {
     const int32_t *pf_off2, *pf_elem2, *pf_tl2;
     const uint8_t *pf_pos2;
     void *pf_slots;
+    int32_t pf_own_kb;              /* shared memory (KB per CTA) for the targets'
+                                       own READ rows in pass 1; 0: read from L1/L2 */
+    int32_t pf_pad;
 } ml_loop_t;
 
 typedef struct ml_device_info {

@@ -129,6 +129,11 @@ struct PFoldParams {
     const uint8_t *pos2;                 // INC-argument position (>= 1) of each
     void *slots;                         // [n][nslot][dgp]
     int32_t nslot, dgp;
+    // own-row staging: READ dats read through the first INC argument's column
+    // (the target itself) are copied once per target to shared memory
+    int32_t own_ngrp;
+    int32_t own_garg[MAX_TGROUPS], own_gdim[MAX_TGROUPS], own_goff[MAX_TGROUPS];
+    int8_t own_grp[MAX_ARGS];
 };
 
 struct LaunchParams {
@@ -640,6 +645,25 @@ struct Engine {
             }
         }
     }
+    // primary fold: READ args on the target's own column read its staged rows
+    template <class TO, size_t... Is>
+    __device__ __forceinline__ static void own_views(Slots &s, const LaunchParams &p, TO *own,
+                                                     cuda::std::index_sequence<Is...>) {
+        (own_view_one<Is>(s, p, own), ...);
+    }
+    template <size_t I, class TO>
+    __device__ __forceinline__ static void own_view_one(Slots &s, const LaunchParams &p, TO *own) {
+        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
+        if constexpr (A::kind == KI && A::mode == MR) {
+            const int g = p.pf.own_grp[I];
+            if (g >= 0) {
+                using T = typename A::type;
+                auto &sl = cuda::std::get<I>(s);
+                sl.ptr = reinterpret_cast<T *>(own) + int64_t(p.pf.own_goff[g]) * blockDim.x;
+                sl.sc = blockDim.x;
+            }
+        }
+    }
     // primary fold: INC arguments at positions >= 1 -> the element's slots
     template <int DGP, size_t... Is>
     __device__ __forceinline__ static void stage_rest(Slots &s, void *row, cuda::std::index_sequence<Is...>) {
@@ -972,22 +996,34 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
     constexpr int NW = ((As::kind == KI && As::mode == MINC) + ...);
     constexpr int DGP = PFoldShape<TG, DG>::DGP;
     __shared__ double red[32];
+    extern __shared__ __align__(16) char dsm[];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     typename E::Slots s;
     E::init_globals(s, p, idx);
     const PFoldParams &pf = p.pf;
+    TG *own = reinterpret_cast<TG *>(dsm) + threadIdx.x;      // this thread's column
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t - threadIdx.x < pf.n1;
          t += int64_t(gridDim.x) * blockDim.x) {
         if (t >= pf.n1) continue;
         const ArgRt &rg = p.a[G];
         const int64_t tg = pf.tl1 ? int64_t(__ldg(pf.tl1 + t)) : t;
         TG *dst = static_cast<TG *>(rg.data) + tg * rg.se;
+        // the target's own READ rows, once per target (consecutive targets: coalesced)
+        for (int g = 0; g < pf.own_ngrp; ++g) {
+            const ArgRt &r = p.a[pf.own_garg[g]];
+            const TG *src = static_cast<const TG *>(r.data) + tg * r.se;
+            TG *o = own + int64_t(pf.own_goff[g]) * blockDim.x;
+            const int dim = pf.own_gdim[g];
+#pragma unroll 4
+            for (int c = 0; c < dim; ++c) o[c * blockDim.x] = __ldg(src + c * r.sc);
+        }
         TG run[DG];
 #pragma unroll
         for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
         for (int k = __ldg(pf.off1 + t), ke = __ldg(pf.off1 + t + 1); k < ke; ++k) {
             const int64_t e = __ldg(pf.elem1 + k);
             E::init_elem(s, p, e, nullptr, idx);
+            if (pf.own_ngrp > 0) E::own_views(s, p, own, idx);
             E::call(s, p, e, idx);
             E::template gather_op<MINC, 0, DG>(s, 0, run, idx);
             if constexpr (NW > 1)
@@ -1515,7 +1551,7 @@ struct FunctorEntry {
     LaunchFn tgather;                                // tile-gather variant
     LaunchFn pfold1, pfold2;                         // primary-fold schedule (INC-only)
     LaunchFn gather_hubs;                            // hub fix-up of the gather schedule (INC)
-    int (*pfold_occupancy)();
+    int (*pfold_occupancy)(size_t smem);
     int32_t pfold_dgp, pfold_nslot;
 };
 
@@ -1588,20 +1624,27 @@ struct Registrar {
         using AG = typename FirstInc<S>::type;
         k_gather_hubs<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, FirstInc<S>::value);
     }
-    static void pfold1(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
-        static bool once = false;
-        if (!once) {
-            cudaFuncSetAttribute(k_pfold1<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-            once = true;
+    static void pfold_attrs(size_t bytes) {
+        static int carve = -1;
+        const int want = bytes ? 100 : 0;
+        if (carve != want) {
+            cudaFuncSetAttribute(k_pfold1<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, want);
+            carve = want;
         }
-        k_pfold1<F, T><<<g, b, 0, s>>>(p);
+        static size_t opted = 48 * 1024;
+        if (bytes > opted) {
+            cudaFuncSetAttribute(k_pfold1<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+            opted = bytes;
+        }
     }
-    static int pfold_occupancy() {
-        static int n = -1;
-        if (n < 0) {
-            cudaFuncSetAttribute(k_pfold1<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pfold1<F, T>, 256, 0) != cudaSuccess) n = 0;
-        }
+    static void pfold1(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
+        pfold_attrs(bytes);
+        k_pfold1<F, T><<<g, b, bytes, s>>>(p);
+    }
+    static int pfold_occupancy(size_t bytes) {
+        pfold_attrs(bytes);
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pfold1<F, T>, 256, bytes) != cudaSuccess) n = 0;
         return n;
     }
     static void pfold2(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {

@@ -315,11 +315,41 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         pf.slots = L->pf_slots;
         pf.nslot = f.pfold_nslot;
         pf.dgp = f.pfold_dgp;
-        const int occ = f.pfold_occupancy ? f.pfold_occupancy() : 0;
+        // own-row staging: READ dats on the first INC argument's column
+        pf.own_ngrp = 0;
+        for (int i = 0; i < MAX_ARGS; ++i) pf.own_grp[i] = -1;
+        size_t own_bytes = 0;
+        if (L->pf_own_kb > 0) {
+            int g0 = -1;
+            for (int i = 0; i < f.nargs && g0 < 0; ++i)
+                if (L->args[i].kind == ML_INDIRECT && L->args[i].mode == ML_INC) g0 = i;
+            const void *gdat[MAX_TGROUPS] = {};
+            int comps = 0;
+            const int budget = L->pf_own_kb * 1024 / (8 * 256);
+            for (int i = 0; i < f.nargs && g0 >= 0; ++i) {
+                const ml_arg_t &a = L->args[i];
+                if (a.kind != ML_INDIRECT || a.mode != ML_READ || p.a[i].map != p.a[g0].map) continue;
+                int g = -1;
+                for (int k = 0; k < pf.own_ngrp; ++k)
+                    if (gdat[k] == a.data) g = k;
+                if (g < 0) {
+                    if (pf.own_ngrp >= MAX_TGROUPS || comps + a.dim > budget) continue;
+                    g = pf.own_ngrp++;
+                    gdat[g] = a.data;
+                    pf.own_garg[g] = i;
+                    pf.own_gdim[g] = a.dim;
+                    pf.own_goff[g] = comps;
+                    comps += a.dim;
+                }
+                pf.own_grp[i] = int8_t(g);
+            }
+            own_bytes = size_t(comps) * 8 * 256;
+        }
+        const int occ = f.pfold_occupancy ? f.pfold_occupancy(own_bytes) : 0;
         nparts = std::max<int64_t>(1, std::min<int64_t>((pf.n1 + 255) / 256,
                                                         occ > 0 ? int64_t(occ) * g_dev.sm_count : INT64_MAX));
         if (nparts > pstride) ML_FAIL(ML_EINVAL, "loop '%s': primary fold needs more scratch", L->name);
-        f.pfold1(p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+        f.pfold1(p, dim3(unsigned(nparts)), dim3(256), own_bytes, stream);
         if (pf.n2 > 0) {
             const int64_t g2 = std::min<int64_t>((pf.n2 + 255) / 256, int64_t(8) * g_dev.sm_count);
             f.pfold2(p, dim3(unsigned(g2)), dim3(256), 0, stream);

@@ -85,6 +85,8 @@ class BackendConfig:
     tile_smem_kb: int = 100                 # tile schedule: shared memory per tile (2 CTAs/SM)
     tile_cmax: int = 512                    # tile schedule: max owned targets per tile
     tile_threads: int = 256                 # tile schedule: CTA size (256: 2 CTAs/SM, 128: 4)
+    pfold_own_kb: int = 0                   # pfold pass 1: smem per CTA for the targets' own rows
+                                            # (0: from L1/L2 — faster on B200, see profiles/)
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -285,6 +287,7 @@ class _LoopEntry:
             L.pf_n1, L.pf_off1, L.pf_elem1, L.pf_tl1 = pf.n1, pf.off1.ptr, pf.elem1.ptr, pf.tl1.ptr
             L.pf_n2, L.pf_off2, L.pf_elem2, L.pf_tl2 = pf.n2, pf.off2.ptr, pf.elem2.ptr, pf.tl2.ptr
             L.pf_pos2 = pf.pos2.ptr
+            L.pf_own_kb = int(config.pfold_own_kb)
             L.functor = self.functor
             nb = C.c_uint64()
             N.check(N.lib().ml_loop_pfold_slot_bytes(C.byref(L), C.byref(nb)))
@@ -577,6 +580,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
            config.dataflow, config.inc_staging, config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.flow_windows,
            config.flow_window_l2_fraction, config.tile_smem_kb, config.tile_cmax, config.tile_threads, config.coord_dat,
+           config.pfold_own_kb,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

@@ -24,6 +24,7 @@ ap.add_argument("--kd", type=int, default=0, help="k-d leaf size: renumber nodes
 ap.add_argument("--tile-smem", type=int, nargs="+", default=[100])
 ap.add_argument("--tile-cmax", type=int, default=512)
 ap.add_argument("--tile-threads", type=int, nargs="+", default=[256])
+ap.add_argument("--own-kb", type=int, nargs="+", default=[100])
 
 args = ap.parse_args()
 mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)
@@ -55,17 +56,19 @@ if args.kd:
         m = next(m for m in mesh.maps.values() if m.from_set.name == sname)
         apply_permutation(mesh, row_order_by_targets(mesh, m))
 import itertools
-for bs, kb, nt in itertools.product(args.block_size, args.tile_smem, args.tile_threads):
+for bs, kb, nt, okb in itertools.product(args.block_size, args.tile_smem, args.tile_threads, args.own_kb):
     for sched in args.inc_schedule:
         if sched != "tile" and (kb != args.tile_smem[0] or nt != args.tile_threads[0]):
             continue
+        if sched != "pfold" and okb != args.own_kb[0]:
+            continue
         cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched, tile_smem_kb=kb,
-                               tile_cmax=args.tile_cmax, tile_threads=nt)
+                               tile_cmax=args.tile_cmax, tile_threads=nt, pfold_own_kb=okb)
         for i in range(args.iters):
             r = ml.run_program(prog, mesh, cfg)
             if i + 1 < args.iters:
                 continue
             tot = sum(p.time_sec for p in r.perf)
-            print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} tile_kb={kb} nt={nt}] total={tot*1e3:.3f}ms " +
+            print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} tile_kb={kb} nt={nt} own={okb}] total={tot*1e3:.3f}ms " +
                   " ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf),
                   flush=True)

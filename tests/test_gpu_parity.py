@@ -477,13 +477,14 @@ def test_tile_schedule_int64_fuzz_and_diffusion(rng):
     np.testing.assert_array_equal(h["u"].fetch(), g["exec/diffusion_n8_int64_s3/u"])
 
 
-def test_pfold_schedule_raw_accumulators_reductions_and_determinism():
+@pytest.mark.parametrize("own_kb", [0, 100])
+def test_pfold_schedule_raw_accumulators_reductions_and_determinism(own_kb):
     """Primary fold: raw INC accumulators within tolerance of the serial oracle,
     int64 bit-exact (fuzz + diffusion), MIN/MAX/READ globals counted once per
-    element, bitwise run to run."""
+    element, bitwise run to run; with and without own-row staging."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(12)
     bulk.run_program(rprog[:5], resolve_kernel)
-    c = cfg(inc_schedule="pfold")
+    c = cfg(inc_schedule="pfold", pfold_own_kb=own_kb)
     ml.run_program(prog[:5], mesh, c)
     for k in ("grad", "res"):
         close(h[k].fetch(), rh[k].fetch(), what=k)
@@ -496,7 +497,7 @@ def test_pfold_schedule_raw_accumulators_reductions_and_determinism():
     g = golden("exec.npz")
     for soa in (4, None):
         mesh, loop, acc, lo, hi = _cases.mixmax_case(auto_soa_threshold=soa)
-        ml.run_program([loop], mesh, cfg(inc_schedule="pfold"))
+        ml.run_program([loop], mesh, cfg(inc_schedule="pfold", pfold_own_kb=own_kb))
         np.testing.assert_array_equal(acc.fetch(), g["exec/mixmax/acc"])
         assert [lo.value, hi.value] == g["exec/mixmax/lohi"].tolist()
     rng = np.random.default_rng(11)
@@ -505,5 +506,5 @@ def test_pfold_schedule_raw_accumulators_reductions_and_determinism():
         ref_mesh, ref_loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
         oserial.run_loop(ref_loop)
         mesh, loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
-        ml.run_program([loop], mesh, cfg(inc_schedule="pfold"))
+        ml.run_program([loop], mesh, cfg(inc_schedule="pfold", pfold_own_kb=own_kb))
         np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref_mesh.dats["vals"].fetch())

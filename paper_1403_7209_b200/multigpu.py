@@ -879,8 +879,17 @@ def bench_distributed(args, metric):
     dev.finish()
     loop_s = dev.loop_seconds()
     graphed = transport.name == "nccl" and os.environ.get("ML_RANK_GRAPH", "1") == "1"
+    graph_error = None
     if graphed:                       # one graph launch per rank step (NCCL inside)
-        dev.capture()
+        try:
+            dev.capture()
+        except Exception as ex:       # capture unsupported by this NCCL/torch: run eagerly
+            graphed, graph_error = False, f"{type(ex).__name__}: {ex}"[:200]
+            dev.finish()
+    flags = torch.tensor([int(graphed)], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN)          # every rank must take the same path
+    if graphed and not int(flags.item()):
+        graphed = False
     step = dev.replay if graphed else dev.run
     dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -933,7 +942,7 @@ def bench_distributed(args, metric):
                            "parallelism": f"owner-compute dp{world} (RCB)",
                            "transport": transport.name, "halo_nodes_per_rank": halo,
                            "overlapped_loops": split,
-                           "cuda_graph": graphed,
+                           "cuda_graph": graphed, "cuda_graph_error": graph_error,
                            "l2": "per-rank working set streamed each step",
                            "timing": "CUDA events on each rank's compute stream around K runs, "
                                      "max over ranks", "setup": setup},

@@ -169,6 +169,84 @@ class ScheduleMirror:
 HUB_ROW = 128
 
 
+def gather_lists_host(loop, n: int, hubs: bool = False, hub_row: int = HUB_ROW) -> dict:
+    """Host arrays of the gather schedule (ml_gather_build): per target row its
+    (element, written-argument position) incidences in serial order.  Rows are
+    compacted to touched targets when fewer than half are touched
+    (``targets``: row -> target id, else None = identity).  With ``hubs`` (INC
+    only) a target with more than ``hub_row`` incidences is split into rows of
+    at most ``hub_row``: ``seg[row]`` is the row's partial slot (-1: ordinary
+    row), ``hub_tl``/``hub_off`` list each hub target and its slots.
+    ``host`` keeps the one-row-per-target lists (pfold, multi-GPU subsets)."""
+    import ctypes as C
+    wr = [a for a in loop.args if a.kind == "indirect" and a.mode.name != "READ"]
+    nset = wr[0].dat.set.size
+    cols = [np.ascontiguousarray(a.map.table[:n, a.slot], dtype=np.int64) for a in wr]
+    L = N.lib()
+    h = C.c_void_p()
+    cptr = (C.c_void_p * len(cols))(*[N.ptr(c) for c in cols])
+    N.check(L.ml_gather_build(n, len(cols), cptr, nset, C.byref(h)), "ml_gather_build")
+    try:
+        off = np.empty(nset + 1, np.int32)
+        elem = np.empty(max(n * len(cols), 1), np.int32)
+        pos = np.empty(max(n * len(cols), 1), np.uint8)
+        N.check(L.ml_gather_export(h, N.ptr(off), N.ptr(elem), N.ptr(pos)), "ml_gather_export")
+    finally:
+        L.ml_gather_free(h)
+    deg = np.diff(off)
+    touched = np.flatnonzero(deg)
+    tl = None
+    if 2 * touched.size < nset:
+        off = np.concatenate([[0], np.cumsum(deg[touched])]).astype(np.int32)
+        tl = touched.astype(np.int32)
+    out = {"host": {"off": off, "elem": elem, "pos": pos,
+                    "targets": tl if tl is not None else np.arange(off.size - 1, dtype=np.int32)},
+           "elem": elem, "pos": pos, "seg": None, "nhub": 0, "nslots": 0,
+           "hub_tl": None, "hub_off": None}
+    deg = np.diff(off)
+    heavy = np.flatnonzero(deg > hub_row)
+    if hubs and heavy.size and wr[0].mode.name == "INC":
+        rows_tl = tl if tl is not None else np.arange(deg.size, dtype=np.int32)
+        nseg = np.where(deg > hub_row, -(-deg // hub_row), 1)
+        row_target = np.repeat(np.arange(deg.size), nseg)
+        first = np.concatenate([[0], np.cumsum(nseg)])[:-1]
+        within = np.arange(row_target.size) - np.repeat(first, nseg)
+        row_lo = off[row_target] + within * hub_row
+        row_hi = np.minimum(row_lo + hub_row, off[row_target + 1])
+        is_hub_row = deg[row_target] > hub_row
+        seg = np.full(row_target.size, -1, np.int32)
+        seg[is_hub_row] = np.arange(int(is_hub_row.sum()), dtype=np.int32)
+        off = np.concatenate([row_lo, row_hi[-1:]]).astype(np.int32)
+        tl = rows_tl[row_target].astype(np.int32)
+        out.update(seg=seg, nhub=int(heavy.size), nslots=int(is_hub_row.sum()),
+                   hub_tl=rows_tl[heavy].astype(np.int32),
+                   hub_off=np.concatenate([[0], np.cumsum(nseg[heavy])]).astype(np.int32))
+    out["off"], out["targets"] = off, tl
+    return out
+
+
+def pfold_lists_host(host: dict) -> dict:
+    """Primary-fold lists from one-row-per-target gather lists: per target, its
+    incidences through the first INC argument (``1``) and through the others
+    (``2``, with positions), element ascending; only targets that have any."""
+    off, elem, pos, tl = host["off"], host["elem"], host["pos"], host["targets"]
+    nt = off.size - 1
+    owner = np.repeat(np.arange(nt), np.diff(off))
+    e, p_ = elem[:off[-1]], pos[:off[-1]]
+    out = {}
+    for which in (1, 2):
+        m = (p_ == 0) if which == 1 else (p_ > 0)
+        cnt = np.bincount(owner[m], minlength=nt)
+        keep = np.flatnonzero(cnt)
+        out[f"n{which}"] = int(keep.size)
+        out[f"off{which}"] = np.concatenate([[0], np.cumsum(cnt[keep])]).astype(np.int32)
+        out[f"elem{which}"] = np.ascontiguousarray(e[m], dtype=np.int32)
+        out[f"tl{which}"] = np.ascontiguousarray(tl[keep], dtype=np.int32)
+        if which == 2:
+            out["pos2"] = np.ascontiguousarray(p_[m], dtype=np.uint8)
+    return out
+
+
 class GatherMirror:
     """Device target-centric incidence lists (ml_gather_build) of a loop whose
     indirect writes are all INC, or all WRITE, of one dat.  When fewer than
@@ -179,61 +257,19 @@ class GatherMirror:
                  "hub_tl", "hub_off")
 
     def __init__(self, loop, n: int, hubs: bool = False):
-        import ctypes as C
         wr = [a for a in loop.args if a.kind == "indirect" and a.mode.name != "READ"]
-        nset = wr[0].dat.set.size
-        cols = [np.ascontiguousarray(a.map.table[:n, a.slot], dtype=np.int64) for a in wr]
-        L = N.lib()
-        h = C.c_void_p()
-        cptr = (C.c_void_p * len(cols))(*[N.ptr(c) for c in cols])
-        N.check(L.ml_gather_build(n, len(cols), cptr, nset, C.byref(h)), "ml_gather_build")
-        try:
-            off = np.empty(nset + 1, np.int32)
-            elem = np.empty(max(n * len(cols), 1), np.int32)
-            pos = np.empty(max(n * len(cols), 1), np.uint8)
-            N.check(L.ml_gather_export(h, N.ptr(off), N.ptr(elem), N.ptr(pos)), "ml_gather_export")
-        finally:
-            L.ml_gather_free(h)
-        deg = np.diff(off)
-        touched = np.flatnonzero(deg)
-        self.targets = None
-        tl = None
-        if 2 * touched.size < nset:
-            off = np.concatenate([[0], np.cumsum(deg[touched])]).astype(np.int32)
-            tl = touched.astype(np.int32)
-        # host copies, one row per target: target subsets (multi-GPU core/boundary
-        # split) and the primary-fold lists are cut from them
-        self.host = {"off": off, "elem": elem, "pos": pos,
-                     "targets": tl if tl is not None else np.arange(off.size - 1, dtype=np.int32)}
-        # hub targets (INC): rows of at most HUB_ROW incidences, accumulated into
-        # partial slots and folded per hub by k_gather_hubs
+        h = gather_lists_host(loop, n, hubs)
+        self.host = h["host"]
         self.seg = self.part = self.hub_tl = self.hub_off = None
-        self.nhub = 0
-        deg = np.diff(off)
-        heavy = np.flatnonzero(deg > HUB_ROW)
-        if hubs and heavy.size and wr[0].mode.name == "INC":
-            rows_tl = tl if tl is not None else np.arange(deg.size, dtype=np.int32)
-            nseg = np.where(deg > HUB_ROW, -(-deg // HUB_ROW), 1)
-            row_target = np.repeat(np.arange(deg.size), nseg)
-            first = np.concatenate([[0], np.cumsum(nseg)])[:-1]
-            within = np.arange(row_target.size) - np.repeat(first, nseg)
-            row_lo = off[row_target] + within * HUB_ROW
-            row_hi = np.minimum(row_lo + HUB_ROW, off[row_target + 1])
-            is_hub_row = deg[row_target] > HUB_ROW
-            seg = np.full(row_target.size, -1, np.int32)
-            seg[is_hub_row] = np.arange(int(is_hub_row.sum()), dtype=np.int32)
-            off = np.concatenate([row_lo, row_hi[-1:]]).astype(np.int32)
-            tl = rows_tl[row_target].astype(np.int32)
-            self.nhub = int(heavy.size)
-            hub_off = np.concatenate([[0], np.cumsum(nseg[heavy])]).astype(np.int32)
-            self.seg = _upload(seg)
-            self.part = N.DeviceBuffer(max(int(is_hub_row.sum()) * wr[0].dat.dim * 8, 8))
-            self.hub_tl = _upload(rows_tl[heavy].astype(np.int32))
-            self.hub_off = _upload(hub_off)
-        if tl is not None:
-            self.targets = _upload(tl)
-        self.ntargets = int(off.size - 1)
-        self.off, self.elem, self.pos = _upload(off), _upload(elem), _upload(pos)
+        self.nhub = h["nhub"]
+        if h["seg"] is not None:
+            self.seg = _upload(h["seg"])
+            self.part = N.DeviceBuffer(max(h["nslots"] * wr[0].dat.dim * 8, 8))
+            self.hub_tl = _upload(h["hub_tl"])
+            self.hub_off = _upload(h["hub_off"])
+        self.targets = _upload(h["targets"]) if h["targets"] is not None else None
+        self.ntargets = int(h["off"].size - 1)
+        self.off, self.elem, self.pos = _upload(h["off"]), _upload(h["elem"]), _upload(h["pos"])
 
     def subset(self, targets_idx: np.ndarray) -> dict:
         """Device lists of a subset of this list's targets (positions into it, ascending)."""
@@ -259,23 +295,10 @@ class PFoldMirror:
     __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2")
 
     def __init__(self, g: GatherMirror):
-        h = g.host
-        off, elem, pos, tl = h["off"], h["elem"], h["pos"], h["targets"]
-        nt = off.size - 1
-        owner = np.repeat(np.arange(nt), np.diff(off))
-        e, p_ = elem[:off[-1]], pos[:off[-1]]
-        for which in (1, 2):
-            m = (p_ == 0) if which == 1 else (p_ > 0)
-            rows = owner[m]
-            cnt = np.bincount(rows, minlength=nt)
-            keep = np.flatnonzero(cnt)
-            o = np.concatenate([[0], np.cumsum(cnt[keep])]).astype(np.int32)
-            setattr(self, f"n{which}", int(keep.size))
-            setattr(self, f"off{which}", _upload(o))
-            setattr(self, f"elem{which}", _upload(np.ascontiguousarray(e[m], dtype=np.int32)))
-            setattr(self, f"tl{which}", _upload(np.ascontiguousarray(tl[keep], dtype=np.int32)))
-            if which == 2:
-                self.pos2 = _upload(np.ascontiguousarray(p_[m], dtype=np.uint8))
+        h = pfold_lists_host(g.host)
+        self.n1, self.n2 = h["n1"], h["n2"]
+        for k in ("off1", "elem1", "tl1", "off2", "elem2", "tl2", "pos2"):
+            setattr(self, k, _upload(h[k]))
 
 
 def pfold_mirror(loop, plan) -> PFoldMirror:

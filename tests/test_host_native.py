@@ -466,3 +466,43 @@ def test_tile_plan_invariants_proxy_mesh_with_coords():
         _check_tile_incidences(h, m.table, m.from_set.size, [0, 1])
     with pytest.raises(ml.ExecError, match="budget"):
         tile_plan_host(loop, m.from_set.size, 500, 64, None)
+
+
+def test_gather_hub_rows_and_pfold_lists(rng):
+    """Gather lists with hub splitting: every target's incidences covered once,
+    in serial order, rows of <= hub_row; pfold lists = the position-0 / >0
+    incidences per target, element ascending."""
+    from paper_1403_7209_b200.device import gather_lists_host, pfold_lists_host
+    for trial in range(6):
+        mesh = apps.gen_hub_mesh(300, 4000, n_hubs=3, hub_share=0.3, seed=trial)
+        prog, _ = apps.build_diffusion(mesh, 1, dtype="int64")
+        loop = prog[1]
+        n = loop.iter_set.size
+        tab = mesh.maps["edge_nodes"].table
+        for hub_row in (7, 128):
+            h = gather_lists_host(loop, n, hubs=True, hub_row=hub_row)
+            off, elem, pos = h["off"], h["elem"], h["pos"]
+            tl = h["targets"] if h["targets"] is not None else np.arange(off.size - 1)
+            assert np.all(np.diff(off) <= hub_row) or h["seg"] is None
+            got = {}
+            for r in range(off.size - 1):
+                got.setdefault(int(tl[r]), []).extend(
+                    zip(elem[off[r]:off[r + 1]].tolist(), pos[off[r]:off[r + 1]].tolist()))
+            want = {}
+            for e in range(n):
+                for a in range(2):
+                    want.setdefault(int(tab[e, a]), []).append((e, a))
+            assert got == want
+            if h["seg"] is not None:
+                seg = h["seg"]
+                assert sorted(seg[seg >= 0].tolist()) == list(range(h["nslots"]))
+                for k, t in enumerate(h["hub_tl"]):
+                    rows = np.flatnonzero((tl == t) & (seg >= 0))
+                    assert seg[rows].tolist() == list(range(h["hub_off"][k], h["hub_off"][k + 1]))
+            pf = pfold_lists_host(h["host"])
+            for which, sel in ((1, lambda a: a == 0), (2, lambda a: a > 0)):
+                o, el, t1 = pf[f"off{which}"], pf[f"elem{which}"], pf[f"tl{which}"]
+                for r in range(pf[f"n{which}"]):
+                    es = el[o[r]:o[r + 1]].tolist()
+                    assert es == sorted(es)
+                    assert es == [e for e, a in want[int(t1[r])] if sel(a)]

@@ -353,6 +353,13 @@ int ml_program_run(ml_program_t *p, int32_t use_graph, int32_t time_loops);
  * between replays (device-throughput measurement); syncs at the end. */
 int ml_program_replay(ml_program_t *p, int32_t count);
 int ml_program_loop_times(const ml_program_t *p, float *ms);
+/* Concurrent loops for untimed runs and graphs: loop j waits only for the
+ * earlier loops sharing a dat/global buffer with it where either writes
+ * (RAW/WAR/WAW), so independent loops overlap on up to four streams; results
+ * are unchanged (each buffer sees the same sequence of writers).  Timed eager
+ * runs stay sequential.  ml_program_deps reports the DAG and the stream. */
+int ml_program_set_concurrent(ml_program_t *p, int32_t on);
+int ml_program_deps(const ml_program_t *p, int32_t loop, int32_t *ndeps, int32_t *deps, int32_t *lane);
 int ml_program_free(ml_program_t *p);
 
 /* ---- multi-GPU owner-compute support: executor.py:484-497 (exchange),

@@ -39,7 +39,7 @@ EXPORTED = [
     "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name",
     "ml_loop_scratch_bytes", "ml_loop_run", "ml_loop_pfold_slot_bytes",
     "ml_program_create", "ml_program_run", "ml_program_replay", "ml_program_loop_times",
-    "ml_program_free",
+    "ml_program_free", "ml_program_set_concurrent", "ml_program_deps",
     "ml_pack_rows", "ml_unpack_rows", "ml_combine_ranks", "ml_stream",
     "ml_flush_l2", "ml_timer_create", "ml_timer_start", "ml_timer_stop", "ml_timer_free",
 ]
@@ -164,6 +164,8 @@ _SIGNATURES = {
     "ml_program_run": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "ml_program_replay": (C.c_int, [_P, C.c_int32]),
     "ml_program_loop_times": (C.c_int, [_P, C.POINTER(C.c_float)]),
+    "ml_program_set_concurrent": (C.c_int, [_P, C.c_int32]),
+    "ml_program_deps": (C.c_int, [_P, C.c_int32, _I32P, _P, _I32P]),
     "ml_program_free": (C.c_int, [_P]),
     "ml_pack_rows": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int64, C.c_int64]),
     "ml_unpack_rows": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int64, C.c_int64]),

@@ -719,17 +719,75 @@ struct ml_program {
     cudaGraph_t graph = nullptr;
     std::vector<cudaEvent_t> events;
     std::vector<float> times;
+    // concurrent loops (untimed runs and graphs): loop j waits only for the
+    // earlier loops it conflicts with — sharing a dat or global buffer that
+    // either of them writes — so independent loops overlap on side streams
+    int32_t concurrent = 0;
+    std::vector<std::vector<int>> deps;
+    std::vector<int> lane;                       // stream of each loop (0: main)
+    std::vector<cudaEvent_t> done;               // per loop, after its last kernel
+    cudaStream_t side[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t fork = nullptr;
 };
+
+static constexpr int kLanes = 4;
+
+// dependency DAG of a program: j depends on i < j when they share a buffer
+// (dat payload or global slot) and at least one of them writes it
+static void program_deps(ml_program *p) {
+    const size_t n = p->loops.size();
+    p->deps.assign(n, {});
+    p->lane.assign(n, 0);
+    for (size_t j = 0; j < n; ++j) {
+        const ml_loop_t &B = p->loops[j];
+        for (size_t i = 0; i < j; ++i) {
+            const ml_loop_t &A = p->loops[i];
+            bool conflict = false;
+            for (int x = 0; x < A.nargs && !conflict; ++x)
+                for (int y = 0; y < B.nargs && !conflict; ++y)
+                    conflict = A.args[x].data && A.args[x].data == B.args[y].data &&
+                               (A.args[x].mode != ML_READ || B.args[y].mode != ML_READ);
+            if (conflict) p->deps[j].push_back(int(i));
+        }
+        // lane: the latest dependency's lane (fewest cross-stream waits), else a free one
+        int lane = -1;
+        if (!p->deps[j].empty()) lane = p->lane[p->deps[j].back()];
+        if (lane < 0) {
+            std::vector<int> last(kLanes, -1);
+            for (size_t i = 0; i < j; ++i) last[p->lane[i]] = int(i);
+            lane = 0;
+            for (int k = 0; k < kLanes; ++k)
+                if (last[k] < last[lane]) lane = k;
+        }
+        p->lane[j] = lane;
+    }
+}
 
 static int program_enqueue(ml_program *p, bool timed) {
     cudaStream_t s = g_dev.stream;
     if (p->gbytes) ML_CUDA(cudaMemcpyAsync(p->gdev, p->ghost, p->gbytes, cudaMemcpyHostToDevice, s));
-    for (size_t i = 0; i < p->loops.size(); ++i) {
-        if (timed) ML_CUDA(cudaEventRecord(p->events[i], s));
-        int rc = enqueue_loop(&p->loops[i], s);
-        if (rc) return rc;
+    if (timed || !p->concurrent) {
+        for (size_t i = 0; i < p->loops.size(); ++i) {
+            if (timed) ML_CUDA(cudaEventRecord(p->events[i], s));
+            int rc = enqueue_loop(&p->loops[i], s);
+            if (rc) return rc;
+        }
+        if (timed) ML_CUDA(cudaEventRecord(p->events[p->loops.size()], s));
+    } else {
+        cudaStream_t lanes[kLanes] = {s, p->side[0], p->side[1], p->side[2]};
+        ML_CUDA(cudaEventRecord(p->fork, s));                 // side lanes join (capture-safe)
+        for (int k = 1; k < kLanes; ++k) ML_CUDA(cudaStreamWaitEvent(lanes[k], p->fork, 0));
+        for (size_t i = 0; i < p->loops.size(); ++i) {
+            cudaStream_t ls = lanes[p->lane[i]];
+            for (int d : p->deps[i])
+                if (p->lane[d] != p->lane[i]) ML_CUDA(cudaStreamWaitEvent(ls, p->done[d], 0));
+            int rc = enqueue_loop(&p->loops[i], ls);
+            if (rc) return rc;
+            ML_CUDA(cudaEventRecord(p->done[i], ls));
+        }
+        for (size_t i = 0; i < p->loops.size(); ++i)          // join every lane's tail
+            if (p->lane[i] != 0) ML_CUDA(cudaStreamWaitEvent(s, p->done[i], 0));
     }
-    if (timed) ML_CUDA(cudaEventRecord(p->events[p->loops.size()], s));
     if (p->gbytes) ML_CUDA(cudaMemcpyAsync(p->ghost, p->gdev, p->gbytes, cudaMemcpyDeviceToHost, s));
     return ML_OK;
 }
@@ -765,6 +823,11 @@ extern "C" int ml_program_create(const ml_loop_t *loops, int32_t nloops, void *g
     p->events.resize(size_t(nloops) + 1);
     for (auto &e : p->events) ML_CUDA(cudaEventCreate(&e));
     p->times.assign(nloops, 0.f);
+    program_deps(p.get());
+    p->done.resize(size_t(nloops));
+    for (auto &e : p->done) ML_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ML_CUDA(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming));
+    for (auto &st : p->side) ML_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     *out = p.release();
     return ML_OK;
     ML_GUARD_END
@@ -817,6 +880,27 @@ extern "C" int ml_program_run(ml_program_t *p, int32_t use_graph, int32_t time_l
     return ML_OK;
 }
 
+extern "C" int ml_program_set_concurrent(ml_program_t *p, int32_t on) {
+    if (!p) ML_FAIL(ML_EINVAL, "ml_program_set_concurrent: null");
+    if (p->concurrent != (on != 0) && p->exec) {          // re-capture with the new structure
+        cudaGraphExecDestroy(p->exec);
+        cudaGraphDestroy(p->graph);
+        p->exec = nullptr;
+        p->graph = nullptr;
+    }
+    p->concurrent = on != 0;
+    return ML_OK;
+}
+
+extern "C" int ml_program_deps(const ml_program_t *p, int32_t loop, int32_t *ndeps, int32_t *deps,
+                               int32_t *lane) {
+    if (!p || loop < 0 || loop >= int32_t(p->loops.size())) ML_FAIL(ML_EINVAL, "ml_program_deps: bad loop");
+    if (ndeps) *ndeps = int32_t(p->deps[loop].size());
+    if (deps) std::copy(p->deps[loop].begin(), p->deps[loop].end(), deps);
+    if (lane) *lane = p->lane[loop];
+    return ML_OK;
+}
+
 extern "C" int ml_program_loop_times(const ml_program_t *p, float *ms) {
     std::copy(p->times.begin(), p->times.end(), ms);
     return ML_OK;
@@ -827,6 +911,10 @@ extern "C" int ml_program_free(ml_program_t *p) {
     if (p->exec) cudaGraphExecDestroy(p->exec);
     if (p->graph) cudaGraphDestroy(p->graph);
     for (auto &e : p->events) cudaEventDestroy(e);
+    for (auto &e : p->done) cudaEventDestroy(e);
+    if (p->fork) cudaEventDestroy(p->fork);
+    for (auto &st : p->side)
+        if (st) cudaStreamDestroy(st);
     delete p;
     return ML_OK;
 }

@@ -85,6 +85,7 @@ class BackendConfig:
     tile_smem_kb: int = 100                 # tile schedule: shared memory per tile (2 CTAs/SM)
     tile_cmax: int = 512                    # tile schedule: max owned targets per tile
     tile_threads: int = 256                 # tile schedule: CTA size (256: 2 CTAs/SM, 128: 4)
+    concurrent_loops: bool = True           # graphs/untimed runs: independent loops overlap on streams
     pfold_own_kb: int = 0                   # pfold pass 1: smem per CTA for the targets' own rows
                                             # (0: from L1/L2 — faster on B200, see profiles/)
 
@@ -416,8 +417,21 @@ class CompiledProgram:
                                           self.gdev.ptr, self.gbytes, C.byref(handle)),
                 "ml_program_create")
         self.handle = handle.value
+        N.check(N.lib().ml_program_set_concurrent(self.handle, int(bool(config.concurrent_loops))))
         self.ptrs = [e.dat_pointers() for e in self.entries]
         self.runs = 0
+
+    def dependencies(self) -> list:
+        """Per loop: (earlier loops it must wait for, stream lane) of the
+        concurrent schedule (ml_program_deps)."""
+        out = []
+        for i in range(len(self.entries)):
+            nd, lane = C.c_int32(), C.c_int32()
+            N.check(N.lib().ml_program_deps(self.handle, i, C.byref(nd), None, C.byref(lane)))
+            deps = (C.c_int32 * max(nd.value, 1))()
+            N.check(N.lib().ml_program_deps(self.handle, i, C.byref(nd), deps, C.byref(lane)))
+            out.append((list(deps[:nd.value]), lane.value))
+        return out
 
     def valid_for(self, mesh: Mesh) -> bool:
         if mesh.version != self.version:
@@ -580,7 +594,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
            config.dataflow, config.inc_staging, config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.flow_windows,
            config.flow_window_l2_fraction, config.tile_smem_kb, config.tile_cmax, config.tile_threads, config.coord_dat,
-           config.pfold_own_kb,
+           config.pfold_own_kb, config.concurrent_loops,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

@@ -46,8 +46,8 @@ def _exec_cases():
 
 
 @pytest.mark.parametrize("case", _exec_cases(), ids=lambda c: c["name"])
-@pytest.mark.parametrize("bs,sched", [(256, "tile"), (256, "pfold"), (256, "gather"), (16, "gather"),
-                                      (256, "colour"), (16, "colour")])
+@pytest.mark.parametrize("bs,sched", [(256, "tile"), (256, "tgather"), (256, "pfold"), (16, "pfold"),
+                                      (256, "gather"), (16, "gather"), (256, "colour"), (16, "colour")])
 def test_apps_match_reference_golden(case, bs, sched):
     g = golden("exec.npz")
     mesh, prog, h = _cases.build_app(case["app"], case["n"], case["dtype"], case["steps"])
@@ -137,11 +137,13 @@ def _proxy_pair(N, seed=0, renumber=True, shuffle=True, soa=4):
 
 
 @pytest.mark.parametrize("soa", [4, None, 0])
-def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa):
-    """Stop before the update so the raw INC accumulators (res, grad) are compared."""
+@pytest.mark.parametrize("sched", ["gather", "pfold", "tgather", "tile"])
+def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa, sched):
+    """Stop before the update so the raw INC accumulators (res, grad) are compared,
+    for every layout (auto-SoA, all AoS, all SoA) and INC schedule."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, soa=soa)
     bulk.run_program(rprog[:5], resolve_kernel)
-    ml.run_program(prog[:5], mesh, cfg())
+    ml.run_program(prog[:5], mesh, cfg(inc_schedule=sched))
     for k in ("grad", "res", "q_old", "dt_loc"):
         close(h[k].fetch(), rh[k].fetch(), what=k)
     np.testing.assert_array_equal(h["dt_min"][0].value, rh["dt_min"][0].value)

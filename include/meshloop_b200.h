@@ -375,6 +375,22 @@ int ml_unpack_rows(void *dat, const void *src, const int32_t *idx, int64_t nidx,
  * (mode ML_INC/ML_MIN/ML_MAX, dtype ML_F64/ML_I64, `dim` components each). */
 int ml_combine_ranks(void *value, const void *gathered, int32_t nranks, int32_t dim, int32_t mode,
                      int32_t dtype);
+/* NVLink halo exchange (replaces the transfer of executor.py:484-497 with
+ * direct peer stores): CUDA IPC handles (64 bytes) of device buffers;
+ * ml_put_rows gathers export rows straight into a peer's import buffer and,
+ * after a system-scope fence, increments the peer's arrival counter for this
+ * rank (`counter`: a zeroed device int per call site, self-resetting);
+ * ml_wait_flag blocks the compute stream until a local arrival counter
+ * reaches *expected + 1 (then stores it back to `expected`, device memory). */
+int ml_ipc_handle(void *dptr, void *handle);
+int ml_ipc_open(const void *handle, void **dptr);
+int ml_ipc_close(void *dptr);
+int ml_put_rows(void *remote_dst, const void *dat, const int32_t *idx, int64_t nidx, int32_t dim,
+                int64_t elem_stride, int64_t comp_stride, uint64_t *remote_flag, int32_t *counter);
+int ml_wait_flag(const uint64_t *flag, uint64_t *expected);
+/* Stream-ordered: after the work enqueued so far, increment a (peer) counter
+ * system-wide — the consumer's "import buffer free again" credit. */
+int ml_signal_flag(uint64_t *remote_flag);
 /* The library's compute stream (cudaStream_t), for ordering NCCL work with it. */
 void *ml_stream(void);
 

@@ -41,6 +41,7 @@ EXPORTED = [
     "ml_program_create", "ml_program_run", "ml_program_replay", "ml_program_loop_times",
     "ml_program_free", "ml_program_set_concurrent", "ml_program_deps",
     "ml_pack_rows", "ml_unpack_rows", "ml_combine_ranks", "ml_stream",
+    "ml_ipc_handle", "ml_ipc_open", "ml_ipc_close", "ml_put_rows", "ml_wait_flag", "ml_signal_flag",
     "ml_flush_l2", "ml_timer_create", "ml_timer_start", "ml_timer_stop", "ml_timer_free",
 ]
 
@@ -171,6 +172,12 @@ _SIGNATURES = {
     "ml_unpack_rows": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int64, C.c_int64]),
     "ml_combine_ranks": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "ml_stream": (C.c_void_p, []),
+    "ml_ipc_handle": (C.c_int, [_P, _P]),
+    "ml_ipc_open": (C.c_int, [_P, _PP]),
+    "ml_ipc_close": (C.c_int, [_P]),
+    "ml_put_rows": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int64, C.c_int64, _P, _P]),
+    "ml_wait_flag": (C.c_int, [_P, _P]),
+    "ml_signal_flag": (C.c_int, [_P]),
     "ml_flush_l2": (C.c_int, []),
     "ml_timer_create": (C.c_int, [_PP]),
     "ml_timer_start": (C.c_int, [_P]),

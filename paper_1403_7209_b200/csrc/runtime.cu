@@ -937,6 +937,43 @@ __global__ void k_unpack_rows(double *dat, const double *src, const int32_t *idx
         dat[int64_t(idx[r]) * se + c * sc] = src[k];
     }
 }
+// NVLink halo exchange: pack the export rows straight into the peer's import
+// buffer (an IPC-mapped pointer), then — once every CTA's remote stores are
+// fenced system-wide — bump the peer's arrival counter for this rank.
+__global__ void k_put_rows(double *rdst, const double *dat, const int32_t *idx, int64_t nidx, int dim,
+                           int64_t se, int64_t sc, unsigned long long *rflag, int *counter) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nidx * dim;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = k / dim, c = k % dim;
+        rdst[k] = dat[int64_t(idx[r]) * se + c * sc];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(counter, 1) == int(gridDim.x) - 1) {
+        *counter = 0;                                   // ready for the next exchange
+        __threadfence_system();
+        atomicAdd_system(rflag, 1ull);
+    }
+}
+// Wait (one thread) until the local arrival counter of a source reaches the
+// next expected value; `expected` lives in device memory so graph replays
+// keep counting.
+__global__ void k_wait_flag(const unsigned long long *flag, unsigned long long *expected) {
+    const unsigned long long want = *expected + 1;
+    *expected = want;
+    unsigned long long v;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+        if (v >= want) break;
+        __nanosleep(256);
+    }
+}
+
+__global__ void k_signal(unsigned long long *rflag) {
+    __threadfence_system();
+    atomicAdd_system(rflag, 1ull);
+}
+
 template <class T, int M>
 __global__ void k_combine_ranks(T *value, const T *gathered, int nranks, int dim) {
     for (int c = threadIdx.x; c < dim; c += blockDim.x) {
@@ -969,6 +1006,54 @@ extern "C" int ml_unpack_rows(void *dat, const void *src, const int32_t *idx, in
     const int grid = int(std::min<int64_t>((work + 255) / 256, 4 * 148));
     k_unpack_rows<<<grid, 256, 0, g_dev.stream>>>(static_cast<double *>(dat), static_cast<const double *>(src),
                                                  idx, nidx, dim, se, sc);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+extern "C" int ml_ipc_handle(void *dptr, void *handle) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    ML_CUDA(cudaIpcGetMemHandle(&h, dptr));
+    std::memcpy(handle, &h, sizeof h);
+    return ML_OK;
+}
+extern "C" int ml_ipc_open(const void *handle, void **dptr) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    ML_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return ML_OK;
+}
+extern "C" int ml_ipc_close(void *dptr) {
+    if (dptr) ML_CUDA(cudaIpcCloseMemHandle(dptr));
+    return ML_OK;
+}
+extern "C" int ml_put_rows(void *remote_dst, const void *dat, const int32_t *idx, int64_t nidx, int32_t dim,
+                           int64_t se, int64_t sc, uint64_t *remote_flag, int32_t *counter) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    const int64_t work = std::max<int64_t>(nidx * dim, 1);
+    const int grid = int(std::min<int64_t>((work + 255) / 256, 2 * 148));
+    k_put_rows<<<grid, 256, 0, g_dev.stream>>>(static_cast<double *>(remote_dst), static_cast<const double *>(dat),
+                                               idx, nidx, dim, se, sc,
+                                               reinterpret_cast<unsigned long long *>(remote_flag), counter);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+extern "C" int ml_signal_flag(uint64_t *remote_flag) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    k_signal<<<1, 1, 0, g_dev.stream>>>(reinterpret_cast<unsigned long long *>(remote_flag));
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+extern "C" int ml_wait_flag(const uint64_t *flag, uint64_t *expected) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    k_wait_flag<<<1, 1, 0, g_dev.stream>>>(reinterpret_cast<const unsigned long long *>(flag),
+                                            reinterpret_cast<unsigned long long *>(expected));
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

@@ -425,6 +425,135 @@ class DeviceRank:
         return len(sends)
 
 
+_LAST_HALO_PATH = ""
+
+
+class NvlinkHalo:
+    """Halo exchange by direct peer stores (CUDA IPC over NVLink/NVSwitch).
+
+    Each rank allocates, per (dat, source rank), the import buffer that source
+    writes into, plus one arrival counter per source; handles are exchanged
+    once (all-gather).  An exchange is then, on the compute stream: for every
+    destination one ``ml_put_rows`` kernel that gathers the export rows
+    straight into the destination's import buffer and bumps its arrival
+    counter after a system-scope fence; for every source one ``ml_wait_flag``
+    (device spin on the counter), the ``ml_unpack_rows`` scatter and a credit
+    back to the source (``ml_signal_flag``): a producer puts only after the
+    destination has consumed its previous delivery, so ranks may drift apart
+    without overwriting an unread import buffer.  No host involvement and no
+    NCCL on the halo path, so it is graph-capturable; the put overlaps
+    whatever the stream runs before the wait (core targets)."""
+
+    def __init__(self, rp: RankProgram, transport):
+        import ctypes as C
+        from . import _native as N
+        self.C, self.N, self.rp = C, N, rp
+        L = N.lib()
+        self.local, self.remote, self.handles = {}, {}, {}
+        self.opened = []
+        nr = rp.nranks
+        names = sorted({n for reads, _w in rp.roles for n in reads if n in rp.dats})
+        keys = []
+        for name in names:
+            d = rp.dats[name]
+            _ex, imports = rp.halo_rows(name)
+            for src, ids in sorted(imports.items()):
+                buf = N.DeviceBuffer(max(ids.size * d.dim * 8, 8))
+                self.local[(name, src)] = buf
+                keys.append((name, src))
+        # per (dat, peer) counters: deliveries [ni*nr + src] (from each source) and
+        # credits [(nn + ni)*nr + dst] (from each destination; start at 1: the
+        # first put needs no credit)
+        nn = len(names)
+        self.names = {n: k for k, n in enumerate(names)}
+        self.nn = nn
+        self.flags = N.DeviceBuffer(16 * nr * max(nn, 1))
+        self.expected = N.DeviceBuffer(16 * nr * max(nn, 1))
+        self.counters = N.DeviceBuffer(4 * max(1, sum(len(rp.halo_rows(n)[0]) for n in names)))
+        for b in (self.expected, self.counters):
+            N.check(L.ml_memset(b.ptr, 0, b.nbytes))
+        init = np.concatenate([np.zeros(nr * max(nn, 1), np.uint64), np.ones(nr * max(nn, 1), np.uint64)])
+        self.flags.upload(init)
+        N.check(L.ml_synchronize())
+        mine = {}
+        for k in keys:
+            h = (C.c_char * 64)()
+            N.check(L.ml_ipc_handle(self.local[k].ptr, h), "ml_ipc_handle")
+            mine[k] = bytes(h)
+        fh = (C.c_char * 64)()
+        N.check(L.ml_ipc_handle(self.flags.ptr, fh), "ml_ipc_handle")
+        allh = transport.allgather_object({"bufs": mine, "flags": bytes(fh)})
+        me = rp.rank
+        ci = 0
+        self.counter_of = {}
+        for name in names:
+            exports, _imp = rp.halo_rows(name)
+            for dst in sorted(exports):
+                h = allh[dst]["bufs"][(name, me)]
+                self.remote[(name, dst)] = self._open(h)
+                self.counter_of[(name, dst)] = self.counters.ptr + 4 * ci
+                ci += 1
+        peer_flags = {}
+        for r in range(nr):
+            if r != me and (any((n, r) in self.remote for n in names)
+                            or any((n, r) in self.local for n in names)):
+                peer_flags[r] = self._open(allh[r]["flags"])
+        self.peer_flags = peer_flags
+
+    def _delivery(self, ni: int, src: int) -> int:
+        return 8 * (ni * self.rp.nranks + src)
+
+    def _credit(self, ni: int, dst: int) -> int:
+        return 8 * ((self.nn + ni) * self.rp.nranks + dst)
+
+    def _open(self, handle: bytes) -> int:
+        C, N = self.C, self.N
+        p = C.c_void_p()
+        N.check(N.lib().ml_ipc_open(C.create_string_buffer(handle, 64), C.byref(p)), "ml_ipc_open")
+        self.opened.append(p.value)
+        return p.value
+
+    def put(self, name: str, index) -> int:
+        """Enqueue the puts of one dat's export rows; returns the messages."""
+        N, rp = self.N, self.rp
+        from .device import dat_mirror
+        d = rp.dats[name]
+        m = dat_mirror(d)
+        se, sc = (d.dim, 1) if d.layout is AOS else (1, d.set.size)
+        exports, _imports = rp.halo_rows(name)
+        ni, me = self.names[name], rp.rank
+        for dst, ids in sorted(exports.items()):
+            N.check(N.lib().ml_wait_flag(self.flags.ptr + self._credit(ni, dst),
+                                         self.expected.ptr + self._credit(ni, dst)),
+                    "ml_wait_flag")                    # dst has consumed our previous delivery
+            N.check(N.lib().ml_put_rows(self.remote[(name, dst)], m.ptr, index(("e", name, dst), ids).ptr,
+                                        ids.size, d.dim, se, sc, self.peer_flags[dst] + self._delivery(ni, me),
+                                        self.counter_of[(name, dst)]), "ml_put_rows")
+        return len(exports)
+
+    def land(self, name: str, index) -> None:
+        """Enqueue the waits and scatters of one dat's import rows."""
+        N, rp = self.N, self.rp
+        from .device import dat_mirror
+        d = rp.dats[name]
+        m = dat_mirror(d)
+        se, sc = (d.dim, 1) if d.layout is AOS else (1, d.set.size)
+        _exports, imports = rp.halo_rows(name)
+        ni, me = self.names[name], rp.rank
+        for src, ids in sorted(imports.items()):
+            N.check(N.lib().ml_wait_flag(self.flags.ptr + self._delivery(ni, src),
+                                         self.expected.ptr + self._delivery(ni, src)), "ml_wait_flag")
+            N.check(N.lib().ml_unpack_rows(m.ptr, self.local[(name, src)].ptr, index(("i", name, src), ids).ptr,
+                                           ids.size, d.dim, se, sc), "ml_unpack_rows")
+            N.check(N.lib().ml_signal_flag(self.peer_flags[src] + self._credit(ni, me)), "ml_signal_flag")
+        m.device_newer = True
+
+    def close(self):
+        for p in self.opened:
+            self.N.lib().ml_ipc_close(p)
+        self.opened = []
+
+
 class StreamRank:
     """Stream-ordered rank executor (the production multi-GPU path).
 
@@ -483,6 +612,23 @@ class StreamRank:
                 dat_mirror(d)
         self._splits: dict = {}
         self.split = [None] * len(self.entries)     # last split used by each loop (reporting)
+        # halo path: direct NVLink stores (CUDA IPC) unless ML_HALO=nccl; every
+        # rank must agree, so a failure anywhere falls back everywhere
+        self.nvlink = None
+        self.halo_error = None
+        if os.environ.get("ML_HALO", "p2p") == "p2p" and rp.nranks > 1:
+            ok = 1
+            try:
+                self.nvlink = NvlinkHalo(rp, transport)
+            except Exception as ex:                     # noqa: BLE001 - reported, not hidden
+                self.halo_error = f"{type(ex).__name__}: {ex}"[:200]
+                ok = 0
+            if min(transport.allgather_object(ok)) == 0:
+                if self.nvlink is not None:
+                    self.nvlink.close()
+                self.nvlink = None
+        global _LAST_HALO_PATH
+        _LAST_HALO_PATH = "nvlink" if self.nvlink is not None else transport.name
 
     # -- setup ---------------------------------------------------------------------------
     def _split(self, i: int, names: tuple):
@@ -619,11 +765,28 @@ class StreamRank:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev0.record(self.lib_stream)
             names = [n for n in reads if dirty.get(n)]
-            packed = [(n, *self._pack(n)) for n in names]
-            messages += sum(len(p[1]) for p in packed)
-            split = self._split(i, tuple(names)) if overlap and packed else None
-            self.split[i] = split
-            if split is not None and tr.name == "nccl":
+            if self.nvlink is not None:
+                for n in names:                         # peer stores start at once
+                    messages += self.nvlink.put(n, self._index)
+                split = self._split(i, tuple(names)) if overlap and names else None
+                self.split[i] = split
+                if split is not None:
+                    self._launch(split[0][0])                   # core targets, overlapped
+                for n in names:
+                    self.nvlink.land(n, self._index)
+                if split is not None:
+                    self._launch(split[1][0])                   # boundary targets
+                else:
+                    self._launch(e.desc)
+                packed = []
+            else:
+                packed = [(n, *self._pack(n)) for n in names]
+                messages += sum(len(p[1]) for p in packed)
+                split = self._split(i, tuple(names)) if overlap and packed else None
+                self.split[i] = split
+            if self.nvlink is not None:
+                pass
+            elif split is not None and tr.name == "nccl":
                 ev_packed = torch.cuda.Event()
                 ev_packed.record(self.lib_stream)
                 self.comm_stream.wait_event(ev_packed)
@@ -941,6 +1104,8 @@ def bench_distributed(args, metric):
                 "config": {"workload": wname, "edges": edges, "nodes": mesh.sets["nodes"].size,
                            "parallelism": f"owner-compute dp{world} (RCB)",
                            "transport": transport.name, "halo_nodes_per_rank": halo,
+                           "halo_path": "nvlink-p2p (CUDA IPC peer stores)" if dev.nvlink is not None
+                           else f"{transport.name} send/recv", "halo_p2p_error": dev.halo_error,
                            "overlapped_loops": split,
                            "cuda_graph": graphed, "cuda_graph_error": graph_error,
                            "l2": "per-rank working set streamed each step",

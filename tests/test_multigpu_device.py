@@ -27,9 +27,12 @@ def _free_port() -> int:
 
 
 def _worker(rank, world, port, case, q, executor="stream"):
+    halo = "p2p"
+    if executor.endswith("+copy"):
+        executor, halo = executor[:-5], "copy"
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK="0", ML_TRANSPORT="gloo",
-                      ML_RANK_EXECUTOR=executor)
+                      ML_RANK_EXECUTOR=executor, ML_HALO=halo)
     sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -51,12 +54,18 @@ def _worker(rank, world, port, case, q, executor="stream"):
                    "dt": np.array([g.value for g in h["dt_min"]])}
         else:
             out = _cases.app_results(app, h)
-        q.put((rank, out, result.messages))
+        need_nvlink = executor == "stream" and halo == "p2p" and world > 1
+        q.put((rank, out, result.messages if not need_nvlink or _nvlink_used() else -2))
     except Exception:
         import traceback
         q.put((rank, traceback.format_exc(), -1))
     finally:
         dist.destroy_process_group()
+
+
+def _nvlink_used() -> bool:
+    import paper_1403_7209_b200.multigpu as mg
+    return bool(getattr(mg, "_LAST_HALO_PATH", "") == "nvlink")
 
 
 def _run(case, world=2, executor="stream"):
@@ -72,6 +81,8 @@ def _run(case, world=2, executor="stream"):
     for p in procs:
         p.join(timeout=60)
     for rank, out, msgs in outs:
+        if msgs == -2:
+            raise AssertionError(f"rank {rank}: the NVLink (IPC) halo path was not used")
         if msgs < 0:
             raise AssertionError(f"rank {rank} failed:\n{out}")
     return sorted(outs, key=lambda x: x[0])
@@ -79,6 +90,7 @@ def _run(case, world=2, executor="stream"):
 
 @pytest.mark.parametrize("world,part,sched,executor", [
     (2, "rcb", "gather", "stream"), (3, "trivial", "gather", "stream"), (2, "rcb", "flow", "stream"),
+    (2, "rcb", "gather", "stream+copy"), (3, "trivial", "pfold", "stream+copy"),
     (3, "trivial", "arrival", "host"), (2, "trivial", "colour", "host"), (2, "rcb", "tile", "stream"),
     (2, "rcb", "pfold", "stream")])
 def test_ranks_on_device_match_reference_int64(world, part, sched, executor):
@@ -91,7 +103,8 @@ def test_ranks_on_device_match_reference_int64(world, part, sched, executor):
             np.testing.assert_array_equal(v, g[f"exec/diffusion_n8_int64_s3/{k}"], f"rank {rank} {k}")
 
 
-@pytest.mark.parametrize("sched,executor", [("gather", "stream"), ("flow", "host")])
+@pytest.mark.parametrize("sched,executor", [("gather", "stream"), ("gather", "stream+copy"),
+                                            ("flow", "host")])
 def test_proxy_two_ranks_on_device_vs_oracle(sched, executor):
     import paper_1403_7209_b200 as ml
     from oracle import bulk

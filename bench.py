@@ -158,11 +158,14 @@ def run_ours(args) -> None:
         for e, t in zip(cp.entries, cp.run(False, True)):
             per_loop[e.loop.name].append(t)
     loops = {}
+    peak, peak_src = peaks_gbs()
     for e in cp.entries:
         t = statistics.mean(per_loop[e.loop.name])
         loops[e.loop.name] = {"ms": round(t * 1e3, 4), "b_alg": e.alg, "useful_bytes": e.useful,
-                              "gbs_alg": round(e.alg / t / 1e9, 1), "nb": e.st.nb, "nc": e.st.nc}
-    peak, peak_src = peaks_gbs()
+                              "gbs_alg": round(e.alg / t / 1e9, 1),
+                              "frac_of_peak": round(e.alg / t / 1e9 / peak, 4),
+                              "schedule": e.sched if e.plan.has_writes else "direct",
+                              "nb": e.st.nb, "nc": e.st.nc}
     names = [e.loop.name for e in cp.entries]
     dom = cp.entries[names.index("vflux") if "vflux" in names
                      else max(range(len(names)), key=lambda i: loops[names[i]]["ms"])]
@@ -210,6 +213,10 @@ def run_ours(args) -> None:
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": dom.alg,
+                     "spec_peak_gbs": 8000.0,
+                     "iteration": {"b_alg": sum(e.alg for e in cp.entries),
+                                   "achieved": round(sum(e.alg for e in cp.entries) / (total_ms * 1e-3 / args.steps) / 1e9, 1),
+                                   "frac": round(sum(e.alg for e in cp.entries) / (total_ms * 1e-3 / args.steps) / 1e9 / peak, 4)},
                      "mean_loop_ms": round(t_dom * 1e3, 4)},
         "loops": loops,
         "eager_ms_per_step": round(sum(v["ms"] for v in loops.values()), 4),

@@ -24,7 +24,7 @@ ap.add_argument("--kd", type=int, default=0, help="k-d leaf size: renumber nodes
 ap.add_argument("--tile-smem", type=int, nargs="+", default=[100])
 ap.add_argument("--tile-cmax", type=int, default=512)
 ap.add_argument("--tile-threads", type=int, nargs="+", default=[256])
-ap.add_argument("--own-kb", type=int, nargs="+", default=[100])
+ap.add_argument("--own-kb", type=int, nargs="+", default=[0])
 
 args = ap.parse_args()
 mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)

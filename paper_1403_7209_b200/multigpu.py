@@ -1091,6 +1091,12 @@ def bench_distributed(args, metric):
                      device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tmax, e2e_max = float(t[0].item()), float(t[1].item())
+    # algorithmic bytes of one step summed over ranks (owned + exec-halo
+    # elements, the reference convention executor.py:458-480)
+    balg = torch.tensor([float(sum(e.alg for e in dev.entries))], dtype=torch.float64,
+                        device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(balg, op=dist.ReduceOp.SUM)
+    balg_step = float(balg.item())
     halo = [len(layout.sets["nodes"][r].nonexec_halo) + len(layout.sets["nodes"][r].exec_halo)
             for r in range(world)]
     split = [e.loop.name for e, sp in zip(dev.entries, dev.split) if sp is not None]
@@ -1115,7 +1121,12 @@ def bench_distributed(args, metric):
                 "halo_messages_per_step": msgs / args.steps,
                 "loops_ms_rank0": {e.loop.name: round(1e3 * t_, 4)
                                    for e, t_ in zip(dev.entries, loop_s)},
-                "roofline": None,
+                "roofline": {"bound": "hbm", "kernel": "whole iteration (all ranks)",
+                             "achieved": round(balg_step / (tmax / args.steps) / 1e9, 1),
+                             "peak": round(world * peak, 1), "unit": "GB/s",
+                             "frac": round(balg_step / (tmax / args.steps) / 1e9 / (world * peak), 4),
+                             "traffic": None, "peak_source": src + f" x {world} GPUs",
+                             "algorithmic_bytes_per_step": balg_step},
                 "e2e": {"value": edges * args.steps / e2e_max, "unit": "edges/s",
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "ms_per_step": 1e3 * e2e_max / args.steps,

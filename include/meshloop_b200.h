@@ -381,13 +381,16 @@ int ml_combine_ranks(void *value, const void *gathered, int32_t nranks, int32_t 
  * after a system-scope fence, increments the peer's arrival counter for this
  * rank (`counter`: a zeroed device int per call site, self-resetting);
  * ml_wait_flag blocks the compute stream until a local arrival counter
- * reaches *expected + 1 (then stores it back to `expected`, device memory). */
+ * reaches *expected + 1 (then stores it back to `expected`, device memory);
+ * after `timeout_ns` (0: none) it stores `code` into *err (if still 0) and
+ * releases the stream — the host then raises ExchangeTimeout. */
 int ml_ipc_handle(void *dptr, void *handle);
 int ml_ipc_open(const void *handle, void **dptr);
 int ml_ipc_close(void *dptr);
 int ml_put_rows(void *remote_dst, const void *dat, const int32_t *idx, int64_t nidx, int32_t dim,
                 int64_t elem_stride, int64_t comp_stride, uint64_t *remote_flag, int32_t *counter);
-int ml_wait_flag(const uint64_t *flag, uint64_t *expected);
+int ml_wait_flag(const uint64_t *flag, uint64_t *expected, uint64_t timeout_ns, int64_t *err,
+                 int64_t code);
 /* Stream-ordered: after the work enqueued so far, increment a (peer) counter
  * system-wide — the consumer's "import buffer free again" credit. */
 int ml_signal_flag(uint64_t *remote_flag);

@@ -176,7 +176,7 @@ _SIGNATURES = {
     "ml_ipc_open": (C.c_int, [_P, _PP]),
     "ml_ipc_close": (C.c_int, [_P]),
     "ml_put_rows": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int64, C.c_int64, _P, _P]),
-    "ml_wait_flag": (C.c_int, [_P, _P]),
+    "ml_wait_flag": (C.c_int, [_P, _P, C.c_uint64, _P, C.c_int64]),
     "ml_signal_flag": (C.c_int, [_P]),
     "ml_flush_l2": (C.c_int, []),
     "ml_timer_create": (C.c_int, [_PP]),

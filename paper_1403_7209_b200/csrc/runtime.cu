@@ -957,14 +957,24 @@ __global__ void k_put_rows(double *rdst, const double *dat, const int32_t *idx, 
 }
 // Wait (one thread) until the local arrival counter of a source reaches the
 // next expected value; `expected` lives in device memory so graph replays
-// keep counting.
-__global__ void k_wait_flag(const unsigned long long *flag, unsigned long long *expected) {
+// keep counting.  Bounded by `timeout_ns` (globaltimer): on expiry the wait
+// records `code` in `err` (first error wins) and lets the stream go on; the
+// host raises ExchangeTimeout after the run (reference executor.py:343-359).
+__global__ void k_wait_flag(const unsigned long long *flag, unsigned long long *expected,
+                            unsigned long long timeout_ns, long long *err, long long code) {
     const unsigned long long want = *expected + 1;
     *expected = want;
-    unsigned long long v;
+    unsigned long long v, t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
         if (v >= want) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (timeout_ns && t - t0 > timeout_ns) {
+            if (err) atomicCAS(reinterpret_cast<unsigned long long *>(err), 0ull,
+                               static_cast<unsigned long long>(code));
+            break;
+        }
         __nanosleep(256);
     }
 }
@@ -1049,11 +1059,13 @@ extern "C" int ml_signal_flag(uint64_t *remote_flag) {
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }
-extern "C" int ml_wait_flag(const uint64_t *flag, uint64_t *expected) {
+extern "C" int ml_wait_flag(const uint64_t *flag, uint64_t *expected, uint64_t timeout_ns, int64_t *err,
+                            int64_t code) {
     int rc = ensure_init();
     if (rc) return rc;
     k_wait_flag<<<1, 1, 0, g_dev.stream>>>(reinterpret_cast<const unsigned long long *>(flag),
-                                            reinterpret_cast<unsigned long long *>(expected));
+                                            reinterpret_cast<unsigned long long *>(expected), timeout_ns,
+                                            reinterpret_cast<long long *>(err), code);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

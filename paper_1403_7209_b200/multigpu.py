@@ -444,10 +444,11 @@ class NvlinkHalo:
     NCCL on the halo path, so it is graph-capturable; the put overlaps
     whatever the stream runs before the wait (core targets)."""
 
-    def __init__(self, rp: RankProgram, transport):
+    def __init__(self, rp: RankProgram, transport, timeout_ms: float = 10000.0):
         import ctypes as C
         from . import _native as N
         self.C, self.N, self.rp = C, N, rp
+        self.timeout_ns = int(max(timeout_ms, 0.0) * 1e6)
         L = N.lib()
         self.local, self.remote, self.handles = {}, {}, {}
         self.opened = []
@@ -470,7 +471,8 @@ class NvlinkHalo:
         self.flags = N.DeviceBuffer(16 * nr * max(nn, 1))
         self.expected = N.DeviceBuffer(16 * nr * max(nn, 1))
         self.counters = N.DeviceBuffer(4 * max(1, sum(len(rp.halo_rows(n)[0]) for n in names)))
-        for b in (self.expected, self.counters):
+        self.err = N.DeviceBuffer(8)              # first halo timeout: code, 0 = none
+        for b in (self.expected, self.counters, self.err):
             N.check(L.ml_memset(b.ptr, 0, b.nbytes))
         init = np.concatenate([np.zeros(nr * max(nn, 1), np.uint64), np.ones(nr * max(nn, 1), np.uint64)])
         self.flags.upload(init)
@@ -524,14 +526,15 @@ class NvlinkHalo:
         ni, me = self.names[name], rp.rank
         for dst, ids in sorted(exports.items()):
             N.check(N.lib().ml_wait_flag(self.flags.ptr + self._credit(ni, dst),
-                                         self.expected.ptr + self._credit(ni, dst)),
+                                         self.expected.ptr + self._credit(ni, dst), self.timeout_ns,
+                                         self.err.ptr, -(1 + ni * rp.nranks + dst)),
                     "ml_wait_flag")                    # dst has consumed our previous delivery
             N.check(N.lib().ml_put_rows(self.remote[(name, dst)], m.ptr, index(("e", name, dst), ids).ptr,
                                         ids.size, d.dim, se, sc, self.peer_flags[dst] + self._delivery(ni, me),
                                         self.counter_of[(name, dst)]), "ml_put_rows")
         return len(exports)
 
-    def land(self, name: str, index) -> None:
+    def land(self, name: str, index, loop_index: int = 0) -> None:
         """Enqueue the waits and scatters of one dat's import rows."""
         N, rp = self.N, self.rp
         from .device import dat_mirror
@@ -541,12 +544,32 @@ class NvlinkHalo:
         _exports, imports = rp.halo_rows(name)
         ni, me = self.names[name], rp.rank
         for src, ids in sorted(imports.items()):
+            code = 1 + (loop_index * self.nn + ni) * rp.nranks + src
             N.check(N.lib().ml_wait_flag(self.flags.ptr + self._delivery(ni, src),
-                                         self.expected.ptr + self._delivery(ni, src)), "ml_wait_flag")
+                                         self.expected.ptr + self._delivery(ni, src), self.timeout_ns,
+                                         self.err.ptr, code), "ml_wait_flag")
             N.check(N.lib().ml_unpack_rows(m.ptr, self.local[(name, src)].ptr, index(("i", name, src), ids).ptr,
                                            ids.size, d.dim, se, sc), "ml_unpack_rows")
             N.check(N.lib().ml_signal_flag(self.peer_flags[src] + self._credit(ni, me)), "ml_signal_flag")
         m.device_newer = True
+
+    def check(self, loop_names) -> None:
+        """Raise ExchangeTimeout (reference executor.py:343-359) if a wait expired."""
+        code = np.zeros(1, np.int64)
+        self.err.download(code)
+        c = int(code[0])
+        if not c:
+            return
+        from .executor import ExchangeTimeout
+        nr, names = self.rp.nranks, sorted(self.names, key=self.names.get)
+        if c < 0:
+            k = -c - 1
+            raise ExchangeTimeout(f"rank {self.rp.rank}: rank {k % nr} did not consume dat "
+                                  f"{names[k // nr]!r} within {self.timeout_ns / 1e6:.0f} ms")
+        k = c - 1
+        src, ni, li = k % nr, (k // nr) % self.nn, k // (nr * self.nn)
+        raise ExchangeTimeout(f"rank {self.rp.rank}: no message from rank {src} for dat {names[ni]!r} "
+                              f"before loop {loop_names[li]!r} within {self.timeout_ns / 1e6:.0f} ms")
 
     def close(self):
         for p in self.opened:
@@ -619,7 +642,7 @@ class StreamRank:
         if os.environ.get("ML_HALO", "p2p") == "p2p" and rp.nranks > 1:
             ok = 1
             try:
-                self.nvlink = NvlinkHalo(rp, transport)
+                self.nvlink = NvlinkHalo(rp, transport, config.timeout_ms)
             except Exception as ex:                     # noqa: BLE001 - reported, not hidden
                 self.halo_error = f"{type(ex).__name__}: {ex}"[:200]
                 ok = 0
@@ -773,7 +796,7 @@ class StreamRank:
                 if split is not None:
                     self._launch(split[0][0])                   # core targets, overlapped
                 for n in names:
-                    self.nvlink.land(n, self._index)
+                    self.nvlink.land(n, self._index, i)
                 if split is not None:
                     self._launch(split[1][0])                   # boundary targets
                 else:
@@ -862,6 +885,8 @@ class StreamRank:
     def finish(self) -> None:
         """Wait for the run and copy the running values back to the host."""
         self.N.check(self.N.lib().ml_synchronize(), "ml_synchronize")
+        if self.nvlink is not None:
+            self.nvlink.check([e.loop.name for e in self.entries])
         host = self.arena.cpu().numpy()
         for gid, val in self.rp.values.items():
             o = self.slots[id(val)]

@@ -169,3 +169,62 @@ def test_rank_step_cuda_graph_with_nccl_matches_eager():
     np.testing.assert_array_equal(a, b)
     for x, y in zip(va, vb):
         np.testing.assert_array_equal(x, y)
+
+
+def _timeout_worker(rank, port, q):
+    """Rank 0 runs a program whose second loop needs rank 1's halo rows; rank 1
+    never runs it: the NVLink wait must expire and surface as ExchangeTimeout
+    (reference executor.py:343-359), not hang."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2",
+                      LOCAL_RANK="0", ML_TRANSPORT="gloo", ML_HALO="p2p")
+    sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        import paper_1403_7209_b200 as ml
+        from paper_1403_7209_b200 import apps
+        from paper_1403_7209_b200.apps import _k_copy, _k_edge_flux
+        from paper_1403_7209_b200.executor import ExchangeTimeout
+        from paper_1403_7209_b200.multigpu import setup_distributed
+        mesh = apps.gen_mesh(10)
+        nodes, edges = mesh.sets["nodes"], mesh.sets["edges"]
+        en = mesh.maps["edge_nodes"]
+        u = mesh.decl_dat("u", nodes, 1, "float64", np.arange(nodes.size, dtype=float))
+        u0 = mesh.decl_dat("u0", nodes, 1, "float64", np.ones(nodes.size))
+        fl = mesh.decl_dat("fl", nodes, 1, "float64", np.zeros(nodes.size))
+        prog = [ml.Loop("write_u", nodes, [ml.arg_direct(u0, ml.READ), ml.arg_direct(u, ml.WRITE)], _k_copy),
+                ml.Loop("flux", edges, [ml.arg_indirect(u, en, 1, ml.READ), ml.arg_indirect(u, en, 2, ml.READ),
+                                        ml.arg_indirect(fl, en, 1, ml.INC), ml.arg_indirect(fl, en, 2, ml.INC)],
+                        _k_edge_flux)]
+        cfg = ml.BackendConfig(nranks=2, partitioner="trivial", device=0, timeout_ms=300.0)
+        rp, dev, tr, layout, cfg = setup_distributed(prog, mesh, cfg)
+        assert dev.nvlink is not None
+        if rank == 0:
+            dev.run()
+            dev.run()                          # the second run exchanges u (dirty after run 1)
+            try:
+                dev.finish()
+                q.put((rank, "no timeout raised"))
+            except ExchangeTimeout as ex:
+                q.put((rank, "ok" if "no message from rank 1" in str(ex) and "'u'" in str(ex) else str(ex)))
+        else:
+            q.put((rank, "ok"))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+def test_nvlink_halo_wait_times_out_as_exchange_timeout():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_timeout_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
+    assert outs == {0: "ok", 1: "ok"}, outs

@@ -391,6 +391,20 @@ int ml_put_rows(void *remote_dst, const void *dat, const int32_t *idx, int64_t n
                 int64_t elem_stride, int64_t comp_stride, uint64_t *remote_flag, int32_t *counter);
 int ml_wait_flag(const uint64_t *flag, uint64_t *expected, uint64_t timeout_ns, int64_t *err,
                  int64_t code);
+/* NVLink all-gather + rank-ordered fold of a reduction (replaces the NCCL
+ * all-gather + ml_combine_ranks of executor.py:652-660): ml_reduce_put
+ * stores this rank's partial (nbytes) into row `me` of every rank's gather
+ * buffer (remote_rows[r], device array of IPC-mapped pointers) after that
+ * rank's credit, and bumps its delivery counter (remote_delivery[r]);
+ * ml_reduce_fold waits for all ranks' deliveries, folds the rows in rank
+ * order onto `value` and returns a credit to every source.  Counter arrays
+ * are device memory; waits are bounded like ml_wait_flag. */
+int ml_reduce_put(const void *partial, int32_t nbytes, void *const *remote_rows, uint64_t *const *remote_delivery,
+                  const uint64_t *credit, uint64_t *credit_expected, int32_t nranks, uint64_t timeout_ns,
+                  int64_t *err, int64_t code);
+int ml_reduce_fold(void *value, const void *rows, const uint64_t *delivery, uint64_t *delivery_expected,
+                   uint64_t *const *remote_credit, int32_t nranks, int32_t dim, int32_t mode, int32_t dtype,
+                   uint64_t timeout_ns, int64_t *err, int64_t code);
 /* Stream-ordered: after the work enqueued so far, increment a (peer) counter
  * system-wide — the consumer's "import buffer free again" credit. */
 int ml_signal_flag(uint64_t *remote_flag);

@@ -42,6 +42,7 @@ EXPORTED = [
     "ml_program_free", "ml_program_set_concurrent", "ml_program_deps",
     "ml_pack_rows", "ml_unpack_rows", "ml_combine_ranks", "ml_stream",
     "ml_ipc_handle", "ml_ipc_open", "ml_ipc_close", "ml_put_rows", "ml_wait_flag", "ml_signal_flag",
+    "ml_reduce_put", "ml_reduce_fold",
     "ml_flush_l2", "ml_timer_create", "ml_timer_start", "ml_timer_stop", "ml_timer_free",
 ]
 
@@ -178,6 +179,9 @@ _SIGNATURES = {
     "ml_put_rows": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.c_int64, C.c_int64, _P, _P]),
     "ml_wait_flag": (C.c_int, [_P, _P, C.c_uint64, _P, C.c_int64]),
     "ml_signal_flag": (C.c_int, [_P]),
+    "ml_reduce_put": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, C.c_uint64, _P, C.c_int64]),
+    "ml_reduce_fold": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
+                                 _P, C.c_int64]),
     "ml_flush_l2": (C.c_int, []),
     "ml_timer_create": (C.c_int, [_PP]),
     "ml_timer_start": (C.c_int, [_P]),

@@ -984,6 +984,65 @@ __global__ void k_signal(unsigned long long *rflag) {
     atomicAdd_system(rflag, 1ull);
 }
 
+__device__ __forceinline__ bool wait_counter(const unsigned long long *flag, unsigned long long want,
+                                             unsigned long long timeout_ns, long long *err, long long code) {
+    unsigned long long v, t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+        if (v >= want) return true;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (timeout_ns && t - t0 > timeout_ns) {
+            if (err) atomicCAS(reinterpret_cast<unsigned long long *>(err), 0ull,
+                               static_cast<unsigned long long>(code));
+            return false;
+        }
+        __nanosleep(64);
+    }
+}
+
+// NVLink all-gather of a reduction partial: thread r waits until rank r has
+// consumed this rank's previous row (credit), stores the partial into row `me`
+// of rank r's gather buffer, fences system-wide and bumps r's delivery counter.
+__global__ void k_reduce_put(const unsigned long long *partial, int nwords, unsigned long long *const *rrow,
+                             unsigned long long *const *rdeliv, const unsigned long long *credit,
+                             unsigned long long *credit_exp, int nranks, unsigned long long timeout_ns,
+                             long long *err, long long code) {
+    const int r = threadIdx.x;
+    if (r >= nranks) return;
+    const unsigned long long want = credit_exp[r] + 1;
+    credit_exp[r] = want;
+    wait_counter(credit + r, want, timeout_ns, err, -code);
+    for (int w = 0; w < nwords; ++w) rrow[r][w] = partial[w];
+    __threadfence_system();
+    atomicAdd_system(rdeliv[r], 1ull);
+}
+// wait for every rank's row, fold the rows in rank order onto the value (the
+// order of ml_combine_ranks), then return a credit to every source
+template <class T, int M>
+__global__ void k_reduce_fold(T *value, const T *rows, const unsigned long long *deliv,
+                              unsigned long long *deliv_exp, unsigned long long *const *rcredit, int nranks,
+                              int dim, unsigned long long timeout_ns, long long *err, long long code) {
+    const int r = threadIdx.x;
+    if (r < nranks) {
+        const unsigned long long want = deliv_exp[r] + 1;
+        deliv_exp[r] = want;
+        wait_counter(deliv + r, want, timeout_ns, err, code);
+    }
+    __syncthreads();
+    __threadfence_system();
+    for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+        T v = value[c];
+        for (int q = 0; q < nranks; ++q) v = combine<M>(v, __ldcv(rows + int64_t(q) * dim + c));
+        value[c] = v;
+    }
+    __syncthreads();
+    if (r < nranks) {
+        __threadfence_system();
+        atomicAdd_system(rcredit[r], 1ull);
+    }
+}
+
 template <class T, int M>
 __global__ void k_combine_ranks(T *value, const T *gathered, int nranks, int dim) {
     for (int c = threadIdx.x; c < dim; c += blockDim.x) {
@@ -1066,6 +1125,51 @@ extern "C" int ml_wait_flag(const uint64_t *flag, uint64_t *expected, uint64_t t
     k_wait_flag<<<1, 1, 0, g_dev.stream>>>(reinterpret_cast<const unsigned long long *>(flag),
                                             reinterpret_cast<unsigned long long *>(expected), timeout_ns,
                                             reinterpret_cast<long long *>(err), code);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+extern "C" int ml_reduce_put(const void *partial, int32_t nbytes, void *const *remote_rows,
+                             uint64_t *const *remote_delivery, const uint64_t *credit, uint64_t *credit_expected,
+                             int32_t nranks, uint64_t timeout_ns, int64_t *err, int64_t code) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (nranks < 1 || nranks > 1024 || nbytes % 8) ML_FAIL(ML_EINVAL, "ml_reduce_put: bad arguments");
+    k_reduce_put<<<1, nranks, 0, g_dev.stream>>>(
+        static_cast<const unsigned long long *>(partial), nbytes / 8,
+        reinterpret_cast<unsigned long long *const *>(remote_rows),
+        reinterpret_cast<unsigned long long *const *>(remote_delivery),
+        reinterpret_cast<const unsigned long long *>(credit), reinterpret_cast<unsigned long long *>(credit_expected),
+        nranks, timeout_ns, reinterpret_cast<long long *>(err), code);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+extern "C" int ml_reduce_fold(void *value, const void *rows, const uint64_t *delivery, uint64_t *delivery_expected,
+                              uint64_t *const *remote_credit, int32_t nranks, int32_t dim, int32_t mode,
+                              int32_t dtype, uint64_t timeout_ns, int64_t *err, int64_t code) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (nranks < 1 || nranks > 1024) ML_FAIL(ML_EINVAL, "ml_reduce_fold: bad arguments");
+    cudaStream_t s = g_dev.stream;
+    const int threads = std::max(32, (std::max<int>(nranks, dim) + 31) / 32 * 32);
+    auto d = reinterpret_cast<const unsigned long long *>(delivery);
+    auto de = reinterpret_cast<unsigned long long *>(delivery_expected);
+    auto rcr = reinterpret_cast<unsigned long long *const *>(remote_credit);
+    auto e = reinterpret_cast<long long *>(err);
+#define ML_RF(T, M) k_reduce_fold<T, M><<<1, threads, 0, s>>>(static_cast<T *>(value), static_cast<const T *>(rows), \
+                                                         d, de, rcr, nranks, dim, timeout_ns, e, code)
+    if (dtype == ML_F64) {
+        if (mode == ML_INC) ML_RF(double, MINC);
+        else if (mode == ML_MIN) ML_RF(double, MMIN);
+        else if (mode == ML_MAX) ML_RF(double, MMAX);
+        else ML_FAIL(ML_EINVAL, "ml_reduce_fold: mode %d is not a reduction", mode);
+    } else {
+        if (mode == ML_INC) ML_RF(int64_t, MINC);
+        else if (mode == ML_MIN) ML_RF(int64_t, MMIN);
+        else if (mode == ML_MAX) ML_RF(int64_t, MMAX);
+        else ML_FAIL(ML_EINVAL, "ml_reduce_fold: mode %d is not a reduction", mode);
+    }
+#undef ML_RF
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

@@ -577,6 +577,106 @@ class NvlinkHalo:
         self.opened = []
 
 
+class NvlinkReduce:
+    """Reductions over NVLink peer memory: per reducing argument a gather
+    buffer [nranks][dim] on every rank; ``ml_reduce_put`` stores this rank's
+    partial into its row of every rank's buffer (IPC-mapped), and
+    ``ml_reduce_fold`` waits for all rows and folds them in rank order onto
+    the device-resident value — the result of the NCCL all-gather +
+    ``ml_combine_ranks`` path, in two single-CTA kernels with no host or NCCL
+    involvement (graph-capturable).  Credits keep a rank from overwriting a
+    row the owner has not folded yet."""
+
+    def __init__(self, rp: RankProgram, transport, timeout_ms: float = 10000.0):
+        import ctypes as C
+        from . import _native as N
+        self.C, self.N, self.rp = C, N, rp
+        L = N.lib()
+        nr, me = rp.nranks, rp.rank
+        self.timeout_ns = int(max(timeout_ms, 0.0) * 1e6)
+        self.slot = {}                                    # id(part) -> (k, offset, nbytes)
+        off = 0
+        k = 0
+        for reds in rp.reductions:
+            for part, _val, _mode in reds:
+                nb = part.buffer.nbytes
+                self.slot[id(part)] = (k, off, nb)
+                off += nr * nb
+                k += 1
+        self.nslot = k
+        self.rows = N.DeviceBuffer(max(off, 8))
+        self.cnt = N.DeviceBuffer(16 * nr * max(k, 1))    # deliveries [k][src], credits [k][dst]
+        self.exp = N.DeviceBuffer(16 * nr * max(k, 1))
+        self.err = N.DeviceBuffer(8)
+        N.check(L.ml_memset(self.exp.ptr, 0, self.exp.nbytes))
+        N.check(L.ml_memset(self.err.ptr, 0, 8))
+        self.cnt.upload(np.concatenate([np.zeros(nr * max(k, 1), np.uint64),
+                                        np.ones(nr * max(k, 1), np.uint64)]))
+        N.check(L.ml_synchronize())
+        hr, hc = (C.c_char * 64)(), (C.c_char * 64)()
+        N.check(L.ml_ipc_handle(self.rows.ptr, hr), "ml_ipc_handle")
+        N.check(L.ml_ipc_handle(self.cnt.ptr, hc), "ml_ipc_handle")
+        allh = transport.allgather_object((bytes(hr), bytes(hc)))
+        self.opened = []
+        peer_rows, peer_cnt = {}, {}
+        for r in range(nr):
+            if r == me:
+                peer_rows[r], peer_cnt[r] = self.rows.ptr, self.cnt.ptr
+            else:
+                peer_rows[r], peer_cnt[r] = self._open(allh[r][0]), self._open(allh[r][1])
+        deliv = lambda kk, src: 8 * (kk * nr + src)                          # noqa: E731
+        credit = lambda kk, dst: 8 * ((self.nslot + kk) * nr + dst)           # noqa: E731
+        self.args = {}
+        for pid, (kk, o, nb) in self.slot.items():
+            rrow = np.array([peer_rows[r] + o + me * nb for r in range(nr)], np.uint64)
+            rdel = np.array([peer_cnt[r] + deliv(kk, me) for r in range(nr)], np.uint64)
+            rcre = np.array([peer_cnt[r] + credit(kk, me) for r in range(nr)], np.uint64)
+            self.args[pid] = dict(rrow=_dev_array(rrow), rdel=_dev_array(rdel), rcre=_dev_array(rcre),
+                                  credit=self.cnt.ptr + credit(kk, 0), credit_exp=self.exp.ptr + credit(kk, 0),
+                                  deliv=self.cnt.ptr + deliv(kk, 0), deliv_exp=self.exp.ptr + deliv(kk, 0),
+                                  rows=self.rows.ptr + o, k=kk)
+
+    def _open(self, handle: bytes) -> int:
+        C, N = self.C, self.N
+        p = C.c_void_p()
+        N.check(N.lib().ml_ipc_open(C.create_string_buffer(handle, 64), C.byref(p)), "ml_ipc_open")
+        self.opened.append(p.value)
+        return p.value
+
+    def reduce(self, part, mode, partial_ptr: int, value_ptr: int, loop_index: int) -> None:
+        N, rp = self.N, self.rp
+        a = self.args[id(part)]
+        code = 1 + loop_index * max(self.nslot, 1) + a["k"]
+        N.check(N.lib().ml_reduce_put(partial_ptr, part.buffer.nbytes, a["rrow"].ptr, a["rdel"].ptr, a["credit"],
+                                      a["credit_exp"], rp.nranks, self.timeout_ns, self.err.ptr, code),
+                "ml_reduce_put")
+        dt = 0 if np.dtype(part.dtype) == np.float64 else 1
+        N.check(N.lib().ml_reduce_fold(value_ptr, a["rows"], a["deliv"], a["deliv_exp"], a["rcre"].ptr,
+                                       rp.nranks, part.dim, {"INC": 3, "MIN": 4, "MAX": 5}[mode.name], dt,
+                                       self.timeout_ns, self.err.ptr, code), "ml_reduce_fold")
+
+    def check(self) -> None:
+        code = np.zeros(1, np.int64)
+        self.err.download(code)
+        if int(code[0]):
+            from .executor import ExchangeTimeout
+            raise ExchangeTimeout(f"rank {self.rp.rank}: a reduction exchange did not complete within "
+                                  f"{self.timeout_ns / 1e6:.0f} ms (code {int(code[0])})")
+
+    def close(self):
+        for p in self.opened:
+            self.N.lib().ml_ipc_close(p)
+        self.opened = []
+
+
+def _dev_array(a: np.ndarray):
+    from . import _native as N
+    buf = N.DeviceBuffer(max(a.nbytes, 8))
+    if a.nbytes:
+        buf.upload(np.ascontiguousarray(a))
+    return buf
+
+
 class StreamRank:
     """Stream-ordered rank executor (the production multi-GPU path).
 
@@ -635,21 +735,34 @@ class StreamRank:
                 dat_mirror(d)
         self._splits: dict = {}
         self.split = [None] * len(self.entries)     # last split used by each loop (reporting)
+        # exchange index lists and staging buffers up front (never inside a capture)
+        for name in sorted({n for reads, _w in rp.roles for n in reads if n in rp.dats}):
+            d = rp.dats[name]
+            exports, imports = rp.halo_rows(name)
+            for dst, ids in exports.items():
+                self._index(("e", name, dst), ids)
+                self._buf(("s", name, dst), ids.size * d.dim, d.dtype)
+            for src, ids in imports.items():
+                self._index(("i", name, src), ids)
+                self._buf(("r", name, src), ids.size * d.dim, d.dtype)
         # halo path: direct NVLink stores (CUDA IPC) unless ML_HALO=nccl; every
         # rank must agree, so a failure anywhere falls back everywhere
         self.nvlink = None
+        self.nvreduce = None
         self.halo_error = None
         if os.environ.get("ML_HALO", "p2p") == "p2p" and rp.nranks > 1:
             ok = 1
             try:
                 self.nvlink = NvlinkHalo(rp, transport, config.timeout_ms)
+                self.nvreduce = NvlinkReduce(rp, transport, config.timeout_ms)
             except Exception as ex:                     # noqa: BLE001 - reported, not hidden
                 self.halo_error = f"{type(ex).__name__}: {ex}"[:200]
                 ok = 0
             if min(transport.allgather_object(ok)) == 0:
-                if self.nvlink is not None:
-                    self.nvlink.close()
-                self.nvlink = None
+                for x in (self.nvlink, self.nvreduce):
+                    if x is not None:
+                        x.close()
+                self.nvlink = self.nvreduce = None
         global _LAST_HALO_PATH
         _LAST_HALO_PATH = "nvlink" if self.nvlink is not None else transport.name
 
@@ -837,6 +950,10 @@ class StreamRank:
             for part, val, mode in rp.reductions[i]:
                 nbytes = part.buffer.nbytes
                 po, go, vo = self.slots[id(part)], self.slots[("gather", id(part))], self.slots[id(val)]
+                if self.nvreduce is not None:
+                    base = self.arena.data_ptr()
+                    self.nvreduce.reduce(part, mode, base + po, base + vo, i)
+                    continue
                 tr.allgather_device(self.arena[go:go + nbytes * rp.nranks], self.arena[po:po + nbytes],
                                     self.lib_stream)
                 code = {"INC": 3, "MIN": 4, "MAX": 5}[mode.name]
@@ -853,6 +970,8 @@ class StreamRank:
         for e in self.entries:
             for d in e.written:
                 d._dev.device_newer = True
+        if not capturing:
+            self._ran = True
         return messages
 
     def capture(self, overlap: bool = True):
@@ -860,10 +979,24 @@ class StreamRank:
         reductions, the overlap fork/join) as a CUDA graph on the compute
         stream; replay() then launches a whole rank step with one call (the
         host no longer paces the GPU).  NCCL transport only."""
-        if self.transport.name != "nccl":
-            raise ExecError("graph capture needs the NCCL transport")
+        if self.transport.name != "nccl" and not (self.nvlink is not None and self.nvreduce is not None):
+            raise ExecError("graph capture needs NCCL or the NVLink halo + reduction paths")
         torch = self.torch
         self.finish()
+        if not self.__dict__.get("_ran"):
+            raise ExecError("capture() needs one eager run first (steady halo pattern)")
+        # build every core/boundary split the captured run will use (host + uploads),
+        # replaying the dirty-bit evolution of one run without touching the device
+        dirty = dict(self.rp.__dict__.get("dirty", {}))
+        for i in range(len(self.entries)):
+            reads, writes = self.rp.roles[i]
+            names = [n for n in reads if dirty.get(n)]
+            if names:
+                self._split(i, tuple(names))
+            for n in names:
+                dirty[n] = False
+            for n in writes:
+                dirty[n] = True
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=self.lib_stream):
             msgs = self.run(overlap, capturing=True)
@@ -887,6 +1020,8 @@ class StreamRank:
         self.N.check(self.N.lib().ml_synchronize(), "ml_synchronize")
         if self.nvlink is not None:
             self.nvlink.check([e.loop.name for e in self.entries])
+        if self.nvreduce is not None:
+            self.nvreduce.check()
         host = self.arena.cpu().numpy()
         for gid, val in self.rp.values.items():
             o = self.slots[id(val)]
@@ -1066,7 +1201,8 @@ def bench_distributed(args, metric):
     dev.run()                         # per-loop device times of one eager step (reported)
     dev.finish()
     loop_s = dev.loop_seconds()
-    graphed = transport.name == "nccl" and os.environ.get("ML_RANK_GRAPH", "1") == "1"
+    graphed = ((transport.name == "nccl" or (dev.nvlink is not None and dev.nvreduce is not None))
+               and os.environ.get("ML_RANK_GRAPH", "1") == "1")
     graph_error = None
     if graphed:                       # one graph launch per rank step (NCCL inside)
         try:
@@ -1137,6 +1273,8 @@ def bench_distributed(args, metric):
                            "transport": transport.name, "halo_nodes_per_rank": halo,
                            "halo_path": "nvlink-p2p (CUDA IPC peer stores)" if dev.nvlink is not None
                            else f"{transport.name} send/recv", "halo_p2p_error": dev.halo_error,
+                           "reduction_path": "nvlink-p2p all-gather + rank-ordered fold"
+                           if dev.nvreduce is not None else f"{transport.name} all-gather",
                            "overlapped_loops": split,
                            "cuda_graph": graphed, "cuda_graph_error": graph_error,
                            "l2": "per-rank working set streamed each step",

@@ -228,3 +228,58 @@ def test_nvlink_halo_wait_times_out_as_exchange_timeout():
         if p.is_alive():
             p.kill()
     assert outs == {0: "ok", 1: "ok"}, outs
+
+
+def _graph2_worker(rank, port, q):
+    """Two ranks on one GPU, NVLink (IPC) halos and reductions: a captured rank
+    step replayed twice equals two eager steps, on both ranks."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2",
+                      LOCAL_RANK="0", ML_TRANSPORT="gloo", ML_HALO="p2p")
+    sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        import paper_1403_7209_b200 as ml
+        from paper_1403_7209_b200 import apps
+        from paper_1403_7209_b200.multigpu import setup_distributed
+        outs = []
+        for graphed in (False, True):
+            mesh = apps.gen_hex_mesh(12, seed=6)
+            prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=6)
+            ml.renumber_mesh(mesh)
+            cfg = ml.BackendConfig(nranks=2, partitioner="rcb", device=0)
+            rp, dev, tr, layout, cfg = setup_distributed(prog, mesh, cfg)
+            assert dev.nvlink is not None and dev.nvreduce is not None
+            dev.run()
+            dev.finish()
+            if graphed:
+                dev.capture()
+                dev.replay()
+                dev.replay()
+            else:
+                dev.run()
+                dev.run()
+            dev.finish()
+            outs.append((rp.dats["q"].fetch()[: rp.n_owned["nodes"]],
+                         [v.buffer.copy() for v in rp.values.values()]))
+        same = (np.array_equal(outs[0][0], outs[1][0])
+                and all(np.array_equal(a, b) for a, b in zip(outs[0][1], outs[1][1])))
+        q.put((rank, "ok" if same else "graph replay differs from eager steps"))
+    except Exception:
+        import traceback
+        traceback.print_exc()
+        q.put((rank, traceback.format_exc()[-3000:]))
+
+
+def test_two_rank_graph_with_nvlink_paths_matches_eager():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_graph2_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert outs == {0: "ok", 1: "ok"}, outs

@@ -167,14 +167,16 @@ typedef struct ml_loop {
      * target, CSRs of its incidences through the first INC argument
      * (pf_off1/pf_elem1) and through the others (pf_off2/pf_elem2/pf_pos2,
      * position >= 1), element ascending; pf_tl* map list rows to target ids
-     * (NULL: identity).  pf_slots: device [n][INC args - 1][dim rounded up
-     * to even] (ml_loop_pfold_slot_bytes). */
+     * (NULL: identity).  pf_slots: device [secondary incidences][dim rounded
+     * up to even], rows in pf_elem2 order (ml_loop_pfold_slot_bytes). */
     int64_t pf_n1;
     const int32_t *pf_off1, *pf_elem1, *pf_tl1;
     int64_t pf_n2;
     const int32_t *pf_off2, *pf_elem2, *pf_tl2;
     const uint8_t *pf_pos2;
     void *pf_slots;
+    const int32_t *pf_slotpos;      /* [n][INC args - 1]: slot row of each secondary
+                                       increment = its index in pf_elem2 */
     int32_t pf_own_kb;              /* shared memory (KB per CTA) for the targets'
                                        own READ rows in pass 1; 0: read from L1/L2 */
     int32_t pf_pad;

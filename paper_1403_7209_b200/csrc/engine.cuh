@@ -127,7 +127,8 @@ struct PFoldParams {
     int64_t n2;                          // targets with secondary incidences
     const int32_t *off2, *elem2, *tl2;
     const uint8_t *pos2;                 // INC-argument position (>= 1) of each
-    void *slots;                         // [n][nslot][dgp]
+    void *slots;                         // [secondary incidences][dgp], in off2 order
+    const int32_t *slotpos;              // [n][nslot]: slot row of (element, INC position >= 1)
     int32_t nslot, dgp;
     // own-row staging: READ dats read through the first INC argument's column
     // (the target itself) are copied once per target to shared memory
@@ -665,18 +666,22 @@ struct Engine {
         }
     }
     // primary fold: INC arguments at positions >= 1 -> the element's slots
+    // slots: the element's secondary increments go to the rows of the targets'
+    // secondary CSR (slotpos[e][pos-1]), so pass 2 reads each target's rows
+    // contiguously
     template <int DGP, size_t... Is>
-    __device__ __forceinline__ static void stage_rest(Slots &s, void *row, cuda::std::index_sequence<Is...>) {
-        (stage_rest_one<Is, DGP>(s, row), ...);
+    __device__ __forceinline__ static void stage_rest(Slots &s, void *slots, const int32_t *slotpos,
+                                                      cuda::std::index_sequence<Is...>) {
+        (stage_rest_one<Is, DGP>(s, slots, slotpos), ...);
     }
     template <size_t I, int DGP>
-    __device__ __forceinline__ static void stage_rest_one(Slots &s, void *row) {
+    __device__ __forceinline__ static void stage_rest_one(Slots &s, void *slots, const int32_t *slotpos) {
         using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
         if constexpr (A::kind == KI && A::mode == MINC) {
             constexpr int pos = IncIndex<As...>::template of<I>();
             if constexpr (pos >= 1) {
                 using T = typename A::type;
-                T *dst = static_cast<T *>(row) + (pos - 1) * DGP;
+                T *dst = static_cast<T *>(slots) + int64_t(__ldg(slotpos + pos - 1)) * DGP;
                 if constexpr (A::dim % 2 == 0 && DGP % 2 == 0 && cuda::std::is_same_v<T, double>) {
 #pragma unroll
                     for (int c = 0; c < A::dim; c += 2)
@@ -1027,7 +1032,7 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
             E::call(s, p, e, idx);
             E::template gather_op<MINC, 0, DG>(s, 0, run, idx);
             if constexpr (NW > 1)
-                E::template stage_rest<DGP>(s, static_cast<TG *>(pf.slots) + e * int64_t(NW - 1) * DGP, idx);
+                E::template stage_rest<DGP>(s, pf.slots, pf.slotpos + e * int64_t(NW - 1), idx);
         }
 #pragma unroll
         for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
@@ -1050,7 +1055,7 @@ __global__ void __launch_bounds__(256) k_pfold_rest(const __grid_constant__ Laun
 #pragma unroll
         for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
         for (int k = __ldg(pf.off2 + t), ke = __ldg(pf.off2 + t + 1); k < ke; ++k) {
-            const T *src = slots + (int64_t(__ldg(pf.elem2 + k)) * pf.nslot + (__ldg(pf.pos2 + k) - 1)) * DGP;
+            const T *src = slots + int64_t(k) * DGP;        // rows in CSR order: contiguous per target
             if constexpr (DG % 2 == 0 && cuda::std::is_same_v<T, double>) {
 #pragma unroll
                 for (int c = 0; c < DG; c += 2) {

@@ -313,6 +313,8 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         pf.tl2 = L->pf_tl2;
         pf.pos2 = L->pf_pos2;
         pf.slots = L->pf_slots;
+        pf.slotpos = L->pf_slotpos;
+        if (f.pfold_nslot > 0 && !pf.slotpos) ML_FAIL(ML_EINVAL, "loop '%s': pfold slot positions missing", L->name);
         pf.nslot = f.pfold_nslot;
         pf.dgp = f.pfold_dgp;
         // own-row staging: READ dats on the first INC argument's column

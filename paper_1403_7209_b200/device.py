@@ -244,6 +244,14 @@ def pfold_lists_host(host: dict) -> dict:
         out[f"tl{which}"] = np.ascontiguousarray(tl[keep], dtype=np.int32)
         if which == 2:
             out["pos2"] = np.ascontiguousarray(p_[m], dtype=np.uint8)
+    # slot row of each (element, position >= 1): its index in the secondary CSR
+    nw = int(p_.max(initial=0)) + 1 if p_.size else 1
+    n_el = int(e.max(initial=-1)) + 1
+    slotpos = np.zeros(max(n_el * max(nw - 1, 1), 1), np.int32)
+    if nw > 1 and out["elem2"].size:
+        slotpos[out["elem2"].astype(np.int64) * (nw - 1) + out["pos2"].astype(np.int64) - 1] = \
+            np.arange(out["elem2"].size, dtype=np.int32)
+    out["slotpos"] = slotpos
     return out
 
 
@@ -292,12 +300,12 @@ class PFoldMirror:
     incidences through the first INC argument (pass 1) and through the others
     (pass 2), element ascending; plus the per-element slot buffer."""
 
-    __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2")
+    __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos")
 
     def __init__(self, g: GatherMirror):
         h = pfold_lists_host(g.host)
         self.n1, self.n2 = h["n1"], h["n2"]
-        for k in ("off1", "elem1", "tl1", "off2", "elem2", "tl2", "pos2"):
+        for k in ("off1", "elem1", "tl1", "off2", "elem2", "tl2", "pos2", "slotpos"):
             setattr(self, k, _upload(h[k]))
 
 

@@ -500,6 +500,9 @@ def test_gather_hub_rows_and_pfold_lists(rng):
                     rows = np.flatnonzero((tl == t) & (seg >= 0))
                     assert seg[rows].tolist() == list(range(h["hub_off"][k], h["hub_off"][k + 1]))
             pf = pfold_lists_host(h["host"])
+            k = np.arange(pf["elem2"].size)
+            np.testing.assert_array_equal(
+                pf["slotpos"][pf["elem2"].astype(np.int64) + pf["pos2"].astype(np.int64) - 1], k)
             for which, sel in ((1, lambda a: a == 0), (2, lambda a: a > 0)):
                 o, el, t1 = pf[f"off{which}"], pf[f"elem{which}"], pf[f"tl{which}"]
                 for r in range(pf[f"n{which}"]):

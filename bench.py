@@ -167,8 +167,8 @@ def run_ours(args) -> None:
                               "schedule": e.sched if e.plan.has_writes else "direct",
                               "nb": e.st.nb, "nc": e.st.nc}
     names = [e.loop.name for e in cp.entries]
-    dom = cp.entries[names.index("vflux") if "vflux" in names
-                     else max(range(len(names)), key=lambda i: loops[names[i]]["ms"])]
+    flux = [i for i, n in enumerate(names) if "vflux" in n.split("+")]
+    dom = cp.entries[flux[0] if flux else max(range(len(names)), key=lambda i: loops[names[i]]["ms"])]
     t_dom = statistics.mean(per_loop[dom.loop.name])
     achieved = dom.alg / t_dom / 1e9
     traffic = None

@@ -333,6 +333,13 @@ int ml_functor_lookup(const char *name, int32_t dtype, int32_t *functor_id);
 int ml_functor_signature(int32_t functor_id, int32_t *nargs, int32_t *kinds,
                          int32_t *modes, int32_t *dims, int32_t *dtypes);
 int ml_functor_count(int32_t *count);
+/* Loop chains (ML_REGISTER_CHAIN in a functor file): a loop of functor
+ * `first` immediately followed by one of `second` may run as one loop of the
+ * returned fused functor; argument i of the first loop binds to fused
+ * argument apos[i] (i < *na), argument j of the second to bpos[j] (j < *nb).
+ * ML_ENOFUNCTOR when no chain exists. */
+int ml_chain_lookup(const char *first, const char *second, char *fused, int32_t buflen, int32_t *na,
+                    int32_t *apos, int32_t *nb, int32_t *bpos);
 int ml_functor_name(int32_t functor_id, char *buf, int32_t buflen, int32_t *dtype);
 /* Device scratch a loop needs (global-reduction partials). */
 int ml_loop_scratch_bytes(const ml_loop_t *loop, uint64_t *bytes);

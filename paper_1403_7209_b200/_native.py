@@ -36,7 +36,7 @@ EXPORTED = [
     "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
     "ml_staging_export_seg", "ml_staging_export_arrival", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
-    "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name",
+    "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name", "ml_chain_lookup",
     "ml_loop_scratch_bytes", "ml_loop_run", "ml_loop_pfold_slot_bytes",
     "ml_program_create", "ml_program_run", "ml_program_replay", "ml_program_loop_times",
     "ml_program_free", "ml_program_set_concurrent", "ml_program_deps",
@@ -159,6 +159,7 @@ _SIGNATURES = {
     "ml_functor_lookup": (C.c_int, [C.c_char_p, C.c_int32, _I32P]),
     "ml_functor_signature": (C.c_int, [C.c_int32, _I32P, _I32P, _I32P, _I32P, _I32P]),
     "ml_functor_count": (C.c_int, [_I32P]),
+    "ml_chain_lookup": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32, _I32P, _P, _I32P, _P]),
     "ml_functor_name": (C.c_int, [C.c_int32, C.c_char_p, C.c_int32, _I32P]),
     "ml_loop_scratch_bytes": (C.c_int, [C.POINTER(MlLoop), C.POINTER(C.c_uint64)]),
     "ml_loop_run": (C.c_int, [C.POINTER(MlLoop)]),

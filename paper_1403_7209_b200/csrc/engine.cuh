@@ -1759,10 +1759,42 @@ struct Registrar {
     }
 };
 
+// ---- loop chains -------------------------------------------------------------
+// A chain declares that a loop running functor FIRST immediately followed by
+// one running SECOND over the same set may execute as one loop of functor
+// FUSED: FUSED::first_args[i] / second_args[j] give the fused argument that
+// argument i of the first loop / j of the second binds to.  Arguments of the
+// two loops that bind to one fused argument must be identical (same dat,
+// map, slot and mode) and the loops may share no other written data — the
+// executor checks both (chain.py) before fusing.
+struct ChainEntry {
+    const char *first, *second, *fused;
+    int32_t na, nb;
+    int32_t apos[MAX_ARGS], bpos[MAX_ARGS];
+};
+void register_chain(const ChainEntry &c);
+
+template <class F>
+struct ChainRegistrar {
+    ChainRegistrar(const char *first, const char *second, const char *fused) {
+        ChainEntry c{};
+        c.first = first;
+        c.second = second;
+        c.fused = fused;
+        c.na = int32_t(sizeof(F::first_args) / sizeof(F::first_args[0]));
+        c.nb = int32_t(sizeof(F::second_args) / sizeof(F::second_args[0]));
+        for (int i = 0; i < c.na; ++i) c.apos[i] = F::first_args[i];
+        for (int i = 0; i < c.nb; ++i) c.bpos[i] = F::second_args[i];
+        register_chain(c);
+    }
+};
+
 #define ML_CAT2(a, b) a##b
 #define ML_CAT(a, b) ML_CAT2(a, b)
 #define ML_REGISTER(NAME, FUNCTOR, T) \
     static ::ml::Registrar<FUNCTOR, T> ML_CAT(ml_reg_, __COUNTER__)(NAME)
+#define ML_REGISTER_CHAIN(FIRST, SECOND, FUSED, FUNCTOR) \
+    static ::ml::ChainRegistrar<FUNCTOR> ML_CAT(ml_chain_, __COUNTER__)(FIRST, SECOND, FUSED)
 
 // integer floor division with Python semantics (numpy int64 //)
 __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {

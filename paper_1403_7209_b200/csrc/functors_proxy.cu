@@ -118,6 +118,30 @@ struct ProxyVflux {
     }
 };
 
+// Loop chain iflux -> vflux (both gather the same edge's node rows and
+// increment res): one pass evaluates iflux then vflux on each edge with the
+// same expression trees, vflux's increments added after iflux's, so each
+// edge's node rows are fetched once for both loops.
+struct ProxyFluxes {
+    // fused argument of each iflux argument (w q1 q2 x1 x2 l1 l2 r1 r2) and
+    // each vflux argument (w q1 q2 g1 g2 x1 x2 a1 a2 r1 r2): w, q, x and res
+    // are shared, grad and aux come from vflux alone
+    static constexpr int first_args[9] = {0, 1, 2, 3, 4, 5, 6, 11, 12};
+    static constexpr int second_args[11] = {0, 1, 2, 7, 8, 3, 4, 9, 10, 11, 12};
+    template <class T>
+    using sig = Sig<Arg<KD, MR, 3, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, 3, T>,
+                    Arg<KI, MR, 3, T>, Arg<KI, MR, NLIM, T>, Arg<KI, MR, NLIM, T>, Arg<KI, MR, NG, T>,
+                    Arg<KI, MR, NG, T>, Arg<KI, MR, NAUX, T>, Arg<KI, MR, NAUX, T>,
+                    Arg<KI, MINC, NQ, T>, Arg<KI, MINC, NQ, T>>;
+    template <class W, class Q1, class Q2, class X1, class X2, class L1, class L2, class G1, class G2,
+              class A1, class A2, class R1, class R2>
+    __device__ static void apply(const Consts &k, W w, Q1 q1, Q2 q2, X1 x1, X2 x2, L1 l1, L2 l2, G1 g1, G2 g2,
+                                 A1 a1, A2 a2, R1 r1, R2 r2) {
+        ProxyIflux::apply(k, w, q1, q2, x1, x2, l1, l2, r1, r2);
+        ProxyVflux::apply(k, w, q1, q2, g1, g2, x1, x2, a1, a2, r1, r2);
+    }
+};
+
 struct ProxyUpdate {
     template <class T>
     using sig = Sig<Arg<KD, MW, NQ, T>, Arg<KD, MR, NQ, T>, Arg<KD, MRW, NQ, T>, Arg<KD, MR, 1, T>,
@@ -159,6 +183,8 @@ ML_REGISTER("proxy_grad", ProxyGrad, double);
 ML_REGISTER("proxy_iflux", ProxyIflux, double);
 ML_REGISTER("proxy_vflux", ProxyVflux, double);
 ML_REGISTER("proxy_update", ProxyUpdate, double);
+ML_REGISTER("proxy_fluxes", ProxyFluxes, double);
+ML_REGISTER_CHAIN("proxy_iflux", "proxy_vflux", "proxy_fluxes", ProxyFluxes);
 ML_REGISTER("proxy_bc", ProxyBc, double);
 
 }  // namespace ml

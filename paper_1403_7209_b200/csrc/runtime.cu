@@ -33,6 +33,11 @@ static std::vector<FunctorEntry> &registry() {
     return r;
 }
 void register_functor(const FunctorEntry &e) { registry().push_back(e); }
+static std::vector<ChainEntry> &chains() {
+    static std::vector<ChainEntry> c;
+    return c;
+}
+void register_chain(const ChainEntry &c) { chains().push_back(c); }
 
 // ---- per-device state ------------------------------------------------------------
 struct DeviceState {
@@ -657,6 +662,23 @@ extern "C" int ml_functor_lookup(const char *name, int32_t dtype, int32_t *funct
             return ML_OK;
         }
     ML_FAIL(ML_ENOFUNCTOR, "no compiled functor '%s' for dtype %s", name, dtype == ML_F64 ? "float64" : "int64");
+}
+
+extern "C" int ml_chain_lookup(const char *first, const char *second, char *fused, int32_t buflen,
+                               int32_t *na, int32_t *apos, int32_t *nb, int32_t *bpos) {
+    for (const ChainEntry &c : chains())
+        if (std::strcmp(c.first, first) == 0 && std::strcmp(c.second, second) == 0) {
+            if (fused && buflen > 0) {
+                std::strncpy(fused, c.fused, size_t(buflen) - 1);
+                fused[buflen - 1] = 0;
+            }
+            if (na) *na = c.na;
+            if (nb) *nb = c.nb;
+            if (apos) std::memcpy(apos, c.apos, sizeof(int32_t) * size_t(c.na));
+            if (bpos) std::memcpy(bpos, c.bpos, sizeof(int32_t) * size_t(c.nb));
+            return ML_OK;
+        }
+    return ML_ENOFUNCTOR;      // no chain: not an error condition, no message set
 }
 
 extern "C" int ml_functor_signature(int32_t id, int32_t *nargs, int32_t *kinds, int32_t *modes,

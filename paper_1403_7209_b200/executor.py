@@ -34,6 +34,7 @@ from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Me
 from .device import (dat_mirror, fold_eligible, gather_eligible, gather_mirror, map_mirror,
                      pfold_mirror, plan_mirror, schedule_mirror, staging_mirror, tile_eligible,
                      tile_mirror)
+from .chain import chain_program
 from .kernels import resolve_kernel
 from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
 from .plan import plan_for, plan_stats
@@ -88,6 +89,7 @@ class BackendConfig:
     concurrent_loops: bool = True           # graphs/untimed runs: independent loops overlap on streams
     pfold_own_kb: int = 0                   # pfold pass 1: smem per CTA for the targets' own rows
                                             # (0: from L1/L2 — faster on B200, see profiles/)
+    chain_loops: bool = True                # run registered adjacent loop pairs as one loop (chain.py)
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -385,6 +387,8 @@ class CompiledProgram:
     def __init__(self, program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
                  iter_counts: dict | None = None, rlim: dict | None = None):
         self.loops = list(program)
+        # loops as launched: registered adjacent pairs fused (chain.py)
+        self.run_loops = chain_program(self.loops, mesh) if config.chain_loops else self.loops
         self.mesh = mesh
         self.version = mesh.version
         globs: list[Global] = []
@@ -401,7 +405,7 @@ class CompiledProgram:
         self.gdev = N.DeviceBuffer(max(off, 256))
         self.ghost = N.PinnedArray((max(off, 256),), np.uint8)
         self.entries = [_LoopEntry(l, mesh, config, self.gslot, self.gdev.ptr, iter_counts, rlim)
-                        for l in self.loops]
+                        for l in self.run_loops]
         self.all_dats = []
         for e in self.entries:
             for d in e.dats:
@@ -595,7 +599,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
            config.dataflow, config.inc_staging, config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.flow_windows,
            config.flow_window_l2_fraction, config.tile_smem_kb, config.tile_cmax, config.tile_threads, config.coord_dat,
-           config.pfold_own_kb, config.concurrent_loops,
+           config.pfold_own_kb, config.concurrent_loops, config.chain_loops,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

@@ -1,0 +1,88 @@
+"""Loop chaining legality (chain.py) on CPU: which adjacent pairs fuse, the
+fused argument list, and — through the serial oracle running the fused
+Python kernel — that a chained program computes the unchained result within
+the reference tolerance.  The device runs of chained loops are in
+test_gpu_parity.py."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import serial
+from paper_1403_7209_b200 import apps
+from paper_1403_7209_b200.chain import chain_lookup, chain_pair, chain_program
+from paper_1403_7209_b200.core import INC, READ, RW, Loop, arg_global, arg_indirect, Global
+
+
+def _proxy(N=5, steps=2, seed=3):
+    mesh = apps.gen_hex_mesh(N, seed=seed)
+    prog, h = apps.build_hydra_proxy(mesh, steps=steps, seed=seed)
+    return mesh, prog, h
+
+
+def test_registered_chain_and_argument_map():
+    fused, apos, bpos = chain_lookup("proxy_iflux", "proxy_vflux")
+    assert fused == "proxy_fluxes" and len(apos) == 9 and len(bpos) == 11
+    assert sorted(set(apos) | set(bpos)) == list(range(13))
+    assert chain_lookup("proxy_vflux", "proxy_iflux") is None
+    assert chain_lookup("edge_flux", "proxy_vflux") is None
+
+
+def test_proxy_program_chains_each_flux_pair():
+    mesh, prog, h = _proxy()
+    out = chain_program(prog, mesh)
+    assert [l.name for l in out] == ["save", "dt_calc", "grad_edge", "iflux+vflux", "update", "bc"] * 2
+    assert chain_program(prog, mesh)[3] is out[3]           # cached: compiled programs stay valid
+    fl = out[3]
+    iflux, vflux = prog[3], prog[4]
+    assert list(fl.args[:7]) == list(iflux.args[:7])
+    assert [fl.args[i] for i in (7, 8, 9, 10)] == [vflux.args[i] for i in (3, 4, 7, 8)]
+    assert [a.mode for a in fl.args[11:]] == [INC, INC] and fl.args[11].dat is h["res"]
+
+
+def test_chained_program_matches_unchained_in_the_oracle():
+    ma, pa, ha = _proxy(6, steps=2, seed=4)
+    mb, pb, hb = _proxy(6, steps=2, seed=4)
+    serial.run_program(pa)
+    serial.run_program(chain_program(pb, mb))
+    for k in ("q", "q_old", "dt_loc"):
+        np.testing.assert_allclose(hb[k].fetch(), ha[k].fetch(), rtol=1e-12, atol=1e-300)
+    ma, pa, ha = _proxy(6, steps=1, seed=4)
+    mb, pb, hb = _proxy(6, steps=1, seed=4)
+    serial.run_program(pa[:5])
+    serial.run_program(chain_program(pb[:5], mb))
+    ref = ha["res"].fetch()
+    np.testing.assert_allclose(hb["res"].fetch(), ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("change", ["other_set", "reads_res", "writes_q", "global", "swapped"])
+def test_illegal_pairs_do_not_chain(change):
+    mesh, prog, h = _proxy(4, steps=1)
+    iflux, vflux = prog[3], prog[4]
+    args = list(vflux.args)
+    en = iflux.args[1].map
+    A, B = iflux, vflux
+    if change == "other_set":
+        B = Loop("vflux", mesh.sets["nodes"], [], vflux.kernel)
+    elif change == "reads_res":          # the second loop READs what the first INCs
+        args[1] = arg_indirect(h["res"], en, 1, READ)
+        B = Loop("vflux", vflux.iter_set, args, vflux.kernel)
+    elif change == "writes_q":           # the second loop modifies what the first reads
+        args[1] = arg_indirect(h["q"], en, 1, RW)
+        B = Loop("vflux", vflux.iter_set, args, vflux.kernel)
+    elif change == "global":
+        g = Global(np.zeros(1), "g")
+        B = Loop("vflux", vflux.iter_set, args + [arg_global(g, INC)], vflux.kernel)
+    elif change == "swapped":
+        A, B = vflux, iflux
+    assert chain_pair(A, B) is None
+    assert [l.name for l in chain_program([A, B], mesh)] == [A.name, B.name]
+
+
+def test_non_identical_shared_argument_does_not_chain():
+    """vflux's x rows not listed in the fused map must equal iflux's exactly."""
+    mesh, prog, h = _proxy(4, steps=1)
+    iflux, vflux = prog[3], prog[4]
+    args = list(vflux.args)
+    args[5] = arg_indirect(h["x"], iflux.args[3].map, 2, READ)     # slot swapped
+    assert chain_pair(iflux, Loop("vflux", vflux.iter_set, args, vflux.kernel)) is None

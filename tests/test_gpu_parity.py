@@ -283,7 +283,8 @@ def test_gather_schedule_reproduces_serial_order_bitwise(soa, sched):
     order, so even float64 raw INC accumulators equal the oracle bit for bit."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(20, soa=soa)
     bulk.run_program(rprog[:5], resolve_kernel)
-    ml.run_program(prog[:5], mesh, cfg(inc_schedule=sched))
+    # unchained: a chained iflux+vflux interleaves the two loops' increments
+    ml.run_program(prog[:5], mesh, cfg(inc_schedule=sched, chain_loops=False))
     for k in ("grad", "res", "q_old", "dt_loc"):
         np.testing.assert_array_equal(h[k].fetch(), rh[k].fetch(), k)
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, seed=3)
@@ -518,21 +519,51 @@ def test_concurrent_loops_match_sequential_and_respect_the_dag():
     sequential ones.  The DAG: iflux does not wait for grad_edge (disjoint
     writes, no shared written buffer); vflux waits for both (reads grad, INCs res)."""
     from paper_1403_7209_b200.executor import compile_program
-    results = []
-    for conc in (False, True):
-        for graph in (True, False):
+    for chain in (False, True):
+        results = []
+        for conc, graph in ((False, True), (True, True), (True, False), (False, False)):
             mesh = apps.gen_hex_mesh(16, seed=2)
             prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=2)
             for _ in range(2):
-                ml.run_program(prog, mesh, cfg(use_graph=graph, time_loops=False, concurrent_loops=conc))
+                ml.run_program(prog, mesh, cfg(use_graph=graph, time_loops=False, concurrent_loops=conc,
+                                               chain_loops=chain))
             results.append((h["q"].fetch(), [g.value for g in h["rms"]], [g.value for g in h["dt_min"]]))
-    for q, rms, dt in results[1:]:
-        np.testing.assert_array_equal(q, results[0][0])
-        assert rms == results[0][1] and dt == results[0][2]
-    cp = compile_program(prog, mesh, cfg(use_graph=True))
+        for q, rms, dt in results[1:]:
+            np.testing.assert_array_equal(q, results[0][0])
+            assert rms == results[0][1] and dt == results[0][2]
+    cp = compile_program(prog, mesh, cfg(use_graph=True, chain_loops=False))
     names = [e.loop.name for e in cp.entries]
     deps = cp.dependencies()
     g, i, v = names.index("grad_edge"), names.index("iflux"), names.index("vflux")
     assert g not in deps[i][0]
     assert g in deps[v][0] and i in deps[v][0]
     assert deps[i][1] != deps[g][1]                      # they run on different streams
+
+
+@pytest.mark.parametrize("sched", ["gather", "pfold", "colour", "tile"])
+def test_chained_flux_loops_match_oracle(sched):
+    """iflux+vflux chained into one loop (chain.py): raw res accumulators within
+    the reference tolerance of the serial oracle running the loops one by one,
+    the same as the unchained run within tolerance, bitwise run to run; the
+    full iteration's q, rms and dt_min too."""
+    from paper_1403_7209_b200.executor import compile_program
+    (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, seed=5)
+    bulk.run_program(rprog[:5], resolve_kernel)
+    c = cfg(inc_schedule=sched)
+    assert [l.name for l in compile_program(prog[:5], mesh, c).run_loops][-1] == "iflux+vflux"
+    ml.run_program(prog[:5], mesh, c)
+    for k in ("grad", "res", "q_old", "dt_loc"):
+        close(h[k].fetch(), rh[k].fetch(), what=k)
+    first = h["res"].fetch().copy()
+    h["res"].data[...] = 0.0
+    (m2, p2, h2), _ = _proxy_pair(16, seed=5)
+    ml.run_program(p2[:5], m2, cfg(inc_schedule=sched, chain_loops=False))
+    close(first, h2["res"].fetch(), what="res chained vs unchained")
+    ml.run_program(prog[3:5], mesh, c)
+    np.testing.assert_array_equal(h["res"].fetch(), first)
+    (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, seed=6)
+    bulk.run_program(rprog, resolve_kernel)
+    ml.run_program(prog, mesh, cfg(inc_schedule=sched, use_graph=True))
+    close(h["q"].fetch(), rh["q"].fetch(), what="q")
+    close([h["rms"][0].value], [rh["rms"][0].value], what="rms")
+    assert h["dt_min"][0].value == rh["dt_min"][0].value

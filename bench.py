@@ -7,11 +7,13 @@ Workload (default): ``build_hydra_proxy`` on the Rotor37-sized 3-D grid
 (94^3 = 830,584 nodes, 2,465,244 edges), numbered randomly (an unstructured
 mesh as read from disk) and then Cuthill–McKee renumbered; float64, one
 iteration = save -> dt_calc (MIN) -> grad_edge -> iflux -> vflux -> update
-(SUM) -> bc (7 op_par_loops).  Inputs (~570 MB of dats + maps) exceed the
+(SUM) -> bc (7 op_par_loops; iflux and vflux run chained as one fused loop
+``iflux+vflux``, chain.py).  Inputs (~570 MB of dats + maps) exceed the
 126 MB L2, so no flush is needed between steps.
 
 Metric (BASELINE.json): edges/s (whole job) and time per solver iteration,
-plus achieved HBM GB/s vs the measured peak for the dominant loop (vflux).
+plus achieved HBM GB/s vs the measured peak for the dominant loop (the one
+containing vflux).
 
 * ``value``      edges/s with all state resident in HBM: K back-to-back CUDA
                  graph replays of the iteration, CUDA events on the library
@@ -21,7 +23,7 @@ plus achieved HBM GB/s vs the measured peak for the dominant loop (vflux).
                  every input dat of the iteration from pinned host memory and
                  downloads every dat it writes plus the reductions; uploads,
                  loops and downloads overlap on three streams.
-* ``roofline``   vflux loop: B_alg / mean loop time from an eager pass with
+* ``roofline``   vflux (``iflux+vflux`` chained): B_alg / mean loop time from an eager pass with
                  CUDA events between loops (same stream).
 * ``cpu_baseline`` the reference CPU path restated (oracle/serial.py:
                  per-element Python kernel callbacks, reference run_serial
@@ -29,7 +31,8 @@ plus achieved HBM GB/s vs the measured peak for the dominant loop (vflux).
 
 ``--impl reference`` times that CPU path alone (rank 0; other ranks exit).
 Multi-GPU (torchrun, N>1): RCB owner-compute partition of the same mesh
-(strong scaling), one GPU per rank, halos over NCCL; value = total edges/s.
+(strong scaling), one GPU per rank, halos over NVLink peer memory (NCCL
+fallback); value = total edges/s.
 """
 from __future__ import annotations
 

@@ -179,7 +179,11 @@ typedef struct ml_loop {
                                        increment = its index in pf_elem2 */
     int32_t pf_own_kb;              /* shared memory (KB per CTA) for the targets'
                                        own READ rows in pass 1; 0: read from L1/L2 */
-    int32_t pf_pad;
+    int32_t pf_ncol;                /* record width (distinct map columns)       */
+    const int32_t *pf_rec;          /* optional [pass-1 incidences][pf_ncol]: the
+                                       map entries of each incidence's element;
+                                       NULL: read through the maps */
+    int8_t pf_rcol[ML_MAX_ARGS];    /* record column of each indirect argument   */
 } ml_loop_t;
 
 typedef struct ml_device_info {

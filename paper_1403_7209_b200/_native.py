@@ -99,7 +99,8 @@ class MlLoop(C.Structure):
                 ("pf_tl1", C.c_void_p), ("pf_n2", C.c_int64), ("pf_off2", C.c_void_p),
                 ("pf_elem2", C.c_void_p), ("pf_tl2", C.c_void_p), ("pf_pos2", C.c_void_p),
                 ("pf_slots", C.c_void_p), ("pf_slotpos", C.c_void_p),
-                ("pf_own_kb", C.c_int32), ("pf_pad", C.c_int32)]
+                ("pf_own_kb", C.c_int32), ("pf_ncol", C.c_int32), ("pf_rec", C.c_void_p),
+                ("pf_rcol", C.c_int8 * 16)]
 
 
 class MlDeviceInfo(C.Structure):

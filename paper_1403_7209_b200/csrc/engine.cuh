@@ -135,6 +135,13 @@ struct PFoldParams {
     int32_t own_ngrp;
     int32_t own_garg[MAX_TGROUPS], own_gdim[MAX_TGROUPS], own_goff[MAX_TGROUPS];
     int8_t own_grp[MAX_ARGS];
+    // element records: per pass-1 incidence k, the map entries of its element
+    // for each distinct (map, column) the loop uses — [n1 incidences][ncol];
+    // rcol: record column of each indirect argument.  The rows' addresses then
+    // depend on one load (the record) instead of two (element id, then map).
+    const int32_t *rec;
+    int32_t ncol;
+    int8_t rcol[MAX_ARGS];
 };
 
 struct LaunchParams {
@@ -259,6 +266,19 @@ struct Slot {
                 ptr = static_cast<T *>(r.data) + t * r.se;
                 sc = r.sc;
             }
+            if constexpr (staged) {
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
+            }
+        }
+    }
+    // pass-1 element record (PFoldParams::rec): indirect targets from the record
+    __device__ __forceinline__ void init_elem_rec(const LaunchParams &p, int i, int64_t e, const int32_t *rk) {
+        if constexpr (!is_global) {
+            const ArgRt &r = p.a[i];
+            const int64_t t = A::kind == KI ? int64_t(__ldg(rk + p.pf.rcol[i])) : e;
+            ptr = static_cast<T *>(r.data) + t * r.se;
+            sc = r.sc;
             if constexpr (staged) {
 #pragma unroll
                 for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
@@ -542,6 +562,11 @@ struct Engine {
     __device__ __forceinline__ static void init_elem(Slots &s, const LaunchParams &p, int64_t e,
                                                      char *smem, cuda::std::index_sequence<Is...>) {
         (cuda::std::get<Is>(s).init_elem(p, int(Is), e, smem), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void init_elem_rec(Slots &s, const LaunchParams &p, int64_t e,
+                                                         const int32_t *rk, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).init_elem_rec(p, int(Is), e, rk), ...);
     }
     template <size_t... Is>
     __device__ __forceinline__ static void init_tile(Slots &s, const LaunchParams &p, int64_t e,
@@ -1027,7 +1052,10 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
         for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
         for (int k = __ldg(pf.off1 + t), ke = __ldg(pf.off1 + t + 1); k < ke; ++k) {
             const int64_t e = __ldg(pf.elem1 + k);
-            E::init_elem(s, p, e, nullptr, idx);
+            if (pf.rec)
+                E::init_elem_rec(s, p, e, pf.rec + int64_t(k) * pf.ncol, idx);
+            else
+                E::init_elem(s, p, e, nullptr, idx);
             if (pf.own_ngrp > 0) E::own_views(s, p, own, idx);
             E::call(s, p, e, idx);
             E::template gather_op<MINC, 0, DG>(s, 0, run, idx);

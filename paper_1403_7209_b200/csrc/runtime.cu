@@ -322,6 +322,13 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         if (f.pfold_nslot > 0 && !pf.slotpos) ML_FAIL(ML_EINVAL, "loop '%s': pfold slot positions missing", L->name);
         pf.nslot = f.pfold_nslot;
         pf.dgp = f.pfold_dgp;
+        pf.rec = L->pf_rec;
+        pf.ncol = L->pf_ncol;
+        for (int i = 0; i < MAX_ARGS; ++i) pf.rcol[i] = L->pf_rcol[i];
+        if (pf.rec)
+            for (int i = 0; i < f.nargs; ++i)
+                if (L->args[i].kind == ML_INDIRECT && (pf.rcol[i] < 0 || pf.rcol[i] >= pf.ncol))
+                    ML_FAIL(ML_EINVAL, "loop '%s': pfold record column of argument %d out of range", L->name, i);
         // own-row staging: READ dats on the first INC argument's column
         pf.own_ngrp = 0;
         for (int i = 0; i < MAX_ARGS; ++i) pf.own_grp[i] = -1;

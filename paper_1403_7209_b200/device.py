@@ -300,20 +300,49 @@ class PFoldMirror:
     incidences through the first INC argument (pass 1) and through the others
     (pass 2), element ascending; plus the per-element slot buffer."""
 
-    __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos")
+    __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos",
+                 "rec", "ncol", "rcol")
 
-    def __init__(self, g: GatherMirror):
+    def __init__(self, g: GatherMirror, loop=None):
         h = pfold_lists_host(g.host)
         self.n1, self.n2 = h["n1"], h["n2"]
         for k in ("off1", "elem1", "tl1", "off2", "elem2", "tl2", "pos2", "slotpos"):
             setattr(self, k, _upload(h[k]))
+        self.rec, self.ncol, self.rcol = None, 0, [-1] * 16
+        if loop is not None:
+            rec, self.rcol = pfold_records_host(loop, h["elem1"])
+            self.ncol = rec.shape[1]
+            self.rec = _upload(rec)
 
 
-def pfold_mirror(loop, plan) -> PFoldMirror:
+def pfold_records_host(loop, elem1: np.ndarray):
+    """Pass-1 element records: for each incidence k, the map entries of element
+    elem1[k] for every distinct (map, column) the loop's indirect arguments
+    use, [incidences][columns] int32; and each argument's record column (-1:
+    not indirect)."""
+    cols, rcol = [], [-1] * 16
+    for i, a in enumerate(loop.args):
+        if a.kind != "indirect":
+            continue
+        key = (id(a.map), a.slot)
+        hit = [j for j, (m, c) in enumerate(cols) if (id(m), c) == key]
+        if hit:
+            rcol[i] = hit[0]
+        else:
+            rcol[i] = len(cols)
+            cols.append((a.map, a.slot))
+    e = elem1.astype(np.int64)
+    rec = np.empty((e.size, max(len(cols), 1)), np.int32)
+    for j, (m, c) in enumerate(cols):
+        rec[:, j] = m.table[e, c]
+    return rec, rcol
+
+
+def pfold_mirror(loop, plan, records: bool = True) -> PFoldMirror:
     cache = plan.__dict__.setdefault("_pfolds", {})
-    key = loop.signature()
+    key = (loop.signature(), records)
     if key not in cache:
-        cache[key] = PFoldMirror(gather_mirror(loop, plan))
+        cache[key] = PFoldMirror(gather_mirror(loop, plan), loop if records else None)
     return cache[key]
 
 

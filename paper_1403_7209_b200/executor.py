@@ -90,6 +90,7 @@ class BackendConfig:
     pfold_own_kb: int = 0                   # pfold pass 1: smem per CTA for the targets' own rows
                                             # (0: from L1/L2 — faster on B200, see profiles/)
     chain_loops: bool = True                # run registered adjacent loop pairs as one loop (chain.py)
+    pfold_records: bool = True              # pfold pass 1 reads per-incidence map records
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -286,12 +287,15 @@ class _LoopEntry:
         self.sched = sched
         if sched == "pfold":
             self.gather = gather_mirror(loop, self.plan)
-            pf = self.pfold = pfold_mirror(loop, self.plan)
+            pf = self.pfold = pfold_mirror(loop, self.plan, config.pfold_records)
             L.pf_n1, L.pf_off1, L.pf_elem1, L.pf_tl1 = pf.n1, pf.off1.ptr, pf.elem1.ptr, pf.tl1.ptr
             L.pf_n2, L.pf_off2, L.pf_elem2, L.pf_tl2 = pf.n2, pf.off2.ptr, pf.elem2.ptr, pf.tl2.ptr
             L.pf_pos2 = pf.pos2.ptr
             L.pf_slotpos = pf.slotpos.ptr
             L.pf_own_kb = int(config.pfold_own_kb)
+            L.pf_rec, L.pf_ncol = (pf.rec.ptr if pf.rec is not None else None), pf.ncol
+            for i, c in enumerate(pf.rcol):
+                L.pf_rcol[i] = c
             L.functor = self.functor
             nb = C.c_uint64()
             N.check(N.lib().ml_loop_pfold_slot_bytes(C.byref(L), C.byref(nb)))
@@ -595,11 +599,12 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
     N.init(config.device_index())
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
-           tuple(config.block_size_for(l.name) for l in program), config.smem_staging,
+           tuple(config.block_size_for(l.name) for l in program), config.block_size,
+           tuple(sorted((config.block_size_table or {}).items())), config.smem_staging,
            config.dataflow, config.inc_staging, config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.flow_windows,
            config.flow_window_l2_fraction, config.tile_smem_kb, config.tile_cmax, config.tile_threads, config.coord_dat,
-           config.pfold_own_kb, config.concurrent_loops, config.chain_loops,
+           config.pfold_own_kb, config.concurrent_loops, config.chain_loops, config.pfold_records,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

@@ -1118,6 +1118,9 @@ def setup_distributed(program, mesh, config, transport=None, executor_factory=No
         from dataclasses import replace
         config = replace(config, nranks=world)
     mesh.freeze()
+    if config.chain_loops:             # fused pairs exchange the union of their halos
+        from .chain import chain_program
+        program = chain_program(list(program), mesh)
     if layout is None:
         layout = build_layout(mesh, program, config)
     elif layout.nranks != world:
@@ -1161,7 +1164,7 @@ def run_program_distributed(program, mesh, config, transport=None, executor_fact
         rp.user_globals[gid].buffer[:] = val.buffer
     msgs = sum(transport.allgather_object(messages))
     collector = collector if collector is not None else PerfCollector()
-    for i, loop in enumerate(program):
+    for i, loop in enumerate(rp.program):
         collector.add(loop.name, float(comm[i] + comp[i]), useful_bytes(loop), comm=float(comm[i]),
                       comp=float(comp[i]))
     return RunResult(collector.finalize(), time.perf_counter() - t_start, messages=msgs,

@@ -25,6 +25,8 @@ ap.add_argument("--tile-smem", type=int, nargs="+", default=[100])
 ap.add_argument("--tile-cmax", type=int, default=512)
 ap.add_argument("--tile-threads", type=int, nargs="+", default=[256])
 ap.add_argument("--own-kb", type=int, nargs="+", default=[0])
+ap.add_argument("--records", type=int, nargs="+", default=[1], help="pfold pass-1 element records on/off")
+ap.add_argument("--chain", type=int, nargs="+", default=[1], help="loop chaining on/off")
 
 args = ap.parse_args()
 mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)
@@ -56,19 +58,26 @@ if args.kd:
         m = next(m for m in mesh.maps.values() if m.from_set.name == sname)
         apply_permutation(mesh, row_order_by_targets(mesh, m))
 import itertools
-for bs, kb, nt, okb in itertools.product(args.block_size, args.tile_smem, args.tile_threads, args.own_kb):
+import statistics
+for bs, kb, nt, okb, rec, ch in itertools.product(args.block_size, args.tile_smem, args.tile_threads,
+                                                  args.own_kb, args.records, args.chain):
     for sched in args.inc_schedule:
         if sched != "tile" and (kb != args.tile_smem[0] or nt != args.tile_threads[0]):
             continue
-        if sched != "pfold" and okb != args.own_kb[0]:
+        if sched != "pfold" and (okb != args.own_kb[0] or rec != args.records[0]):
             continue
         cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched, tile_smem_kb=kb,
-                               tile_cmax=args.tile_cmax, tile_threads=nt, pfold_own_kb=okb)
+                               tile_cmax=args.tile_cmax, tile_threads=nt, pfold_own_kb=okb,
+                               pfold_records=bool(rec), chain_loops=bool(ch))
+        per = {}
         for i in range(args.iters):
             r = ml.run_program(prog, mesh, cfg)
-            if i + 1 < args.iters:
-                continue
-            tot = sum(p.time_sec for p in r.perf)
-            print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} tile_kb={kb} nt={nt} own={okb}] total={tot*1e3:.3f}ms " +
-                  " ".join(f"{p.loop}={p.time_sec*1e3:.3f}ms/{p.gb_per_sec_alg:.0f}GBs" for p in r.perf),
-                  flush=True)
+            if i == 0 and args.iters > 1:
+                continue                                   # compile + upload
+            for p in r.perf:
+                per.setdefault(p.loop, []).append((p.time_sec, p.gb_per_sec_alg))
+        med = {k: (statistics.median(t for t, _ in v), statistics.median(g for _, g in v)) for k, v in per.items()}
+        tot = sum(t for t, _ in med.values())
+        print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} tile_kb={kb} nt={nt} own={okb} rec={rec} chain={ch}] "
+              f"total={tot*1e3:.3f}ms " +
+              " ".join(f"{k}={t*1e3:.3f}ms/{g:.0f}GBs" for k, (t, g) in med.items()), flush=True)

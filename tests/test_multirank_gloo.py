@@ -84,11 +84,18 @@ def _worker(rank, world, port, case, q):
             from paper_1403_7209_b200 import apps
             mesh = apps.gen_mesh(4)
             prog = _read_program(mesh, steps)
+        elif app == "proxy":
+            from paper_1403_7209_b200 import apps
+            mesh = apps.gen_hex_mesh(n, seed=7)
+            prog, h = apps.build_hydra_proxy(mesh, steps=steps, seed=7)
         else:
             mesh, prog, h = _cases.build_app(app, n, dtype, steps)
         cfg = ml.BackendConfig(nranks=world, partitioner=part)
         result = run_program_distributed(prog, mesh, cfg, executor_factory=OracleRank)
-        if app == "fuzz":
+        if app == "proxy":
+            out = {"q": h["q"].fetch(), "rms": np.array([r.value for r in h["rms"]]),
+                   "loops": [r.loop for r in result.perf]}
+        elif app == "fuzz":
             out = {"vals": mesh.dats["vals"].fetch()}
         elif app == "reads":
             out = {}
@@ -171,3 +178,20 @@ def test_consecutive_reads_move_no_extra_messages():
     m1 = _run(("reads", 0, "float64", 1, "trivial"))[0][2]
     m3 = _run(("reads", 0, "float64", 3, "trivial"))[0][2]
     assert m1 > 0 and m1 == m3
+
+
+def test_two_ranks_chained_proxy_matches_serial():
+    """The proxy's iflux+vflux chain runs as one loop per rank (its halo is the
+    union of both loops'); q and rms within the reference rtol of the serial
+    oracle running the unchained program on one process."""
+    import paper_1403_7209_b200 as ml  # noqa: F401
+    from oracle import serial
+    from paper_1403_7209_b200 import apps
+    mesh = apps.gen_hex_mesh(5, seed=7)
+    prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=7)
+    serial.run_program(prog)
+    for rank, out, msgs in _run(("proxy", 5, "float64", 2, "rcb")):
+        assert msgs > 0 and "iflux+vflux" in out["loops"] and "vflux" not in out["loops"]
+        ref = h["q"].fetch()
+        np.testing.assert_allclose(out["q"], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+        np.testing.assert_allclose(out["rms"], [r.value for r in h["rms"]], rtol=1e-12)

@@ -497,6 +497,11 @@ def test_pfold_schedule_raw_accumulators_reductions_and_determinism(own_kb):
     ml.run_program(prog[:5], mesh, c)
     for k in ("grad", "res"):
         np.testing.assert_array_equal(h[k].fetch(), first[k])
+    for k in ("grad", "res"):              # map reads instead of element records: same arithmetic
+        h[k].data[...] = 0.0
+    ml.run_program(prog[:5], mesh, cfg(inc_schedule="pfold", pfold_own_kb=own_kb, pfold_records=False))
+    for k in ("grad", "res"):
+        np.testing.assert_array_equal(h[k].fetch(), first[k])
     g = golden("exec.npz")
     for soa in (4, None):
         mesh, loop, acc, lo, hi = _cases.mixmax_case(auto_soa_threshold=soa)

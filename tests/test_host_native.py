@@ -509,3 +509,23 @@ def test_gather_hub_rows_and_pfold_lists(rng):
                     es = el[o[r]:o[r + 1]].tolist()
                     assert es == sorted(es)
                     assert es == [e for e, a in want[int(t1[r])] if sel(a)]
+
+
+def test_pfold_element_records_hold_each_arguments_map_entry():
+    """pfold pass-1 records: record column of every indirect argument holds
+    the map entry that argument reads for the incidence's element; arguments
+    on one (map, column) share a record column."""
+    from paper_1403_7209_b200.device import gather_lists_host, pfold_lists_host, pfold_records_host
+    mesh = apps.gen_hex_mesh(6, seed=1)
+    prog, _ = apps.build_hydra_proxy(mesh, steps=1, seed=1)
+    for loop in (prog[2], prog[3], prog[4]):
+        h = gather_lists_host(loop, loop.iter_set.size, hubs=False)
+        pf = pfold_lists_host(h["host"])
+        rec, rcol = pfold_records_host(loop, pf["elem1"])
+        assert rec.shape == (pf["elem1"].size, 2)                # edge_nodes columns 1 and 2
+        for i, a in enumerate(loop.args):
+            if a.kind != "indirect":
+                assert rcol[i] == -1
+                continue
+            np.testing.assert_array_equal(rec[:, rcol[i]], a.map.table[pf["elem1"], a.slot])
+        assert len({rcol[i] for i, a in enumerate(loop.args) if a.kind == "indirect"}) == 2

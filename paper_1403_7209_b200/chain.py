@@ -13,8 +13,11 @@ Legality (a chained pair must give the result of running the loops in
 order, up to the order of floating-point increments):
 
 * the loops are adjacent in the program and iterate over the same set;
-* neither has a global argument (a reduction read by the second loop would
-  see a partial value);
+* a global one loop reduces (INC/MIN/MAX) does not appear in the other (a
+  reduction read by the second loop would see a partial value); READ
+  globals may appear in both;
+* at most one of the two kernels takes constants (the fused functor hands
+  the same constant block to both halves);
 * every dat both loops touch is READ in both, or INC in both (increments
   commute); a dat one loop writes any other way does not appear in the other
   loop at all;
@@ -36,7 +39,7 @@ import ctypes as C
 
 from . import _native as N
 from .core import INC, READ, Loop, Mesh
-from .kernels import resolve_kernel
+from .kernels import KernelBinding, resolve_kernel
 
 __all__ = ["chain_lookup", "chain_program", "chain_pair"]
 
@@ -60,11 +63,13 @@ def _same(a, b) -> bool:
 
 
 def _hazard_free(A: Loop, B: Loop) -> bool:
-    if any(a.kind == "global" for a in A.args + B.args):
-        return False
+    for X, Y in ((A, B), (B, A)):
+        for a in X.args:              # a reduced global stays private to its loop
+            if a.kind == "global" and a.mode is not READ and any(b.glob is a.glob for b in Y.args):
+                return False
     for a in A.args:
         for b in B.args:
-            if a.dat is not b.dat:
+            if a.kind == "global" or b.kind == "global" or a.dat is not b.dat:
                 continue
             if not ((a.mode is READ and b.mode is READ) or (a.mode is INC and b.mode is INC)):
                 return False
@@ -79,8 +84,8 @@ def chain_pair(A: Loop, B: Loop) -> Loop | None:
         ba, bb = resolve_kernel(A.kernel), resolve_kernel(B.kernel)
     except Exception:
         return None
-    if ba.fconsts or ba.iconsts or bb.fconsts or bb.iconsts:
-        return None
+    if (ba.fconsts or ba.iconsts) and (bb.fconsts or bb.iconsts):
+        return None                   # the fused functor passes one constant block to both
     hit = chain_lookup(ba.functor, bb.functor)
     if hit is None:
         return None
@@ -104,8 +109,7 @@ def chain_pair(A: Loop, B: Loop) -> Loop | None:
         fa(*[views[k] for k in apos])
         fb(*[views[k] for k in bpos])
 
-    kernel.__ml_functor__ = fused
-    kernel.__ml_consts__ = None
+    kernel.__ml_binding__ = KernelBinding(fused, ba.fconsts or bb.fconsts, ba.iconsts or bb.iconsts)
     kernel.__qualname__ = f"chain[{ba.functor}+{bb.functor}]"
     return Loop(f"{A.name}+{B.name}", A.iter_set, slots, kernel)
 

@@ -34,6 +34,22 @@ struct ProxyDt {
     }
 };
 
+// Loop chain save -> dt_calc (both direct over the nodes, both read q): one
+// pass copies q to q_old and computes the local time step from the same
+// loaded q row.
+struct ProxySaveDt {
+    static constexpr int first_args[2] = {0, 1};           // save: q q_old
+    static constexpr int second_args[4] = {0, 2, 3, 4};    // dt_calc: q vol dt_loc dt_min
+    template <class T>
+    using sig = Sig<Arg<KD, MR, NQ, T>, Arg<KD, MW, NQ, T>, Arg<KD, MR, 1, T>, Arg<KD, MW, 1, T>,
+                    Arg<KG, MMIN, 1, T>>;
+    template <class Q, class QO, class V, class D, class M>
+    __device__ static void apply(const Consts &k, Q q, QO q_old, V vol, D dt_loc, M dt_min) {
+        ProxySave::apply(k, q, q_old);
+        ProxyDt::apply(k, q, vol, dt_loc, dt_min);
+    }
+};
+
 struct ProxyGrad {
     template <class T>
     using sig = Sig<Arg<KD, MR, 3, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, 3, T>,
@@ -179,6 +195,8 @@ struct ProxyBc {
 
 ML_REGISTER("proxy_save", ProxySave, double);
 ML_REGISTER("proxy_dt", ProxyDt, double);
+ML_REGISTER("proxy_save_dt", ProxySaveDt, double);
+ML_REGISTER_CHAIN("proxy_save", "proxy_dt", "proxy_save_dt", ProxySaveDt);
 ML_REGISTER("proxy_grad", ProxyGrad, double);
 ML_REGISTER("proxy_iflux", ProxyIflux, double);
 ML_REGISTER("proxy_vflux", ProxyVflux, double);

@@ -90,6 +90,9 @@ _BY_QUALNAME: dict[str, tuple[str, Callable]] = {
 
 def resolve_kernel(fn: Callable) -> KernelBinding:
     """Return the functor binding for ``fn`` or raise ExecError."""
+    bound = getattr(fn, "__ml_binding__", None)       # fused loops (chain.py)
+    if isinstance(bound, KernelBinding):
+        return bound
     hit = _EXPLICIT.get(id(fn))
     if hit is not None and hit[0] is fn:
         fc, ic = hit[2](fn)

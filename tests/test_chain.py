@@ -31,13 +31,32 @@ def test_registered_chain_and_argument_map():
 def test_proxy_program_chains_each_flux_pair():
     mesh, prog, h = _proxy()
     out = chain_program(prog, mesh)
-    assert [l.name for l in out] == ["save", "dt_calc", "grad_edge", "iflux+vflux", "update", "bc"] * 2
-    assert chain_program(prog, mesh)[3] is out[3]           # cached: compiled programs stay valid
-    fl = out[3]
+    assert [l.name for l in out] == ["save+dt_calc", "grad_edge", "iflux+vflux", "update", "bc"] * 2
+    assert chain_program(prog, mesh)[2] is out[2]           # cached: compiled programs stay valid
+    fl = out[2]
     iflux, vflux = prog[3], prog[4]
     assert list(fl.args[:7]) == list(iflux.args[:7])
     assert [fl.args[i] for i in (7, 8, 9, 10)] == [vflux.args[i] for i in (3, 4, 7, 8)]
     assert [a.mode for a in fl.args[11:]] == [INC, INC] and fl.args[11].dat is h["res"]
+
+
+def test_direct_chain_carries_constants_and_reductions():
+    """save -> dt_calc: two direct loops, the second with a constant (cfl) and
+    a MIN reduction, fuse; the MIN global must not appear in the first loop."""
+    from paper_1403_7209_b200.chain import _hazard_free
+    from paper_1403_7209_b200.kernels import resolve_kernel
+    mesh, prog, h = _proxy()
+    sd = chain_program(prog, mesh)[0]
+    assert sd.name == "save+dt_calc" and len(sd.args) == 5
+    b = resolve_kernel(sd.kernel)
+    assert b.functor == "proxy_save_dt" and b.fconsts == resolve_kernel(prog[1].kernel).fconsts
+    assert sd.args[4].glob is h["dt_min"][0]
+    save, dt = prog[0], prog[1]
+    assert _hazard_free(save, dt)
+    reads_min = Loop("save", save.iter_set, list(save.args) + [arg_global(h["dt_min"][0], READ)],
+                     save.kernel)
+    assert not _hazard_free(reads_min, dt)                # dt_calc's MIN read by the other loop
+    assert not _hazard_free(dt, reads_min)
 
 
 def test_chained_program_matches_unchained_in_the_oracle():
@@ -47,6 +66,7 @@ def test_chained_program_matches_unchained_in_the_oracle():
     serial.run_program(chain_program(pb, mb))
     for k in ("q", "q_old", "dt_loc"):
         np.testing.assert_allclose(hb[k].fetch(), ha[k].fetch(), rtol=1e-12, atol=1e-300)
+    assert [g.value for g in hb["dt_min"]] == [g.value for g in ha["dt_min"]]
     ma, pa, ha = _proxy(6, steps=1, seed=4)
     mb, pb, hb = _proxy(6, steps=1, seed=4)
     serial.run_program(pa[:5])

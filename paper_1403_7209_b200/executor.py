@@ -49,7 +49,30 @@ class ExchangeTimeout(ExecError):
     """A rank waited longer than the configured bound for a halo message."""
 
 
-SCHEDULES = ("gather", "pfold", "tile", "tgather", "fold", "colour", "flow", "arrival")
+SCHEDULES = ("auto", "gather", "pfold", "tile", "tgather", "fold", "colour", "flow", "arrival")
+
+# "auto": primary fold when an element gathers many more indirect components
+# than it increments (its neighbour rows are then read once per element instead
+# of once per incidence, and the secondary slots are cheap), gather otherwise.
+# Measured on B200 (profiles/README.md): vflux (92 read / 10 INC components per
+# element) and iflux+vflux (126 / 10) are faster as pfold; iflux (34 / 10),
+# grad_edge (16 / 36) and the diffusion edge flux (2 / 2) as gather.
+AUTO_PFOLD_RATIO = 6
+AUTO_PFOLD_MAX_DEGREE = 128        # pfold has no hub splitting: hub targets -> gather
+
+
+def auto_schedule(loop) -> str:
+    """The INC schedule "auto" resolves to for ``loop`` (see AUTO_PFOLD_RATIO)."""
+    if not fold_eligible(loop) or loop.iter_set.size == 0:
+        return "gather"
+    reads = sum(a.dat.dim for a in loop.args if a.kind == "indirect" and a.mode is READ)
+    incs = [a for a in loop.args if a.kind == "indirect" and a.mode is INC]
+    if reads < AUTO_PFOLD_RATIO * sum(a.dat.dim for a in incs):
+        return "gather"
+    deg = np.zeros(incs[0].dat.set.size, np.int64)
+    for a in incs:
+        deg += np.bincount(a.map.table[:, a.slot], minlength=deg.size)
+    return "pfold" if deg.max(initial=0) <= AUTO_PFOLD_MAX_DEGREE else "gather"
 
 
 @dataclass
@@ -79,7 +102,7 @@ class BackendConfig:
     smem_staging: bool = True               # INC increments staged in shared memory
     dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
     inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
-    inc_schedule: str = "gather"            # "gather" | "pfold" | "tile" | "fold" | "colour" | "flow" | "arrival"
+    inc_schedule: str = "auto"              # "auto" | "gather" | "pfold" | "tile" | "tgather" | "fold" | "colour" | "flow" | "arrival"
     inc_schedule_table: dict | None = None  # per-loop override (tuner.tune_schedule)
     flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
     flow_window_l2_fraction: float = 0.5
@@ -274,6 +297,8 @@ class _LoopEntry:
         self.pfold = None
         self.pf_slots = None
         sched = config.schedule_for(loop.name)
+        if sched == "auto":
+            sched = auto_schedule(loop)
         if sched == "pfold" and not (self.n > 0 and fold_eligible(loop)):
             sched = "gather"
         one_inc = len({a.dat.name for a in loop.args if a.kind == "indirect" and a.mode is INC}) == 1

@@ -106,3 +106,29 @@ def test_non_identical_shared_argument_does_not_chain():
     args = list(vflux.args)
     args[5] = arg_indirect(h["x"], iflux.args[3].map, 2, READ)     # slot swapped
     assert chain_pair(iflux, Loop("vflux", vflux.iter_set, args, vflux.kernel)) is None
+
+
+def test_auto_schedule_follows_measured_choices():
+    """"auto" (the default INC schedule) resolves as the B200 measurements
+    chose: pfold for the wide-gather flux loops, gather for iflux, grad_edge,
+    the diffusion edge flux and for any loop with hub targets."""
+    from paper_1403_7209_b200.executor import auto_schedule
+    mesh, prog, h = _proxy(6, steps=1)
+    out = chain_program(prog, mesh)
+    assert auto_schedule(prog[2]) == "gather"           # grad_edge: 16 read / 36 INC
+    assert auto_schedule(prog[3]) == "gather"           # iflux: 34 / 10
+    assert auto_schedule(prog[4]) == "pfold"            # vflux: 92 / 10
+    assert auto_schedule(out[2]) == "pfold"             # iflux+vflux: 126 / 10
+    assert auto_schedule(prog[6]) == "gather"           # bc: indirect WRITE
+    d = apps.gen_mesh(20)
+    dprog, _ = apps.build_diffusion(d, 1, dtype="float64")
+    assert auto_schedule(dprog[1]) == "gather"
+    hub = apps.gen_hub_mesh(2000, 20000, n_hubs=4, hub_share=0.2, seed=1)
+    from paper_1403_7209_b200.core import Loop as L
+    e = hub.sets["edges"]
+    en = hub.maps["edge_nodes"]
+    wide = hub.decl_dat("wide", hub.sets["nodes"], 8, "float64", np.zeros(hub.sets["nodes"].size * 8))
+    acc = hub.decl_dat("acc1", hub.sets["nodes"], 1, "float64", np.zeros(hub.sets["nodes"].size))
+    loop = L("wide", e, [arg_indirect(wide, en, 1, READ), arg_indirect(wide, en, 2, READ),
+                         arg_indirect(acc, en, 1, INC), arg_indirect(acc, en, 2, INC)], lambda *a: None)
+    assert auto_schedule(loop) == "gather"              # 16 / 2, but hub degrees > 128

@@ -184,6 +184,14 @@ typedef struct ml_loop {
                                        map entries of each incidence's element;
                                        NULL: read through the maps */
     int8_t pf_rcol[ML_MAX_ARGS];    /* record column of each indirect argument   */
+    /* hub rows (either pass): targets with > 128 incidences are split into
+     * rows accumulating from zero into partial slot pf_seg*[row] (-1:
+     * ordinary row) of pf_part* ([slots][dim]); each hub's slots
+     * pf_hub*_off[h]..[h+1] are then added onto target pf_hub*_tl[h] in order */
+    const int32_t *pf_seg1, *pf_seg2;
+    void *pf_part1, *pf_part2;
+    int64_t pf_nhub1, pf_nhub2;
+    const int32_t *pf_hub1_tl, *pf_hub1_off, *pf_hub2_tl, *pf_hub2_off;
 } ml_loop_t;
 
 typedef struct ml_device_info {

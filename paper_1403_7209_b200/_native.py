@@ -100,7 +100,11 @@ class MlLoop(C.Structure):
                 ("pf_elem2", C.c_void_p), ("pf_tl2", C.c_void_p), ("pf_pos2", C.c_void_p),
                 ("pf_slots", C.c_void_p), ("pf_slotpos", C.c_void_p),
                 ("pf_own_kb", C.c_int32), ("pf_ncol", C.c_int32), ("pf_rec", C.c_void_p),
-                ("pf_rcol", C.c_int8 * 16)]
+                ("pf_rcol", C.c_int8 * 16),
+                ("pf_seg1", C.c_void_p), ("pf_seg2", C.c_void_p), ("pf_part1", C.c_void_p),
+                ("pf_part2", C.c_void_p), ("pf_nhub1", C.c_int64), ("pf_nhub2", C.c_int64),
+                ("pf_hub1_tl", C.c_void_p), ("pf_hub1_off", C.c_void_p), ("pf_hub2_tl", C.c_void_p),
+                ("pf_hub2_off", C.c_void_p)]
 
 
 class MlDeviceInfo(C.Structure):

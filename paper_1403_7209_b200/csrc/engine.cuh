@@ -142,6 +142,12 @@ struct PFoldParams {
     const int32_t *rec;
     int32_t ncol;
     int8_t rcol[MAX_ARGS];
+    // hub rows: a target with more than HUB_ROW incidences in a pass is split
+    // into several rows; a split row accumulates from zero into partial slot
+    // seg[row] of part (-1: ordinary row) and k_fold_parts adds each hub's
+    // slots onto it in row (= element) order after the pass
+    const int32_t *seg1, *seg2;
+    void *part1, *part2;
 };
 
 struct LaunchParams {
@@ -1038,6 +1044,7 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
         const ArgRt &rg = p.a[G];
         const int64_t tg = pf.tl1 ? int64_t(__ldg(pf.tl1 + t)) : t;
         TG *dst = static_cast<TG *>(rg.data) + tg * rg.se;
+        const int32_t seg = pf.seg1 ? __ldg(pf.seg1 + t) : -1;
         // the target's own READ rows, once per target (consecutive targets: coalesced)
         for (int g = 0; g < pf.own_ngrp; ++g) {
             const ArgRt &r = p.a[pf.own_garg[g]];
@@ -1049,7 +1056,7 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
         }
         TG run[DG];
 #pragma unroll
-        for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+        for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : TG(0);
         for (int k = __ldg(pf.off1 + t), ke = __ldg(pf.off1 + t + 1); k < ke; ++k) {
             const int64_t e = __ldg(pf.elem1 + k);
             if (pf.rec)
@@ -1062,8 +1069,14 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
             if constexpr (NW > 1)
                 E::template stage_rest<DGP>(s, pf.slots, pf.slotpos + e * int64_t(NW - 1), idx);
         }
+        if (seg >= 0) {
+            TG *part = static_cast<TG *>(pf.part1) + int64_t(seg) * DG;
 #pragma unroll
-        for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+            for (int c = 0; c < DG; ++c) part[c] = run[c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+        }
     }
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
 }
@@ -1079,9 +1092,10 @@ __global__ void __launch_bounds__(256) k_pfold_rest(const __grid_constant__ Laun
          t += int64_t(gridDim.x) * blockDim.x) {
         const int64_t tg = pf.tl2 ? int64_t(__ldg(pf.tl2 + t)) : t;
         T *dst = static_cast<T *>(rg.data) + tg * rg.se;
+        const int32_t seg = pf.seg2 ? __ldg(pf.seg2 + t) : -1;
         T run[DG];
 #pragma unroll
-        for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+        for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : T(0);
         for (int k = __ldg(pf.off2 + t), ke = __ldg(pf.off2 + t + 1); k < ke; ++k) {
             const T *src = slots + int64_t(k) * DGP;        // rows in CSR order: contiguous per target
             if constexpr (DG % 2 == 0 && cuda::std::is_same_v<T, double>) {
@@ -1096,9 +1110,35 @@ __global__ void __launch_bounds__(256) k_pfold_rest(const __grid_constant__ Laun
                 for (int c = 0; c < DG; ++c) run[c] += __ldcs(src + c);
             }
         }
+        if (seg >= 0) {
+            T *part = static_cast<T *>(pf.part2) + int64_t(seg) * DG;
 #pragma unroll
-        for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+            for (int c = 0; c < DG; ++c) part[c] = run[c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+        }
     }
+}
+
+// Hub targets of a split pass (pfold): value + each partial slot in order.
+template <class T, int DG>
+__global__ void __launch_bounds__(256) k_fold_parts(const __grid_constant__ LaunchParams p, int ga, int64_t nhub,
+                                                    const int32_t *hub_tl, const int32_t *hub_off,
+                                                    const void *parts) {
+    const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (h >= nhub) return;
+    const ArgRt &rg = p.a[ga];
+    T *dst = static_cast<T *>(rg.data) + int64_t(__ldg(hub_tl + h)) * rg.se;
+    const T *part = static_cast<const T *>(parts);
+    T run[DG];
+#pragma unroll
+    for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
+    for (int q = __ldg(hub_off + h), qe = __ldg(hub_off + h + 1); q < qe; ++q)
+#pragma unroll
+        for (int c = 0; c < DG; ++c) run[c] += part[int64_t(q) * DG + c];
+#pragma unroll
+    for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
 }
 
 // Fold schedule, pass 1 — every element evaluated exactly once, like a direct
@@ -1585,6 +1625,8 @@ struct FunctorEntry {
     LaunchFn pfold1, pfold2;                         // primary-fold schedule (INC-only)
     LaunchFn gather_hubs;                            // hub fix-up of the gather schedule (INC)
     int (*pfold_occupancy)(size_t smem);
+    void (*pfold_hubs)(const LaunchParams &, int64_t nhub, const int32_t *tl, const int32_t *off,
+                       const void *parts, cudaStream_t);
     int32_t pfold_dgp, pfold_nslot;
 };
 
@@ -1680,6 +1722,13 @@ struct Registrar {
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pfold1<F, T>, 256, bytes) != cudaSuccess) n = 0;
         return n;
     }
+    static void pfold_hubs(const LaunchParams &p, int64_t nhub, const int32_t *tl, const int32_t *off,
+                           const void *parts, cudaStream_t s) {
+        using S = typename F::template sig<T>;
+        using AG = typename FirstInc<S>::type;
+        k_fold_parts<typename AG::type, AG::dim>
+            <<<unsigned((nhub + 255) / 256), 256, 0, s>>>(p, FirstInc<S>::value, nhub, tl, off, parts);
+    }
     static void pfold2(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
         using AG = typename FirstInc<S>::type;
@@ -1763,6 +1812,7 @@ struct Registrar {
             e.pfold1 = &pfold1;
             e.pfold2 = &pfold2;
             e.pfold_occupancy = &pfold_occupancy;
+            e.pfold_hubs = &pfold_hubs;
             using AG = typename FirstInc<S>::type;
             e.pfold_dgp = PFoldShape<typename AG::type, AG::dim>::DGP;
             e.pfold_nslot = SigInfo<S>::n_inc - 1;

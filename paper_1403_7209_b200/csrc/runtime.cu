@@ -322,6 +322,13 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         if (f.pfold_nslot > 0 && !pf.slotpos) ML_FAIL(ML_EINVAL, "loop '%s': pfold slot positions missing", L->name);
         pf.nslot = f.pfold_nslot;
         pf.dgp = f.pfold_dgp;
+        pf.seg1 = L->pf_seg1;
+        pf.seg2 = L->pf_seg2;
+        pf.part1 = L->pf_part1;
+        pf.part2 = L->pf_part2;
+        if ((L->pf_nhub1 > 0 && (!pf.seg1 || !pf.part1 || !L->pf_hub1_tl || !L->pf_hub1_off)) ||
+            (L->pf_nhub2 > 0 && (!pf.seg2 || !pf.part2 || !L->pf_hub2_tl || !L->pf_hub2_off)))
+            ML_FAIL(ML_EINVAL, "loop '%s': primary-fold hub lists missing", L->name);
         pf.rec = L->pf_rec;
         pf.ncol = L->pf_ncol;
         for (int i = 0; i < MAX_ARGS; ++i) pf.rcol[i] = L->pf_rcol[i];
@@ -364,9 +371,11 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
                                                         occ > 0 ? int64_t(occ) * g_dev.sm_count : INT64_MAX));
         if (nparts > pstride) ML_FAIL(ML_EINVAL, "loop '%s': primary fold needs more scratch", L->name);
         f.pfold1(p, dim3(unsigned(nparts)), dim3(256), own_bytes, stream);
+        if (L->pf_nhub1 > 0) f.pfold_hubs(p, L->pf_nhub1, L->pf_hub1_tl, L->pf_hub1_off, pf.part1, stream);
         if (pf.n2 > 0) {
             const int64_t g2 = std::min<int64_t>((pf.n2 + 255) / 256, int64_t(8) * g_dev.sm_count);
             f.pfold2(p, dim3(unsigned(g2)), dim3(256), 0, stream);
+            if (L->pf_nhub2 > 0) f.pfold_hubs(p, L->pf_nhub2, L->pf_hub2_tl, L->pf_hub2_off, pf.part2, stream);
         }
     }
     size_t tile_smem = 0;

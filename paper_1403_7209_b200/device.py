@@ -203,32 +203,48 @@ def gather_lists_host(loop, n: int, hubs: bool = False, hub_row: int = HUB_ROW) 
                     "targets": tl if tl is not None else np.arange(off.size - 1, dtype=np.int32)},
            "elem": elem, "pos": pos, "seg": None, "nhub": 0, "nslots": 0,
            "hub_tl": None, "hub_off": None}
-    deg = np.diff(off)
-    heavy = np.flatnonzero(deg > hub_row)
-    if hubs and heavy.size and wr[0].mode.name == "INC":
-        rows_tl = tl if tl is not None else np.arange(deg.size, dtype=np.int32)
-        nseg = np.where(deg > hub_row, -(-deg // hub_row), 1)
-        row_target = np.repeat(np.arange(deg.size), nseg)
-        first = np.concatenate([[0], np.cumsum(nseg)])[:-1]
-        within = np.arange(row_target.size) - np.repeat(first, nseg)
-        row_lo = off[row_target] + within * hub_row
-        row_hi = np.minimum(row_lo + hub_row, off[row_target + 1])
-        is_hub_row = deg[row_target] > hub_row
-        seg = np.full(row_target.size, -1, np.int32)
-        seg[is_hub_row] = np.arange(int(is_hub_row.sum()), dtype=np.int32)
-        off = np.concatenate([row_lo, row_hi[-1:]]).astype(np.int32)
-        tl = rows_tl[row_target].astype(np.int32)
-        out.update(seg=seg, nhub=int(heavy.size), nslots=int(is_hub_row.sum()),
-                   hub_tl=rows_tl[heavy].astype(np.int32),
-                   hub_off=np.concatenate([[0], np.cumsum(nseg[heavy])]).astype(np.int32))
+    if hubs and wr[0].mode.name == "INC":
+        sp = split_hub_rows(off, tl if tl is not None else np.arange(off.size - 1, dtype=np.int32),
+                            hub_row)
+        if sp is not None:
+            off, tl = sp["off"], sp["targets"]
+            out.update({k: sp[k] for k in ("seg", "nhub", "nslots", "hub_tl", "hub_off")})
     out["off"], out["targets"] = off, tl
     return out
 
 
-def pfold_lists_host(host: dict) -> dict:
+def split_hub_rows(off: np.ndarray, rows_tl: np.ndarray, hub_row: int = HUB_ROW):
+    """Split every row of a CSR with more than ``hub_row`` entries into rows of
+    at most ``hub_row`` (same entry order).  Returns None when no row is that
+    long, else the new ``off``/``targets`` and, per new row, its partial slot
+    ``seg`` (-1: ordinary row); ``hub_tl``/``hub_off``: each split target and
+    its partial slots, in row (= element) order."""
+    deg = np.diff(off)
+    heavy = np.flatnonzero(deg > hub_row)
+    if not heavy.size:
+        return None
+    nseg = np.where(deg > hub_row, -(-deg // hub_row), 1)
+    row_target = np.repeat(np.arange(deg.size), nseg)
+    first = np.concatenate([[0], np.cumsum(nseg)])[:-1]
+    within = np.arange(row_target.size) - np.repeat(first, nseg)
+    row_lo = off[row_target] + within * hub_row
+    row_hi = np.minimum(row_lo + hub_row, off[row_target + 1])
+    is_hub_row = deg[row_target] > hub_row
+    seg = np.full(row_target.size, -1, np.int32)
+    seg[is_hub_row] = np.arange(int(is_hub_row.sum()), dtype=np.int32)
+    return {"off": np.concatenate([row_lo, row_hi[-1:]]).astype(np.int32),
+            "targets": rows_tl[row_target].astype(np.int32), "seg": seg,
+            "nhub": int(heavy.size), "nslots": int(is_hub_row.sum()),
+            "hub_tl": rows_tl[heavy].astype(np.int32),
+            "hub_off": np.concatenate([[0], np.cumsum(nseg[heavy])]).astype(np.int32)}
+
+
+def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW) -> dict:
     """Primary-fold lists from one-row-per-target gather lists: per target, its
     incidences through the first INC argument (``1``) and through the others
-    (``2``, with positions), element ascending; only targets that have any."""
+    (``2``, with positions), element ascending; only targets that have any.
+    Rows longer than ``hub_row`` are split (``split_hub_rows``): ``seg{1,2}``,
+    ``nhub{1,2}``, ``nslots{1,2}``, ``hub{1,2}_tl``, ``hub{1,2}_off``."""
     off, elem, pos, tl = host["off"], host["elem"], host["pos"], host["targets"]
     nt = off.size - 1
     owner = np.repeat(np.arange(nt), np.diff(off))
@@ -252,6 +268,16 @@ def pfold_lists_host(host: dict) -> dict:
         slotpos[out["elem2"].astype(np.int64) * (nw - 1) + out["pos2"].astype(np.int64) - 1] = \
             np.arange(out["elem2"].size, dtype=np.int32)
     out["slotpos"] = slotpos
+    for which in (1, 2):
+        sp = split_hub_rows(out[f"off{which}"], out[f"tl{which}"], hub_row) if hub_row else None
+        if sp is None:
+            out.update({f"seg{which}": None, f"nhub{which}": 0, f"nslots{which}": 0,
+                        f"hub{which}_tl": None, f"hub{which}_off": None})
+            continue
+        out[f"off{which}"], out[f"tl{which}"] = sp["off"], sp["targets"]
+        out[f"n{which}"] = int(sp["off"].size - 1)
+        out.update({f"seg{which}": sp["seg"], f"nhub{which}": sp["nhub"], f"nslots{which}": sp["nslots"],
+                    f"hub{which}_tl": sp["hub_tl"], f"hub{which}_off": sp["hub_off"]})
     return out
 
 
@@ -301,15 +327,25 @@ class PFoldMirror:
     (pass 2), element ascending; plus the per-element slot buffer."""
 
     __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos",
-                 "rec", "ncol", "rcol")
+                 "rec", "ncol", "rcol", "seg1", "seg2", "nhub1", "nhub2", "hub1_tl", "hub1_off",
+                 "hub2_tl", "hub2_off", "part1", "part2")
 
-    def __init__(self, g: GatherMirror, loop=None):
+    def __init__(self, g: GatherMirror, loop, records: bool = True):
         h = pfold_lists_host(g.host)
         self.n1, self.n2 = h["n1"], h["n2"]
         for k in ("off1", "elem1", "tl1", "off2", "elem2", "tl2", "pos2", "slotpos"):
             setattr(self, k, _upload(h[k]))
+        inc = next(a for a in loop.args if a.kind == "indirect" and a.mode.name == "INC")
+        row = inc.dat.dim * np.dtype(inc.dat.dtype).itemsize
+        for w in (1, 2):
+            seg = h[f"seg{w}"]
+            setattr(self, f"nhub{w}", h[f"nhub{w}"])
+            for k in ("seg", "hub_tl", "hub_off"):
+                key = f"{k[:3]}{w}{k[3:]}" if k != "seg" else f"seg{w}"
+                setattr(self, key, _upload(h[key]) if seg is not None else None)
+            setattr(self, f"part{w}", N.DeviceBuffer(max(h[f"nslots{w}"] * row, 8)) if seg is not None else None)
         self.rec, self.ncol, self.rcol = None, 0, [-1] * 16
-        if loop is not None:
+        if records:
             rec, self.rcol = pfold_records_host(loop, h["elem1"])
             self.ncol = rec.shape[1]
             self.rec = _upload(rec)
@@ -342,7 +378,7 @@ def pfold_mirror(loop, plan, records: bool = True) -> PFoldMirror:
     cache = plan.__dict__.setdefault("_pfolds", {})
     key = (loop.signature(), records)
     if key not in cache:
-        cache[key] = PFoldMirror(gather_mirror(loop, plan), loop if records else None)
+        cache[key] = PFoldMirror(gather_mirror(loop, plan), loop, records)
     return cache[key]
 
 

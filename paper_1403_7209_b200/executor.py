@@ -58,7 +58,6 @@ SCHEDULES = ("auto", "gather", "pfold", "tile", "tgather", "fold", "colour", "fl
 # element) and iflux+vflux (126 / 10) are faster as pfold; iflux (34 / 10),
 # grad_edge (16 / 36) and the diffusion edge flux (2 / 2) as gather.
 AUTO_PFOLD_RATIO = 6
-AUTO_PFOLD_MAX_DEGREE = 128        # pfold has no hub splitting: hub targets -> gather
 
 
 def auto_schedule(loop) -> str:
@@ -69,10 +68,7 @@ def auto_schedule(loop) -> str:
     incs = [a for a in loop.args if a.kind == "indirect" and a.mode is INC]
     if reads < AUTO_PFOLD_RATIO * sum(a.dat.dim for a in incs):
         return "gather"
-    deg = np.zeros(incs[0].dat.set.size, np.int64)
-    for a in incs:
-        deg += np.bincount(a.map.table[:, a.slot], minlength=deg.size)
-    return "pfold" if deg.max(initial=0) <= AUTO_PFOLD_MAX_DEGREE else "gather"
+    return "pfold"
 
 
 @dataclass
@@ -319,6 +315,13 @@ class _LoopEntry:
             L.pf_slotpos = pf.slotpos.ptr
             L.pf_own_kb = int(config.pfold_own_kb)
             L.pf_rec, L.pf_ncol = (pf.rec.ptr if pf.rec is not None else None), pf.ncol
+            for w in (1, 2):
+                if getattr(pf, f"seg{w}") is not None:
+                    setattr(L, f"pf_seg{w}", getattr(pf, f"seg{w}").ptr)
+                    setattr(L, f"pf_part{w}", getattr(pf, f"part{w}").ptr)
+                    setattr(L, f"pf_nhub{w}", getattr(pf, f"nhub{w}"))
+                    setattr(L, f"pf_hub{w}_tl", getattr(pf, f"hub{w}_tl").ptr)
+                    setattr(L, f"pf_hub{w}_off", getattr(pf, f"hub{w}_off").ptr)
             for i, c in enumerate(pf.rcol):
                 L.pf_rcol[i] = c
             L.functor = self.functor

@@ -110,8 +110,8 @@ def test_non_identical_shared_argument_does_not_chain():
 
 def test_auto_schedule_follows_measured_choices():
     """"auto" (the default INC schedule) resolves as the B200 measurements
-    chose: pfold for the wide-gather flux loops, gather for iflux, grad_edge,
-    the diffusion edge flux and for any loop with hub targets."""
+    chose: pfold for the wide-gather flux loops (hub meshes included: pfold
+    splits hub rows), gather for iflux, grad_edge and the diffusion edge flux."""
     from paper_1403_7209_b200.executor import auto_schedule
     mesh, prog, h = _proxy(6, steps=1)
     out = chain_program(prog, mesh)
@@ -131,4 +131,4 @@ def test_auto_schedule_follows_measured_choices():
     acc = hub.decl_dat("acc1", hub.sets["nodes"], 1, "float64", np.zeros(hub.sets["nodes"].size))
     loop = L("wide", e, [arg_indirect(wide, en, 1, READ), arg_indirect(wide, en, 2, READ),
                          arg_indirect(acc, en, 1, INC), arg_indirect(acc, en, 2, INC)], lambda *a: None)
-    assert auto_schedule(loop) == "gather"              # 16 / 2, but hub degrees > 128
+    assert auto_schedule(loop) == "pfold"               # 16 / 2, hub rows split

@@ -499,7 +499,7 @@ def test_gather_hub_rows_and_pfold_lists(rng):
                 for k, t in enumerate(h["hub_tl"]):
                     rows = np.flatnonzero((tl == t) & (seg >= 0))
                     assert seg[rows].tolist() == list(range(h["hub_off"][k], h["hub_off"][k + 1]))
-            pf = pfold_lists_host(h["host"])
+            pf = pfold_lists_host(h["host"], hub_row=None)
             k = np.arange(pf["elem2"].size)
             np.testing.assert_array_equal(
                 pf["slotpos"][pf["elem2"].astype(np.int64) + pf["pos2"].astype(np.int64) - 1], k)
@@ -509,6 +509,20 @@ def test_gather_hub_rows_and_pfold_lists(rng):
                     es = el[o[r]:o[r + 1]].tolist()
                     assert es == sorted(es)
                     assert es == [e for e, a in want[int(t1[r])] if sel(a)]
+            # hub rows: split rows concatenate, in row order, to each target's list
+            ps = pfold_lists_host(h["host"], hub_row=hub_row)
+            for which in (1, 2):
+                o, el, t1, seg = ps[f"off{which}"], ps[f"elem{which}"], ps[f"tl{which}"], ps[f"seg{which}"]
+                assert ps[f"n{which}"] == o.size - 1 and np.all(np.diff(o) <= hub_row)
+                np.testing.assert_array_equal(el, pf[f"elem{which}"])
+                if seg is None:
+                    continue
+                assert sorted(seg[seg >= 0].tolist()) == list(range(ps[f"nslots{which}"]))
+                for q, t in enumerate(ps[f"hub{which}_tl"]):
+                    rows = np.flatnonzero((t1 == t) & (seg >= 0))
+                    assert seg[rows].tolist() == list(range(ps[f"hub{which}_off"][q],
+                                                            ps[f"hub{which}_off"][q + 1]))
+                    assert np.all(seg[t1 == t] >= 0)
 
 
 def test_pfold_element_records_hold_each_arguments_map_entry():

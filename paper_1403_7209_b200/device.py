@@ -328,10 +328,11 @@ class PFoldMirror:
 
     __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos",
                  "rec", "ncol", "rcol", "seg1", "seg2", "nhub1", "nhub2", "hub1_tl", "hub1_off",
-                 "hub2_tl", "hub2_off", "part1", "part2")
+                 "hub2_tl", "hub2_off", "part1", "part2", "host", "rec_host")
 
     def __init__(self, g: GatherMirror, loop, records: bool = True):
         h = pfold_lists_host(g.host)
+        self.host, self.rec_host = h, None
         self.n1, self.n2 = h["n1"], h["n2"]
         for k in ("off1", "elem1", "tl1", "off2", "elem2", "tl2", "pos2", "slotpos"):
             setattr(self, k, _upload(h[k]))
@@ -349,6 +350,25 @@ class PFoldMirror:
             rec, self.rcol = pfold_records_host(loop, h["elem1"])
             self.ncol = rec.shape[1]
             self.rec = _upload(rec)
+            self.rec_host = rec
+
+    def pass1_subset(self, rows: np.ndarray) -> dict:
+        """Device pass-1 lists of a subset of the pass-1 rows (ascending
+        positions): ``n1``, ``off1``, ``elem1``, ``tl1``, ``seg1``, ``rec``
+        (multi-GPU core/boundary launches)."""
+        h = self.host
+        off = h["off1"]
+        deg = (off[rows + 1] - off[rows]).astype(np.int64)
+        new_off = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+        take = (np.repeat(off[rows].astype(np.int64) - new_off[:-1], deg)
+                + np.arange(int(deg.sum()))).astype(np.int64)
+        out = {"n1": int(rows.size), "off1": _upload(new_off),
+               "elem1": _upload(np.ascontiguousarray(h["elem1"][take])),
+               "tl1": _upload(np.ascontiguousarray(h["tl1"][rows])),
+               "seg1": _upload(np.ascontiguousarray(h["seg1"][rows])) if h["seg1"] is not None else None,
+               "rec": (_upload(np.ascontiguousarray(self.rec_host[take]))
+                       if self.rec_host is not None else None)}
+        return out
 
 
 def pfold_records_host(loop, elem1: np.ndarray):

@@ -426,6 +426,7 @@ class DeviceRank:
 
 
 _LAST_HALO_PATH = ""
+_LAST_OVERLAPPED: list = []          # (loop, schedule) split into core/boundary launches in the last run
 
 
 class NvlinkHalo:
@@ -777,7 +778,7 @@ class StreamRank:
 
     def _build_split(self, i: int, names: tuple):
         e = self.entries[i]
-        if (e.gather is None or e.pfold is not None or e.gather.nhub or not names
+        if (e.gather is None or (e.pfold is None and e.gather.nhub) or not names
                 or e.loop.iter_set.size == 0):
             return None
         ex_names = set(names)
@@ -797,6 +798,8 @@ class StreamRank:
                 for ids in imports.values():
                     imported[ids] = True
                 bad_elem |= imported[a.map.table[:e.n, a.slot]]
+        if e.pfold is not None:
+            return self._build_pfold_split(e, bad_elem)
         g = e.gather
         off = g.host["off"]
         deg = np.diff(off)
@@ -814,6 +817,38 @@ class StreamRank:
             desc.gather_ntargets = sub["ntargets"]
             desc.gather_off, desc.gather_elem = sub["off"].ptr, sub["elem"].ptr
             desc.gather_pos, desc.gather_targets = sub["pos"].ptr, sub["targets"].ptr
+            out.append((desc, sub))
+        return out
+
+    def _build_pfold_split(self, e, bad_elem: np.ndarray):
+        """Primary fold: pass-1 rows none of whose elements read an imported row
+        run first (overlapped with the exchange), without pass 2 or the hub
+        folds; the other rows, the hub folds and pass 2 run after it."""
+        pf = e.pfold
+        h = pf.host
+        off = h["off1"]
+        if not off[-1]:
+            return None
+        bad = bad_elem[h["elem1"][:off[-1]]].astype(np.int64)
+        per_row = np.add.reduceat(bad, off[:-1]) if off.size > 1 else np.zeros(0, np.int64)
+        per_row = np.where(np.diff(off) > 0, per_row, 0)
+        rows = np.arange(off.size - 1)
+        core, bnd = rows[per_row == 0], rows[per_row > 0]
+        if core.size == 0 or bnd.size == 0:
+            return None
+        out = []
+        for k, part in enumerate((core, bnd)):
+            sub = pf.pass1_subset(part)
+            desc = type(e.desc).from_buffer_copy(e.desc)
+            desc.pf_n1, desc.pf_off1 = sub["n1"], sub["off1"].ptr
+            desc.pf_elem1, desc.pf_tl1 = sub["elem1"].ptr, sub["tl1"].ptr
+            if sub["seg1"] is not None:
+                desc.pf_seg1 = sub["seg1"].ptr
+            if sub["rec"] is not None:
+                desc.pf_rec = sub["rec"].ptr
+            if k == 0:                 # pass 2 and the hub folds wait for every pass-1 row
+                desc.pf_n2 = 0
+                desc.pf_nhub1 = desc.pf_nhub2 = 0
             out.append((desc, sub))
         return out
 
@@ -1017,6 +1052,9 @@ class StreamRank:
 
     def finish(self) -> None:
         """Wait for the run and copy the running values back to the host."""
+        global _LAST_OVERLAPPED
+        _LAST_OVERLAPPED = [(e.loop.name, e.sched) for e, sp in zip(self.entries, self.split)
+                            if sp is not None]
         self.N.check(self.N.lib().ml_synchronize(), "ml_synchronize")
         if self.nvlink is not None:
             self.nvlink.check([e.loop.name for e in self.entries])
@@ -1191,7 +1229,7 @@ def bench_distributed(args, metric):
     edges = mesh.sets["edges"].size
     local_dev = int(os.environ.get("ML_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     cfg = ml.BackendConfig(device=local_dev, nranks=world, partitioner="rcb", coord_dat="coords",
-                           inc_schedule=("gather" if getattr(args, "inc_schedule", "gather") == "tuned"
+                           inc_schedule=("auto" if getattr(args, "inc_schedule", "auto") == "tuned"
                                          else args.inc_schedule))
     t0 = time.perf_counter()
     rp, dev, transport, layout, cfg = setup_distributed(prog, mesh, cfg, transport)

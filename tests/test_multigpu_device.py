@@ -50,8 +50,9 @@ def _worker(rank, world, port, case, q, executor="stream"):
         cfg = ml.BackendConfig(nranks=world, partitioner=part, device=0, inc_schedule=sched)
         result = ml.run_program(prog, mesh, cfg)
         if app == "proxy":
+            import paper_1403_7209_b200.multigpu as mg
             out = {"q": h["q"].fetch(), "rms": np.array([g.value for g in h["rms"]]),
-                   "dt": np.array([g.value for g in h["dt_min"]])}
+                   "dt": np.array([g.value for g in h["dt_min"]]), "overlapped": list(mg._LAST_OVERLAPPED)}
         else:
             out = _cases.app_results(app, h)
         need_nvlink = executor == "stream" and halo == "p2p" and world > 1
@@ -104,7 +105,7 @@ def test_ranks_on_device_match_reference_int64(world, part, sched, executor):
 
 
 @pytest.mark.parametrize("sched,executor", [("gather", "stream"), ("gather", "stream+copy"),
-                                            ("flow", "host")])
+                                            ("flow", "host"), ("pfold", "stream"), ("auto", "stream+copy")])
 def test_proxy_two_ranks_on_device_vs_oracle(sched, executor):
     import paper_1403_7209_b200 as ml
     from oracle import bulk
@@ -117,6 +118,9 @@ def test_proxy_two_ranks_on_device_vs_oracle(sched, executor):
     outs = _run(("proxy", 12, "float64", 2, "rcb", sched), 2, executor)
     ref_q = h["q"].fetch()
     for rank, out, _ in outs:
+        if executor.startswith("stream") and sched in ("pfold", "auto"):
+            # the fused flux loop runs as pfold, its pass-1 rows split around the exchange
+            assert ("iflux+vflux", "pfold") in out["overlapped"], out["overlapped"]
         np.testing.assert_allclose(out["q"], ref_q, rtol=1e-12, atol=1e-12 * np.abs(ref_q).max())
         np.testing.assert_allclose(out["rms"], [r.value for r in h["rms"]], rtol=1e-12)
         np.testing.assert_array_equal(out["dt"], [r.value for r in h["dt_min"]])

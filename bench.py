@@ -22,7 +22,9 @@ containing vflux).
                  every step ``run_program(..., residency="host")`` uploads
                  every input dat of the iteration from pinned host memory and
                  downloads every dat it writes plus the reductions; uploads,
-                 loops and downloads overlap on three streams.
+                 loops and downloads overlap on three streams.  ``e2e.pcie``:
+                 measured pinned H2D / D2H bandwidth and the step times they
+                 bound (all inputs through H2D; + the serial D2H).
 * ``roofline``   vflux (``iflux+vflux`` chained): B_alg / mean loop time from an eager pass with
                  CUDA events between loops (same stream).
 * ``cpu_baseline`` the reference CPU path restated (oracle/serial.py:
@@ -104,6 +106,31 @@ def _replay_seconds(cp) -> float:
     t0 = time.perf_counter()
     cp.replay(1)
     return time.perf_counter() - t0
+
+
+def pcie_bounds(h2d: int, d2h: int) -> dict:
+    """Pinned host<->device copy bandwidth on this box (256 MB each way, CUDA
+    events, best of 3) and the e2e step time it bounds: inputs cannot all be
+    on the device before the H2D stream has moved them, so an e2e step takes
+    at least h2d / H2D bandwidth (the D2H of early-written dats overlaps it)."""
+    import torch
+    n = 256 << 20
+    host = torch.empty(n, dtype=torch.uint8).pin_memory()
+    dev = torch.empty(n, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, dst, src in (("h2d_gbs", dev, host), ("d2h_gbs", host, dev)):
+        best = 0.0
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = max(best, n / (a.elapsed_time(b) * 1e-3) / 1e9)
+        out[name] = round(best, 1)
+    out["h2d_bound_ms"] = round(h2d / (out["h2d_gbs"] * 1e9) * 1e3, 3)
+    out["serial_bound_ms"] = round((h2d / out["h2d_gbs"] + d2h / out["d2h_gbs"]) / 1e6, 3)
+    return out
 
 
 def run_ours(args) -> None:
@@ -196,6 +223,7 @@ def run_ours(args) -> None:
     e2e_s = time.perf_counter() - t0
     e2e = {"value": edges * args.steps / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s / args.steps}
+    e2e["pcie"] = pcie_bounds(h2d, d2h)
 
     cb = cpu_baseline(args) if not args.no_cpu else None
     line = {

@@ -36,12 +36,15 @@ has no loop chaining (its executors run ``program`` loop by loop,
 from __future__ import annotations
 
 import ctypes as C
+from collections import OrderedDict
 
 from . import _native as N
 from .core import INC, READ, Loop, Mesh
 from .kernels import KernelBinding, resolve_kernel
 
 __all__ = ["chain_lookup", "chain_program", "chain_pair"]
+
+_CHAIN_CACHE_SIZE = 256          # adjacent pairs remembered per mesh
 
 
 def chain_lookup(first: str, second: str):
@@ -118,7 +121,7 @@ def chain_program(program: list[Loop], mesh: Mesh) -> list[Loop]:
     """``program`` with every legal adjacent chained pair replaced by its
     fused loop (left to right; fused loops are cached on the mesh so a
     program's compiled form stays valid across calls)."""
-    cache = mesh.__dict__.setdefault("_ml_chains", {})
+    cache = mesh.__dict__.setdefault("_ml_chains", OrderedDict())
     out: list[Loop] = []
     i = 0
     while i < len(program):
@@ -129,6 +132,10 @@ def chain_program(program: list[Loop], mesh: Mesh) -> list[Loop]:
             if hit is None or hit[0] is not A or hit[1] is not B:
                 hit = (A, B, chain_pair(A, B))
                 cache[key] = hit
+                while len(cache) > _CHAIN_CACHE_SIZE:
+                    cache.popitem(last=False)
+            else:
+                cache.move_to_end(key)
             if hit[2] is not None:
                 out.append(hit[2])
                 i += 2

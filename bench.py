@@ -50,7 +50,8 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_1403_7209_b200.bench_support import build_workload, clock_sampler, peaks_gbs  # noqa: E402
+from paper_1403_7209_b200.bench_support import (build_workload, clock_sampler, peaks_gbs,  # noqa: E402
+                                                  workload_name)
 
 METRIC = "edges/sec and time per solver iteration; achieved HBM GB/s vs peak, 1/2/4/8 B200"
 
@@ -94,8 +95,10 @@ def run_reference(args) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "edges/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cb["sample"].split(";")[0], "parallelism": "cpu-serial"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args),
+                       "parallelism": "cpu-serial (1 core: the reference's backends are GIL-bound)",
+                       "sample_per_step": cb["sample"].split(";")[0]},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "edges/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}

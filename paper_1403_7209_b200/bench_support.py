@@ -94,6 +94,13 @@ def clock_sampler(index: int) -> ClockSampler:
     return ClockSampler(index)
 
 
+def workload_name(args) -> str:
+    """``config.workload`` of a bench line (both arms)."""
+    if args.workload == "proxy":
+        return f"hydra-proxy iteration, 3-D grid {args.grid}^3"
+    return f"diffusion step, gen_mesh({args.grid})"
+
+
 def build_workload(args):
     """(mesh, program, handles, name, setup timings) for ``args.workload`` / ``args.grid``."""
     from . import apps
@@ -103,12 +110,12 @@ def build_workload(args):
         mesh = apps.gen_hex_mesh(args.grid, seed=0)
         apps.shuffle_mesh(mesh, seed=1)
         prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
-        name = f"hydra-proxy iteration, 3-D grid {args.grid}^3"
+        name = workload_name(args)
     else:
         mesh = apps.gen_mesh(args.grid)
         apps.shuffle_mesh(mesh, seed=1)
         prog, h = apps.build_diffusion(mesh, steps=1, dtype="float64")
-        name = f"diffusion step, gen_mesh({args.grid})"
+        name = workload_name(args)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     renumber_mesh(mesh)

@@ -572,3 +572,29 @@ def test_chained_flux_loops_match_oracle(sched):
     close(h["q"].fetch(), rh["q"].fetch(), what="q")
     close([h["rms"][0].value], [rh["rms"][0].value], what="rms")
     assert h["dt_min"][0].value == rh["dt_min"][0].value
+
+
+@pytest.mark.parametrize("sched", ["auto", "pfold"])
+def test_config_d_8m_edges_int64_bit_exact(sched):
+    """Config D (gen_mesh(1633): 2,669,956 nodes / 8,003,333 edges), int64
+    diffusion twin, two steps: bit-exact vs the oracle at the largest
+    single-GPU size BASELINE.json names."""
+    ref = apps.gen_mesh(1633)
+    rprog, rh = apps.build_diffusion(ref, 2, dtype="int64")
+    bulk.run_program(rprog, resolve_kernel)
+    mesh = apps.gen_mesh(1633)
+    prog, h = apps.build_diffusion(mesh, 2, dtype="int64")
+    ml.run_program(prog, mesh, cfg(inc_schedule=sched))
+    np.testing.assert_array_equal(h["u"].fetch(), rh["u"].fetch())
+    assert [r.value for r in h["residuals"]] == [r.value for r in rh["residuals"]]
+
+
+def test_config_d_proxy_iteration_vs_oracle():
+    """139^3 grid (7,998,894 edges): one chained Hydra-proxy iteration with the
+    default schedules vs the oracle running the loops one by one."""
+    (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(139, seed=2)
+    bulk.run_program(rprog, resolve_kernel)
+    ml.run_program(prog, mesh, cfg())
+    close(h["q"].fetch(), rh["q"].fetch(), what="q")
+    close([h["rms"][0].value], [rh["rms"][0].value], what="rms")
+    assert h["dt_min"][0].value == rh["dt_min"][0].value

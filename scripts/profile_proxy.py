@@ -27,6 +27,7 @@ ap.add_argument("--tile-threads", type=int, nargs="+", default=[256])
 ap.add_argument("--own-kb", type=int, nargs="+", default=[0])
 ap.add_argument("--records", type=int, nargs="+", default=[1], help="pfold pass-1 element records on/off")
 ap.add_argument("--chain", type=int, nargs="+", default=[1], help="loop chaining on/off")
+ap.add_argument("--aos-dats", nargs="*", default=[], help="dats switched to AoS after generation")
 
 args = ap.parse_args()
 mesh = apps.gen_hex_mesh(args.grid, seed=0, auto_soa_threshold=None if args.soa < 0 else args.soa)
@@ -34,6 +35,9 @@ apps.shuffle_mesh(mesh, seed=1)
 prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
 if not args.no_renumber:
     ml.renumber_mesh(mesh)
+for name in args.aos_dats:
+    from paper_1403_7209_b200.core import AOS, transform_layout
+    transform_layout(mesh.dats[name], AOS)
 if args.kd:
     import numpy as np
     from paper_1403_7209_b200.renumber import Permutation, apply_permutation, row_order_by_targets, _forward

@@ -106,6 +106,11 @@ def chain_pair(A: Loop, B: Loop) -> Loop | None:
             return None
     if any(s is None for s in slots):
         return None
+    from .executor import _loop_dtype
+    fid = C.c_int32()
+    for L in (A, B):                  # the fused functor must exist for the loops' type
+        if N.lib().ml_functor_lookup(fused.encode(), _loop_dtype(L), C.byref(fid)) != 0:
+            return None
     fa, fb = A.kernel, B.kernel
 
     def kernel(*views):

@@ -132,3 +132,29 @@ def test_auto_schedule_follows_measured_choices():
     loop = L("wide", e, [arg_indirect(wide, en, 1, READ), arg_indirect(wide, en, 2, READ),
                          arg_indirect(acc, en, 1, INC), arg_indirect(acc, en, 2, INC)], lambda *a: None)
     assert auto_schedule(loop) == "pfold"               # 16 / 2, hub rows split
+
+
+def test_chain_needs_the_fused_functor_for_the_loops_type():
+    """The proxy chain is registered for float64 only: int64 copies of the
+    same loops stay unchained (no missing-functor failure at compile time)."""
+    from paper_1403_7209_b200 import _native as N
+    import ctypes as C
+    fid = C.c_int32()
+    assert N.lib().ml_functor_lookup(b"proxy_fluxes", N.ML_I64, C.byref(fid)) != 0
+    mesh, prog, h = _proxy(4, steps=1)
+    iflux, vflux = prog[3], prog[4]
+    ints = {}
+
+    def as_int(a):
+        if a.kind == "global":
+            return a
+        d = a.dat
+        if d.name not in ints:
+            ints[d.name] = mesh.decl_dat(d.name + "_i", d.set, d.dim, "int64",
+                                         np.zeros(d.set.size * d.dim, np.int64))
+        return (arg_indirect(ints[d.name], a.map, a.slot + 1, a.mode) if a.kind == "indirect"
+                else type(a)("direct", a.mode, dat=ints[d.name]))
+    A = Loop("iflux", iflux.iter_set, [as_int(a) for a in iflux.args], iflux.kernel)
+    B = Loop("vflux", vflux.iter_set, [as_int(a) for a in vflux.args], vflux.kernel)
+    assert chain_pair(iflux, vflux) is not None
+    assert chain_pair(A, B) is None

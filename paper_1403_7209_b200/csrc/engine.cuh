@@ -43,6 +43,33 @@ enum : int { KD = 0, KI = 1, KG = 2 };                        // direct / indire
 enum : int { MR = 0, MW = 1, MRW = 2, MINC = 3, MMIN = 4, MMAX = 5 };
 constexpr int MAX_ARGS = 16;
 
+// Programmatic dependent launch: the hot kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs can
+// be resident while its predecessor on the stream drains; each such kernel
+// waits (griddepcontrol.wait) for the predecessor's completion — and memory —
+// before touching any data.  Without the attribute the wait is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+
+template <class... KArgs, class... Args>
+inline void launch_k(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args &&...args) {
+    if (!pdl_enabled()) {
+        k<<<g, b, smem, s>>>(static_cast<KArgs>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 template <int K, int M, int DIM, class T>
 struct Arg {
     static constexpr int kind = K, mode = M, dim = DIM;
@@ -991,6 +1018,7 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
 // rows, in row (= element) order.
 template <class T, int DG>
 __global__ void __launch_bounds__(256) k_gather_hubs(const __grid_constant__ LaunchParams p, int ga) {
+    pdl_wait();
     const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (h >= p.g_nhub) return;
     const ArgRt &rg = p.a[ga];
@@ -1084,6 +1112,7 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
 // Primary-fold schedule, pass 2: each target adds its slots in element order.
 template <class T, int DG>
 __global__ void __launch_bounds__(256) k_pfold_rest(const __grid_constant__ LaunchParams p, int ga) {
+    pdl_wait();
     constexpr int DGP = PFoldShape<T, DG>::DGP;
     const PFoldParams &pf = p.pf;
     const ArgRt &rg = p.a[ga];
@@ -1126,6 +1155,7 @@ template <class T, int DG>
 __global__ void __launch_bounds__(256) k_fold_parts(const __grid_constant__ LaunchParams p, int ga, int64_t nhub,
                                                     const int32_t *hub_tl, const int32_t *hub_off,
                                                     const void *parts) {
+    pdl_wait();
     const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (h >= nhub) return;
     const ArgRt &rg = p.a[ga];
@@ -1519,6 +1549,7 @@ __device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
 
 template <class F, class T>
 __global__ void __launch_bounds__(256) k_direct(const __grid_constant__ LaunchParams p) {
+    pdl_wait();
     run_direct<F>(p, typename F::template sig<T>{});
 }
 template <class F, class T>
@@ -1555,10 +1586,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_tgather(const __grid_constant_
 }
 template <class F, class T>
 __global__ void __launch_bounds__(256) k_pfold1(const __grid_constant__ LaunchParams p) {
+    pdl_wait();
     run_pfold1<F>(p, typename F::template sig<T>{});
 }
 template <class F, class T>
 __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ LaunchParams p) {
+    pdl_wait();
     run_gather<F>(p, typename F::template sig<T>{});
 }
 template <class F, class T, int MINB>
@@ -1635,7 +1668,7 @@ void register_functor(const FunctorEntry &e);
 template <class F, class T>
 struct Registrar {
     static void direct(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
-        k_direct<F, T><<<g, b, 0, s>>>(p);
+        launch_k(k_direct<F, T>, g, b, 0, s, p);
     }
     static int direct_occupancy(int threads) {
         int n = 0;
@@ -1672,7 +1705,7 @@ struct Registrar {
             cudaFuncSetAttribute(k_gather<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
             once = true;
         }
-        k_gather<F, T><<<g, b, 0, s>>>(p);
+        launch_k(k_gather<F, T>, g, b, 0, s, p);
     }
     // resident CTAs of 256 threads per SM (sizes the persistent gather grid)
     static int gather_occupancy() {
@@ -1697,7 +1730,7 @@ struct Registrar {
     static void gather_hubs(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
         using AG = typename FirstInc<S>::type;
-        k_gather_hubs<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, FirstInc<S>::value);
+        launch_k(k_gather_hubs<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
     }
     static void pfold_attrs(size_t bytes) {
         static int carve = -1;
@@ -1714,7 +1747,7 @@ struct Registrar {
     }
     static void pfold1(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
         pfold_attrs(bytes);
-        k_pfold1<F, T><<<g, b, bytes, s>>>(p);
+        launch_k(k_pfold1<F, T>, g, b, bytes, s, p);
     }
     static int pfold_occupancy(size_t bytes) {
         pfold_attrs(bytes);
@@ -1726,13 +1759,13 @@ struct Registrar {
                            const void *parts, cudaStream_t s) {
         using S = typename F::template sig<T>;
         using AG = typename FirstInc<S>::type;
-        k_fold_parts<typename AG::type, AG::dim>
-            <<<unsigned((nhub + 255) / 256), 256, 0, s>>>(p, FirstInc<S>::value, nhub, tl, off, parts);
+        launch_k(k_fold_parts<typename AG::type, AG::dim>, dim3(unsigned((nhub + 255) / 256)), dim3(256), 0, s, p,
+                 int(FirstInc<S>::value), nhub, tl, off, parts);
     }
     static void pfold2(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
         using AG = typename FirstInc<S>::type;
-        k_pfold_rest<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, FirstInc<S>::value);
+        launch_k(k_pfold_rest<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
     }
     static void fold_targets(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;

@@ -60,8 +60,17 @@ static int ensure_init() {
 }
 
 // ---- reduction combine ------------------------------------------------------------
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("ML_PDL");          // ML_PDL=0 turns it off
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
 template <class T, int M>
 __global__ void __launch_bounds__(256) k_combine(T *g, const T *part, int64_t nparts, int dim) {
+    pdl_wait();
     __shared__ double smem[32];
     for (int c = 0; c < dim; ++c) {
         T v = reduce_identity<T, M>();
@@ -74,9 +83,9 @@ __global__ void __launch_bounds__(256) k_combine(T *g, const T *part, int64_t np
 
 template <class T>
 static void launch_combine(int mode, T *g, const T *part, int64_t nparts, int dim, cudaStream_t s) {
-    if (mode == MINC) k_combine<T, MINC><<<1, 256, 0, s>>>(g, part, nparts, dim);
-    else if (mode == MMIN) k_combine<T, MMIN><<<1, 256, 0, s>>>(g, part, nparts, dim);
-    else k_combine<T, MMAX><<<1, 256, 0, s>>>(g, part, nparts, dim);
+    if (mode == MINC) launch_k(k_combine<T, MINC>, dim3(1), dim3(256), 0, s, g, part, nparts, dim);
+    else if (mode == MMIN) launch_k(k_combine<T, MMIN>, dim3(1), dim3(256), 0, s, g, part, nparts, dim);
+    else launch_k(k_combine<T, MMAX>, dim3(1), dim3(256), 0, s, g, part, nparts, dim);
 }
 
 static int round_up32(int64_t x) { return int((x + 31) / 32 * 32); }

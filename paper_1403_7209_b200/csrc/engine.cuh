@@ -50,6 +50,7 @@ constexpr int MAX_ARGS = 16;
 // before touching any data.  Without the attribute the wait is a no-op.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool pdl_enabled();
+bool pass2_warp();
 
 template <class... KArgs, class... Args>
 inline void launch_k(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args &&...args) {
@@ -1150,6 +1151,66 @@ __global__ void __launch_bounds__(256) k_pfold_rest(const __grid_constant__ Laun
     }
 }
 
+// Pass 2, warp-cooperative: a warp owns 32 consecutive pass-2 rows, whose
+// slots are one contiguous range; the lanes copy it through shared memory in
+// coalesced 16-byte chunks, then each lane adds its own rows in order — the
+// same per-target arithmetic as k_pfold_rest, with full-sector DRAM reads.
+template <class T, int DG>
+__global__ void __launch_bounds__(256) k_pfold_rest_w(const __grid_constant__ LaunchParams p, int ga) {
+    pdl_wait();
+    constexpr int DGP = PFoldShape<T, DG>::DGP;
+    constexpr int CH = 5632 / int(DGP * sizeof(T));          // slot rows per chunk and warp (5.5 KB)
+    __shared__ __align__(16) T buf[8][CH * DGP];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const PFoldParams &pf = p.pf;
+    const ArgRt &rg = p.a[ga];
+    const uint4 *slots = static_cast<const uint4 *>(pf.slots);
+    for (int64_t t0 = (int64_t(blockIdx.x) * 8 + w) * 32; t0 < pf.n2; t0 += int64_t(gridDim.x) * 256) {
+        const int64_t t = t0 + lane;
+        const bool act = t < pf.n2;
+        const int64_t te = t0 + 32 < pf.n2 ? t0 + 32 : pf.n2;
+        const int wk0 = __ldg(pf.off2 + t0), wk1 = __ldg(pf.off2 + te);
+        int k0 = 0, k1 = 0;
+        T *dst = nullptr;
+        int32_t seg = -1;
+        T run[DG];
+        if (act) {
+            k0 = __ldg(pf.off2 + t);
+            k1 = __ldg(pf.off2 + t + 1);
+            const int64_t tg = pf.tl2 ? int64_t(__ldg(pf.tl2 + t)) : t;
+            dst = static_cast<T *>(rg.data) + tg * rg.se;
+            seg = pf.seg2 ? __ldg(pf.seg2 + t) : -1;
+#pragma unroll
+            for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : T(0);
+        }
+        for (int c0 = wk0; c0 < wk1; c0 += CH) {
+            const int n = wk1 - c0 < CH ? wk1 - c0 : CH;
+            const uint4 *src = slots + int64_t(c0) * (DGP * sizeof(T) / 16);
+            uint4 *dstb = reinterpret_cast<uint4 *>(buf[w]);
+            for (int i = lane; i < n * int(DGP * sizeof(T) / 16); i += 32) dstb[i] = __ldcs(src + i);
+            __syncwarp();
+            if (act) {
+                const int a = k0 > c0 ? k0 : c0, b = k1 < c0 + n ? k1 : c0 + n;
+                for (int k = a; k < b; ++k) {
+#pragma unroll
+                    for (int c = 0; c < DG; ++c) run[c] += buf[w][(k - c0) * DGP + c];
+                }
+            }
+            __syncwarp();
+        }
+        if (act) {
+            if (seg >= 0) {
+                T *part = static_cast<T *>(pf.part2) + int64_t(seg) * DG;
+#pragma unroll
+                for (int c = 0; c < DG; ++c) part[c] = run[c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+            }
+        }
+    }
+}
+
 // Hub targets of a split pass (pfold): value + each partial slot in order.
 template <class T, int DG>
 __global__ void __launch_bounds__(256) k_fold_parts(const __grid_constant__ LaunchParams p, int ga, int64_t nhub,
@@ -1765,7 +1826,10 @@ struct Registrar {
     static void pfold2(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
         using AG = typename FirstInc<S>::type;
-        launch_k(k_pfold_rest<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
+        if (pass2_warp())
+            launch_k(k_pfold_rest_w<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
+        else
+            launch_k(k_pfold_rest<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
     }
     static void fold_targets(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;

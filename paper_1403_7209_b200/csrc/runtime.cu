@@ -68,6 +68,14 @@ bool pdl_enabled() {
     return on;
 }
 
+bool pass2_warp() {
+    static const bool on = [] {
+        const char *e = std::getenv("ML_PASS2W");       // ML_PASS2W=0: thread-per-row pass 2
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
 template <class T, int M>
 __global__ void __launch_bounds__(256) k_combine(T *g, const T *part, int64_t nparts, int dim) {
     pdl_wait();

@@ -598,3 +598,39 @@ def test_config_d_proxy_iteration_vs_oracle():
     close(h["q"].fetch(), rh["q"].fetch(), what="q")
     close([h["rms"][0].value], [rh["rms"][0].value], what="rms")
     assert h["dt_min"][0].value == rh["dt_min"][0].value
+
+
+_PASS2_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1403_7209_b200 as ml
+from paper_1403_7209_b200 import apps
+mesh = apps.gen_hub_mesh(3000, 30000, n_hubs=3, hub_share=0.1, seed=4)
+prog, h = apps.build_diffusion(mesh, 2, dtype="float64")
+ml.run_program(prog, mesh, ml.BackendConfig(inc_schedule="pfold"))
+m2 = apps.gen_hex_mesh(10, seed=3)
+p2, h2 = apps.build_hydra_proxy(m2, steps=1, seed=3)
+ml.run_program(p2[:5], m2, ml.BackendConfig(inc_schedule="pfold"))
+np.savez({out!r}, u=h["u"].fetch(), res=h2["res"].fetch(), grad=h2["grad"].fetch())
+"""
+
+
+def test_pass2_warp_cooperative_equals_thread_per_row(tmp_path):
+    """The warp-cooperative pass 2 (default) adds each target's slots in the
+    same order as the thread-per-row kernel (ML_PASS2W=0): bitwise equal,
+    hub rows included."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    outs = []
+    for flag in ("0", "1"):
+        out = str(tmp_path / f"p{flag}.npz")
+        env = dict(os.environ, ML_PASS2W=flag)
+        r = subprocess.run([sys.executable, "-c", _PASS2_SCRIPT.format(root=root, out=out)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    for k in ("u", "res", "grad"):
+        np.testing.assert_array_equal(outs[0][k], outs[1][k], k)

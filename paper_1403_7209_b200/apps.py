@@ -484,17 +484,26 @@ def _k_proxy_bc(q1, q2, b1, b2):
         q2[v] = b2[v]
 
 
-def build_hydra_proxy(mesh: Mesh, steps: int = 1, seed: int = 0, cfl: float = 0.05):
+def build_hydra_proxy(mesh: Mesh, steps: int = 1, seed: int = 0, cfl: float = 0.05, api=None):
     """Hydra-shaped solver iteration repeated ``steps`` times (the benchmark program).
 
     Per iteration: ``save`` (q→q_old) → ``dt_calc`` (local dt + global MIN)
     → ``grad_edge`` (indirect INC dim 18) → ``iflux`` (34/12) → ``vflux``
     (92/12) → ``update`` (reads the MIN as a READ global, SUM residual,
     zeroes res/grad) → ``bc`` (indirect WRITE on boundary edges).
-    Returns ``(program, handles)``.
+    Returns ``(program, handles)``.  ``api``: the package whose ``Global``,
+    ``Loop``, ``arg_*`` and access modes build the program (default this one;
+    the reference ``meshloop`` module builds it from reference objects, for
+    the stock reference's own executors and the reference-object path).
     """
     _require(mesh, sets=("nodes", "edges", "bedges"), maps=("edge_nodes", "bedge_nodes"),
              dats=("coords",))
+    if api is not None:
+        Global, Loop = api.Global, api.Loop
+        arg_direct, arg_indirect, arg_global = api.arg_direct, api.arg_indirect, api.arg_global
+        READ, WRITE, RW, INC, MIN = api.READ, api.WRITE, api.RW, api.INC, api.MIN
+    else:
+        from .core import Global, Loop, arg_direct, arg_indirect, arg_global, READ, WRITE, RW, INC, MIN
     nodes, edges, bedges = (mesh.sets[k] for k in ("nodes", "edges", "bedges"))
     en, bn = mesh.maps["edge_nodes"], mesh.maps["bedge_nodes"]
     n, m = nodes.size, edges.size

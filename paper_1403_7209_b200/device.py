@@ -49,8 +49,9 @@ class DatMirror:
         self.device_newer = False
 
 
-def dat_mirror(dat: Dat, force_upload: bool = False) -> DatMirror:
-    """The up-to-date device mirror of ``dat`` (allocating/uploading as needed)."""
+def dat_mirror(dat: Dat, force_upload: bool = False, upload: bool = True) -> DatMirror:
+    """The up-to-date device mirror of ``dat`` (allocating/uploading as needed;
+    ``upload=False`` only allocates — the caller copies the contents)."""
     m = dat._dev
     if m is None:
         m = dat._dev = DatMirror()
@@ -64,7 +65,7 @@ def dat_mirror(dat: Dat, force_upload: bool = False) -> DatMirror:
     if m.layout is not dat.layout:
         m.layout = dat.layout
         m.host_newer = True
-    if (m.host_newer or force_upload) and not m.device_newer:
+    if upload and (m.host_newer or force_upload) and not m.device_newer:
         if host.nbytes:
             if not host.flags.c_contiguous:
                 dat._host = host = np.ascontiguousarray(host)

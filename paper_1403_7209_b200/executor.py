@@ -456,6 +456,8 @@ class CompiledProgram:
         self.handle = handle.value
         N.check(N.lib().ml_program_set_concurrent(self.handle, int(bool(config.concurrent_loops))))
         self.ptrs = [e.dat_pointers() for e in self.entries]
+        # each loop descriptor bakes its dats' layouts into strides (runtime.cu)
+        self.layouts = [d.layout for d in self.all_dats]
         self.runs = 0
 
     def dependencies(self) -> list:
@@ -472,6 +474,8 @@ class CompiledProgram:
 
     def valid_for(self, mesh: Mesh) -> bool:
         if mesh.version != self.version:
+            return False
+        if [d.layout for d in self.all_dats] != self.layouts:
             return False
         for d in self.all_dats:
             dat_mirror(d)
@@ -540,11 +544,19 @@ class CompiledProgram:
         for g in self.globs:
             o = self.gslot[id(g)]
             hv[o:o + g.buffer.nbytes] = g.buffer.view(np.uint8)
+        # a dat whose device copy is newer than the host payload (left by a
+        # device-resident run) is already current on the device: uploading the
+        # stale host copy would lose it
+        stale_host = {id(d) for d in self.all_dats if d._dev is not None and d._dev.device_newer}
         for d in self.all_dats:
-            dat_mirror(d)                      # allocation; contents come below
+            dat_mirror(d, upload=False)        # allocation; contents come below
         N.check(L.ml_copy_h2d(self.gdev.ptr, N.ptr(hv), self.gbytes), "ml_copy_h2d")
+        uploaded = []
         for i, e in enumerate(self.entries):
             for d in first[i]:
+                if id(d) in stale_host:
+                    continue
+                uploaded.append(d)
                 host = d._host
                 if host.nbytes:
                     if not host.flags.c_contiguous:
@@ -564,7 +576,9 @@ class CompiledProgram:
         for g in self.globs:
             o = self.gslot[id(g)]
             g.buffer[:] = hv[o:o + g.buffer.nbytes].view(g.buffer.dtype)
-        for d in self.all_dats:
+        for d in uploaded:
+            d._dev.host_newer = False
+        for d in self.written:                 # downloaded after their last writer
             d._dev.host_newer = False
             d._dev.device_newer = False
         self.runs += 1
@@ -657,7 +671,14 @@ def _record(collector: PerfCollector, cp: CompiledProgram, times) -> None:
 
 def run_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig | None = None
                 ) -> RunResult:
-    """Execute a loop program on B200 and collect per-loop device timings."""
+    """Execute a loop program on B200 and collect per-loop device timings.
+
+    ``mesh`` may also be a reference ``meshloop.Mesh`` with a program of
+    reference objects (run through :mod:`.foreign`: shadow mesh sharing its
+    arrays, host-resident coherence)."""
+    if not isinstance(mesh, Mesh):
+        from .foreign import run_foreign
+        return run_foreign(program, mesh, config)
     config = config or BackendConfig()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if config.nranks > 1 or world > 1:

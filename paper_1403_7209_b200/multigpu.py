@@ -32,6 +32,7 @@ with an injected CPU executor, on CPU).
 from __future__ import annotations
 
 import os
+from collections import OrderedDict
 import time
 from dataclasses import dataclass, field
 from typing import Sequence
@@ -205,6 +206,15 @@ class RankProgram:
             self.loops.append(Loop(loop.name, sets[loop.iter_set.name], args, loop.kernel))
             self.reductions.append(reds)
         self.roles = loop_dat_roles(self.program, layout)
+
+    def refresh_from_global(self) -> None:
+        """Re-read every local dat (owned + halo rows) from the global mesh — the
+        user-visible truth between runs — and mark all halos fresh."""
+        for name, ld in self.dats.items():
+            gd = self.global_dats[name]
+            ld.put(gd.fetch()[self.local_ids[gd.set.name]])
+        self.__dict__["dirty"] = {}
+        self.refresh_globals()
 
     def reset_partials(self, entry: int) -> None:
         for part, _val, mode in self.reductions[entry]:
@@ -1065,6 +1075,23 @@ class StreamRank:
             o = self.slots[id(val)]
             val.buffer[:] = host[o:o + val.buffer.nbytes].view(val.buffer.dtype)
 
+    def sync_inputs(self) -> None:
+        """Upload every local dat whose host payload is newer (after
+        ``RankProgram.refresh_from_global``)."""
+        from .device import dat_mirror
+        for e in self.entries:
+            for d in e.dats:
+                dat_mirror(d)
+
+    def close(self) -> None:
+        """Unmap the peers' IPC buffers, then wait for every rank to have done
+        so before this rank's exported buffers may be freed."""
+        for x in (self.nvlink, self.nvreduce):
+            if x is not None:
+                x.close()
+        self.nvlink = self.nvreduce = None
+        self.transport.barrier()
+
     def launches_per_run(self) -> int:
         total = 0
         for i, e in enumerate(self.entries):
@@ -1174,14 +1201,62 @@ def setup_distributed(program, mesh, config, transport=None, executor_factory=No
     return rp, dev, transport, layout, config
 
 
+_DIST_CACHE_SIZE = 4
+
+
+def _config_key(config) -> tuple:
+    from dataclasses import fields
+    out = []
+    for f in fields(config):
+        v = getattr(config, f.name)
+        if isinstance(v, dict):
+            v = tuple(sorted(v.items()))
+        elif callable(v):
+            v = id(v)
+        out.append((f.name, v))
+    return tuple(out)
+
+
+def _cached_setup(program, mesh, config, transport, executor_factory, layout):
+    """``setup_distributed`` once per (program, mesh version, config, layout):
+    a repeated ``run_program`` (one call per time step) reuses the rank
+    program, its device state and the opened IPC mappings, re-reading the
+    local dats from the global mesh.  Evicted entries close their mappings
+    (collectively: every rank makes the same calls in the same order)."""
+    import torch.distributed as dist
+    world = dist.get_world_size() if dist.is_initialized() else int(os.environ.get("WORLD_SIZE", "1"))
+    cache = mesh.__dict__.setdefault("_ml_dist", OrderedDict())
+    key = (tuple(id(l) for l in program), mesh.version, _config_key(config), world,
+           id(layout) if layout is not None else None, id(executor_factory) if executor_factory else None,
+           id(transport) if transport is not None else None)
+    hit = cache.get(key)
+    pinned = (layout, executor_factory, transport)
+    if (hit is not None and len(hit[0]) == len(program)
+            and all(a is b for a, b in zip(hit[0], program))
+            and all(a is b for a, b in zip(hit[2], pinned))):
+        cache.move_to_end(key)
+        rp, dev = hit[1][0], hit[1][1]
+        rp.refresh_from_global()
+        if isinstance(dev, StreamRank):
+            dev.sync_inputs()
+        return hit[1]
+    out = setup_distributed(program, mesh, config, transport, executor_factory, layout)
+    cache[key] = (list(program), out, pinned)
+    while len(cache) > _DIST_CACHE_SIZE:
+        _, (_, old, _) = cache.popitem(last=False)
+        if isinstance(old[1], StreamRank):
+            old[1].close()
+    return out
+
+
 def run_program_distributed(program, mesh, config, transport=None, executor_factory=None,
                             layout=None, collector=None):
     """Owner-compute execution of a program on ``WORLD_SIZE`` processes (one GPU each)."""
     from .executor import RunResult
     from .perf import PerfCollector, useful_bytes
     t_start = time.perf_counter()
-    rp, dev, transport, layout, config = setup_distributed(program, mesh, config, transport,
-                                                           executor_factory, layout)
+    rp, dev, transport, layout, config = _cached_setup(program, mesh, config, transport,
+                                                       executor_factory, layout)
     if isinstance(dev, StreamRank):
         messages = dev.run()
         dev.finish()

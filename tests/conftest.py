@@ -62,3 +62,27 @@ def golden(name: str) -> Golden:
 
 def golden_bytes() -> dict:
     return json.loads((GOLDEN / "bytes.json").read_text())
+
+
+def import_reference():
+    """The stock reference package ``meshloop``: the driver's install under
+    ``baseline/_ref`` (travels to the GPU box), else the read-only source tree
+    of this container; None if neither is present.  Imported under its own
+    name, so ``meshloop.apps`` kernels keep their reference qualified names."""
+    import importlib
+    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "meshloop" / "__init__.py").exists():
+            if str(p) not in sys.path:
+                sys.path.append(str(p))
+            mod = importlib.import_module("meshloop")
+            importlib.import_module("meshloop.apps")
+            return mod
+    return None
+
+
+@pytest.fixture(scope="session")
+def R():
+    mod = import_reference()
+    if mod is None:
+        pytest.skip("stock reference package not available (baseline/_ref)")
+    return mod

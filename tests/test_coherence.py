@@ -1,0 +1,67 @@
+"""Host/device coherence across runs (GPU).
+
+* A compiled program bakes each dat's layout into its loop descriptors; a
+  ``transform_layout`` between runs must invalidate it (the reference reads
+  ``d.layout`` on every run, core.py:179-192 / executor.py:149-160).
+* A device-resident run leaves written dats newer on the device; a following
+  host-residency run (streamed or not) must not overwrite them with the
+  stale host payload.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1403_7209_b200 as ml
+from paper_1403_7209_b200 import apps
+from oracle import bulk
+
+
+def _proxy(N=9, seed=3):
+    mesh = apps.gen_hex_mesh(N, seed=seed)
+    prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=seed)
+    return mesh, prog, h
+
+
+def _close(a, b):
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-12 * max(np.abs(b).max(), 1e-300))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_transform_layout_between_runs(use_graph):
+    mesh, prog, h = _proxy()
+    ref, rprog, rh = _proxy()
+    cfg = ml.BackendConfig(use_graph=use_graph)
+    ml.run_program(prog, mesh, cfg)
+    bulk.run_program(rprog)
+    for name in ("q", "aux", "grad"):
+        target = ml.AOS if mesh.dats[name].layout is ml.SOA else ml.SOA
+        ml.transform_layout(mesh.dats[name], target)
+        ml.transform_layout(ref.dats[name], target)
+    ml.run_program(prog, mesh, cfg)
+    bulk.run_program(rprog)
+    for k in ("q", "q_old", "res", "grad", "dt_loc"):
+        _close(h[k].fetch(), rh[k].fetch())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("host_mode", ["streamed", "eager"])
+def test_device_then_host_residency_keeps_device_results(host_mode):
+    mesh, prog, h = _proxy()
+    ref, rprog, rh = _proxy()
+    ml.run_program(prog, mesh, ml.BackendConfig())                 # device-resident
+    bulk.run_program(rprog)
+    hcfg = (ml.BackendConfig(residency="host", use_graph=True) if host_mode == "streamed"
+            else ml.BackendConfig(residency="host"))
+    ml.run_program(prog, mesh, hcfg)
+    bulk.run_program(rprog)
+    for k in ("q", "q_old", "res", "grad", "dt_loc"):
+        _close(h[k].fetch(), rh[k].fetch())
+    # and back to device residency after a host write
+    mesh.dats["q"].data[:5] += 1.0
+    ref.dats["q"].data[:5] += 1.0
+    ml.run_program(prog, mesh, ml.BackendConfig())
+    bulk.run_program(rprog)
+    for k in ("q", "q_old", "res", "grad", "dt_loc"):
+        _close(h[k].fetch(), rh[k].fetch())

@@ -16,7 +16,7 @@ import paper_1403_7209_b200 as ml
 from conftest import golden
 from oracle import bulk, serial as oserial
 from paper_1403_7209_b200 import apps
-from paper_1403_7209_b200.kernels import device_kernel, resolve_kernel
+from paper_1403_7209_b200.kernels import device_kernel
 
 pytestmark = pytest.mark.gpu
 
@@ -142,7 +142,7 @@ def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa, sched):
     """Stop before the update so the raw INC accumulators (res, grad) are compared,
     for every layout (auto-SoA, all AoS, all SoA) and INC schedule."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, soa=soa)
-    bulk.run_program(rprog[:5], resolve_kernel)
+    bulk.run_program(rprog[:5])
     ml.run_program(prog[:5], mesh, cfg(inc_schedule=sched))
     for k in ("grad", "res", "q_old", "dt_loc"):
         close(h[k].fetch(), rh[k].fetch(), what=k)
@@ -153,7 +153,7 @@ def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa, sched):
 def test_proxy_full_size_iteration_vs_oracle(sched):
     """Config B (Rotor37-sized, 2.47M edges): one full iteration, shuffled + CM-renumbered."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(94, seed=0)
-    bulk.run_program(rprog, resolve_kernel)
+    bulk.run_program(rprog)
     ml.run_program(prog, mesh, cfg(inc_schedule=sched))
     close(h["q"].fetch(), rh["q"].fetch(), what="q")
     close([h["rms"][0].value], [rh["rms"][0].value], what="rms")
@@ -164,7 +164,7 @@ def test_int64_diffusion_rotor37_size_bit_exact():
     """gen_mesh(913): 835,396 nodes / 2,502,533 edges, int64 twin, bit-exact vs oracle."""
     ref = apps.gen_mesh(913)
     rprog, rh = apps.build_diffusion(ref, 2, dtype="int64")
-    bulk.run_program(rprog, resolve_kernel)
+    bulk.run_program(rprog)
     mesh = apps.gen_mesh(913)
     prog, h = apps.build_diffusion(mesh, 2, dtype="int64")
     ml.run_program(prog, mesh, cfg())
@@ -282,13 +282,13 @@ def test_gather_schedule_reproduces_serial_order_bitwise(soa, sched):
     """Target-centric schedule accumulates every target in the reference serial
     order, so even float64 raw INC accumulators equal the oracle bit for bit."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(20, soa=soa)
-    bulk.run_program(rprog[:5], resolve_kernel)
+    bulk.run_program(rprog[:5])
     # unchained: a chained iflux+vflux interleaves the two loops' increments
     ml.run_program(prog[:5], mesh, cfg(inc_schedule=sched, chain_loops=False))
     for k in ("grad", "res", "q_old", "dt_loc"):
         np.testing.assert_array_equal(h[k].fetch(), rh[k].fetch(), k)
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, seed=3)
-    bulk.run_program(rprog, resolve_kernel)
+    bulk.run_program(rprog)
     ml.run_program(prog, mesh, cfg(inc_schedule=sched))
     close(h["q"].fetch(), rh["q"].fetch(), what="q")
     for app in ("diffusion", "cell-area"):
@@ -445,7 +445,7 @@ def test_tile_schedule_matches_oracle_and_is_deterministic(smem_kb, cmax, sched)
     accumulators within tolerance of the serial oracle at several tile sizes,
     int64 bit-exact, reductions counted once per element, bitwise run to run."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(12)
-    bulk.run_program(rprog[:5], resolve_kernel)
+    bulk.run_program(rprog[:5])
     c = cfg(inc_schedule=sched, tile_smem_kb=smem_kb, tile_cmax=cmax)
     ml.run_program(prog[:5], mesh, c)
     for k in ("grad", "res"):
@@ -486,7 +486,7 @@ def test_pfold_schedule_raw_accumulators_reductions_and_determinism(own_kb):
     int64 bit-exact (fuzz + diffusion), MIN/MAX/READ globals counted once per
     element, bitwise run to run; with and without own-row staging."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(12)
-    bulk.run_program(rprog[:5], resolve_kernel)
+    bulk.run_program(rprog[:5])
     c = cfg(inc_schedule="pfold", pfold_own_kb=own_kb)
     ml.run_program(prog[:5], mesh, c)
     for k in ("grad", "res"):
@@ -553,7 +553,7 @@ def test_chained_flux_loops_match_oracle(sched):
     full iteration's q, rms and dt_min too."""
     from paper_1403_7209_b200.executor import compile_program
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, seed=5)
-    bulk.run_program(rprog[:5], resolve_kernel)
+    bulk.run_program(rprog[:5])
     c = cfg(inc_schedule=sched)
     assert [l.name for l in compile_program(prog[:5], mesh, c).run_loops][-1] == "iflux+vflux"
     ml.run_program(prog[:5], mesh, c)
@@ -567,7 +567,7 @@ def test_chained_flux_loops_match_oracle(sched):
     ml.run_program(prog[3:5], mesh, c)
     np.testing.assert_array_equal(h["res"].fetch(), first)
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(16, seed=6)
-    bulk.run_program(rprog, resolve_kernel)
+    bulk.run_program(rprog)
     ml.run_program(prog, mesh, cfg(inc_schedule=sched, use_graph=True))
     close(h["q"].fetch(), rh["q"].fetch(), what="q")
     close([h["rms"][0].value], [rh["rms"][0].value], what="rms")
@@ -581,7 +581,7 @@ def test_config_d_8m_edges_int64_bit_exact(sched):
     single-GPU size BASELINE.json names."""
     ref = apps.gen_mesh(1633)
     rprog, rh = apps.build_diffusion(ref, 2, dtype="int64")
-    bulk.run_program(rprog, resolve_kernel)
+    bulk.run_program(rprog)
     mesh = apps.gen_mesh(1633)
     prog, h = apps.build_diffusion(mesh, 2, dtype="int64")
     ml.run_program(prog, mesh, cfg(inc_schedule=sched))
@@ -593,7 +593,7 @@ def test_config_d_proxy_iteration_vs_oracle():
     """139^3 grid (7,998,894 edges): one chained Hydra-proxy iteration with the
     default schedules vs the oracle running the loops one by one."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(139, seed=2)
-    bulk.run_program(rprog, resolve_kernel)
+    bulk.run_program(rprog)
     ml.run_program(prog, mesh, cfg())
     close(h["q"].fetch(), rh["q"].fetch(), what="q")
     close([h["rms"][0].value], [rh["rms"][0].value], what="rms")

@@ -110,11 +110,10 @@ def test_proxy_two_ranks_on_device_vs_oracle(sched, executor):
     import paper_1403_7209_b200 as ml
     from oracle import bulk
     from paper_1403_7209_b200 import apps
-    from paper_1403_7209_b200.kernels import resolve_kernel
     mesh = apps.gen_hex_mesh(12, seed=5)
     prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=5)
     ml.renumber_mesh(mesh)
-    bulk.run_program(prog, resolve_kernel)
+    bulk.run_program(prog)
     outs = _run(("proxy", 12, "float64", 2, "rcb", sched), 2, executor)
     ref_q = h["q"].fetch()
     for rank, out, _ in outs:

@@ -88,9 +88,26 @@ def _worker(rank, world, port, case, q):
             from paper_1403_7209_b200 import apps
             mesh = apps.gen_hex_mesh(n, seed=7)
             prog, h = apps.build_hydra_proxy(mesh, steps=steps, seed=7)
+        elif app == "repeat":
+            mesh, prog, h = _cases.build_app("diffusion", n, dtype, 1)
         else:
             mesh, prog, h = _cases.build_app(app, n, dtype, steps)
         cfg = ml.BackendConfig(nranks=world, partitioner=part)
+        if app == "repeat":
+            # one run_program call per time step: the cached rank setup is reused
+            # and a host write to a global dat between calls is seen
+            from paper_1403_7209_b200 import multigpu
+            setups = []
+            for k in range(steps):
+                result = run_program_distributed(prog, mesh, cfg, executor_factory=OracleRank)
+                setups.append(id(next(iter(mesh.__dict__["_ml_dist"].values()))[1][0]))
+                u = mesh.dats["u"].fetch()
+                u[::5] += k + 1
+                mesh.dats["u"].put(u)
+            out = {"u": mesh.dats["u"].fetch(), "res": np.array([g.value for g in h["residuals"]]),
+                   "setups": len(set(setups))}
+            q.put((rank, out, result.messages))
+            return
         result = run_program_distributed(prog, mesh, cfg, executor_factory=OracleRank)
         if app == "proxy":
             out = {"q": h["q"].fetch(), "rms": np.array([r.value for r in h["rms"]]),
@@ -195,3 +212,22 @@ def test_two_ranks_chained_proxy_matches_serial():
         ref = h["q"].fetch()
         np.testing.assert_allclose(out["q"], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
         np.testing.assert_allclose(out["rms"], [r.value for r in h["rms"]], rtol=1e-12)
+
+
+def test_repeated_run_program_reuses_rank_setup_and_sees_host_writes():
+    """a multi-rank program run once per time step must not rebuild
+    its layout / rank program / IPC mappings, and must start every run from
+    the global mesh's current values."""
+    import _cases
+    from oracle import serial
+    mesh, prog, h = _cases.build_app("diffusion", 8, "int64", 1)
+    for k in range(3):
+        serial.run_program(prog)
+        u = mesh.dats["u"].fetch()
+        u[::5] += k + 1
+        mesh.dats["u"].put(u)
+    outs = _run(("repeat", 8, "int64", 3, "rcb"))
+    for _rank, out, _msgs in outs:
+        assert out["setups"] == 1
+        np.testing.assert_array_equal(out["u"], mesh.dats["u"].fetch())
+        np.testing.assert_array_equal(out["res"], [g.value for g in h["residuals"]])

@@ -11,7 +11,6 @@ import _cases
 from oracle import bulk, partition as opart, perf as operf, plan as oplan, renumber as oren
 from oracle import serial as oserial
 from paper_1403_7209_b200 import apps
-from paper_1403_7209_b200.kernels import resolve_kernel
 
 
 # -- plans ------------------------------------------------------------------------------
@@ -171,7 +170,7 @@ def test_oracle_serial_reproduces_reference_bit_for_bit(case):
 def test_oracle_bulk_is_bit_identical_to_serial(case):
     g = golden("exec.npz")
     mesh, prog, h = _cases.build_app(case["app"], case["n"], case["dtype"], case["steps"])
-    bulk.run_program(prog, resolve_kernel)
+    bulk.run_program(prog)
     for k, v in _cases.app_results(case["app"], h).items():
         np.testing.assert_array_equal(v, g[f"exec/{case['name']}/{k}"], k)
 
@@ -209,7 +208,7 @@ def test_oracle_proxy_matches_reference(N, steps, which):
     if which == "serial":
         oserial.run_program(prog)
     else:
-        bulk.run_program(prog, resolve_kernel)
+        bulk.run_program(prog)
     name = f"proxy_hex{N}_s{steps}"
     for k in ("q", "q_old", "res", "grad", "dt_loc"):
         np.testing.assert_array_equal(h[k].fetch(), g[f"exec/{name}/{k}"], k)

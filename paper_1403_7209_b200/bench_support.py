@@ -21,7 +21,8 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 FALLBACK_PEAK_GBS = 6650.0
 
-__all__ = ["build_workload", "clock_sampler", "peaks_gbs", "ClockSampler"]
+__all__ = ["build_workload", "clock_sampler", "peaks_gbs", "ClockSampler", "load_reference",
+           "cpu_model", "time_reference", "reference_modes"]
 
 
 def peaks_gbs() -> tuple[float, str]:
@@ -121,3 +122,88 @@ def build_workload(args):
     renumber_mesh(mesh)
     t_ren = time.perf_counter() - t0
     return mesh, prog, h, name, {"generate_s": round(t_gen, 3), "renumber_s": round(t_ren, 3)}
+
+
+# -- the stock reference on the host CPU (bench.py's cpu_baseline and reference arm) ------
+
+def load_reference():
+    """The stock reference package ``meshloop``: the driver's offline install in
+    ``baseline/_ref`` (it travels to the GPU box), else an importable one; None
+    if absent.  This is the reference itself, not a restatement."""
+    import importlib
+    import sys
+    p = ROOT / "baseline" / "_ref"
+    if (p / "meshloop" / "__init__.py").exists() and str(p) not in sys.path:
+        sys.path.append(str(p))
+    try:
+        return importlib.import_module("meshloop")
+    except ImportError:
+        return None
+
+
+def cpu_model() -> str:
+    """``lscpu`` model name of this host."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_modes(cores: int) -> dict:
+    """The reference's CPU execution modes (executor.py:707-729) with all host
+    threads: serial, threads (nthreads = cores), ranks (largest power of two
+    <= cores, RCB on the ``coords`` dat: partition.py:81-106)."""
+    p = 1
+    while p * 2 <= cores:
+        p *= 2
+    return {"serial": {}, "threads": {"backend": "threads", "nthreads": cores},
+            "ranks": {"backend": "ranks", "nranks": p, "partitioner": "rcb"}}
+
+
+def _split_at_reduced_reads(program):
+    """Programs to run one after another so that a global a loop reduces is
+    final before a later loop READs it.  The reference's ranks backend folds
+    reductions only when the whole program ends (executor.py:653-660), so one
+    call over the proxy iteration would hand ``update`` the initial +inf of
+    ``dt_min``; splitting after ``dt_calc`` keeps its arithmetic finite."""
+    parts, cur, reduced = [], [], set()
+    for l in program:
+        reads = {id(a.glob) for a in l.args if a.kind == "global" and a.mode.name == "READ"}
+        if reads & reduced and cur:
+            parts.append(cur)
+            cur, reduced = [], set()
+        cur.append(l)
+        reduced |= {id(a.glob) for a in l.args if a.kind == "global" and a.mode.name != "READ"}
+    if cur:
+        parts.append(cur)
+    return parts
+
+
+def time_reference(R, mesh, prog, mode: str, cores: int, runs: int = 1, warm: int = 0):
+    """Seconds per stock ``meshloop.run_program`` call of ``prog`` (exported to
+    reference objects) in ``mode``; ``warm`` untimed calls first (the threads
+    backend builds and caches its plans on the first call).  Returns
+    (seconds per run, number of run_program calls per run)."""
+    from .foreign import export_mesh, export_program
+    ref = export_mesh(mesh, R)
+    rprog = export_program(prog, ref, R)
+    cfg = R.BackendConfig(**reference_modes(cores)[mode])
+    parts = _split_at_reduced_reads(rprog) if mode == "ranks" else [rprog]
+    for _ in range(warm):
+        for p in parts:
+            R.run_program(p, ref, cfg)
+    t0 = time.perf_counter()
+    for _ in range(runs):
+        for p in parts:
+            R.run_program(p, ref, cfg)
+    return (time.perf_counter() - t0) / runs, len(parts)

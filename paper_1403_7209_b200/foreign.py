@@ -45,7 +45,7 @@ from . import core
 from .core import ExecError
 
 __all__ = ["is_foreign_mesh", "shadow_mesh", "run_foreign", "install", "to_backend_config",
-           "export_mesh"]
+           "export_mesh", "export_program"]
 
 _SHADOWS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 _PROGRAMS_PER_MESH = 32
@@ -238,3 +238,26 @@ def export_mesh(mesh: core.Mesh, api, auto_soa_threshold=_DEFAULT):
     for n, d in mesh.dats.items():
         out.decl_dat(n, sets[d.set.name], d.dim, d.dtype.name, d.fetch().reshape(-1))
     return out
+
+
+def export_program(program, ref, api):
+    """``program`` (loops over a product mesh) as loops of package ``api`` over
+    ``ref`` — a mesh exported from it by :func:`export_mesh` (matched by name);
+    each product ``Global`` becomes one fresh ``api.Global`` with the same values."""
+    gmap: dict = {}
+    loops = []
+    for l in program:
+        args = []
+        for a in l.args:
+            mode = getattr(api, a.mode.name)
+            if a.kind == "global":
+                g = gmap.get(id(a.glob))
+                if g is None:
+                    g = gmap[id(a.glob)] = api.Global(a.glob.buffer.copy(), name=a.glob.name)
+                args.append(api.arg_global(g, mode))
+            elif a.kind == "direct":
+                args.append(api.arg_direct(ref.dats[a.dat.name], mode))
+            else:
+                args.append(api.arg_indirect(ref.dats[a.dat.name], ref.maps[a.map.name], a.slot + 1, mode))
+        loops.append(api.Loop(l.name, ref.sets[l.iter_set.name], args, l.kernel))
+    return loops

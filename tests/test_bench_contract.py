@@ -23,6 +23,27 @@ def test_reference_arm_prints_one_contract_line():
               "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["impl"] == "reference" and d["unit"] == "edges/s" and d["higher_is_better"] is True
-    assert d["config"]["workload"] == "hydra-proxy iteration, 3-D grid 94^3"
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] == 1
+    # the workload label is the sample that actually ran, not the 94^3 target
+    assert d["config"]["workload"] == "hydra-proxy iteration, 3-D grid 6^3"
+    assert d["config"]["sample_of"] == "hydra-proxy iteration, 3-D grid 94^3"
+    import conftest
+    want = "reference" if conftest.import_reference() is not None else "port"
+    assert d["cpu_baseline"]["kind"] == want and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"] > 0
+
+
+def test_cpu_baseline_runs_stock_reference_modes():
+    """cpu_baseline times the stock reference in serial / threads / ranks mode."""
+    import argparse
+    import conftest
+    if conftest.import_reference() is None:
+        import pytest
+        pytest.skip("stock reference not installed")
+    sys.path.insert(0, str(ROOT))
+    import bench
+    args = argparse.Namespace(workload="proxy", grid=5, cpu_grid=4, cpu_sample_only=False)
+    cb = bench.cpu_baseline(args)
+    assert cb["kind"] == "reference" and set(cb["modes"]) == {"serial", "threads", "ranks"}
+    assert cb["modes"]["serial"]["workload"].endswith("5^3")
+    assert cb["modes"]["ranks"]["run_program_calls"] == 2 and cb["value"] > 0
+    assert cb["cpu_model"]

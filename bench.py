@@ -194,6 +194,32 @@ def pcie_bounds(h2d: int, d2h: int) -> dict:
     return out
 
 
+def scaling_base(args) -> dict:
+    """The N=1 point of the multi-GPU curve: ``--scale-grid`` (default 139^3,
+    BASELINE configs[3]) through the same rank executor the 2/4/8-GPU runs use
+    (StreamRank, world size 1, RCB layout of one rank, CUDA-graph rank step),
+    device time only.  ``value`` of this line stays the configs[1] number."""
+    from paper_1403_7209_b200.multigpu import bench_distributed
+    env = {"RANK": "0", "LOCAL_RANK": "0", "WORLD_SIZE": "1", "MASTER_ADDR": "127.0.0.1",
+           "MASTER_PORT": str(_free_port())}
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        a = argparse.Namespace(**{**vars(args), "grid": args.scale_grid, "inc_schedule": "auto"})
+        line = bench_distributed(a, METRIC, emit=False, with_e2e=False)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return {"workload": line["config"]["workload"], "edges": line["config"]["edges"],
+            "value": line["value"], "unit": "edges/s", "ms_per_step": line["ms_per_step"],
+            "n_gpus": 1, "executor": "StreamRank (multigpu.py), world size 1",
+            "cuda_graph": line["config"]["cuda_graph"],
+            "roofline_frac": line["roofline"]["frac"], "loops_ms": line["loops_ms_rank0"]}
+
+
 def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
@@ -286,6 +312,7 @@ def run_ours(args) -> None:
            "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s / args.steps}
     e2e["pcie"] = pcie_bounds(h2d, d2h)
 
+    scale_base = scaling_base(args) if args.scale_grid and args.workload == "proxy" else None
     cb = cpu_baseline(args) if not args.no_cpu else None
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": 1, "steps": args.steps,
@@ -314,8 +341,62 @@ def run_ours(args) -> None:
         "eager_ms_per_step": round(sum(v["ms"] for v in loops.values()), 4),
         "e2e": e2e,
         "cpu_baseline": cb,
+        "scaling_base": scale_base,
     }
     print(json.dumps(line))
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(n: int) -> int:
+    """``--gpus N`` without torchrun: start N rank processes of this script
+    (RANK/LOCAL_RANK = GPU index, rendezvous on 127.0.0.1 — the reference's
+    ``run_ranks`` needs no launcher either, executor.py:690-695).  Rank 0's
+    stdout is the bench line; the others are silenced.  The first rank to fail
+    stops the rest; the exit code is the first non-zero one."""
+    import subprocess
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), *sys.argv[1:]],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    live = list(procs)
+    while live:
+        for p in list(live):
+            code = p.poll()
+            if code is None:
+                continue
+            live.remove(p)
+            if code != 0 and rc == 0:
+                rc = code
+                for q in live:
+                    q.terminate()
+        time.sleep(0.05)
+    return rc
+
+
+def launch_probe(args) -> None:
+    """``--launch-probe``: each rank joins a gloo group and all-reduces its rank;
+    rank 0 prints one JSON line (tests the launcher without a GPU)."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    if args.launch_probe_fail == rank:
+        sys.exit(3)
+    dist.init_process_group("gloo")
+    t = torch.tensor([rank + 1.0])
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"probe": "ok", "world": dist.get_world_size(), "sum": float(t.item())}))
+    dist.destroy_process_group()
 
 
 def main():
@@ -334,9 +415,21 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-only", action="store_true",
                     help="cpu_baseline: time the serial mode on the sample too (not the full workload)")
+    ap.add_argument("--scale-grid", type=int, default=139,
+                    help="N=1: also time this grid through the multi-GPU executor at world size 1 "
+                         "(the base of the 2/4/8-GPU curve); 0 skips it")
+    ap.add_argument("--launch-probe", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--launch-probe-fail", type=int, default=-1, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(self_launch(args.gpus))
+    if args.launch_probe:
+        launch_probe(args)
+        return
     if args.grid is None:
-        args.grid = 94 if args.workload == "proxy" else 913
+        # N>1: BASELINE configs[3], the ~8M-edge mesh (139^3 = 7,998,894 edges)
+        multi = args.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1
+        args.grid = (139 if multi else 94) if args.workload == "proxy" else (1633 if multi else 913)
     if args.cpu_grid is None:          # ~2-3 s of CPU per reference-arm step / sampled mode
         if args.impl == "reference":
             args.cpu_grid = 30 if args.workload == "proxy" else 200

@@ -1284,7 +1284,7 @@ def run_program_distributed(program, mesh, config, transport=None, executor_fact
                      layout=layout, assignments=layout.assignments)
 
 
-def bench_distributed(args, metric):
+def bench_distributed(args, metric, emit: bool = True, with_e2e: bool = True):
     """bench.py at N GPUs (torchrun, one process per GPU): same workload as N=1
     (strong scaling), RCB partition, halos over NCCL with the exchange
     overlapped with core targets (StreamRank).  ``value``: K program runs timed
@@ -1347,23 +1347,26 @@ def bench_distributed(args, metric):
         dev.finish()
     dev_s = start.elapsed_time(stop) * 1e-3
     # end to end: host buffers in and out every step
-    for d in rp.dats.values():
-        d._pull()
-    pin_mesh(rp.local)
-    h2d = sum(d.nbytes for d in rp.dats.values())
-    written = {d.name: d for e in dev.entries for d in e.written}
-    d2h = sum(d.nbytes for d in written.values())
-    from .device import dat_mirror
-    dist.barrier()
-    t_e2e = time.perf_counter()
-    for _ in range(args.steps):
+    h2d = d2h = 0
+    e2e_s = float("nan")
+    if with_e2e:
         for d in rp.dats.values():
-            dat_mirror(d, force_upload=True)
-        dev.run()
-        dev.finish()
-        for d in written.values():
             d._pull()
-    e2e_s = time.perf_counter() - t_e2e
+        pin_mesh(rp.local)
+        h2d = sum(d.nbytes for d in rp.dats.values())
+        written = {d.name: d for e in dev.entries for d in e.written}
+        d2h = sum(d.nbytes for d in written.values())
+        from .device import dat_mirror
+        dist.barrier()
+        t_e2e = time.perf_counter()
+        for _ in range(args.steps):
+            for d in rp.dats.values():
+                dat_mirror(d, force_upload=True)
+            dev.run()
+            dev.finish()
+            for d in written.values():
+                d._pull()
+        e2e_s = time.perf_counter() - t_e2e
     t = torch.tensor([dev_s, e2e_s], dtype=torch.float64,
                      device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -1377,6 +1380,7 @@ def bench_distributed(args, metric):
     halo = [len(layout.sets["nodes"][r].nonexec_halo) + len(layout.sets["nodes"][r].exec_halo)
             for r in range(world)]
     split = [e.loop.name for e, sp in zip(dev.entries, dev.split) if sp is not None]
+    line = None
     if rank == 0:
         peak, src = peaks_gbs()
         line = {"metric": metric, "value": edges * args.steps / tmax, "unit": "edges/s",
@@ -1411,6 +1415,11 @@ def bench_distributed(args, metric):
                         "ms_per_step": 1e3 * e2e_max / args.steps,
                         "note": "rank 0's bytes; wall clock, max over ranks"},
                 "cpu_baseline": None}
-        print(json.dumps(line), flush=True)
+        if not with_e2e:
+            line["e2e"] = None
+        if emit:
+            print(json.dumps(line), flush=True)
     dist.barrier()
+    dev.close()
     dist.destroy_process_group()
+    return line

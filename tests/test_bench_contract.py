@@ -47,3 +47,26 @@ def test_cpu_baseline_runs_stock_reference_modes():
     assert cb["modes"]["serial"]["workload"].endswith("5^3")
     assert cb["modes"]["ranks"]["run_program_calls"] == 2 and cb["value"] > 0
     assert cb["cpu_model"]
+
+
+def test_gpus_n_self_launches_ranks_without_torchrun():
+    """``python bench.py --gpus 2`` with no WORLD_SIZE starts its own rank
+    processes (127.0.0.1 rendezvous), prints rank 0's one line, exits 0."""
+    import os
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--launch-probe"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d == {"probe": "ok", "world": 2, "sum": 3.0}
+
+
+def test_gpus_n_self_launch_propagates_rank_failure():
+    import os
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--launch-probe",
+                          "--launch-probe-fail", "1"], capture_output=True, text=True, timeout=300,
+                         cwd=ROOT, env=env)
+    assert out.returncode == 3

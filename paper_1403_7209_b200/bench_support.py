@@ -12,6 +12,7 @@
 from __future__ import annotations
 
 import json
+import os
 import statistics
 import subprocess
 import threading
@@ -21,7 +22,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 FALLBACK_PEAK_GBS = 6650.0
 
-__all__ = ["build_workload", "clock_sampler", "peaks_gbs", "ClockSampler", "load_reference",
+__all__ = ["stdout_to_stderr", "build_workload", "clock_sampler", "peaks_gbs", "ClockSampler", "load_reference",
            "cpu_model", "time_reference", "reference_modes"]
 
 
@@ -207,3 +208,25 @@ def time_reference(R, mesh, prog, mode: str, cores: int, runs: int = 1, warm: in
         for p in parts:
             R.run_program(p, ref, cfg)
     return (time.perf_counter() - t0) / runs, len(parts)
+
+
+class stdout_to_stderr:
+    """Route file descriptor 1 to stderr for the duration (NCCL and other
+    native libraries print banners on stdout, which must carry only the one
+    JSON bench line); ``write_line`` prints to the real stdout meanwhile."""
+
+    def __enter__(self):
+        import sys
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def write_line(self, text: str) -> None:
+        os.write(self.saved, (text + "\n").encode())
+
+    def __exit__(self, *exc):
+        import sys
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)

@@ -1291,12 +1291,19 @@ def bench_distributed(args, metric, emit: bool = True, with_e2e: bool = True):
     with CUDA events on each rank's compute stream, max over ranks.  ``e2e``:
     the same K runs through the host-resident path — every step uploads the
     rank's dats from pinned memory and downloads its owned rows of the written
-    dats and the global values (wall clock, max over ranks)."""
+    dats and the global values (wall clock, max over ranks).  Native banners
+    (NCCL) are kept off stdout, which carries only the JSON line."""
+    from .bench_support import stdout_to_stderr
+    with stdout_to_stderr() as out:
+        return _bench_distributed(args, metric, emit, with_e2e, out)
+
+
+def _bench_distributed(args, metric, emit, with_e2e, out):
     import json
     import torch
     import torch.distributed as dist
     import paper_1403_7209_b200 as ml
-    from . import _native as N
+    from . import _native as N  # noqa: F401
     from .bench_support import build_workload, clock_sampler, peaks_gbs
     from .device import pin_mesh
     rank, world, transport = init_distributed()
@@ -1418,7 +1425,7 @@ def bench_distributed(args, metric, emit: bool = True, with_e2e: bool = True):
         if not with_e2e:
             line["e2e"] = None
         if emit:
-            print(json.dumps(line), flush=True)
+            out.write_line(json.dumps(line))
     dist.barrier()
     dev.close()
     dist.destroy_process_group()

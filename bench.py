@@ -409,7 +409,7 @@ def main():
     ap.add_argument("--grid", type=int, default=None)
     ap.add_argument("--cpu-grid", type=int, default=None)
     ap.add_argument("--inc-schedule", default="tuned",
-                    choices=["tuned", "auto", "gather", "pfold", "tile", "tgather", "fold", "colour", "flow", "arrival"])
+                    choices=["tuned", "auto", "gather", "pfold", "colour"])
     ap.add_argument("--schedule-table", default=None,
                     help="per-loop INC schedules, e.g. vflux=pfold,iflux=gather (skips tuning)")
     ap.add_argument("--no-cpu", action="store_true")

@@ -51,7 +51,11 @@ typedef struct ml_arg {
     void *data;            /* device payload of the dat, or device global buffer  */
     const int32_t *map;    /* device map table, column-major int32 [arity][from]  */
     int64_t map_from;      /* from-set size of the map (column stride)            */
-    int64_t set_size;      /* size of the dat's set (SOA component stride)        */
+    int64_t set_size;      /* size of the dat's set                               */
+    int64_t pitch;         /* SOA component stride in elements of the device copy
+                              (>= set_size; the library pads it to 32 elements so
+                              every component row is 256-byte aligned); 0 means
+                              set_size                                            */
 } ml_arg_t;
 
 /* Device copy of an execution plan (plan.py:30-45).  `color_offsets` is a
@@ -64,47 +68,9 @@ typedef struct ml_plan_dev {
     const int32_t *blocks;          /* device: block ids ordered by colour      */
     const uint16_t *elem_color;     /* device [n]; NULL when no indirect writes */
     const int32_t *elem_ncolors;    /* device [nblocks]; NULL likewise          */
-    /* Optional dataflow schedule (ml_schedule_build): one persistent launch
-     * walks `queue`; a block writes back only after the earlier-queued blocks
-     * it conflicts with did (no inter-colour barriers).  NULL disables it. */
-    const int32_t *queue;           /* device [nblocks] block ids in queue order */
-    const int32_t *dep_off;         /* device [nblocks+1]                        */
-    const int32_t *dep_list;        /* device conflicting earlier-queued blocks  */
-    int32_t *flow_state;            /* device scratch [nblocks+1], zeroed per run */
 } ml_plan_dev_t;
 
-/* Shared-memory staging of indirect increments (optional; ngroups == 0 turns
- * it off).  A group is one dat written with INC through a map: per block the
- * sorted unique targets (`off`/`list`, from ml_staging_build) and, per INC
- * argument, the local position of each element's target (`loc`). */
 #define ML_MAX_ARGS 16
-#define ML_MAX_GROUPS 2
-typedef struct ml_staging_dev {
-    int32_t ngroups;
-    int32_t group[ML_MAX_ARGS];          /* group of each arg, -1 if not staged  */
-    const int32_t *off[ML_MAX_GROUPS];   /* device [nblocks+1]                    */
-    const int32_t *list[ML_MAX_GROUPS];  /* device unique targets                 */
-    int32_t umax[ML_MAX_GROUPS];         /* max unique targets in one block       */
-    const uint16_t *loc[ML_MAX_ARGS];    /* device [n] per staged arg             */
-    /* segmented mode (seg != 0): every (element, INC arg) owns a private
-     * shared-memory slot; per unique target, `toff` delimits its contributing
-     * slots in `src` (a*256 + element-in-block, element order), summed in that
-     * fixed order during the write-back — no element colour phases. */
-    int32_t seg;
-    const int32_t *toff[ML_MAX_GROUPS];  /* device [total+1]                      */
-    const uint16_t *src[ML_MAX_GROUPS];  /* device [n * args in group]            */
-    /* arrival mode (arrive != 0, needs seg): one launch over the blocks in
-     * natural order, no block colours.  A target touched by one block is
-     * updated directly; a shared target's per-block sums go to `partial` slots
-     * and the last block to arrive (atomic counter) adds them in block order —
-     * deterministic, no inter-block waiting.  Counters return to 0. */
-    int32_t arrive;
-    const int32_t *pslot[ML_MAX_GROUPS]; /* device [total]                        */
-    const int32_t *poff[ML_MAX_GROUPS];  /* device [targets]                      */
-    const int32_t *nblk[ML_MAX_GROUPS];  /* device [targets]                      */
-    int32_t *count[ML_MAX_GROUPS];       /* device [targets], zero between runs   */
-    void *partial[ML_MAX_GROUPS];        /* device [nslots][dim]                  */
-} ml_staging_dev_t;
 
 typedef struct ml_loop {
     const char *name;               /* for error messages                       */
@@ -116,7 +82,6 @@ typedef struct ml_loop {
     double fconst[4];               /* kernel constants (e.g. dt)               */
     int64_t iconst[4];              /* kernel constants (e.g. integer scale)    */
     void *scratch;                  /* device scratch >= ml_loop_scratch_bytes  */
-    ml_staging_dev_t staging;
     int64_t rlim;                   /* elements >= rlim skip global reductions
                                        (exec-halo elements on multi-GPU runs);
                                        < 0 means n                               */
@@ -137,32 +102,6 @@ typedef struct ml_loop {
     int64_t gather_nhub;
     const int32_t *gather_hub_tl;   /* device [nhub]                             */
     const int32_t *gather_hub_off;  /* device [nhub+1]                           */
-    void *fold_buf;                 /* fold schedule (needs the gather lists):
-                                       device [n][INC args][dim] increment slots;
-                                       NULL selects the gather schedule          */
-    /* tile schedule (ml_tile_build export, on the device); tile_count == 0
-     * disables it.  All indirect args must use one map; INC dats must not be
-     * accessed otherwise; no direct writes. */
-    int64_t tile_count;
-    int32_t tile_arity;             /* map arity (loc row length)                */
-    int32_t tile_umax;              /* max staged targets of a tile              */
-    int32_t tile_cmax;              /* max owned targets of a tile               */
-    int32_t tile_threads;           /* CTA size: 256 (2 CTAs/SM) or 128 (4/SM)   */
-    const int32_t *tile_list_off;   /* [tile_count+1]                            */
-    const int32_t *tile_nown;       /* [tile_count]                              */
-    const int32_t *tile_list;       /* staged targets, owned first               */
-    const int32_t *tile_elem_off;   /* [tile_count+1]                            */
-    const int32_t *tile_elem;       /* evaluated elements                        */
-    const int32_t *tile_ncol;       /* [tile_count] colours                      */
-    const uint16_t *tile_loc;       /* [elements][arity] local target indices    */
-    const uint8_t *tile_ecol;       /* colour | 0x80 reduction owner             */
-    /* tile-gather variant (non-NULL tile_inc_off selects it): one thread per
-     * owned target accumulates its incidences in element order from the
-     * staged rows (ml_tile_export_incidences) */
-    const int32_t *tile_inc_base;
-    const int32_t *tile_inc_off;
-    const uint16_t *tile_inc_k;
-    const uint8_t *tile_inc_c;
     /* primary-fold schedule (INC-only loops); pf_n1 == 0 disables it.  Per
      * target, CSRs of its incidences through the first INC argument
      * (pf_off1/pf_elem1) and through the others (pf_off2/pf_elem2/pf_pos2,
@@ -177,8 +116,6 @@ typedef struct ml_loop {
     void *pf_slots;
     const int32_t *pf_slotpos;      /* [n][INC args - 1]: slot row of each secondary
                                        increment = its index in pf_elem2 */
-    int32_t pf_own_kb;              /* shared memory (KB per CTA) for the targets'
-                                       own READ rows in pass 1; 0: read from L1/L2 */
     int32_t pf_ncol;                /* record width (distinct map columns)       */
     const int32_t *pf_rec;          /* optional [pass-1 incidences][pf_ncol]: the
                                        map entries of each incidence's element;
@@ -219,6 +156,13 @@ int ml_host_free(void *hptr);
 int ml_upload(void *dst, const void *src, uint64_t bytes);    /* H2D, stream-ordered */
 int ml_download(void *dst, const void *src, uint64_t bytes);  /* D2H, synchronous    */
 int ml_memset(void *dst, int value, uint64_t bytes);
+/* Pitched copies (rows of `width` bytes, `height` rows; host and device row
+ * pitches in bytes): a SOA dat's host payload [dim][set_size] to/from its
+ * device copy [dim][pitch].  Same stream behaviour as ml_upload/ml_download. */
+int ml_upload2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
+                uint64_t height);
+int ml_download2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
+                  uint64_t height);
 /* Copy engines for the host-resident path (streamed residency): H2D and D2H
  * run on their own streams so input uploads, loop execution and result
  * downloads overlap; ml_order(from, to) makes stream `to` wait for all work
@@ -226,6 +170,10 @@ int ml_memset(void *dst, int value, uint64_t bytes);
 enum { ML_STREAM_COMPUTE = 0, ML_STREAM_H2D = 1, ML_STREAM_D2H = 2 };
 int ml_copy_h2d(void *dst, const void *src, uint64_t bytes);
 int ml_copy_d2h(void *dst, const void *src, uint64_t bytes);
+int ml_copy_h2d_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
+                   uint64_t height);
+int ml_copy_d2h_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
+                   uint64_t height);
 int ml_order(int32_t from, int32_t to);
 int ml_sync_all(void);
 /* Upload an int64 0-based (rows, arity) row-major map table as the device's
@@ -248,20 +196,6 @@ int ml_plan_export(const ml_plan_t *p, int64_t *block_color, int64_t *elem_ncolo
                    int64_t *color_offsets, int64_t *blocks_by_color,
                    int64_t *elem_color, int64_t *block_elem_order);
 int ml_plan_free(ml_plan_t *p);
-/* Dataflow schedule of an indirect-write loop (csrc/host_schedule.cpp): a
- * block queue in (window, colour, index) order — windows of consecutive
- * blocks sized to the L2 — and, per block, the blocks sharing a write target
- * that precede it in the queue (its dependencies).  Export sizes: queue
- * [nblocks], dep_off [nblocks+1], dep_list [*ndeps]; *ndeps is -1 when a hub
- * target makes the lists quadratic (use per-colour launches instead). */
-typedef struct ml_schedule ml_schedule_t;
-int ml_schedule_build(int64_t n, int32_t ncols, const int64_t *const *cols, const int32_t *col_key,
-                      int64_t block_size, const int64_t *block_color, int32_t nwindows,
-                      ml_schedule_t **out);
-int ml_schedule_export(const ml_schedule_t *s, int64_t *ndeps, int32_t *queue, int32_t *dep_off,
-                       int32_t *dep_list);
-int ml_schedule_free(ml_schedule_t *s);
-
 /* Target-centric ("gather") schedule of a loop whose indirect writes all go to
  * one dat with one mode (INC, or WRITE): per target, its (element, argument
  * position) incidences in serial order (element, then argument) — the order
@@ -273,61 +207,6 @@ int ml_gather_build(int64_t n, int32_t ncols, const int64_t *const *cols, int64_
                     ml_gather_t **out);
 int ml_gather_export(const ml_gather_t *g, int32_t *off, int32_t *elem, uint8_t *pos);
 int ml_gather_free(ml_gather_t *g);
-
-/* Tile plan of an indirect-increment loop (csrc/host_tile.cpp; the B200
- * counterpart of OP2's locality blocking — plan.py:55-131 is the reference
- * plan, which this does not replace).  The target set is cut into compact
- * tiles; a tile owns its targets, evaluates every element that increments
- * one of them (elements on the cut are evaluated by both tiles, each keeping
- * its own targets' increments) and stages its owned + halo targets in shared
- * memory.  `table` is the loop's map, 0-based row-major [n][arity];
- * `inc_mask` bit c marks column c as INC-written; `red_col` is the column
- * whose owner counts the element in global reductions.  A tile satisfies
- * staged*stage_bytes + owned*own_bytes <= budget and owned <= cmax.  Tiles
- * come from recursive bisection of the targets along `coords` ([ntargets]
- * [cdim] row-major, e.g. the mesh's coordinate dat) or, when NULL, along
- * hop-distance pseudo-coordinates from three far-apart landmarks.
- * Fails (ML_EINVAL) when one target alone exceeds the budget or a tile needs
- * more than 127 colours (hub targets): use the gather schedule then.
- * Export sizes: list_off/elem_off [ntiles+1], nown/ncol [ntiles],
- * list [nlist], elem/ecol [nelem], loc [nelem*arity]. */
-typedef struct ml_tile ml_tile_t;
-int ml_tile_build(int64_t n, int32_t arity, const int64_t *table, int64_t ntargets,
-                  uint32_t inc_mask, int32_t red_col, int64_t stage_bytes, int64_t own_bytes,
-                  int64_t budget, int32_t cmax, const double *coords, int32_t cdim,
-                  ml_tile_t **out);
-int ml_tile_sizes(const ml_tile_t *t, int64_t *ntiles, int64_t *nlist, int64_t *nelem,
-                  int64_t *umax, int64_t *cmax, int64_t *emax, int32_t *maxcol);
-int ml_tile_export(const ml_tile_t *t, int32_t *list_off, int32_t *nown, int32_t *list,
-                   int32_t *elem_off, int32_t *elem, uint16_t *loc, uint8_t *ecol, int32_t *ncol);
-/* Per owned target of each tile, its incidences (element index within the
- * tile, map column) in element-then-column order (tile-gather variant).
- * Sizes: inc_base [ntiles] (start of the tile's rows in inc_off), inc_off
- * [sum(nown + 1)] (absolute offsets into inc_k/inc_c), inc_k/inc_c [*ninc];
- * pass NULL arrays to query *ninc. */
-int ml_tile_export_incidences(const ml_tile_t *t, int64_t *ninc, int32_t *inc_base, int32_t *inc_off,
-                              uint16_t *inc_k, uint8_t *inc_c);
-int ml_tile_free(ml_tile_t *t);
-
-/* Staging lists for shared-memory increment accumulation (derived from the
- * plan's blocking; the plan itself is unchanged).  `col_group[j]` assigns the
- * j-th INC column to a group (one group per INC dat). */
-typedef struct ml_staging ml_staging_t;
-int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols, const int64_t *const *cols,
-                     const int32_t *col_group, ml_staging_t **out);
-int ml_staging_sizes(const ml_staging_t *s, int32_t group, int64_t *total, int64_t *umax);
-int ml_staging_export(const ml_staging_t *s, int32_t group, int32_t *off, int32_t *list);
-int ml_staging_export_loc(const ml_staging_t *s, int32_t col, uint16_t *loc);
-/* Segmented-mode lists of a group: toff [total+1], src [*nrefs]. */
-int ml_staging_export_seg(const ml_staging_t *s, int32_t group, int64_t *nrefs, int32_t *toff,
-                          uint16_t *src);
-/* Arrival-mode lists of a group: per list entry the partial slot (-1 when the
- * block is the only one touching the target): pslot [total]; per target id:
- * first slot poff [*ntargets] and number of touching blocks nblk [*ntargets];
- * *nslots partial slots in all. */
-int ml_staging_export_arrival(const ml_staging_t *s, int32_t group, int64_t *ntargets,
-                              int64_t *nslots, int32_t *pslot, int32_t *poff, int32_t *nblk);
-int ml_staging_free(ml_staging_t *s);
 
 /* ---- renumbering: renumber.py:53-128 ------------------------------------- */
 /* Co-occurrence adjacency of a set from `nmaps` tables that target it

@@ -28,13 +28,10 @@ ML_STREAM_COMPUTE, ML_STREAM_H2D, ML_STREAM_D2H = 0, 1, 2
 EXPORTED = [
     "ml_last_error", "ml_version", "ml_init", "ml_device_info", "ml_synchronize",
     "ml_alloc", "ml_free", "ml_host_alloc", "ml_host_free", "ml_upload", "ml_download",
-    "ml_memset", "ml_map_upload", "ml_copy_h2d", "ml_copy_d2h", "ml_order", "ml_sync_all",
+    "ml_memset", "ml_upload2d", "ml_download2d", "ml_map_upload", "ml_copy_h2d", "ml_copy_d2h",
+    "ml_copy_h2d_2d", "ml_copy_d2h_2d", "ml_order", "ml_sync_all",
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
-    "ml_schedule_build", "ml_schedule_export", "ml_schedule_free",
     "ml_gather_build", "ml_gather_export", "ml_gather_free",
-    "ml_tile_build", "ml_tile_sizes", "ml_tile_export", "ml_tile_export_incidences", "ml_tile_free",
-    "ml_staging_build", "ml_staging_sizes", "ml_staging_export", "ml_staging_export_loc",
-    "ml_staging_export_seg", "ml_staging_export_arrival", "ml_staging_free",
     "ml_co_occurrence", "ml_cm_order",
     "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name", "ml_chain_lookup",
     "ml_loop_scratch_bytes", "ml_loop_run", "ml_loop_pfold_slot_bytes",
@@ -51,55 +48,33 @@ class MlArg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("mode", C.c_int32), ("dim", C.c_int32),
                 ("dtype", C.c_int32), ("layout", C.c_int32), ("slot", C.c_int32),
                 ("data", C.c_void_p), ("map", C.c_void_p), ("map_from", C.c_int64),
-                ("set_size", C.c_int64)]
+                ("set_size", C.c_int64), ("pitch", C.c_int64)]
 
 
 class MlPlanDev(C.Structure):
     _fields_ = [("nblocks", C.c_int64), ("ncolors", C.c_int64), ("block_size", C.c_int64),
                 ("color_offsets", C.POINTER(C.c_int64)), ("blocks", C.c_void_p),
-                ("elem_color", C.c_void_p), ("elem_ncolors", C.c_void_p),
-                ("queue", C.c_void_p), ("dep_off", C.c_void_p), ("dep_list", C.c_void_p),
-                ("flow_state", C.c_void_p)]
+                ("elem_color", C.c_void_p), ("elem_ncolors", C.c_void_p)]
 
 
-MAX_ARGS, MAX_GROUPS = 16, 2
-
-
-class MlStagingDev(C.Structure):
-    _fields_ = [("ngroups", C.c_int32), ("group", C.c_int32 * MAX_ARGS),
-                ("off", C.c_void_p * MAX_GROUPS), ("list", C.c_void_p * MAX_GROUPS),
-                ("umax", C.c_int32 * MAX_GROUPS), ("loc", C.c_void_p * MAX_ARGS),
-                ("seg", C.c_int32), ("toff", C.c_void_p * MAX_GROUPS),
-                ("src", C.c_void_p * MAX_GROUPS), ("arrive", C.c_int32),
-                ("pslot", C.c_void_p * MAX_GROUPS), ("poff", C.c_void_p * MAX_GROUPS),
-                ("nblk", C.c_void_p * MAX_GROUPS), ("count", C.c_void_p * MAX_GROUPS),
-                ("partial", C.c_void_p * MAX_GROUPS)]
+MAX_ARGS = 16
 
 
 class MlLoop(C.Structure):
     _fields_ = [("name", C.c_char_p), ("functor", C.c_int32), ("nargs", C.c_int32),
                 ("args", C.POINTER(MlArg)), ("n", C.c_int64), ("plan", MlPlanDev),
                 ("fconst", C.c_double * 4), ("iconst", C.c_int64 * 4), ("scratch", C.c_void_p),
-                ("staging", MlStagingDev), ("rlim", C.c_int64),
+                ("rlim", C.c_int64),
                 ("gather_ntargets", C.c_int64), ("gather_off", C.c_void_p),
                 ("gather_elem", C.c_void_p), ("gather_pos", C.c_void_p),
                 ("gather_targets", C.c_void_p),
                 ("gather_seg", C.c_void_p), ("gather_part", C.c_void_p), ("gather_nhub", C.c_int64),
                 ("gather_hub_tl", C.c_void_p), ("gather_hub_off", C.c_void_p),
-                ("fold_buf", C.c_void_p),
-                ("tile_count", C.c_int64), ("tile_arity", C.c_int32), ("tile_umax", C.c_int32),
-                ("tile_cmax", C.c_int32), ("tile_threads", C.c_int32),
-                ("tile_list_off", C.c_void_p), ("tile_nown", C.c_void_p),
-                ("tile_list", C.c_void_p), ("tile_elem_off", C.c_void_p),
-                ("tile_elem", C.c_void_p), ("tile_ncol", C.c_void_p),
-                ("tile_loc", C.c_void_p), ("tile_ecol", C.c_void_p),
-                ("tile_inc_base", C.c_void_p), ("tile_inc_off", C.c_void_p),
-                ("tile_inc_k", C.c_void_p), ("tile_inc_c", C.c_void_p),
                 ("pf_n1", C.c_int64), ("pf_off1", C.c_void_p), ("pf_elem1", C.c_void_p),
                 ("pf_tl1", C.c_void_p), ("pf_n2", C.c_int64), ("pf_off2", C.c_void_p),
                 ("pf_elem2", C.c_void_p), ("pf_tl2", C.c_void_p), ("pf_pos2", C.c_void_p),
                 ("pf_slots", C.c_void_p), ("pf_slotpos", C.c_void_p),
-                ("pf_own_kb", C.c_int32), ("pf_ncol", C.c_int32), ("pf_rec", C.c_void_p),
+                ("pf_ncol", C.c_int32), ("pf_rec", C.c_void_p),
                 ("pf_rcol", C.c_int8 * 16),
                 ("pf_seg1", C.c_void_p), ("pf_seg2", C.c_void_p), ("pf_part1", C.c_void_p),
                 ("pf_part2", C.c_void_p), ("pf_nhub1", C.c_int64), ("pf_nhub2", C.c_int64),
@@ -130,6 +105,10 @@ _SIGNATURES = {
     "ml_upload": (C.c_int, [_P, _P, C.c_uint64]),
     "ml_download": (C.c_int, [_P, _P, C.c_uint64]),
     "ml_memset": (C.c_int, [_P, C.c_int, C.c_uint64]),
+    "ml_upload2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "ml_download2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "ml_copy_h2d_2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "ml_copy_d2h_2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ml_map_upload": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
     "ml_copy_h2d": (C.c_int, [_P, _P, C.c_uint64]),
     "ml_copy_d2h": (C.c_int, [_P, _P, C.c_uint64]),
@@ -139,26 +118,9 @@ _SIGNATURES = {
     "ml_plan_sizes": (C.c_int, [_P, _I64P, _I64P, _I64P]),
     "ml_plan_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "ml_plan_free": (C.c_int, [_P]),
-    "ml_schedule_build": (C.c_int, [C.c_int64, C.c_int32, _PP, _I32P, C.c_int64, _P, C.c_int32,
-                                    _PP]),
-    "ml_schedule_export": (C.c_int, [_P, _I64P, _P, _P, _P]),
-    "ml_schedule_free": (C.c_int, [_P]),
     "ml_gather_build": (C.c_int, [C.c_int64, C.c_int32, _PP, C.c_int64, _PP]),
     "ml_gather_export": (C.c_int, [_P, _P, _P, _P]),
     "ml_gather_free": (C.c_int, [_P]),
-    "ml_tile_build": (C.c_int, [C.c_int64, C.c_int32, _P, C.c_int64, C.c_uint32, C.c_int32,
-                                C.c_int64, C.c_int64, C.c_int64, C.c_int32, _P, C.c_int32, _PP]),
-    "ml_tile_sizes": (C.c_int, [_P, _I64P, _I64P, _I64P, _I64P, _I64P, _I64P, _I32P]),
-    "ml_tile_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "ml_tile_export_incidences": (C.c_int, [_P, _I64P, _P, _P, _P, _P]),
-    "ml_tile_free": (C.c_int, [_P]),
-    "ml_staging_build": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, _PP, _I32P, _PP]),
-    "ml_staging_sizes": (C.c_int, [_P, C.c_int32, _I64P, _I64P]),
-    "ml_staging_export": (C.c_int, [_P, C.c_int32, _P, _P]),
-    "ml_staging_export_loc": (C.c_int, [_P, C.c_int32, _P]),
-    "ml_staging_export_seg": (C.c_int, [_P, C.c_int32, _I64P, _P, _P]),
-    "ml_staging_export_arrival": (C.c_int, [_P, C.c_int32, _I64P, _I64P, _P, _P, _P]),
-    "ml_staging_free": (C.c_int, [_P]),
     "ml_co_occurrence": (C.c_int, [C.c_int64, C.c_int32, _PP, _I64P, _I32P, _P, _P, _I64P]),
     "ml_cm_order": (C.c_int, [C.c_int64, _P, _P, _P]),
     "ml_functor_lookup": (C.c_int, [C.c_char_p, C.c_int32, _I32P]),

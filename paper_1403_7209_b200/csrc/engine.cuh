@@ -5,27 +5,43 @@
 //
 // A functor declares its argument signature (kind, access mode, dim, type)
 // and a device `apply(consts, view0, view1, ...)`.  Views are
-//   * Ref<T>/Ref<const T>  — strided references straight into HBM for
+//   * Ref<T>/RefA<T>  — strided / contiguous references straight into HBM for
 //     direct args, indirect READ args and (phased mode) indirect WRITE/RW
 //     args; loads are issued at first use, so the compiler schedules them
 //     and register pressure stays bounded for wide dats;
-//   * T*                   — a register array: increments of an indirect INC
-//     argument (applied colour by colour after the element is computed) and
-//     global INC/MIN/MAX accumulators (block-reduced afterwards).
+//   * T*              — a register array: increments of an indirect INC
+//     argument, the running value of a gathered target, global INC/MIN/MAX
+//     accumulators (block-reduced afterwards), and the two elements' rows a
+//     thread of a vectorised direct loop owns.
 //
-// Kernels
-//   k_direct  — loops without indirect writes: one launch over all plan
-//               blocks, per-block reduction partials.
-//   k_staged  — loops whose only indirect writes are INC and bs <= blockDim:
-//               every thread computes its element at once, then element
-//               colour phases (separated by __syncthreads) apply the
-//               register increments with plain read-modify-write.  One
-//               launch per block colour; blocks of one colour share no
-//               target, so no atomics are needed and the result is
-//               deterministic run to run.
-//   k_phased  — general case (indirect WRITE/RW, or bs > blockDim): each
-//               element executes entirely inside its colour phase.
-// Global reductions: warp shuffle -> shared -> one partial per plan block;
+// Layout policy (template parameter LP of every hot kernel).  LP = 0 reads
+// each argument's strides at run time (element stride `se`, component stride
+// `sc`: any AOS/SOA mix).  LP = 1 is the reference's default auto-SOA policy
+// (core.py:403-404, threshold 4) fixed at compile time: a dat of dim <= 4 is
+// AOS (se = dim, sc = 1: component offsets are immediates), wider dats SOA
+// (se = 1, sc = the device pitch, a uniform value).  The runtime picks LP = 1
+// when the loop's dats follow that policy — the common case — which removes
+// the 64-bit stride arithmetic from every gathered load.
+//
+// Kernels (selected by runtime.cu enqueue_loop)
+//   k_direct   — loops without indirect writes: persistent grid; with LP = 1
+//                each thread owns two consecutive elements and moves their
+//                direct rows with 16-byte loads/stores (north_star: coalesced
+//                128-bit direct access).
+//   k_gather   — target-centric INC-only or WRITE-only loops: one thread per
+//                target re-evaluates the kernel for each incidence in serial
+//                order (bitwise the serial result); hub targets split in rows
+//                (k_gather_hubs folds them).
+//   k_pfold1 + k_pfold_rest_w — primary fold for INC-only loops: each element
+//                evaluated once by the owner of its first INC target; the other
+//                increments through slots folded in element order (pass 2).
+//   k_staged   — reference plan colours (one launch per block colour), INC
+//                increments staged in registers and applied in element-colour
+//                phases (run_threads, and loops the target-centric schedules
+//                do not cover).
+//   k_phased   — general colour schedule (indirect WRITE/RW): each element runs
+//                entirely inside its colour phase.
+// Global reductions: warp shuffle -> shared -> one partial per CTA;
 // k_combine folds the partials in a fixed order onto the initial value.
 #pragma once
 
@@ -42,6 +58,7 @@ namespace ml {
 enum : int { KD = 0, KI = 1, KG = 2 };                        // direct / indirect / global
 enum : int { MR = 0, MW = 1, MRW = 2, MINC = 3, MMIN = 4, MMAX = 5 };
 constexpr int MAX_ARGS = 16;
+constexpr int AUTO_SOA_DIM = 4;    // reference Mesh(auto_soa_threshold=4): dim > 4 is SOA
 
 // Programmatic dependent launch: the hot kernels are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs can
@@ -50,7 +67,6 @@ constexpr int MAX_ARGS = 16;
 // before touching any data.  Without the attribute the wait is a no-op.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool pdl_enabled();
-bool pass2_warp();
 
 template <class... KArgs, class... Args>
 inline void launch_k(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args &&...args) {
@@ -96,55 +112,6 @@ struct Consts {
     int64_t i[4];
 };
 
-constexpr int MAX_GROUPS = 2;
-
-// Shared-memory staging of indirect increments (OP2-style): per block, the
-// sorted unique targets of each INC dat ("group") and, per element and INC
-// argument, the target's position in that list.
-struct Staging {
-    int32_t group[MAX_ARGS];             // staging group of each arg (-1: none)
-    int32_t leader[MAX_ARGS];            // 1 on the arg that writes its group back
-    const int32_t *off[MAX_GROUPS];      // [nblocks+1] offsets into list
-    const int32_t *list[MAX_GROUPS];     // unique targets, ascending per block
-    const uint16_t *loc[MAX_ARGS];       // [n] local position of the arg's target
-    int32_t umax[MAX_GROUPS];            // max unique targets per block (smem stride)
-    int32_t soff[MAX_GROUPS];            // byte offset of the group in dynamic smem
-    // segmented mode: private slot per (element, INC arg); per unique target the
-    // contributing slots in element order (src = arg position * 256 + element)
-    const int32_t *toff[MAX_GROUPS];     // [total+1] into src (global target index)
-    const uint16_t *src[MAX_GROUPS];
-    int32_t gpos[MAX_ARGS];              // position of the arg inside its group
-    // arrival mode: shared targets go through per-block partial slots; the last
-    // block to arrive (atomic counter) folds them in block order
-    const int32_t *pslot[MAX_GROUPS];    // [total] partial slot per list entry (-1: sole block)
-    const int32_t *poff[MAX_GROUPS];     // [targets] first slot of a shared target
-    const int32_t *nblk[MAX_GROUPS];     // [targets] blocks touching the target
-    int32_t *count[MAX_GROUPS];          // [targets] arrivals (back to 0 after each run)
-    void *partial[MAX_GROUPS];           // [slots][dim]
-    int32_t foff[MAX_GROUPS];            // byte offset of the finaliser list in dynamic smem
-};
-
-// Tile schedule (csrc/host_tile.cpp): per tile, the staged target list (owned
-// first), the elements it evaluates with their local target indices per map
-// column, element colours (bit 7: reduction owner) and the colour count.
-constexpr int MAX_TGROUPS = 8;
-struct TileParams {
-    const int32_t *list_off, *nown, *list, *elem_off, *elem, *ncol;
-    const uint16_t *loc;
-    const uint8_t *ecol;
-    int32_t arity;
-    int32_t nread, ninc;                 // staged READ dats, accumulated INC dats
-    int32_t garg[MAX_TGROUPS];           // an argument of each group (read groups, then INC)
-    int32_t gdim[MAX_TGROUPS];           // components of each group's dat
-    int8_t grp[MAX_ARGS];                // group of each indirect argument
-    int8_t slot[MAX_ARGS];               // map column of each indirect argument
-    // tile-gather variant: per owned target, (element-in-tile, column) incidences
-    const int32_t *inc_base, *inc_off;
-    const uint16_t *inc_k;
-    const uint8_t *inc_c;
-    int32_t red_col;                     // column whose incidence counts the element in reductions
-};
-
 // Primary-fold schedule (INC-only loops): pass 1 gives each target the elements
 // whose FIRST INC argument targets it; each element is evaluated once there,
 // its first increment accumulated in the thread's registers and the others
@@ -158,11 +125,6 @@ struct PFoldParams {
     void *slots;                         // [secondary incidences][dgp], in off2 order
     const int32_t *slotpos;              // [n][nslot]: slot row of (element, INC position >= 1)
     int32_t nslot, dgp;
-    // own-row staging: READ dats read through the first INC argument's column
-    // (the target itself) are copied once per target to shared memory
-    int32_t own_ngrp;
-    int32_t own_garg[MAX_TGROUPS], own_gdim[MAX_TGROUPS], own_goff[MAX_TGROUPS];
-    int8_t own_grp[MAX_ARGS];
     // element records: per pass-1 incidence k, the map entries of its element
     // for each distinct (map, column) the loop uses — [n1 incidences][ncol];
     // rcol: record column of each indirect argument.  The rows' addresses then
@@ -181,15 +143,10 @@ struct PFoldParams {
 struct LaunchParams {
     ArgRt a[MAX_ARGS];
     void *part[MAX_ARGS];       // reduction partials [nblocks][dim] per global reduce arg
-    Staging st;
     int64_t n;
     int64_t rlim;               // elements >= rlim do not contribute to reductions
     int32_t bs;
-    const int32_t *blocks;      // block ids of this launch (nullptr: identity)
-    const int32_t *dep_off;     // dataflow: per block, lower-colour conflicting blocks
-    const int32_t *dep_list;
-    int32_t *flags;             // dataflow: [nblocks] done flags + queue counter at [nblocks]
-    int32_t nqueue;             // dataflow: number of blocks in the queue
+    const int32_t *blocks;      // block ids of this launch (colour schedules)
     const uint16_t *ecol;       // element colours
     const int32_t *encol;       // per-block element colour count
     Consts k;
@@ -207,20 +164,41 @@ struct LaunchParams {
     void *g_part;
     int64_t g_nhub;
     const int32_t *g_hub_tl, *g_hub_off;
-    // fold schedule: per (element, INC-arg position) increment slots, element-major
-    void *g_buf;
-    int32_t g_nw;               // INC arguments per element
-    TileParams t;
     PFoldParams pf;
 };
 
-// strided view of one element's components
+// ---- views ----------------------------------------------------------------------------
+// strided view of one element's components (runtime or SOA component stride)
 template <class T>
 struct Ref {
     T *p;
     int64_t sc;
     __device__ __forceinline__ T &operator[](int c) const { return p[c * sc]; }
 };
+// contiguous view (AOS with a compile-time layout): component offsets are immediates
+template <class T>
+struct RefA {
+    T *p;
+    __device__ __forceinline__ T &operator[](int c) const { return p[c]; }
+};
+
+// layout class of argument A under policy LP: 0 runtime strides, 1 AOS (se =
+// dim, sc = 1), 2 SOA (se = 1, sc = runtime pitch)
+template <class A, int LP>
+__host__ __device__ constexpr int lay_of() {
+    return (LP == 0 || A::kind == KG) ? 0 : (A::dim <= AUTO_SOA_DIM ? 1 : 2);
+}
+template <class A, int L>
+__device__ __forceinline__ int64_t se_of(const ArgRt &r) {
+    if constexpr (L == 1) return A::dim;
+    else if constexpr (L == 2) return 1;
+    else return r.se;
+}
+template <class A, int L>
+__device__ __forceinline__ int64_t sc_of(const ArgRt &r) {
+    if constexpr (L == 1) return 1;
+    else return r.sc;
+}
 
 template <class T, int M>
 __device__ __forceinline__ T reduce_identity() {
@@ -240,36 +218,44 @@ __device__ __forceinline__ T combine(T a, T b) {
     return a + b;
 }
 
-// ---- per-argument slot --------------------------------------------------------
-// MODE 0: no staging (views into HBM); 1: indirect INC staged in registers and
-// applied to HBM in colour phases; 2: staged in registers, applied to shared
-// memory in colour phases, written back once per block.
-// MODE 3 (ST_SEG): the functor increments a private shared-memory slot of its
-// own (no registers held, no phases); the write-back sums each target's slots
-// in element order — a deterministic segmented reduction.
-// MODE 4 (ST_GATHER): target-centric schedule — INC and WRITE indirect args
-// are staged in registers (zero-initialised); the kernel keeps one of them.
-// MODE 5 (ST_TILE): tile schedule — indirect READ args view the tile's staged
-// copy in shared memory, INC args are staged in registers and added in colour
-// phases to the tile's shared-memory accumulators of owned targets (increments
-// of targets owned by another tile are dropped: that tile evaluates the
-// element too).
-enum : int { ST_NONE = 0, ST_REG = 1, ST_SMEM = 2, ST_SEG = 3, ST_GATHER = 4, ST_TILE = 5 };
+// 16-byte moves of two consecutive 8-byte values (16-byte aligned)
+template <class T>
+__device__ __forceinline__ void ld2(const T *p, T &a, T &b) {
+    if constexpr (cuda::std::is_same_v<T, double>) {
+        const double2 v = *reinterpret_cast<const double2 *>(p);
+        a = v.x;
+        b = v.y;
+    } else {
+        const longlong2 v = *reinterpret_cast<const longlong2 *>(p);
+        a = T(v.x);
+        b = T(v.y);
+    }
+}
+template <class T>
+__device__ __forceinline__ void st2(T *p, T a, T b) {
+    if constexpr (cuda::std::is_same_v<T, double>) *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+    else *reinterpret_cast<longlong2 *>(p) = make_longlong2(static_cast<long long>(a), static_cast<long long>(b));
+}
 
-template <class A, int MODE>
+// ---- per-argument slot ------------------------------------------------------------
+// MODE ST_NONE: views into HBM; ST_REG: indirect INC staged in registers and
+// applied to HBM in colour phases; ST_GATHER: INC and WRITE indirect args
+// staged in registers (zero-initialised); the target-centric kernels keep one.
+enum : int { ST_NONE = 0, ST_REG = 1, ST_GATHER = 2 };
+
+template <class A, int MODE, int L>
 struct Slot {
     using T = typename A::type;
     static constexpr bool is_global = A::kind == KG;
     static constexpr bool is_reduce = is_global && A::mode != MR;
     static constexpr bool is_inc = A::kind == KI && A::mode == MINC;
-    static constexpr bool seg = is_inc && MODE == ST_SEG;
     static constexpr bool is_ind_write = A::kind == KI && A::mode == MW;
-    static constexpr bool staged = (is_inc && MODE != ST_NONE && MODE != ST_SEG) || is_reduce ||
+    static constexpr bool staged = (is_inc && MODE != ST_NONE) || is_reduce ||
                                    (is_ind_write && MODE == ST_GATHER);
 
     T acc[staged ? A::dim : 1];
     T bak[is_reduce ? A::dim : 1];
-    T *ptr;          // element base pointer (HBM or shared memory)
+    T *ptr;          // element base pointer
     int64_t sc;
 
     __device__ __forceinline__ void init_global(const LaunchParams &p, int i) {
@@ -281,75 +267,30 @@ struct Slot {
             sc = 1;
         }
     }
-    __device__ __forceinline__ void init_elem(const LaunchParams &p, int i, int64_t e, char *smem) {
+    __device__ __forceinline__ void bind(const ArgRt &r, int64_t t) {
+        ptr = static_cast<T *>(r.data) + t * se_of<A, L>(r);
+        sc = sc_of<A, L>(r);
+        if constexpr (staged) {
+#pragma unroll
+            for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
+        }
+    }
+    __device__ __forceinline__ void init_elem(const LaunchParams &p, int i, int64_t e) {
         if constexpr (!is_global) {
-            if constexpr (is_inc && MODE == ST_SMEM) {
-                const int g = p.st.group[i];
-                ptr = reinterpret_cast<T *>(smem + p.st.soff[g]) + __ldg(p.st.loc[i] + e);
-                sc = p.st.umax[g];
-            } else if constexpr (seg) {
-                const int g = p.st.group[i];
-                ptr = reinterpret_cast<T *>(smem + p.st.soff[g]) +
-                      int64_t(p.st.gpos[i]) * A::dim * blockDim.x + threadIdx.x;
-                sc = blockDim.x;
-#pragma unroll
-                for (int c = 0; c < A::dim; ++c) ptr[c * sc] = T(0);
-            } else {
-                const ArgRt &r = p.a[i];
-                const int64_t t = A::kind == KI ? int64_t(__ldg(r.map + e)) : e;
-                ptr = static_cast<T *>(r.data) + t * r.se;
-                sc = r.sc;
-            }
-            if constexpr (staged) {
-#pragma unroll
-                for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
-            }
+            const ArgRt &r = p.a[i];
+            bind(r, A::kind == KI ? int64_t(__ldg(r.map + e)) : e);
         }
     }
     // pass-1 element record (PFoldParams::rec): indirect targets from the record
     __device__ __forceinline__ void init_elem_rec(const LaunchParams &p, int i, int64_t e, const int32_t *rk) {
-        if constexpr (!is_global) {
-            const ArgRt &r = p.a[i];
-            const int64_t t = A::kind == KI ? int64_t(__ldg(rk + p.pf.rcol[i])) : e;
-            ptr = static_cast<T *>(r.data) + t * r.se;
-            sc = r.sc;
-            if constexpr (staged) {
-#pragma unroll
-                for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
-            }
-        }
-    }
-    // gather schedule with CTA-local staging: READ args whose target lies in
-    // the CTA's range [t0, t0 + blockDim) read the staged copy
-    // tile schedule: `gb` are the group bases in shared memory, U the staged
-    // count (component stride of READ copies), C the owned count
-    __device__ __forceinline__ void init_tile(const LaunchParams &p, int i, int64_t e, const uint16_t *locs,
-                                              char *const *gb, int U, int C) {
-        if constexpr (!is_global) {
-            if constexpr (A::kind == KI) {
-                const int l = locs[p.t.slot[i]];
-                T *base = reinterpret_cast<T *>(gb[p.t.grp[i]]);
-                if constexpr (is_inc) {
-                    ptr = l < C ? base + l : nullptr;
-                    sc = C;
-                } else {
-                    ptr = base + l;
-                    sc = U;
-                }
-            } else {
-                const ArgRt &r = p.a[i];
-                ptr = static_cast<T *>(r.data) + e * r.se;
-                sc = r.sc;
-            }
-            if constexpr (staged) {
-#pragma unroll
-                for (int c = 0; c < A::dim; ++c) acc[c] = T(0);
-            }
-        }
+        if constexpr (!is_global) bind(p.a[i], A::kind == KI ? int64_t(__ldg(rk + p.pf.rcol[i])) : e);
     }
     __device__ __forceinline__ auto view() {
         if constexpr (staged) {
             return static_cast<T *>(acc);
+        } else if constexpr (L == 1) {
+            if constexpr (A::mode == MR) return RefA<const T>{ptr};
+            else return RefA<T>{ptr};
         } else if constexpr (A::mode == MR) {
             return Ref<const T>{ptr, sc};
         } else {
@@ -358,8 +299,6 @@ struct Slot {
     }
     __device__ __forceinline__ void apply_staged() {
         if constexpr (staged && !is_global) {
-            if constexpr (MODE == ST_TILE)
-                if (!ptr) return;
             // the components are distinct addresses: issue every load before
             // the first store so the read-modify-writes overlap
             T old[A::dim];
@@ -379,165 +318,6 @@ struct Slot {
         if constexpr (is_reduce) {
 #pragma unroll
             for (int c = 0; c < A::dim; ++c) acc[c] = bak[c];
-        }
-    }
-    // shared memory -> HBM, once per block (MODE 2, group leader only)
-    __device__ __forceinline__ void zero_smem(const LaunchParams &p, int i, int32_t b, char *smem) {
-        if constexpr (is_inc && MODE == ST_SMEM) {
-            const int g = p.st.group[i];
-            if (!p.st.leader[i]) return;
-            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo, um = p.st.umax[g];
-            T *s = reinterpret_cast<T *>(smem + p.st.soff[g]);
-            for (int k = threadIdx.x; k < u * A::dim; k += blockDim.x) s[(k / u) * um + (k % u)] = T(0);
-        }
-    }
-    __device__ __forceinline__ void write_back(const LaunchParams &p, int i, int32_t b, char *smem) {
-        if constexpr (is_inc && MODE == ST_SMEM) {
-            const int g = p.st.group[i];
-            if (!p.st.leader[i]) return;
-            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo, um = p.st.umax[g];
-            const T *s = reinterpret_cast<const T *>(smem + p.st.soff[g]);
-            const int32_t *__restrict__ list = p.st.list[g] + lo;
-            const ArgRt &r = p.a[i];
-            T *d = static_cast<T *>(r.data);
-            const int total = u * A::dim;
-            const bool aos = r.sc == 1 && A::dim > 1;   // AOS: component-fastest is contiguous
-            constexpr int U = 4;
-            for (int k0 = threadIdx.x; k0 < total; k0 += U * blockDim.x) {
-                int64_t addr[U];
-                T val[U];
-#pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const int k = k0 + q * blockDim.x;
-                    if (k < total) {
-                        const int c = aos ? k % A::dim : k / u, j = aos ? k / A::dim : k % u;
-                        addr[q] = int64_t(__ldg(list + j)) * r.se + c * r.sc;
-                        val[q] = s[c * um + j];
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < U; ++q)
-                    if (k0 + q * blockDim.x < total) val[q] += __ldcg(d + addr[q]);
-#pragma unroll
-                for (int q = 0; q < U; ++q)
-                    if (k0 + q * blockDim.x < total) d[addr[q]] = val[q];
-            }
-        } else if constexpr (seg) {
-            const int g = p.st.group[i];
-            if (!p.st.leader[i]) return;
-            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo;
-            const T *s = reinterpret_cast<const T *>(smem + p.st.soff[g]);
-            const int32_t *__restrict__ list = p.st.list[g] + lo;
-            const int32_t *__restrict__ toff = p.st.toff[g] + lo;
-            const uint16_t *__restrict__ src = p.st.src[g];
-            const ArgRt &r = p.a[i];
-            T *d = static_cast<T *>(r.data);
-            const int total = u * A::dim, nt = blockDim.x;
-            const bool aos = r.sc == 1 && A::dim > 1;
-            constexpr int U = 4;
-            for (int k0 = threadIdx.x; k0 < total; k0 += U * nt) {
-                int64_t addr[U];
-                T val[U];
-#pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const int k = k0 + q * nt;
-                    if (k < total) {
-                        const int c = aos ? k % A::dim : k / u, j = aos ? k / A::dim : k % u;
-                        addr[q] = int64_t(__ldg(list + j)) * r.se + c * r.sc;
-                        T acc = T(0);
-                        for (int m = __ldg(toff + j), me = __ldg(toff + j + 1); m < me; ++m) {
-                            const int v = __ldg(src + m);
-                            acc += s[((v >> 8) * A::dim + c) * nt + (v & 255)];
-                        }
-                        val[q] = acc;
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < U; ++q)
-                    if (k0 + q * nt < total) val[q] = __ldcg(d + addr[q]) + val[q];
-#pragma unroll
-                for (int q = 0; q < U; ++q)
-                    if (k0 + q * nt < total) d[addr[q]] = val[q];
-            }
-        }
-    }
-
-    // ---- arrival mode (segmented slots, no block colours) ------------------------
-    // phase 1: per (target, component) fold this block's slots in element order;
-    // a target owned by this block alone is updated in HBM, a shared one writes
-    // its block sum into the target's partial slot for this block.
-    __device__ __forceinline__ void arrive_sums(const LaunchParams &p, int i, int32_t b, char *smem) {
-        if constexpr (seg) {
-            const int g = p.st.group[i];
-            if (!p.st.leader[i]) return;
-            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo;
-            const T *s = reinterpret_cast<const T *>(smem + p.st.soff[g]);
-            const int32_t *__restrict__ list = p.st.list[g] + lo;
-            const int32_t *__restrict__ toff = p.st.toff[g] + lo;
-            const int32_t *__restrict__ pslot = p.st.pslot[g] + lo;
-            const uint16_t *__restrict__ src = p.st.src[g];
-            T *part = static_cast<T *>(p.st.partial[g]);
-            const ArgRt &r = p.a[i];
-            T *d = static_cast<T *>(r.data);
-            const int total = u * A::dim, nt = blockDim.x;
-            const bool aos = r.sc == 1 && A::dim > 1;
-            for (int k = threadIdx.x; k < total; k += nt) {
-                const int c = aos ? k % A::dim : k / u, j = aos ? k / A::dim : k % u;
-                T acc = T(0);
-                for (int m = __ldg(toff + j), me = __ldg(toff + j + 1); m < me; ++m) {
-                    const int v = __ldg(src + m);
-                    acc += s[((v >> 8) * A::dim + c) * nt + (v & 255)];
-                }
-                const int32_t ps = __ldg(pslot + j);
-                if (ps < 0) {
-                    const int64_t a = int64_t(__ldg(list + j)) * r.se + c * r.sc;
-                    d[a] = __ldcg(d + a) + acc;
-                } else {
-                    __stcg(part + int64_t(ps) * A::dim + c, acc);
-                }
-            }
-        }
-    }
-    // phase 2 (after a fence + barrier): count this block's arrival at every
-    // shared target; the last arriver queues the target for finalisation and
-    // resets its counter for the next run.
-    __device__ __forceinline__ void arrive_count(const LaunchParams &p, int i, int32_t b, char *smem,
-                                                 int *nfin) {
-        if constexpr (seg) {
-            const int g = p.st.group[i];
-            if (!p.st.leader[i]) return;
-            const int32_t lo = p.st.off[g][b], u = p.st.off[g][b + 1] - lo;
-            int32_t *fin = reinterpret_cast<int32_t *>(smem + p.st.foff[g]);
-            for (int j = threadIdx.x; j < u; j += blockDim.x) {
-                if (__ldg(p.st.pslot[g] + lo + j) < 0) continue;
-                const int32_t t = __ldg(p.st.list[g] + lo + j);
-                const int32_t need = __ldg(p.st.nblk[g] + t);
-                if (atomicAdd(p.st.count[g] + t, 1) == need - 1) {
-                    p.st.count[g][t] = 0;
-                    fin[atomicAdd(nfin + g, 1)] = t;
-                }
-            }
-        }
-    }
-    // phase 3: fold the partial slots of finalised targets in block order
-    __device__ __forceinline__ void arrive_final(const LaunchParams &p, int i, char *smem, const int *nfin) {
-        if constexpr (seg) {
-            const int g = p.st.group[i];
-            if (!p.st.leader[i]) return;
-            const int nf = nfin[g];
-            const int32_t *fin = reinterpret_cast<const int32_t *>(smem + p.st.foff[g]);
-            const T *part = static_cast<const T *>(p.st.partial[g]);
-            const ArgRt &r = p.a[i];
-            T *d = static_cast<T *>(r.data);
-            for (int k = threadIdx.x; k < nf * A::dim; k += blockDim.x) {
-                const int c = k % A::dim;
-                const int32_t t = fin[k / A::dim];
-                const int32_t o = __ldg(p.st.poff[g] + t), nb = __ldg(p.st.nblk[g] + t);
-                T acc = T(0);
-                for (int q = 0; q < nb; ++q) acc += __ldcg(part + int64_t(o + q) * A::dim + c);
-                const int64_t a = int64_t(t) * r.se + c * r.sc;
-                d[a] = __ldcg(d + a) + acc;
-            }
         }
     }
 };
@@ -582,9 +362,9 @@ struct ModeIndex {
 template <class... As>
 using IncIndex = ModeIndex<MINC, As...>;
 
-template <class F, int MODE, class... As>
+template <class F, int MODE, int LP, class... As>
 struct Engine {
-    using Slots = cuda::std::tuple<Slot<As, MODE>...>;
+    using Slots = cuda::std::tuple<Slot<As, MODE, lay_of<As, LP>()>...>;
     static constexpr int N = sizeof...(As);
 
     template <size_t... Is>
@@ -594,19 +374,13 @@ struct Engine {
     }
     template <size_t... Is>
     __device__ __forceinline__ static void init_elem(Slots &s, const LaunchParams &p, int64_t e,
-                                                     char *smem, cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).init_elem(p, int(Is), e, smem), ...);
+                                                     cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).init_elem(p, int(Is), e), ...);
     }
     template <size_t... Is>
     __device__ __forceinline__ static void init_elem_rec(Slots &s, const LaunchParams &p, int64_t e,
                                                          const int32_t *rk, cuda::std::index_sequence<Is...>) {
         (cuda::std::get<Is>(s).init_elem_rec(p, int(Is), e, rk), ...);
-    }
-    template <size_t... Is>
-    __device__ __forceinline__ static void init_tile(Slots &s, const LaunchParams &p, int64_t e,
-                                                     const uint16_t *locs, char *const *gb, int U, int C,
-                                                     cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).init_tile(p, int(Is), e, locs, gb, U, C), ...);
     }
     template <size_t... Is>
     __device__ __forceinline__ static void call_raw(Slots &s, const LaunchParams &p,
@@ -618,7 +392,7 @@ struct Engine {
     template <size_t... Is>
     __device__ __forceinline__ static void call(Slots &s, const LaunchParams &p, int64_t e,
                                                 cuda::std::index_sequence<Is...> idx) {
-        if constexpr (((As::kind == KG && As::mode != MR) || ...)) {
+        if constexpr (has_reduce) {
             if (e >= p.rlim) {
                 (cuda::std::get<Is>(s).backup(), ...);
                 call_raw(s, p, idx);
@@ -629,16 +403,6 @@ struct Engine {
         call_raw(s, p, idx);
     }
     template <size_t... Is>
-    __device__ __forceinline__ static void zero_smem(Slots &s, const LaunchParams &p, int32_t b,
-                                                     char *smem, cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).zero_smem(p, int(Is), b, smem), ...);
-    }
-    template <size_t... Is>
-    __device__ __forceinline__ static void write_back(Slots &s, const LaunchParams &p, int32_t b,
-                                                      char *smem, cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).write_back(p, int(Is), b, smem), ...);
-    }
-    template <size_t... Is>
     __device__ __forceinline__ static void backup_all(Slots &s, cuda::std::index_sequence<Is...>) {
         (cuda::std::get<Is>(s).backup(), ...);
     }
@@ -646,9 +410,14 @@ struct Engine {
     __device__ __forceinline__ static void restore_all(Slots &s, cuda::std::index_sequence<Is...>) {
         (cuda::std::get<Is>(s).restore(), ...);
     }
-    // gather schedule, argument at position `a` among the mode-MM indirect args:
-    // OP 0: run += its increments (INC); 1: its registers = run (WRITE, before
-    // the call: the kernel sees the target's current value); 2: run = its registers
+    template <size_t... Is>
+    __device__ __forceinline__ static void apply_staged(Slots &s, cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(s).apply_staged(), ...);
+    }
+    // target-centric schedules, argument at position `a` among the mode-MM
+    // indirect args: OP 0: run += its increments (INC); 1: its registers = run
+    // (WRITE, before the call: the kernel sees the target's current value);
+    // 2: run = its registers
     template <int MM, int OP, int DG, class TG, size_t... Is>
     __device__ __forceinline__ static void gather_op(Slots &s, int a, TG *run,
                                                      cuda::std::index_sequence<Is...>) {
@@ -670,62 +439,8 @@ struct Engine {
             }
         }
     }
-    // fold schedule: copy each INC argument's register increments into its
-    // (position) slot of this element's shared-memory staging row
-    template <int DGP, size_t... Is>
-    __device__ __forceinline__ static void stage_incs(Slots &s, void *row,
-                                                      cuda::std::index_sequence<Is...>) {
-        (stage_inc_one<Is, DGP>(s, row), ...);
-    }
-    template <size_t I, int DGP>
-    __device__ __forceinline__ static void stage_inc_one(Slots &s, void *row) {
-        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
-        if constexpr (A::kind == KI && A::mode == MINC) {
-            constexpr int pos = IncIndex<As...>::template of<I>();
-            using T = typename A::type;
-            T *dst = static_cast<T *>(row) + pos * DGP;
-#pragma unroll
-            for (int c = 0; c < A::dim; ++c) dst[c] = cuda::std::get<I>(s).acc[c];
-        }
-    }
-    // tile gather: run += increments of the INC arguments on map column c
-    template <int DG, class TG, size_t... Is>
-    __device__ __forceinline__ static void gather_col(Slots &s, const LaunchParams &p, int c, TG *run,
-                                                      cuda::std::index_sequence<Is...>) {
-        (gather_col_one<Is, DG>(s, p, c, run), ...);
-    }
-    template <size_t I, int DG, class TG>
-    __device__ __forceinline__ static void gather_col_one(Slots &s, const LaunchParams &p, int c, TG *run) {
-        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
-        if constexpr (A::kind == KI && A::mode == MINC) {
-            if (p.t.slot[I] == c) {
-                auto &acc = cuda::std::get<I>(s).acc;
-#pragma unroll
-                for (int q = 0; q < DG; ++q) run[q] += acc[q];
-            }
-        }
-    }
-    // primary fold: READ args on the target's own column read its staged rows
-    template <class TO, size_t... Is>
-    __device__ __forceinline__ static void own_views(Slots &s, const LaunchParams &p, TO *own,
-                                                     cuda::std::index_sequence<Is...>) {
-        (own_view_one<Is>(s, p, own), ...);
-    }
-    template <size_t I, class TO>
-    __device__ __forceinline__ static void own_view_one(Slots &s, const LaunchParams &p, TO *own) {
-        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
-        if constexpr (A::kind == KI && A::mode == MR) {
-            const int g = p.pf.own_grp[I];
-            if (g >= 0) {
-                using T = typename A::type;
-                auto &sl = cuda::std::get<I>(s);
-                sl.ptr = reinterpret_cast<T *>(own) + int64_t(p.pf.own_goff[g]) * blockDim.x;
-                sl.sc = blockDim.x;
-            }
-        }
-    }
-    // primary fold: INC arguments at positions >= 1 -> the element's slots
-    // slots: the element's secondary increments go to the rows of the targets'
+    // primary fold: INC arguments at positions >= 1 -> the element's slots;
+    // the element's secondary increments go to the rows of the targets'
     // secondary CSR (slotpos[e][pos-1]), so pass 2 reads each target's rows
     // contiguously
     template <int DGP, size_t... Is>
@@ -753,26 +468,6 @@ struct Engine {
             }
         }
     }
-    template <size_t... Is>
-    __device__ __forceinline__ static void arrive_sums(Slots &s, const LaunchParams &p, int32_t b,
-                                                       char *smem, cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).arrive_sums(p, int(Is), b, smem), ...);
-    }
-    template <size_t... Is>
-    __device__ __forceinline__ static void arrive_count(Slots &s, const LaunchParams &p, int32_t b,
-                                                        char *smem, int *nfin,
-                                                        cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).arrive_count(p, int(Is), b, smem, nfin), ...);
-    }
-    template <size_t... Is>
-    __device__ __forceinline__ static void arrive_final(Slots &s, const LaunchParams &p, char *smem,
-                                                        const int *nfin, cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).arrive_final(p, int(Is), smem, nfin), ...);
-    }
-    template <size_t... Is>
-    __device__ __forceinline__ static void apply_staged(Slots &s, cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).apply_staged(), ...);
-    }
     template <size_t I>
     __device__ __forceinline__ static void reduce_one(Slots &s, const LaunchParams &p, int32_t b,
                                                       double *smem) {
@@ -796,29 +491,163 @@ struct Engine {
     static constexpr bool has_reduce = ((As::kind == KG && As::mode != MR) || ...);
 };
 
+// ---- direct loops -----------------------------------------------------------------
+// Generic layouts: one element per thread, persistent grid striding over the
+// elements; one reduction partial per CTA (folded in CTA order by k_combine).
 template <class F, class... As>
 __device__ __forceinline__ void run_direct(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_NONE, As...>;
+    using E = Engine<F, ST_NONE, 0, As...>;
     __shared__ double smem[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     typename E::Slots s;
     E::init_globals(s, p, idx);
-    // persistent grid: CTA-strided over the plan blocks; one reduction
-    // partial per CTA (folded in CTA order by k_combine)
-    const int64_t nb = (p.n + p.bs - 1) / p.bs;
-    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-        const int64_t lo = b * p.bs, hi = lo + p.bs < p.n ? lo + p.bs : p.n;
-        for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-            E::init_elem(s, p, e, nullptr, idx);
-            E::call(s, p, e, idx);
-        }
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < p.n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        E::init_elem(s, p, e, idx);
+        E::call(s, p, e, idx);
     }
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, smem, idx);
 }
 
+// Direct rows of the two elements a vectorised thread owns: READ/RW/INC rows
+// are loaded with 16-byte loads, WRITE/RW/INC rows stored with 16-byte stores
+// (a WRITE row is loaded first unless the functor declares dense_writes —
+// every component of a direct WRITE argument written, OP2's OP_WRITE).
+template <class F, class = void>
+struct DenseWrites : cuda::std::false_type {};
+template <class F>
+struct DenseWrites<F, cuda::std::void_t<decltype(F::dense_writes)>> : cuda::std::bool_constant<F::dense_writes> {};
+template <class F>
+__host__ __device__ constexpr bool dense_writes() { return DenseWrites<F>::value; }
+
+template <class A, class F, int LP>
+struct DirRows {
+    static constexpr bool on = A::kind == KD;
+    static constexpr int L = lay_of<A, LP>();
+    using T = typename A::type;
+    T v[on ? 2 : 1][on ? A::dim : 1];
+    // element e0 (even) and e0 + 1 (when two): 16-byte aligned pairs
+    __device__ __forceinline__ void load(const ArgRt &r, int64_t e0, bool two) {
+        if constexpr (on) {
+            if constexpr (A::mode == MW && dense_writes<F>()) return;
+            const T *b = static_cast<const T *>(r.data);
+            if (!two) {
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) v[0][c] = b[e0 * se_of<A, L>(r) + c * sc_of<A, L>(r)];
+                return;
+            }
+            if constexpr (L == 1) {             // AOS: the pair's rows are 2*dim consecutive values
+                T f[2 * A::dim];
+#pragma unroll
+                for (int k = 0; k < A::dim; ++k) ld2(b + e0 * A::dim + 2 * k, f[2 * k], f[2 * k + 1]);
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) {
+                    v[0][c] = f[c];
+                    v[1][c] = f[A::dim + c];
+                }
+            } else {                            // SOA: one pair per component
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) ld2(b + c * r.sc + e0, v[0][c], v[1][c]);
+            }
+        }
+    }
+    __device__ __forceinline__ void store(const ArgRt &r, int64_t e0, bool two) {
+        if constexpr (on && A::mode != MR) {
+            T *b = static_cast<T *>(r.data);
+            if (!two) {
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) b[e0 * se_of<A, L>(r) + c * sc_of<A, L>(r)] = v[0][c];
+                return;
+            }
+            if constexpr (L == 1) {
+                T f[2 * A::dim];
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) {
+                    f[c] = v[0][c];
+                    f[A::dim + c] = v[1][c];
+                }
+#pragma unroll
+                for (int k = 0; k < A::dim; ++k) st2(b + e0 * A::dim + 2 * k, f[2 * k], f[2 * k + 1]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < A::dim; ++c) st2(b + c * r.sc + e0, v[0][c], v[1][c]);
+            }
+        }
+    }
+};
+
+template <class F, class... As>
+struct DirectVec {
+    using E = Engine<F, ST_NONE, 1, As...>;
+    using Rows = cuda::std::tuple<DirRows<As, F, 1>...>;
+
+    template <size_t I>
+    __device__ __forceinline__ static auto view(typename E::Slots &s, Rows &rows, int k) {
+        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
+        if constexpr (A::kind == KD) {
+            using T = typename A::type;
+            if constexpr (A::mode == MR) return static_cast<const T *>(cuda::std::get<I>(rows).v[k]);
+            else return static_cast<T *>(cuda::std::get<I>(rows).v[k]);
+        } else {
+            return cuda::std::get<I>(s).view();
+        }
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void call(typename E::Slots &s, Rows &rows, const LaunchParams &p,
+                                                int64_t e, int k, cuda::std::index_sequence<Is...>) {
+        if constexpr (E::has_reduce) {
+            if (e >= p.rlim) {
+                (cuda::std::get<Is>(s).backup(), ...);
+                F::apply(p.k, view<Is>(s, rows, k)...);
+                (cuda::std::get<Is>(s).restore(), ...);
+                return;
+            }
+        }
+        F::apply(p.k, view<Is>(s, rows, k)...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void load(Rows &rows, const LaunchParams &p, int64_t e0, bool two,
+                                                cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(rows).load(p.a[Is], e0, two), ...);
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void store(Rows &rows, const LaunchParams &p, int64_t e0, bool two,
+                                                 cuda::std::index_sequence<Is...>) {
+        (cuda::std::get<Is>(rows).store(p.a[Is], e0, two), ...);
+    }
+};
+
+// Reference auto-SOA layout (LP = 1, 16-byte aligned rows and even SOA
+// pitch): each thread owns elements e0 = 2k and e0 + 1, moves their direct
+// rows with 16-byte accesses and applies the functor to both in order.
+template <class F, class... As>
+__device__ __forceinline__ void run_direct_vec(const LaunchParams &p, Sig<As...>) {
+    using DV = DirectVec<F, As...>;
+    using E = typename DV::E;
+    __shared__ double smem[32];
+    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
+    typename E::Slots s;
+    E::init_globals(s, p, idx);
+    for (int64_t e0 = 2 * (int64_t(blockIdx.x) * blockDim.x + threadIdx.x); e0 < p.n;
+         e0 += 2 * int64_t(gridDim.x) * blockDim.x) {
+        const bool two = e0 + 1 < p.n;
+        typename DV::Rows rows;
+        DV::load(rows, p, e0, two, idx);
+        E::init_elem(s, p, e0, idx);
+        DV::call(s, rows, p, e0, 0, idx);
+        if (two) {
+            E::init_elem(s, p, e0 + 1, idx);
+            DV::call(s, rows, p, e0 + 1, 1, idx);
+        }
+        DV::store(rows, p, e0, two, idx);
+    }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, smem, idx);
+}
+
+// ---- colour schedules (reference plan: run_threads, general indirect writes) --------
 template <class F, class... As>
 __device__ __forceinline__ void run_staged(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_REG, As...>;
+    using E = Engine<F, ST_REG, 0, As...>;
     __shared__ double smem[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     const int32_t b = p.blocks[blockIdx.x];
@@ -830,7 +659,7 @@ __device__ __forceinline__ void run_staged(const LaunchParams &p, Sig<As...>) {
     typename E::Slots s;
     E::init_globals(s, p, idx);
     if (active) {
-        E::init_elem(s, p, e, nullptr, idx);
+        E::init_elem(s, p, e, idx);
         E::call(s, p, e, idx);
     }
     if (ncol == 1) {
@@ -844,124 +673,41 @@ __device__ __forceinline__ void run_staged(const LaunchParams &p, Sig<As...>) {
     if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
 }
 
-// Increments staged in shared memory: compute -> colour phases into smem ->
-// one coalesced read-modify-write of the block's unique targets.
-template <class F, int MODE, class... As>
-__device__ __forceinline__ void run_smem(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, MODE, As...>;
-    __shared__ double red[32];
-    extern __shared__ __align__(16) char dsm[];
+template <class F, class... As>
+__device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
+    using E = Engine<F, ST_NONE, 0, As...>;
+    __shared__ double smem[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     const int32_t b = p.blocks[blockIdx.x];
-    const int64_t e = int64_t(b) * p.bs + threadIdx.x;
-    const int64_t hi = int64_t(b) * p.bs + p.bs < p.n ? int64_t(b) * p.bs + p.bs : p.n;
-    const bool active = threadIdx.x < p.bs && e < hi;
+    const int64_t lo = int64_t(b) * p.bs, hi = lo + p.bs < p.n ? lo + p.bs : p.n;
     const int ncol = p.encol[b];
-    const int mine = active ? int(p.ecol[e]) : -1;
     typename E::Slots s;
-    if constexpr (MODE == ST_SMEM) E::zero_smem(s, p, b, dsm, idx);
     E::init_globals(s, p, idx);
-    if (active) {
-        E::init_elem(s, p, e, dsm, idx);
-        E::call(s, p, e, idx);
-    }
-    __syncthreads();
-    if constexpr (MODE == ST_SMEM) {
-        for (int c = 0; c < ncol; ++c) {
-            if (mine == c) E::apply_staged(s, idx);
-            __syncthreads();
-        }
-    }
-    E::write_back(s, p, b, dsm, idx);
-    if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
-}
-
-// Dataflow schedule: a persistent grid pulls blocks in plan (colour) order from
-// a global counter.  Gather + compute + in-block colour phases run at once; the
-// write-back waits only for the lower-colour blocks this block conflicts with,
-// so colours overlap without grid-wide barriers while every target still sees
-// its increments in exactly the order of the per-colour launch schedule.
-// Polling uses relaxed gpu-scope loads: an acquire load would invalidate the
-// whole L1 (CCTL.IVALL) on every spin, evicting the gathered data of every
-// CTA on the SM.  The write-back reads its targets with ld.global.cg (L2, the
-// coherence point), after the flag was observed and a CTA barrier, and the
-// producer publishes with st.release after its CTA barrier — so the targets
-// it wrote are visible in L2 before the flag is.
-__device__ __forceinline__ int ld_relaxed(const int32_t *p) {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(int32_t *p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <class F, int MODE, class... As>
-__device__ __forceinline__ void run_flow(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, MODE, As...>;
-    __shared__ double red[32];
-    __shared__ int s_q;
-    extern __shared__ __align__(16) char dsm[];
-    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    int32_t *counter = p.flags + p.nqueue;
-    if (threadIdx.x == 0) s_q = atomicAdd(counter, 1);
-    __syncthreads();
-    int q = s_q;
-    while (q < p.nqueue) {
-        // prefetch the next queue position while this block is processed
-        int next = 0;
-        if (threadIdx.x == 0) next = atomicAdd(counter, 1);
-        const int32_t b = p.blocks[q];
-        const int d0 = p.dep_off[b], d1 = p.dep_off[b + 1];
-        const int32_t dep = d0 + int(threadIdx.x) < d1 ? p.dep_list[d0 + threadIdx.x] : -1;
-        const int64_t e = int64_t(b) * p.bs + threadIdx.x;
-        const int64_t hi = int64_t(b) * p.bs + p.bs < p.n ? int64_t(b) * p.bs + p.bs : p.n;
-        const bool active = threadIdx.x < p.bs && e < hi;
-        const int ncol = p.encol[b];
-        const int mine = active ? int(p.ecol[e]) : -1;
-        typename E::Slots s;
-        if constexpr (MODE == ST_SMEM) E::zero_smem(s, p, b, dsm, idx);
-        E::init_globals(s, p, idx);
-        if (active) {
-            E::init_elem(s, p, e, dsm, idx);
+    for (int c = 0; c < ncol; ++c) {
+        for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+            if (int(p.ecol[e]) != c) continue;
+            E::init_elem(s, p, e, idx);
             E::call(s, p, e, idx);
         }
         __syncthreads();
-        if constexpr (MODE == ST_SMEM) {
-            for (int c = 0; c < ncol; ++c) {
-                if (mine == c) E::apply_staged(s, idx);
-                __syncthreads();
-            }
-        }
-        // wait for the conflicting earlier-queued blocks (one thread per dependency)
-        if (dep >= 0)
-            while (ld_relaxed(p.flags + dep) == 0) __nanosleep(32);
-        for (int k = d0 + int(threadIdx.x) + int(blockDim.x); k < d1; k += blockDim.x)
-            while (ld_relaxed(p.flags + p.dep_list[k]) == 0) __nanosleep(32);
-        __syncthreads();
-        E::write_back(s, p, b, dsm, idx);
-        if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
-        if (threadIdx.x == 0) s_q = next;
-        __syncthreads();
-        if (threadIdx.x == 0) st_release(p.flags + b, 1);
-        q = s_q;
     }
+    if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
 }
 
-// Target-centric ("gather") schedule for loops whose indirect writes all go to
-// one dat with one mode — INC, or WRITE — and that write no direct argument: one
-// thread per target element re-evaluates the kernel for every (element,
-// argument) incidence of that target, in serial order, and keeps only that
-// argument's effect on a running value that starts from the target's current
-// value: INC adds the increment, WRITE replaces the value (the kernel is handed
-// the running value in that argument, so it sees what the serial order would
-// show it).  The target's final value is therefore exactly the serial one.  No
-// colours, no shared memory, no atomics; a target's running value never leaves
-// the thread's registers.  Global reductions count each element once (on its
+// ---- target-centric ("gather") schedule ----------------------------------------------
+// For loops whose indirect writes all go to one dat with one mode — INC, or
+// WRITE — and that write no direct argument: one thread per target element
+// re-evaluates the kernel for every (element, argument) incidence of that
+// target, in serial order, and keeps only that argument's effect on a running
+// value that starts from the target's current value: INC adds the increment,
+// WRITE replaces the value (the kernel is handed the running value in that
+// argument, so it sees what the serial order would show it).  The target's
+// final value is therefore exactly the serial one.  No colours, no shared
+// memory, no atomics.  Global reductions count each element once (on its
 // incidence through the first such argument).
-template <class F, class... As>
+template <class F, int LP, class... As>
 __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_GATHER, As...>;
+    using E = Engine<F, ST_GATHER, LP, As...>;
     constexpr bool has_inc = ((As::kind == KI && As::mode == MINC) || ...);
     constexpr int MM = has_inc ? MINC : MW;
     constexpr int G = ModeIndex<MM, As...>::template first<0>();
@@ -969,26 +715,26 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
     using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
     using TG = typename AG::type;
     constexpr int DG = AG::dim;
+    constexpr int LG = lay_of<AG, LP>();
     __shared__ double red[32];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     typename E::Slots s;
     E::init_globals(s, p, idx);
-    // grid-stride over blocks of targets (a smaller grid keeps fewer targets'
-    // rows in flight per SM; the default grid covers every target once)
+    const ArgRt &rg = p.a[G];
+    const int64_t gse = se_of<AG, LG>(rg), gsc = sc_of<AG, LG>(rg);
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
          t - threadIdx.x < p.g_ntargets; t += int64_t(gridDim.x) * blockDim.x) {
         if (t >= p.g_ntargets) continue;
-        const ArgRt &rg = p.a[G];
         const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
-        TG *dst = static_cast<TG *>(rg.data) + tg * rg.se;
+        TG *dst = static_cast<TG *>(rg.data) + tg * gse;
         const int32_t seg = (MM == MINC && p.g_seg) ? __ldg(p.g_seg + t) : -1;
         TG run[DG];
 #pragma unroll
-        for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : TG(0);
+        for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * gsc] : TG(0);
         for (int k = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1); k < ke; ++k) {
             const int64_t e = __ldg(p.g_elem + k);
             const int a = __ldg(p.g_pos + k);
-            E::init_elem(s, p, e, nullptr, idx);
+            E::init_elem(s, p, e, idx);
             if constexpr (MM == MW) E::template gather_op<MW, 1, DG>(s, a, run, idx);
             if constexpr (E::has_reduce) {
                 if (a != 0 || e >= p.rlim) {
@@ -1009,7 +755,7 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
             for (int c = 0; c < DG; ++c) part[c] = run[c];
         } else {
 #pragma unroll
-            for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+            for (int c = 0; c < DG; ++c) dst[c * gsc] = run[c];
         }
     }
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
@@ -1035,64 +781,55 @@ __global__ void __launch_bounds__(256) k_gather_hubs(const __grid_constant__ Lau
     for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
 }
 
-// Primary-fold schedule, pass 1 (see PFoldParams): a persistent grid strides
-// over the targets; thread t evaluates, in element order, every element whose
-// first INC argument targets it — each element exactly once in the whole
-// launch, its neighbours' rows read once per element instead of once per
-// incidence — adds that argument's increments to a running value that starts
-// from the target's current value, and stores the other INC arguments'
-// increments in the element's slots.  Global reductions count every element
-// here (once).  Pass 2 (k_pfold_rest) adds each target's slots in element
-// order.  Per target the result is value + primary increments + secondary
-// increments: deterministic, within rounding of the serial order.
+// ---- primary fold ---------------------------------------------------------------------
+// Pass 1 (see PFoldParams): a persistent grid strides over the targets; thread
+// t evaluates, in element order, every element whose first INC argument
+// targets it — each element exactly once in the whole launch, its
+// neighbours' rows read once per element instead of once per incidence —
+// adds that argument's increments to a running value that starts from the
+// target's current value, and stores the other INC arguments' increments in
+// the element's slots.  Global reductions count every element here (once).
+// Pass 2 (k_pfold_rest_w) adds each target's slots in element order.  Per
+// target the result is value + primary increments + secondary increments:
+// deterministic, within rounding of the serial order.
 template <class TG, int DG>
 struct PFoldShape {
     static constexpr int DGP = (DG + 1) / 2 * 2;   // slot rows of whole 16-byte pairs
 };
 
-template <class F, class... As>
+template <class F, int LP, class... As>
 __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_GATHER, As...>;
+    using E = Engine<F, ST_GATHER, LP, As...>;
     constexpr int G = IncIndex<As...>::template first<0>();
     static_assert(G >= 0, "primary fold needs an INC argument");
     using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
     using TG = typename AG::type;
     constexpr int DG = AG::dim;
+    constexpr int LG = lay_of<AG, LP>();
     constexpr int NW = ((As::kind == KI && As::mode == MINC) + ...);
     constexpr int DGP = PFoldShape<TG, DG>::DGP;
     __shared__ double red[32];
-    extern __shared__ __align__(16) char dsm[];
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     typename E::Slots s;
     E::init_globals(s, p, idx);
     const PFoldParams &pf = p.pf;
-    TG *own = reinterpret_cast<TG *>(dsm) + threadIdx.x;      // this thread's column
+    const ArgRt &rg = p.a[G];
+    const int64_t gse = se_of<AG, LG>(rg), gsc = sc_of<AG, LG>(rg);
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t - threadIdx.x < pf.n1;
          t += int64_t(gridDim.x) * blockDim.x) {
         if (t >= pf.n1) continue;
-        const ArgRt &rg = p.a[G];
         const int64_t tg = pf.tl1 ? int64_t(__ldg(pf.tl1 + t)) : t;
-        TG *dst = static_cast<TG *>(rg.data) + tg * rg.se;
+        TG *dst = static_cast<TG *>(rg.data) + tg * gse;
         const int32_t seg = pf.seg1 ? __ldg(pf.seg1 + t) : -1;
-        // the target's own READ rows, once per target (consecutive targets: coalesced)
-        for (int g = 0; g < pf.own_ngrp; ++g) {
-            const ArgRt &r = p.a[pf.own_garg[g]];
-            const TG *src = static_cast<const TG *>(r.data) + tg * r.se;
-            TG *o = own + int64_t(pf.own_goff[g]) * blockDim.x;
-            const int dim = pf.own_gdim[g];
-#pragma unroll 4
-            for (int c = 0; c < dim; ++c) o[c * blockDim.x] = __ldg(src + c * r.sc);
-        }
         TG run[DG];
 #pragma unroll
-        for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : TG(0);
+        for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * gsc] : TG(0);
         for (int k = __ldg(pf.off1 + t), ke = __ldg(pf.off1 + t + 1); k < ke; ++k) {
             const int64_t e = __ldg(pf.elem1 + k);
             if (pf.rec)
                 E::init_elem_rec(s, p, e, pf.rec + int64_t(k) * pf.ncol, idx);
             else
-                E::init_elem(s, p, e, nullptr, idx);
-            if (pf.own_ngrp > 0) E::own_views(s, p, own, idx);
+                E::init_elem(s, p, e, idx);
             E::call(s, p, e, idx);
             E::template gather_op<MINC, 0, DG>(s, 0, run, idx);
             if constexpr (NW > 1)
@@ -1104,57 +841,16 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
             for (int c = 0; c < DG; ++c) part[c] = run[c];
         } else {
 #pragma unroll
-            for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+            for (int c = 0; c < DG; ++c) dst[c * gsc] = run[c];
         }
     }
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
 }
 
-// Primary-fold schedule, pass 2: each target adds its slots in element order.
-template <class T, int DG>
-__global__ void __launch_bounds__(256) k_pfold_rest(const __grid_constant__ LaunchParams p, int ga) {
-    pdl_wait();
-    constexpr int DGP = PFoldShape<T, DG>::DGP;
-    const PFoldParams &pf = p.pf;
-    const ArgRt &rg = p.a[ga];
-    const T *slots = static_cast<const T *>(pf.slots);
-    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < pf.n2;
-         t += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t tg = pf.tl2 ? int64_t(__ldg(pf.tl2 + t)) : t;
-        T *dst = static_cast<T *>(rg.data) + tg * rg.se;
-        const int32_t seg = pf.seg2 ? __ldg(pf.seg2 + t) : -1;
-        T run[DG];
-#pragma unroll
-        for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : T(0);
-        for (int k = __ldg(pf.off2 + t), ke = __ldg(pf.off2 + t + 1); k < ke; ++k) {
-            const T *src = slots + int64_t(k) * DGP;        // rows in CSR order: contiguous per target
-            if constexpr (DG % 2 == 0 && cuda::std::is_same_v<T, double>) {
-#pragma unroll
-                for (int c = 0; c < DG; c += 2) {
-                    const double2 v = __ldcs(reinterpret_cast<const double2 *>(src + c));
-                    run[c] += v.x;
-                    run[c + 1] += v.y;
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < DG; ++c) run[c] += __ldcs(src + c);
-            }
-        }
-        if (seg >= 0) {
-            T *part = static_cast<T *>(pf.part2) + int64_t(seg) * DG;
-#pragma unroll
-            for (int c = 0; c < DG; ++c) part[c] = run[c];
-        } else {
-#pragma unroll
-            for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
-        }
-    }
-}
-
 // Pass 2, warp-cooperative: a warp owns 32 consecutive pass-2 rows, whose
 // slots are one contiguous range; the lanes copy it through shared memory in
-// coalesced 16-byte chunks, then each lane adds its own rows in order — the
-// same per-target arithmetic as k_pfold_rest, with full-sector DRAM reads.
+// coalesced 16-byte chunks, then each lane adds its own rows in order, with
+// full-sector DRAM reads.
 template <class T, int DG>
 __global__ void __launch_bounds__(256) k_pfold_rest_w(const __grid_constant__ LaunchParams p, int ga) {
     pdl_wait();
@@ -1232,386 +928,12 @@ __global__ void __launch_bounds__(256) k_fold_parts(const __grid_constant__ Laun
     for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
 }
 
-// Fold schedule, pass 1 — every element evaluated exactly once, like a direct
-// loop (coalesced direct access, no colours): its INC increments, computed
-// from zero in registers, go to the element's slots of an element-major
-// buffer [n][INC args][DGP] (DGP = dim rounded up to 4 doubles, so a slot is
-// whole 32-byte sectors) instead of the targets.  The slots of a CTA's 256
-// elements are one contiguous region: they are staged through shared memory
-// (rows padded by one word against bank conflicts) and stored coalesced.
-// Pass 2 (k_fold_targets) adds each target's slots onto it in serial order.
-// The increments are the very values the serial run adds (same functor, same
-// zero start), added in the same order, so the result is the serial one bit
-// for bit — with the kernel evaluated once per element instead of once per
-// incidence as in the gather schedule.
-template <class T, int DG>
-struct FoldShape {
-    static constexpr int DGP = (DG + 3) / 4 * 4;
-};
-
-template <class F, class... As>
-__device__ __forceinline__ void run_fold_edges(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_REG, As...>;
-    constexpr int G = IncIndex<As...>::template first<0>();
-    using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
-    using TG = typename AG::type;
-    constexpr int NW = ((As::kind == KI && As::mode == MINC) + ...);
-    constexpr int DGP = FoldShape<TG, AG::dim>::DGP;
-    constexpr int ROW = NW * DGP, SROW = ROW + 1;
-    __shared__ double red[32];
-    extern __shared__ __align__(16) char dsm[];
-    TG *st = reinterpret_cast<TG *>(dsm);
-    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    const int64_t e0 = int64_t(blockIdx.x) * blockDim.x, e = e0 + threadIdx.x;
-    typename E::Slots s;
-    E::init_globals(s, p, idx);
-    if (e < p.n) {
-        E::init_elem(s, p, e, nullptr, idx);
-        E::call(s, p, e, idx);
-        E::template stage_incs<DGP>(s, st + threadIdx.x * SROW, idx);
-    }
-    __syncthreads();
-    const int64_t rows = p.n - e0 < int64_t(blockDim.x) ? p.n - e0 : int64_t(blockDim.x);
-    TG *out = static_cast<TG *>(p.g_buf) + e0 * ROW;
-    for (int k = threadIdx.x; k < rows * ROW; k += blockDim.x) {
-        const int r = k / ROW, c = k - r * ROW;
-        if (c % DGP < AG::dim) __stcg(out + k, st[r * SROW + c]);
-    }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
-}
-
-template <class S>
-struct FoldSmem;
-template <class... As>
-struct FoldSmem<Sig<As...>> {
-    static size_t bytes(int threads) {
-        constexpr int G = IncIndex<As...>::template first<0>() < 0 ? 0 : IncIndex<As...>::template first<0>();
-        using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
-        constexpr int NW = ((As::kind == KI && As::mode == MINC) + ...);
-        constexpr int DGP = FoldShape<typename AG::type, AG::dim>::DGP;
-        return size_t(threads) * (NW * DGP + 1) * sizeof(typename AG::type);
-    }
-};
-
-// Fold schedule, pass 2: one thread per target, slots in serial order.
-template <class T, int DG>
-__global__ void __launch_bounds__(256) k_fold_targets(const __grid_constant__ LaunchParams p, int ga) {
-    constexpr int DGP = FoldShape<T, DG>::DGP;
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= p.g_ntargets) return;
-    const ArgRt &rg = p.a[ga];
-    const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
-    T *dst = static_cast<T *>(rg.data) + tg * rg.se;
-    const T *buf = static_cast<const T *>(p.g_buf);
-    const int64_t row = int64_t(p.g_nw) * DGP;
-    T run[DG];
-#pragma unroll
-    for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
-    for (int k = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1); k < ke; ++k) {
-        const T *src = buf + int64_t(__ldg(p.g_elem + k)) * row + int(__ldg(p.g_pos + k)) * DGP;
-        if constexpr (DG % 2 == 0 && cuda::std::is_same_v<T, double>) {
-#pragma unroll
-            for (int c = 0; c < DG; c += 2) {   // 16-byte loads: slots are 32-byte aligned
-                const double2 v = __ldcs(reinterpret_cast<const double2 *>(src + c));
-                run[c] += v.x;
-                run[c + 1] += v.y;
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < DG; ++c) run[c] += __ldcs(src + c);
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
-}
-
-// Tile schedule (see host_tile.cpp): one CTA per tile.
-//  1. stage: the tile's target list, then every READ dat's rows of the staged
-//     targets, copied HBM/L2 -> shared memory with cp.async (8-byte copies,
-//     no registers held, thousands in flight per CTA), component-major
-//     [dim][U]; INC accumulators of the owned targets [dim][C] zeroed;
-//  2. evaluate: the tile's elements in chunks of blockDim; READ args are
-//     shared-memory views, direct args HBM views, INC args registers;
-//  3. apply: element-colour phases add the register increments of owned
-//     targets into the accumulators (elements of one colour share no owned
-//     target), so no atomics and a fixed order — deterministic run to run;
-//  4. write back: one read-modify-write per owned target and component.
-// A target's increments all come from its owning tile, so tiles never
-// conflict: one launch, no block colours, no inter-CTA synchronisation.
-__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
-
-template <class S>
-struct TileType;
-template <class... As>
-struct TileType<Sig<As...>> {
-    static constexpr int G = IncIndex<As...>::template first<0>() < 0 ? 0 : IncIndex<As...>::template first<0>();
-    using type = typename cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>::type;
-};
-
-__host__ __device__ inline size_t tile_align(size_t x) { return (x + 15) / 16 * 16; }
-
-template <class F, class... As>
-__device__ __forceinline__ void run_tile(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_TILE, As...>;
-    using T = typename TileType<Sig<As...>>::type;
-    __shared__ double red[32];
-    extern __shared__ __align__(16) char dsm[];
-    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    const TileParams &tp = p.t;
-    const int32_t t = blockIdx.x;
-    const int32_t l0 = tp.list_off[t], U = tp.list_off[t + 1] - l0, C = tp.nown[t];
-    const int ng = tp.nread + tp.ninc;
-#ifdef ML_TILE_PROFILE
-    long long tk0 = clock64(), tk1 = 0, tk2 = 0, tk3 = 0, tk4 = 0;
-#endif
-    int32_t *slist = reinterpret_cast<int32_t *>(dsm);
-    __shared__ char *gb[MAX_TGROUPS];        // group bases (shared: indexed at run time)
-    if (threadIdx.x == 0) {
-        size_t off = tile_align(size_t(U) * 4);
-        for (int g = 0; g < ng; ++g) {
-            gb[g] = dsm + off;
-            off += tile_align(sizeof(T) * size_t(tp.gdim[g]) * size_t(g < tp.nread ? U : C));
-        }
-    }
-    __syncthreads();
-    for (int g = tp.nread; g < ng; ++g) {
-        T *acc = reinterpret_cast<T *>(gb[g]);
-        for (int k = threadIdx.x; k < tp.gdim[g] * C; k += blockDim.x) acc[k] = T(0);
-    }
-    // one staged target per thread and pass: its id is loaded once, then every
-    // component of every READ dat is copied (lanes = consecutive list entries)
-    for (int j = threadIdx.x; j < U; j += blockDim.x) {
-        const int64_t v = __ldg(tp.list + l0 + j);
-        slist[j] = int32_t(v);
-        for (int g = 0; g < tp.nread; ++g) {
-            const ArgRt &r = p.a[tp.garg[g]];
-            const T *src = static_cast<const T *>(r.data) + v * r.se;
-            T *dst = reinterpret_cast<T *>(gb[g]) + j;
-            const int dim = tp.gdim[g];
-#pragma unroll 4
-            for (int c = 0; c < dim; ++c) cp_async8(dst + c * U, src + c * r.sc);
-        }
-    }
-#ifdef ML_TILE_PROFILE
-    tk1 = clock64();
-#endif
-    cp_async_wait_all();
-    __syncthreads();
-#ifdef ML_TILE_PROFILE
-    tk2 = clock64();
-#endif
-
-    typename E::Slots s;
-    E::init_globals(s, p, idx);
-    const int32_t k1 = tp.elem_off[t + 1];
-    const int ncol = tp.ncol[t];
-    for (int32_t k0 = tp.elem_off[t]; k0 < k1; k0 += blockDim.x) {
-        const int32_t k = k0 + threadIdx.x;
-        int mine = -1;
-        if (k < k1) {
-            const int64_t e = __ldg(tp.elem + k);
-            const uint8_t fl = __ldg(tp.ecol + k);
-            mine = fl & 127;
-            E::init_tile(s, p, e, tp.loc + int64_t(k) * tp.arity, gb, U, C, idx);
-            if constexpr (E::has_reduce) {
-                if (!(fl & 128) || e >= p.rlim) {
-                    E::backup_all(s, idx);
-                    E::call_raw(s, p, idx);
-                    E::restore_all(s, idx);
-                } else {
-                    E::call_raw(s, p, idx);
-                }
-            } else {
-                E::call_raw(s, p, idx);
-            }
-        }
-        for (int c = 0; c < ncol; ++c) {
-            if (mine == c) E::apply_staged(s, idx);
-            __syncthreads();
-        }
-    }
-#ifdef ML_TILE_PROFILE
-    tk3 = clock64();
-#endif
-    // write back: 4 independent read-modify-writes in flight per thread
-    for (int g = tp.nread; g < ng; ++g) {
-        const ArgRt &r = p.a[tp.garg[g]];
-        T *d = static_cast<T *>(r.data);
-        const T *acc = reinterpret_cast<const T *>(gb[g]);
-        const int total = tp.gdim[g] * C;
-        constexpr int UN = 4;
-        for (int k0 = threadIdx.x; k0 < total; k0 += UN * blockDim.x) {
-            int64_t a[UN];
-            T v[UN];
-#pragma unroll
-            for (int q = 0; q < UN; ++q) {
-                const int k = k0 + q * blockDim.x;
-                if (k < total) {
-                    const int c = k / C, j = k - c * C;
-                    a[q] = int64_t(slist[j]) * r.se + c * r.sc;
-                    v[q] = d[a[q]];
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < UN; ++q)
-                if (k0 + q * blockDim.x < total) d[a[q]] = v[q] + acc[k0 + q * blockDim.x];
-        }
-    }
-#ifdef ML_TILE_PROFILE
-    __syncthreads();
-    tk4 = clock64();
-    if (threadIdx.x == 0 && p.g_buf) {
-        long long *o = static_cast<long long *>(p.g_buf) + int64_t(t) * 4;
-        o[0] = tk1 - tk0; o[1] = tk2 - tk1; o[2] = tk3 - tk2; o[3] = tk4 - tk3;
-    }
-#endif
-    if constexpr (E::has_reduce) E::reduce_all(s, p, t, red, idx);
-}
-
-// Tile-gather variant: the tile's staged rows as in run_tile, then one thread
-// per owned target re-evaluates each of its incidences (element order, then
-// column) from shared memory and keeps its own increments in registers — no
-// colour phases, no accumulators, one barrier.  Elements are evaluated once
-// per incidence (like the gather schedule) but every node row comes from
-// shared memory, staged once per tile.  Reductions count an element at its
-// `red_col` incidence (exactly one tile owns that target).
-template <class F, class... As>
-__device__ __forceinline__ void run_tgather(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_TILE, As...>;
-    constexpr int G = IncIndex<As...>::template first<0>();
-    using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
-    using T = typename AG::type;
-    constexpr int DG = AG::dim;
-    __shared__ double red[32];
-    __shared__ char *gb[MAX_TGROUPS];
-    extern __shared__ __align__(16) char dsm[];
-    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    const TileParams &tp = p.t;
-    const int32_t t = blockIdx.x;
-    const int32_t l0 = tp.list_off[t], U = tp.list_off[t + 1] - l0, C = tp.nown[t];
-    const int ng = tp.nread;
-    int32_t *slist = reinterpret_cast<int32_t *>(dsm);
-    if (threadIdx.x == 0) {
-        size_t off = tile_align(size_t(U) * 4);
-        for (int g = 0; g < ng; ++g) {
-            gb[g] = dsm + off;
-            off += tile_align(sizeof(T) * size_t(tp.gdim[g]) * size_t(U));
-        }
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < U; j += blockDim.x) {
-        const int64_t v = __ldg(tp.list + l0 + j);
-        slist[j] = int32_t(v);
-        for (int g = 0; g < ng; ++g) {
-            const ArgRt &r = p.a[tp.garg[g]];
-            const T *src = static_cast<const T *>(r.data) + v * r.se;
-            T *dst = reinterpret_cast<T *>(gb[g]) + j;
-            const int dim = tp.gdim[g];
-#pragma unroll 4
-            for (int c = 0; c < dim; ++c) cp_async8(dst + c * U, src + c * r.sc);
-        }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    typename E::Slots s;
-    E::init_globals(s, p, idx);
-    const int32_t e0 = tp.elem_off[t];
-    const int32_t *ioff = tp.inc_off + tp.inc_base[t];
-    const ArgRt &rg = p.a[G];
-    for (int j = threadIdx.x; j < C; j += blockDim.x) {
-        T *dst = static_cast<T *>(rg.data) + int64_t(slist[j]) * rg.se;
-        T run[DG];
-#pragma unroll
-        for (int c = 0; c < DG; ++c) run[c] = dst[c * rg.sc];
-        for (int q = __ldg(ioff + j), qe = __ldg(ioff + j + 1); q < qe; ++q) {
-            const int k = e0 + __ldg(tp.inc_k + q);
-            const int col = __ldg(tp.inc_c + q);
-            const int64_t e = __ldg(tp.elem + k);
-            E::init_tile(s, p, e, tp.loc + int64_t(k) * tp.arity, gb, U, 0, idx);
-            if constexpr (E::has_reduce) {
-                if (col != tp.red_col || e >= p.rlim) {
-                    E::backup_all(s, idx);
-                    E::call_raw(s, p, idx);
-                    E::restore_all(s, idx);
-                } else {
-                    E::call_raw(s, p, idx);
-                }
-            } else {
-                E::call_raw(s, p, idx);
-            }
-            E::template gather_col<DG>(s, p, col, run, idx);
-        }
-#pragma unroll
-        for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
-    }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, t, red, idx);
-}
-
-// Arrival schedule: one launch over the plan blocks in natural order (best
-// locality), no block colours and no inter-block waiting.  Targets touched by
-// one block are updated directly; shared targets are completed by whichever
-// block arrives last, folding the per-block partials in block order, so the
-// result is deterministic run to run.  Partials of neighbouring blocks are
-// written and read within a short time window, so they live in L2.
-template <class F, class... As>
-__device__ __forceinline__ void run_arrive(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_SEG, As...>;
-    __shared__ double red[32];
-    __shared__ int nfin[MAX_GROUPS];
-    extern __shared__ __align__(16) char dsm[];
-    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    const int32_t b = blockIdx.x;
-    const int64_t e = int64_t(b) * p.bs + threadIdx.x;
-    const int64_t hi = int64_t(b) * p.bs + p.bs < p.n ? int64_t(b) * p.bs + p.bs : p.n;
-    const bool active = threadIdx.x < p.bs && e < hi;
-    if (threadIdx.x < MAX_GROUPS) nfin[threadIdx.x] = 0;
-    typename E::Slots s;
-    E::init_globals(s, p, idx);
-    if (active) {
-        E::init_elem(s, p, e, dsm, idx);
-        E::call(s, p, e, idx);
-    }
-    __syncthreads();
-    E::arrive_sums(s, p, b, dsm, idx);
-    __threadfence();
-    __syncthreads();
-    E::arrive_count(s, p, b, dsm, nfin, idx);
-    __syncthreads();
-    E::arrive_final(s, p, dsm, nfin, idx);
-    if constexpr (E::has_reduce) E::reduce_all(s, p, b, red, idx);
-}
-
-template <class F, class... As>
-__device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_NONE, As...>;
-    __shared__ double smem[32];
-    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    const int32_t b = p.blocks[blockIdx.x];
-    const int64_t lo = int64_t(b) * p.bs, hi = lo + p.bs < p.n ? lo + p.bs : p.n;
-    const int ncol = p.encol[b];
-    typename E::Slots s;
-    E::init_globals(s, p, idx);
-    for (int c = 0; c < ncol; ++c) {
-        for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-            if (int(p.ecol[e]) != c) continue;
-            E::init_elem(s, p, e, nullptr, idx);
-            E::call(s, p, e, idx);
-        }
-        __syncthreads();
-    }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, b, smem, idx);
-}
-
-template <class F, class T>
+// ---- kernels ------------------------------------------------------------------------
+template <class F, class T, int LP>
 __global__ void __launch_bounds__(256) k_direct(const __grid_constant__ LaunchParams p) {
     pdl_wait();
-    run_direct<F>(p, typename F::template sig<T>{});
+    if constexpr (LP == 1) run_direct_vec<F>(p, typename F::template sig<T>{});
+    else run_direct<F>(p, typename F::template sig<T>{});
 }
 template <class F, class T>
 __global__ void __launch_bounds__(256) k_staged(const __grid_constant__ LaunchParams p) {
@@ -1621,43 +943,15 @@ template <class F, class T>
 __global__ void __launch_bounds__(256) k_phased(const __grid_constant__ LaunchParams p) {
     run_phased<F>(p, typename F::template sig<T>{});
 }
-template <class F, class T, int MODE>
-__global__ void __launch_bounds__(256) k_smem(const __grid_constant__ LaunchParams p) {
-    run_smem<F, MODE>(p, typename F::template sig<T>{});
-}
-template <class F, class T, int MODE>
-__global__ void __launch_bounds__(256) k_flow(const __grid_constant__ LaunchParams p) {
-    run_flow<F, MODE>(p, typename F::template sig<T>{});
-}
-template <class F, class T>
-__global__ void __launch_bounds__(256) k_fold_edges(const __grid_constant__ LaunchParams p) {
-    run_fold_edges<F>(p, typename F::template sig<T>{});
-}
-template <class F, class T>
-__global__ void __launch_bounds__(256) k_arrive(const __grid_constant__ LaunchParams p) {
-    run_arrive<F>(p, typename F::template sig<T>{});
-}
-template <class F, class T, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) k_tile(const __grid_constant__ LaunchParams p) {
-    run_tile<F>(p, typename F::template sig<T>{});
-}
-template <class F, class T, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) k_tgather(const __grid_constant__ LaunchParams p) {
-    run_tgather<F>(p, typename F::template sig<T>{});
-}
-template <class F, class T>
+template <class F, class T, int LP>
 __global__ void __launch_bounds__(256) k_pfold1(const __grid_constant__ LaunchParams p) {
     pdl_wait();
-    run_pfold1<F>(p, typename F::template sig<T>{});
+    run_pfold1<F, LP>(p, typename F::template sig<T>{});
 }
-template <class F, class T>
+template <class F, class T, int LP>
 __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ LaunchParams p) {
     pdl_wait();
-    run_gather<F>(p, typename F::template sig<T>{});
-}
-template <class F, class T, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_gather_occ(const __grid_constant__ LaunchParams p) {
-    run_gather<F>(p, typename F::template sig<T>{});
+    run_gather<F, LP>(p, typename F::template sig<T>{});
 }
 
 // ---- compile-time signature introspection -------------------------------------
@@ -1680,11 +974,8 @@ struct SigInfo<Sig<As...>> {
     static constexpr bool ind_rw = ((As::kind == KI && As::mode == MRW) || ...);
     // target-centric schedule: indirect writes of one mode (INC or WRITE), no direct writes
     static constexpr bool gather_ok = ind_write && !ind_rw && !(ind_inc && ind_w) && !direct_write;
-    // fold schedule: indirect writes all INC (direct writes allowed)
+    // primary fold: indirect writes all INC (direct writes allowed)
     static constexpr bool fold_ok = ind_inc && !ind_rw && !ind_w;
-    // tile schedule: indirect writes all INC, no direct writes (cut elements
-    // are evaluated by two tiles)
-    static constexpr bool tile_ok = ind_inc && !ind_rw && !ind_w && !direct_write;
 };
 
 template <class S>
@@ -1704,21 +995,12 @@ struct FunctorEntry {
     int32_t nargs;
     int32_t kind[MAX_ARGS], mode[MAX_ARGS], dim[MAX_ARGS], atype[MAX_ARGS];
     bool ind_write, ind_write_non_inc;
-    LaunchFn direct, staged, phased;
-    LaunchFn smem[2], flow[2];                       // [0] colour phases, [1] segmented
-    LaunchFn arrive;                                 // segmented, no block colours
-    LaunchFn gather[4];                              // target-centric (INC-only or WRITE-only):
-                                                     // free / >=2 / >=3 / >=4 CTAs of 256 per SM
-    int (*flow_occupancy[2])(int threads, size_t smem);
-    int (*gather_occupancy)();
-    int (*direct_occupancy)(int threads);
-    LaunchFn fold_edges, fold_targets;               // fold schedule (INC-only indirect writes)
-    int32_t fold_dim, fold_arg;                      // INC dim, first INC argument
-    LaunchFn tile;                                   // tile schedule (INC-only, no direct writes)
-    LaunchFn tgather;                                // tile-gather variant
-    LaunchFn pfold1, pfold2;                         // primary-fold schedule (INC-only)
-    LaunchFn gather_hubs;                            // hub fix-up of the gather schedule (INC)
-    int (*pfold_occupancy)(size_t smem);
+    LaunchFn direct[2], staged, phased;              // [LP]
+    LaunchFn gather[2], gather_hubs;                 // target-centric (INC-only or WRITE-only)
+    LaunchFn pfold1[2], pfold2;                      // primary fold (INC-only)
+    int (*direct_occupancy[2])(int threads);
+    int (*gather_occupancy[2])();
+    int (*pfold_occupancy[2])();
     void (*pfold_hubs)(const LaunchParams &, int64_t nhub, const int32_t *tl, const int32_t *off,
                        const void *parts, cudaStream_t);
     int32_t pfold_dgp, pfold_nslot;
@@ -1728,12 +1010,14 @@ void register_functor(const FunctorEntry &e);
 
 template <class F, class T>
 struct Registrar {
+    template <int LP>
     static void direct(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
-        launch_k(k_direct<F, T>, g, b, 0, s, p);
+        launch_k(k_direct<F, T, LP>, g, b, 0, s, p);
     }
+    template <int LP>
     static int direct_occupancy(int threads) {
         int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_direct<F, T>, threads, 0) != cudaSuccess) n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_direct<F, T, LP>, threads, 0) != cudaSuccess) n = 0;
         return n;
     }
     static void staged(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
@@ -1742,78 +1026,48 @@ struct Registrar {
     static void phased(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         k_phased<F, T><<<g, b, 0, s>>>(p);
     }
-    template <int MODE>
-    static void smem(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
-        static bool opted = false;
-        if (!opted && bytes > 48 * 1024) {
-            cudaFuncSetAttribute(k_smem<F, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            opted = true;
-        }
-        k_smem<F, T, MODE><<<g, b, bytes, s>>>(p);
-    }
-    template <int MODE>
-    static void flow(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
-        static bool opted = false;
-        if (!opted && bytes > 48 * 1024) {
-            cudaFuncSetAttribute(k_flow<F, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            opted = true;
-        }
-        k_flow<F, T, MODE><<<g, b, bytes, s>>>(p);
-    }
-    static void gather(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+    // the target-centric kernels use no shared memory to speak of: the SM's
+    // storage goes to L1, where consecutive targets share neighbour rows
+    template <class K>
+    static void carve_l1(K kernel) {
         static bool once = false;
-        if (!once) {   // no shared memory to speak of: give the SM's storage to L1
-            cudaFuncSetAttribute(k_gather<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        if (!once) {
+            cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
             once = true;
         }
-        launch_k(k_gather<F, T>, g, b, 0, s, p);
     }
-    // resident CTAs of 256 threads per SM (sizes the persistent gather grid)
+    template <int LP>
+    static void gather(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        carve_l1(k_gather<F, T, LP>);
+        launch_k(k_gather<F, T, LP>, g, b, 0, s, p);
+    }
+    // resident CTAs of 256 threads per SM (sizes the persistent grids)
+    template <int LP>
     static int gather_occupancy() {
         static int n = -1;
         if (n < 0) {
-            cudaFuncSetAttribute(k_gather<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gather<F, T>, 256, 0) != cudaSuccess) n = 0;
+            carve_l1(k_gather<F, T, LP>);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gather<F, T, LP>, 256, 0) != cudaSuccess) n = 0;
         }
         return n;
-    }
-    static void fold_edges(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
-        using S = typename F::template sig<T>;
-        const size_t bytes = FoldSmem<S>::bytes(int(b.x));
-        static bool once = false;
-        if (!once) {
-            if (bytes > 48 * 1024)
-                cudaFuncSetAttribute(k_fold_edges<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            once = true;
-        }
-        k_fold_edges<F, T><<<g, b, bytes, s>>>(p);
     }
     static void gather_hubs(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
         using AG = typename FirstInc<S>::type;
         launch_k(k_gather_hubs<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
     }
-    static void pfold_attrs(size_t bytes) {
-        static int carve = -1;
-        const int want = bytes ? 100 : 0;
-        if (carve != want) {
-            cudaFuncSetAttribute(k_pfold1<F, T>, cudaFuncAttributePreferredSharedMemoryCarveout, want);
-            carve = want;
-        }
-        static size_t opted = 48 * 1024;
-        if (bytes > opted) {
-            cudaFuncSetAttribute(k_pfold1<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-            opted = bytes;
-        }
+    template <int LP>
+    static void pfold1(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
+        carve_l1(k_pfold1<F, T, LP>);
+        launch_k(k_pfold1<F, T, LP>, g, b, 0, s, p);
     }
-    static void pfold1(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
-        pfold_attrs(bytes);
-        launch_k(k_pfold1<F, T>, g, b, bytes, s, p);
-    }
-    static int pfold_occupancy(size_t bytes) {
-        pfold_attrs(bytes);
-        int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pfold1<F, T>, 256, bytes) != cudaSuccess) n = 0;
+    template <int LP>
+    static int pfold_occupancy() {
+        static int n = -1;
+        if (n < 0) {
+            carve_l1(k_pfold1<F, T, LP>);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pfold1<F, T, LP>, 256, 0) != cudaSuccess) n = 0;
+        }
         return n;
     }
     static void pfold_hubs(const LaunchParams &p, int64_t nhub, const int32_t *tl, const int32_t *off,
@@ -1826,63 +1080,7 @@ struct Registrar {
     static void pfold2(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
         using AG = typename FirstInc<S>::type;
-        if (pass2_warp())
-            launch_k(k_pfold_rest_w<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
-        else
-            launch_k(k_pfold_rest<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
-    }
-    static void fold_targets(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
-        using S = typename F::template sig<T>;
-        constexpr int G = FirstInc<S>::value;
-        using AG = typename FirstInc<S>::type;
-        k_fold_targets<typename AG::type, AG::dim><<<g, b, 0, s>>>(p, G);
-    }
-    template <int NT>
-    static void tile_launch(const LaunchParams &p, dim3 g, size_t bytes, cudaStream_t s) {
-        static size_t opted = 48 * 1024;
-        if (bytes > opted) {
-            cudaFuncSetAttribute(k_tile<F, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-            opted = bytes;
-        }
-        k_tile<F, T, NT><<<g, NT, bytes, s>>>(p);
-    }
-    template <int NT>
-    static void tgather_launch(const LaunchParams &p, dim3 g, size_t bytes, cudaStream_t s) {
-        static size_t opted = 48 * 1024;
-        if (bytes > opted) {
-            cudaFuncSetAttribute(k_tgather<F, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-            opted = bytes;
-        }
-        k_tgather<F, T, NT><<<g, NT, bytes, s>>>(p);
-    }
-    static void tgather(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
-        if (b.x == 128) tgather_launch<128>(p, g, bytes, s);
-        else tgather_launch<256>(p, g, bytes, s);
-    }
-    static void tile(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
-        if (b.x == 128) tile_launch<128>(p, g, bytes, s);
-        else tile_launch<256>(p, g, bytes, s);
-    }
-    template <int MINB>
-    static void gather_occ(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
-        k_gather_occ<F, T, MINB><<<g, b, 0, s>>>(p);
-    }
-    static void arrive(const LaunchParams &p, dim3 g, dim3 b, size_t bytes, cudaStream_t s) {
-        static bool opted = false;
-        if (!opted && bytes > 48 * 1024) {
-            cudaFuncSetAttribute(k_arrive<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            opted = true;
-        }
-        k_arrive<F, T><<<g, b, bytes, s>>>(p);
-    }
-    template <int MODE>
-    static int flow_occupancy(int threads, size_t bytes) {
-        if (bytes > 48 * 1024)
-            cudaFuncSetAttribute(k_flow<F, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_flow<F, T, MODE>, threads, bytes) != cudaSuccess)
-            return 0;
-        return n;
+        launch_k(k_pfold_rest_w<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
     }
     explicit Registrar(const char *name) {
         using S = typename F::template sig<T>;
@@ -1893,42 +1091,32 @@ struct Registrar {
         SigInfo<S>::fill(e.kind, e.mode, e.dim, e.atype);
         e.ind_write = SigInfo<S>::ind_write;
         e.ind_write_non_inc = SigInfo<S>::ind_write_non_inc;
-        e.direct = &direct;
-        e.direct_occupancy = &direct_occupancy;
-        e.staged = SigInfo<S>::ind_write && !SigInfo<S>::ind_write_non_inc ? &staged : nullptr;
-        e.phased = SigInfo<S>::ind_write ? &phased : nullptr;
-        const bool st = e.staged != nullptr;
-        e.smem[0] = st ? &smem<ST_SMEM> : nullptr;
-        e.smem[1] = st ? &smem<ST_SEG> : nullptr;
-        e.flow[0] = st ? &flow<ST_SMEM> : nullptr;
-        e.flow[1] = st ? &flow<ST_SEG> : nullptr;
-        e.flow_occupancy[0] = st ? &flow_occupancy<ST_SMEM> : nullptr;
-        e.flow_occupancy[1] = st ? &flow_occupancy<ST_SEG> : nullptr;
-        e.arrive = st ? &arrive : nullptr;
+        if constexpr (!SigInfo<S>::ind_write) {
+            e.direct[0] = &direct<0>;
+            e.direct[1] = &direct<1>;
+            e.direct_occupancy[0] = &direct_occupancy<0>;
+            e.direct_occupancy[1] = &direct_occupancy<1>;
+        } else {
+            e.staged = !SigInfo<S>::ind_write_non_inc ? &staged : nullptr;
+            e.phased = &phased;
+        }
         if constexpr (SigInfo<S>::fold_ok) {
-            e.pfold1 = &pfold1;
+            e.pfold1[0] = &pfold1<0>;
+            e.pfold1[1] = &pfold1<1>;
+            e.pfold_occupancy[0] = &pfold_occupancy<0>;
+            e.pfold_occupancy[1] = &pfold_occupancy<1>;
             e.pfold2 = &pfold2;
-            e.pfold_occupancy = &pfold_occupancy;
             e.pfold_hubs = &pfold_hubs;
             using AG = typename FirstInc<S>::type;
             e.pfold_dgp = PFoldShape<typename AG::type, AG::dim>::DGP;
             e.pfold_nslot = SigInfo<S>::n_inc - 1;
-            e.fold_edges = &fold_edges;
-            e.fold_targets = &fold_targets;
-            e.fold_arg = FirstInc<S>::value;
-            e.fold_dim = FirstInc<S>::type::dim;
-        }
-        if constexpr (SigInfo<S>::tile_ok) {
-            e.tile = &tile;
-            e.tgather = &tgather;
         }
         if constexpr (SigInfo<S>::gather_ok && SigInfo<S>::ind_inc) e.gather_hubs = &gather_hubs;
         if constexpr (SigInfo<S>::gather_ok) {
-            e.gather_occupancy = &gather_occupancy;
-            e.gather[0] = &gather;
-            e.gather[1] = &gather_occ<2>;
-            e.gather[2] = &gather_occ<3>;
-            e.gather[3] = &gather_occ<4>;
+            e.gather[0] = &gather<0>;
+            e.gather[1] = &gather<1>;
+            e.gather_occupancy[0] = &gather_occupancy<0>;
+            e.gather_occupancy[1] = &gather_occupancy<1>;
         }
         register_functor(e);
     }

@@ -23,6 +23,7 @@ template <class V>
 using elem_t = cuda::std::remove_cv_t<cuda::std::remove_reference_t<decltype(cuda::std::declval<V>()[0])>>;
 
 struct Copy {
+    static constexpr bool dense_writes = true;   // every direct WRITE component is written
     template <class T> using sig = Sig<Arg<KD, MR, 1, T>, Arg<KD, MW, 1, T>>;
     template <class S, class D>
     __device__ static void apply(const Consts &, S src, D dst) { dst[0] = src[0]; }
@@ -50,6 +51,7 @@ struct BoundaryFix {
 };
 
 struct DiffusionUpdate {
+    static constexpr bool dense_writes = true;   // every direct WRITE component is written
     template <class T>
     using sig = Sig<Arg<KD, MW, 1, T>, Arg<KD, MR, 1, T>, Arg<KD, MRW, 1, T>, Arg<KG, MINC, 1, T>>;
     template <class U, class UP, class F, class R>
@@ -72,6 +74,7 @@ struct DiffusionUpdate {
 };
 
 struct TriArea {
+    static constexpr bool dense_writes = true;   // every direct WRITE component is written
     template <class T>
     using sig = Sig<Arg<KI, MR, 2, T>, Arg<KI, MR, 2, T>, Arg<KI, MR, 2, T>, Arg<KD, MW, 1, T>>;
     template <class C1, class C2, class C3, class O>
@@ -165,6 +168,7 @@ struct ScaleRW {   // test_executor.test_threads_direct_loop_is_exact_even_float
 };
 
 struct SetOne {   // test_executor.test_no_exchange_between_consecutive_reads ("init")
+    static constexpr bool dense_writes = true;   // every direct WRITE component is written
     template <class T> using sig = Sig<Arg<KD, MW, 1, T>>;
     template <class V>
     __device__ static void apply(const Consts &, V v) { v[0] = 1; }

@@ -12,6 +12,7 @@ namespace {
 constexpr int NQ = 6, NG = 18, NLIM = 8, NAUX = 19;
 
 struct ProxySave {
+    static constexpr bool dense_writes = true;   // every direct WRITE component is written
     template <class T> using sig = Sig<Arg<KD, MR, NQ, T>, Arg<KD, MW, NQ, T>>;
     template <class Q, class QO>
     __device__ static void apply(const Consts &, Q q, QO q_old) {
@@ -21,6 +22,7 @@ struct ProxySave {
 };
 
 struct ProxyDt {
+    static constexpr bool dense_writes = true;   // every direct WRITE component is written
     template <class T>
     using sig = Sig<Arg<KD, MR, NQ, T>, Arg<KD, MR, 1, T>, Arg<KD, MW, 1, T>, Arg<KG, MMIN, 1, T>>;
     template <class Q, class V, class D, class M>
@@ -38,6 +40,7 @@ struct ProxyDt {
 // pass copies q to q_old and computes the local time step from the same
 // loaded q row.
 struct ProxySaveDt {
+    static constexpr bool dense_writes = true;   // every direct WRITE component is written
     static constexpr int first_args[2] = {0, 1};           // save: q q_old
     static constexpr int second_args[4] = {0, 2, 3, 4};    // dt_calc: q vol dt_loc dt_min
     template <class T>
@@ -159,6 +162,7 @@ struct ProxyFluxes {
 };
 
 struct ProxyUpdate {
+    static constexpr bool dense_writes = true;   // every direct WRITE component is written
     template <class T>
     using sig = Sig<Arg<KD, MW, NQ, T>, Arg<KD, MR, NQ, T>, Arg<KD, MRW, NQ, T>, Arg<KD, MR, 1, T>,
                     Arg<KD, MW, NG, T>, Arg<KG, MR, 1, T>, Arg<KG, MINC, 1, T>>;

@@ -256,172 +256,3 @@ extern "C" int ml_plan_free(ml_plan_t *p) {
     delete p;
     return ML_OK;
 }
-
-// ---- staging lists for shared-memory increment accumulation -------------------------
-// Per block and per group (one INC dat), the ascending unique targets of the
-// group's columns over the block's elements, and for every (element, column)
-// the target's position in that list (uint16: a block has <= 65535 targets).
-struct ml_staging {
-    int64_t n = 0, bs = 1, nb = 0;
-    int32_t ngroups = 0;
-    std::vector<std::vector<int32_t>> off, list;   // per group
-    std::vector<int64_t> umax;                     // per group
-    std::vector<std::vector<uint16_t>> loc;        // per column
-    // segmented mode: per unique target (global index into list), its
-    // contributing (arg position, element in block) slots in element order
-    std::vector<std::vector<int32_t>> toff;        // per group [total+1]
-    std::vector<std::vector<uint16_t>> src;        // per group
-    // arrival mode: per list entry, the partial slot of a target shared by
-    // several blocks (-1: the block owns the target alone); per target id,
-    // the first slot and the number of blocks touching it
-    std::vector<std::vector<int32_t>> pslot, poff, nblk;
-    std::vector<int64_t> nslots;
-};
-
-extern "C" int ml_staging_build(int64_t n, int64_t block_size, int32_t ncols,
-                                const int64_t *const *cols, const int32_t *col_group,
-                                ml_staging_t **out) {
-    if (!out || block_size < 1 || n < 0 || ncols < 0) ML_FAIL(ML_EINVAL, "ml_staging_build: bad arguments");
-    ML_GUARD_BEGIN
-    auto s = std::make_unique<ml_staging>();
-    s->n = n;
-    s->bs = block_size;
-    s->nb = n ? (n + block_size - 1) / block_size : 0;
-    int32_t ng = 0;
-    for (int32_t j = 0; j < ncols; ++j) ng = std::max(ng, col_group[j] + 1);
-    s->ngroups = ng;
-    s->off.assign(ng, std::vector<int32_t>(size_t(s->nb) + 1, 0));
-    s->list.assign(ng, {});
-    s->umax.assign(ng, 0);
-    s->loc.assign(ncols, std::vector<uint16_t>(size_t(n), 0));
-    std::vector<int64_t> buf;
-    s->toff.assign(ng, {});
-    s->src.assign(ng, {});
-    struct Ref { int64_t tgt; int32_t elem, pos; };
-    std::vector<Ref> refs;
-    for (int32_t g = 0; g < ng; ++g) {
-        auto &list = s->list[g];
-        auto &toff = s->toff[g];
-        auto &src = s->src[g];
-        toff.push_back(0);
-        for (int64_t b = 0; b < s->nb; ++b) {
-            const int64_t lo = b * block_size, hi = std::min(n, lo + block_size);
-            buf.clear();
-            refs.clear();
-            int32_t pos = 0;
-            for (int32_t j = 0; j < ncols; ++j)
-                if (col_group[j] == g) {
-                    for (int64_t e = lo; e < hi; ++e) {
-                        buf.push_back(cols[j][e]);
-                        refs.push_back({cols[j][e], int32_t(e - lo), pos});
-                    }
-                    ++pos;
-                }
-            std::sort(buf.begin(), buf.end());
-            buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
-            if (buf.size() > 65535) throw std::length_error("more than 65535 staged targets in one block");
-            if (buf.size() && buf.back() >= (int64_t(1) << 31)) throw std::length_error("target id exceeds int32");
-            s->umax[g] = std::max<int64_t>(s->umax[g], int64_t(buf.size()));
-            for (int32_t j = 0; j < ncols; ++j)
-                if (col_group[j] == g)
-                    for (int64_t e = lo; e < hi; ++e)
-                        s->loc[j][e] = uint16_t(std::lower_bound(buf.begin(), buf.end(), cols[j][e]) - buf.begin());
-            for (int64_t t : buf) list.push_back(int32_t(t));
-            s->off[g][b + 1] = int32_t(list.size());
-            // contributions per target in element order, then argument order
-            std::sort(refs.begin(), refs.end(), [](const Ref &x, const Ref &y) {
-                if (x.tgt != y.tgt) return x.tgt < y.tgt;
-                if (x.elem != y.elem) return x.elem < y.elem;
-                return x.pos < y.pos;
-            });
-            size_t r = 0;
-            for (int64_t t : buf) {
-                while (r < refs.size() && refs[r].tgt == t) {
-                    if (refs[r].elem > 255 || refs[r].pos > 255)
-                        throw std::length_error("segmented staging needs block_size <= 256");
-                    src.push_back(uint16_t(refs[r].pos * 256 + refs[r].elem));
-                    ++r;
-                }
-                toff.push_back(int32_t(src.size()));
-            }
-        }
-    }
-    // arrival lists: blocks touching each target, in block order
-    s->pslot.assign(ng, {});
-    s->poff.assign(ng, {});
-    s->nblk.assign(ng, {});
-    s->nslots.assign(ng, 0);
-    for (int32_t g = 0; g < ng; ++g) {
-        const auto &list = s->list[g];
-        int64_t ntgt = 0;
-        for (int32_t t : list) ntgt = std::max<int64_t>(ntgt, int64_t(t) + 1);
-        auto &nblk = s->nblk[g];
-        auto &poff = s->poff[g];
-        nblk.assign(size_t(ntgt), 0);
-        for (int32_t t : list) nblk[t]++;
-        poff.assign(size_t(ntgt), -1);
-        int64_t slots = 0;
-        for (int64_t t = 0; t < ntgt; ++t)
-            if (nblk[t] > 1) {
-                poff[t] = int32_t(slots);
-                slots += nblk[t];
-            }
-        if (slots >= (int64_t(1) << 31)) throw std::length_error("too many partial slots");
-        s->nslots[g] = slots;
-        std::vector<int32_t> seen(size_t(ntgt), 0);
-        auto &pslot = s->pslot[g];
-        pslot.resize(list.size());
-        for (size_t k = 0; k < list.size(); ++k) {     // list is block-major: block order
-            const int32_t t = list[k];
-            pslot[k] = nblk[t] > 1 ? poff[t] + seen[t]++ : -1;
-        }
-    }
-    *out = s.release();
-    return ML_OK;
-    ML_GUARD_END
-}
-
-extern "C" int ml_staging_sizes(const ml_staging_t *s, int32_t g, int64_t *total, int64_t *umax) {
-    if (!s || g < 0 || g >= s->ngroups) ML_FAIL(ML_EINVAL, "ml_staging_sizes: bad group");
-    if (total) *total = int64_t(s->list[g].size());
-    if (umax) *umax = s->umax[g];
-    return ML_OK;
-}
-
-extern "C" int ml_staging_export(const ml_staging_t *s, int32_t g, int32_t *off, int32_t *list) {
-    if (!s || g < 0 || g >= s->ngroups) ML_FAIL(ML_EINVAL, "ml_staging_export: bad group");
-    if (off) std::copy(s->off[g].begin(), s->off[g].end(), off);
-    if (list) std::copy(s->list[g].begin(), s->list[g].end(), list);
-    return ML_OK;
-}
-
-extern "C" int ml_staging_export_loc(const ml_staging_t *s, int32_t col, uint16_t *loc) {
-    if (!s || col < 0 || col >= int32_t(s->loc.size())) ML_FAIL(ML_EINVAL, "ml_staging_export_loc: bad column");
-    std::copy(s->loc[col].begin(), s->loc[col].end(), loc);
-    return ML_OK;
-}
-
-extern "C" int ml_staging_export_seg(const ml_staging_t *s, int32_t g, int64_t *nrefs, int32_t *toff,
-                                     uint16_t *src) {
-    if (!s || g < 0 || g >= s->ngroups) ML_FAIL(ML_EINVAL, "ml_staging_export_seg: bad group");
-    if (nrefs) *nrefs = int64_t(s->src[g].size());
-    if (toff) std::copy(s->toff[g].begin(), s->toff[g].end(), toff);
-    if (src) std::copy(s->src[g].begin(), s->src[g].end(), src);
-    return ML_OK;
-}
-
-extern "C" int ml_staging_export_arrival(const ml_staging_t *s, int32_t g, int64_t *ntargets,
-                                         int64_t *nslots, int32_t *pslot, int32_t *poff, int32_t *nblk) {
-    if (!s || g < 0 || g >= s->ngroups) ML_FAIL(ML_EINVAL, "ml_staging_export_arrival: bad group");
-    if (ntargets) *ntargets = int64_t(s->nblk[g].size());
-    if (nslots) *nslots = s->nslots[g];
-    if (pslot) std::copy(s->pslot[g].begin(), s->pslot[g].end(), pslot);
-    if (poff) std::copy(s->poff[g].begin(), s->poff[g].end(), poff);
-    if (nblk) std::copy(s->nblk[g].begin(), s->nblk[g].end(), nblk);
-    return ML_OK;
-}
-
-extern "C" int ml_staging_free(ml_staging_t *s) {
-    delete s;
-    return ML_OK;
-}

@@ -8,6 +8,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "engine.cuh"
@@ -68,14 +69,6 @@ bool pdl_enabled() {
     return on;
 }
 
-bool pass2_warp() {
-    static const bool on = [] {
-        const char *e = std::getenv("ML_PASS2W");       // ML_PASS2W=0: thread-per-row pass 2
-        return e ? std::atoi(e) != 0 : true;
-    }();
-    return on;
-}
-
 template <class T, int M>
 __global__ void __launch_bounds__(256) k_combine(T *g, const T *part, int64_t nparts, int dim) {
     pdl_wait();
@@ -98,32 +91,6 @@ static void launch_combine(int mode, T *g, const T *part, int64_t nparts, int di
 
 static int round_up32(int64_t x) { return int((x + 31) / 32 * 32); }
 
-// k_gather occupancy variant: ML_GATHER_MINB unset/0/1 = the compiler's register
-// choice; 2, 3 or 4 = registers capped for that many resident CTAs of 256 per SM
-static int gather_variant() {
-    static const int v = [] {
-        const char *s = std::getenv("ML_GATHER_MINB");
-        const int m = s ? std::atoi(s) : 0;
-        return m <= 1 ? 0 : m >= 4 ? 3 : m - 1;
-    }();
-    return v;
-}
-
-// k_gather grid: persistent by default — as many CTAs as fit on the SMs at
-// once, grid-striding over the targets (each SM keeps exactly its resident
-// CTAs busy, no tail wave).  ML_GATHER_GRID=k forces k CTAs per SM, "full"
-// one CTA per 256 targets.
-static int gather_grid_per_sm(const FunctorEntry &f) {
-    static const int v = [] {
-        const char *s = std::getenv("ML_GATHER_GRID");
-        if (!s) return -1;
-        if (std::string(s) == "full") return 0;
-        return std::max(0, std::atoi(s));
-    }();
-    if (v >= 0) return v;
-    return f.gather_occupancy ? f.gather_occupancy() : 0;
-}
-
 static int validate(const ml_loop_t *L, const FunctorEntry &f) {
     const char *nm = L->name ? L->name : "?";
     if (L->nargs != f.nargs)
@@ -141,75 +108,50 @@ static int validate(const ml_loop_t *L, const FunctorEntry &f) {
             ML_FAIL(ML_EINVAL, "loop '%s' arg %d: null device pointer", nm, i);
         if (a.kind == ML_INDIRECT && !a.map && L->n > 0)
             ML_FAIL(ML_EINVAL, "loop '%s' arg %d: indirect arg without device map", nm, i);
+        if (a.kind != ML_GLOBAL && a.layout == ML_SOA && a.pitch != 0 && a.pitch < a.set_size)
+            ML_FAIL(ML_EINVAL, "loop '%s' arg %d: SOA pitch %lld below the set size %lld", nm, i,
+                    (long long)a.pitch, (long long)a.set_size);
     }
     return ML_OK;
+}
+
+// Layout policy of a launch (engine.cuh): 1 when every dat argument follows the
+// reference's auto-SOA policy (dim <= 4 AOS — or any layout at dim 1 — wider
+// dats SOA) with 16-byte aligned payloads and an even SOA pitch, so the
+// compile-time strides of the LP = 1 kernels apply; 0 otherwise.
+static int layout_policy(const ml_loop_t *L) {
+    for (int i = 0; i < L->nargs; ++i) {
+        const ml_arg_t &a = L->args[i];
+        if (a.kind == ML_GLOBAL) continue;
+        if (a.dim > AUTO_SOA_DIM) {
+            const int64_t pitch = a.pitch ? a.pitch : a.set_size;
+            if (a.layout != ML_SOA || (pitch & 1)) return 0;
+        } else if (a.dim > 1 && a.layout != ML_AOS) {
+            return 0;
+        }
+        if (reinterpret_cast<uintptr_t>(a.data) & 15) return 0;
+    }
+    return 1;
 }
 
 static uint64_t scratch_bytes(const ml_loop_t *L, const FunctorEntry &f) {
     uint64_t bytes = 0;
     const int64_t nb = std::max<int64_t>({L->plan.nblocks, (L->gather_ntargets + 255) / 256,
-                                          (L->n + 255) / 256, L->tile_count, int64_t(1)});
+                                          (L->n + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i)
         if (f.kind[i] == KG && f.mode[i] != MR) bytes += uint64_t(nb) * f.dim[i] * 8 + 256;
     return bytes;
 }
 
-// Tile schedule parameters: READ dats staged per tile (one group per distinct
-// dat), INC dats accumulated per owned target; all indirect args on one map.
-static int tile_setup(const ml_loop_t *L, const FunctorEntry &f, LaunchParams &p, size_t &smem) {
-    const char *nm = L->name ? L->name : "?";
-    if (!f.tile) ML_FAIL(ML_EINVAL, "loop '%s': functor '%s' has no tile schedule", nm, f.name);
-    if (!L->tile_list_off || !L->tile_nown || !L->tile_list || !L->tile_elem_off || !L->tile_elem ||
-        !L->tile_ncol || !L->tile_loc || !L->tile_ecol || L->tile_arity < 1)
-        ML_FAIL(ML_EINVAL, "loop '%s': tile plan arrays missing", nm);
-    TileParams &t = p.t;
-    t.list_off = L->tile_list_off;
-    t.nown = L->tile_nown;
-    t.list = L->tile_list;
-    t.elem_off = L->tile_elem_off;
-    t.elem = L->tile_elem;
-    t.ncol = L->tile_ncol;
-    t.loc = L->tile_loc;
-    t.ecol = L->tile_ecol;
-    t.arity = L->tile_arity;
-    const int32_t *map0 = nullptr;
-    const void *gdat[MAX_TGROUPS] = {};
-    int nr = 0, ni = 0;
-    for (int pass = 0; pass < 2; ++pass)             // READ groups first, then INC groups
-        for (int i = 0; i < f.nargs; ++i) {
-            const ml_arg_t &a = L->args[i];
-            if (a.kind != ML_INDIRECT) continue;
-            if (!map0) map0 = a.map;
-            if (a.map != map0) ML_FAIL(ML_EINVAL, "loop '%s': tile schedule needs one map", nm);
-            if (a.slot < 0 || a.slot >= L->tile_arity) ML_FAIL(ML_EINVAL, "loop '%s': bad slot", nm);
-            const bool inc = a.mode == ML_INC;
-            if (inc != (pass == 1)) continue;
-            int g = -1;
-            for (int k = (inc ? nr : 0); k < (inc ? nr + ni : nr); ++k)
-                if (gdat[k] == a.data) g = k;
-            if (g < 0) {
-                g = nr + ni;
-                if (g >= MAX_TGROUPS) ML_FAIL(ML_EINVAL, "loop '%s': too many dats for the tile schedule", nm);
-                gdat[g] = a.data;
-                t.garg[g] = i;
-                t.gdim[g] = a.dim;
-                (inc ? ni : nr)++;
-            }
-            t.grp[i] = int8_t(g);
-            t.slot[i] = int8_t(a.slot);
-        }
-    for (int g = nr; g < nr + ni; ++g)
-        for (int i = 0; i < f.nargs; ++i)
-            if (L->args[i].kind != ML_GLOBAL && L->args[i].mode != ML_INC && L->args[i].data == gdat[g])
-                ML_FAIL(ML_EINVAL, "loop '%s': an INC dat is also accessed otherwise (tile schedule)", nm);
-    t.nread = nr;
-    t.ninc = ni;
-    smem = tile_align(size_t(L->tile_umax) * 4);
-    for (int g = 0; g < nr + ni; ++g)
-        smem += tile_align(size_t(8) * t.gdim[g] * size_t(g < nr ? L->tile_umax : L->tile_cmax));
-    if (smem > 227 * 1024)
-        ML_FAIL(ML_EINVAL, "loop '%s': tile needs %zu bytes of shared memory", nm, smem);
-    return ML_OK;
+// resident-CTA counts per (functor, kernel, threads) — occupancy queries are not free
+static int cached_occupancy(int functor, int kernel, int threads, int (*query)(int)) {
+    static std::vector<std::pair<std::tuple<int, int, int>, int>> cache;
+    const auto key = std::make_tuple(functor, kernel, threads);
+    for (auto &kv : cache)
+        if (kv.first == key) return kv.second;
+    const int occ = query ? query(threads) : 0;
+    cache.push_back({key, occ});
+    return occ;
 }
 
 static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
@@ -229,14 +171,13 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     p.n = L->n;
     p.rlim = L->rlim < 0 ? L->n : L->rlim;
     p.bs = int32_t(bs);
-    for (int i = 0; i < MAX_ARGS; ++i) p.st.group[i] = -1;
     for (int i = 0; i < 4; ++i) {
         p.k.f[i] = L->fconst[i];
         p.k.i[i] = L->iconst[i];
     }
     char *scratch = static_cast<char *>(L->scratch);
     const int64_t pstride = std::max<int64_t>({nb, (L->gather_ntargets + 255) / 256,
-                                               (L->n + 255) / 256, L->tile_count, int64_t(1)});
+                                               (L->n + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i) {
         const ml_arg_t &a = L->args[i];
         ArgRt &r = p.a[i];
@@ -255,73 +196,16 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
             r.sc = 1;
         } else {
             r.se = 1;
-            r.sc = a.set_size;
+            r.sc = a.pitch ? a.pitch : a.set_size;
         }
     }
-
-    // shared-memory staging of INC increments (every INC-indirect arg in a group)
-    size_t smem_bytes = 0;
-    bool use_smem = false;
-    const ml_staging_dev_t &sg = L->staging;
-    const int seg = sg.seg ? 1 : 0;
-    const int sthreads = round_up32(bs);
-    if (f.smem[seg] && bs <= 256 && sg.ngroups > 0 && sg.ngroups <= MAX_GROUPS) {
-        use_smem = true;
-        int leader[MAX_GROUPS] = {-1, -1}, count[MAX_GROUPS] = {0, 0};
-        for (int i = 0; i < f.nargs; ++i) {
-            const bool inc = f.kind[i] == KI && f.mode[i] == MINC;
-            const int g = sg.group[i];
-            if (inc != (g >= 0) || g >= sg.ngroups || (inc && !seg && !sg.loc[i]) ||
-                (inc && seg && (!sg.toff[g] || !sg.src[g]))) {
-                use_smem = false;
-                break;
-            }
-            if (g < 0) continue;
-            p.st.group[i] = g;
-            p.st.loc[i] = sg.loc[i];
-            p.st.gpos[i] = count[g]++;
-            if (leader[g] < 0) {
-                leader[g] = i;
-                p.st.leader[i] = 1;
-                p.st.off[g] = sg.off[g];
-                p.st.list[g] = sg.list[g];
-                p.st.umax[g] = sg.umax[g];
-                p.st.toff[g] = sg.toff[g];
-                p.st.src[g] = sg.src[g];
-            }
-        }
-        for (int g = 0; use_smem && g < sg.ngroups; ++g) {
-            if (leader[g] < 0) { use_smem = false; break; }
-            p.st.soff[g] = int32_t(smem_bytes);
-            const size_t slots = seg ? size_t(count[g]) * sthreads : size_t(sg.umax[g]);
-            smem_bytes += (slots * f.dim[leader[g]] * 8 + 15) / 16 * 16;
-        }
-        if (use_smem && seg && sg.arrive) {
-            for (int g = 0; g < sg.ngroups; ++g) {
-                if (!sg.pslot[g] || !sg.poff[g] || !sg.nblk[g] || !sg.count[g] || !sg.partial[g])
-                    ML_FAIL(ML_EINVAL, "loop '%s': arrival staging lists missing", L->name);
-                p.st.pslot[g] = sg.pslot[g];
-                p.st.poff[g] = sg.poff[g];
-                p.st.nblk[g] = sg.nblk[g];
-                p.st.count[g] = sg.count[g];
-                p.st.partial[g] = sg.partial[g];
-                p.st.foff[g] = int32_t(smem_bytes);
-                smem_bytes += (size_t(sg.umax[g]) * 4 + 15) / 16 * 16;
-            }
-        }
-        if (!use_smem || smem_bytes > 200 * 1024) {
-            use_smem = false;
-            smem_bytes = 0;
-            for (int i = 0; i < MAX_ARGS; ++i) p.st.group[i] = -1;
-        }
-    }
+    const int lp = layout_policy(L);
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
-    const bool lists = L->gather_ntargets > 0 && L->gather_off && L->gather_elem && L->gather_pos;
     if (L->pf_n1 > 0) {
         // primary fold: pass 1 over targets' primary incidences (persistent grid),
         // pass 2 folds the secondary slots
-        if (!f.pfold1 || !L->pf_off1 || !L->pf_elem1 || (f.pfold_nslot > 0 && (!L->pf_slots ||
+        if (!f.pfold1[0] || !L->pf_off1 || !L->pf_elem1 || (f.pfold_nslot > 0 && (!L->pf_slots ||
             (L->pf_n2 > 0 && (!L->pf_off2 || !L->pf_elem2 || !L->pf_pos2)))))
             ML_FAIL(ML_EINVAL, "loop '%s': primary-fold lists missing", L->name);
         PFoldParams &pf = p.pf;
@@ -353,99 +237,28 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
             for (int i = 0; i < f.nargs; ++i)
                 if (L->args[i].kind == ML_INDIRECT && (pf.rcol[i] < 0 || pf.rcol[i] >= pf.ncol))
                     ML_FAIL(ML_EINVAL, "loop '%s': pfold record column of argument %d out of range", L->name, i);
-        // own-row staging: READ dats on the first INC argument's column
-        pf.own_ngrp = 0;
-        for (int i = 0; i < MAX_ARGS; ++i) pf.own_grp[i] = -1;
-        size_t own_bytes = 0;
-        if (L->pf_own_kb > 0) {
-            int g0 = -1;
-            for (int i = 0; i < f.nargs && g0 < 0; ++i)
-                if (L->args[i].kind == ML_INDIRECT && L->args[i].mode == ML_INC) g0 = i;
-            const void *gdat[MAX_TGROUPS] = {};
-            int comps = 0;
-            const int budget = L->pf_own_kb * 1024 / (8 * 256);
-            for (int i = 0; i < f.nargs && g0 >= 0; ++i) {
-                const ml_arg_t &a = L->args[i];
-                if (a.kind != ML_INDIRECT || a.mode != ML_READ || p.a[i].map != p.a[g0].map) continue;
-                int g = -1;
-                for (int k = 0; k < pf.own_ngrp; ++k)
-                    if (gdat[k] == a.data) g = k;
-                if (g < 0) {
-                    if (pf.own_ngrp >= MAX_TGROUPS || comps + a.dim > budget) continue;
-                    g = pf.own_ngrp++;
-                    gdat[g] = a.data;
-                    pf.own_garg[g] = i;
-                    pf.own_gdim[g] = a.dim;
-                    pf.own_goff[g] = comps;
-                    comps += a.dim;
-                }
-                pf.own_grp[i] = int8_t(g);
-            }
-            own_bytes = size_t(comps) * 8 * 256;
-        }
-        const int occ = f.pfold_occupancy ? f.pfold_occupancy(own_bytes) : 0;
+        const int occ = f.pfold_occupancy[lp] ? f.pfold_occupancy[lp]() : 0;
         nparts = std::max<int64_t>(1, std::min<int64_t>((pf.n1 + 255) / 256,
                                                         occ > 0 ? int64_t(occ) * g_dev.sm_count : INT64_MAX));
         if (nparts > pstride) ML_FAIL(ML_EINVAL, "loop '%s': primary fold needs more scratch", L->name);
-        f.pfold1(p, dim3(unsigned(nparts)), dim3(256), own_bytes, stream);
+        f.pfold1[lp](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
         if (L->pf_nhub1 > 0) f.pfold_hubs(p, L->pf_nhub1, L->pf_hub1_tl, L->pf_hub1_off, pf.part1, stream);
         if (pf.n2 > 0) {
             const int64_t g2 = std::min<int64_t>((pf.n2 + 255) / 256, int64_t(8) * g_dev.sm_count);
             f.pfold2(p, dim3(unsigned(g2)), dim3(256), 0, stream);
             if (L->pf_nhub2 > 0) f.pfold_hubs(p, L->pf_nhub2, L->pf_hub2_tl, L->pf_hub2_off, pf.part2, stream);
         }
-    }
-    size_t tile_smem = 0;
-    if (L->pf_n1 > 0) {
-    } else if (L->tile_count > 0) {
-        rc = tile_setup(L, f, p, tile_smem);
-        if (rc) return rc;
-    }
-    if (L->pf_n1 > 0) {
-        // launched above
-    } else if (L->tile_count > 0) {
-        // tile schedule: one CTA per tile, owner-computes, no inter-CTA conflicts
-        nparts = L->tile_count;
-        p.g_buf = L->fold_buf;   // per-tile phase timings when built with ML_TILE_PROFILE
-        if (L->tile_inc_off) {
-            // tile-gather: staged READ rows only; one INC dat
-            if (!L->tile_inc_base || !L->tile_inc_k || !L->tile_inc_c || !f.tgather || p.t.ninc != 1)
-                ML_FAIL(ML_EINVAL, "loop '%s': tile-gather needs its incidence lists and one INC dat", L->name);
-            p.t.inc_base = L->tile_inc_base;
-            p.t.inc_off = L->tile_inc_off;
-            p.t.inc_k = L->tile_inc_k;
-            p.t.inc_c = L->tile_inc_c;
-            int rc2 = -1;
-            for (int i = 0; i < f.nargs && rc2 < 0; ++i)
-                if (L->args[i].kind == ML_INDIRECT && L->args[i].mode == ML_INC) rc2 = L->args[i].slot;
-            p.t.red_col = rc2;
-            const size_t smem = tile_smem - tile_align(size_t(8) * p.t.gdim[p.t.nread] * size_t(L->tile_cmax));
-            f.tgather(p, dim3(unsigned(L->tile_count)), dim3(L->tile_threads == 128 ? 128 : 256), smem, stream);
-        } else
-        f.tile(p, dim3(unsigned(L->tile_count)), dim3(L->tile_threads == 128 ? 128 : 256), tile_smem, stream);
-    } else if (L->fold_buf && f.fold_edges && lists) {
-        // fold: each element once -> increment slots; then per target, serial order
-        p.g_ntargets = L->gather_ntargets;
-        p.g_off = L->gather_off;
-        p.g_elem = L->gather_elem;
-        p.g_pos = L->gather_pos;
-        p.g_tlist = L->gather_targets;
-        p.g_buf = L->fold_buf;
-        p.g_nw = 0;
-        for (int i = 0; i < f.nargs; ++i) p.g_nw += (f.kind[i] == KI && f.mode[i] == MINC) ? 1 : 0;
-        nparts = (L->n + 255) / 256;
-        f.fold_edges(p, dim3(unsigned(nparts)), dim3(256), 0, stream);
-        f.fold_targets(p, dim3(unsigned((L->gather_ntargets + 255) / 256)), dim3(256), 0, stream);
     } else if (f.ind_write && f.gather[0] && L->gather_ntargets > 0 && L->gather_off && L->gather_elem &&
-        L->gather_pos) {
-        // target-centric: one thread per target, serial-order accumulation
+               L->gather_pos) {
+        // target-centric: one thread per target, serial-order accumulation,
+        // persistent grid (resident CTAs x SMs striding over the targets)
         p.g_ntargets = L->gather_ntargets;
         p.g_off = L->gather_off;
         p.g_elem = L->gather_elem;
         p.g_pos = L->gather_pos;
         p.g_tlist = L->gather_targets;
         nparts = (L->gather_ntargets + 255) / 256;
-        if (const int per_sm = gather_grid_per_sm(f); per_sm > 0)
+        if (const int per_sm = f.gather_occupancy[lp] ? f.gather_occupancy[lp]() : 0; per_sm > 0)
             nparts = std::min<int64_t>(nparts, int64_t(per_sm) * g_dev.sm_count);
         if (nparts > pstride)
             ML_FAIL(ML_EINVAL, "loop '%s': gather schedule needs more reduction scratch", L->name);
@@ -458,57 +271,33 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
             p.g_hub_tl = L->gather_hub_tl;
             p.g_hub_off = L->gather_hub_off;
         }
-        f.gather[gather_variant()](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+        f.gather[lp](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
         if (L->gather_seg && L->gather_nhub > 0)
             f.gather_hubs(p, dim3(unsigned((L->gather_nhub + 255) / 256)), dim3(256), 0, stream);
     } else if (!f.ind_write) {
-        const int threads = std::clamp(round_up32(bs), 32, 256);
-        p.blocks = nullptr;
-        // persistent grid: resident CTAs x SMs (occupancy cached per block size)
-        static std::vector<std::pair<std::pair<int, int>, int>> occ_cache;
-        int occ = -1;
-        for (auto &kv : occ_cache)
-            if (kv.first == std::make_pair(L->functor, threads)) occ = kv.second;
-        if (occ < 0) {
-            occ = f.direct_occupancy ? f.direct_occupancy(threads) : 0;
-            occ_cache.push_back({{L->functor, threads}, occ});
-        }
-        nparts = occ > 0 ? std::min<int64_t>(nb, int64_t(occ) * g_dev.sm_count) : nb;
-        f.direct(p, dim3(unsigned(nparts)), dim3(unsigned(threads)), 0, stream);
+        // direct: persistent grid (resident CTAs x SMs); LP = 1 threads own two
+        // elements each (16-byte direct accesses)
+        const int threads = 256;
+        const int occ = cached_occupancy(L->functor, lp, threads, f.direct_occupancy[lp]);
+        const int64_t per = lp ? 2 * threads : threads;
+        nparts = std::max<int64_t>(1, (L->n + per - 1) / per);
+        if (occ > 0) nparts = std::min<int64_t>(nparts, int64_t(occ) * g_dev.sm_count);
+        if (nparts > pstride) ML_FAIL(ML_EINVAL, "loop '%s': direct loop needs more scratch", L->name);
+        f.direct[lp](p, dim3(unsigned(nparts)), dim3(unsigned(threads)), 0, stream);
     } else {
+        // the reference plan's colours: one launch per block colour
         if (!L->plan.color_offsets || !L->plan.blocks || !L->plan.elem_color || !L->plan.elem_ncolors)
             ML_FAIL(ML_EINVAL, "loop '%s': indirect writes need a coloured plan", L->name);
         p.ecol = L->plan.elem_color;
         p.encol = L->plan.elem_ncolors;
         const bool staged = f.staged && bs <= 256;
-        const LaunchFn fn = use_smem ? f.smem[seg] : (staged ? f.staged : f.phased);
+        const LaunchFn fn = staged ? f.staged : f.phased;
         const int threads = staged ? round_up32(bs) : std::clamp(round_up32(bs), 32, 256);
-        int occ = 0;
-        const bool arrive = use_smem && seg && sg.arrive && f.arrive;
-        if (!arrive && use_smem && f.flow[seg] && L->plan.queue && L->plan.dep_off && L->plan.dep_list &&
-            L->plan.flow_state && L->plan.ncolors > 1)
-            occ = f.flow_occupancy[seg](threads, smem_bytes);
-        if (arrive) {
-            // one launch, blocks in natural order, no colours (see run_arrive)
-            p.blocks = nullptr;
-            f.arrive(p, dim3(unsigned(nb)), dim3(unsigned(threads)), smem_bytes, stream);
-            occ = -1;
-        } else if (occ > 0) {
-            // one persistent launch: dataflow over the colour-ordered block queue
-            const int64_t grid = std::min<int64_t>(nb, int64_t(occ) * g_dev.sm_count);
-            ML_CUDA(cudaMemsetAsync(L->plan.flow_state, 0, size_t(nb + 1) * sizeof(int32_t), stream));
-            p.blocks = L->plan.queue;
-            p.dep_off = L->plan.dep_off;
-            p.dep_list = L->plan.dep_list;
-            p.flags = L->plan.flow_state;
-            p.nqueue = int32_t(nb);
-            f.flow[seg](p, dim3(unsigned(grid)), dim3(unsigned(threads)), smem_bytes, stream);
-        }
-        for (int64_t c = 0; occ == 0 && c < L->plan.ncolors; ++c) {
+        for (int64_t c = 0; c < L->plan.ncolors; ++c) {
             const int64_t off = L->plan.color_offsets[c], cnt = L->plan.color_offsets[c + 1] - off;
             if (cnt <= 0) continue;
             p.blocks = L->plan.blocks + off;
-            fn(p, dim3(unsigned(cnt)), dim3(unsigned(threads)), smem_bytes, stream);
+            fn(p, dim3(unsigned(cnt)), dim3(unsigned(threads)), 0, stream);
         }
     }
     cudaError_t err = cudaGetLastError();
@@ -636,6 +425,39 @@ extern "C" int ml_memset(void *dst, int value, uint64_t bytes) {
     if (bytes) ML_CUDA(cudaMemsetAsync(dst, value, bytes, g_dev.stream));
     return ML_OK;
 }
+extern "C" int ml_upload2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
+                           uint64_t height) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (width && height)
+        ML_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice, g_dev.stream));
+    return ML_OK;
+}
+extern "C" int ml_download2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
+                             uint64_t height) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (width && height)
+        ML_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, g_dev.stream));
+    ML_CUDA(cudaStreamSynchronize(g_dev.stream));
+    return ML_OK;
+}
+extern "C" int ml_copy_h2d_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
+                              uint64_t height) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (width && height)
+        ML_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice, g_dev.copy[0]));
+    return ML_OK;
+}
+extern "C" int ml_copy_d2h_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
+                              uint64_t height) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (width && height)
+        ML_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, g_dev.copy[1]));
+    return ML_OK;
+}
 static cudaStream_t stream_of(int32_t which) {
     return which == ML_STREAM_H2D ? g_dev.copy[0] : which == ML_STREAM_D2H ? g_dev.copy[1] : g_dev.stream;
 }
@@ -754,7 +576,7 @@ extern "C" int ml_loop_pfold_slot_bytes(const ml_loop_t *L, uint64_t *bytes) {
     if (!L || !bytes || L->functor < 0 || L->functor >= int(reg.size()))
         ML_FAIL(ML_EINVAL, "ml_loop_pfold_slot_bytes: bad arguments");
     const FunctorEntry &f = reg[L->functor];
-    *bytes = f.pfold1 ? uint64_t(L->n) * uint64_t(f.pfold_nslot) * uint64_t(f.pfold_dgp) * 8 : 0;
+    *bytes = f.pfold1[0] ? uint64_t(L->n) * uint64_t(f.pfold_nslot) * uint64_t(f.pfold_dgp) * 8 : 0;
     return ML_OK;
 }
 

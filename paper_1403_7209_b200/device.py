@@ -2,9 +2,11 @@
 
 Layout in HBM:
 
-* a dat is one contiguous float64/int64 buffer in the dat's own layout
-  (AOS ``e*dim+c`` or SOA ``c*size+e``), uploaded on first use and kept
-  resident across ``run_program`` calls;
+* a dat is one float64/int64 buffer in the dat's own layout — AOS
+  ``e*dim+c`` as on the host, SOA ``c*pitch+e`` with the component rows
+  padded to a 256-byte multiple (``device_pitch``; pitched 2-D copies to and
+  from the host's ``c*size+e``) — uploaded on first use and kept resident
+  across ``run_program`` calls;
 * a map is stored int32 and column-major (``[arity][from_size]``), so the
   index reads of one map column by consecutive elements are coalesced and
   cost 4 B per element instead of the host table's 8 B;
@@ -22,13 +24,31 @@ import numpy as np
 from . import _native as N
 from .core import AOS, Dat, ExecError, Map
 
-__all__ = ["DatMirror", "dat_mirror", "map_mirror", "plan_mirror", "pin_mesh"]
+__all__ = ["DatMirror", "dat_mirror", "device_pitch", "map_mirror", "plan_mirror", "pin_mesh",
+           "gather_mirror", "pfold_mirror", "gather_eligible", "fold_eligible", "PITCH_ALIGN"]
+
+
+#: SOA component rows of a device copy are padded to a multiple of this many
+#: elements (256 bytes of float64/int64): every component row starts 256-byte
+#: aligned, so the 16-byte direct accesses and full-sector gathers stay aligned
+PITCH_ALIGN = 32
+
+
+def device_pitch(dat: Dat) -> int:
+    """Component stride (elements) of ``dat``'s device copy: the set size for
+    AOS and single-component dats, the set size rounded up to PITCH_ALIGN for
+    SOA dats of dim > 1."""
+    n = dat.set.size
+    if dat.layout is AOS or dat.dim == 1:
+        return n
+    return -(-n // PITCH_ALIGN) * PITCH_ALIGN
 
 
 class DatMirror:
-    """Device copy of one dat payload."""
+    """Device copy of one dat payload: AOS rows as on the host; SOA component
+    rows at ``pitch`` elements (host pitch: the set size)."""
 
-    __slots__ = ("buf", "layout", "nbytes", "host_newer", "device_newer")
+    __slots__ = ("buf", "layout", "nbytes", "host_newer", "device_newer", "pitch", "rows", "row_bytes")
 
     def __init__(self):
         self.buf = None
@@ -36,17 +56,67 @@ class DatMirror:
         self.nbytes = -1
         self.host_newer = True
         self.device_newer = False
+        self.pitch = 0
+        self.rows = 1            # > 1: pitched SOA copy of `rows` component rows
+        self.row_bytes = 0       # host bytes of one component row
 
     @property
     def ptr(self) -> int:
         return self.buf.ptr if self.buf is not None else 0
 
+    @property
+    def padded(self) -> bool:
+        return self.rows > 1
+
+    def strides(self, dat: Dat) -> tuple[int, int]:
+        """(element stride, component stride) of the device copy, in elements."""
+        return (dat.dim, 1) if dat.layout is AOS else (1, self.pitch)
+
+    def upload(self, host: np.ndarray) -> None:
+        if self.buf is None or not host.nbytes:
+            return
+        if self.padded:
+            isz = host.dtype.itemsize
+            N.check(N.lib().ml_upload2d(self.buf.ptr, self.pitch * isz, N.ptr(host), self.row_bytes,
+                                        self.row_bytes, self.rows), "ml_upload2d")
+        else:
+            self.buf.upload(host)
+
     def download(self, host: np.ndarray) -> None:
         if self.buf is not None and host.nbytes:
             if not host.flags.c_contiguous:
                 raise ExecError("dat payload must be contiguous to receive device data")
-            self.buf.download(host)
+            if self.padded:
+                isz = host.dtype.itemsize
+                N.check(N.lib().ml_download2d(N.ptr(host), self.row_bytes, self.buf.ptr, self.pitch * isz,
+                                              self.row_bytes, self.rows), "ml_download2d")
+            else:
+                self.buf.download(host)
         self.device_newer = False
+
+    def copy_h2d(self, host: np.ndarray) -> None:
+        """Asynchronous upload on the H2D copy stream (streamed residency)."""
+        if self.buf is None or not host.nbytes:
+            return
+        L = N.lib()
+        if self.padded:
+            isz = host.dtype.itemsize
+            N.check(L.ml_copy_h2d_2d(self.buf.ptr, self.pitch * isz, N.ptr(host), self.row_bytes,
+                                     self.row_bytes, self.rows), "ml_copy_h2d_2d")
+        else:
+            N.check(L.ml_copy_h2d(self.buf.ptr, N.ptr(host), host.nbytes), "ml_copy_h2d")
+
+    def copy_d2h(self, host: np.ndarray) -> None:
+        """Asynchronous download on the D2H copy stream (streamed residency)."""
+        if self.buf is None or not host.nbytes:
+            return
+        L = N.lib()
+        if self.padded:
+            isz = host.dtype.itemsize
+            N.check(L.ml_copy_d2h_2d(N.ptr(host), self.row_bytes, self.buf.ptr, self.pitch * isz,
+                                     self.row_bytes, self.rows), "ml_copy_d2h_2d")
+        else:
+            N.check(L.ml_copy_d2h(N.ptr(host), self.buf.ptr, host.nbytes), "ml_copy_d2h")
 
 
 def dat_mirror(dat: Dat, force_upload: bool = False, upload: bool = True) -> DatMirror:
@@ -56,12 +126,18 @@ def dat_mirror(dat: Dat, force_upload: bool = False, upload: bool = True) -> Dat
     if m is None:
         m = dat._dev = DatMirror()
     host = dat._host
-    if m.buf is None or m.nbytes != host.nbytes:
+    pitch = device_pitch(dat)
+    dev_bytes = dat.dim * pitch * host.dtype.itemsize if host.nbytes else 0
+    if m.buf is None or m.nbytes != dev_bytes or m.pitch != pitch:
         if m.device_newer:
             raise ExecError(f"dat {dat.name!r}: payload resized while device data is newer")
-        m.buf = N.DeviceBuffer(host.nbytes) if host.nbytes else None
-        m.nbytes = host.nbytes
+        m.buf = N.DeviceBuffer(dev_bytes) if dev_bytes else None
+        m.nbytes = dev_bytes
+        m.pitch = pitch
         m.host_newer = True
+    padded = pitch != dat.set.size
+    m.rows = dat.dim if padded else 1
+    m.row_bytes = dat.set.size * host.dtype.itemsize if padded else host.nbytes
     if m.layout is not dat.layout:
         m.layout = dat.layout
         m.host_newer = True
@@ -69,7 +145,7 @@ def dat_mirror(dat: Dat, force_upload: bool = False, upload: bool = True) -> Dat
         if host.nbytes:
             if not host.flags.c_contiguous:
                 dat._host = host = np.ascontiguousarray(host)
-            m.buf.upload(host)
+            m.upload(host)
         m.host_newer = False
     return m
 
@@ -124,46 +200,6 @@ def plan_mirror(plan) -> PlanMirror:
     if plan._dev is None:
         plan._dev = PlanMirror(plan)
     return plan._dev
-
-
-class ScheduleMirror:
-    """Device copy of a dataflow schedule (ml_schedule_build): block queue in
-    (window, colour, index) order, dependency CSR and the per-run flag array."""
-
-    __slots__ = ("queue", "dep_off", "dep_list", "flow_state", "nwindows")
-
-    def __init__(self, loop, plan, nwindows: int):
-        import ctypes as C
-        from .plan import write_columns
-        wc = write_columns(loop)
-        keys: dict = {}
-        cols = [np.ascontiguousarray(c[:plan.n], dtype=np.int64) for _, c in wc]
-        kid = np.array([keys.setdefault(k, len(keys)) for k, _ in wc], dtype=np.int32)
-        colour = np.ascontiguousarray(plan.block_color, dtype=np.int64)
-        L = N.lib()
-        h = C.c_void_p()
-        cptr = (C.c_void_p * max(len(cols), 1))(*[N.ptr(c) for c in cols])
-        N.check(L.ml_schedule_build(plan.n, len(cols), cptr, kid.ctypes.data_as(C.POINTER(C.c_int32)),
-                                    plan.block_size, N.ptr(colour), int(nwindows), C.byref(h)),
-                "ml_schedule_build")
-        self.nwindows = int(nwindows)
-        self.queue = self.dep_off = self.dep_list = self.flow_state = None
-        try:
-            nd = C.c_int64()
-            N.check(L.ml_schedule_export(h, C.byref(nd), None, None, None))
-            if nd.value >= 0:
-                queue = np.empty(max(plan.nblocks, 1), np.int32)
-                off = np.empty(plan.nblocks + 1, np.int32)
-                lst = np.empty(max(nd.value, 1), np.int32)
-                N.check(L.ml_schedule_export(h, C.byref(nd), N.ptr(queue), N.ptr(off), N.ptr(lst)))
-                self.queue, self.dep_off, self.dep_list = _upload(queue), _upload(off), _upload(lst)
-                self.flow_state = N.DeviceBuffer(4 * (plan.nblocks + 1))
-        finally:
-            L.ml_schedule_free(h)
-
-    @property
-    def usable(self) -> bool:
-        return self.queue is not None
 
 
 #: incidences per gather row before a target is split across rows (hub targets)
@@ -435,134 +471,6 @@ def fold_eligible(loop) -> bool:
                    for a in loop.args)
 
 
-class TileMirror:
-    """Device tile plan (ml_tile_build) of an indirect-increment loop: compact
-    tiles of the INC target set, each owning its targets and staging them plus
-    their halo in shared memory (see csrc/host_tile.cpp)."""
-
-    __slots__ = ("count", "arity", "umax", "cmax", "emax", "maxcol", "list_off", "nown", "list",
-                 "elem_off", "elem", "ncol", "loc", "ecol", "staged_total", "elem_total",
-                 "inc_base", "inc_off", "inc_k", "inc_c")
-
-    def __init__(self, loop, n: int, budget: int, cmax: int, coords: np.ndarray | None,
-                 gather: bool = False):
-        h = tile_plan_host(loop, n, budget, cmax, coords, accumulate=not gather)
-        for k in ("count", "arity", "umax", "cmax", "emax", "maxcol"):
-            setattr(self, k, h[k])
-        self.staged_total, self.elem_total = int(h["list"].size), int(h["elem"].size)
-        for k in ("list_off", "nown", "list", "elem_off", "elem", "loc", "ecol", "ncol"):
-            setattr(self, k, _upload(h[k]))
-        self.inc_base = self.inc_off = self.inc_k = self.inc_c = None
-        if gather:
-            for k in ("inc_base", "inc_off", "inc_k", "inc_c"):
-                setattr(self, k, _upload(h[k]))
-
-
-def tile_plan_host(loop, n: int, budget: int, cmax: int, coords: np.ndarray | None,
-                   accumulate: bool = True) -> dict:
-    """Host arrays of the tile plan of ``loop`` over its first ``n`` elements
-    (ml_tile_build; see include/meshloop_b200.h for their meaning)."""
-    import ctypes as C
-    ind = [a for a in loop.args if a.kind == "indirect"]
-    m = ind[0].map
-    table = np.ascontiguousarray(m.table[:n], dtype=np.int64)
-    inc_mask = 0
-    for a in ind:
-        if a.mode.name == "INC":
-            inc_mask |= 1 << a.slot
-    red_col = next(a.slot for a in ind if a.mode.name == "INC")
-    stage = 4 + 8 * sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name != "INC"))
-    own = 8 * sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name == "INC"))
-    if not accumulate:                    # tile-gather: owned targets live in registers
-        own = 0
-    L = N.lib()
-    h = C.c_void_p()
-    if coords is not None:
-        coords = np.ascontiguousarray(coords, dtype=np.float64)
-    cptr = coords.ctypes.data if coords is not None else None
-    cdim = int(coords.shape[1]) if coords is not None else 0
-    N.check(L.ml_tile_build(n, m.arity, N.ptr(table), m.to_set.size, inc_mask, red_col, stage, own,
-                            int(budget), int(cmax), cptr, cdim, C.byref(h)), "ml_tile_build")
-    try:
-        sz = [C.c_int64() for _ in range(6)]
-        mc = C.c_int32()
-        N.check(L.ml_tile_sizes(h, *[C.byref(x) for x in sz], C.byref(mc)))
-        nt, nl, ne, umax, cm, emax = (x.value for x in sz)
-        out = dict(list_off=np.empty(nt + 1, np.int32), nown=np.empty(nt, np.int32),
-                   list=np.empty(nl, np.int32), elem_off=np.empty(nt + 1, np.int32),
-                   elem=np.empty(ne, np.int32), loc=np.empty(ne * m.arity, np.uint16),
-                   ecol=np.empty(ne, np.uint8), ncol=np.empty(nt, np.int32))
-        N.check(L.ml_tile_export(h, *[N.ptr(out[k]) for k in ("list_off", "nown", "list", "elem_off",
-                                                                "elem", "loc", "ecol", "ncol")]))
-        ni = C.c_int64()
-        N.check(L.ml_tile_export_incidences(h, C.byref(ni), None, None, None, None))
-        out["inc_base"] = np.empty(nt, np.int32)
-        out["inc_off"] = np.empty(int(out["nown"].sum()) + nt, np.int32)
-        out["inc_k"] = np.empty(ni.value, np.uint16)
-        out["inc_c"] = np.empty(ni.value, np.uint8)
-        N.check(L.ml_tile_export_incidences(h, C.byref(ni), *[N.ptr(out[k]) for k in
-                                                                ("inc_base", "inc_off", "inc_k", "inc_c")]))
-    finally:
-        L.ml_tile_free(h)
-    out.update(count=nt, arity=m.arity, umax=umax, cmax=cm, emax=emax, maxcol=mc.value,
-               inc_mask=inc_mask, red_col=red_col, stage_bytes=stage, own_bytes=own)
-    return out
-
-
-def _distinct(dats):
-    out = []
-    for d in dats:
-        if all(d is not x for x in out):
-            out.append(d)
-    return out
-
-
-def tile_eligible(loop) -> bool:
-    """The tile schedule applies when every indirect argument goes through one
-    map, the indirect writes are all INC, nothing is written directly, the INC
-    dats are accessed in no other way and at most 8 dats are staged."""
-    ind = [a for a in loop.args if a.kind == "indirect"]
-    if not ind or not any(a.mode.name == "INC" for a in ind):
-        return False
-    if any(a.mode.name not in ("READ", "INC") for a in ind):
-        return False
-    if any(a.map is not ind[0].map for a in ind):
-        return False
-    if any(a.kind == "direct" and a.mode.name != "READ" for a in loop.args):
-        return False
-    inc = {a.dat.name for a in ind if a.mode.name == "INC"}
-    if any(a.kind != "global" and a.dat.name in inc and a.mode.name != "INC" for a in loop.args):
-        return False
-    return len(_distinct(a.dat for a in ind)) <= 8
-
-
-def tile_mirror(loop, mesh, n: int, budget: int, cmax: int, coord_dat: str | None,
-                gather: bool = False) -> TileMirror | None:
-    """Tile plan of ``loop`` (cached on the mesh per map version and budget);
-    None when a target alone exceeds the budget or a tile would need more than
-    127 colours (hub targets) — the gather schedule handles those."""
-    ind = [a for a in loop.args if a.kind == "indirect"]
-    m = ind[0].map
-    coords = None
-    cd = mesh.dats.get(coord_dat) if coord_dat else None
-    if (cd is not None and cd.set is m.to_set and cd.dim in (2, 3)
-            and np.dtype(cd.dtype) == np.float64):
-        coords = np.ascontiguousarray(cd.fetch(), dtype=np.float64)
-    inc_mask = tuple(sorted({a.slot for a in ind if a.mode.name == "INC"}))
-    stage = sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name != "INC"))
-    own = sum(d.dim for d in _distinct(a.dat for a in ind if a.mode.name == "INC"))
-    red_col = next(a.slot for a in ind if a.mode.name == "INC")
-    key = (m.name, mesh.version, n, inc_mask, red_col, stage, own, int(budget), int(cmax),
-           coords is not None, gather)
-    cache = mesh.__dict__.setdefault("_ml_tiles", {})
-    if key not in cache:
-        try:
-            cache[key] = TileMirror(loop, n, budget, cmax, coords, gather)
-        except ExecError:
-            cache[key] = None
-    return cache[key]
-
-
 def gather_mirror(loop, plan, hubs: bool = False) -> GatherMirror:
     """Gather lists of ``loop``; ``hubs`` splits heavy targets into several
     rows (the gather kernel only — the fold kernels need one row per target)."""
@@ -573,104 +481,11 @@ def gather_mirror(loop, plan, hubs: bool = False) -> GatherMirror:
     return cache[key]
 
 
-def schedule_mirror(loop, plan, nwindows: int) -> ScheduleMirror:
-    cache = plan.__dict__.setdefault("_schedules", {})
-    key = (loop.signature(), int(nwindows))
-    if key not in cache:
-        cache[key] = ScheduleMirror(loop, plan, nwindows)
-    return cache[key]
-
-
-class StagingMirror:
-    """Device staging lists of one loop's INC arguments (see ml_staging_build).
-
-    ``group[i]`` is the staging group of argument i (one group per INC dat),
-    -1 for arguments that are not indirect INC."""
-
-    __slots__ = ("group", "ngroups", "off", "list", "umax", "loc", "toff", "src",
-                 "pslot", "poff", "nblk", "count", "partial")
-
-    def __init__(self, loop, plan):
-        import ctypes as C
-        inc = [i for i, a in enumerate(loop.args) if a.kind == "indirect" and a.mode.name == "INC"]
-        names: list[str] = []
-        self.group = [-1] * len(loop.args)
-        for i in inc:
-            nm = loop.args[i].dat.name
-            if nm not in names:
-                names.append(nm)
-            self.group[i] = names.index(nm)
-        self.ngroups = len(names)
-        cols = [np.ascontiguousarray(loop.args[i].map.table[:plan.n, loop.args[i].slot], dtype=np.int64)
-                for i in inc]
-        cgrp = np.array([self.group[i] for i in inc], dtype=np.int32)
-        L = N.lib()
-        handle = C.c_void_p()
-        cptr = (C.c_void_p * max(len(cols), 1))(*[N.ptr(c) for c in cols])
-        N.check(L.ml_staging_build(plan.n, plan.block_size, len(cols), cptr,
-                                   cgrp.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(handle)),
-                "ml_staging_build")
-        try:
-            self.off, self.list, self.umax, self.loc = [], [], [], {}
-            self.toff, self.src = [], []
-            self.pslot, self.poff, self.nblk, self.count, self.partial = [], [], [], [], []
-            for g in range(self.ngroups):
-                tot, um = C.c_int64(), C.c_int64()
-                N.check(L.ml_staging_sizes(handle, g, C.byref(tot), C.byref(um)))
-                off = np.empty(plan.nblocks + 1, np.int32)
-                lst = np.empty(max(tot.value, 1), np.int32)
-                N.check(L.ml_staging_export(handle, g, N.ptr(off), N.ptr(lst)))
-                self.off.append(_upload(off))
-                self.list.append(_upload(lst))
-                self.umax.append(int(um.value))
-                nref = C.c_int64()
-                N.check(L.ml_staging_export_seg(handle, g, C.byref(nref), None, None))
-                toff = np.empty(tot.value + 1, np.int32)
-                src = np.empty(max(nref.value, 1), np.uint16)
-                N.check(L.ml_staging_export_seg(handle, g, C.byref(nref), N.ptr(toff), N.ptr(src)))
-                self.toff.append(_upload(toff))
-                self.src.append(_upload(src))
-                # arrival mode: partial slots of targets shared by several blocks
-                ntg, nsl = C.c_int64(), C.c_int64()
-                N.check(L.ml_staging_export_arrival(handle, g, C.byref(ntg), C.byref(nsl), None, None,
-                                                    None))
-                pslot = np.empty(max(tot.value, 1), np.int32)
-                poff = np.empty(max(ntg.value, 1), np.int32)
-                nblk = np.empty(max(ntg.value, 1), np.int32)
-                N.check(L.ml_staging_export_arrival(handle, g, C.byref(ntg), C.byref(nsl), N.ptr(pslot),
-                                                    N.ptr(poff), N.ptr(nblk)))
-                dim = loop.args[self.group.index(g)].dat.dim
-                self.pslot.append(_upload(pslot))
-                self.poff.append(_upload(poff))
-                self.nblk.append(_upload(nblk))
-                cnt = N.DeviceBuffer(4 * max(ntg.value, 1))
-                N.check(L.ml_memset(cnt.ptr, 0, cnt.nbytes))
-                self.count.append(cnt)
-                self.partial.append(N.DeviceBuffer(8 * dim * max(nsl.value, 1)))
-            for j, i in enumerate(inc):
-                loc = np.empty(max(plan.n, 1), np.uint16)
-                N.check(L.ml_staging_export_loc(handle, j, N.ptr(loc)))
-                self.loc[i] = _upload(loc)
-        finally:
-            L.ml_staging_free(handle)
-
-
 def _upload(host: np.ndarray):
     buf = N.DeviceBuffer(max(host.nbytes, 4))
     if host.nbytes:
         buf.upload(host)
     return buf
-
-
-def staging_mirror(loop, plan) -> StagingMirror | None:
-    """Staging lists for ``loop`` (cached on the plan), or None if not applicable."""
-    cache = plan.__dict__.setdefault("_staging", {})
-    key = loop.signature()
-    if key not in cache:
-        inc = {a.dat.name for a in loop.args if a.kind == "indirect" and a.mode.name == "INC"}
-        ok = 0 < len(inc) <= N.MAX_GROUPS and plan.block_size <= 256 and plan.n > 0
-        cache[key] = StagingMirror(loop, plan) if ok else None
-    return cache[key]
 
 
 _PINNED_KEEPALIVE: dict = {}

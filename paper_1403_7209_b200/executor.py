@@ -32,8 +32,7 @@ import numpy as np
 from . import _native as N
 from .core import (INC, MAX, MIN, READ, WRITE_MODES, ExecError, Global, Loop, Mesh, MeshError)
 from .device import (dat_mirror, fold_eligible, gather_eligible, gather_mirror, map_mirror,
-                     pfold_mirror, plan_mirror, schedule_mirror, staging_mirror, tile_eligible,
-                     tile_mirror)
+                     pfold_mirror, plan_mirror)
 from .chain import chain_program
 from .kernels import resolve_kernel
 from .perf import PerfCollector, PerfRecord, b_alg, useful_bytes
@@ -49,7 +48,7 @@ class ExchangeTimeout(ExecError):
     """A rank waited longer than the configured bound for a halo message."""
 
 
-SCHEDULES = ("auto", "gather", "pfold", "tile", "tgather", "fold", "colour", "flow", "arrival")
+SCHEDULES = ("auto", "gather", "pfold", "colour")
 
 # "auto": primary fold when an element gathers many more indirect components
 # than it increments (its neighbour rows are then read once per element instead
@@ -95,19 +94,9 @@ class BackendConfig:
     use_graph: bool = False                 # replay the program as one CUDA graph
     time_loops: bool = True                 # per-loop CUDA-event timing (eager mode)
     residency: str = "device"               # "device": lazy; "host": copy in/out every run
-    smem_staging: bool = True               # INC increments staged in shared memory
-    dataflow: bool = True                   # one persistent launch per INC loop (no colour barriers)
-    inc_staging: str = "segmented"          # "segmented" | "colour": in-block increment scheme
-    inc_schedule: str = "auto"              # "auto" | "gather" | "pfold" | "tile" | "tgather" | "fold" | "colour" | "flow" | "arrival"
+    inc_schedule: str = "auto"              # "auto" | "gather" | "pfold" | "colour"
     inc_schedule_table: dict | None = None  # per-loop override (tuner.tune_schedule)
-    flow_windows: int | None = None         # dataflow queue windows (None: sized to the L2)
-    flow_window_l2_fraction: float = 0.5
-    tile_smem_kb: int = 100                 # tile schedule: shared memory per tile (2 CTAs/SM)
-    tile_cmax: int = 512                    # tile schedule: max owned targets per tile
-    tile_threads: int = 256                 # tile schedule: CTA size (256: 2 CTAs/SM, 128: 4)
     concurrent_loops: bool = True           # graphs/untimed runs: independent loops overlap on streams
-    pfold_own_kb: int = 0                   # pfold pass 1: smem per CTA for the targets' own rows
-                                            # (0: from L1/L2 — faster on B200, see profiles/)
     chain_loops: bool = True                # run registered adjacent loop pairs as one loop (chain.py)
     pfold_records: bool = True              # pfold pass 1 reads per-incidence map records
 
@@ -123,18 +112,13 @@ class BackendConfig:
             raise MeshError(f"unknown partitioner {self.partitioner!r}")
         if self.residency not in ("device", "host"):
             raise MeshError(f"unknown residency {self.residency!r}")
-        if not 8 <= self.tile_smem_kb <= 227 or self.tile_cmax < 1 or self.tile_threads not in (128, 256):
-            raise MeshError("tile_smem_kb must be in [8, 227], tile_cmax positive, tile_threads 128|256")
-        if self.inc_staging not in ("segmented", "colour"):
-            raise MeshError(f"unknown inc_staging {self.inc_staging!r}")
         for sched in [self.inc_schedule, *(self.inc_schedule_table or {}).values()]:
             if sched not in SCHEDULES:
                 raise MeshError(f"unknown inc_schedule {sched!r}; expected one of {SCHEDULES}")
 
     def schedule_for(self, loop_name: str) -> str:
-        """The INC schedule of one loop ("tile" and "fold" fall back to "gather",
-        "gather" to "colour" for loops they do not apply to; "flow"/"arrival"
-        need ``dataflow``)."""
+        """The INC schedule of one loop ("pfold" falls back to "gather", "gather"
+        to "colour" for loops they do not apply to)."""
         if self.inc_schedule_table and loop_name in self.inc_schedule_table:
             return self.inc_schedule_table[loop_name]
         return self.inc_schedule
@@ -206,33 +190,6 @@ def _loop_dtype(loop: Loop) -> int:
     return N.ML_F64
 
 
-_L2_BYTES: list = []
-
-
-def _flow_windows(loop: Loop, config: "BackendConfig") -> int:
-    """Windows of the dataflow queue: the loop's dat footprint / (fraction of L2)."""
-    if config.flow_windows is not None:
-        return max(1, int(config.flow_windows))
-    if not _L2_BYTES:
-        _L2_BYTES.append(N.device_info()["l2_bytes"] or 126 << 20)
-    seen, total = set(), 0
-    for a in loop.args:
-        if a.kind != "global" and a.dat.name not in seen:
-            seen.add(a.dat.name)
-            total += a.dat.nbytes
-    for a in loop.args:
-        if a.kind == "indirect":
-            total += 4 * a.map.from_set.size
-    return max(1, -(-total // int(_L2_BYTES[0] * config.flow_window_l2_fraction)))
-
-
-def _inc_aliased(loop: Loop) -> bool:
-    """A dat both incremented and otherwise accessed in one loop: its reads would
-    observe a schedule-dependent mix, so keep the strict per-colour launches."""
-    inc = {a.dat.name for a in loop.args if a.kind == "indirect" and a.mode is INC}
-    return any(a.kind != "global" and a.dat.name in inc and a.mode is not INC for a in loop.args)
-
-
 class _LoopEntry:
     """Everything one loop needs on the device, kept alive with the program."""
 
@@ -267,7 +224,9 @@ class _LoopEntry:
             r.layout = N.ML_AOS if d.layout.name == "AOS" else N.ML_SOA
             r.set_size = d.set.size
             self.dats.append(d)
-            r.data = dat_mirror(d).ptr or None
+            m = dat_mirror(d)
+            r.data = m.ptr or None
+            r.pitch = m.pitch
             if a.kind == "indirect":
                 r.slot = a.slot
                 r.map = map_mirror(a.map) or None
@@ -288,22 +247,12 @@ class _LoopEntry:
         L.plan.elem_color = pm.ecol.ptr if pm.ecol is not None else None
         L.plan.elem_ncolors = pm.encol.ptr if pm.encol is not None else None
         self.gather = None
-        self.fold = None
-        self.tile = None
         self.pfold = None
         self.pf_slots = None
         sched = config.schedule_for(loop.name)
         if sched == "auto":
             sched = auto_schedule(loop)
         if sched == "pfold" and not (self.n > 0 and fold_eligible(loop)):
-            sched = "gather"
-        one_inc = len({a.dat.name for a in loop.args if a.kind == "indirect" and a.mode is INC}) == 1
-        if (sched == "tile" or (sched == "tgather" and one_inc)) and self.n > 0 and tile_eligible(loop):
-            self.tile = tile_mirror(loop, mesh, self.n, config.tile_smem_kb * 1024, config.tile_cmax,
-                                    config.coord_dat, gather=sched == "tgather")
-            if self.tile is None:
-                sched = "gather"
-        elif sched in ("tile", "tgather"):
             sched = "gather"
         self.sched = sched
         if sched == "pfold":
@@ -313,7 +262,6 @@ class _LoopEntry:
             L.pf_n2, L.pf_off2, L.pf_elem2, L.pf_tl2 = pf.n2, pf.off2.ptr, pf.elem2.ptr, pf.tl2.ptr
             L.pf_pos2 = pf.pos2.ptr
             L.pf_slotpos = pf.slotpos.ptr
-            L.pf_own_kb = int(config.pfold_own_kb)
             L.pf_rec, L.pf_ncol = (pf.rec.ptr if pf.rec is not None else None), pf.ncol
             for w in (1, 2):
                 if getattr(pf, f"seg{w}") is not None:
@@ -329,26 +277,7 @@ class _LoopEntry:
             N.check(N.lib().ml_loop_pfold_slot_bytes(C.byref(L), C.byref(nb)))
             self.pf_slots = N.DeviceBuffer(max(nb.value, 8))
             L.pf_slots = self.pf_slots.ptr
-        elif self.tile is not None:
-            t = self.tile
-            L.tile_count = t.count
-            L.tile_arity = t.arity
-            L.tile_umax = t.umax
-            L.tile_cmax = t.cmax
-            L.tile_threads = config.tile_threads
-            L.tile_list_off, L.tile_nown, L.tile_list = t.list_off.ptr, t.nown.ptr, t.list.ptr
-            L.tile_elem_off, L.tile_elem, L.tile_ncol = t.elem_off.ptr, t.elem.ptr, t.ncol.ptr
-            L.tile_loc, L.tile_ecol = t.loc.ptr, t.ecol.ptr
-            if t.inc_off is not None:
-                L.tile_inc_base, L.tile_inc_off = t.inc_base.ptr, t.inc_off.ptr
-                L.tile_inc_k, L.tile_inc_c = t.inc_k.ptr, t.inc_c.ptr
-        elif sched == "fold" and self.n > 0 and fold_eligible(loop):
-            self.gather = gather_mirror(loop, self.plan)
-            inc = [a for a in loop.args if a.kind == "indirect" and a.mode is INC]
-            dgp = (inc[0].dat.dim + 3) // 4 * 4          # slots padded to 32-byte sectors
-            self.fold = N.DeviceBuffer(self.n * len(inc) * dgp * inc[0].dat.dtype.itemsize)
-            L.fold_buf = self.fold.ptr
-        elif sched in ("gather", "fold") and self.n > 0 and gather_eligible(loop):
+        elif sched == "gather" and self.n > 0 and gather_eligible(loop):
             self.gather = gather_mirror(loop, self.plan, hubs=True)
         if self.gather is not None and self.pfold is None:
             L.gather_ntargets = self.gather.ntargets
@@ -360,46 +289,11 @@ class _LoopEntry:
                 g = self.gather
                 L.gather_seg, L.gather_part, L.gather_nhub = g.seg.ptr, g.part.ptr, g.nhub
                 L.gather_hub_tl, L.gather_hub_off = g.hub_tl.ptr, g.hub_off.ptr
-        self.schedule = None
-        if (self.gather is None and config.dataflow and sched in ("flow", "arrival")
-                and self.plan.has_writes and self.plan.ncolors > 1 and not _inc_aliased(loop)):
-            sm = schedule_mirror(loop, self.plan, _flow_windows(loop, config))
-            if sm.usable:
-                self.schedule = sm
-                L.plan.queue = sm.queue.ptr
-                L.plan.dep_off = sm.dep_off.ptr
-                L.plan.dep_list = sm.dep_list.ptr
-                L.plan.flow_state = sm.flow_state.ptr
         for k, v in enumerate(binding.fconsts[:4]):
             L.fconst[k] = v
         for k, v in enumerate(binding.iconsts[:4]):
             L.iconst[k] = v
         L.rlim = int(rlim[sname]) if rlim and sname in rlim else -1
-        self.staging = (staging_mirror(loop, self.plan)
-                        if config.smem_staging and self.gather is None and self.tile is None
-                        and self.pfold is None else None)
-        if self.staging is not None:
-            sg = self.staging
-            L.staging.ngroups = sg.ngroups
-            for i in range(N.MAX_ARGS):
-                L.staging.group[i] = sg.group[i] if i < len(sg.group) else -1
-            for g in range(sg.ngroups):
-                L.staging.off[g] = sg.off[g].ptr
-                L.staging.list[g] = sg.list[g].ptr
-                L.staging.umax[g] = sg.umax[g]
-            for i, buf in sg.loc.items():
-                L.staging.loc[i] = buf.ptr
-            L.staging.seg = 1 if config.inc_staging == "segmented" else 0
-            L.staging.arrive = 1 if (sched == "arrival" and L.staging.seg
-                                     and not _inc_aliased(loop)) else 0
-            for g in range(sg.ngroups):
-                L.staging.toff[g] = sg.toff[g].ptr
-                L.staging.src[g] = sg.src[g].ptr
-                L.staging.pslot[g] = sg.pslot[g].ptr
-                L.staging.poff[g] = sg.poff[g].ptr
-                L.staging.nblk[g] = sg.nblk[g].ptr
-                L.staging.count[g] = sg.count[g].ptr
-                L.staging.partial[g] = sg.partial[g].ptr
         nbytes = C.c_uint64()
         N.check(N.lib().ml_loop_scratch_bytes(C.byref(L), C.byref(nbytes)))
         self.scratch = N.DeviceBuffer(nbytes.value) if nbytes.value else None
@@ -561,15 +455,14 @@ class CompiledProgram:
                 if host.nbytes:
                     if not host.flags.c_contiguous:
                         d._host = host = np.ascontiguousarray(host)
-                    N.check(L.ml_copy_h2d(d._dev.ptr, N.ptr(host), host.nbytes), "ml_copy_h2d")
+                    d._dev.copy_h2d(host)
             if first[i] or i == 0:
                 N.check(L.ml_order(N.ML_STREAM_H2D, N.ML_STREAM_COMPUTE))
             N.check(L.ml_loop_run(C.byref(e.desc)), f"loop {e.loop.name!r}")
             if last[i]:
                 N.check(L.ml_order(N.ML_STREAM_COMPUTE, N.ML_STREAM_D2H))
                 for d in last[i]:
-                    if d._host.nbytes:
-                        N.check(L.ml_copy_d2h(N.ptr(d._host), d._dev.ptr, d._host.nbytes), "ml_copy_d2h")
+                    d._dev.copy_d2h(d._host)
         N.check(L.ml_order(N.ML_STREAM_COMPUTE, N.ML_STREAM_D2H))
         N.check(L.ml_copy_d2h(N.ptr(hv), self.gdev.ptr, self.gbytes), "ml_copy_d2h")
         N.check(L.ml_sync_all(), "ml_sync_all")
@@ -606,16 +499,11 @@ class CompiledProgram:
         for e in self.entries:
             if e.loop.iter_set.size == 0:
                 continue
-            if e.fold is not None:
-                total += 2
-            elif e.pfold is not None:
-                total += 1 + (1 if e.pfold.n2 > 0 else 0)
-            elif e.tile is not None:
-                total += 1
+            if e.pfold is not None:
+                total += 1 + (1 if e.pfold.n2 > 0 else 0) + (1 if e.pfold.nhub1 else 0) + (
+                    1 if e.pfold.n2 > 0 and e.pfold.nhub2 else 0)
             elif e.gather is not None or not e.plan.has_writes:
                 total += 1 + (1 if e.gather is not None and e.gather.nhub else 0)
-            elif e.schedule is not None or (e.staging is not None and e.desc.staging.arrive):
-                total += 1
             else:
                 total += e.plan.ncolors
             total += sum(1 for a in e.loop.args if a.kind == "global" and a.mode.name != "READ")
@@ -642,11 +530,9 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
     cache = mesh.__dict__.setdefault("_ml_programs", OrderedDict())
     key = (tuple(id(l) for l in program),
            tuple(config.block_size_for(l.name) for l in program), config.block_size,
-           tuple(sorted((config.block_size_table or {}).items())), config.smem_staging,
-           config.dataflow, config.inc_staging, config.inc_schedule,
-           tuple(sorted((config.inc_schedule_table or {}).items())), config.flow_windows,
-           config.flow_window_l2_fraction, config.tile_smem_kb, config.tile_cmax, config.tile_threads, config.coord_dat,
-           config.pfold_own_kb, config.concurrent_loops, config.chain_loops, config.pfold_records,
+           tuple(sorted((config.block_size_table or {}).items())), config.inc_schedule,
+           tuple(sorted((config.inc_schedule_table or {}).items())), config.coord_dat,
+           config.concurrent_loops, config.chain_loops, config.pfold_records,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

@@ -415,7 +415,7 @@ class DeviceRank:
         from .device import dat_mirror
         d = self.rp.dats[name]
         m = dat_mirror(d)
-        se, sc = (d.dim, 1) if d.layout is AOS else (1, d.set.size)
+        se, sc = m.strides(d)
         exports, imports = self.rp.halo_rows(name)
         L = N.lib()
         sends = {}
@@ -532,7 +532,7 @@ class NvlinkHalo:
         from .device import dat_mirror
         d = rp.dats[name]
         m = dat_mirror(d)
-        se, sc = (d.dim, 1) if d.layout is AOS else (1, d.set.size)
+        se, sc = m.strides(d)
         exports, _imports = rp.halo_rows(name)
         ni, me = self.names[name], rp.rank
         for dst, ids in sorted(exports.items()):
@@ -551,7 +551,7 @@ class NvlinkHalo:
         from .device import dat_mirror
         d = rp.dats[name]
         m = dat_mirror(d)
-        se, sc = (d.dim, 1) if d.layout is AOS else (1, d.set.size)
+        se, sc = m.strides(d)
         _exports, imports = rp.halo_rows(name)
         ni, me = self.names[name], rp.rank
         for src, ids in sorted(imports.items()):
@@ -889,7 +889,7 @@ class StreamRank:
         d = self.rp.dats[name]
         from .device import dat_mirror
         m = dat_mirror(d)
-        se, sc = (d.dim, 1) if d.layout is AOS else (1, d.set.size)
+        se, sc = m.strides(d)
         exports, imports = self.rp.halo_rows(name)
         sends, recvs = {}, {}
         for dst, ids in exports.items():
@@ -1098,9 +1098,9 @@ class StreamRank:
             if e.loop.iter_set.size == 0:
                 continue
             base = 0
-            if e.fold is not None:
-                base = 2
-            elif e.tile is not None or e.gather is not None or not e.plan.has_writes:
+            if e.pfold is not None:
+                base = 1 + (1 if e.pfold.n2 > 0 else 0)
+            elif e.gather is not None or not e.plan.has_writes:
                 base = 1
             else:
                 base = e.plan.ncolors

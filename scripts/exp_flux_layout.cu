@@ -1,0 +1,421 @@
+// Experiment (not product code): the fused iflux+vflux loop's primary-fold
+// pass 1 written by hand for three device layouts of the wide node dats, to
+// measure how much of the loop's time is address arithmetic and latency
+// rather than bytes.  Same arithmetic as csrc/functors_proxy.cu ProxyFluxes.
+//
+//   SOA    component c of node e at c*pitch + e        (runtime pitch: the engine today)
+//   AOSOA  blocks of 32 nodes: (e/32)*32*D + c*32 + e%32  (compile-time component offsets)
+//   x, w   AoS (dim 3) in every variant, as the auto-SOA policy stores them
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -shared
+//        -Xcompiler -fPIC -o scripts/_exp_flux.so scripts/exp_flux_layout.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace {
+
+constexpr int NQ = 6, NG = 18, NLIM = 8, NAUX = 19;
+
+struct Data {
+    const double *w, *q, *x, *lim, *grad, *aux;
+    double *res, *slots;
+    const int32_t *off1, *elem1, *tl1, *rec, *slotpos;
+    int64_t n1, pitch;
+};
+
+template <int LAY>
+struct View {
+    const double *p;
+    int64_t pitch;
+    __device__ __forceinline__ double operator[](int c) const {
+        if constexpr (LAY == 0) return p[c * pitch];
+        else return p[c * 32];
+    }
+};
+
+template <int LAY, int D>
+__device__ __forceinline__ View<LAY> view(const double *base, int64_t e, int64_t pitch) {
+    if constexpr (LAY == 0) return View<LAY>{base + e, pitch};
+    else return View<LAY>{base + (e >> 5) * (32 * D) + (e & 31), pitch};
+}
+
+template <int LAY, int D>
+__device__ __forceinline__ int64_t idx(int64_t e, int c, int64_t pitch) {
+    if constexpr (LAY == 0) return c * pitch + e;
+    else return (e >> 5) * (32 * D) + c * 32 + (e & 31);
+}
+
+template <int LAY>
+__device__ __forceinline__ void eval_edge(const Data &d, int64_t e, int64_t a, int64_t b, double *r1,
+                                          double *r2) {
+    const int64_t P = d.pitch;
+    const double *w = d.w + e * 3, *x1 = d.x + a * 3, *x2 = d.x + b * 3;
+    const auto q1 = view<LAY, NQ>(d.q, a, P), q2 = view<LAY, NQ>(d.q, b, P);
+    const auto l1 = view<LAY, NLIM>(d.lim, a, P), l2 = view<LAY, NLIM>(d.lim, b, P);
+    const auto g1 = view<LAY, NG>(d.grad, a, P), g2 = view<LAY, NG>(d.grad, b, P);
+    const auto a1 = view<LAY, NAUX>(d.aux, a, P), a2 = view<LAY, NAUX>(d.aux, b, P);
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double an = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NLIM; ++j) {
+            const double tt = l1[j] + l2[j];
+            s = s + tt * tt;
+        }
+        const double lam = an / ((1.0 + ds) * (1.0 + 0.0625 * s));
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const double f = lam * (q2[v] - q1[v]);
+            r1[v] = 0.0 + f;
+            r2[v] = 0.0 - f;
+        }
+    }
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds2 = d0 * d0 + d1 * d1 + d2 * d2 + 1e-12;
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double wd = w0 * d0 + w1 * d1 + w2 * d2;
+        double mu = 0.0;
+#pragma unroll
+        for (int j = 0; j < NAUX; ++j) mu = mu + (a1[j] + a2[j]);
+        mu = 0.01 * mu / (2.0 * NAUX);
+        const double awd = fabs(wd);
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const int bb = 3 * v;
+            const double gx = 0.5 * (g1[bb] + g2[bb]);
+            const double gy = 0.5 * (g1[bb + 1] + g2[bb + 1]);
+            const double gz = 0.5 * (g1[bb + 2] + g2[bb + 2]);
+            const double dq = q2[v] - q1[v];
+            const double corr = (dq - (gx * d0 + gy * d1 + gz * d2)) / ds2;
+            const double f = mu * (0.001 * (gx * w0 + gy * w1 + gz * w2) + corr * awd);
+            r1[v] += f;
+            r2[v] -= f;
+        }
+    }
+}
+
+__device__ __forceinline__ void store_slot(const Data &d, int64_t e, const double *r2) {
+    double *dst = d.slots + int64_t(__ldg(d.slotpos + e)) * NQ;
+#pragma unroll
+    for (int c = 0; c < NQ; c += 2)
+        __stcg(reinterpret_cast<double2 *>(dst + c), make_double2(r2[c], r2[c + 1]));
+}
+
+// thread per target, its primary edges in sequence (the engine's pfold pass 1)
+template <int LAY, int MINB>
+__global__ void __launch_bounds__(256 / (MINB > 2 ? 2 : 1), MINB) k_flux(const __grid_constant__ Data d) {
+    const int64_t P = d.pitch;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < d.n1;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t tg = __ldg(d.tl1 + t);
+        double run[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(tg, c, P)];
+        for (int k = __ldg(d.off1 + t), ke = __ldg(d.off1 + t + 1); k < ke; ++k) {
+            const int64_t e = __ldg(d.elem1 + k);
+            const int64_t a = __ldg(d.rec + 2 * int64_t(k)), b = __ldg(d.rec + 2 * int64_t(k) + 1);
+            double r1[NQ], r2[NQ];
+            eval_edge<LAY>(d, e, a, b, r1, r2);
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] += r1[c];
+            store_slot(d, e, r2);
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(tg, c, P)] = run[c];
+    }
+}
+
+// lane per edge: a warp takes whole rows (targets) whose primary edges fit in
+// 32 lanes (wrow: first row of each warp task); the row's first lane adds the
+// row's increments in edge order via shuffles
+template <int LAY>
+__global__ void __launch_bounds__(256) k_flux_lanes(const __grid_constant__ Data d, const int32_t *wrow,
+                                                    int64_t ntask) {
+    const int64_t P = d.pitch;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t w = wid; w < ntask; w += nw) {
+        const int r0 = __ldg(wrow + w), rN = __ldg(wrow + w + 1);
+        const int base = __ldg(d.off1 + r0), end = __ldg(d.off1 + rN);
+        const int k = base + lane;
+        const bool act = k < end;
+        // segment starts: lane j <= r1-r0 marks the lane where row r0+j starts
+        unsigned bit = 0;
+        if (lane <= rN - r0) {
+            const int st = __ldg(d.off1 + r0 + lane) - base;
+            bit = st < 32 ? (1u << st) : 0u;
+        }
+        const unsigned starts = __reduce_or_sync(0xffffffffu, bit);
+        const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+        const int lead = 31 - __clz(starts & upto);
+        const bool is_lead = act && lead == lane;
+        double r1[NQ], r2[NQ];
+        if (act) {
+            const int64_t e = __ldg(d.elem1 + k);
+            const int64_t a = __ldg(d.rec + 2 * int64_t(k)), b = __ldg(d.rec + 2 * int64_t(k) + 1);
+            eval_edge<LAY>(d, e, a, b, r1, r2);
+            store_slot(d, e, r2);
+        } else {
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) r1[c] = 0.0;
+        }
+        // row length of this lane's row (leaders only matter)
+        const unsigned after = starts & ~upto;
+        const int nxt = after ? __ffs(after) - 1 : (end - base);
+        const int len = act ? nxt - lane : 0;
+        const int maxlen = __reduce_max_sync(0xffffffffu, is_lead ? len : 0);
+        double run[NQ];
+        int64_t tg = 0;
+        if (is_lead) {
+            tg = __ldg(d.tl1 + r0 + __popc(starts & upto) - 1);
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(tg, c, P)];
+        }
+        for (int j = 0; j < maxlen; ++j) {
+            const int src = lane + j < 32 ? lane + j : 31;
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) {
+                const double v = __shfl_sync(0xffffffffu, r1[c], src);
+                if (is_lead && j < len) run[c] += v;
+            }
+        }
+        if (is_lead) {
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(tg, c, P)] = run[c];
+        }
+    }
+}
+
+// lane per edge with per-lane records: lane record {a, b, e, slot row} (a < 0:
+// idle lane) and per warp task the mask of lanes that start a row; the row's
+// first lane (whose a is the row's target) loads the target's res early and
+// adds the row's increments in edge order via shuffles
+template <int LAY>
+__global__ void __launch_bounds__(256) k_flux_lrec(const __grid_constant__ Data d, const int4 *lrec,
+                                                   const uint32_t *tmask, int64_t ntask) {
+    const int64_t P = d.pitch;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t w = wid; w < ntask; w += nw) {
+        const int4 r = __ldg(lrec + w * 32 + lane);
+        const unsigned starts = __ldg(tmask + w);
+        const bool act = r.x >= 0;
+        const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+        const bool is_lead = act && ((starts >> lane) & 1u);
+        const unsigned after = starts & ~upto;
+        const unsigned actm = __ballot_sync(0xffffffffu, act);
+        const int nact = __popc(actm);
+        const int nxt = after ? __ffs(after) - 1 : nact;
+        const int len = is_lead ? nxt - lane : 0;
+        double run[NQ];
+        if (is_lead) {
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(r.x, c, P)];
+        }
+        double r1[NQ], r2[NQ];
+        if (act) {
+            eval_edge<LAY>(d, r.z, r.x, r.y, r1, r2);
+            double *dst = d.slots + int64_t(r.w) * NQ;
+#pragma unroll
+            for (int c = 0; c < NQ; c += 2)
+                __stcg(reinterpret_cast<double2 *>(dst + c), make_double2(r2[c], r2[c + 1]));
+        } else {
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) r1[c] = 0.0;
+        }
+        const int maxlen = __reduce_max_sync(0xffffffffu, len);
+        for (int j = 0; j < maxlen; ++j) {
+            const int src = lane + j < 32 ? lane + j : 31;
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) {
+                const double v = __shfl_sync(0xffffffffu, r1[c], src);
+                if (j < len) run[c] += v;
+            }
+        }
+        if (is_lead) {
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(r.x, c, P)] = run[c];
+        }
+    }
+}
+
+// thread per target, its primary edges evaluated K at a time in lockstep: the
+// target's own components are loaded once per group and used by all K edges;
+// per component the K increments are added to the target's running value in
+// edge order (the same per-target order as k_flux)
+template <int LAY, int K>
+__global__ void __launch_bounds__(256, 2) k_flux_lock(const __grid_constant__ Data d) {
+    const int64_t P = d.pitch;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < d.n1;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t a = __ldg(d.tl1 + t);
+        double run[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(a, c, P)];
+        const auto q1 = view<LAY, NQ>(d.q, a, P);
+        const auto l1 = view<LAY, NLIM>(d.lim, a, P);
+        const auto g1 = view<LAY, NG>(d.grad, a, P);
+        const auto a1 = view<LAY, NAUX>(d.aux, a, P);
+        const double *x1 = d.x + a * 3;
+        for (int k0 = __ldg(d.off1 + t), ke = __ldg(d.off1 + t + 1); k0 < ke; k0 += K) {
+            const int nk = ke - k0 < K ? ke - k0 : K;
+            int64_t e[K], b[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const int k = j < nk ? k0 + j : k0;           // idle slots repeat the first edge
+                e[j] = __ldg(d.elem1 + k);
+                b[j] = __ldg(d.rec + 2 * int64_t(k) + 1);
+            }
+            double d0[K], d1[K], d2[K], w0[K], w1[K], w2[K], lam[K], mu[K], ds2[K], awd[K];
+            const double xa0 = x1[0], xa1 = x1[1], xa2 = x1[2];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const double *x2 = d.x + b[j] * 3, *w = d.w + e[j] * 3;
+                d0[j] = x2[0] - xa0; d1[j] = x2[1] - xa1; d2[j] = x2[2] - xa2;
+                w0[j] = w[0]; w1[j] = w[1]; w2[j] = w[2];
+            }
+            // iflux scalars
+            double s[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) s[j] = 0.0;
+#pragma unroll
+            for (int c = 0; c < NLIM; ++c) {
+                const double own = l1[c];
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const double tt = own + view<LAY, NLIM>(d.lim, b[j], P)[c];
+                    s[j] = s[j] + tt * tt;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const double ds = sqrt(d0[j] * d0[j] + d1[j] * d1[j] + d2[j] * d2[j]);
+                const double an = sqrt(w0[j] * w0[j] + w1[j] * w1[j] + w2[j] * w2[j]);
+                lam[j] = an / ((1.0 + ds) * (1.0 + 0.0625 * s[j]));
+                ds2[j] = d0[j] * d0[j] + d1[j] * d1[j] + d2[j] * d2[j] + 1e-12;
+                awd[j] = fabs(w0[j] * d0[j] + w1[j] * d1[j] + w2[j] * d2[j]);
+                mu[j] = 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < NAUX; ++c) {
+                const double own = a1[c];
+#pragma unroll
+                for (int j = 0; j < K; ++j) mu[j] = mu[j] + (own + view<LAY, NAUX>(d.aux, b[j], P)[c]);
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j) mu[j] = 0.01 * mu[j] / (2.0 * NAUX);
+            double *slot[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) slot[j] = d.slots + int64_t(__ldg(d.slotpos + e[j])) * NQ;
+#pragma unroll
+            for (int v = 0; v < NQ; ++v) {
+                const int bb = 3 * v;
+                const double qa = q1[v], ga0 = g1[bb], ga1 = g1[bb + 1], ga2 = g1[bb + 2];
+                double r2v[K];
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const auto q2 = view<LAY, NQ>(d.q, b[j], P);
+                    const auto g2 = view<LAY, NG>(d.grad, b[j], P);
+                    const double dqi = q2[v] - qa;
+                    const double fi = lam[j] * dqi;
+                    const double gx = 0.5 * (ga0 + g2[bb]);
+                    const double gy = 0.5 * (ga1 + g2[bb + 1]);
+                    const double gz = 0.5 * (ga2 + g2[bb + 2]);
+                    const double corr = (dqi - (gx * d0[j] + gy * d1[j] + gz * d2[j])) / ds2[j];
+                    const double fv = mu[j] * (0.001 * (gx * w0[j] + gy * w1[j] + gz * w2[j]) + corr * awd[j]);
+                    if (j < nk) run[v] += (0.0 + fi) + fv;
+                    r2v[j] = (0.0 - fi) - fv;
+                }
+#pragma unroll
+                for (int j = 0; j < K; ++j)
+                    if (j < nk) __stcg(slot[j] + v, r2v[j]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(a, c, P)] = run[c];
+    }
+}
+
+}  // namespace
+
+extern "C" int exp_flux_run(int layout, const void *w, const void *q, const void *x, const void *lim,
+                            const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                            const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                            int64_t n1, int64_t pitch, int grid, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int lay = layout & 1, occ = layout >> 1;   // occ 0: 256x2, 1: 128x5, 2: 128x6
+    if (occ == 0) {
+        if (lay == 0) k_flux<0, 2><<<grid, 256, 0, s>>>(d);
+        else k_flux<1, 2><<<grid, 256, 0, s>>>(d);
+    } else if (occ == 1) {
+        if (lay == 0) k_flux<0, 5><<<grid * 5, 128, 0, s>>>(d);
+        else k_flux<1, 5><<<grid * 5, 128, 0, s>>>(d);
+    } else {
+        if (lay == 0) k_flux<0, 6><<<grid * 6, 128, 0, s>>>(d);
+        else k_flux<1, 6><<<grid * 6, 128, 0, s>>>(d);
+    }
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_lanes(int layout, const void *w, const void *q, const void *x, const void *lim,
+                              const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                              const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                              int64_t n1, int64_t pitch, const void *wrow, int64_t ntask, int grid,
+                              void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int32_t *wr = static_cast<const int32_t *>(wrow);
+    if (layout == 0) k_flux_lanes<0><<<grid, 256, 0, s>>>(d, wr, ntask);
+    else k_flux_lanes<1><<<grid, 256, 0, s>>>(d, wr, ntask);
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_lrec(int layout, const void *w, const void *q, const void *x, const void *lim,
+                             const void *grad, const void *aux, void *res, void *slots, int64_t pitch,
+                             const void *lrec, const void *tmask, int64_t ntask, int grid, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           nullptr, nullptr, nullptr, nullptr, nullptr, 0, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int4 *lr = static_cast<const int4 *>(lrec);
+    const uint32_t *tm = static_cast<const uint32_t *>(tmask);
+    if (layout == 0) k_flux_lrec<0><<<grid, 256, 0, s>>>(d, lr, tm, ntask);
+    else k_flux_lrec<1><<<grid, 256, 0, s>>>(d, lr, tm, ntask);
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_lock(int layout, const void *w, const void *q, const void *x, const void *lim,
+                             const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                             const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                             int64_t n1, int64_t pitch, int grid, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int lay = layout & 1, k = layout >> 1;
+    if (k == 3) { if (lay == 0) k_flux_lock<0, 3><<<grid, 256, 0, s>>>(d); else k_flux_lock<1, 3><<<grid, 256, 0, s>>>(d); }
+    else if (k == 2) { if (lay == 0) k_flux_lock<0, 2><<<grid, 256, 0, s>>>(d); else k_flux_lock<1, 2><<<grid, 256, 0, s>>>(d); }
+    else { if (lay == 0) k_flux_lock<0, 4><<<grid, 256, 0, s>>>(d); else k_flux_lock<1, 4><<<grid, 256, 0, s>>>(d); }
+    return int(cudaGetLastError());
+}

@@ -1,0 +1,160 @@
+"""Experiment driver for scripts/exp_flux_layout.cu (not product code).
+
+Builds the bench mesh (94^3, shuffled, CM-renumbered) and the primary-fold
+lists of the fused iflux+vflux loop, runs the hand-written pass-1 kernel for
+the SOA and AOSOA layouts, checks they agree bit for bit (same arithmetic),
+and times each with CUDA events (mean of --reps launches after warm-up).
+
+    python scripts/exp_flux_layout.py [--grid 94] [--reps 50]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def to_aosoa(v: np.ndarray) -> np.ndarray:
+    """(n, D) logical -> flat AoSoA with 32-node blocks, padded to whole blocks."""
+    n, D = v.shape
+    nb = -(-n // 32)
+    pad = np.zeros((nb * 32, D))
+    pad[:n] = v
+    return np.ascontiguousarray(pad.reshape(nb, 32, D).transpose(0, 2, 1)).reshape(-1)
+
+
+def from_aosoa(f: np.ndarray, n: int, D: int) -> np.ndarray:
+    nb = -(-n // 32)
+    return f.reshape(nb, D, 32).transpose(0, 2, 1).reshape(nb * 32, D)[:n]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--grid", type=int, default=94)
+    ap.add_argument("--reps", type=int, default=50)
+    args = ap.parse_args()
+    from paper_1403_7209_b200 import apps, renumber_mesh
+    mesh = apps.gen_hex_mesh(args.grid, seed=0)
+    apps.shuffle_mesh(mesh, seed=1)
+    prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=0)
+    renumber_mesh(mesh)
+    t = mesh.maps["edge_nodes"].table
+    n, m = mesh.sets["nodes"].size, mesh.sets["edges"].size
+    # primary-fold lists: pass-1 rows by first target, secondary slots by second
+    o1 = np.lexsort((np.arange(m), t[:, 0]))
+    c1 = np.bincount(t[:, 0], minlength=n)
+    tl1 = np.flatnonzero(c1).astype(np.int32)
+    off1 = np.concatenate([[0], np.cumsum(c1[tl1])]).astype(np.int32)
+    elem1 = o1.astype(np.int32)
+    rec = np.ascontiguousarray(t[elem1]).astype(np.int32)
+    o2 = np.lexsort((np.arange(m), t[:, 1]))
+    slotpos = np.empty(m, np.int32)
+    slotpos[o2] = np.arange(m, dtype=np.int32)
+
+    # warp tasks for the lane-per-edge kernel: consecutive rows packed greedily
+    # while their primary edges fit in 32 lanes
+    cnt = np.diff(off1)
+    wrow = [0]
+    acc = 0
+    for r, c in enumerate(cnt):
+        if acc + c > 32:
+            wrow.append(r)
+            acc = 0
+        acc += c
+    wrow.append(cnt.size)
+    wrow = np.asarray(wrow, np.int32)
+    # per-lane records of the warp tasks
+    ntask = wrow.size - 1
+    lrec = np.full((ntask, 32, 4), -1, np.int32)
+    tmask = np.zeros(ntask, np.uint32)
+    kk0 = off1[wrow[:-1]]
+    for tsk in range(ntask):
+        r0, r1_ = wrow[tsk], wrow[tsk + 1]
+        b0, b1 = off1[r0], off1[r1_]
+        ks = np.arange(b0, b1)
+        e = elem1[ks]
+        lrec[tsk, :ks.size] = np.stack([rec[ks, 0], rec[ks, 1], e, slotpos[e]], 1)
+        tmask[tsk] = np.bitwise_or.reduce((1 << (off1[r0:r1_] - b0)).astype(np.uint32))
+    dev = torch.device("cuda")
+    lib = C.CDLL(str(ROOT / "scripts" / "_exp_flux.so"))
+    lib.exp_flux_run.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_lanes.argtypes = ([C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_void_p,
+                                   C.c_int64, C.c_int, C.c_void_p])
+    lib.exp_flux_lock.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_lrec.argtypes = ([C.c_int] + [C.c_void_p] * 8 + [C.c_int64, C.c_void_p, C.c_void_p,
+                                  C.c_int64, C.c_int, C.c_void_p])
+    vals = {k: h[k].fetch() for k in ("q", "x", "lim", "grad", "aux", "res", "w")}
+    vals["grad"] = np.random.default_rng(0).random(vals["grad"].shape)   # nonzero gradients
+    vals["res"] = np.random.default_rng(1).random(vals["res"].shape)
+    ints = {k: torch.from_numpy(v).to(dev) for k, v in
+            (("off1", off1), ("elem1", elem1), ("tl1", tl1), ("rec", rec.reshape(-1)), ("slotpos", slotpos),
+             ("wrow", wrow), ("lrec", lrec.reshape(-1)), ("tmask", tmask.view(np.int32)))}
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    out = {}
+    results = {}
+    for lay, lanes, name in ((0, 0, "soa"), (1, 0, "aosoa"), (0, 1, "soa_lanes"), (1, 1, "aosoa_lanes"),
+                             (0, 2, "soa_lrec"), (1, 2, "aosoa_lrec"), (2, 0, "soa_128x5"),
+                             (3, 0, "aosoa_128x5"), (0, 3, "soa_lock3"), (1, 3, "aosoa_lock3"),
+                             (0, 4, "soa_lock2"), (1, 4, "aosoa_lock2"), (0, 5, "soa_lock4"),
+                             (1, 5, "aosoa_lock4")):
+        def put(k):
+            v = vals[k]
+            if k in ("x", "w"):
+                return torch.from_numpy(np.ascontiguousarray(v).reshape(-1)).to(dev)
+            if lay % 2 == 0:
+                return torch.from_numpy(np.ascontiguousarray(v.T).reshape(-1)).to(dev)
+            return torch.from_numpy(to_aosoa(v)).to(dev)
+        T = {k: put(k) for k in vals}
+        res0 = T["res"].clone()
+        slots = torch.zeros(m * 6, dtype=torch.float64, device=dev)
+        stream = torch.cuda.current_stream().cuda_stream
+
+        def launch():
+            common = (lay, T["w"].data_ptr(), T["q"].data_ptr(), T["x"].data_ptr(),
+                      T["lim"].data_ptr(), T["grad"].data_ptr(), T["aux"].data_ptr(),
+                      T["res"].data_ptr(), slots.data_ptr(), ints["off1"].data_ptr(),
+                      ints["elem1"].data_ptr(), ints["tl1"].data_ptr(), ints["rec"].data_ptr(),
+                      ints["slotpos"].data_ptr(), int(tl1.size), n)
+            if lanes >= 3:
+                kk = {3: 3, 4: 2, 5: 4}[lanes]
+                rc = lib.exp_flux_lock(lay + 2 * kk, *common[1:], sms * 2, stream)
+            elif lanes == 2:
+                rc = lib.exp_flux_lrec(lay, T["w"].data_ptr(), T["q"].data_ptr(), T["x"].data_ptr(),
+                                       T["lim"].data_ptr(), T["grad"].data_ptr(), T["aux"].data_ptr(),
+                                       T["res"].data_ptr(), slots.data_ptr(), n, ints["lrec"].data_ptr(),
+                                       ints["tmask"].data_ptr(), ntask, sms * 2, stream)
+            elif lanes:
+                rc = lib.exp_flux_lanes(*common, ints["wrow"].data_ptr(), int(wrow.size - 1), sms * 2, stream)
+            else:
+                rc = lib.exp_flux_run(*common, sms, stream) if lay >= 2 else lib.exp_flux_run(*common, sms * 2, stream)
+            assert rc == 0, rc
+        launch()
+        torch.cuda.synchronize()
+        r = T["res"].cpu().numpy()
+        results[name] = (r.reshape(6, n).T if lay % 2 == 0 else from_aosoa(r, n, 6)), slots.cpu().numpy()
+        T["res"].copy_(res0)
+        for _ in range(5):
+            launch()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(args.reps):
+            launch()
+        b.record()
+        b.synchronize()
+        out[name] = a.elapsed_time(b) / args.reps
+    same = {k: all(np.array_equal(results["soa"][i], results[k][i]) for i in range(2)) for k in results}
+    print(json.dumps({"grid": args.grid, "edges": m, "warp_tasks": int(wrow.size - 1),
+                      "lane_util": float(m / (32 * (wrow.size - 1))), "ms": out, "bitwise_equal_to_soa": same}))
+
+
+if __name__ == "__main__":
+    main()

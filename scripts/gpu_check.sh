@@ -10,7 +10,7 @@ nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
 python -c "import __graft_entry__ as g; g.build()" > "$OUT/build.log" 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?" >> "$OUT/status.txt"
 timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider --durations=15 > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/status.txt"
-timeout 300 python scripts/profile_proxy.py --iters 3 --inc-schedule gather pfold tile colour > "$OUT/schedules.log" 2>&1; echo "sched rc=$?" >> "$OUT/status.txt"
+timeout 300 python scripts/profile_proxy.py --iters 3 --inc-schedule gather pfold colour > "$OUT/schedules.log" 2>&1; echo "sched rc=$?" >> "$OUT/status.txt"
 timeout 600 python bench.py --steps 20 --warmup 3 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/status.txt"
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"; echo "bench-ref rc=$?" >> "$OUT/status.txt"
 TABLE=$(python -c "import json,sys; t=json.load(open('$OUT/bench.json'))['config'].get('inc_schedule_table') or {}; print(','.join(f'{k}={v}' for k,v in t.items()))" 2>/dev/null)

@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # GPU tests + a profile_proxy sweep + ncu of kernels matching NCU_RE.
-#   SWEEP="--inc-schedule gather --own-kb 0 96" NCU_RE=k_gather NCU_ARGS="--inc-schedule gather" gpurun -- bash scripts/gpu_sweep2.sh <tag>
+#   SWEEP="--inc-schedule gather pfold" NCU_RE=k_gather NCU_ARGS="--inc-schedule gather" gpurun -- bash scripts/gpu_sweep2.sh <tag>
 set -u
 TAG=${1:-sweep}
 OUT=gpurun_out/$TAG; mkdir -p "$OUT"

@@ -2,7 +2,7 @@
 layout / block-size sweeps).
 
     python scripts/profile_proxy.py [--grid 94] [--iters 3] [--block-size 256 128]
-                                    [--inc-schedule gather colour flow arrival] [--soa 4]
+                                    [--inc-schedule gather pfold colour] [--soa 4]
 """
 import argparse
 import sys
@@ -21,10 +21,6 @@ ap.add_argument("--soa", type=int, default=4, help="auto-SOA threshold; -1 = all
 ap.add_argument("--inc-schedule", nargs="+", default=["gather"])
 ap.add_argument("--no-renumber", action="store_true")
 ap.add_argument("--kd", type=int, default=0, help="k-d leaf size: renumber nodes in k-d order after CM")
-ap.add_argument("--tile-smem", type=int, nargs="+", default=[100])
-ap.add_argument("--tile-cmax", type=int, default=512)
-ap.add_argument("--tile-threads", type=int, nargs="+", default=[256])
-ap.add_argument("--own-kb", type=int, nargs="+", default=[0])
 ap.add_argument("--records", type=int, nargs="+", default=[1], help="pfold pass-1 element records on/off")
 ap.add_argument("--chain", type=int, nargs="+", default=[1], help="loop chaining on/off")
 ap.add_argument("--aos-dats", nargs="*", default=[], help="dats switched to AoS after generation")
@@ -63,15 +59,11 @@ if args.kd:
         apply_permutation(mesh, row_order_by_targets(mesh, m))
 import itertools
 import statistics
-for bs, kb, nt, okb, rec, ch in itertools.product(args.block_size, args.tile_smem, args.tile_threads,
-                                                  args.own_kb, args.records, args.chain):
+for bs, rec, ch in itertools.product(args.block_size, args.records, args.chain):
     for sched in args.inc_schedule:
-        if sched != "tile" and (kb != args.tile_smem[0] or nt != args.tile_threads[0]):
+        if sched != "pfold" and rec != args.records[0]:
             continue
-        if sched != "pfold" and (okb != args.own_kb[0] or rec != args.records[0]):
-            continue
-        cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched, tile_smem_kb=kb,
-                               tile_cmax=args.tile_cmax, tile_threads=nt, pfold_own_kb=okb,
+        cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched,
                                pfold_records=bool(rec), chain_loops=bool(ch))
         per = {}
         for i in range(args.iters):
@@ -82,6 +74,6 @@ for bs, kb, nt, okb, rec, ch in itertools.product(args.block_size, args.tile_sme
                 per.setdefault(p.loop, []).append((p.time_sec, p.gb_per_sec_alg))
         med = {k: (statistics.median(t for t, _ in v), statistics.median(g for _, g in v)) for k, v in per.items()}
         tot = sum(t for t, _ in med.values())
-        print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} tile_kb={kb} nt={nt} own={okb} rec={rec} chain={ch}] "
+        print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} rec={rec} chain={ch}] "
               f"total={tot*1e3:.3f}ms " +
               " ".join(f"{k}={t*1e3:.3f}ms/{g:.0f}GBs" for k, (t, g) in med.items()), flush=True)

@@ -34,7 +34,7 @@ def close(got, ref, rtol=RTOL, what=""):
     assert not bad.any(), f"{what}: {bad.sum()} mismatches, max |d| {np.max(np.abs(got - ref))}"
 
 
-SCHEDULES = ("tile", "tgather", "gather", "pfold", "fold", "colour", "flow", "arrival")
+SCHEDULES = ("gather", "pfold", "colour")
 
 
 def cfg(**kw):
@@ -46,8 +46,8 @@ def _exec_cases():
 
 
 @pytest.mark.parametrize("case", _exec_cases(), ids=lambda c: c["name"])
-@pytest.mark.parametrize("bs,sched", [(256, "tile"), (256, "tgather"), (256, "pfold"), (16, "pfold"),
-                                      (256, "gather"), (16, "gather"), (256, "colour"), (16, "colour")])
+@pytest.mark.parametrize("bs,sched", [(256, "pfold"), (16, "pfold"), (256, "gather"), (16, "gather"),
+                                      (256, "colour"), (16, "colour")])
 def test_apps_match_reference_golden(case, bs, sched):
     g = golden("exec.npz")
     mesh, prog, h = _cases.build_app(case["app"], case["n"], case["dtype"], case["steps"])
@@ -137,7 +137,7 @@ def _proxy_pair(N, seed=0, renumber=True, shuffle=True, soa=4):
 
 
 @pytest.mark.parametrize("soa", [4, None, 0])
-@pytest.mark.parametrize("sched", ["gather", "pfold", "tgather", "tile"])
+@pytest.mark.parametrize("sched", ["gather", "pfold", "colour"])
 def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa, sched):
     """Stop before the update so the raw INC accumulators (res, grad) are compared,
     for every layout (auto-SoA, all AoS, all SoA) and INC schedule."""
@@ -149,7 +149,7 @@ def test_proxy_partial_iteration_raw_accumulators_vs_oracle(soa, sched):
     np.testing.assert_array_equal(h["dt_min"][0].value, rh["dt_min"][0].value)
 
 
-@pytest.mark.parametrize("sched", ["tile", "tgather", "pfold", "gather", "colour"])
+@pytest.mark.parametrize("sched", ["pfold", "gather", "colour"])
 def test_proxy_full_size_iteration_vs_oracle(sched):
     """Config B (Rotor37-sized, 2.47M edges): one full iteration, shuffled + CM-renumbered."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(94, seed=0)
@@ -249,35 +249,7 @@ def test_graph_replay_and_host_residency_match_eager():
         np.testing.assert_array_equal(qo, results[0][3])
 
 
-@pytest.mark.parametrize("bs", [32, 256])
-def test_dataflow_schedule_matches_colour_launches(bs):
-    """One window: same per-target increment order as per-colour launches, so float
-    results match bit for bit; several windows reorder increments (tolerance)."""
-    outs = []
-    for kw in ({"inc_schedule": "colour"}, {"inc_schedule": "flow", "flow_windows": 1},
-               {"inc_schedule": "flow", "flow_windows": 7}):
-        mesh = apps.gen_hex_mesh(20, seed=8)
-        apps.shuffle_mesh(mesh, seed=9)
-        prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=8)
-        ml.renumber_mesh(mesh)
-        ml.run_program(prog[:5], mesh, cfg(block_size=bs, **kw))
-        outs.append((h["res"].fetch(), h["grad"].fetch()))
-    np.testing.assert_array_equal(outs[1][0], outs[0][0])
-    np.testing.assert_array_equal(outs[1][1], outs[0][1])
-    close(outs[2][0], outs[0][0], what="res")
-    close(outs[2][1], outs[0][1], what="grad")
-    for make in (lambda: apps.gen_hub_mesh(5000, 60000, n_hubs=64, hub_share=0.05, seed=3),
-                 lambda: _shuffled_hex(16)):
-        ref, mesh = make(), make()
-        ml.run_program([_cases.inc_loop(ref, "edge_nodes")], ref,
-                       cfg(block_size=bs, inc_schedule="colour"))
-        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh,
-                       cfg(block_size=bs, inc_schedule="flow"))
-        np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
-
-
-@pytest.mark.parametrize("soa,sched", [(4, "gather"), (None, "gather"), (4, "fold"),
-                                       (None, "fold")])
+@pytest.mark.parametrize("soa,sched", [(4, "gather"), (None, "gather"), (0, "gather")])
 def test_gather_schedule_reproduces_serial_order_bitwise(soa, sched):
     """Target-centric schedule accumulates every target in the reference serial
     order, so even float64 raw INC accumulators equal the oracle bit for bit."""
@@ -310,59 +282,6 @@ def test_gather_schedule_reproduces_serial_order_bitwise(soa, sched):
     gg = golden("exec.npz")
     np.testing.assert_array_equal(acc.fetch(), gg["exec/mixmax/acc"])
     assert [lo.value, hi.value] == gg["exec/mixmax/lohi"].tolist()
-
-
-@pytest.mark.parametrize("bs", [16, 64, 256])
-def test_arrival_schedule_matches_and_is_deterministic(bs):
-    """Arrival schedule (no block colours): int64 bit-exact, float within tolerance of
-    the colour schedule, and bitwise reproducible run to run (counters self-reset)."""
-    outs = []
-    for kw in ({"inc_schedule": "colour"}, {"inc_schedule": "arrival"},
-               {"inc_schedule": "arrival"}):
-        mesh = apps.gen_hex_mesh(18, seed=3)
-        apps.shuffle_mesh(mesh, seed=4)
-        prog, h = apps.build_hydra_proxy(mesh, steps=2, seed=3)
-        ml.renumber_mesh(mesh)
-        ml.run_program(prog, mesh, cfg(block_size=bs, **kw))
-        ml.run_program(prog[:5], mesh, cfg(block_size=bs, **kw))       # replay: counters reused
-        outs.append((h["res"].fetch(), h["grad"].fetch(), h["q"].fetch()))
-    for k in range(3):
-        close(outs[1][k], outs[0][k], what=f"field {k}")
-        np.testing.assert_array_equal(outs[1][k], outs[2][k])
-    for make in (lambda: apps.gen_hub_mesh(5000, 60000, n_hubs=8, hub_share=0.2, seed=3),
-                 lambda: _shuffled_hex(16), lambda: apps.gen_mesh(50)):
-        ref, mesh = make(), make()
-        rl = _cases.inc_loop(ref, "edge_nodes")
-        oserial.run_loop(rl)
-        l = _cases.inc_loop(mesh, "edge_nodes")
-        for _ in range(2):
-            mesh.dats["acc"].put(np.zeros((mesh.sets["nodes"].size, 1), np.int64))
-            ml.run_program([l], mesh, cfg(block_size=bs, inc_schedule="arrival"))
-            np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
-
-
-@pytest.mark.parametrize("bs", [32, 128, 256])
-def test_smem_and_register_staging_agree(bs):
-    outs = []
-    variants = ({"smem_staging": False}, {"inc_staging": "colour"}, {"inc_staging": "segmented"})
-    for kw in variants:
-        mesh = apps.gen_hex_mesh(14, seed=5)
-        apps.shuffle_mesh(mesh, seed=6)
-        prog, h = apps.build_hydra_proxy(mesh, steps=1, seed=5)
-        ml.renumber_mesh(mesh)
-        ml.run_program(prog[:5], mesh, cfg(block_size=bs, inc_schedule="colour", **kw))
-        outs.append((h["res"].fetch(), h["grad"].fetch()))
-    for o in outs[1:]:
-        close(o[0], outs[0][0], what="res")
-        close(o[1], outs[0][1], what="grad")
-    ref = apps.gen_mesh(40)
-    ml.run_program([_cases.inc_loop(ref, "edge_nodes")], ref,
-                   cfg(block_size=bs, smem_staging=False, inc_schedule="colour"))
-    for kw in variants[1:]:
-        mesh = apps.gen_mesh(40)
-        ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh,
-                       cfg(block_size=bs, inc_schedule="colour", **kw))
-        np.testing.assert_array_equal(mesh.dats["acc"].fetch(), ref.dats["acc"].fetch())
 
 
 def test_host_writes_between_runs_are_uploaded():
@@ -438,56 +357,14 @@ def test_gather_write_is_serial_last_writer(seed):
         np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref.dats["vals"].fetch())
 
 
-@pytest.mark.parametrize("smem_kb,cmax,sched", [(100, 512, "tile"), (12, 4, "tile"), (227, 4096, "tile"),
-                                               (100, 512, "tgather"), (12, 4, "tgather")])
-def test_tile_schedule_matches_oracle_and_is_deterministic(smem_kb, cmax, sched):
-    """Tile schedule (owner-computes tiles, shared-memory staging): raw INC
-    accumulators within tolerance of the serial oracle at several tile sizes,
-    int64 bit-exact, reductions counted once per element, bitwise run to run."""
-    (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(12)
-    bulk.run_program(rprog[:5])
-    c = cfg(inc_schedule=sched, tile_smem_kb=smem_kb, tile_cmax=cmax)
-    ml.run_program(prog[:5], mesh, c)
-    for k in ("grad", "res"):
-        close(h[k].fetch(), rh[k].fetch(), what=k)
-    first = {k: h[k].fetch().copy() for k in ("grad", "res")}
-    for k in ("grad", "res"):
-        h[k].data[...] = 0.0
-    ml.run_program(prog[:5], mesh, c)
-    for k in ("grad", "res"):
-        np.testing.assert_array_equal(h[k].fetch(), first[k])
-    for soa in (4, None):
-        mesh, loop, acc, lo, hi = _cases.mixmax_case(auto_soa_threshold=soa)
-        ml.run_program([loop], mesh, cfg(inc_schedule=sched, tile_smem_kb=8, tile_cmax=3))
-        g = golden("exec.npz")
-        np.testing.assert_array_equal(acc.fetch(), g["exec/mixmax/acc"])
-        assert [lo.value, hi.value] == g["exec/mixmax/lohi"].tolist()
-
-
-def test_tile_schedule_int64_fuzz_and_diffusion(rng):
-    for _ in range(10):
-        seed = int(rng.integers(0, 2 ** 31))
-        ref_mesh, ref_loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
-        oserial.run_loop(ref_loop)
-        mesh, loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
-        ml.run_program([loop], mesh, cfg(inc_schedule="tile",
-                                         tile_smem_kb=int(rng.choice([8, 16, 100])),
-                                         tile_cmax=int(rng.choice([1, 7, 512]))))
-        np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref_mesh.dats["vals"].fetch())
-    g = golden("exec.npz")
-    mesh, prog, h = _cases.build_app("diffusion", 8, "int64", 3)
-    ml.run_program(prog, mesh, cfg(inc_schedule="tile", tile_smem_kb=8, tile_cmax=5))
-    np.testing.assert_array_equal(h["u"].fetch(), g["exec/diffusion_n8_int64_s3/u"])
-
-
-@pytest.mark.parametrize("own_kb", [0, 100])
-def test_pfold_schedule_raw_accumulators_reductions_and_determinism(own_kb):
+@pytest.mark.parametrize("records", [True, False])
+def test_pfold_schedule_raw_accumulators_reductions_and_determinism(records):
     """Primary fold: raw INC accumulators within tolerance of the serial oracle,
     int64 bit-exact (fuzz + diffusion), MIN/MAX/READ globals counted once per
-    element, bitwise run to run; with and without own-row staging."""
+    element, bitwise run to run; with and without pass-1 element records."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(12)
     bulk.run_program(rprog[:5])
-    c = cfg(inc_schedule="pfold", pfold_own_kb=own_kb)
+    c = cfg(inc_schedule="pfold", pfold_records=records)
     ml.run_program(prog[:5], mesh, c)
     for k in ("grad", "res"):
         close(h[k].fetch(), rh[k].fetch(), what=k)
@@ -499,13 +376,13 @@ def test_pfold_schedule_raw_accumulators_reductions_and_determinism(own_kb):
         np.testing.assert_array_equal(h[k].fetch(), first[k])
     for k in ("grad", "res"):              # map reads instead of element records: same arithmetic
         h[k].data[...] = 0.0
-    ml.run_program(prog[:5], mesh, cfg(inc_schedule="pfold", pfold_own_kb=own_kb, pfold_records=False))
+    ml.run_program(prog[:5], mesh, cfg(inc_schedule="pfold", pfold_records=not records))
     for k in ("grad", "res"):
         np.testing.assert_array_equal(h[k].fetch(), first[k])
     g = golden("exec.npz")
     for soa in (4, None):
         mesh, loop, acc, lo, hi = _cases.mixmax_case(auto_soa_threshold=soa)
-        ml.run_program([loop], mesh, cfg(inc_schedule="pfold", pfold_own_kb=own_kb))
+        ml.run_program([loop], mesh, cfg(inc_schedule="pfold", pfold_records=records))
         np.testing.assert_array_equal(acc.fetch(), g["exec/mixmax/acc"])
         assert [lo.value, hi.value] == g["exec/mixmax/lohi"].tolist()
     rng = np.random.default_rng(11)
@@ -514,7 +391,7 @@ def test_pfold_schedule_raw_accumulators_reductions_and_determinism(own_kb):
         ref_mesh, ref_loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
         oserial.run_loop(ref_loop)
         mesh, loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
-        ml.run_program([loop], mesh, cfg(inc_schedule="pfold", pfold_own_kb=own_kb))
+        ml.run_program([loop], mesh, cfg(inc_schedule="pfold", pfold_records=records))
         np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref_mesh.dats["vals"].fetch())
 
 
@@ -545,7 +422,7 @@ def test_concurrent_loops_match_sequential_and_respect_the_dag():
     assert deps[i][1] != deps[g][1]                      # they run on different streams
 
 
-@pytest.mark.parametrize("sched", ["gather", "pfold", "colour", "tile"])
+@pytest.mark.parametrize("sched", ["gather", "pfold", "colour"])
 def test_chained_flux_loops_match_oracle(sched):
     """iflux+vflux chained into one loop (chain.py): raw res accumulators within
     the reference tolerance of the serial oracle running the loops one by one,
@@ -600,37 +477,3 @@ def test_config_d_proxy_iteration_vs_oracle():
     assert h["dt_min"][0].value == rh["dt_min"][0].value
 
 
-_PASS2_SCRIPT = """
-import sys, numpy as np
-sys.path.insert(0, {root!r})
-import paper_1403_7209_b200 as ml
-from paper_1403_7209_b200 import apps
-mesh = apps.gen_hub_mesh(3000, 30000, n_hubs=3, hub_share=0.1, seed=4)
-prog, h = apps.build_diffusion(mesh, 2, dtype="float64")
-ml.run_program(prog, mesh, ml.BackendConfig(inc_schedule="pfold"))
-m2 = apps.gen_hex_mesh(10, seed=3)
-p2, h2 = apps.build_hydra_proxy(m2, steps=1, seed=3)
-ml.run_program(p2[:5], m2, ml.BackendConfig(inc_schedule="pfold"))
-np.savez({out!r}, u=h["u"].fetch(), res=h2["res"].fetch(), grad=h2["grad"].fetch())
-"""
-
-
-def test_pass2_warp_cooperative_equals_thread_per_row(tmp_path):
-    """The warp-cooperative pass 2 (default) adds each target's slots in the
-    same order as the thread-per-row kernel (ML_PASS2W=0): bitwise equal,
-    hub rows included."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
-    root = str(Path(__file__).resolve().parent.parent)
-    outs = []
-    for flag in ("0", "1"):
-        out = str(tmp_path / f"p{flag}.npz")
-        env = dict(os.environ, ML_PASS2W=flag)
-        r = subprocess.run([sys.executable, "-c", _PASS2_SCRIPT.format(root=root, out=out)], env=env,
-                           capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stderr[-2000:]
-        outs.append(np.load(out))
-    for k in ("u", "res", "grad"):
-        np.testing.assert_array_equal(outs[0][k], outs[1][k], k)

@@ -283,191 +283,6 @@ def test_backend_config_validation():
     assert BackendConfig(block_size_table={"a": 64}).block_size_for("a") == 64
 
 
-@pytest.mark.parametrize("nwin", [1, 3, 8])
-def test_dataflow_schedule_orders_every_conflicting_pair(rng, nwin):
-    """ml_schedule_build: the queue is a permutation of the blocks in (window,
-    colour) order, dependencies point backwards, and every pair of blocks that
-    share a write target is ordered by a dependency (no write-back race)."""
-    import ctypes as C
-    from paper_1403_7209_b200 import _native as N
-    for _ in range(6):
-        mesh, loop = _cases.random_loop_mesh(rng, max_elems=2500)
-        bs = int(rng.choice([4, 16, 64]))
-        plan = ml.plan_for(loop, mesh, bs)
-        wc = oplan.write_columns(loop)
-        cols = [np.ascontiguousarray(c) for _, c in wc]
-        kid = np.zeros(len(cols), np.int32)
-        colour = np.ascontiguousarray(plan.block_color)
-        h = C.c_void_p()
-        ptrs = (C.c_void_p * len(cols))(*[N.ptr(c) for c in cols])
-        assert N.lib().ml_schedule_build(plan.n, len(cols), ptrs, kid.ctypes.data_as(C.POINTER(C.c_int32)),
-                                         bs, N.ptr(colour), nwin, C.byref(h)) == 0
-        nd = C.c_int64()
-        N.lib().ml_schedule_export(h, C.byref(nd), None, None, None)
-        if nd.value < 0:
-            continue
-        queue = np.empty(plan.nblocks, np.int32)
-        off = np.empty(plan.nblocks + 1, np.int32)
-        lst = np.empty(max(nd.value, 1), np.int32)
-        N.lib().ml_schedule_export(h, C.byref(nd), N.ptr(queue), N.ptr(off), N.ptr(lst))
-        N.lib().ml_schedule_free(h)
-        assert sorted(queue.tolist()) == list(range(plan.nblocks))
-        win = np.arange(plan.nblocks) * nwin // plan.nblocks
-        keys = list(zip(win[queue], colour[queue]))
-        assert keys == sorted(keys)
-        pos = np.empty(plan.nblocks, np.int64)
-        pos[queue] = np.arange(plan.nblocks)
-        deps = {(b, int(d)) for b in range(plan.nblocks) for d in lst[off[b]:off[b + 1]]}
-        assert all(pos[d] < pos[b] for b, d in deps)
-        tgt_blocks: dict = {}
-        for c in cols:
-            for e, t in enumerate(c):
-                tgt_blocks.setdefault(int(t), set()).add(e // bs)
-        for blocks in tgt_blocks.values():
-            bl = sorted(blocks, key=lambda b: pos[b])
-            for i in range(len(bl)):
-                for j in range(i + 1, len(bl)):
-                    assert (bl[j], bl[i]) in deps
-
-
-def test_staging_lists_resolve_every_increment(rng):
-    """ml_staging_build: list[off[b] + loc[e]] is exactly element e's target."""
-    import ctypes as C
-    from paper_1403_7209_b200 import _native as N
-    for _ in range(10):
-        mesh, loop = _cases.random_loop_mesh(rng, max_elems=3000)
-        bs = int(rng.choice([1, 7, 64, 256]))
-        n = loop.iter_set.size
-        cols = [np.ascontiguousarray(a.map.table[:, a.slot]) for a in loop.args if a.kind == "indirect"]
-        grp = np.zeros(len(cols), np.int32)
-        h = C.c_void_p()
-        ptrs = (C.c_void_p * len(cols))(*[N.ptr(c) for c in cols])
-        assert N.lib().ml_staging_build(n, bs, len(cols), ptrs, grp.ctypes.data_as(C.POINTER(C.c_int32)),
-                                        C.byref(h)) == 0
-        tot, um = C.c_int64(), C.c_int64()
-        N.lib().ml_staging_sizes(h, 0, C.byref(tot), C.byref(um))
-        nb = (n + bs - 1) // bs
-        off = np.empty(nb + 1, np.int32)
-        lst = np.empty(tot.value, np.int32)
-        N.lib().ml_staging_export(h, 0, N.ptr(off), N.ptr(lst))
-        for j, c in enumerate(cols):
-            loc = np.empty(n, np.uint16)
-            N.lib().ml_staging_export_loc(h, j, N.ptr(loc))
-            blk = np.arange(n) // bs
-            np.testing.assert_array_equal(lst[off[blk] + loc], c)
-        for b in range(nb):
-            seg = lst[off[b]:off[b + 1]]
-            assert np.all(np.diff(seg) > 0) and seg.size <= um.value
-        # segmented lists: each target's contributing (arg, element) slots, element order
-        nref = C.c_int64()
-        N.lib().ml_staging_export_seg(h, 0, C.byref(nref), None, None)
-        assert nref.value == n * len(cols)
-        toff = np.empty(tot.value + 1, np.int32)
-        src = np.empty(nref.value, np.uint16)
-        N.lib().ml_staging_export_seg(h, 0, C.byref(nref), N.ptr(toff), N.ptr(src))
-        for u in range(tot.value):
-            b = int(np.searchsorted(off, u, side="right") - 1)
-            slots = src[toff[u]:toff[u + 1]]
-            elems, args = b * bs + (slots & 255), slots >> 8
-            assert np.all([cols[a][e] == lst[u] for a, e in zip(args, elems)])
-            assert np.all(np.diff(elems.astype(np.int64) * 8 + args) > 0)
-        N.lib().ml_staging_free(h)
-
-
-def _check_tile_plan(h, table, n, inc_cols, red_col, budget, cmax):
-    """Invariants of a tile plan (csrc/host_tile.cpp): every INC incidence is
-    evaluated by exactly the tile owning its target, staged lists resolve every
-    map entry of every evaluated element, colours separate elements sharing an
-    owned target, every element has exactly one reduction owner, budgets hold."""
-    table = np.asarray(table[:n], dtype=np.int64)
-    owner = np.full(int(table.max(initial=-1)) + 1, -1)
-    red_count = np.zeros(n, np.int64)
-    evaluated = set()
-    for t in range(h["count"]):
-        lst = h["list"][h["list_off"][t]:h["list_off"][t + 1]]
-        c = int(h["nown"][t])
-        own, halo = lst[:c], lst[c:]
-        assert np.all(np.diff(own) > 0) and np.all(np.diff(halo) > 0)
-        assert not set(own.tolist()) & set(halo.tolist())
-        assert np.all(owner[own] < 0)
-        owner[own] = t
-        assert c <= cmax and lst.size * h["stage_bytes"] + c * h["own_bytes"] <= budget
-        k0, k1 = h["elem_off"][t], h["elem_off"][t + 1]
-        el = h["elem"][k0:k1]
-        assert np.all(np.diff(el) > 0)
-        loc = h["loc"][k0 * h["arity"]:k1 * h["arity"]].reshape(-1, h["arity"])
-        np.testing.assert_array_equal(lst[loc], table[el])
-        col = h["ecol"][k0:k1] & 127
-        assert col.size == 0 or col.max() < h["ncol"][t]
-        seen = {}
-        for i, e in enumerate(el.tolist()):
-            for j in inc_cols:
-                if loc[i, j] < c:
-                    key = (int(loc[i, j]), int(col[i]))
-                    assert seen.get(key, e) == e, "two elements of one colour share an owned target"
-                    seen[key] = e
-            evaluated.add((t, e))
-        red_count[el[(h["ecol"][k0:k1] & 128) > 0]] += 1
-    for e in range(n):
-        for j in inc_cols:
-            assert (owner[table[e, j]], e) in evaluated
-    assert np.all(red_count == 1)
-    for e in range(n):
-        assert (owner[table[e, red_col]], e) in evaluated
-
-
-def test_tile_plan_invariants_fuzz(rng):
-    from paper_1403_7209_b200.device import tile_plan_host
-    for trial in range(30):
-        mesh, loop = _cases.random_loop_mesh(rng, max_elems=400)
-        m = mesh.maps["m"]
-        n = m.from_set.size
-        budget = int(rng.choice([200, 600, 4000]))
-        cmax = int(rng.choice([1, 3, 16, 512]))
-        try:
-            h = tile_plan_host(loop, n, budget, cmax, None)
-        except ml.ExecError as ex:               # a hub target alone over budget / > 127 colours
-            assert "budget" in str(ex) or "colours" in str(ex)
-            continue
-        _check_tile_plan(h, m.table, n, list(range(m.arity)), 0, budget, cmax)
-        _check_tile_incidences(h, m.table, n, list(range(m.arity)))
-
-
-def _check_tile_incidences(h, table, n, inc_cols):
-    """Tile-gather lists: per owned target, exactly its (element, INC column)
-    incidences in the tile, element-then-column order."""
-    table = np.asarray(table[:n], dtype=np.int64)
-    for t in range(h["count"]):
-        lst = h["list"][h["list_off"][t]:h["list_off"][t + 1]]
-        c = int(h["nown"][t])
-        k0, k1 = h["elem_off"][t], h["elem_off"][t + 1]
-        el = h["elem"][k0:k1]
-        base = h["inc_base"][t]
-        for j in range(c):
-            q0, q1 = h["inc_off"][base + j], h["inc_off"][base + j + 1]
-            got = [(int(el[k]), int(col)) for k, col in zip(h["inc_k"][q0:q1], h["inc_c"][q0:q1])]
-            want = sorted((int(e), col) for e in el for col in inc_cols if table[e, col] == lst[j])
-            assert got == want
-
-
-def test_tile_plan_invariants_proxy_mesh_with_coords():
-    from paper_1403_7209_b200.device import tile_plan_host
-    mesh = apps.gen_hex_mesh(7, seed=2)
-    apps.shuffle_mesh(mesh, seed=3)
-    prog, _ = apps.build_hydra_proxy(mesh, steps=1, seed=0)
-    ml.renumber_mesh(mesh)
-    loop = next(l for l in prog if l.name == "vflux")
-    m = mesh.maps["edge_nodes"]
-    coords = mesh.dats["coords"].fetch()
-    for c in (coords, None):
-        h = tile_plan_host(loop, m.from_set.size, 20_000, 64, c)
-        assert h["count"] > 1
-        _check_tile_plan(h, m.table, m.from_set.size, [0, 1], 0, 20_000, 64)
-        _check_tile_incidences(h, m.table, m.from_set.size, [0, 1])
-    with pytest.raises(ml.ExecError, match="budget"):
-        tile_plan_host(loop, m.from_set.size, 500, 64, None)
-
-
 def test_gather_hub_rows_and_pfold_lists(rng):
     """Gather lists with hub splitting: every target's incidences covered once,
     in serial order, rows of <= hub_row; pfold lists = the position-0 / >0

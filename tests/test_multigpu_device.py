@@ -90,9 +90,9 @@ def _run(case, world=2, executor="stream"):
 
 
 @pytest.mark.parametrize("world,part,sched,executor", [
-    (2, "rcb", "gather", "stream"), (3, "trivial", "gather", "stream"), (2, "rcb", "flow", "stream"),
+    (2, "rcb", "gather", "stream"), (3, "trivial", "gather", "stream"), (2, "rcb", "colour", "stream"),
     (2, "rcb", "gather", "stream+copy"), (3, "trivial", "pfold", "stream+copy"),
-    (3, "trivial", "arrival", "host"), (2, "trivial", "colour", "host"), (2, "rcb", "tile", "stream"),
+    (3, "trivial", "colour", "host"), (2, "trivial", "colour", "host"),
     (2, "rcb", "pfold", "stream")])
 def test_ranks_on_device_match_reference_int64(world, part, sched, executor):
     from conftest import golden
@@ -105,7 +105,7 @@ def test_ranks_on_device_match_reference_int64(world, part, sched, executor):
 
 
 @pytest.mark.parametrize("sched,executor", [("gather", "stream"), ("gather", "stream+copy"),
-                                            ("flow", "host"), ("pfold", "stream"), ("auto", "stream+copy")])
+                                            ("colour", "host"), ("pfold", "stream"), ("auto", "stream+copy")])
 def test_proxy_two_ranks_on_device_vs_oracle(sched, executor):
     import paper_1403_7209_b200 as ml
     from oracle import bulk

@@ -129,6 +129,11 @@ typedef struct ml_loop {
     void *pf_part1, *pf_part2;
     int64_t pf_nhub1, pf_nhub2;
     const int32_t *pf_hub1_tl, *pf_hub1_off, *pf_hub2_tl, *pf_hub2_off;
+    /* colour schedule: launch only block colours [colour_begin, colour_end)
+     * (colour_end <= 0: all).  The reduction combine runs with the launch
+     * that reaches the last colour, so a host loop over single colours (the
+     * reference's per-phase callback, executor.py:251-252) reduces once. */
+    int32_t colour_begin, colour_end;
 } ml_loop_t;
 
 typedef struct ml_device_info {

@@ -202,6 +202,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     const int lp = layout_policy(L);
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
+    bool last_colour = true;   // false: a partial colour range that does not end the loop
     if (L->pf_n1 > 0) {
         // primary fold: pass 1 over targets' primary incidences (persistent grid),
         // pass 2 folds the secondary slots
@@ -293,7 +294,10 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
         const bool staged = f.staged && bs <= 256;
         const LaunchFn fn = staged ? f.staged : f.phased;
         const int threads = staged ? round_up32(bs) : std::clamp(round_up32(bs), 32, 256);
-        for (int64_t c = 0; c < L->plan.ncolors; ++c) {
+        const int64_t c0 = std::max<int64_t>(0, L->colour_begin);
+        const int64_t c1 = L->colour_end > 0 ? std::min<int64_t>(L->colour_end, L->plan.ncolors) : L->plan.ncolors;
+        if (c1 < L->plan.ncolors) last_colour = false;
+        for (int64_t c = c0; c < c1; ++c) {
             const int64_t off = L->plan.color_offsets[c], cnt = L->plan.color_offsets[c + 1] - off;
             if (cnt <= 0) continue;
             p.blocks = L->plan.blocks + off;
@@ -303,7 +307,7 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) ML_FAIL(ML_ECUDA, "loop '%s': launch failed: %s", L->name, cudaGetErrorString(err));
 
-    for (int i = 0; i < f.nargs; ++i) {
+    for (int i = 0; i < f.nargs && last_colour; ++i) {
         const ml_arg_t &a = L->args[i];
         if (a.kind != ML_GLOBAL || a.mode == ML_READ) continue;
         if (a.dtype == ML_F64)

@@ -397,6 +397,39 @@ class CompiledProgram:
             return [float(ms[i]) * 1e-3 for i in range(len(self.entries))]
         return None
 
+    def run_phases(self, callback) -> None:
+        """Eager run with the reference's per-phase hook (executor.py:251-252):
+        a loop on the colour schedule is launched one block colour at a time,
+        ``callback(loop name, colour)`` called before each colour, with the
+        device synchronised after it; loops on the target-centric and direct
+        schedules have no colour phases and run without callbacks."""
+        L = N.lib()
+        for d in self.all_dats:
+            dat_mirror(d)
+        hv = self.ghost.array
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            hv[o:o + g.buffer.nbytes] = g.buffer.view(np.uint8)
+        N.check(L.ml_upload(self.gdev.ptr, N.ptr(hv), self.gbytes), "ml_upload")
+        for e in self.entries:
+            coloured = (e.gather is None and e.pfold is None and e.plan.has_writes and e.n > 0)
+            if not coloured:
+                N.check(L.ml_loop_run(C.byref(e.desc)), f"loop {e.loop.name!r}")
+                continue
+            for c in range(e.plan.ncolors):
+                callback(e.loop.name, c)
+                desc = type(e.desc).from_buffer_copy(e.desc)
+                desc.colour_begin, desc.colour_end = c, c + 1
+                N.check(L.ml_loop_run(C.byref(desc)), f"loop {e.loop.name!r} colour {c}")
+                N.check(L.ml_synchronize(), "ml_synchronize")
+        N.check(L.ml_download(N.ptr(hv), self.gdev.ptr, self.gbytes), "ml_download")
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            g.buffer[:] = hv[o:o + g.buffer.nbytes].view(g.buffer.dtype)
+        for d in self.written:
+            d._dev.device_newer = True
+        self.runs += 1
+
     def _stream_plan(self):
         """Per loop: the input dats first used there (uploaded just before it)
         and the written dats last written there (downloaded right after it).
@@ -578,9 +611,10 @@ def run_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig | Non
         return RunResult([], 0.0)
     cp = compile_program(program, mesh, config)
     if config.phase_callback is not None:
-        for e in cp.entries:
-            for c in range(e.plan.ncolors):
-                config.phase_callback(e.loop.name, c)
+        cp.run_phases(config.phase_callback)
+        if config.residency == "host":
+            _sync_host(cp.written)
+        return RunResult(collector.finalize(), time.perf_counter() - t0)
     host = config.residency == "host"
     if host and (config.use_graph or not config.time_loops):
         cp.run_streamed()
@@ -600,6 +634,9 @@ def run_loop(loop: Loop, mesh: Mesh, config: BackendConfig | None = None,
     config = config or BackendConfig()
     mesh.freeze()
     cp = compile_program([loop], mesh, config)
+    if config.phase_callback is not None:
+        cp.run_phases(config.phase_callback)
+        return
     times = cp.run(False, config.time_loops or collector is not None)
     if collector is not None and times is not None:
         _record(collector, cp, times)

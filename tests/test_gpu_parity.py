@@ -477,3 +477,48 @@ def test_config_d_proxy_iteration_vs_oracle():
     assert h["dt_min"][0].value == rh["dt_min"][0].value
 
 
+
+
+def test_phase_callback_instruments_each_colour_phase():
+    """Reference tests/test_executor.py:324-364 instruments the threads
+    backend's colour phases with BackendConfig.phase_callback.  Here the
+    callback fires before each block colour's launch (colour schedule) and the
+    device state between two callbacks shows exactly the increments of that
+    colour's blocks; the result equals the serial oracle."""
+    import ctypes as C
+    from paper_1403_7209_b200 import _native as N
+    from paper_1403_7209_b200.plan import plan_for
+    ref = apps.gen_mesh(12)
+    oserial.run_loop(_cases.inc_loop(ref, "edge_nodes"))
+    mesh = apps.gen_mesh(12)
+    loop = _cases.inc_loop(mesh, "edge_nodes")
+    acc = mesh.dats["acc"]
+    bs = 16
+    snaps, calls = [], []
+
+    def device_acc():
+        m = acc._dev
+        out = np.empty(acc.set.size, np.int64)
+        N.check(N.lib().ml_download(N.ptr(out), m.ptr, out.nbytes))
+        return out
+
+    def cb(name, colour):
+        calls.append((name, colour))
+        snaps.append(device_acc())
+
+    ml.run_threads(loop, mesh, cfg(block_size=bs, phase_callback=cb))
+    plan = plan_for(loop, mesh, bs)
+    assert calls == [(loop.name, c) for c in range(plan.ncolors)] and plan.ncolors > 1
+    snaps.append(acc.fetch().ravel())
+    np.testing.assert_array_equal(snaps[-1], ref.dats["acc"].fetch().ravel())
+    table = mesh.maps["edge_nodes"].table
+    for c in range(plan.ncolors):
+        blocks = np.flatnonzero(plan.block_color == c)
+        elems = np.concatenate([np.arange(b * bs, min((b + 1) * bs, table.shape[0])) for b in blocks])
+        touched = np.unique(table[elems].ravel())
+        changed = np.flatnonzero(snaps[c + 1] != snaps[c])
+        assert set(changed) <= set(touched)
+    # loops on the target-centric schedules have no colour phases
+    calls.clear()
+    ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh, cfg(phase_callback=cb, inc_schedule="gather"))
+    assert calls == []

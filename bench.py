@@ -25,8 +25,11 @@ containing vflux).
                  loops and downloads overlap on three streams.  ``e2e.pcie``:
                  measured pinned H2D / D2H bandwidth and the step times they
                  bound (all inputs through H2D; + the serial D2H).
-* ``roofline``   vflux (``iflux+vflux`` chained): B_alg / mean loop time from an eager pass with
-                 CUDA events between loops (same stream).
+* ``roofline``   vflux (``iflux+vflux`` chained): B_alg / its mean device time in
+                 the steady-state CUDA graph (a sequential capture of the same
+                 program with a timing event between loops, K replays); the
+                 per-loop ``loops`` table is measured the same way (``eager_ms``:
+                 eager launches with events, for comparison).
 * ``cpu_baseline`` the stock reference (``meshloop.run_program`` from
                  baseline/_ref) on this host's CPUs in its three modes:
                  serial on the full workload (once), threads (all CPUs) and
@@ -269,16 +272,21 @@ def run_ours(args) -> None:
     total_ms = ms.value
     value = edges * args.steps / (total_ms * 1e-3)
 
-    # -- per-loop breakdown (eager, CUDA events between loops on the same stream) ----------
-    per_loop = {e.loop.name: [] for e in cp.entries}
+    # -- per-loop breakdown: the steady-state graph with a timing event between
+    #    loops (sequential capture, mean of K replays); eager launches beside it
+    graph_loop_s = cp.replay_timed(max(3, args.steps))
+    per_loop = {e.loop.name: [t] for e, t in zip(cp.entries, graph_loop_s)}
+    eager = {e.loop.name: [] for e in cp.entries}
     for _ in range(max(3, args.steps // 2)):
         for e, t in zip(cp.entries, cp.run(False, True)):
-            per_loop[e.loop.name].append(t)
+            eager[e.loop.name].append(t)
     loops = {}
     peak, peak_src = peaks_gbs()
     for e in cp.entries:
         t = statistics.mean(per_loop[e.loop.name])
-        loops[e.loop.name] = {"ms": round(t * 1e3, 4), "b_alg": e.alg, "useful_bytes": e.useful,
+        loops[e.loop.name] = {"ms": round(t * 1e3, 4),
+                              "eager_ms": round(statistics.mean(eager[e.loop.name]) * 1e3, 4),
+                              "b_alg": e.alg, "useful_bytes": e.useful,
                               "gbs_alg": round(e.alg / t / 1e9, 1),
                               "frac_of_peak": round(e.alg / t / 1e9 / peak, 4),
                               "schedule": e.sched if e.plan.has_writes else "direct",
@@ -338,7 +346,8 @@ def run_ours(args) -> None:
                                    "frac": round(sum(e.alg for e in cp.entries) / (total_ms * 1e-3 / args.steps) / 1e9 / peak, 4)},
                      "mean_loop_ms": round(t_dom * 1e3, 4)},
         "loops": loops,
-        "eager_ms_per_step": round(sum(v["ms"] for v in loops.values()), 4),
+        "eager_ms_per_step": round(sum(v["eager_ms"] for v in loops.values()), 4),
+        "graph_loops_ms_per_step": round(sum(v["ms"] for v in loops.values()), 4),
         "e2e": e2e,
         "cpu_baseline": cb,
         "scaling_base": scale_base,

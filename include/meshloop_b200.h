@@ -258,6 +258,10 @@ int ml_program_run(ml_program_t *p, int32_t use_graph, int32_t time_loops);
  * between replays (device-throughput measurement); syncs at the end. */
 int ml_program_replay(ml_program_t *p, int32_t count);
 int ml_program_loop_times(const ml_program_t *p, float *ms);
+/* Per-loop device milliseconds of the steady-state graph: `count` replays of a
+ * sequential capture with a timing event between loops; ms[i] is loop i's
+ * mean (globals travel as in ml_program_run). */
+int ml_program_replay_timed(ml_program_t *p, int32_t count, float *ms);
 /* Concurrent loops for untimed runs and graphs: loop j waits only for the
  * earlier loops sharing a dat/global buffer with it where either writes
  * (RAW/WAR/WAW), so independent loops overlap on up to four streams; results

@@ -36,6 +36,7 @@ EXPORTED = [
     "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name", "ml_chain_lookup",
     "ml_loop_scratch_bytes", "ml_loop_run", "ml_loop_pfold_slot_bytes",
     "ml_program_create", "ml_program_run", "ml_program_replay", "ml_program_loop_times",
+    "ml_program_replay_timed",
     "ml_program_free", "ml_program_set_concurrent", "ml_program_deps",
     "ml_pack_rows", "ml_unpack_rows", "ml_combine_ranks", "ml_stream",
     "ml_ipc_handle", "ml_ipc_open", "ml_ipc_close", "ml_put_rows", "ml_wait_flag", "ml_signal_flag",
@@ -135,6 +136,7 @@ _SIGNATURES = {
     "ml_program_run": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "ml_program_replay": (C.c_int, [_P, C.c_int32]),
     "ml_program_loop_times": (C.c_int, [_P, C.POINTER(C.c_float)]),
+    "ml_program_replay_timed": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_float)]),
     "ml_program_set_concurrent": (C.c_int, [_P, C.c_int32]),
     "ml_program_deps": (C.c_int, [_P, C.c_int32, _I32P, _P, _I32P]),
     "ml_program_free": (C.c_int, [_P]),

@@ -11,6 +11,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "engine.cuh"
 #include "ml_common.h"
 
@@ -154,7 +156,18 @@ static int cached_occupancy(int functor, int kernel, int threads, int (*query)(i
     return occ;
 }
 
+static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream);
+
+// NVTX range per loop enqueue (named after the loop), so nsys/ncu timelines
+// attribute every launch and combine to its op_par_loop
 static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
+    nvtxRangePushA(L && L->name ? L->name : "loop");
+    const int rc = enqueue_loop_impl(L, stream);
+    nvtxRangePop();
+    return rc;
+}
+
+static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
     auto &reg = registry();
     if (L->functor < 0 || L->functor >= int(reg.size()))
         ML_FAIL(ML_ENOFUNCTOR, "loop '%s': bad functor id %d", L->name ? L->name : "?", L->functor);
@@ -600,6 +613,8 @@ struct ml_program {
     uint64_t gbytes = 0;
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
+    cudaGraphExec_t texec = nullptr;             // sequential graph with per-loop timing events
+    cudaGraph_t tgraph = nullptr;
     std::vector<cudaEvent_t> events;
     std::vector<float> times;
     // concurrent loops (untimed runs and graphs): loop j waits only for the
@@ -646,16 +661,19 @@ static void program_deps(ml_program *p) {
     }
 }
 
-static int program_enqueue(ml_program *p, bool timed) {
+// `external`: the timing events become event-record nodes of a graph being
+// captured (cudaEventRecordExternal), so their elapsed times are readable
+static int program_enqueue(ml_program *p, bool timed, bool external = false) {
     cudaStream_t s = g_dev.stream;
+    const unsigned rec = external ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (p->gbytes) ML_CUDA(cudaMemcpyAsync(p->gdev, p->ghost, p->gbytes, cudaMemcpyHostToDevice, s));
     if (timed || !p->concurrent) {
         for (size_t i = 0; i < p->loops.size(); ++i) {
-            if (timed) ML_CUDA(cudaEventRecord(p->events[i], s));
+            if (timed) ML_CUDA(cudaEventRecordWithFlags(p->events[i], s, rec));
             int rc = enqueue_loop(&p->loops[i], s);
             if (rc) return rc;
         }
-        if (timed) ML_CUDA(cudaEventRecord(p->events[p->loops.size()], s));
+        if (timed) ML_CUDA(cudaEventRecordWithFlags(p->events[p->loops.size()], s, rec));
     } else {
         cudaStream_t lanes[kLanes] = {s, p->side[0], p->side[1], p->side[2]};
         ML_CUDA(cudaEventRecord(p->fork, s));                 // side lanes join (capture-safe)
@@ -733,6 +751,45 @@ static int program_capture(ml_program *p) {
     return ML_OK;
 }
 
+// per-loop device times of the steady-state graph: a sequential capture with
+// an event record node between loops (timing events work inside graphs)
+static int program_capture_timed(ml_program *p) {
+    if (p->texec) return ML_OK;
+    cudaStream_t s = g_dev.stream;
+    ML_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int rc = program_enqueue(p, true, true);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) ML_FAIL(ML_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    p->tgraph = g;
+    ML_CUDA(cudaGraphInstantiate(&p->texec, g, 0));
+    return ML_OK;
+}
+
+extern "C" int ml_program_replay_timed(ml_program_t *p, int32_t count, float *ms) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (!p || !ms || count < 1) ML_FAIL(ML_EINVAL, "ml_program_replay_timed: bad arguments");
+    rc = program_capture_timed(p);
+    if (rc) return rc;
+    std::vector<double> acc(p->loops.size(), 0.0);
+    for (int32_t i = 0; i < count; ++i) {
+        ML_CUDA(cudaGraphLaunch(p->texec, g_dev.stream));
+        ML_CUDA(cudaStreamSynchronize(g_dev.stream));
+        for (size_t j = 0; j < p->loops.size(); ++j) {
+            float t = 0.f;
+            ML_CUDA(cudaEventElapsedTime(&t, p->events[j], p->events[j + 1]));
+            acc[j] += t;
+        }
+    }
+    for (size_t j = 0; j < p->loops.size(); ++j) ms[j] = float(acc[j] / count);
+    return ML_OK;
+}
+
 extern "C" int ml_program_replay(ml_program_t *p, int32_t count) {
     int rc = ensure_init();
     if (rc) return rc;
@@ -793,6 +850,8 @@ extern "C" int ml_program_free(ml_program_t *p) {
     if (!p) return ML_OK;
     if (p->exec) cudaGraphExecDestroy(p->exec);
     if (p->graph) cudaGraphDestroy(p->graph);
+    if (p->texec) cudaGraphExecDestroy(p->texec);
+    if (p->tgraph) cudaGraphDestroy(p->tgraph);
     for (auto &e : p->events) cudaEventDestroy(e);
     for (auto &e : p->done) cudaEventDestroy(e);
     if (p->fork) cudaEventDestroy(p->fork);

@@ -276,6 +276,9 @@ class _LoopEntry:
             nb = C.c_uint64()
             N.check(N.lib().ml_loop_pfold_slot_bytes(C.byref(L), C.byref(nb)))
             self.pf_slots = N.DeviceBuffer(max(nb.value, 8))
+            # slot rows are padded to whole 16-byte pairs that pass 2 copies in
+            # full; zero the pads once (pass 1 never writes them)
+            N.check(N.lib().ml_memset(self.pf_slots.ptr, 0, self.pf_slots.nbytes), "ml_memset")
             L.pf_slots = self.pf_slots.ptr
         elif sched == "gather" and self.n > 0 and gather_eligible(loop):
             self.gather = gather_mirror(loop, self.plan, hubs=True)
@@ -525,6 +528,26 @@ class CompiledProgram:
         for d in self.written:
             d._dev.device_newer = True
         self.runs += count
+
+    def replay_timed(self, count: int) -> list:
+        """Per-loop device seconds of the steady-state CUDA graph (mean of
+        ``count`` replays of a sequential capture with timing events between
+        loops); globals are written back as after a run."""
+        for d in self.all_dats:
+            dat_mirror(d)
+        hv = self.ghost.array
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            hv[o:o + g.buffer.nbytes] = g.buffer.view(np.uint8)
+        ms = (C.c_float * max(len(self.entries), 1))()
+        N.check(N.lib().ml_program_replay_timed(self.handle, int(count), ms), "ml_program_replay_timed")
+        for g in self.globs:
+            o = self.gslot[id(g)]
+            g.buffer[:] = hv[o:o + g.buffer.nbytes].view(g.buffer.dtype)
+        for d in self.written:
+            d._dev.device_newer = True
+        self.runs += count
+        return [float(ms[i]) * 1e-3 for i in range(len(self.entries))]
 
     def launches_per_run(self) -> int:
         """Kernel launches one run enqueues (colour launches + reduction combines)."""

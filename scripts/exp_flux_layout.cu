@@ -33,6 +33,34 @@ struct View {
     }
 };
 
+__device__ __forceinline__ double ld_keep(const double *p) {
+    double v;
+    asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double *p) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+// HINT 0: plain; 1: evict_last (own rows); 2: no_allocate (neighbour rows)
+template <int LAY, int HINT>
+struct HView {
+    const double *p;
+    int64_t pitch;
+    __device__ __forceinline__ double operator[](int c) const {
+        const double *q = LAY == 0 ? p + c * pitch : p + c * 32;
+        if constexpr (HINT == 1) return ld_keep(q);
+        else if constexpr (HINT == 2) return ld_stream(q);
+        else return *q;
+    }
+};
+template <int LAY, int D, int HINT>
+__device__ __forceinline__ HView<LAY, HINT> hview(const double *base, int64_t e, int64_t pitch) {
+    if constexpr (LAY == 0) return HView<LAY, HINT>{base + e, pitch};
+    else return HView<LAY, HINT>{base + (e >> 5) * (32 * D) + (e & 31), pitch};
+}
+
 template <int LAY, int D>
 __device__ __forceinline__ View<LAY> view(const double *base, int64_t e, int64_t pitch) {
     if constexpr (LAY == 0) return View<LAY>{base + e, pitch};
@@ -342,6 +370,216 @@ __global__ void __launch_bounds__(256, 2) k_flux_lock(const __grid_constant__ Da
     }
 }
 
+// thread per target; the neighbour's (second endpoint's) rows are loaded into
+// registers in one wave before the arithmetic, the next edge's record is
+// prefetched while the current edge computes.  MINB CTAs of 256 per SM.
+template <int LAY>
+struct RegRow {
+    double q[NQ], x[3], l[NLIM], g[NG], a[NAUX];
+    __device__ __forceinline__ void load(const Data &d, int64_t b) {
+        const int64_t P = d.pitch;
+        const auto vq = view<LAY, NQ>(d.q, b, P);
+        const auto vl = view<LAY, NLIM>(d.lim, b, P);
+        const auto vg = view<LAY, NG>(d.grad, b, P);
+        const auto va = view<LAY, NAUX>(d.aux, b, P);
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) q[c] = vq[c];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) x[c] = d.x[b * 3 + c];
+#pragma unroll
+        for (int c = 0; c < NLIM; ++c) l[c] = vl[c];
+#pragma unroll
+        for (int c = 0; c < NG; ++c) g[c] = vg[c];
+#pragma unroll
+        for (int c = 0; c < NAUX; ++c) a[c] = va[c];
+    }
+};
+
+template <int LAY>
+__device__ __forceinline__ void eval_edge_reg(const Data &d, int64_t e, int64_t a, const RegRow<LAY> &nb,
+                                              double *r1, double *r2) {
+    const int64_t P = d.pitch;
+    const double *w = d.w + e * 3, *x1 = d.x + a * 3;
+    const double *x2 = nb.x;
+    const auto q1 = view<LAY, NQ>(d.q, a, P);
+    const auto l1 = view<LAY, NLIM>(d.lim, a, P);
+    const auto g1 = view<LAY, NG>(d.grad, a, P);
+    const auto a1 = view<LAY, NAUX>(d.aux, a, P);
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double an = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NLIM; ++j) {
+            const double tt = l1[j] + nb.l[j];
+            s = s + tt * tt;
+        }
+        const double lam = an / ((1.0 + ds) * (1.0 + 0.0625 * s));
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const double f = lam * (nb.q[v] - q1[v]);
+            r1[v] = 0.0 + f;
+            r2[v] = 0.0 - f;
+        }
+    }
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds2 = d0 * d0 + d1 * d1 + d2 * d2 + 1e-12;
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double wd = w0 * d0 + w1 * d1 + w2 * d2;
+        double mu = 0.0;
+#pragma unroll
+        for (int j = 0; j < NAUX; ++j) mu = mu + (a1[j] + nb.a[j]);
+        mu = 0.01 * mu / (2.0 * NAUX);
+        const double awd = fabs(wd);
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const int bb = 3 * v;
+            const double gx = 0.5 * (g1[bb] + nb.g[bb]);
+            const double gy = 0.5 * (g1[bb + 1] + nb.g[bb + 1]);
+            const double gz = 0.5 * (g1[bb + 2] + nb.g[bb + 2]);
+            const double dq = nb.q[v] - q1[v];
+            const double corr = (dq - (gx * d0 + gy * d1 + gz * d2)) / ds2;
+            const double f = mu * (0.001 * (gx * w0 + gy * w1 + gz * w2) + corr * awd);
+            r1[v] += f;
+            r2[v] -= f;
+        }
+    }
+}
+
+template <int LAY, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_flux_reg(const __grid_constant__ Data d) {
+    const int64_t P = d.pitch;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < d.n1;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t tg = __ldg(d.tl1 + t);
+        double run[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(tg, c, P)];
+        int k = __ldg(d.off1 + t);
+        const int ke = __ldg(d.off1 + t + 1);
+        int64_t e = k < ke ? __ldg(d.elem1 + k) : 0;
+        int64_t b = k < ke ? __ldg(d.rec + 2 * int64_t(k) + 1) : 0;
+        for (; k < ke; ++k) {
+            RegRow<LAY> nb;
+            nb.load(d, b);
+            const int64_t ecur = e;
+            if (k + 1 < ke) {                      // next record while this edge computes
+                e = __ldg(d.elem1 + k + 1);
+                b = __ldg(d.rec + 2 * int64_t(k + 1) + 1);
+            }
+            double r1[NQ], r2[NQ];
+            eval_edge_reg<LAY>(d, ecur, tg, nb, r1, r2);
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] += r1[c];
+            store_slot(d, ecur, r2);
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(tg, c, P)] = run[c];
+    }
+}
+
+template <int LAY, int H1, int H2>
+__device__ __forceinline__ void eval_edge_h(const Data &d, int64_t e, int64_t a, int64_t b, double *r1,
+                                            double *r2) {
+    const int64_t P = d.pitch;
+    const double *w = d.w + e * 3, *x1 = d.x + a * 3, *x2 = d.x + b * 3;
+    const auto q1 = hview<LAY, NQ, H1>(d.q, a, P);
+    const auto q2 = hview<LAY, NQ, H2>(d.q, b, P);
+    const auto l1 = hview<LAY, NLIM, H1>(d.lim, a, P);
+    const auto l2 = hview<LAY, NLIM, H2>(d.lim, b, P);
+    const auto g1 = hview<LAY, NG, H1>(d.grad, a, P);
+    const auto g2 = hview<LAY, NG, H2>(d.grad, b, P);
+    const auto a1 = hview<LAY, NAUX, H1>(d.aux, a, P);
+    const auto a2 = hview<LAY, NAUX, H2>(d.aux, b, P);
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double an = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NLIM; ++j) {
+            const double tt = l1[j] + l2[j];
+            s = s + tt * tt;
+        }
+        const double lam = an / ((1.0 + ds) * (1.0 + 0.0625 * s));
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const double f = lam * (q2[v] - q1[v]);
+            r1[v] = 0.0 + f;
+            r2[v] = 0.0 - f;
+        }
+    }
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds2 = d0 * d0 + d1 * d1 + d2 * d2 + 1e-12;
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double wd = w0 * d0 + w1 * d1 + w2 * d2;
+        double mu = 0.0;
+#pragma unroll
+        for (int j = 0; j < NAUX; ++j) mu = mu + (a1[j] + a2[j]);
+        mu = 0.01 * mu / (2.0 * NAUX);
+        const double awd = fabs(wd);
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const int bb = 3 * v;
+            const double gx = 0.5 * (g1[bb] + g2[bb]);
+            const double gy = 0.5 * (g1[bb + 1] + g2[bb + 1]);
+            const double gz = 0.5 * (g1[bb + 2] + g2[bb + 2]);
+            const double dq = q2[v] - q1[v];
+            const double corr = (dq - (gx * d0 + gy * d1 + gz * d2)) / ds2;
+            const double f = mu * (0.001 * (gx * w0 + gy * w1 + gz * w2) + corr * awd);
+            r1[v] += f;
+            r2[v] -= f;
+        }
+    }
+}
+
+// thread per target with cache hints (H1 own rows, H2 neighbour rows) and, with
+// PF, the next edge's record prefetched while the current edge computes
+template <int LAY, int H1, int H2, int PF>
+__global__ void __launch_bounds__(256, 2) k_flux_h(const __grid_constant__ Data d) {
+    const int64_t P = d.pitch;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < d.n1;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t tg = __ldg(d.tl1 + t);
+        double run[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(tg, c, P)];
+        int k = __ldg(d.off1 + t);
+        const int ke = __ldg(d.off1 + t + 1);
+        int64_t e = 0, b = 0;
+        if (PF && k < ke) {
+            e = __ldg(d.elem1 + k);
+            b = __ldg(d.rec + 2 * int64_t(k) + 1);
+        }
+        for (; k < ke; ++k) {
+            int64_t ecur, bcur;
+            if (PF) {
+                ecur = e;
+                bcur = b;
+                if (k + 1 < ke) {
+                    e = __ldg(d.elem1 + k + 1);
+                    b = __ldg(d.rec + 2 * int64_t(k + 1) + 1);
+                }
+            } else {
+                ecur = __ldg(d.elem1 + k);
+                bcur = __ldg(d.rec + 2 * int64_t(k) + 1);
+            }
+            double r1[NQ], r2[NQ];
+            eval_edge_h<LAY, H1, H2>(d, ecur, tg, bcur, r1, r2);
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] += r1[c];
+            store_slot(d, ecur, r2);
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(tg, c, P)] = run[c];
+    }
+}
+
 }  // namespace
 
 extern "C" int exp_flux_run(int layout, const void *w, const void *q, const void *x, const void *lim,
@@ -417,5 +655,46 @@ extern "C" int exp_flux_lock(int layout, const void *w, const void *q, const voi
     if (k == 3) { if (lay == 0) k_flux_lock<0, 3><<<grid, 256, 0, s>>>(d); else k_flux_lock<1, 3><<<grid, 256, 0, s>>>(d); }
     else if (k == 2) { if (lay == 0) k_flux_lock<0, 2><<<grid, 256, 0, s>>>(d); else k_flux_lock<1, 2><<<grid, 256, 0, s>>>(d); }
     else { if (lay == 0) k_flux_lock<0, 4><<<grid, 256, 0, s>>>(d); else k_flux_lock<1, 4><<<grid, 256, 0, s>>>(d); }
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_reg(int layout, const void *w, const void *q, const void *x, const void *lim,
+                            const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                            const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                            int64_t n1, int64_t pitch, int sms, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int lay = layout & 1, minb = layout >> 1;
+    if (minb == 1) { if (lay == 0) k_flux_reg<0, 1><<<sms, 256, 0, s>>>(d); else k_flux_reg<1, 1><<<sms, 256, 0, s>>>(d); }
+    else { if (lay == 0) k_flux_reg<0, 2><<<2 * sms, 256, 0, s>>>(d); else k_flux_reg<1, 2><<<2 * sms, 256, 0, s>>>(d); }
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_h(int variant, const void *w, const void *q, const void *x, const void *lim,
+                          const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                          const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                          int64_t n1, int64_t pitch, int grid, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (variant) {          // layout bit 0; then (hints, prefetch) combos
+    case 0: k_flux_h<0, 0, 0, 1><<<grid, 256, 0, s>>>(d); break;
+    case 1: k_flux_h<1, 0, 0, 1><<<grid, 256, 0, s>>>(d); break;
+    case 2: k_flux_h<0, 1, 2, 0><<<grid, 256, 0, s>>>(d); break;
+    case 3: k_flux_h<1, 1, 2, 0><<<grid, 256, 0, s>>>(d); break;
+    case 4: k_flux_h<0, 1, 2, 1><<<grid, 256, 0, s>>>(d); break;
+    case 5: k_flux_h<1, 1, 2, 1><<<grid, 256, 0, s>>>(d); break;
+    case 6: k_flux_h<0, 0, 2, 0><<<grid, 256, 0, s>>>(d); break;
+    default: k_flux_h<1, 0, 2, 0><<<grid, 256, 0, s>>>(d); break;
+    }
     return int(cudaGetLastError());
 }

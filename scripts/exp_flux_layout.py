@@ -89,6 +89,8 @@ def main():
     lib.exp_flux_lanes.argtypes = ([C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_void_p,
                                    C.c_int64, C.c_int, C.c_void_p])
     lib.exp_flux_lock.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_reg.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_h.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_lrec.argtypes = ([C.c_int] + [C.c_void_p] * 8 + [C.c_int64, C.c_void_p, C.c_void_p,
                                   C.c_int64, C.c_int, C.c_void_p])
     vals = {k: h[k].fetch() for k in ("q", "x", "lim", "grad", "aux", "res", "w")}
@@ -104,7 +106,11 @@ def main():
                              (0, 2, "soa_lrec"), (1, 2, "aosoa_lrec"), (2, 0, "soa_128x5"),
                              (3, 0, "aosoa_128x5"), (0, 3, "soa_lock3"), (1, 3, "aosoa_lock3"),
                              (0, 4, "soa_lock2"), (1, 4, "aosoa_lock2"), (0, 5, "soa_lock4"),
-                             (1, 5, "aosoa_lock4")):
+                             (1, 5, "aosoa_lock4"), (0, 6, "soa_reg1"), (1, 6, "aosoa_reg1"),
+                             (0, 7, "soa_reg2"), (1, 7, "aosoa_reg2"),
+                             (0, 10, "soa_pf"), (1, 11, "aosoa_pf"), (0, 12, "soa_hint"), (1, 13, "aosoa_hint"),
+                             (0, 14, "soa_hint_pf"), (1, 15, "aosoa_hint_pf"), (0, 16, "soa_nbr_noalloc"),
+                             (1, 17, "aosoa_nbr_noalloc")):
         def put(k):
             v = vals[k]
             if k in ("x", "w"):
@@ -123,7 +129,11 @@ def main():
                       T["res"].data_ptr(), slots.data_ptr(), ints["off1"].data_ptr(),
                       ints["elem1"].data_ptr(), ints["tl1"].data_ptr(), ints["rec"].data_ptr(),
                       ints["slotpos"].data_ptr(), int(tl1.size), n)
-            if lanes >= 3:
+            if lanes >= 10:
+                rc = lib.exp_flux_h(lanes - 10, *common[1:], sms * 2, stream)
+            elif lanes >= 6:
+                rc = lib.exp_flux_reg(lay + 2 * (lanes - 5), *common[1:], sms, stream)
+            elif lanes >= 3:
                 kk = {3: 3, 4: 2, 5: 4}[lanes]
                 rc = lib.exp_flux_lock(lay + 2 * kk, *common[1:], sms * 2, stream)
             elif lanes == 2:

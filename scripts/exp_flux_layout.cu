@@ -580,6 +580,114 @@ __global__ void __launch_bounds__(256, 2) k_flux_h(const __grid_constant__ Data 
     }
 }
 
+// warp-pair split: CTA = 4 warp pairs; pair p owns 32 targets (one per lane).
+// Warp 2p (role A) loads q, grad, x, w and forms the per-component terms;
+// warp 2p+1 (role B) loads lim, aux, x, w and forms the scalars lam and mu,
+// handed to A through shared memory between two named barriers per edge.
+// Same arithmetic (expression trees) as eval_edge.
+__device__ __forceinline__ void bar_pair(int id) {
+    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
+template <int LAY, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_flux_split(const __grid_constant__ Data d) {
+    __shared__ double sh[4][2][32];
+    const int64_t P = d.pitch;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = warp >> 1;
+    const bool roleA = (warp & 1) == 0;
+    const int bid = 1 + pair;                     // named barrier per pair (0 is __syncthreads)
+    for (int64_t t0 = (int64_t(blockIdx.x) * 4 + pair) * 32; t0 < d.n1; t0 += int64_t(gridDim.x) * 128) {
+        const int64_t t = t0 + lane;
+        const bool act = t < d.n1;
+        const int64_t tg = act ? __ldg(d.tl1 + t) : 0;
+        const int k0 = act ? __ldg(d.off1 + t) : 0, k1 = act ? __ldg(d.off1 + t + 1) : 0;
+        int len = k1 - k0;
+        // both warps of the pair walk max(len) steps in lockstep
+        for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+        double run[NQ];
+        if (roleA && act) {
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(tg, c, P)];
+        }
+        for (int j = 0; j < len; ++j) {
+            const bool live = act && k0 + j < k1;
+            const int k = k0 + j;
+            int64_t e = 0, b = 0;
+            if (live) {
+                e = __ldg(d.elem1 + k);
+                b = __ldg(d.rec + 2 * int64_t(k) + 1);
+            }
+            const double *x1 = d.x + tg * 3, *x2 = d.x + b * 3, *w = d.w + e * 3;
+            if (!roleA) {
+                double lam = 0.0, mu = 0.0;
+                if (live) {
+                    const auto l1 = view<LAY, NLIM>(d.lim, tg, P), l2 = view<LAY, NLIM>(d.lim, b, P);
+                    const auto a1 = view<LAY, NAUX>(d.aux, tg, P), a2 = view<LAY, NAUX>(d.aux, b, P);
+                    const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+                    const double ds = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+                    const double w0 = w[0], w1 = w[1], w2 = w[2];
+                    const double an = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+                    double s = 0.0;
+#pragma unroll
+                    for (int jj = 0; jj < NLIM; ++jj) {
+                        const double tt = l1[jj] + l2[jj];
+                        s = s + tt * tt;
+                    }
+                    lam = an / ((1.0 + ds) * (1.0 + 0.0625 * s));
+#pragma unroll
+                    for (int jj = 0; jj < NAUX; ++jj) mu = mu + (a1[jj] + a2[jj]);
+                    mu = 0.01 * mu / (2.0 * NAUX);
+                }
+                sh[pair][0][lane] = lam;
+                sh[pair][1][lane] = mu;
+                bar_pair(bid);                        // values ready
+                bar_pair(bid);                        // A has read them
+            } else {
+                double fq[NQ], dqs[NQ], corr[NQ];
+                double awd = 0.0;
+                if (live) {
+                    const auto q1 = view<LAY, NQ>(d.q, tg, P), q2 = view<LAY, NQ>(d.q, b, P);
+                    const auto g1 = view<LAY, NG>(d.grad, tg, P), g2 = view<LAY, NG>(d.grad, b, P);
+                    const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+                    const double ds2 = d0 * d0 + d1 * d1 + d2 * d2 + 1e-12;
+                    const double w0 = w[0], w1 = w[1], w2 = w[2];
+                    const double wd = w0 * d0 + w1 * d1 + w2 * d2;
+                    awd = fabs(wd);
+#pragma unroll
+                    for (int v = 0; v < NQ; ++v) {
+                        const int bb = 3 * v;
+                        const double gx = 0.5 * (g1[bb] + g2[bb]);
+                        const double gy = 0.5 * (g1[bb + 1] + g2[bb + 1]);
+                        const double gz = 0.5 * (g1[bb + 2] + g2[bb + 2]);
+                        const double dq = q2[v] - q1[v];
+                        dqs[v] = dq;
+                        corr[v] = (dq - (gx * d0 + gy * d1 + gz * d2)) / ds2;
+                        fq[v] = 0.001 * (gx * w0 + gy * w1 + gz * w2);
+                    }
+                }
+                bar_pair(bid);
+                const double lam = sh[pair][0][lane], mu = sh[pair][1][lane];
+                bar_pair(bid);
+                if (live) {
+                    double r2[NQ];
+#pragma unroll
+                    for (int v = 0; v < NQ; ++v) {
+                        const double fi = lam * dqs[v];
+                        const double f = mu * (fq[v] + corr[v] * awd);
+                        run[v] += (0.0 + fi) + f;
+                        r2[v] = (0.0 - fi) - f;
+                    }
+                    store_slot(d, e, r2);
+                }
+            }
+        }
+        if (roleA && act) {
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(tg, c, P)] = run[c];
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" int exp_flux_run(int layout, const void *w, const void *q, const void *x, const void *lim,
@@ -695,6 +803,28 @@ extern "C" int exp_flux_h(int variant, const void *w, const void *q, const void 
     case 5: k_flux_h<1, 1, 2, 1><<<grid, 256, 0, s>>>(d); break;
     case 6: k_flux_h<0, 0, 2, 0><<<grid, 256, 0, s>>>(d); break;
     default: k_flux_h<1, 0, 2, 0><<<grid, 256, 0, s>>>(d); break;
+    }
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_split(int variant, const void *w, const void *q, const void *x, const void *lim,
+                              const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                              const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                              int64_t n1, int64_t pitch, int sms, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (variant) {
+    case 0: k_flux_split<0, 2><<<2 * sms, 256, 0, s>>>(d); break;
+    case 1: k_flux_split<1, 2><<<2 * sms, 256, 0, s>>>(d); break;
+    case 2: k_flux_split<0, 3><<<3 * sms, 256, 0, s>>>(d); break;
+    case 3: k_flux_split<1, 3><<<3 * sms, 256, 0, s>>>(d); break;
+    case 4: k_flux_split<0, 4><<<4 * sms, 256, 0, s>>>(d); break;
+    default: k_flux_split<1, 4><<<4 * sms, 256, 0, s>>>(d); break;
     }
     return int(cudaGetLastError());
 }

@@ -40,6 +40,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--grid", type=int, default=94)
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--only", nargs="*", default=[], help="variant names to run (plus soa, the reference)")
     args = ap.parse_args()
     from paper_1403_7209_b200 import apps, renumber_mesh
     mesh = apps.gen_hex_mesh(args.grid, seed=0)
@@ -91,6 +92,7 @@ def main():
     lib.exp_flux_lock.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_reg.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_h.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_split.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_lrec.argtypes = ([C.c_int] + [C.c_void_p] * 8 + [C.c_int64, C.c_void_p, C.c_void_p,
                                   C.c_int64, C.c_int, C.c_void_p])
     vals = {k: h[k].fetch() for k in ("q", "x", "lim", "grad", "aux", "res", "w")}
@@ -110,7 +112,11 @@ def main():
                              (0, 7, "soa_reg2"), (1, 7, "aosoa_reg2"),
                              (0, 10, "soa_pf"), (1, 11, "aosoa_pf"), (0, 12, "soa_hint"), (1, 13, "aosoa_hint"),
                              (0, 14, "soa_hint_pf"), (1, 15, "aosoa_hint_pf"), (0, 16, "soa_nbr_noalloc"),
-                             (1, 17, "aosoa_nbr_noalloc")):
+                             (1, 17, "aosoa_nbr_noalloc"), (0, 20, "soa_split2"), (1, 21, "aosoa_split2"),
+                             (0, 22, "soa_split3"), (1, 23, "aosoa_split3"), (0, 24, "soa_split4"),
+                             (1, 25, "aosoa_split4")):
+        if args.only and name not in args.only and name != "soa":
+            continue
         def put(k):
             v = vals[k]
             if k in ("x", "w"):
@@ -129,7 +135,9 @@ def main():
                       T["res"].data_ptr(), slots.data_ptr(), ints["off1"].data_ptr(),
                       ints["elem1"].data_ptr(), ints["tl1"].data_ptr(), ints["rec"].data_ptr(),
                       ints["slotpos"].data_ptr(), int(tl1.size), n)
-            if lanes >= 10:
+            if lanes >= 20:
+                rc = lib.exp_flux_split(lanes - 20, *common[1:], sms, stream)
+            elif lanes >= 10:
                 rc = lib.exp_flux_h(lanes - 10, *common[1:], sms * 2, stream)
             elif lanes >= 6:
                 rc = lib.exp_flux_reg(lay + 2 * (lanes - 5), *common[1:], sms, stream)

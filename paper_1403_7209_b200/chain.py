@@ -122,15 +122,17 @@ def chain_pair(A: Loop, B: Loop) -> Loop | None:
     return Loop(f"{A.name}+{B.name}", A.iter_set, slots, kernel)
 
 
-def chain_program(program: list[Loop], mesh: Mesh) -> list[Loop]:
+def chain_program(program: list[Loop], mesh: Mesh, pinned=frozenset()) -> list[Loop]:
     """``program`` with every legal adjacent chained pair replaced by its
     fused loop (left to right; fused loops are cached on the mesh so a
-    program's compiled form stays valid across calls)."""
+    program's compiled form stays valid across calls).  Loops named in
+    ``pinned`` — those a per-loop table (block size, INC schedule) names —
+    are never fused, so the table entry applies to the loop as written."""
     cache = mesh.__dict__.setdefault("_ml_chains", OrderedDict())
     out: list[Loop] = []
     i = 0
     while i < len(program):
-        if i + 1 < len(program):
+        if i + 1 < len(program) and program[i].name not in pinned and program[i + 1].name not in pinned:
             A, B = program[i], program[i + 1]
             key = (id(A), id(B))
             hit = cache.get(key)

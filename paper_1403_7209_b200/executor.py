@@ -317,7 +317,9 @@ class CompiledProgram:
                  iter_counts: dict | None = None, rlim: dict | None = None):
         self.loops = list(program)
         # loops as launched: registered adjacent pairs fused (chain.py)
-        self.run_loops = chain_program(self.loops, mesh) if config.chain_loops else self.loops
+        # a loop a per-loop table names keeps its own entry: it is not fused
+        pinned = frozenset(config.block_size_table or ()) | frozenset(config.inc_schedule_table or ())
+        self.run_loops = chain_program(self.loops, mesh, pinned) if config.chain_loops else self.loops
         self.mesh = mesh
         self.version = mesh.version
         globs: list[Global] = []

@@ -1185,7 +1185,8 @@ def setup_distributed(program, mesh, config, transport=None, executor_factory=No
     mesh.freeze()
     if config.chain_loops:             # fused pairs exchange the union of their halos
         from .chain import chain_program
-        program = chain_program(list(program), mesh)
+        pinned = frozenset(config.block_size_table or ()) | frozenset(config.inc_schedule_table or ())
+        program = chain_program(list(program), mesh, pinned)
     if layout is None:
         layout = build_layout(mesh, program, config)
     elif layout.nranks != world:

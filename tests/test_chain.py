@@ -158,3 +158,16 @@ def test_chain_needs_the_fused_functor_for_the_loops_type():
     B = Loop("vflux", vflux.iter_set, [as_int(a) for a in vflux.args], vflux.kernel)
     assert chain_pair(iflux, vflux) is not None
     assert chain_pair(A, B) is None
+
+
+def test_loops_named_by_a_per_loop_table_are_not_fused():
+    """a block_size_table / inc_schedule_table entry for a member
+    loop must apply to that loop, so the pair is left unfused."""
+    from paper_1403_7209_b200.chain import chain_program
+    mesh = apps.gen_hex_mesh(4, seed=1)
+    prog, _h = apps.build_hydra_proxy(mesh, steps=1, seed=1)
+    names = [l.name for l in chain_program(prog, mesh)]
+    assert "iflux+vflux" in names
+    for pinned in ({"vflux"}, {"iflux"}):
+        names = [l.name for l in chain_program(prog, mesh, frozenset(pinned))]
+        assert "iflux" in names and "vflux" in names and "iflux+vflux" not in names

@@ -52,11 +52,15 @@ typedef struct ml_arg {
     const int32_t *map;    /* device map table, column-major int32 [arity][from]  */
     int64_t map_from;      /* from-set size of the map (column stride)            */
     int64_t set_size;      /* size of the dat's set                               */
-    int64_t pitch;         /* SOA component stride in elements of the device copy
-                              (>= set_size; the library pads it to 32 elements so
-                              every component row is 256-byte aligned); 0 means
-                              set_size                                            */
+    int64_t pitch;         /* plain SOA (seg_shift 0): component stride in elements
+                              of the device copy (>= set_size; 0 means set_size) */
+    int32_t seg_shift;     /* segmented SOA: the device copy stores segments of
+                              2^seg_shift elements, each segment's components one
+                              after another: (e, c) at (e >> s) * 2^s * dim +
+                              c * 2^s + (e & (2^s - 1)).  The library's own copies
+                              of SOA dats use s = 12 (ML_SEG_SHIFT); 0: plain  */
 } ml_arg_t;
+#define ML_SEG_SHIFT 12
 
 /* Device copy of an execution plan (plan.py:30-45).  `color_offsets` is a
  * HOST array; the rest are device arrays produced by ml_plan_* below. */
@@ -162,8 +166,7 @@ int ml_upload(void *dst, const void *src, uint64_t bytes);    /* H2D, stream-ord
 int ml_download(void *dst, const void *src, uint64_t bytes);  /* D2H, synchronous    */
 int ml_memset(void *dst, int value, uint64_t bytes);
 /* Pitched copies (rows of `width` bytes, `height` rows; host and device row
- * pitches in bytes): a SOA dat's host payload [dim][set_size] to/from its
- * device copy [dim][pitch].  Same stream behaviour as ml_upload/ml_download. */
+ * pitches in bytes).  Same stream behaviour as ml_upload/ml_download. */
 int ml_upload2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
                 uint64_t height);
 int ml_download2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
@@ -177,6 +180,13 @@ int ml_copy_h2d(void *dst, const void *src, uint64_t bytes);
 int ml_copy_d2h(void *dst, const void *src, uint64_t bytes);
 int ml_copy_h2d_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
                    uint64_t height);
+/* A SOA dat's host payload [dim][n] (itemsize bytes per value) to/from its
+ * segmented device copy (see ml_arg_t.seg_shift): one 2-D copy of the full
+ * segments plus one tail copy per component.  `to_device` 1: H2D, 0: D2H;
+ * `stream` ML_STREAM_COMPUTE (D2H waits for completion, like ml_download) or
+ * ML_STREAM_H2D / ML_STREAM_D2H (asynchronous, streamed residency). */
+int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_t itemsize, int32_t seg_shift,
+                int32_t to_device, int32_t stream);
 int ml_copy_d2h_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
                    uint64_t height);
 int ml_order(int32_t from, int32_t to);
@@ -275,7 +285,8 @@ int ml_program_free(ml_program_t *p);
  *      163-173 (_gather_rows/_scatter_rows), 652-660 (rank-ordered reduce) ---- */
 /* Gather rows `idx` (device int32, local element ids) of an 8-byte-element dat
  * with strides (elem_stride, comp_stride) into a contiguous [nidx][dim] buffer,
- * and the inverse scatter.  Stream-ordered on the compute stream. */
+ * and the inverse scatter.  elem_stride 0 means a segmented SOA copy with
+ * segments of comp_stride elements.  Stream-ordered on the compute stream. */
 int ml_pack_rows(void *dst, const void *dat, const int32_t *idx, int64_t nidx, int32_t dim,
                  int64_t elem_stride, int64_t comp_stride);
 int ml_unpack_rows(void *dat, const void *src, const int32_t *idx, int64_t nidx, int32_t dim,

@@ -22,6 +22,7 @@ ML_DIRECT, ML_INDIRECT, ML_GLOBAL = 0, 1, 2
 MODE_CODE = {"READ": 0, "WRITE": 1, "RW": 2, "INC": 3, "MIN": 4, "MAX": 5}
 ML_F64, ML_I64 = 0, 1
 ML_AOS, ML_SOA = 0, 1
+ML_SEG_SHIFT = 12          # segmented SOA device copies: 4096-element segments
 ML_STREAM_COMPUTE, ML_STREAM_H2D, ML_STREAM_D2H = 0, 1, 2
 
 #: every symbol include/meshloop_b200.h declares (checked by tests/test_abi.py)
@@ -29,7 +30,7 @@ EXPORTED = [
     "ml_last_error", "ml_version", "ml_init", "ml_device_info", "ml_synchronize",
     "ml_alloc", "ml_free", "ml_host_alloc", "ml_host_free", "ml_upload", "ml_download",
     "ml_memset", "ml_upload2d", "ml_download2d", "ml_map_upload", "ml_copy_h2d", "ml_copy_d2h",
-    "ml_copy_h2d_2d", "ml_copy_d2h_2d", "ml_order", "ml_sync_all",
+    "ml_copy_h2d_2d", "ml_copy_d2h_2d", "ml_seg_copy", "ml_order", "ml_sync_all",
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
     "ml_gather_build", "ml_gather_export", "ml_gather_free",
     "ml_co_occurrence", "ml_cm_order",
@@ -49,7 +50,7 @@ class MlArg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("mode", C.c_int32), ("dim", C.c_int32),
                 ("dtype", C.c_int32), ("layout", C.c_int32), ("slot", C.c_int32),
                 ("data", C.c_void_p), ("map", C.c_void_p), ("map_from", C.c_int64),
-                ("set_size", C.c_int64), ("pitch", C.c_int64)]
+                ("set_size", C.c_int64), ("pitch", C.c_int64), ("seg_shift", C.c_int32)]
 
 
 class MlPlanDev(C.Structure):
@@ -110,6 +111,7 @@ _SIGNATURES = {
     "ml_download2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ml_copy_h2d_2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ml_copy_d2h_2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "ml_seg_copy": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "ml_map_upload": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
     "ml_copy_h2d": (C.c_int, [_P, _P, C.c_uint64]),
     "ml_copy_d2h": (C.c_int, [_P, _P, C.c_uint64]),

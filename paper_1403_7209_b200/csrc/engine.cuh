@@ -18,10 +18,10 @@
 // each argument's strides at run time (element stride `se`, component stride
 // `sc`: any AOS/SOA mix).  LP = 1 is the reference's default auto-SOA policy
 // (core.py:403-404, threshold 4) fixed at compile time: a dat of dim <= 4 is
-// AOS (se = dim, sc = 1: component offsets are immediates), wider dats SOA
-// (se = 1, sc = the device pitch, a uniform value).  The runtime picks LP = 1
-// when the loop's dats follow that policy — the common case — which removes
-// the 64-bit stride arithmetic from every gathered load.
+// AOS (base e * dim, component offsets are immediates), wider dats SOA in the
+// device's segmented form (component offsets c * SEG, immediates too).  The
+// runtime picks LP = 1 when the loop's dats follow that policy — the common
+// case — which removes the 64-bit stride arithmetic from every gathered load.
 //
 // Kernels (selected by runtime.cu enqueue_loop)
 //   k_direct   — loops without indirect writes: persistent grid; with LP = 1
@@ -59,6 +59,16 @@ enum : int { KD = 0, KI = 1, KG = 2 };                        // direct / indire
 enum : int { MR = 0, MW = 1, MRW = 2, MINC = 3, MMIN = 4, MMAX = 5 };
 constexpr int MAX_ARGS = 16;
 constexpr int AUTO_SOA_DIM = 4;    // reference Mesh(auto_soa_threshold=4): dim > 4 is SOA
+// Device SOA copies are *segmented*: the set is cut into segments of SEG
+// elements and each segment stores its components one after another,
+// element (e, c) at (e >> SEG_SHIFT) * SEG * dim + c * SEG + (e & (SEG - 1)).
+// Inside a segment a component is one contiguous run, so a warp's access is
+// as coalesced as plain SOA; but the offset of component c from an element's
+// base is the compile-time c * SEG * 8 bytes — a load immediate — instead of
+// c * set_size (a 64-bit multiply-add per load).  SEG * 8 = 32 KB rows also
+// keep host<->device copies DMA-efficient (one 2-D copy per component).
+constexpr int SEG_SHIFT = 12;
+constexpr int64_t SEG = int64_t(1) << SEG_SHIFT;
 
 // Programmatic dependent launch: the hot kernels are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs can
@@ -105,7 +115,15 @@ struct ArgRt {
     void *data;
     const int32_t *map;   // map column (already offset by slot*from)
     int64_t se, sc;       // element stride, component stride (in elements)
+    int32_t sh;           // segmented SOA: log2 of the segment length (0: linear)
+    int64_t sb;           // segmented SOA: elements per segment (segment length * dim)
 };
+
+// offset (in elements) of element e's first component
+__host__ __device__ __forceinline__ int64_t elem_base(const ArgRt &r, int64_t e) {
+    if (r.sh) return (e >> r.sh) * r.sb + (e & ((int64_t(1) << r.sh) - 1));
+    return e * r.se;
+}
 
 struct Consts {
     double f[4];
@@ -182,21 +200,23 @@ struct RefA {
     __device__ __forceinline__ T &operator[](int c) const { return p[c]; }
 };
 
-// layout class of argument A under policy LP: 0 runtime strides, 1 AOS (se =
-// dim, sc = 1), 2 SOA (se = 1, sc = runtime pitch)
+// layout class of argument A under policy LP: 0 runtime strides, 1 AOS (base
+// e * dim, component stride 1), 2 segmented SOA (SEG_SHIFT, component stride SEG)
 template <class A, int LP>
 __host__ __device__ constexpr int lay_of() {
     return (LP == 0 || A::kind == KG) ? 0 : (A::dim <= AUTO_SOA_DIM ? 1 : 2);
 }
+// element base offset and component stride under layout class L
 template <class A, int L>
-__device__ __forceinline__ int64_t se_of(const ArgRt &r) {
-    if constexpr (L == 1) return A::dim;
-    else if constexpr (L == 2) return 1;
-    else return r.se;
+__device__ __forceinline__ int64_t base_of(const ArgRt &r, int64_t e) {
+    if constexpr (L == 1) return e * A::dim;
+    else if constexpr (L == 2) return (e >> SEG_SHIFT) * (SEG * A::dim) + (e & (SEG - 1));
+    else return elem_base(r, e);
 }
 template <class A, int L>
 __device__ __forceinline__ int64_t sc_of(const ArgRt &r) {
     if constexpr (L == 1) return 1;
+    else if constexpr (L == 2) return SEG;
     else return r.sc;
 }
 
@@ -268,7 +288,7 @@ struct Slot {
         }
     }
     __device__ __forceinline__ void bind(const ArgRt &r, int64_t t) {
-        ptr = static_cast<T *>(r.data) + t * se_of<A, L>(r);
+        ptr = static_cast<T *>(r.data) + base_of<A, L>(r, t);
         sc = sc_of<A, L>(r);
         if constexpr (staged) {
 #pragma unroll
@@ -533,7 +553,7 @@ struct DirRows {
             const T *b = static_cast<const T *>(r.data);
             if (!two) {
 #pragma unroll
-                for (int c = 0; c < A::dim; ++c) v[0][c] = b[e0 * se_of<A, L>(r) + c * sc_of<A, L>(r)];
+                for (int c = 0; c < A::dim; ++c) v[0][c] = b[base_of<A, L>(r, e0) + c * sc_of<A, L>(r)];
                 return;
             }
             if constexpr (L == 1) {             // AOS: the pair's rows are 2*dim consecutive values
@@ -545,9 +565,10 @@ struct DirRows {
                     v[0][c] = f[c];
                     v[1][c] = f[A::dim + c];
                 }
-            } else {                            // SOA: one pair per component
+            } else {                            // segmented SOA: one pair per component
+                const T *bb = b + base_of<A, L>(r, e0);
 #pragma unroll
-                for (int c = 0; c < A::dim; ++c) ld2(b + c * r.sc + e0, v[0][c], v[1][c]);
+                for (int c = 0; c < A::dim; ++c) ld2(bb + c * SEG, v[0][c], v[1][c]);
             }
         }
     }
@@ -556,7 +577,7 @@ struct DirRows {
             T *b = static_cast<T *>(r.data);
             if (!two) {
 #pragma unroll
-                for (int c = 0; c < A::dim; ++c) b[e0 * se_of<A, L>(r) + c * sc_of<A, L>(r)] = v[0][c];
+                for (int c = 0; c < A::dim; ++c) b[base_of<A, L>(r, e0) + c * sc_of<A, L>(r)] = v[0][c];
                 return;
             }
             if constexpr (L == 1) {
@@ -569,8 +590,9 @@ struct DirRows {
 #pragma unroll
                 for (int k = 0; k < A::dim; ++k) st2(b + e0 * A::dim + 2 * k, f[2 * k], f[2 * k + 1]);
             } else {
+                T *bb = b + base_of<A, L>(r, e0);
 #pragma unroll
-                for (int c = 0; c < A::dim; ++c) st2(b + c * r.sc + e0, v[0][c], v[1][c]);
+                for (int c = 0; c < A::dim; ++c) st2(bb + c * SEG, v[0][c], v[1][c]);
             }
         }
     }
@@ -721,12 +743,12 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
     typename E::Slots s;
     E::init_globals(s, p, idx);
     const ArgRt &rg = p.a[G];
-    const int64_t gse = se_of<AG, LG>(rg), gsc = sc_of<AG, LG>(rg);
+    const int64_t gsc = sc_of<AG, LG>(rg);
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
          t - threadIdx.x < p.g_ntargets; t += int64_t(gridDim.x) * blockDim.x) {
         if (t >= p.g_ntargets) continue;
         const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
-        TG *dst = static_cast<TG *>(rg.data) + tg * gse;
+        TG *dst = static_cast<TG *>(rg.data) + base_of<AG, LG>(rg, tg);
         const int32_t seg = (MM == MINC && p.g_seg) ? __ldg(p.g_seg + t) : -1;
         TG run[DG];
 #pragma unroll
@@ -769,7 +791,7 @@ __global__ void __launch_bounds__(256) k_gather_hubs(const __grid_constant__ Lau
     const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (h >= p.g_nhub) return;
     const ArgRt &rg = p.a[ga];
-    T *dst = static_cast<T *>(rg.data) + int64_t(__ldg(p.g_hub_tl + h)) * rg.se;
+    T *dst = static_cast<T *>(rg.data) + elem_base(rg, int64_t(__ldg(p.g_hub_tl + h)));
     const T *part = static_cast<const T *>(p.g_part);
     T run[DG];
 #pragma unroll
@@ -814,12 +836,12 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
     E::init_globals(s, p, idx);
     const PFoldParams &pf = p.pf;
     const ArgRt &rg = p.a[G];
-    const int64_t gse = se_of<AG, LG>(rg), gsc = sc_of<AG, LG>(rg);
+    const int64_t gsc = sc_of<AG, LG>(rg);
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t - threadIdx.x < pf.n1;
          t += int64_t(gridDim.x) * blockDim.x) {
         if (t >= pf.n1) continue;
         const int64_t tg = pf.tl1 ? int64_t(__ldg(pf.tl1 + t)) : t;
-        TG *dst = static_cast<TG *>(rg.data) + tg * gse;
+        TG *dst = static_cast<TG *>(rg.data) + base_of<AG, LG>(rg, tg);
         const int32_t seg = pf.seg1 ? __ldg(pf.seg1 + t) : -1;
         TG run[DG];
 #pragma unroll
@@ -874,7 +896,7 @@ __global__ void __launch_bounds__(256) k_pfold_rest_w(const __grid_constant__ La
             k0 = __ldg(pf.off2 + t);
             k1 = __ldg(pf.off2 + t + 1);
             const int64_t tg = pf.tl2 ? int64_t(__ldg(pf.tl2 + t)) : t;
-            dst = static_cast<T *>(rg.data) + tg * rg.se;
+            dst = static_cast<T *>(rg.data) + elem_base(rg, tg);
             seg = pf.seg2 ? __ldg(pf.seg2 + t) : -1;
 #pragma unroll
             for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : T(0);
@@ -916,7 +938,7 @@ __global__ void __launch_bounds__(256) k_fold_parts(const __grid_constant__ Laun
     const int64_t h = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (h >= nhub) return;
     const ArgRt &rg = p.a[ga];
-    T *dst = static_cast<T *>(rg.data) + int64_t(__ldg(hub_tl + h)) * rg.se;
+    T *dst = static_cast<T *>(rg.data) + elem_base(rg, int64_t(__ldg(hub_tl + h)));
     const T *part = static_cast<const T *>(parts);
     T run[DG];
 #pragma unroll

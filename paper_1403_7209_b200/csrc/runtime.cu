@@ -110,9 +110,11 @@ static int validate(const ml_loop_t *L, const FunctorEntry &f) {
             ML_FAIL(ML_EINVAL, "loop '%s' arg %d: null device pointer", nm, i);
         if (a.kind == ML_INDIRECT && !a.map && L->n > 0)
             ML_FAIL(ML_EINVAL, "loop '%s' arg %d: indirect arg without device map", nm, i);
-        if (a.kind != ML_GLOBAL && a.layout == ML_SOA && a.pitch != 0 && a.pitch < a.set_size)
+        if (a.kind != ML_GLOBAL && a.layout == ML_SOA && a.seg_shift == 0 && a.pitch != 0 && a.pitch < a.set_size)
             ML_FAIL(ML_EINVAL, "loop '%s' arg %d: SOA pitch %lld below the set size %lld", nm, i,
                     (long long)a.pitch, (long long)a.set_size);
+        if (a.kind != ML_GLOBAL && (a.seg_shift < 0 || a.seg_shift > 30))
+            ML_FAIL(ML_EINVAL, "loop '%s' arg %d: bad segment shift %d", nm, i, a.seg_shift);
     }
     return ML_OK;
 }
@@ -126,8 +128,7 @@ static int layout_policy(const ml_loop_t *L) {
         const ml_arg_t &a = L->args[i];
         if (a.kind == ML_GLOBAL) continue;
         if (a.dim > AUTO_SOA_DIM) {
-            const int64_t pitch = a.pitch ? a.pitch : a.set_size;
-            if (a.layout != ML_SOA || (pitch & 1)) return 0;
+            if (a.layout != ML_SOA || a.seg_shift != SEG_SHIFT) return 0;
         } else if (a.dim > 1 && a.layout != ML_AOS) {
             return 0;
         }
@@ -204,9 +205,14 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
                 p.part[i] = scratch;
                 scratch += uint64_t(pstride) * a.dim * 8 + 256;
             }
-        } else if (a.layout == ML_AOS) {
+        } else if (a.layout == ML_AOS || a.dim == 1) {
             r.se = a.dim;
             r.sc = 1;
+        } else if (a.seg_shift > 0) {             // segmented SOA
+            r.se = 0;
+            r.sh = a.seg_shift;
+            r.sc = int64_t(1) << a.seg_shift;
+            r.sb = r.sc * a.dim;
         } else {
             r.se = 1;
             r.sc = a.pitch ? a.pitch : a.set_size;
@@ -473,6 +479,35 @@ extern "C" int ml_copy_d2h_2d(void *dst, uint64_t dpitch, const void *src, uint6
     if (rc) return rc;
     if (width && height)
         ML_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, g_dev.copy[1]));
+    return ML_OK;
+}
+static cudaStream_t stream_of(int32_t which);
+extern "C" int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_t itemsize, int32_t seg_shift,
+                           int32_t to_device, int32_t stream) {
+    int rc = ensure_init();
+    if (rc) return rc;
+    if (n < 0 || dim < 1 || itemsize < 1 || seg_shift < 1 || seg_shift > 30)
+        ML_FAIL(ML_EINVAL, "ml_seg_copy: bad arguments");
+    if (n == 0) return ML_OK;
+    cudaStream_t s = stream_of(stream);
+    const uint64_t S = uint64_t(1) << seg_shift, isz = uint64_t(itemsize);
+    const uint64_t nfull = uint64_t(n) >> seg_shift, rem = uint64_t(n) - nfull * S;
+    char *d = static_cast<char *>(dev), *h = static_cast<char *>(host);
+    for (uint64_t c = 0; c < uint64_t(dim); ++c) {
+        char *dc = d + c * S * isz, *hc = h + c * uint64_t(n) * isz;
+        if (nfull) {
+            if (to_device)
+                ML_CUDA(cudaMemcpy2DAsync(dc, S * dim * isz, hc, S * isz, S * isz, nfull, cudaMemcpyHostToDevice, s));
+            else
+                ML_CUDA(cudaMemcpy2DAsync(hc, S * isz, dc, S * dim * isz, S * isz, nfull, cudaMemcpyDeviceToHost, s));
+        }
+        if (rem) {
+            char *dt = dc + nfull * S * dim * isz, *ht = hc + nfull * S * isz;
+            if (to_device) ML_CUDA(cudaMemcpyAsync(dt, ht, rem * isz, cudaMemcpyHostToDevice, s));
+            else ML_CUDA(cudaMemcpyAsync(ht, dt, rem * isz, cudaMemcpyDeviceToHost, s));
+        }
+    }
+    if (!to_device && stream == ML_STREAM_COMPUTE) ML_CUDA(cudaStreamSynchronize(s));
     return ML_OK;
 }
 static cudaStream_t stream_of(int32_t which) {
@@ -863,12 +898,18 @@ extern "C" int ml_program_free(ml_program_t *p) {
 
 // ---- ABI: multi-GPU helpers --------------------------------------------------------------------
 namespace ml {
+// element (e, c) of a dat given the ABI's (elem_stride, comp_stride):
+// elem_stride 0 means segmented SOA with segments of comp_stride elements
+__device__ __forceinline__ int64_t row_index(int64_t e, int c, int dim, int64_t se, int64_t sc) {
+    if (se == 0) return (e / sc) * sc * dim + c * sc + (e % sc);
+    return e * se + c * sc;
+}
 __global__ void k_pack_rows(double *dst, const double *dat, const int32_t *idx, int64_t nidx, int dim,
                             int64_t se, int64_t sc) {
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nidx * dim;
          k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = k / dim, c = k % dim;
-        dst[k] = dat[int64_t(idx[r]) * se + c * sc];
+        dst[k] = dat[row_index(idx[r], int(c), dim, se, sc)];
     }
 }
 __global__ void k_unpack_rows(double *dat, const double *src, const int32_t *idx, int64_t nidx, int dim,
@@ -876,7 +917,7 @@ __global__ void k_unpack_rows(double *dat, const double *src, const int32_t *idx
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nidx * dim;
          k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = k / dim, c = k % dim;
-        dat[int64_t(idx[r]) * se + c * sc] = src[k];
+        dat[row_index(idx[r], int(c), dim, se, sc)] = src[k];
     }
 }
 // NVLink halo exchange: pack the export rows straight into the peer's import
@@ -887,7 +928,7 @@ __global__ void k_put_rows(double *rdst, const double *dat, const int32_t *idx, 
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nidx * dim;
          k += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = k / dim, c = k % dim;
-        rdst[k] = dat[int64_t(idx[r]) * se + c * sc];
+        rdst[k] = dat[row_index(idx[r], int(c), dim, se, sc)];
     }
     __threadfence_system();
     __syncthreads();

@@ -2,11 +2,11 @@
 
 Layout in HBM:
 
-* a dat is one float64/int64 buffer in the dat's own layout — AOS
-  ``e*dim+c`` as on the host, SOA ``c*pitch+e`` with the component rows
-  padded to a 256-byte multiple (``device_pitch``; pitched 2-D copies to and
-  from the host's ``c*size+e``) — uploaded on first use and kept resident
-  across ``run_program`` calls;
+* a dat is one float64/int64 buffer, uploaded on first use and kept
+  resident across ``run_program`` calls: AOS ``e*dim+c`` as on the host; SOA
+  (dim > 1) *segmented* — 4096-element segments each storing its components
+  one after another (``SEG_SHIFT``), copied to/from the host's ``c*size+e``
+  with one 2-D transfer of 32 KB rows plus a tail per component;
 * a map is stored int32 and column-major (``[arity][from_size]``), so the
   index reads of one map column by consecutive elements are coalesced and
   cost 4 B per element instead of the host table's 8 B;
@@ -24,31 +24,40 @@ import numpy as np
 from . import _native as N
 from .core import AOS, Dat, ExecError, Map
 
-__all__ = ["DatMirror", "dat_mirror", "device_pitch", "map_mirror", "plan_mirror", "pin_mesh",
-           "gather_mirror", "pfold_mirror", "gather_eligible", "fold_eligible", "PITCH_ALIGN"]
+__all__ = ["DatMirror", "dat_mirror", "segmented", "device_elems", "map_mirror", "plan_mirror", "pin_mesh",
+           "gather_mirror", "pfold_mirror", "gather_eligible", "fold_eligible", "SEG_SHIFT"]
 
 
-#: SOA component rows of a device copy are padded to a multiple of this many
-#: elements (256 bytes of float64/int64): every component row starts 256-byte
-#: aligned, so the 16-byte direct accesses and full-sector gathers stay aligned
-PITCH_ALIGN = 32
+#: SOA dats of dim > 1 are stored *segmented* on the device: segments of
+#: 2**SEG_SHIFT elements, each holding its components one after another —
+#: (e, c) at (e >> s) * 2**s * dim + c * 2**s + (e & (2**s - 1)).  Inside a
+#: segment a component is a contiguous run (coalesced like plain SOA); the
+#: offset of component c from an element's base is the compile-time
+#: c * 2**s * 8 bytes, a load immediate in the kernels (engine.cuh).
+SEG_SHIFT = N.ML_SEG_SHIFT
 
 
-def device_pitch(dat: Dat) -> int:
-    """Component stride (elements) of ``dat``'s device copy: the set size for
-    AOS and single-component dats, the set size rounded up to PITCH_ALIGN for
-    SOA dats of dim > 1."""
+def segmented(dat: Dat) -> bool:
+    """Whether ``dat``'s device copy is segmented SOA."""
+    return dat.layout is not AOS and dat.dim > 1
+
+
+def device_elems(dat: Dat) -> int:
+    """Elements of ``dat``'s device copy (segmented copies round the set up to
+    whole segments)."""
     n = dat.set.size
-    if dat.layout is AOS or dat.dim == 1:
-        return n
-    return -(-n // PITCH_ALIGN) * PITCH_ALIGN
+    if not segmented(dat):
+        return n * dat.dim
+    seg = 1 << SEG_SHIFT
+    return -(-n // seg) * seg * dat.dim
 
 
 class DatMirror:
-    """Device copy of one dat payload: AOS rows as on the host; SOA component
-    rows at ``pitch`` elements (host pitch: the set size)."""
+    """Device copy of one dat payload: AOS rows (and dim-1 dats) as on the
+    host; SOA dats segmented (``SEG_SHIFT``), copied with one 2-D transfer of
+    the full segments plus one tail copy per component (``ml_seg_copy``)."""
 
-    __slots__ = ("buf", "layout", "nbytes", "host_newer", "device_newer", "pitch", "rows", "row_bytes")
+    __slots__ = ("buf", "layout", "nbytes", "host_newer", "device_newer", "seg", "n", "dim", "isz")
 
     def __init__(self):
         self.buf = None
@@ -56,29 +65,39 @@ class DatMirror:
         self.nbytes = -1
         self.host_newer = True
         self.device_newer = False
-        self.pitch = 0
-        self.rows = 1            # > 1: pitched SOA copy of `rows` component rows
-        self.row_bytes = 0       # host bytes of one component row
+        self.seg = False
+        self.n = self.dim = self.isz = 0
 
     @property
     def ptr(self) -> int:
         return self.buf.ptr if self.buf is not None else 0
 
     @property
-    def padded(self) -> bool:
-        return self.rows > 1
+    def pitch(self) -> int:
+        """ABI ``pitch`` of the copy (plain layouts: the set size)."""
+        return self.n
+
+    @property
+    def seg_shift(self) -> int:
+        return SEG_SHIFT if self.seg else 0
 
     def strides(self, dat: Dat) -> tuple[int, int]:
-        """(element stride, component stride) of the device copy, in elements."""
-        return (dat.dim, 1) if dat.layout is AOS else (1, self.pitch)
+        """(element stride, component stride) in the ABI's row-kernel
+        convention (ml_pack_rows): element stride 0 = segmented SOA with
+        segments of the component stride."""
+        if self.seg:
+            return 0, 1 << SEG_SHIFT
+        return (dat.dim, 1) if dat.layout is AOS else (1, self.n)
+
+    def _seg_copy(self, host: np.ndarray, to_device: bool, stream: int) -> None:
+        N.check(N.lib().ml_seg_copy(self.buf.ptr, N.ptr(host), self.n, self.dim, self.isz, SEG_SHIFT,
+                                    int(to_device), stream), "ml_seg_copy")
 
     def upload(self, host: np.ndarray) -> None:
         if self.buf is None or not host.nbytes:
             return
-        if self.padded:
-            isz = host.dtype.itemsize
-            N.check(N.lib().ml_upload2d(self.buf.ptr, self.pitch * isz, N.ptr(host), self.row_bytes,
-                                        self.row_bytes, self.rows), "ml_upload2d")
+        if self.seg:
+            self._seg_copy(host, True, N.ML_STREAM_COMPUTE)
         else:
             self.buf.upload(host)
 
@@ -86,10 +105,8 @@ class DatMirror:
         if self.buf is not None and host.nbytes:
             if not host.flags.c_contiguous:
                 raise ExecError("dat payload must be contiguous to receive device data")
-            if self.padded:
-                isz = host.dtype.itemsize
-                N.check(N.lib().ml_download2d(N.ptr(host), self.row_bytes, self.buf.ptr, self.pitch * isz,
-                                              self.row_bytes, self.rows), "ml_download2d")
+            if self.seg:
+                self._seg_copy(host, False, N.ML_STREAM_COMPUTE)
             else:
                 self.buf.download(host)
         self.device_newer = False
@@ -98,25 +115,19 @@ class DatMirror:
         """Asynchronous upload on the H2D copy stream (streamed residency)."""
         if self.buf is None or not host.nbytes:
             return
-        L = N.lib()
-        if self.padded:
-            isz = host.dtype.itemsize
-            N.check(L.ml_copy_h2d_2d(self.buf.ptr, self.pitch * isz, N.ptr(host), self.row_bytes,
-                                     self.row_bytes, self.rows), "ml_copy_h2d_2d")
+        if self.seg:
+            self._seg_copy(host, True, N.ML_STREAM_H2D)
         else:
-            N.check(L.ml_copy_h2d(self.buf.ptr, N.ptr(host), host.nbytes), "ml_copy_h2d")
+            N.check(N.lib().ml_copy_h2d(self.buf.ptr, N.ptr(host), host.nbytes), "ml_copy_h2d")
 
     def copy_d2h(self, host: np.ndarray) -> None:
         """Asynchronous download on the D2H copy stream (streamed residency)."""
         if self.buf is None or not host.nbytes:
             return
-        L = N.lib()
-        if self.padded:
-            isz = host.dtype.itemsize
-            N.check(L.ml_copy_d2h_2d(N.ptr(host), self.row_bytes, self.buf.ptr, self.pitch * isz,
-                                     self.row_bytes, self.rows), "ml_copy_d2h_2d")
+        if self.seg:
+            self._seg_copy(host, False, N.ML_STREAM_D2H)
         else:
-            N.check(L.ml_copy_d2h(N.ptr(host), self.buf.ptr, host.nbytes), "ml_copy_d2h")
+            N.check(N.lib().ml_copy_d2h(N.ptr(host), self.buf.ptr, host.nbytes), "ml_copy_d2h")
 
 
 def dat_mirror(dat: Dat, force_upload: bool = False, upload: bool = True) -> DatMirror:
@@ -126,18 +137,15 @@ def dat_mirror(dat: Dat, force_upload: bool = False, upload: bool = True) -> Dat
     if m is None:
         m = dat._dev = DatMirror()
     host = dat._host
-    pitch = device_pitch(dat)
-    dev_bytes = dat.dim * pitch * host.dtype.itemsize if host.nbytes else 0
-    if m.buf is None or m.nbytes != dev_bytes or m.pitch != pitch:
+    seg = segmented(dat)
+    dev_bytes = device_elems(dat) * host.dtype.itemsize if host.nbytes else 0
+    if m.buf is None or m.nbytes != dev_bytes or m.seg != seg:
         if m.device_newer:
             raise ExecError(f"dat {dat.name!r}: payload resized while device data is newer")
         m.buf = N.DeviceBuffer(dev_bytes) if dev_bytes else None
         m.nbytes = dev_bytes
-        m.pitch = pitch
         m.host_newer = True
-    padded = pitch != dat.set.size
-    m.rows = dat.dim if padded else 1
-    m.row_bytes = dat.set.size * host.dtype.itemsize if padded else host.nbytes
+    m.seg, m.n, m.dim, m.isz = seg, dat.set.size, dat.dim, host.dtype.itemsize
     if m.layout is not dat.layout:
         m.layout = dat.layout
         m.host_newer = True

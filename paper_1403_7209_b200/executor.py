@@ -227,6 +227,7 @@ class _LoopEntry:
             m = dat_mirror(d)
             r.data = m.ptr or None
             r.pitch = m.pitch
+            r.seg_shift = m.seg_shift
             if a.kind == "indirect":
                 r.slot = a.slot
                 r.map = map_mirror(a.map) or None

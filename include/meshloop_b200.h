@@ -55,12 +55,23 @@ typedef struct ml_arg {
     int64_t pitch;         /* plain SOA (seg_shift 0): component stride in elements
                               of the device copy (>= set_size; 0 means set_size) */
     int32_t seg_shift;     /* segmented SOA: the device copy stores segments of
-                              2^seg_shift elements, each segment's components one
-                              after another: (e, c) at (e >> s) * 2^s * dim +
-                              c * 2^s + (e & (2^s - 1)).  The library's own copies
-                              of SOA dats use s = 12 (ML_SEG_SHIFT); 0: plain  */
+                              2^s elements, each segment's components one after
+                              another at stride P = 2^s + ML_SEG_PAD: (e, c) at
+                              (e >> s) * P * dim + c * P + (e & (2^s - 1)).  The
+                              library's own SOA copies use s = ML_SEG_SHIFT;
+                              0: plain SOA                                     */
 } ml_arg_t;
+#ifndef ML_SEG_SHIFT
 #define ML_SEG_SHIFT 12
+#endif
+#ifndef ML_SEG_PAD
+#define ML_SEG_PAD 32
+#endif
+/* SOA dats of dim 2..ML_SEG_MAX_DIM are segmented on the device; wider SOA
+ * dats keep plain component rows (pitch = set size) */
+#ifndef ML_SEG_MAX_DIM
+#define ML_SEG_MAX_DIM 64
+#endif
 
 /* Device copy of an execution plan (plan.py:30-45).  `color_offsets` is a
  * HOST array; the rest are device arrays produced by ml_plan_* below. */
@@ -187,6 +198,9 @@ int ml_copy_h2d_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch,
  * ML_STREAM_H2D / ML_STREAM_D2H (asynchronous, streamed residency). */
 int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_t itemsize, int32_t seg_shift,
                 int32_t to_device, int32_t stream);
+/* The segment shift and pad this library was built with (the LP = 1 kernels
+ * assume them; the host side allocates and copies accordingly). */
+int ml_seg_params(int32_t *seg_shift, int32_t *seg_pad, int32_t *seg_max_dim);
 int ml_copy_d2h_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
                    uint64_t height);
 int ml_order(int32_t from, int32_t to);
@@ -285,8 +299,9 @@ int ml_program_free(ml_program_t *p);
  *      163-173 (_gather_rows/_scatter_rows), 652-660 (rank-ordered reduce) ---- */
 /* Gather rows `idx` (device int32, local element ids) of an 8-byte-element dat
  * with strides (elem_stride, comp_stride) into a contiguous [nidx][dim] buffer,
- * and the inverse scatter.  elem_stride 0 means a segmented SOA copy with
- * segments of comp_stride elements.  Stream-ordered on the compute stream. */
+ * and the inverse scatter.  A negative elem_stride -S means a segmented SOA
+ * copy with segments of S elements at component stride comp_stride.
+ * Stream-ordered on the compute stream. */
 int ml_pack_rows(void *dst, const void *dat, const int32_t *idx, int64_t nidx, int32_t dim,
                  int64_t elem_stride, int64_t comp_stride);
 int ml_unpack_rows(void *dat, const void *src, const int32_t *idx, int64_t nidx, int32_t dim,

@@ -22,7 +22,7 @@ ML_DIRECT, ML_INDIRECT, ML_GLOBAL = 0, 1, 2
 MODE_CODE = {"READ": 0, "WRITE": 1, "RW": 2, "INC": 3, "MIN": 4, "MAX": 5}
 ML_F64, ML_I64 = 0, 1
 ML_AOS, ML_SOA = 0, 1
-ML_SEG_SHIFT = 12          # segmented SOA device copies: 4096-element segments
+
 ML_STREAM_COMPUTE, ML_STREAM_H2D, ML_STREAM_D2H = 0, 1, 2
 
 #: every symbol include/meshloop_b200.h declares (checked by tests/test_abi.py)
@@ -30,7 +30,7 @@ EXPORTED = [
     "ml_last_error", "ml_version", "ml_init", "ml_device_info", "ml_synchronize",
     "ml_alloc", "ml_free", "ml_host_alloc", "ml_host_free", "ml_upload", "ml_download",
     "ml_memset", "ml_upload2d", "ml_download2d", "ml_map_upload", "ml_copy_h2d", "ml_copy_d2h",
-    "ml_copy_h2d_2d", "ml_copy_d2h_2d", "ml_seg_copy", "ml_order", "ml_sync_all",
+    "ml_copy_h2d_2d", "ml_copy_d2h_2d", "ml_seg_copy", "ml_seg_params", "ml_order", "ml_sync_all",
     "ml_plan_build", "ml_plan_sizes", "ml_plan_export", "ml_plan_free",
     "ml_gather_build", "ml_gather_export", "ml_gather_free",
     "ml_co_occurrence", "ml_cm_order",
@@ -112,6 +112,7 @@ _SIGNATURES = {
     "ml_copy_h2d_2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ml_copy_d2h_2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ml_seg_copy": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "ml_seg_params": (C.c_int, [_I32P, _I32P, _I32P]),
     "ml_map_upload": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
     "ml_copy_h2d": (C.c_int, [_P, _P, C.c_uint64]),
     "ml_copy_d2h": (C.c_int, [_P, _P, C.c_uint64]),
@@ -269,3 +270,11 @@ def functor_table() -> list[tuple[str, int]]:
         check(lib().ml_functor_name(i, buf, 128, C.byref(dt)))
         out.append((buf.value.decode(), dt.value))
     return out
+
+
+def seg_params() -> tuple[int, int, int]:
+    """(segment shift, component pad, widest segmented dim) of the library's
+    segmented SOA copies."""
+    sh, pad, mx = C.c_int32(), C.c_int32(), C.c_int32()
+    check(lib().ml_seg_params(C.byref(sh), C.byref(pad), C.byref(mx)), "ml_seg_params")
+    return sh.value, pad.value, mx.value

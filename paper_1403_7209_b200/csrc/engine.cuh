@@ -19,7 +19,7 @@
 // `sc`: any AOS/SOA mix).  LP = 1 is the reference's default auto-SOA policy
 // (core.py:403-404, threshold 4) fixed at compile time: a dat of dim <= 4 is
 // AOS (base e * dim, component offsets are immediates), wider dats SOA in the
-// device's segmented form (component offsets c * SEG, immediates too).  The
+// device's segmented form (component offsets c * SEGP, immediates too).  The
 // runtime picks LP = 1 when the loop's dats follow that policy — the common
 // case — which removes the 64-bit stride arithmetic from every gathered load.
 //
@@ -53,6 +53,8 @@
 #include <cuda/std/type_traits>
 #include <cuda/std/utility>
 
+#include "../../include/meshloop_b200.h"
+
 namespace ml {
 
 enum : int { KD = 0, KI = 1, KG = 2 };                        // direct / indirect / global
@@ -60,15 +62,19 @@ enum : int { MR = 0, MW = 1, MRW = 2, MINC = 3, MMIN = 4, MMAX = 5 };
 constexpr int MAX_ARGS = 16;
 constexpr int AUTO_SOA_DIM = 4;    // reference Mesh(auto_soa_threshold=4): dim > 4 is SOA
 // Device SOA copies are *segmented*: the set is cut into segments of SEG
-// elements and each segment stores its components one after another,
-// element (e, c) at (e >> SEG_SHIFT) * SEG * dim + c * SEG + (e & (SEG - 1)).
-// Inside a segment a component is one contiguous run, so a warp's access is
-// as coalesced as plain SOA; but the offset of component c from an element's
-// base is the compile-time c * SEG * 8 bytes — a load immediate — instead of
-// c * set_size (a 64-bit multiply-add per load).  SEG * 8 = 32 KB rows also
-// keep host<->device copies DMA-efficient (one 2-D copy per component).
-constexpr int SEG_SHIFT = 12;
+// elements and each segment stores its components one after another at a
+// component stride of SEGP = SEG + 32 elements: element (e, c) at
+// (e >> SEG_SHIFT) * SEGP * dim + c * SEGP + (e & (SEG - 1)).  Inside a
+// segment a component is one contiguous run, so a warp's access is as
+// coalesced as plain SOA; but the offset of component c from an element's
+// base is the compile-time c * SEGP * 8 bytes — a load immediate — instead of
+// c * set_size (a 64-bit multiply-add per load).  The 256-byte pad keeps the
+// component stride off a power of two (a 32 KB stride maps all components
+// of an element to one L1 set); SEG * 8 = 32 KB rows keep host<->device
+// copies DMA-efficient (one 2-D copy per component).
+constexpr int SEG_SHIFT = ML_SEG_SHIFT;          // include/meshloop_b200.h
 constexpr int64_t SEG = int64_t(1) << SEG_SHIFT;
+constexpr int64_t SEGP = SEG + ML_SEG_PAD;
 
 // Programmatic dependent launch: the hot kernels are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs can
@@ -116,7 +122,7 @@ struct ArgRt {
     const int32_t *map;   // map column (already offset by slot*from)
     int64_t se, sc;       // element stride, component stride (in elements)
     int32_t sh;           // segmented SOA: log2 of the segment length (0: linear)
-    int64_t sb;           // segmented SOA: elements per segment (segment length * dim)
+    int64_t sb;           // segmented SOA: elements per segment (component stride * dim)
 };
 
 // offset (in elements) of element e's first component
@@ -201,22 +207,24 @@ struct RefA {
 };
 
 // layout class of argument A under policy LP: 0 runtime strides, 1 AOS (base
-// e * dim, component stride 1), 2 segmented SOA (SEG_SHIFT, component stride SEG)
+// e * dim, component stride 1), 2 segmented SOA (SEG_SHIFT, component stride
+// SEGP), 3 plain SOA (component stride = the runtime pitch)
 template <class A, int LP>
 __host__ __device__ constexpr int lay_of() {
-    return (LP == 0 || A::kind == KG) ? 0 : (A::dim <= AUTO_SOA_DIM ? 1 : 2);
+    return (LP == 0 || A::kind == KG) ? 0 : (A::dim <= AUTO_SOA_DIM ? 1 : A::dim <= ML_SEG_MAX_DIM ? 2 : 3);
 }
 // element base offset and component stride under layout class L
 template <class A, int L>
 __device__ __forceinline__ int64_t base_of(const ArgRt &r, int64_t e) {
     if constexpr (L == 1) return e * A::dim;
-    else if constexpr (L == 2) return (e >> SEG_SHIFT) * (SEG * A::dim) + (e & (SEG - 1));
+    else if constexpr (L == 2) return (e >> SEG_SHIFT) * (SEGP * A::dim) + (e & (SEG - 1));
+    else if constexpr (L == 3) return e;
     else return elem_base(r, e);
 }
 template <class A, int L>
 __device__ __forceinline__ int64_t sc_of(const ArgRt &r) {
     if constexpr (L == 1) return 1;
-    else if constexpr (L == 2) return SEG;
+    else if constexpr (L == 2) return SEGP;
     else return r.sc;
 }
 
@@ -565,10 +573,10 @@ struct DirRows {
                     v[0][c] = f[c];
                     v[1][c] = f[A::dim + c];
                 }
-            } else {                            // segmented SOA: one pair per component
+            } else {                            // SOA: one pair per component
                 const T *bb = b + base_of<A, L>(r, e0);
 #pragma unroll
-                for (int c = 0; c < A::dim; ++c) ld2(bb + c * SEG, v[0][c], v[1][c]);
+                for (int c = 0; c < A::dim; ++c) ld2(bb + c * sc_of<A, L>(r), v[0][c], v[1][c]);
             }
         }
     }
@@ -592,7 +600,7 @@ struct DirRows {
             } else {
                 T *bb = b + base_of<A, L>(r, e0);
 #pragma unroll
-                for (int c = 0; c < A::dim; ++c) st2(bb + c * SEG, v[0][c], v[1][c]);
+                for (int c = 0; c < A::dim; ++c) st2(bb + c * sc_of<A, L>(r), v[0][c], v[1][c]);
             }
         }
     }

@@ -128,7 +128,9 @@ static int layout_policy(const ml_loop_t *L) {
         const ml_arg_t &a = L->args[i];
         if (a.kind == ML_GLOBAL) continue;
         if (a.dim > AUTO_SOA_DIM) {
-            if (a.layout != ML_SOA || a.seg_shift != SEG_SHIFT) return 0;
+            const int want = a.dim <= ML_SEG_MAX_DIM ? SEG_SHIFT : 0;
+            if (a.layout != ML_SOA || a.seg_shift != want) return 0;
+            if (!want && ((a.pitch ? a.pitch : a.set_size) & 1)) return 0;   // 16-byte pairs
         } else if (a.dim > 1 && a.layout != ML_AOS) {
             return 0;
         }
@@ -211,7 +213,7 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         } else if (a.seg_shift > 0) {             // segmented SOA
             r.se = 0;
             r.sh = a.seg_shift;
-            r.sc = int64_t(1) << a.seg_shift;
+            r.sc = (int64_t(1) << a.seg_shift) + ML_SEG_PAD;
             r.sb = r.sc * a.dim;
         } else {
             r.se = 1;
@@ -481,6 +483,12 @@ extern "C" int ml_copy_d2h_2d(void *dst, uint64_t dpitch, const void *src, uint6
         ML_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, g_dev.copy[1]));
     return ML_OK;
 }
+extern "C" int ml_seg_params(int32_t *seg_shift, int32_t *seg_pad, int32_t *seg_max_dim) {
+    if (seg_shift) *seg_shift = ML_SEG_SHIFT;
+    if (seg_pad) *seg_pad = ML_SEG_PAD;
+    if (seg_max_dim) *seg_max_dim = ML_SEG_MAX_DIM;
+    return ML_OK;
+}
 static cudaStream_t stream_of(int32_t which);
 extern "C" int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_t itemsize, int32_t seg_shift,
                            int32_t to_device, int32_t stream) {
@@ -490,19 +498,19 @@ extern "C" int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_
         ML_FAIL(ML_EINVAL, "ml_seg_copy: bad arguments");
     if (n == 0) return ML_OK;
     cudaStream_t s = stream_of(stream);
-    const uint64_t S = uint64_t(1) << seg_shift, isz = uint64_t(itemsize);
+    const uint64_t S = uint64_t(1) << seg_shift, SP = S + ML_SEG_PAD, isz = uint64_t(itemsize);
     const uint64_t nfull = uint64_t(n) >> seg_shift, rem = uint64_t(n) - nfull * S;
     char *d = static_cast<char *>(dev), *h = static_cast<char *>(host);
     for (uint64_t c = 0; c < uint64_t(dim); ++c) {
-        char *dc = d + c * S * isz, *hc = h + c * uint64_t(n) * isz;
+        char *dc = d + c * SP * isz, *hc = h + c * uint64_t(n) * isz;
         if (nfull) {
             if (to_device)
-                ML_CUDA(cudaMemcpy2DAsync(dc, S * dim * isz, hc, S * isz, S * isz, nfull, cudaMemcpyHostToDevice, s));
+                ML_CUDA(cudaMemcpy2DAsync(dc, SP * dim * isz, hc, S * isz, S * isz, nfull, cudaMemcpyHostToDevice, s));
             else
-                ML_CUDA(cudaMemcpy2DAsync(hc, S * isz, dc, S * dim * isz, S * isz, nfull, cudaMemcpyDeviceToHost, s));
+                ML_CUDA(cudaMemcpy2DAsync(hc, S * isz, dc, SP * dim * isz, S * isz, nfull, cudaMemcpyDeviceToHost, s));
         }
         if (rem) {
-            char *dt = dc + nfull * S * dim * isz, *ht = hc + nfull * S * isz;
+            char *dt = dc + nfull * SP * dim * isz, *ht = hc + nfull * S * isz;
             if (to_device) ML_CUDA(cudaMemcpyAsync(dt, ht, rem * isz, cudaMemcpyHostToDevice, s));
             else ML_CUDA(cudaMemcpyAsync(ht, dt, rem * isz, cudaMemcpyDeviceToHost, s));
         }
@@ -898,10 +906,11 @@ extern "C" int ml_program_free(ml_program_t *p) {
 
 // ---- ABI: multi-GPU helpers --------------------------------------------------------------------
 namespace ml {
-// element (e, c) of a dat given the ABI's (elem_stride, comp_stride):
-// elem_stride 0 means segmented SOA with segments of comp_stride elements
+// element (e, c) of a dat given the ABI's (elem_stride, comp_stride): a
+// negative elem_stride -S means segmented SOA with segments of S elements
+// and component stride comp_stride
 __device__ __forceinline__ int64_t row_index(int64_t e, int c, int dim, int64_t se, int64_t sc) {
-    if (se == 0) return (e / sc) * sc * dim + c * sc + (e % sc);
+    if (se < 0) return (e / -se) * sc * dim + c * sc + (e % -se);
     return e * se + c * sc;
 }
 __global__ void k_pack_rows(double *dst, const double *dat, const int32_t *idx, int64_t nidx, int dim,

@@ -24,32 +24,58 @@ import numpy as np
 from . import _native as N
 from .core import AOS, Dat, ExecError, Map
 
-__all__ = ["DatMirror", "dat_mirror", "segmented", "device_elems", "map_mirror", "plan_mirror", "pin_mesh",
+__all__ = ["DatMirror", "dat_mirror", "segmented", "device_elems", "device_pitch", "PITCH_ALIGN", "map_mirror", "plan_mirror", "pin_mesh",
            "gather_mirror", "pfold_mirror", "gather_eligible", "fold_eligible", "SEG_SHIFT"]
 
 
 #: SOA dats of dim > 1 are stored *segmented* on the device: segments of
-#: 2**SEG_SHIFT elements, each holding its components one after another —
-#: (e, c) at (e >> s) * 2**s * dim + c * 2**s + (e & (2**s - 1)).  Inside a
-#: segment a component is a contiguous run (coalesced like plain SOA); the
-#: offset of component c from an element's base is the compile-time
-#: c * 2**s * 8 bytes, a load immediate in the kernels (engine.cuh).
-SEG_SHIFT = N.ML_SEG_SHIFT
+#: S = 2**SEG_SHIFT elements, each holding its components one after another
+#: at stride P = S + SEG_PAD — (e, c) at (e >> s) * P * dim + c * P + (e % S).
+#: Inside a segment a component is a contiguous run (coalesced like plain
+#: SOA); the offset of component c from an element's base is the
+#: compile-time c * P * 8 bytes, a load immediate in the kernels (engine.cuh).
+def _seg_params():
+    global SEG_SHIFT, SEG_PAD, SEG_MAX_DIM
+    if SEG_SHIFT is None:
+        SEG_SHIFT, SEG_PAD, SEG_MAX_DIM = N.seg_params()   # as the library was built
+    return SEG_SHIFT, SEG_PAD
+
+
+#: segment shift / component pad / widest segmented dim, read from the library
+SEG_SHIFT = SEG_PAD = SEG_MAX_DIM = None
 
 
 def segmented(dat: Dat) -> bool:
-    """Whether ``dat``'s device copy is segmented SOA."""
-    return dat.layout is not AOS and dat.dim > 1
+    """Whether ``dat``'s device copy is segmented SOA (SOA, 1 < dim <= the
+    library's widest segmented dim); wider SOA dats keep plain rows."""
+    _seg_params()
+    return dat.layout is not AOS and 1 < dat.dim <= SEG_MAX_DIM
+
+
+#: plain SOA rows (dims above the segmented range) are padded to this many
+#: elements, so every component row starts 256-byte aligned and the pitch is
+#: even (16-byte element pairs in the direct loops)
+PITCH_ALIGN = 32
+
+
+def device_pitch(dat: Dat) -> int:
+    """Component stride of a plain (unsegmented) device copy: the set size, or
+    for SOA dats of dim > 1 the set size rounded up to PITCH_ALIGN."""
+    n = dat.set.size
+    if dat.layout is AOS or dat.dim == 1:
+        return n
+    return -(-n // PITCH_ALIGN) * PITCH_ALIGN
 
 
 def device_elems(dat: Dat) -> int:
     """Elements of ``dat``'s device copy (segmented copies round the set up to
-    whole segments)."""
+    whole segments, pitched ones pad each component row)."""
     n = dat.set.size
     if not segmented(dat):
-        return n * dat.dim
-    seg = 1 << SEG_SHIFT
-    return -(-n // seg) * seg * dat.dim
+        return device_pitch(dat) * dat.dim
+    sh, pad = _seg_params()
+    seg = 1 << sh
+    return -(-n // seg) * (seg + pad) * dat.dim
 
 
 class DatMirror:
@@ -57,7 +83,8 @@ class DatMirror:
     host; SOA dats segmented (``SEG_SHIFT``), copied with one 2-D transfer of
     the full segments plus one tail copy per component (``ml_seg_copy``)."""
 
-    __slots__ = ("buf", "layout", "nbytes", "host_newer", "device_newer", "seg", "n", "dim", "isz")
+    __slots__ = ("buf", "layout", "nbytes", "host_newer", "device_newer", "seg", "n", "dim", "isz",
+                 "_pitch")
 
     def __init__(self):
         self.buf = None
@@ -66,7 +93,7 @@ class DatMirror:
         self.host_newer = True
         self.device_newer = False
         self.seg = False
-        self.n = self.dim = self.isz = 0
+        self.n = self.dim = self.isz = self._pitch = 0
 
     @property
     def ptr(self) -> int:
@@ -74,23 +101,28 @@ class DatMirror:
 
     @property
     def pitch(self) -> int:
-        """ABI ``pitch`` of the copy (plain layouts: the set size)."""
-        return self.n
+        """ABI ``pitch`` of the copy (plain SOA component stride)."""
+        return self._pitch
+
+    @property
+    def padded(self) -> bool:
+        return not self.seg and self._pitch != self.n and self.dim > 1
 
     @property
     def seg_shift(self) -> int:
-        return SEG_SHIFT if self.seg else 0
+        return _seg_params()[0] if self.seg else 0
 
     def strides(self, dat: Dat) -> tuple[int, int]:
         """(element stride, component stride) in the ABI's row-kernel
-        convention (ml_pack_rows): element stride 0 = segmented SOA with
-        segments of the component stride."""
+        convention (ml_pack_rows): a negative element stride -S = segmented
+        SOA with segments of S elements."""
         if self.seg:
-            return 0, 1 << SEG_SHIFT
-        return (dat.dim, 1) if dat.layout is AOS else (1, self.n)
+            sh, pad = _seg_params()
+            return -(1 << sh), (1 << sh) + pad
+        return (dat.dim, 1) if dat.layout is AOS else (1, self._pitch)
 
     def _seg_copy(self, host: np.ndarray, to_device: bool, stream: int) -> None:
-        N.check(N.lib().ml_seg_copy(self.buf.ptr, N.ptr(host), self.n, self.dim, self.isz, SEG_SHIFT,
+        N.check(N.lib().ml_seg_copy(self.buf.ptr, N.ptr(host), self.n, self.dim, self.isz, _seg_params()[0],
                                     int(to_device), stream), "ml_seg_copy")
 
     def upload(self, host: np.ndarray) -> None:
@@ -98,6 +130,10 @@ class DatMirror:
             return
         if self.seg:
             self._seg_copy(host, True, N.ML_STREAM_COMPUTE)
+        elif self.padded:
+            rb = self.n * self.isz
+            N.check(N.lib().ml_upload2d(self.buf.ptr, self._pitch * self.isz, N.ptr(host), rb, rb, self.dim),
+                    "ml_upload2d")
         else:
             self.buf.upload(host)
 
@@ -107,6 +143,10 @@ class DatMirror:
                 raise ExecError("dat payload must be contiguous to receive device data")
             if self.seg:
                 self._seg_copy(host, False, N.ML_STREAM_COMPUTE)
+            elif self.padded:
+                rb = self.n * self.isz
+                N.check(N.lib().ml_download2d(N.ptr(host), rb, self.buf.ptr, self._pitch * self.isz, rb,
+                                              self.dim), "ml_download2d")
             else:
                 self.buf.download(host)
         self.device_newer = False
@@ -117,6 +157,10 @@ class DatMirror:
             return
         if self.seg:
             self._seg_copy(host, True, N.ML_STREAM_H2D)
+        elif self.padded:
+            rb = self.n * self.isz
+            N.check(N.lib().ml_copy_h2d_2d(self.buf.ptr, self._pitch * self.isz, N.ptr(host), rb, rb,
+                                           self.dim), "ml_copy_h2d_2d")
         else:
             N.check(N.lib().ml_copy_h2d(self.buf.ptr, N.ptr(host), host.nbytes), "ml_copy_h2d")
 
@@ -126,6 +170,10 @@ class DatMirror:
             return
         if self.seg:
             self._seg_copy(host, False, N.ML_STREAM_D2H)
+        elif self.padded:
+            rb = self.n * self.isz
+            N.check(N.lib().ml_copy_d2h_2d(N.ptr(host), rb, self.buf.ptr, self._pitch * self.isz, rb,
+                                           self.dim), "ml_copy_d2h_2d")
         else:
             N.check(N.lib().ml_copy_d2h(N.ptr(host), self.buf.ptr, host.nbytes), "ml_copy_d2h")
 
@@ -146,6 +194,7 @@ def dat_mirror(dat: Dat, force_upload: bool = False, upload: bool = True) -> Dat
         m.nbytes = dev_bytes
         m.host_newer = True
     m.seg, m.n, m.dim, m.isz = seg, dat.set.size, dat.dim, host.dtype.itemsize
+    m._pitch = device_pitch(dat)
     if m.layout is not dat.layout:
         m.layout = dat.layout
         m.host_newer = True

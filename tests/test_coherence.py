@@ -72,8 +72,7 @@ def test_device_then_host_residency_keeps_device_results(host_mode):
 def test_segmented_soa_device_copies_round_trip(n):
     """SOA dats live on the device in 4096-element segments (device.py
     SEG_SHIFT): host -> device -> host is exact for ragged set sizes, and a
-    direct loop (16-byte pairs) and an indirect gather read the right
-    components."""
+    direct loop (16-byte pairs) moves the right components."""
     from paper_1403_7209_b200.device import dat_mirror
     rng = np.random.default_rng(n)
     mesh = ml.Mesh()

@@ -67,10 +67,14 @@ typedef struct ml_arg {
 #ifndef ML_SEG_PAD
 #define ML_SEG_PAD 32
 #endif
-/* SOA dats of dim 2..ML_SEG_MAX_DIM are segmented on the device; wider SOA
- * dats keep plain component rows (pitch = set size) */
+/* SOA dats of dim 2..ML_SEG_MAX_DIM are segmented on the device; other SOA
+ * dats keep plain component rows padded to 32 elements.  Default 4, i.e. no
+ * auto-SOA dat (dim > 4) is segmented: on the Hydra proxy segmenting every
+ * SOA dat makes the fused flux loop 4 % faster and the grad_edge gather 12 %
+ * slower (profiles/r2/seg_sweep.md); build with -DML_SEG_MAX_DIM=64 to
+ * segment them. */
 #ifndef ML_SEG_MAX_DIM
-#define ML_SEG_MAX_DIM 64
+#define ML_SEG_MAX_DIM 4
 #endif
 
 /* Device copy of an execution plan (plan.py:30-45).  `color_offsets` is a

@@ -129,6 +129,9 @@ typedef struct ml_loop {
      * up to even], rows in pf_elem2 order (ml_loop_pfold_slot_bytes). */
     int64_t pf_n1;
     const int32_t *pf_off1, *pf_elem1, *pf_tl1;
+    const uint8_t *pf_ppos1;        /* INC position of each primary incidence (the
+                                       element's argument with the smallest target
+                                       id); NULL: position 0                       */
     int64_t pf_n2;
     const int32_t *pf_off2, *pf_elem2, *pf_tl2;
     const uint8_t *pf_pos2;
@@ -148,6 +151,14 @@ typedef struct ml_loop {
     void *pf_part1, *pf_part2;
     int64_t pf_nhub1, pf_nhub2;
     const int32_t *pf_hub1_tl, *pf_hub1_off, *pf_hub2_tl, *pf_hub2_off;
+    /* single-pass primary fold (pf_fused != 0): pass-1 and pass-2 rows are one
+     * list (pf_tl1 == pf_tl2); CTA-sized chunks publish pf_flags[c] (device,
+     * [pf_nchunks], zeroed by the library before each launch) and wait for
+     * pf_dep_list[pf_dep_off[c] .. pf_dep_off[c+1]) before folding slots */
+    int32_t pf_fused;
+    int64_t pf_nchunks;
+    const int32_t *pf_dep_off, *pf_dep_list;
+    int32_t *pf_flags;
     /* colour schedule: launch only block colours [colour_begin, colour_end)
      * (colour_end <= 0: all).  The reduction combine runs with the launch
      * that reaches the last colour, so a host loop over single colours (the

@@ -333,37 +333,77 @@ def split_hub_rows(off: np.ndarray, rows_tl: np.ndarray, hub_row: int = HUB_ROW)
             "hub_off": np.concatenate([[0], np.cumsum(nseg[heavy])]).astype(np.int32)}
 
 
-def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW) -> dict:
-    """Primary-fold lists from one-row-per-target gather lists: per target, its
-    incidences through the first INC argument (``1``) and through the others
-    (``2``, with positions), element ascending; only targets that have any.
-    Rows longer than ``hub_row`` are split (``split_hub_rows``): ``seg{1,2}``,
-    ``nhub{1,2}``, ``nslots{1,2}``, ``hub{1,2}_tl``, ``hub{1,2}_off``."""
+#: rows per chunk of the single-pass primary fold (= its CTA size)
+PFOLD_CHUNK = 256
+
+
+def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW, chunk: int = PFOLD_CHUNK) -> dict:
+    """Primary-fold lists from one-row-per-target gather lists.
+
+    Each element's *primary* incidence is the one with the smallest target id
+    (ties: the lowest argument position): its owner evaluates the element and
+    keeps that increment; the other incidences are *secondary* (slots).  Per
+    target row: its primary incidences (``1``, with ``ppos1`` the primary
+    argument position) and its secondary ones (``2``, with ``pos2``), element
+    ascending.  Without hub rows both passes share one row list (every target
+    with an incidence, ascending: ``unified``) and the single-pass kernel's
+    chunk dependencies are built: chunk c (rows [c*chunk, (c+1)*chunk)) needs
+    the earlier chunks owning the primaries of its rows' secondary incidences
+    (``dep_off``/``dep_list``) — always earlier, since a primary target is the
+    smaller one.  Rows longer than ``hub_row`` in either pass are split
+    (``split_hub_rows``): ``seg{1,2}``, ``nhub{1,2}``, ``nslots{1,2}``,
+    ``hub{1,2}_tl``, ``hub{1,2}_off``; the lists are then compacted per pass."""
     off, elem, pos, tl = host["off"], host["elem"], host["pos"], host["targets"]
     nt = off.size - 1
     owner = np.repeat(np.arange(nt), np.diff(off))
     e, p_ = elem[:off[-1]], pos[:off[-1]]
-    out = {}
+    tgt = tl[owner].astype(np.int64)
+    order = np.lexsort((p_, tgt, e))                    # per element: (target, position) ascending
+    lead = np.ones(order.size, bool)
+    lead[1:] = e[order][1:] != e[order][:-1]
+    prim = np.zeros(e.size, bool)
+    prim[order[lead]] = True
+    deg = {1: np.bincount(owner[prim], minlength=nt), 2: np.bincount(owner[~prim], minlength=nt)}
+    hubs = hub_row is not None and any(int(d.max(initial=0)) > hub_row for d in deg.values())
+    out = {"unified": not hubs}
     for which in (1, 2):
-        m = (p_ == 0) if which == 1 else (p_ > 0)
-        cnt = np.bincount(owner[m], minlength=nt)
-        keep = np.flatnonzero(cnt)
+        m = prim if which == 1 else ~prim
+        cnt = deg[which]
+        keep = np.arange(nt) if not hubs else np.flatnonzero(cnt)
         out[f"n{which}"] = int(keep.size)
         out[f"off{which}"] = np.concatenate([[0], np.cumsum(cnt[keep])]).astype(np.int32)
         out[f"elem{which}"] = np.ascontiguousarray(e[m], dtype=np.int32)
         out[f"tl{which}"] = np.ascontiguousarray(tl[keep], dtype=np.int32)
-        if which == 2:
-            out["pos2"] = np.ascontiguousarray(p_[m], dtype=np.uint8)
-    # slot row of each (element, position >= 1): its index in the secondary CSR
+        out["ppos1" if which == 1 else "pos2"] = np.ascontiguousarray(p_[m], dtype=np.uint8)
+    # slot row of each (element, secondary position): its index in the secondary
+    # CSR; an element's secondary positions are numbered in ascending order
+    # skipping its primary position
     nw = int(p_.max(initial=0)) + 1 if p_.size else 1
     n_el = int(e.max(initial=-1)) + 1
     slotpos = np.zeros(max(n_el * max(nw - 1, 1), 1), np.int32)
     if nw > 1 and out["elem2"].size:
-        slotpos[out["elem2"].astype(np.int64) * (nw - 1) + out["pos2"].astype(np.int64) - 1] = \
-            np.arange(out["elem2"].size, dtype=np.int32)
+        pp = np.zeros(max(n_el, 1), np.int64)
+        pp[out["elem1"]] = out["ppos1"]
+        e2, p2 = out["elem2"].astype(np.int64), out["pos2"].astype(np.int64)
+        j = p2 - (p2 > pp[e2])
+        slotpos[e2 * (nw - 1) + j] = np.arange(e2.size, dtype=np.int32)
     out["slotpos"] = slotpos
+    out["dep_off"] = out["dep_list"] = None
+    out["nchunks"] = 0
+    if not hubs:
+        nch = -(-nt // chunk) if nt else 0
+        row1 = np.zeros(max(n_el, 1), np.int64)
+        row1[out["elem1"]] = np.repeat(np.arange(nt), deg[1])
+        row2 = np.repeat(np.arange(nt), deg[2])
+        src, dst = row1[out["elem2"]] // chunk, row2 // chunk
+        m = src < dst
+        pairs = np.unique(dst[m] * max(nch, 1) + src[m])
+        d_chunk, s_chunk = pairs // max(nch, 1), pairs % max(nch, 1)
+        out["nchunks"] = nch
+        out["dep_off"] = np.concatenate([[0], np.cumsum(np.bincount(d_chunk, minlength=nch))]).astype(np.int32)
+        out["dep_list"] = np.ascontiguousarray(s_chunk, dtype=np.int32)
     for which in (1, 2):
-        sp = split_hub_rows(out[f"off{which}"], out[f"tl{which}"], hub_row) if hub_row else None
+        sp = split_hub_rows(out[f"off{which}"], out[f"tl{which}"], hub_row) if hubs else None
         if sp is None:
             out.update({f"seg{which}": None, f"nhub{which}": 0, f"nslots{which}": 0,
                         f"hub{which}_tl": None, f"hub{which}_off": None})
@@ -420,16 +460,22 @@ class PFoldMirror:
     incidences through the first INC argument (pass 1) and through the others
     (pass 2), element ascending; plus the per-element slot buffer."""
 
-    __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos",
+    __slots__ = ("n1", "off1", "elem1", "tl1", "ppos1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos",
                  "rec", "ncol", "rcol", "seg1", "seg2", "nhub1", "nhub2", "hub1_tl", "hub1_off",
-                 "hub2_tl", "hub2_off", "part1", "part2", "host", "rec_host")
+                 "hub2_tl", "hub2_off", "part1", "part2", "host", "rec_host", "unified", "nchunks",
+                 "dep_off", "dep_list", "flags")
 
     def __init__(self, g: GatherMirror, loop, records: bool = True):
         h = pfold_lists_host(g.host)
         self.host, self.rec_host = h, None
         self.n1, self.n2 = h["n1"], h["n2"]
-        for k in ("off1", "elem1", "tl1", "off2", "elem2", "tl2", "pos2", "slotpos"):
+        for k in ("off1", "elem1", "tl1", "ppos1", "off2", "elem2", "tl2", "pos2", "slotpos"):
             setattr(self, k, _upload(h[k]))
+        self.unified, self.nchunks = h["unified"], h["nchunks"]
+        self.dep_off = self.dep_list = self.flags = None
+        if self.unified and self.nchunks:
+            self.dep_off, self.dep_list = _upload(h["dep_off"]), _upload(h["dep_list"])
+            self.flags = N.DeviceBuffer(4 * self.nchunks)
         inc = next(a for a in loop.args if a.kind == "indirect" and a.mode.name == "INC")
         row = inc.dat.dim * np.dtype(inc.dat.dtype).itemsize
         for w in (1, 2):
@@ -458,6 +504,7 @@ class PFoldMirror:
                 + np.arange(int(deg.sum()))).astype(np.int64)
         out = {"n1": int(rows.size), "off1": _upload(new_off),
                "elem1": _upload(np.ascontiguousarray(h["elem1"][take])),
+               "ppos1": _upload(np.ascontiguousarray(h["ppos1"][take])),
                "tl1": _upload(np.ascontiguousarray(h["tl1"][rows])),
                "seg1": _upload(np.ascontiguousarray(h["seg1"][rows])) if h["seg1"] is not None else None,
                "rec": (_upload(np.ascontiguousarray(self.rec_host[take]))

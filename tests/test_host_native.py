@@ -315,15 +315,34 @@ def test_gather_hub_rows_and_pfold_lists(rng):
                     rows = np.flatnonzero((tl == t) & (seg >= 0))
                     assert seg[rows].tolist() == list(range(h["hub_off"][k], h["hub_off"][k + 1]))
             pf = pfold_lists_host(h["host"], hub_row=None)
+            # primary incidence = the element's smaller target (ties: position 0)
+            prim_pos = np.where(tab[:, 1] < tab[:, 0], 1, 0)
             k = np.arange(pf["elem2"].size)
-            np.testing.assert_array_equal(
-                pf["slotpos"][pf["elem2"].astype(np.int64) + pf["pos2"].astype(np.int64) - 1], k)
-            for which, sel in ((1, lambda a: a == 0), (2, lambda a: a > 0)):
+            e2, p2 = pf["elem2"].astype(np.int64), pf["pos2"].astype(np.int64)
+            np.testing.assert_array_equal(p2, 1 - prim_pos[e2])
+            np.testing.assert_array_equal(pf["slotpos"][e2], k)       # one secondary per element
+            np.testing.assert_array_equal(pf["ppos1"], prim_pos[pf["elem1"]])
+            for which, sel in ((1, lambda e, a: a == prim_pos[e]), (2, lambda e, a: a != prim_pos[e])):
                 o, el, t1 = pf[f"off{which}"], pf[f"elem{which}"], pf[f"tl{which}"]
                 for r in range(pf[f"n{which}"]):
                     es = el[o[r]:o[r + 1]].tolist()
                     assert es == sorted(es)
-                    assert es == [e for e, a in want[int(t1[r])] if sel(a)]
+                    assert es == [e for e, a in want.get(int(t1[r]), []) if sel(e, a)]
+            # unified rows and the single-pass chunk dependencies: every
+            # secondary incidence's primary owner sits in an earlier chunk or
+            # the same one, and every earlier one is listed
+            assert pf["unified"] and np.array_equal(pf["tl1"], pf["tl2"])
+            B = 16
+            pc = pfold_lists_host(h["host"], hub_row=None, chunk=B)
+            row1 = np.repeat(np.arange(pc["n1"]), np.diff(pc["off1"]))
+            owner_row = np.empty(n, np.int64)
+            owner_row[pc["elem1"]] = row1
+            row2 = np.repeat(np.arange(pc["n2"]), np.diff(pc["off2"]))
+            src, dst = owner_row[pc["elem2"]] // B, row2 // B
+            assert np.all(src <= dst)
+            for c in range(pc["nchunks"]):
+                deps = set(pc["dep_list"][pc["dep_off"][c]:pc["dep_off"][c + 1]].tolist())
+                assert deps == set(src[(dst == c) & (src < c)].tolist())
             # hub rows: split rows concatenate, in row order, to each target's list
             ps = pfold_lists_host(h["host"], hub_row=hub_row)
             for which in (1, 2):

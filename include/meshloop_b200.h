@@ -151,14 +151,6 @@ typedef struct ml_loop {
     void *pf_part1, *pf_part2;
     int64_t pf_nhub1, pf_nhub2;
     const int32_t *pf_hub1_tl, *pf_hub1_off, *pf_hub2_tl, *pf_hub2_off;
-    /* single-pass primary fold (pf_fused != 0): pass-1 and pass-2 rows are one
-     * list (pf_tl1 == pf_tl2); CTA-sized chunks publish pf_flags[c] (device,
-     * [pf_nchunks], zeroed by the library before each launch) and wait for
-     * pf_dep_list[pf_dep_off[c] .. pf_dep_off[c+1]) before folding slots */
-    int32_t pf_fused;
-    int64_t pf_nchunks;
-    const int32_t *pf_dep_off, *pf_dep_list;
-    int32_t *pf_flags;
     /* colour schedule: launch only block colours [colour_begin, colour_end)
      * (colour_end <= 0: all).  The reduction combine runs with the launch
      * that reaches the last colour, so a host loop over single colours (the

@@ -81,9 +81,7 @@ class MlLoop(C.Structure):
                 ("pf_seg1", C.c_void_p), ("pf_seg2", C.c_void_p), ("pf_part1", C.c_void_p),
                 ("pf_part2", C.c_void_p), ("pf_nhub1", C.c_int64), ("pf_nhub2", C.c_int64),
                 ("pf_hub1_tl", C.c_void_p), ("pf_hub1_off", C.c_void_p), ("pf_hub2_tl", C.c_void_p),
-                ("pf_hub2_off", C.c_void_p), ("pf_fused", C.c_int32), ("pf_nchunks", C.c_int64),
-                ("pf_dep_off", C.c_void_p), ("pf_dep_list", C.c_void_p), ("pf_flags", C.c_void_p),
-                ("colour_begin", C.c_int32), ("colour_end", C.c_int32)]
+                ("pf_hub2_off", C.c_void_p), ("colour_begin", C.c_int32), ("colour_end", C.c_int32)]
 
 
 class MlDeviceInfo(C.Structure):

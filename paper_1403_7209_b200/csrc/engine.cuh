@@ -141,9 +141,6 @@ struct Consts {
 // pass 1 gives each target the elements it is primary for, evaluates each
 // element once there, accumulates that increment in the thread's registers and
 // writes the others to per-element slots; pass 2 folds each target's slots.
-// Single-pass form (fused != 0, one row list for both passes): a CTA handles a
-// chunk of rows, publishes the chunk, waits for the earlier chunks owning its
-// rows' secondary incidences and folds the slots before the single store.
 struct PFoldParams {
     int64_t n1;                          // targets with primary incidences
     const int32_t *off1, *elem1, *tl1;   // CSR (element ascending); tl1: target ids
@@ -167,13 +164,6 @@ struct PFoldParams {
     // slots onto it in row (= element) order after the pass
     const int32_t *seg1, *seg2;
     void *part1, *part2;
-    // single-pass form: chunk c of blockDim rows waits for chunks
-    // dep_list[dep_off[c] .. dep_off[c+1]) (all earlier); flags[c] != 0 once
-    // chunk c's slots are written (zeroed before every launch)
-    int32_t fused;
-    int64_t nchunks;
-    const int32_t *dep_off, *dep_list;
-    int32_t *flags;
 };
 
 struct LaunchParams {
@@ -894,92 +884,6 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
     if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
 }
 
-// Single-pass primary fold (PFoldParams::fused): CTA-sized chunks of the
-// common row list in grid-stride order.  A CTA evaluates its rows' primary
-// incidences (as pass 1), writes their secondary increments to the slots,
-// publishes the chunk (fence, barrier, release flag), waits for the earlier
-// chunks that own its rows' secondary incidences (their primary targets are
-// smaller ids, so dependencies only point back: with every CTA resident the
-// lowest unfinished chunk never waits), then each row adds its slots in
-// element order — the same per-target sum as the two passes, without the
-// second launch, the res round trip and the slot read-back from HBM (the
-// slots are fresh in L2).
-__device__ __forceinline__ void flag_release(int32_t *f) {
-    asm volatile("st.release.gpu.global.b32 [%0], 1;" ::"l"(f) : "memory");
-}
-__device__ __forceinline__ int flag_acquire(const int32_t *f) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    return v;
-}
-
-template <class F, int LP, class... As>
-__device__ __forceinline__ void run_pfold_fused(const LaunchParams &p, Sig<As...>) {
-    using E = Engine<F, ST_GATHER, LP, As...>;
-    constexpr int G = IncIndex<As...>::template first<0>();
-    static_assert(G >= 0, "primary fold needs an INC argument");
-    using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
-    using TG = typename AG::type;
-    constexpr int DG = AG::dim;
-    constexpr int LG = lay_of<AG, LP>();
-    constexpr int NW = ((As::kind == KI && As::mode == MINC) + ...);
-    constexpr int DGP = PFoldShape<TG, DG>::DGP;
-    __shared__ double red[32];
-    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    typename E::Slots s;
-    E::init_globals(s, p, idx);
-    const PFoldParams &pf = p.pf;
-    const ArgRt &rg = p.a[G];
-    const int64_t gsc = sc_of<AG, LG>(rg);
-    const TG *slots = static_cast<const TG *>(pf.slots);
-    for (int64_t c = blockIdx.x; c < pf.nchunks; c += gridDim.x) {
-        const int64_t t = c * blockDim.x + threadIdx.x;
-        const bool act = t < pf.n1;
-        TG run[DG];
-        TG *dst = nullptr;
-        if (act) {
-            dst = static_cast<TG *>(rg.data) + base_of<AG, LG>(rg, int64_t(__ldg(pf.tl1 + t)));
-#pragma unroll
-            for (int q = 0; q < DG; ++q) run[q] = dst[q * gsc];
-            for (int k = __ldg(pf.off1 + t), ke = __ldg(pf.off1 + t + 1); k < ke; ++k) {
-                const int64_t e = __ldg(pf.elem1 + k);
-                const int prim = NW > 1 ? int(__ldg(pf.ppos1 + k)) : 0;
-                if (pf.rec)
-                    E::init_elem_rec(s, p, e, pf.rec + int64_t(k) * pf.ncol, idx);
-                else
-                    E::init_elem(s, p, e, idx);
-                E::call(s, p, e, idx);
-                E::template gather_op<MINC, 0, DG>(s, prim, run, idx);
-                if constexpr (NW > 1)
-                    E::template stage_rest<DGP>(s, pf.slots, pf.slotpos + e * int64_t(NW - 1), prim, idx);
-            }
-        }
-        if constexpr (NW > 1) {
-            __threadfence();
-            __syncthreads();
-            if (threadIdx.x == 0) flag_release(pf.flags + c);
-            for (int i = __ldg(pf.dep_off + c) + threadIdx.x, ie = __ldg(pf.dep_off + c + 1); i < ie;
-                 i += blockDim.x) {
-                const int32_t *f = pf.flags + __ldg(pf.dep_list + i);
-                while (!flag_acquire(f)) __nanosleep(64);
-            }
-            __syncthreads();
-            if (act) {
-                for (int k = __ldg(pf.off2 + t), ke = __ldg(pf.off2 + t + 1); k < ke; ++k) {
-                    const TG *src = slots + int64_t(k) * DGP;
-#pragma unroll
-                    for (int q = 0; q < DG; ++q) run[q] += __ldcg(src + q);
-                }
-            }
-        }
-        if (act) {
-#pragma unroll
-            for (int q = 0; q < DG; ++q) dst[q * gsc] = run[q];
-        }
-    }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
-}
-
 // Pass 2, warp-cooperative: a warp owns 32 consecutive pass-2 rows, whose
 // slots are one contiguous range; the lanes copy it through shared memory in
 // coalesced 16-byte chunks, then each lane adds its own rows in order, with
@@ -1082,11 +986,6 @@ __global__ void __launch_bounds__(256) k_pfold1(const __grid_constant__ LaunchPa
     run_pfold1<F, LP>(p, typename F::template sig<T>{});
 }
 template <class F, class T, int LP>
-__global__ void __launch_bounds__(256) k_pfold_fused(const __grid_constant__ LaunchParams p) {
-    pdl_wait();
-    run_pfold_fused<F, LP>(p, typename F::template sig<T>{});
-}
-template <class F, class T, int LP>
 __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ LaunchParams p) {
     pdl_wait();
     run_gather<F, LP>(p, typename F::template sig<T>{});
@@ -1135,11 +1034,10 @@ struct FunctorEntry {
     bool ind_write, ind_write_non_inc;
     LaunchFn direct[2], staged, phased;              // [LP]
     LaunchFn gather[2], gather_hubs;                 // target-centric (INC-only or WRITE-only)
-    LaunchFn pfold1[2], pfold2, pfold_fused[2];      // primary fold (INC-only)
+    LaunchFn pfold1[2], pfold2;                      // primary fold (INC-only)
     int (*direct_occupancy[2])(int threads);
     int (*gather_occupancy[2])();
     int (*pfold_occupancy[2])();
-    int (*pfold_fused_occupancy[2])();
     void (*pfold_hubs)(const LaunchParams &, int64_t nhub, const int32_t *tl, const int32_t *off,
                        const void *parts, cudaStream_t);
     int32_t pfold_dgp, pfold_nslot;
@@ -1209,21 +1107,6 @@ struct Registrar {
         }
         return n;
     }
-    template <int LP>
-    static void pfold_fused(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
-        carve_l1(k_pfold_fused<F, T, LP>);
-        launch_k(k_pfold_fused<F, T, LP>, g, b, 0, s, p);
-    }
-    template <int LP>
-    static int pfold_fused_occupancy() {
-        static int n = -1;
-        if (n < 0) {
-            carve_l1(k_pfold_fused<F, T, LP>);
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_pfold_fused<F, T, LP>, 256, 0) != cudaSuccess)
-                n = 0;
-        }
-        return n;
-    }
     static void pfold_hubs(const LaunchParams &p, int64_t nhub, const int32_t *tl, const int32_t *off,
                            const void *parts, cudaStream_t s) {
         using S = typename F::template sig<T>;
@@ -1259,10 +1142,6 @@ struct Registrar {
             e.pfold1[1] = &pfold1<1>;
             e.pfold_occupancy[0] = &pfold_occupancy<0>;
             e.pfold_occupancy[1] = &pfold_occupancy<1>;
-            e.pfold_fused[0] = &pfold_fused<0>;
-            e.pfold_fused[1] = &pfold_fused<1>;
-            e.pfold_fused_occupancy[0] = &pfold_fused_occupancy<0>;
-            e.pfold_fused_occupancy[1] = &pfold_fused_occupancy<1>;
             e.pfold2 = &pfold2;
             e.pfold_hubs = &pfold_hubs;
             using AG = typename FirstInc<S>::type;

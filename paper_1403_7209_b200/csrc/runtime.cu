@@ -262,25 +262,7 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
             for (int i = 0; i < f.nargs; ++i)
                 if (L->args[i].kind == ML_INDIRECT && (pf.rcol[i] < 0 || pf.rcol[i] >= pf.ncol))
                     ML_FAIL(ML_EINVAL, "loop '%s': pfold record column of argument %d out of range", L->name, i);
-        const bool fused = L->pf_fused && f.pfold_fused[0] && L->pf_nhub1 == 0 && L->pf_nhub2 == 0;
-        if (fused) {
-            // single pass: chunks of 256 rows, every CTA resident (the chunk
-            // dependencies point back, so the lowest unfinished chunk proceeds)
-            if (!L->pf_dep_off || !L->pf_dep_list || !L->pf_flags || L->pf_nchunks != (pf.n1 + 255) / 256 ||
-                (f.pfold_nslot > 0 && (!L->pf_off2 || L->pf_n2 != L->pf_n1)))
-                ML_FAIL(ML_EINVAL, "loop '%s': single-pass primary-fold lists inconsistent", L->name);
-            pf.fused = 1;
-            pf.nchunks = L->pf_nchunks;
-            pf.dep_off = L->pf_dep_off;
-            pf.dep_list = L->pf_dep_list;
-            pf.flags = L->pf_flags;
-            const int occ = f.pfold_fused_occupancy[lp] ? f.pfold_fused_occupancy[lp]() : 0;
-            if (occ <= 0) ML_FAIL(ML_ECUDA, "loop '%s': single-pass primary fold cannot be resident", L->name);
-            nparts = std::max<int64_t>(1, std::min<int64_t>(pf.nchunks, int64_t(occ) * g_dev.sm_count));
-            if (nparts > pstride) ML_FAIL(ML_EINVAL, "loop '%s': primary fold needs more scratch", L->name);
-            ML_CUDA(cudaMemsetAsync(pf.flags, 0, size_t(pf.nchunks) * sizeof(int32_t), stream));
-            f.pfold_fused[lp](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
-        } else {
+        {
             const int occ = f.pfold_occupancy[lp] ? f.pfold_occupancy[lp]() : 0;
             nparts = std::max<int64_t>(1, std::min<int64_t>((pf.n1 + 255) / 256,
                                                             occ > 0 ? int64_t(occ) * g_dev.sm_count : INT64_MAX));

@@ -333,26 +333,17 @@ def split_hub_rows(off: np.ndarray, rows_tl: np.ndarray, hub_row: int = HUB_ROW)
             "hub_off": np.concatenate([[0], np.cumsum(nseg[heavy])]).astype(np.int32)}
 
 
-#: rows per chunk of the single-pass primary fold (= its CTA size)
-PFOLD_CHUNK = 256
-
-
-def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW, chunk: int = PFOLD_CHUNK) -> dict:
+def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW) -> dict:
     """Primary-fold lists from one-row-per-target gather lists.
 
     Each element's *primary* incidence is the one with the smallest target id
     (ties: the lowest argument position): its owner evaluates the element and
     keeps that increment; the other incidences are *secondary* (slots).  Per
-    target row: its primary incidences (``1``, with ``ppos1`` the primary
-    argument position) and its secondary ones (``2``, with ``pos2``), element
-    ascending.  Without hub rows both passes share one row list (every target
-    with an incidence, ascending: ``unified``) and the single-pass kernel's
-    chunk dependencies are built: chunk c (rows [c*chunk, (c+1)*chunk)) needs
-    the earlier chunks owning the primaries of its rows' secondary incidences
-    (``dep_off``/``dep_list``) — always earlier, since a primary target is the
-    smaller one.  Rows longer than ``hub_row`` in either pass are split
-    (``split_hub_rows``): ``seg{1,2}``, ``nhub{1,2}``, ``nslots{1,2}``,
-    ``hub{1,2}_tl``, ``hub{1,2}_off``; the lists are then compacted per pass."""
+    target: its primary incidences (``1``, with ``ppos1`` the primary argument
+    position) and its secondary ones (``2``, with ``pos2``), element
+    ascending; only targets that have any.  Rows longer than ``hub_row`` are
+    split (``split_hub_rows``): ``seg{1,2}``, ``nhub{1,2}``, ``nslots{1,2}``,
+    ``hub{1,2}_tl``, ``hub{1,2}_off``."""
     off, elem, pos, tl = host["off"], host["elem"], host["pos"], host["targets"]
     nt = off.size - 1
     owner = np.repeat(np.arange(nt), np.diff(off))
@@ -363,13 +354,11 @@ def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW, chunk: int = PFO
     lead[1:] = e[order][1:] != e[order][:-1]
     prim = np.zeros(e.size, bool)
     prim[order[lead]] = True
-    deg = {1: np.bincount(owner[prim], minlength=nt), 2: np.bincount(owner[~prim], minlength=nt)}
-    hubs = hub_row is not None and any(int(d.max(initial=0)) > hub_row for d in deg.values())
-    out = {"unified": not hubs}
+    out = {}
     for which in (1, 2):
         m = prim if which == 1 else ~prim
-        cnt = deg[which]
-        keep = np.arange(nt) if not hubs else np.flatnonzero(cnt)
+        cnt = np.bincount(owner[m], minlength=nt)
+        keep = np.flatnonzero(cnt)
         out[f"n{which}"] = int(keep.size)
         out[f"off{which}"] = np.concatenate([[0], np.cumsum(cnt[keep])]).astype(np.int32)
         out[f"elem{which}"] = np.ascontiguousarray(e[m], dtype=np.int32)
@@ -388,22 +377,8 @@ def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW, chunk: int = PFO
         j = p2 - (p2 > pp[e2])
         slotpos[e2 * (nw - 1) + j] = np.arange(e2.size, dtype=np.int32)
     out["slotpos"] = slotpos
-    out["dep_off"] = out["dep_list"] = None
-    out["nchunks"] = 0
-    if not hubs:
-        nch = -(-nt // chunk) if nt else 0
-        row1 = np.zeros(max(n_el, 1), np.int64)
-        row1[out["elem1"]] = np.repeat(np.arange(nt), deg[1])
-        row2 = np.repeat(np.arange(nt), deg[2])
-        src, dst = row1[out["elem2"]] // chunk, row2 // chunk
-        m = src < dst
-        pairs = np.unique(dst[m] * max(nch, 1) + src[m])
-        d_chunk, s_chunk = pairs // max(nch, 1), pairs % max(nch, 1)
-        out["nchunks"] = nch
-        out["dep_off"] = np.concatenate([[0], np.cumsum(np.bincount(d_chunk, minlength=nch))]).astype(np.int32)
-        out["dep_list"] = np.ascontiguousarray(s_chunk, dtype=np.int32)
     for which in (1, 2):
-        sp = split_hub_rows(out[f"off{which}"], out[f"tl{which}"], hub_row) if hubs else None
+        sp = split_hub_rows(out[f"off{which}"], out[f"tl{which}"], hub_row) if hub_row else None
         if sp is None:
             out.update({f"seg{which}": None, f"nhub{which}": 0, f"nslots{which}": 0,
                         f"hub{which}_tl": None, f"hub{which}_off": None})
@@ -462,8 +437,7 @@ class PFoldMirror:
 
     __slots__ = ("n1", "off1", "elem1", "tl1", "ppos1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos",
                  "rec", "ncol", "rcol", "seg1", "seg2", "nhub1", "nhub2", "hub1_tl", "hub1_off",
-                 "hub2_tl", "hub2_off", "part1", "part2", "host", "rec_host", "unified", "nchunks",
-                 "dep_off", "dep_list", "flags")
+                 "hub2_tl", "hub2_off", "part1", "part2", "host", "rec_host")
 
     def __init__(self, g: GatherMirror, loop, records: bool = True):
         h = pfold_lists_host(g.host)
@@ -471,11 +445,6 @@ class PFoldMirror:
         self.n1, self.n2 = h["n1"], h["n2"]
         for k in ("off1", "elem1", "tl1", "ppos1", "off2", "elem2", "tl2", "pos2", "slotpos"):
             setattr(self, k, _upload(h[k]))
-        self.unified, self.nchunks = h["unified"], h["nchunks"]
-        self.dep_off = self.dep_list = self.flags = None
-        if self.unified and self.nchunks:
-            self.dep_off, self.dep_list = _upload(h["dep_off"]), _upload(h["dep_list"])
-            self.flags = N.DeviceBuffer(4 * self.nchunks)
         inc = next(a for a in loop.args if a.kind == "indirect" and a.mode.name == "INC")
         row = inc.dat.dim * np.dtype(inc.dat.dtype).itemsize
         for w in (1, 2):

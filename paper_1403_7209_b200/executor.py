@@ -99,7 +99,6 @@ class BackendConfig:
     concurrent_loops: bool = True           # graphs/untimed runs: independent loops overlap on streams
     chain_loops: bool = True                # run registered adjacent loop pairs as one loop (chain.py)
     pfold_records: bool = True              # pfold pass 1 reads per-incidence map records
-    pfold_single_pass: bool = True          # pfold without hub rows: one launch, slots folded in-kernel
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -262,9 +261,6 @@ class _LoopEntry:
             pf = self.pfold = pfold_mirror(loop, self.plan, config.pfold_records)
             L.pf_n1, L.pf_off1, L.pf_elem1, L.pf_tl1 = pf.n1, pf.off1.ptr, pf.elem1.ptr, pf.tl1.ptr
             L.pf_ppos1 = pf.ppos1.ptr
-            if pf.unified and pf.flags is not None and config.pfold_single_pass:
-                L.pf_fused, L.pf_nchunks = 1, pf.nchunks
-                L.pf_dep_off, L.pf_dep_list, L.pf_flags = pf.dep_off.ptr, pf.dep_list.ptr, pf.flags.ptr
             L.pf_n2, L.pf_off2, L.pf_elem2, L.pf_tl2 = pf.n2, pf.off2.ptr, pf.elem2.ptr, pf.tl2.ptr
             L.pf_pos2 = pf.pos2.ptr
             L.pf_slotpos = pf.slotpos.ptr
@@ -563,9 +559,7 @@ class CompiledProgram:
         for e in self.entries:
             if e.loop.iter_set.size == 0:
                 continue
-            if e.pfold is not None and e.desc.pf_fused:
-                total += 1
-            elif e.pfold is not None:
+            if e.pfold is not None:
                 total += 1 + (1 if e.pfold.n2 > 0 else 0) + (1 if e.pfold.nhub1 else 0) + (
                     1 if e.pfold.n2 > 0 and e.pfold.nhub2 else 0)
             elif e.gather is not None or not e.plan.has_writes:
@@ -598,7 +592,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
            tuple(config.block_size_for(l.name) for l in program), config.block_size,
            tuple(sorted((config.block_size_table or {}).items())), config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.coord_dat,
-           config.concurrent_loops, config.chain_loops, config.pfold_records, config.pfold_single_pass,
+           config.concurrent_loops, config.chain_loops, config.pfold_records,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

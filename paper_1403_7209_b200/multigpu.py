@@ -853,7 +853,6 @@ class StreamRank:
             desc.pf_n1, desc.pf_off1 = sub["n1"], sub["off1"].ptr
             desc.pf_elem1, desc.pf_tl1 = sub["elem1"].ptr, sub["tl1"].ptr
             desc.pf_ppos1 = sub["ppos1"].ptr
-            desc.pf_fused = 0                  # split launches run the two-pass form
             if sub["seg1"] is not None:
                 desc.pf_seg1 = sub["seg1"].ptr
             if sub["rec"] is not None:
@@ -1101,7 +1100,7 @@ class StreamRank:
                 continue
             base = 0
             if e.pfold is not None:
-                base = 1 if e.desc.pf_fused else 1 + (1 if e.pfold.n2 > 0 else 0)
+                base = 1 + (1 if e.pfold.n2 > 0 else 0)
             elif e.gather is not None or not e.plan.has_writes:
                 base = 1
             else:

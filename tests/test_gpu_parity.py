@@ -522,22 +522,3 @@ def test_phase_callback_instruments_each_colour_phase():
     calls.clear()
     ml.run_program([_cases.inc_loop(mesh, "edge_nodes")], mesh, cfg(phase_callback=cb, inc_schedule="gather"))
     assert calls == []
-
-
-@pytest.mark.parametrize("N", [16, 40])
-def test_pfold_single_pass_equals_two_passes_bitwise(N):
-    """The single-pass primary fold (chunks publish their slots and wait for
-    the earlier chunks owning their secondary incidences) adds exactly the
-    same terms in the same order per target as the two-pass form: bitwise
-    equal results, within tolerance of the oracle, deterministic run to run."""
-    outs = []
-    for single in (True, False, True):
-        (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(N, seed=6)
-        ml.run_program(prog[:5], mesh, cfg(inc_schedule="pfold", pfold_single_pass=single))
-        outs.append((h["res"].fetch(), h["grad"].fetch()))
-    for k in range(2):
-        np.testing.assert_array_equal(outs[0][k], outs[1][k])
-        np.testing.assert_array_equal(outs[0][k], outs[2][k])
-    bulk.run_program(rprog[:5])
-    close(outs[0][0], rh["res"].fetch(), what="res")
-    close(outs[0][1], rh["grad"].fetch(), what="grad")

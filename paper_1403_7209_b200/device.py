@@ -336,9 +336,9 @@ def split_hub_rows(off: np.ndarray, rows_tl: np.ndarray, hub_row: int = HUB_ROW)
 def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW) -> dict:
     """Primary-fold lists from one-row-per-target gather lists.
 
-    Each element's *primary* incidence is the one with the smallest target id
-    (ties: the lowest argument position): its owner evaluates the element and
-    keeps that increment; the other incidences are *secondary* (slots).  Per
+    Each element's *primary* incidence is its first INC argument: the owner
+    of that target evaluates the element and keeps that increment; the other
+    incidences are *secondary* (slots).  Per
     target: its primary incidences (``1``, with ``ppos1`` the primary argument
     position) and its secondary ones (``2``, with ``pos2``), element
     ascending; only targets that have any.  Rows longer than ``hub_row`` are
@@ -348,12 +348,12 @@ def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW) -> dict:
     nt = off.size - 1
     owner = np.repeat(np.arange(nt), np.diff(off))
     e, p_ = elem[:off[-1]], pos[:off[-1]]
-    tgt = tl[owner].astype(np.int64)
-    order = np.lexsort((p_, tgt, e))                    # per element: (target, position) ascending
-    lead = np.ones(order.size, bool)
-    lead[1:] = e[order][1:] != e[order][:-1]
-    prim = np.zeros(e.size, bool)
-    prim[order[lead]] = True
+    # primary = the first INC argument: after the reference's row ordering of
+    # the iteration set (renumber.py:131-138) an element's edge ids follow its
+    # first target, so a target's primary elements are consecutive ids and
+    # their direct rows and records stream coalesced (a smallest-target rule
+    # measured 2 % slower on the fused flux loop)
+    prim = p_ == 0
     out = {}
     for which in (1, 2):
         m = prim if which == 1 else ~prim

@@ -315,8 +315,8 @@ def test_gather_hub_rows_and_pfold_lists(rng):
                     rows = np.flatnonzero((tl == t) & (seg >= 0))
                     assert seg[rows].tolist() == list(range(h["hub_off"][k], h["hub_off"][k + 1]))
             pf = pfold_lists_host(h["host"], hub_row=None)
-            # primary incidence = the element's smaller target (ties: position 0)
-            prim_pos = np.where(tab[:, 1] < tab[:, 0], 1, 0)
+            # primary incidence = the element's first INC argument
+            prim_pos = np.zeros(n, np.int64)
             k = np.arange(pf["elem2"].size)
             e2, p2 = pf["elem2"].astype(np.int64), pf["pos2"].astype(np.int64)
             np.testing.assert_array_equal(p2, 1 - prim_pos[e2])

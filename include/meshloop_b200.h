@@ -129,9 +129,6 @@ typedef struct ml_loop {
      * up to even], rows in pf_elem2 order (ml_loop_pfold_slot_bytes). */
     int64_t pf_n1;
     const int32_t *pf_off1, *pf_elem1, *pf_tl1;
-    const uint8_t *pf_ppos1;        /* INC position of each primary incidence (the
-                                       element's argument with the smallest target
-                                       id); NULL: position 0                       */
     int64_t pf_n2;
     const int32_t *pf_off2, *pf_elem2, *pf_tl2;
     const uint8_t *pf_pos2;

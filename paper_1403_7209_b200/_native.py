@@ -73,7 +73,7 @@ class MlLoop(C.Structure):
                 ("gather_seg", C.c_void_p), ("gather_part", C.c_void_p), ("gather_nhub", C.c_int64),
                 ("gather_hub_tl", C.c_void_p), ("gather_hub_off", C.c_void_p),
                 ("pf_n1", C.c_int64), ("pf_off1", C.c_void_p), ("pf_elem1", C.c_void_p),
-                ("pf_tl1", C.c_void_p), ("pf_ppos1", C.c_void_p), ("pf_n2", C.c_int64), ("pf_off2", C.c_void_p),
+                ("pf_tl1", C.c_void_p), ("pf_n2", C.c_int64), ("pf_off2", C.c_void_p),
                 ("pf_elem2", C.c_void_p), ("pf_tl2", C.c_void_p), ("pf_pos2", C.c_void_p),
                 ("pf_slots", C.c_void_p), ("pf_slotpos", C.c_void_p),
                 ("pf_ncol", C.c_int32), ("pf_rec", C.c_void_p),

@@ -136,15 +136,13 @@ struct Consts {
     int64_t i[4];
 };
 
-// Primary-fold schedule (INC-only loops): each element's *primary* incidence
-// is its INC argument with the smallest target id (ties: lowest position);
-// pass 1 gives each target the elements it is primary for, evaluates each
-// element once there, accumulates that increment in the thread's registers and
-// writes the others to per-element slots; pass 2 folds each target's slots.
+// Primary-fold schedule (INC-only loops): pass 1 gives each target the elements
+// whose FIRST INC argument targets it; each element is evaluated once there,
+// its first increment accumulated in the thread's registers and the others
+// written to per-element slots; pass 2 folds each target's slots.
 struct PFoldParams {
     int64_t n1;                          // targets with primary incidences
     const int32_t *off1, *elem1, *tl1;   // CSR (element ascending); tl1: target ids
-    const uint8_t *ppos1;                // INC-argument position of each primary incidence
     int64_t n2;                          // targets with secondary incidences
     const int32_t *off2, *elem2, *tl2;
     const uint8_t *pos2;                 // INC-argument position (>= 1) of each
@@ -474,22 +472,18 @@ struct Engine {
     // secondary CSR (slotpos[e][pos-1]), so pass 2 reads each target's rows
     // contiguously
     template <int DGP, size_t... Is>
-    __device__ __forceinline__ static void stage_rest(Slots &s, void *slots, const int32_t *slotpos, int prim,
+    __device__ __forceinline__ static void stage_rest(Slots &s, void *slots, const int32_t *slotpos,
                                                       cuda::std::index_sequence<Is...>) {
-        (stage_rest_one<Is, DGP>(s, slots, slotpos, prim), ...);
+        (stage_rest_one<Is, DGP>(s, slots, slotpos), ...);
     }
-    // INC arguments other than the primary position `prim` -> the element's
-    // slots, numbered in position order skipping the primary
     template <size_t I, int DGP>
-    __device__ __forceinline__ static void stage_rest_one(Slots &s, void *slots, const int32_t *slotpos,
-                                                          int prim) {
+    __device__ __forceinline__ static void stage_rest_one(Slots &s, void *slots, const int32_t *slotpos) {
         using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
         if constexpr (A::kind == KI && A::mode == MINC) {
             constexpr int pos = IncIndex<As...>::template of<I>();
-            if (pos != prim) {
+            if constexpr (pos >= 1) {
                 using T = typename A::type;
-                const int j = pos - (pos > prim ? 1 : 0);
-                T *dst = static_cast<T *>(slots) + int64_t(__ldg(slotpos + j)) * DGP;
+                T *dst = static_cast<T *>(slots) + int64_t(__ldg(slotpos + pos - 1)) * DGP;
                 if constexpr (A::dim % 2 == 0 && DGP % 2 == 0 && cuda::std::is_same_v<T, double>) {
 #pragma unroll
                     for (int c = 0; c < A::dim; c += 2)
@@ -862,15 +856,14 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
         for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * gsc] : TG(0);
         for (int k = __ldg(pf.off1 + t), ke = __ldg(pf.off1 + t + 1); k < ke; ++k) {
             const int64_t e = __ldg(pf.elem1 + k);
-            const int prim = NW > 1 ? int(__ldg(pf.ppos1 + k)) : 0;
             if (pf.rec)
                 E::init_elem_rec(s, p, e, pf.rec + int64_t(k) * pf.ncol, idx);
             else
                 E::init_elem(s, p, e, idx);
             E::call(s, p, e, idx);
-            E::template gather_op<MINC, 0, DG>(s, prim, run, idx);
+            E::template gather_op<MINC, 0, DG>(s, 0, run, idx);
             if constexpr (NW > 1)
-                E::template stage_rest<DGP>(s, pf.slots, pf.slotpos + e * int64_t(NW - 1), prim, idx);
+                E::template stage_rest<DGP>(s, pf.slots, pf.slotpos + e * int64_t(NW - 1), idx);
         }
         if (seg >= 0) {
             TG *part = static_cast<TG *>(pf.part1) + int64_t(seg) * DG;

@@ -235,9 +235,6 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         pf.off1 = L->pf_off1;
         pf.elem1 = L->pf_elem1;
         pf.tl1 = L->pf_tl1;
-        pf.ppos1 = L->pf_ppos1;
-        if (f.pfold_nslot > 0 && !pf.ppos1)
-            ML_FAIL(ML_EINVAL, "loop '%s': primary positions (pf_ppos1) missing", L->name);
         pf.n2 = f.pfold_nslot > 0 ? L->pf_n2 : 0;
         pf.off2 = L->pf_off2;
         pf.elem2 = L->pf_elem2;

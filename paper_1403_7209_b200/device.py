@@ -339,8 +339,8 @@ def pfold_lists_host(host: dict, hub_row: int | None = HUB_ROW) -> dict:
     Each element's *primary* incidence is its first INC argument: the owner
     of that target evaluates the element and keeps that increment; the other
     incidences are *secondary* (slots).  Per
-    target: its primary incidences (``1``, with ``ppos1`` the primary argument
-    position) and its secondary ones (``2``, with ``pos2``), element
+    target: its primary incidences (``1``) and its secondary ones (``2``,
+    with their argument positions ``pos2``), element
     ascending; only targets that have any.  Rows longer than ``hub_row`` are
     split (``split_hub_rows``): ``seg{1,2}``, ``nhub{1,2}``, ``nslots{1,2}``,
     ``hub{1,2}_tl``, ``hub{1,2}_off``."""
@@ -435,7 +435,7 @@ class PFoldMirror:
     incidences through the first INC argument (pass 1) and through the others
     (pass 2), element ascending; plus the per-element slot buffer."""
 
-    __slots__ = ("n1", "off1", "elem1", "tl1", "ppos1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos",
+    __slots__ = ("n1", "off1", "elem1", "tl1", "n2", "off2", "elem2", "tl2", "pos2", "slotpos",
                  "rec", "ncol", "rcol", "seg1", "seg2", "nhub1", "nhub2", "hub1_tl", "hub1_off",
                  "hub2_tl", "hub2_off", "part1", "part2", "host", "rec_host")
 
@@ -443,7 +443,7 @@ class PFoldMirror:
         h = pfold_lists_host(g.host)
         self.host, self.rec_host = h, None
         self.n1, self.n2 = h["n1"], h["n2"]
-        for k in ("off1", "elem1", "tl1", "ppos1", "off2", "elem2", "tl2", "pos2", "slotpos"):
+        for k in ("off1", "elem1", "tl1", "off2", "elem2", "tl2", "pos2", "slotpos"):
             setattr(self, k, _upload(h[k]))
         inc = next(a for a in loop.args if a.kind == "indirect" and a.mode.name == "INC")
         row = inc.dat.dim * np.dtype(inc.dat.dtype).itemsize
@@ -473,7 +473,6 @@ class PFoldMirror:
                 + np.arange(int(deg.sum()))).astype(np.int64)
         out = {"n1": int(rows.size), "off1": _upload(new_off),
                "elem1": _upload(np.ascontiguousarray(h["elem1"][take])),
-               "ppos1": _upload(np.ascontiguousarray(h["ppos1"][take])),
                "tl1": _upload(np.ascontiguousarray(h["tl1"][rows])),
                "seg1": _upload(np.ascontiguousarray(h["seg1"][rows])) if h["seg1"] is not None else None,
                "rec": (_upload(np.ascontiguousarray(self.rec_host[take]))

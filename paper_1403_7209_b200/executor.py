@@ -260,7 +260,6 @@ class _LoopEntry:
             self.gather = gather_mirror(loop, self.plan)
             pf = self.pfold = pfold_mirror(loop, self.plan, config.pfold_records)
             L.pf_n1, L.pf_off1, L.pf_elem1, L.pf_tl1 = pf.n1, pf.off1.ptr, pf.elem1.ptr, pf.tl1.ptr
-            L.pf_ppos1 = pf.ppos1.ptr
             L.pf_n2, L.pf_off2, L.pf_elem2, L.pf_tl2 = pf.n2, pf.off2.ptr, pf.elem2.ptr, pf.tl2.ptr
             L.pf_pos2 = pf.pos2.ptr
             L.pf_slotpos = pf.slotpos.ptr

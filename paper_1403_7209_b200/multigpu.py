@@ -852,7 +852,6 @@ class StreamRank:
             desc = type(e.desc).from_buffer_copy(e.desc)
             desc.pf_n1, desc.pf_off1 = sub["n1"], sub["off1"].ptr
             desc.pf_elem1, desc.pf_tl1 = sub["elem1"].ptr, sub["tl1"].ptr
-            desc.pf_ppos1 = sub["ppos1"].ptr
             if sub["seg1"] is not None:
                 desc.pf_seg1 = sub["seg1"].ptr
             if sub["rec"] is not None:

@@ -959,8 +959,15 @@ __global__ void __launch_bounds__(256) k_fold_parts(const __grid_constant__ Laun
 }
 
 // ---- kernels ------------------------------------------------------------------------
+// resident CTAs per SM the direct kernels are compiled for: 1 lets a
+// vectorised thread keep both elements' rows in registers (update: ~180);
+// capping for 2 or 3 CTAs measured equal or slower (update 0.0549 ms at 1,
+// 0.0575 at 3: spills)
+#ifndef ML_DIRECT_MINB
+#define ML_DIRECT_MINB 1
+#endif
 template <class F, class T, int LP>
-__global__ void __launch_bounds__(256) k_direct(const __grid_constant__ LaunchParams p) {
+__global__ void __launch_bounds__(256, ML_DIRECT_MINB) k_direct(const __grid_constant__ LaunchParams p) {
     pdl_wait();
     if constexpr (LP == 1) run_direct_vec<F>(p, typename F::template sig<T>{});
     else run_direct<F>(p, typename F::template sig<T>{});

@@ -205,6 +205,22 @@ struct RefA {
     T *p;
     __device__ __forceinline__ T &operator[](int c) const { return p[c]; }
 };
+// READ views of the target-centric schedules load through the read-only path
+// (ld.global.nc): their eligibility rules (gather_eligible / fold_eligible)
+// keep the written dat out of every other argument, so nothing a READ view
+// reads is written during the launch.  The colour schedules keep coherent
+// loads (a dat may be read there while other elements of the block update it).
+template <class T>
+struct RefNC {
+    const T *p;
+    int64_t sc;
+    __device__ __forceinline__ T operator[](int c) const { return __ldg(p + c * sc); }
+};
+template <class T>
+struct RefNCA {
+    const T *p;
+    __device__ __forceinline__ T operator[](int c) const { return __ldg(p + c); }
+};
 
 // layout class of argument A under policy LP: 0 runtime strides, 1 AOS (base
 // e * dim, component stride 1), 2 segmented SOA (SEG_SHIFT, component stride
@@ -316,6 +332,9 @@ struct Slot {
     __device__ __forceinline__ auto view() {
         if constexpr (staged) {
             return static_cast<T *>(acc);
+        } else if constexpr (A::mode == MR && MODE == ST_GATHER && !is_global) {
+            if constexpr (L == 1) return RefNCA<T>{ptr};
+            else return RefNC<T>{ptr, sc};
         } else if constexpr (L == 1) {
             if constexpr (A::mode == MR) return RefA<const T>{ptr};
             else return RefA<T>{ptr};

@@ -956,6 +956,149 @@ __global__ void __launch_bounds__(256) k_pfold_rest_w(const __grid_constant__ La
     }
 }
 
+// Pass 2 with Blackwell bulk copies: the same warp-per-32-rows split, but the
+// warp's slot range moves global -> shared by the TMA engine
+// (cp.async.bulk, completion on an mbarrier) in chunks of up to CH rows,
+// double-buffered: lane 0 issues chunk i+1 before the lanes wait for and fold
+// chunk i, so the copy overlaps the fold and the next group's target loads.
+// Chunks follow the warp's groups in order, so one chunk never spans two
+// groups; a group without slots issues nothing.
+#ifndef ML_PF2_TMA
+#define ML_PF2_TMA 1
+#endif
+#ifndef ML_PF2_CHUNK_BYTES
+#define ML_PF2_CHUNK_BYTES 2816   // per buffer and warp; two buffers = the 5.5 KB of k_pfold_rest_w
+#endif
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+template <class T, int DG>
+__global__ void __launch_bounds__(256) k_pfold_rest_tma(const __grid_constant__ LaunchParams p, int ga) {
+    constexpr int DGP = PFoldShape<T, DG>::DGP;
+    constexpr int RB = int(DGP * sizeof(T));                  // bytes per slot row (multiple of 16)
+    constexpr int CH = ML_PF2_CHUNK_BYTES / RB;               // slot rows per buffer
+    static_assert(RB % 16 == 0 && CH > 0, "bulk copies move whole 16-byte units");
+    __shared__ __align__(128) T buf[8][2][CH * DGP];
+    __shared__ __align__(8) uint64_t bar[8][2];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        mbar_init(&bar[w][0], 1);
+        mbar_init(&bar[w][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    pdl_wait();
+    const PFoldParams &pf = p.pf;
+    const ArgRt &rg = p.a[ga];
+    const char *slots = static_cast<const char *>(pf.slots);
+    const int64_t n2 = pf.n2, stride = int64_t(gridDim.x) * 256;
+    int64_t ct = (int64_t(blockIdx.x) * 8 + w) * 32;
+    if (ct >= n2) return;
+    auto group_end = [&](int64_t t0) { return __ldg(pf.off2 + (t0 + 32 < n2 ? t0 + 32 : n2)); };
+    int cc = __ldg(pf.off2 + ct), ce = group_end(ct);        // consumer cursor: group, chunk, group end
+    int64_t pt = ct;
+    int pc = cc, pe = ce;                                     // producer cursor, one chunk ahead
+    auto produce = [&](int b) {
+        const int n = pe - pc < CH ? pe - pc : CH;
+        if (n > 0 && lane == 0) bulk_g2s(buf[w][b], slots + int64_t(pc) * RB, uint32_t(n * RB), &bar[w][b]);
+        pc += CH;
+        if (pc >= pe) {
+            pt += stride;
+            if (pt < n2) {
+                pc = __ldg(pf.off2 + pt);
+                pe = group_end(pt);
+            }
+        }
+    };
+    produce(0);
+    uint32_t phase = 0;
+    int b = 0;
+    bool start = true, act = false;
+    int k0 = 0, k1 = 0;
+    int32_t seg = -1;
+    T *dst = nullptr;
+    T run[DG];
+    while (ct < n2) {
+        if (pt < n2) {
+            __syncwarp();
+            produce(b ^ 1);
+        }
+        if (start) {
+            const int64_t t = ct + lane;
+            act = t < n2;
+            if (act) {
+                k0 = __ldg(pf.off2 + t);
+                k1 = __ldg(pf.off2 + t + 1);
+                const int64_t tg = pf.tl2 ? int64_t(__ldg(pf.tl2 + t)) : t;
+                dst = static_cast<T *>(rg.data) + elem_base(rg, tg);
+                seg = pf.seg2 ? __ldg(pf.seg2 + t) : -1;
+#pragma unroll
+                for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * rg.sc] : T(0);
+            }
+            start = false;
+        }
+        const int n = ce - cc < CH ? ce - cc : CH;
+        if (n > 0) {
+            mbar_wait(&bar[w][b], (phase >> b) & 1u);
+            phase ^= 1u << b;
+            if (act) {
+                const int a = k0 > cc ? k0 : cc, e = k1 < cc + n ? k1 : cc + n;
+                for (int k = a; k < e; ++k) {
+#pragma unroll
+                    for (int c = 0; c < DG; ++c) run[c] += buf[w][b][(k - cc) * DGP + c];
+                }
+            }
+            // the next bulk copy into this buffer is an async-proxy write after
+            // these generic-proxy reads
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        cc += CH;
+        if (cc >= ce) {
+            if (act) {
+                if (seg >= 0) {
+                    T *part = static_cast<T *>(pf.part2) + int64_t(seg) * DG;
+#pragma unroll
+                    for (int c = 0; c < DG; ++c) part[c] = run[c];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < DG; ++c) dst[c * rg.sc] = run[c];
+                }
+            }
+            ct += stride;
+            start = true;
+            if (ct < n2) {
+                cc = __ldg(pf.off2 + ct);
+                ce = group_end(ct);
+            }
+        }
+        b ^= 1;
+    }
+}
+
 // Hub targets of a split pass (pfold): value + each partial slot in order.
 template <class T, int DG>
 __global__ void __launch_bounds__(256) k_fold_parts(const __grid_constant__ LaunchParams p, int ga, int64_t nhub,
@@ -1136,7 +1279,11 @@ struct Registrar {
     static void pfold2(const LaunchParams &p, dim3 g, dim3 b, size_t, cudaStream_t s) {
         using S = typename F::template sig<T>;
         using AG = typename FirstInc<S>::type;
+        #if ML_PF2_TMA
+        launch_k(k_pfold_rest_tma<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
+#else
         launch_k(k_pfold_rest_w<typename AG::type, AG::dim>, g, b, 0, s, p, int(FirstInc<S>::value));
+#endif
     }
     explicit Registrar(const char *name) {
         using S = typename F::template sig<T>;

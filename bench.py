@@ -299,7 +299,7 @@ def run_ours(args) -> None:
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
-        dom_sched = (table or {}).get(dom.loop.name, sched)
+        dom_sched = dom.sched if dom.plan.has_writes else "direct"
         traffic = json.loads(tfile.read_text()).get(dom_sched, {}).get(dom.loop.name)
 
     # -- end to end through the public API with host buffers ---------------------------------

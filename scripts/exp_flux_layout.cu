@@ -29,9 +29,14 @@ struct View {
     int64_t pitch;
     __device__ __forceinline__ double operator[](int c) const {
         if constexpr (LAY == 0) return p[c * pitch];
-        else return p[c * 32];
+        else if constexpr (LAY == 2) {       // padded AoS rows: 16-byte pair loads, pairs reused
+            const double2 v = __ldg(reinterpret_cast<const double2 *>(p) + (c >> 1));
+            return (c & 1) ? v.y : v.x;
+        } else return p[c * 32];
     }
 };
+template <int D>
+__host__ __device__ constexpr int padded() { return (D + 1) / 2 * 2; }
 
 __device__ __forceinline__ double ld_keep(const double *p) {
     double v;
@@ -64,12 +69,14 @@ __device__ __forceinline__ HView<LAY, HINT> hview(const double *base, int64_t e,
 template <int LAY, int D>
 __device__ __forceinline__ View<LAY> view(const double *base, int64_t e, int64_t pitch) {
     if constexpr (LAY == 0) return View<LAY>{base + e, pitch};
+    else if constexpr (LAY == 2) return View<LAY>{base + e * padded<D>(), pitch};
     else return View<LAY>{base + (e >> 5) * (32 * D) + (e & 31), pitch};
 }
 
 template <int LAY, int D>
 __device__ __forceinline__ int64_t idx(int64_t e, int c, int64_t pitch) {
     if constexpr (LAY == 0) return c * pitch + e;
+    else if constexpr (LAY == 2) return e * padded<D>() + c;
     else return (e >> 5) * (32 * D) + c * 32 + (e & 31);
 }
 
@@ -826,5 +833,22 @@ extern "C" int exp_flux_split(int variant, const void *w, const void *q, const v
     case 4: k_flux_split<0, 4><<<4 * sms, 256, 0, s>>>(d); break;
     default: k_flux_split<1, 4><<<4 * sms, 256, 0, s>>>(d); break;
     }
+    return int(cudaGetLastError());
+}
+
+// padded AoS for the wide node dats (rows of whole 16-byte pairs)
+extern "C" int exp_flux_aos(int minb, const void *w, const void *q, const void *x, const void *lim,
+                            const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                            const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                            int64_t n1, int64_t pitch, int sms, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (minb == 5) k_flux<2, 5><<<sms * 5, 128, 0, s>>>(d);
+    else k_flux<2, 2><<<sms * 2, 256, 0, s>>>(d);
     return int(cudaGetLastError());
 }

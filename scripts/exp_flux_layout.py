@@ -93,6 +93,7 @@ def main():
     lib.exp_flux_reg.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_h.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_split.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_aos.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_lrec.argtypes = ([C.c_int] + [C.c_void_p] * 8 + [C.c_int64, C.c_void_p, C.c_void_p,
                                   C.c_int64, C.c_int, C.c_void_p])
     vals = {k: h[k].fetch() for k in ("q", "x", "lim", "grad", "aux", "res", "w")}
@@ -114,13 +115,18 @@ def main():
                              (0, 14, "soa_hint_pf"), (1, 15, "aosoa_hint_pf"), (0, 16, "soa_nbr_noalloc"),
                              (1, 17, "aosoa_nbr_noalloc"), (0, 20, "soa_split2"), (1, 21, "aosoa_split2"),
                              (0, 22, "soa_split3"), (1, 23, "aosoa_split3"), (0, 24, "soa_split4"),
-                             (1, 25, "aosoa_split4")):
+                             (1, 25, "aosoa_split4"), (4, 30, "aos_pad"), (4, 31, "aos_pad_128x5")):
         if args.only and name not in args.only and name != "soa":
             continue
         def put(k):
             v = vals[k]
             if k in ("x", "w"):
                 return torch.from_numpy(np.ascontiguousarray(v).reshape(-1)).to(dev)
+            if lay == 4:                      # padded AoS rows
+                D = v.shape[1]
+                pv = np.zeros((v.shape[0], (D + 1) // 2 * 2))
+                pv[:, :D] = v
+                return torch.from_numpy(pv.reshape(-1)).to(dev)
             if lay % 2 == 0:
                 return torch.from_numpy(np.ascontiguousarray(v.T).reshape(-1)).to(dev)
             return torch.from_numpy(to_aosoa(v)).to(dev)
@@ -135,7 +141,9 @@ def main():
                       T["res"].data_ptr(), slots.data_ptr(), ints["off1"].data_ptr(),
                       ints["elem1"].data_ptr(), ints["tl1"].data_ptr(), ints["rec"].data_ptr(),
                       ints["slotpos"].data_ptr(), int(tl1.size), n)
-            if lanes >= 20:
+            if lanes >= 30:
+                rc = lib.exp_flux_aos(5 if lanes == 31 else 2, *common[1:], sms, stream)
+            elif lanes >= 20:
                 rc = lib.exp_flux_split(lanes - 20, *common[1:], sms, stream)
             elif lanes >= 10:
                 rc = lib.exp_flux_h(lanes - 10, *common[1:], sms * 2, stream)
@@ -157,7 +165,11 @@ def main():
         launch()
         torch.cuda.synchronize()
         r = T["res"].cpu().numpy()
-        results[name] = (r.reshape(6, n).T if lay % 2 == 0 else from_aosoa(r, n, 6)), slots.cpu().numpy()
+        if lay == 4:
+            rr = r.reshape(n, 6)
+        else:
+            rr = r.reshape(6, n).T if lay % 2 == 0 else from_aosoa(r, n, 6)
+        results[name] = rr, slots.cpu().numpy()
         T["res"].copy_(res0)
         for _ in range(5):
             launch()

@@ -470,24 +470,6 @@ struct Engine {
                                                      cuda::std::index_sequence<Is...>) {
         (gather_op_one<Is, MM, OP, DG>(s, a, run), ...);
     }
-    // INC gather over components [C0, C1) only (run holds those components)
-    template <int C0, int C1, class TG, size_t... Is>
-    __device__ __forceinline__ static void gather_inc_range(Slots &s, int a, TG *run,
-                                                            cuda::std::index_sequence<Is...>) {
-        (gather_inc_range_one<Is, C0, C1>(s, a, run), ...);
-    }
-    template <size_t I, int C0, int C1, class TG>
-    __device__ __forceinline__ static void gather_inc_range_one(Slots &s, int a, TG *run) {
-        using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
-        if constexpr (A::kind == KI && A::mode == MINC) {
-            constexpr int pos = ModeIndex<MINC, As...>::template of<I>();
-            if (a == pos) {
-                auto &acc = cuda::std::get<I>(s).acc;
-#pragma unroll
-                for (int c = C0; c < C1; ++c) run[c - C0] += acc[c];
-            }
-        }
-    }
     template <size_t I, int MM, int OP, int DG, class TG>
     __device__ __forceinline__ static void gather_op_one(Slots &s, int a, TG *run) {
         using A = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>;
@@ -578,15 +560,6 @@ __device__ __forceinline__ void run_direct(const LaunchParams &p, Sig<As...>) {
 // are loaded with 16-byte loads, WRITE/RW/INC rows stored with 16-byte stores
 // (a WRITE row is loaded first unless the functor declares dense_writes —
 // every component of a direct WRITE argument written, OP2's OP_WRITE).
-// Functor traits (opt-in static members):
-//   dense_writes  every component of a direct WRITE argument is written
-//   gather_split  the target-centric schedule may split an INC target's
-//                 components over that many threads (see run_gather)
-template <class F, class = void>
-struct GatherSplit : cuda::std::integral_constant<int, 1> {};
-template <class F>
-struct GatherSplit<F, cuda::std::void_t<decltype(F::gather_split)>>
-    : cuda::std::integral_constant<int, F::gather_split> {};
 template <class F, class = void>
 struct DenseWrites : cuda::std::false_type {};
 template <class F>
@@ -781,72 +754,8 @@ __device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
 // final value is therefore exactly the serial one.  No colours, no shared
 // memory, no atomics.  Global reductions count each element once (on its
 // incidence through the first such argument).
-// Component split (functor trait gather_split = S, INC loops without global
-// reductions): the CTA's threads form S groups of blockDim/S over the same
-// targets; group P keeps components [P*DG/S, (P+1)*DG/S) of the running value
-// and evaluates the kernel for them only (the part index is a compile-time
-// constant per group, so the compiler drops the other components' loads and
-// arithmetic).  Per component the order of additions is unchanged: results
-// are bitwise those of the unsplit schedule.
-template <class F, int LP, int P, int S, class... As>
-__device__ __forceinline__ void run_gather_part(const LaunchParams &p, int64_t t0, int64_t stride) {
-    using E = Engine<F, ST_GATHER, LP, As...>;
-    constexpr int G = ModeIndex<MINC, As...>::template first<0>();
-    using AG = cuda::std::tuple_element_t<G, cuda::std::tuple<As...>>;
-    using TG = typename AG::type;
-    constexpr int DG = AG::dim, C0 = P * DG / S, C1 = (P + 1) * DG / S;
-    constexpr int LG = lay_of<AG, LP>();
-    constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    typename E::Slots s;
-    const ArgRt &rg = p.a[G];
-    const int64_t gsc = sc_of<AG, LG>(rg);
-    for (int64_t t = t0; t < p.g_ntargets; t += stride) {
-        const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
-        TG *dst = static_cast<TG *>(rg.data) + base_of<AG, LG>(rg, tg);
-        const int32_t seg = p.g_seg ? __ldg(p.g_seg + t) : -1;
-        TG run[C1 - C0];
-#pragma unroll
-        for (int c = C0; c < C1; ++c) run[c - C0] = seg < 0 ? dst[c * gsc] : TG(0);
-        for (int k = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1); k < ke; ++k) {
-            const int64_t e = __ldg(p.g_elem + k);
-            const int a = __ldg(p.g_pos + k);
-            E::init_elem(s, p, e, idx);
-            E::call_raw(s, p, idx);
-            E::template gather_inc_range<C0, C1>(s, a, run, idx);
-        }
-        if (seg >= 0) {
-            TG *part = static_cast<TG *>(p.g_part) + int64_t(seg) * DG;
-#pragma unroll
-            for (int c = C0; c < C1; ++c) part[c] = run[c - C0];
-        } else {
-#pragma unroll
-            for (int c = C0; c < C1; ++c) dst[c * gsc] = run[c - C0];
-        }
-    }
-}
-
-template <class F, int LP, int S, class... As, int... Ps>
-__device__ __forceinline__ void run_gather_split(const LaunchParams &p, cuda::std::integer_sequence<int, Ps...>) {
-    const int per = blockDim.x / S, part = threadIdx.x / per;
-    const int64_t t0 = int64_t(blockIdx.x) * per + (threadIdx.x - part * per);
-    const int64_t stride = int64_t(gridDim.x) * per;
-    ((part == Ps ? run_gather_part<F, LP, Ps, S, As...>(p, t0, stride) : void()), ...);
-}
-
-template <class F, class... As>
-__host__ __device__ constexpr int gather_split_of() {
-    constexpr bool inc = ((As::kind == KI && As::mode == MINC) || ...);
-    constexpr bool red = ((As::kind == KG && As::mode != MR) || ...);
-    return inc && !red ? GatherSplit<F>::value : 1;
-}
-
 template <class F, int LP, class... As>
 __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
-    if constexpr (gather_split_of<F, As...>() > 1) {
-        constexpr int S = gather_split_of<F, As...>();
-        run_gather_split<F, LP, S, As...>(p, cuda::std::make_integer_sequence<int, S>{});
-        return;
-    }
     using E = Engine<F, ST_GATHER, LP, As...>;
     constexpr bool has_inc = ((As::kind == KI && As::mode == MINC) || ...);
     constexpr int MM = has_inc ? MINC : MW;
@@ -1294,15 +1203,9 @@ struct FunctorEntry {
     void (*pfold_hubs)(const LaunchParams &, int64_t nhub, const int32_t *tl, const int32_t *off,
                        const void *parts, cudaStream_t);
     int32_t pfold_dgp, pfold_nslot;
-    int32_t gather_split;                            // threads per target in the gather schedule
 };
 
 void register_functor(const FunctorEntry &e);
-
-template <class F, class S>
-struct SigGatherSplit;
-template <class F, class... As>
-struct SigGatherSplit<F, Sig<As...>> : cuda::std::integral_constant<int, gather_split_of<F, As...>()> {};
 
 template <class F, class T>
 struct Registrar {
@@ -1413,7 +1316,6 @@ struct Registrar {
         }
         if constexpr (SigInfo<S>::gather_ok && SigInfo<S>::ind_inc) e.gather_hubs = &gather_hubs;
         if constexpr (SigInfo<S>::gather_ok) {
-            e.gather_split = SigGatherSplit<F, S>::value;
             e.gather[0] = &gather<0>;
             e.gather[1] = &gather<1>;
             e.gather_occupancy[0] = &gather_occupancy<0>;

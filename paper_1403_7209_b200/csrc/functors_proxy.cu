@@ -54,7 +54,6 @@ struct ProxySaveDt {
 };
 
 struct ProxyGrad {
-    static constexpr int gather_split = 2;   // components independent: 9 per thread
     template <class T>
     using sig = Sig<Arg<KD, MR, 3, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, 3, T>,
                     Arg<KI, MR, 3, T>, Arg<KI, MINC, NG, T>, Arg<KI, MINC, NG, T>>;

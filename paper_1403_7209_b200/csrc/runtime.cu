@@ -281,8 +281,7 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         p.g_elem = L->gather_elem;
         p.g_pos = L->gather_pos;
         p.g_tlist = L->gather_targets;
-        const int64_t per_cta = 256 / (f.gather_split > 0 ? f.gather_split : 1);   // targets per CTA
-        nparts = (L->gather_ntargets + per_cta - 1) / per_cta;
+        nparts = (L->gather_ntargets + 255) / 256;
         if (const int per_sm = f.gather_occupancy[lp] ? f.gather_occupancy[lp]() : 0; per_sm > 0)
             nparts = std::min<int64_t>(nparts, int64_t(per_sm) * g_dev.sm_count);
         if (nparts > pstride)

@@ -100,7 +100,8 @@ typedef struct ml_loop {
     ml_plan_dev_t plan;
     double fconst[4];               /* kernel constants (e.g. dt)               */
     int64_t iconst[4];              /* kernel constants (e.g. integer scale)    */
-    void *scratch;                  /* device scratch >= ml_loop_scratch_bytes  */
+    void *scratch;                  /* device scratch >= ml_loop_scratch_bytes,
+                                       zero-filled when allocated               */
     int64_t rlim;                   /* elements >= rlim skip global reductions
                                        (exec-halo elements on multi-GPU runs);
                                        < 0 means n                               */
@@ -265,7 +266,8 @@ int ml_functor_count(int32_t *count);
 int ml_chain_lookup(const char *first, const char *second, char *fused, int32_t buflen, int32_t *na,
                     int32_t *apos, int32_t *nb, int32_t *bpos);
 int ml_functor_name(int32_t functor_id, char *buf, int32_t buflen, int32_t *dtype);
-/* Device scratch a loop needs (global-reduction partials). */
+/* Device scratch a loop needs (global-reduction partials and the arrival
+ * ticket of the in-kernel combine; zero-fill it once when allocating). */
 int ml_loop_scratch_bytes(const ml_loop_t *loop, uint64_t *bytes);
 /* Bytes of the primary-fold slot buffer a loop needs (0: not applicable). */
 int ml_loop_pfold_slot_bytes(const ml_loop_t *loop, uint64_t *bytes);

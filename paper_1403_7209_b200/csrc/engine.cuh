@@ -167,6 +167,8 @@ struct PFoldParams {
 struct LaunchParams {
     ArgRt a[MAX_ARGS];
     void *part[MAX_ARGS];       // reduction partials [nblocks][dim] per global reduce arg
+    unsigned *ticket;           // single-launch schedules: CTA arrival counter, the last CTA
+                                // folds the partials (nullptr: k_combine after the launches)
     int64_t n;
     int64_t rlim;               // elements >= rlim do not contribute to reductions
     int32_t bs;
@@ -536,6 +538,49 @@ struct Engine {
         (reduce_one<Is>(s, p, b, smem), ...);
     }
     static constexpr bool has_reduce = ((As::kind == KG && As::mode != MR) || ...);
+
+    // Last-CTA combine of a single-launch schedule: every CTA, after storing
+    // its partials, takes a ticket; the CTA that arrives last folds all
+    // gridDim.x partials onto the global exactly as k_combine would (same
+    // strided accumulation and block tree over 256 threads, so the result is
+    // bitwise k_combine's) and resets the ticket for the next launch or graph
+    // replay.  Saves the combine kernel (and its graph node) per reduction loop.
+    template <size_t I>
+    __device__ __forceinline__ static void fold_one(const LaunchParams &p, double *smem) {
+        using S = cuda::std::tuple_element_t<I, Slots>;
+        if constexpr (S::is_reduce) {
+            using T = typename S::T;
+            constexpr int M = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>::mode;
+            constexpr int D = cuda::std::tuple_element_t<I, cuda::std::tuple<As...>>::dim;
+            T *g = static_cast<T *>(p.a[I].data);
+            const T *part = static_cast<const T *>(p.part[I]);
+#pragma unroll 1
+            for (int c = 0; c < D; ++c) {
+                T v = reduce_identity<T, M>();
+                for (int64_t i = threadIdx.x; i < int64_t(gridDim.x); i += blockDim.x)
+                    v = combine<M>(v, __ldcg(part + i * D + c));
+                v = block_reduce<T, M>(v, reinterpret_cast<T *>(smem));
+                if (threadIdx.x == 0) g[c] = combine<M>(g[c], v);
+                __syncthreads();
+            }
+        }
+    }
+    template <size_t... Is>
+    __device__ __forceinline__ static void finish_reduce(const LaunchParams &p, double *smem,
+                                                         cuda::std::index_sequence<Is...>) {
+        if (!p.ticket) return;
+        __shared__ unsigned last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();                                   // this CTA's partials before its ticket
+            last = atomicAdd(p.ticket, 1u) == gridDim.x - 1u;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        (fold_one<Is>(p, smem), ...);
+        if (threadIdx.x == 0) *p.ticket = 0u;
+    }
 };
 
 // ---- direct loops -----------------------------------------------------------------
@@ -553,7 +598,10 @@ __device__ __forceinline__ void run_direct(const LaunchParams &p, Sig<As...>) {
         E::init_elem(s, p, e, idx);
         E::call(s, p, e, idx);
     }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, smem, idx);
+    if constexpr (E::has_reduce) {
+        E::reduce_all(s, p, blockIdx.x, smem, idx);
+        E::finish_reduce(p, smem, idx);
+    }
 }
 
 // Direct rows of the two elements a vectorised thread owns: READ/RW/INC rows
@@ -690,7 +738,10 @@ __device__ __forceinline__ void run_direct_vec(const LaunchParams &p, Sig<As...>
         }
         DV::store(rows, p, e0, two, idx);
     }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, smem, idx);
+    if constexpr (E::has_reduce) {
+        E::reduce_all(s, p, blockIdx.x, smem, idx);
+        E::finish_reduce(p, smem, idx);
+    }
 }
 
 // ---- colour schedules (reference plan: run_threads, general indirect writes) --------
@@ -807,7 +858,10 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
             for (int c = 0; c < DG; ++c) dst[c * gsc] = run[c];
         }
     }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
+    if constexpr (E::has_reduce) {
+        E::reduce_all(s, p, blockIdx.x, red, idx);
+        E::finish_reduce(p, red, idx);
+    }
 }
 
 // Hub targets of the gather schedule: value + the partial of each of its
@@ -893,7 +947,10 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
             for (int c = 0; c < DG; ++c) dst[c * gsc] = run[c];
         }
     }
-    if constexpr (E::has_reduce) E::reduce_all(s, p, blockIdx.x, red, idx);
+    if constexpr (E::has_reduce) {
+        E::reduce_all(s, p, blockIdx.x, red, idx);
+        E::finish_reduce(p, red, idx);
+    }
 }
 
 // Pass 2, warp-cooperative: a warp owns 32 consecutive pass-2 rows, whose

@@ -145,7 +145,7 @@ static uint64_t scratch_bytes(const ml_loop_t *L, const FunctorEntry &f) {
                                           (L->n + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i)
         if (f.kind[i] == KG && f.mode[i] != MR) bytes += uint64_t(nb) * f.dim[i] * 8 + 256;
-    return bytes;
+    return bytes ? bytes + 256 : 0;   // + the last-CTA ticket (zero-filled at allocation)
 }
 
 // resident-CTA counts per (functor, kernel, threads) — occupancy queries are not free
@@ -192,6 +192,7 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         p.k.i[i] = L->iconst[i];
     }
     char *scratch = static_cast<char *>(L->scratch);
+    bool has_reduce = false;
     const int64_t pstride = std::max<int64_t>({nb, (L->gather_ntargets + 255) / 256,
                                                (L->n + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i) {
@@ -206,6 +207,7 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
                 if (!scratch) ML_FAIL(ML_EINVAL, "loop '%s': reduction needs scratch", L->name);
                 p.part[i] = scratch;
                 scratch += uint64_t(pstride) * a.dim * 8 + 256;
+                has_reduce = true;
             }
         } else if (a.layout == ML_AOS || a.dim == 1) {
             r.se = a.dim;
@@ -224,6 +226,10 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
     bool last_colour = true;   // false: a partial colour range that does not end the loop
+    // single-launch schedules fold their partials in the kernel (last CTA);
+    // the colour schedules launch k_combine after their colour launches
+    unsigned *const ticket = has_reduce ? reinterpret_cast<unsigned *>(scratch) : nullptr;
+    bool single_launch = false;
     if (L->pf_n1 > 0) {
         // primary fold: pass 1 over targets' primary incidences (persistent grid),
         // pass 2 folds the secondary slots
@@ -255,6 +261,8 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         pf.rec = L->pf_rec;
         pf.ncol = L->pf_ncol;
         for (int i = 0; i < MAX_ARGS; ++i) pf.rcol[i] = L->pf_rcol[i];
+        p.ticket = ticket;
+        single_launch = true;
         if (pf.rec)
             for (int i = 0; i < f.nargs; ++i)
                 if (L->args[i].kind == ML_INDIRECT && (pf.rcol[i] < 0 || pf.rcol[i] >= pf.ncol))
@@ -281,6 +289,8 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         p.g_elem = L->gather_elem;
         p.g_pos = L->gather_pos;
         p.g_tlist = L->gather_targets;
+        p.ticket = ticket;
+        single_launch = true;
         nparts = (L->gather_ntargets + 255) / 256;
         if (const int per_sm = f.gather_occupancy[lp] ? f.gather_occupancy[lp]() : 0; per_sm > 0)
             nparts = std::min<int64_t>(nparts, int64_t(per_sm) * g_dev.sm_count);
@@ -307,6 +317,8 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         nparts = std::max<int64_t>(1, (L->n + per - 1) / per);
         if (occ > 0) nparts = std::min<int64_t>(nparts, int64_t(occ) * g_dev.sm_count);
         if (nparts > pstride) ML_FAIL(ML_EINVAL, "loop '%s': direct loop needs more scratch", L->name);
+        p.ticket = ticket;
+        single_launch = true;
         f.direct[lp](p, dim3(unsigned(nparts)), dim3(unsigned(threads)), 0, stream);
     } else {
         // the reference plan's colours: one launch per block colour
@@ -330,7 +342,7 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) ML_FAIL(ML_ECUDA, "loop '%s': launch failed: %s", L->name, cudaGetErrorString(err));
 
-    for (int i = 0; i < f.nargs && last_colour; ++i) {
+    for (int i = 0; i < f.nargs && last_colour && !single_launch; ++i) {
         const ml_arg_t &a = L->args[i];
         if (a.kind != ML_GLOBAL || a.mode == ML_READ) continue;
         if (a.dtype == ML_F64)

@@ -301,6 +301,9 @@ class _LoopEntry:
         nbytes = C.c_uint64()
         N.check(N.lib().ml_loop_scratch_bytes(C.byref(L), C.byref(nbytes)))
         self.scratch = N.DeviceBuffer(nbytes.value) if nbytes.value else None
+        if self.scratch:        # the last-CTA reduction ticket starts at zero
+            N.check(N.lib().ml_memset(self.scratch.ptr, 0, nbytes.value), "ml_memset")
+            N.check(N.lib().ml_synchronize(), "ml_synchronize")
         L.scratch = self.scratch.ptr if self.scratch else None
         self.desc = L
         self.useful = useful_bytes(loop)
@@ -565,7 +568,9 @@ class CompiledProgram:
                 total += 1 + (1 if e.gather is not None and e.gather.nhub else 0)
             else:
                 total += e.plan.ncolors
-            total += sum(1 for a in e.loop.args if a.kind == "global" and a.mode.name != "READ")
+                # colour schedules fold reduction partials with k_combine; the
+                # single-launch schedules fold them in their last CTA
+                total += sum(1 for a in e.loop.args if a.kind == "global" and a.mode.name != "READ")
         return total
 
     def __del__(self):

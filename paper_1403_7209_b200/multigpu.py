@@ -1097,16 +1097,18 @@ class StreamRank:
         for i, e in enumerate(self.entries):
             if e.loop.iter_set.size == 0:
                 continue
-            base = 0
+            base, colour = 0, False
             if e.pfold is not None:
                 base = 1 + (1 if e.pfold.n2 > 0 else 0)
             elif e.gather is not None or not e.plan.has_writes:
                 base = 1
             else:
-                base = e.plan.ncolors
+                base, colour = e.plan.ncolors, True
             if self.split[i] is not None:
                 base = 2
-            total += base + sum(1 for a in e.loop.args if a.kind == "global" and a.mode.name != "READ")
+            if colour:      # k_combine per reduction (single-launch schedules fold in-kernel)
+                total += sum(1 for a in e.loop.args if a.kind == "global" and a.mode.name != "READ")
+            total += base
             total += 2 * len(self.rp.reductions[i])              # combine_ranks (+ gather is NCCL)
         return total
 

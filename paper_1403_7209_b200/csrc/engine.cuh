@@ -614,6 +614,13 @@ template <class F>
 struct DenseWrites<F, cuda::std::void_t<decltype(F::dense_writes)>> : cuda::std::bool_constant<F::dense_writes> {};
 template <class F>
 __host__ __device__ constexpr bool dense_writes() { return DenseWrites<F>::value; }
+// write_only: every component of every indirect WRITE argument is written and
+// none is read (OP2's OP_WRITE taken literally): a target's final value is
+// the one its last incidence in serial order writes
+template <class F, class = void>
+struct WriteOnly : cuda::std::false_type {};
+template <class F>
+struct WriteOnly<F, cuda::std::void_t<decltype(F::write_only)>> : cuda::std::bool_constant<F::write_only> {};
 
 template <class A, class F, int LP>
 struct DirRows {
@@ -831,7 +838,11 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
         TG run[DG];
 #pragma unroll
         for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * gsc] : TG(0);
-        for (int k = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1); k < ke; ++k) {
+        // write-only WRITE loops without reductions: only the last incidence
+        // in serial order decides the target's value
+        constexpr bool last_only = MM == MW && !E::has_reduce && WriteOnly<F>::value;
+        const int kb = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1);
+        for (int k = last_only && ke > kb ? ke - 1 : kb; k < ke; ++k) {
             const int64_t e = __ldg(p.g_elem + k);
             const int a = __ldg(p.g_pos + k);
             E::init_elem(s, p, e, idx);

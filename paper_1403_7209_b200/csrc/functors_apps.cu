@@ -41,6 +41,7 @@ struct EdgeFlux {
 };
 
 struct BoundaryFix {
+    static constexpr bool write_only = true;   // indirect WRITE components all written, none read
     template <class T>
     using sig = Sig<Arg<KI, MW, 1, T>, Arg<KI, MW, 1, T>, Arg<KI, MR, 1, T>, Arg<KI, MR, 1, T>>;
     template <class U1, class U2, class G1, class G2>

@@ -183,6 +183,7 @@ struct ProxyUpdate {
 };
 
 struct ProxyBc {
+    static constexpr bool write_only = true;   // indirect WRITE components all written, none read
     template <class T>
     using sig = Sig<Arg<KI, MW, NQ, T>, Arg<KI, MW, NQ, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NQ, T>>;
     template <class Q1, class Q2, class B1, class B2>

@@ -842,6 +842,11 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
         // in serial order decides the target's value
         constexpr bool last_only = MM == MW && !E::has_reduce && WriteOnly<F>::value;
         const int kb = __ldg(p.g_off + t), ke = __ldg(p.g_off + t + 1);
+#ifndef ML_GATHER_UNROLL
+#define ML_GATHER_UNROLL 4   // incidence loop unroll (1 / 2 / 3 / 4 / 6 / 8 measured; 4 best)
+#endif
+        constexpr int kUnroll = ML_GATHER_UNROLL;
+#pragma unroll kUnroll
         for (int k = last_only && ke > kb ? ke - 1 : kb; k < ke; ++k) {
             const int64_t e = __ldg(p.g_elem + k);
             const int a = __ldg(p.g_pos + k);

@@ -11,6 +11,7 @@
 //        -Xcompiler -fPIC -o scripts/_exp_flux.so scripts/exp_flux_layout.cu
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cuda/std/type_traits>
 
 namespace {
 
@@ -695,6 +696,112 @@ __global__ void __launch_bounds__(256, MINB) k_flux_split(const __grid_constant_
     }
 }
 
+// Own-row cache: the target's own rows of the dats in MASK (bit 0 q, 1 lim,
+// 2 grad, 3 aux) are copied once per target into shared memory
+// (component-major, stride blockDim) and the edge evaluations read them
+// there; neighbour rows as in k_flux<0> (SOA).
+template <class Q1, class L1, class G1, class A1>
+__device__ __forceinline__ void eval_edge_v(const Data &d, int64_t e, int64_t a, int64_t b, Q1 q1, L1 l1,
+                                            G1 g1, A1 a1, double *r1, double *r2) {
+    const int64_t P = d.pitch;
+    const double *w = d.w + e * 3, *x1 = d.x + a * 3, *x2 = d.x + b * 3;
+    const auto q2 = view<0, NQ>(d.q, b, P);
+    const auto l2 = view<0, NLIM>(d.lim, b, P);
+    const auto g2 = view<0, NG>(d.grad, b, P);
+    const auto a2 = view<0, NAUX>(d.aux, b, P);
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double an = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NLIM; ++j) {
+            const double tt = l1[j] + l2[j];
+            s = s + tt * tt;
+        }
+        const double lam = an / ((1.0 + ds) * (1.0 + 0.0625 * s));
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const double f = lam * (q2[v] - q1[v]);
+            r1[v] = 0.0 + f;
+            r2[v] = 0.0 - f;
+        }
+    }
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds2 = d0 * d0 + d1 * d1 + d2 * d2 + 1e-12;
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double wd = w0 * d0 + w1 * d1 + w2 * d2;
+        double mu = 0.0;
+#pragma unroll
+        for (int j = 0; j < NAUX; ++j) mu = mu + (a1[j] + a2[j]);
+        mu = 0.01 * mu / (2.0 * NAUX);
+        const double awd = fabs(wd);
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const int bb = 3 * v;
+            const double gx = 0.5 * (g1[bb] + g2[bb]);
+            const double gy = 0.5 * (g1[bb + 1] + g2[bb + 1]);
+            const double gz = 0.5 * (g1[bb + 2] + g2[bb + 2]);
+            const double dq = q2[v] - q1[v];
+            const double corr = (dq - (gx * d0 + gy * d1 + gz * d2)) / ds2;
+            const double f = mu * (0.001 * (gx * w0 + gy * w1 + gz * w2) + corr * awd);
+            r1[v] += f;
+            r2[v] -= f;
+        }
+    }
+}
+
+struct SView {           // shared-memory own row, component stride = blockDim
+    const double *p;
+    __device__ __forceinline__ double operator[](int c) const { return p[c * 256]; }
+};
+
+template <int D>
+__device__ __forceinline__ void cache_row(double *dst, const double *src, int64_t a, int64_t P) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) dst[c * 256] = __ldg(src + c * P + a);
+}
+
+template <int MASK>
+__global__ void __launch_bounds__(256, 2) k_flux_own(const __grid_constant__ Data d) {
+    extern __shared__ double sm[];
+    constexpr int OQ = 0, OL = OQ + ((MASK & 1) ? NQ : 0), OG = OL + ((MASK & 2) ? NLIM : 0),
+                  OA = OG + ((MASK & 4) ? NG : 0);
+    double *my = sm + threadIdx.x;
+    const int64_t P = d.pitch;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < d.n1;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t tg = __ldg(d.tl1 + t);
+        if constexpr (MASK & 1) cache_row<NQ>(my + OQ * 256, d.q, tg, P);
+        if constexpr (MASK & 2) cache_row<NLIM>(my + OL * 256, d.lim, tg, P);
+        if constexpr (MASK & 4) cache_row<NG>(my + OG * 256, d.grad, tg, P);
+        if constexpr (MASK & 8) cache_row<NAUX>(my + OA * 256, d.aux, tg, P);
+        double run[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] = d.res[c * P + tg];
+        for (int k = __ldg(d.off1 + t), ke = __ldg(d.off1 + t + 1); k < ke; ++k) {
+            const int64_t e = __ldg(d.elem1 + k);
+            const int64_t a = __ldg(d.rec + 2 * int64_t(k)), b = __ldg(d.rec + 2 * int64_t(k) + 1);
+            double r1[NQ], r2[NQ];
+            auto pick = [&](auto cached, const double *base, int off) {
+                if constexpr (decltype(cached)::value) return SView{my + off * 256};
+                else return view<0, 1>(base, a, P);
+            };
+            eval_edge_v(d, e, a, b, pick(cuda::std::bool_constant<(MASK & 1) != 0>{}, d.q, OQ),
+                        pick(cuda::std::bool_constant<(MASK & 2) != 0>{}, d.lim, OL),
+                        pick(cuda::std::bool_constant<(MASK & 4) != 0>{}, d.grad, OG),
+                        pick(cuda::std::bool_constant<(MASK & 8) != 0>{}, d.aux, OA), r1, r2);
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] += r1[c];
+            store_slot(d, e, r2);
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) d.res[c * P + tg] = run[c];
+    }
+}
+
 }  // namespace
 
 extern "C" int exp_flux_run(int layout, const void *w, const void *q, const void *x, const void *lim,
@@ -850,5 +957,31 @@ extern "C" int exp_flux_aos(int minb, const void *w, const void *q, const void *
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (minb == 5) k_flux<2, 5><<<sms * 5, 128, 0, s>>>(d);
     else k_flux<2, 2><<<sms * 2, 256, 0, s>>>(d);
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_own(int mask, const void *w, const void *q, const void *x, const void *lim,
+                            const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                            const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                            int64_t n1, int64_t pitch, int sms, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto go = [&](auto kern, int dims) {
+        const size_t bytes = size_t(dims) * 256 * 8;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+        kern<<<2 * sms, 256, bytes, s>>>(d);
+    };
+    switch (mask) {
+    case 8: go(k_flux_own<8>, NAUX); break;
+    case 12: go(k_flux_own<12>, NAUX + NG); break;
+    case 4: go(k_flux_own<4>, NG); break;
+    case 15: go(k_flux_own<15>, NAUX + NG + NLIM + NQ); break;
+    default: go(k_flux_own<0>, 1); break;
+    }
     return int(cudaGetLastError());
 }

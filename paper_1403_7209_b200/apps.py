@@ -30,7 +30,7 @@ import math
 
 import numpy as np
 
-from .core import (INC, MAX, MIN, READ, RW, WRITE, ExecError, Global, Loop, Mesh,
+from .core import (INC, MIN, READ, RW, WRITE, ExecError, Global, Loop, Mesh,
                    arg_direct, arg_global, arg_indirect)
 from .kernels import device_kernel
 

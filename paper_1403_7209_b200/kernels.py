@@ -21,7 +21,7 @@ from ``fn.__defaults__``.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Callable
 
 from .core import ExecError

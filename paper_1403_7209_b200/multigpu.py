@@ -39,7 +39,7 @@ from typing import Sequence
 
 import numpy as np
 
-from .core import (AOS, INC, MAX, MIN, READ, RW, SOA, WRITE_MODES, ExecError, Global, Loop, Mesh,
+from .core import (INC, MAX, MIN, READ, RW, SOA, WRITE_MODES, ExecError, Global, Loop, Mesh,
                    MeshError, arg_direct, arg_global, arg_indirect, transform_layout)
 from .partition import (RankLayout, build_halos, derive_assignments, partition_rcb,
                         partition_trivial)

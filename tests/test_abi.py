@@ -7,7 +7,6 @@ import re
 import subprocess
 from pathlib import Path
 
-import numpy as np
 
 from paper_1403_7209_b200 import _native as N
 

@@ -7,7 +7,6 @@ import re
 import subprocess
 from pathlib import Path
 
-
 from paper_1403_7209_b200 import _native as N
 
 HEADER = Path(__file__).resolve().parent.parent / "include" / "meshloop_b200.h"

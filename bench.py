@@ -274,42 +274,33 @@ def run_ours(args) -> None:
 
     # -- per-loop breakdown: the steady-state graph with a timing event between
     #    loops (sequential capture, mean of K replays); eager launches beside it
-    # (a direct loop run as a gather loop's prologue is reported with it,
-    #  named "direct+gather": one kernel, one time, both loops' bytes)
     graph_loop_s = cp.replay_timed(max(3, args.steps))
-    by_entry = {id(e): t for e, t in zip(cp.entries, graph_loop_s)}
-    runs = cp.run_names()
-    per_loop = {name: [sum(by_entry[id(x)] for x in es)] for name, es in runs}
-    eager = {name: [] for name, _ in runs}
+    per_loop = {e.loop.name: [t] for e, t in zip(cp.entries, graph_loop_s)}
+    eager = {e.loop.name: [] for e in cp.entries}
     for _ in range(max(3, args.steps // 2)):
-        te = {id(e): t for e, t in zip(cp.entries, cp.run(False, True))}
-        for name, es in runs:
-            eager[name].append(sum(te[id(x)] for x in es))
+        for e, t in zip(cp.entries, cp.run(False, True)):
+            eager[e.loop.name].append(t)
     loops = {}
     peak, peak_src = peaks_gbs()
-    alg_of = {name: sum(x.alg for x in es) for name, es in runs}
-    for name, es in runs:
-        e = es[-1]
-        t = statistics.mean(per_loop[name])
-        loops[name] = {"ms": round(t * 1e3, 4),
-                       "eager_ms": round(statistics.mean(eager[name]) * 1e3, 4),
-                       "b_alg": alg_of[name], "useful_bytes": sum(x.useful for x in es),
-                       "gbs_alg": round(alg_of[name] / t / 1e9, 1),
-                       "frac_of_peak": round(alg_of[name] / t / 1e9 / peak, 4),
-                       "schedule": (e.sched if e.plan.has_writes else "direct") + (
-                           " (direct prologue)" if len(es) > 1 else ""),
-                       "nb": e.st.nb, "nc": e.st.nc}
-    names = [name for name, _ in runs]
+    for e in cp.entries:
+        t = statistics.mean(per_loop[e.loop.name])
+        loops[e.loop.name] = {"ms": round(t * 1e3, 4),
+                              "eager_ms": round(statistics.mean(eager[e.loop.name]) * 1e3, 4),
+                              "b_alg": e.alg, "useful_bytes": e.useful,
+                              "gbs_alg": round(e.alg / t / 1e9, 1),
+                              "frac_of_peak": round(e.alg / t / 1e9 / peak, 4),
+                              "schedule": e.sched if e.plan.has_writes else "direct",
+                              "nb": e.st.nb, "nc": e.st.nc}
+    names = [e.loop.name for e in cp.entries]
     flux = [i for i, n in enumerate(names) if "vflux" in n.split("+")]
-    dom_name = names[flux[0] if flux else max(range(len(names)), key=lambda i: loops[names[i]]["ms"])]
-    dom = dict(runs)[dom_name][-1]
-    t_dom = statistics.mean(per_loop[dom_name])
-    achieved = alg_of[dom_name] / t_dom / 1e9
+    dom = cp.entries[flux[0] if flux else max(range(len(names)), key=lambda i: loops[names[i]]["ms"])]
+    t_dom = statistics.mean(per_loop[dom.loop.name])
+    achieved = dom.alg / t_dom / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         dom_sched = dom.sched if dom.plan.has_writes else "direct"
-        traffic = json.loads(tfile.read_text()).get(dom_sched, {}).get(dom_name)
+        traffic = json.loads(tfile.read_text()).get(dom_sched, {}).get(dom.loop.name)
 
     # -- end to end through the public API with host buffers ---------------------------------
     pin_mesh(mesh)
@@ -345,10 +336,10 @@ def run_ours(args) -> None:
                    "parallelism": "single GPU", "device": info["name"], "setup": setup},
         "gpu_launches": cp.launches_per_run() * args.steps,
         "clocks": clk.summary(),
-        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": dom.loop.name, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg_of[dom_name],
+                     "algorithmic_bytes_per_launch": dom.alg,
                      "spec_peak_gbs": 8000.0,
                      "iteration": {"b_alg": sum(e.alg for e in cp.entries),
                                    "achieved": round(sum(e.alg for e in cp.entries) / (total_ms * 1e-3 / args.steps) / 1e9, 1),

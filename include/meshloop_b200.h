@@ -154,14 +154,6 @@ typedef struct ml_loop {
      * that reaches the last colour, so a host loop over single colours (the
      * reference's per-phase callback, executor.py:251-252) reduces once. */
     int32_t colour_begin, colour_end;
-    /* cross-set prologue (ml_prologue_lookup): a direct loop over this
-     * gather loop's target set, run by the same kernel — element t of the
-     * prologue by the thread that owns target t — instead of its own launch.
-     * `prologue` is used by ml_loop_run; ml_program_create takes
-     * `prologue_at` (1 + position of the prologue loop in the same program,
-     * 0: none) and then skips that loop's own enqueue. */
-    const struct ml_loop *prologue;
-    int32_t prologue_pair, prologue_at;
 } ml_loop_t;
 
 typedef struct ml_device_info {
@@ -274,11 +266,6 @@ int ml_functor_count(int32_t *count);
 int ml_chain_lookup(const char *first, const char *second, char *fused, int32_t buflen, int32_t *na,
                     int32_t *apos, int32_t *nb, int32_t *bpos);
 int ml_functor_name(int32_t functor_id, char *buf, int32_t buflen, int32_t *dtype);
-/* Prologue pairs (ML_REGISTER_PROLOGUE in a functor file): a direct loop of
- * functor `direct` immediately followed by a target-centric (gather) loop of
- * functor `gather` whose targets are the direct loop's elements may run as
- * one kernel; *pair = the pair id for ml_loop_t.prologue_pair, or -1. */
-int ml_prologue_lookup(int32_t direct, int32_t gather, int32_t *pair);
 /* Device scratch a loop needs (global-reduction partials and the arrival
  * ticket of the in-kernel combine; zero-fill it once when allocating). */
 int ml_loop_scratch_bytes(const ml_loop_t *loop, uint64_t *bytes);

@@ -812,37 +812,8 @@ __device__ __forceinline__ void run_phased(const LaunchParams &p, Sig<As...>) {
 // final value is therefore exactly the serial one.  No colours, no shared
 // memory, no atomics.  Global reductions count each element once (on its
 // incidence through the first such argument).
-// Cross-set prologue of the gather schedule (ML_REGISTER_PROLOGUE): a direct
-// loop over the gather's target set, element t applied by the thread that
-// owns target t (identity target list) before it gathers; its reductions
-// fold like a direct loop's (per-CTA partials, last CTA).
-struct NoPrologue {
-    __device__ __forceinline__ void init(const LaunchParams *) {}
-    __device__ __forceinline__ void run(const LaunchParams *, int64_t) {}
-    __device__ __forceinline__ void finish(const LaunchParams *, double *) {}
-};
-template <class FD, int LP, class S>
-struct DirectPrologue;
-template <class FD, int LP, class... Ds>
-struct DirectPrologue<FD, LP, Sig<Ds...>> {
-    using E = Engine<FD, ST_NONE, LP, Ds...>;
-    static constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
-    typename E::Slots s;
-    __device__ __forceinline__ void init(const LaunchParams *pd) { E::init_globals(s, *pd, idx); }
-    __device__ __forceinline__ void run(const LaunchParams *pd, int64_t e) {
-        E::init_elem(s, *pd, e, idx);
-        E::call(s, *pd, e, idx);
-    }
-    __device__ __forceinline__ void finish(const LaunchParams *pd, double *smem) {
-        if constexpr (E::has_reduce) {
-            E::reduce_all(s, *pd, blockIdx.x, smem, idx);
-            E::finish_reduce(*pd, smem, idx);
-        }
-    }
-};
-
-template <class F, int LP, class PRO = NoPrologue, class... As>
-__device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>, const LaunchParams *pd = nullptr) {
+template <class F, int LP, class... As>
+__device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
     using E = Engine<F, ST_GATHER, LP, As...>;
     constexpr bool has_inc = ((As::kind == KI && As::mode == MINC) || ...);
     constexpr int MM = has_inc ? MINC : MW;
@@ -856,14 +827,11 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>, co
     constexpr auto idx = cuda::std::make_index_sequence<E::N>{};
     typename E::Slots s;
     E::init_globals(s, p, idx);
-    PRO pro;
-    pro.init(pd);
     const ArgRt &rg = p.a[G];
     const int64_t gsc = sc_of<AG, LG>(rg);
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
          t - threadIdx.x < p.g_ntargets; t += int64_t(gridDim.x) * blockDim.x) {
         if (t >= p.g_ntargets) continue;
-        pro.run(pd, t);
         const int64_t tg = p.g_tlist ? int64_t(__ldg(p.g_tlist + t)) : t;
         TG *dst = static_cast<TG *>(rg.data) + base_of<AG, LG>(rg, tg);
         const int32_t seg = (MM == MINC && p.g_seg) ? __ldg(p.g_seg + t) : -1;
@@ -910,7 +878,6 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>, co
         E::reduce_all(s, p, blockIdx.x, red, idx);
         E::finish_reduce(p, red, idx);
     }
-    pro.finish(pd, red);
 }
 
 // Hub targets of the gather schedule: value + the partial of each of its
@@ -1258,13 +1225,6 @@ __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ LaunchPa
     pdl_wait();
     run_gather<F, LP>(p, typename F::template sig<T>{});
 }
-template <class FG, class FD, class T, int LP>
-__global__ void __launch_bounds__(256) k_gather_pro(const __grid_constant__ LaunchParams p,
-                                                    const __grid_constant__ LaunchParams pd) {
-    pdl_wait();
-    run_gather<FG, LP, DirectPrologue<FD, LP, typename FD::template sig<T>>>(p, typename FG::template sig<T>{},
-                                                                            &pd);
-}
 
 // ---- compile-time signature introspection -------------------------------------
 template <class S>
@@ -1468,52 +1428,10 @@ struct ChainRegistrar {
     }
 };
 
-// Prologue pairs: a direct loop of FD followed by a gather loop of FG over
-// FD's elements, as one kernel (k_gather_pro)
-using PairLaunchFn = void (*)(const LaunchParams &, const LaunchParams &, dim3, dim3, cudaStream_t);
-struct PairEntry {
-    const char *direct, *gather;
-    int32_t dtype;
-    PairLaunchFn launch[2];                          // [LP]
-    int (*occupancy[2])();
-};
-void register_pair(const PairEntry &e);
-
-template <class FD, class FG, class T>
-struct PairRegistrar {
-    template <int LP>
-    static void launch(const LaunchParams &p, const LaunchParams &pd, dim3 g, dim3 b, cudaStream_t s) {
-        launch_k(k_gather_pro<FG, FD, T, LP>, g, b, 0, s, p, pd);
-    }
-    template <int LP>
-    static int occupancy() {
-        int n = 0;
-        cudaFuncSetAttribute(k_gather_pro<FG, FD, T, LP>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             int(cudaSharedmemCarveoutMaxL1));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gather_pro<FG, FD, T, LP>, 256, 0) != cudaSuccess)
-            n = 0;
-        return n;
-    }
-    PairRegistrar(const char *direct, const char *gather) {
-        static_assert(!SigInfo<typename FD::template sig<T>>::ind_write, "the prologue must be a direct loop");
-        PairEntry e{};
-        e.direct = direct;
-        e.gather = gather;
-        e.dtype = type_code<T>();
-        e.launch[0] = &launch<0>;
-        e.launch[1] = &launch<1>;
-        e.occupancy[0] = &occupancy<0>;
-        e.occupancy[1] = &occupancy<1>;
-        register_pair(e);
-    }
-};
-
 #define ML_CAT2(a, b) a##b
 #define ML_CAT(a, b) ML_CAT2(a, b)
 #define ML_REGISTER(NAME, FUNCTOR, T) \
     static ::ml::Registrar<FUNCTOR, T> ML_CAT(ml_reg_, __COUNTER__)(NAME)
-#define ML_REGISTER_PROLOGUE(DIRECT, FD, GATHER, FG, T) \
-    static ::ml::PairRegistrar<FD, FG, T> ML_CAT(ml_pair_, __COUNTER__)(DIRECT, GATHER)
 #define ML_REGISTER_CHAIN(FIRST, SECOND, FUSED, FUNCTOR) \
     static ::ml::ChainRegistrar<FUNCTOR> ML_CAT(ml_chain_, __COUNTER__)(FIRST, SECOND, FUSED)
 

@@ -209,7 +209,5 @@ ML_REGISTER("proxy_update", ProxyUpdate, double);
 ML_REGISTER("proxy_fluxes", ProxyFluxes, double);
 ML_REGISTER_CHAIN("proxy_iflux", "proxy_vflux", "proxy_fluxes", ProxyFluxes);
 ML_REGISTER("proxy_bc", ProxyBc, double);
-// save+dt_calc (direct over nodes) runs inside grad_edge's gather over nodes
-ML_REGISTER_PROLOGUE("proxy_save_dt", ProxySaveDt, "proxy_grad", ProxyGrad, double);
 
 }  // namespace ml

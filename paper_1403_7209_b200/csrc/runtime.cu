@@ -170,89 +170,20 @@ static int enqueue_loop(const ml_loop_t *L, cudaStream_t stream) {
     return rc;
 }
 
-// Launch parameters of one loop: arguments with their strides, constants,
-// reduction partials in the loop's scratch (and the last-CTA ticket after them)
-// ---- prologue pairs (ML_REGISTER_PROLOGUE) ------------------------------------
-static std::vector<PairEntry> &pairs() {
-    static std::vector<PairEntry> v;
-    return v;
-}
-void register_pair(const PairEntry &e) { pairs().push_back(e); }
-
-static int build_params(const ml_loop_t *L, const FunctorEntry &f, LaunchParams &p, unsigned *&ticket);
-static int64_t part_stride(const ml_loop_t *L);
-
-// the gather loop L and its direct prologue loop as one k_gather_pro launch;
-// p holds L's gather parameters (grid: the pair kernel's resident CTAs)
-static int launch_with_prologue(const ml_loop_t *L, const FunctorEntry &f, LaunchParams &p, int lp,
-                                cudaStream_t stream) {
+static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
     auto &reg = registry();
-    auto &prs = pairs();
-    const ml_loop_t *D = L->prologue;
-    if (L->prologue_pair < 0 || L->prologue_pair >= int(prs.size()))
-        ML_FAIL(ML_EINVAL, "loop '%s': bad prologue pair %d", L->name, L->prologue_pair);
-    const PairEntry &pe = prs[L->prologue_pair];
-    if (D->functor < 0 || D->functor >= int(reg.size()))
-        ML_FAIL(ML_ENOFUNCTOR, "loop '%s': prologue has a bad functor id", L->name);
-    const FunctorEntry &fd = reg[D->functor];
-    if (std::strcmp(fd.name, pe.direct) || std::strcmp(f.name, pe.gather) || fd.dtype != pe.dtype ||
-        f.dtype != pe.dtype || fd.ind_write)
-        ML_FAIL(ML_EINVAL, "loop '%s': prologue '%s' does not match pair %d (%s, %s)", L->name,
-                D->name ? D->name : "?", L->prologue_pair, pe.direct, pe.gather);
-    int rc = validate(D, fd);
+    if (L->functor < 0 || L->functor >= int(reg.size()))
+        ML_FAIL(ML_ENOFUNCTOR, "loop '%s': bad functor id %d", L->name ? L->name : "?", L->functor);
+    const FunctorEntry &f = reg[L->functor];
+    int rc = validate(L, f);
     if (rc) return rc;
-    for (int i = 0; i < D->nargs; ++i)
-        if (D->args[i].kind == ML_INDIRECT)
-            ML_FAIL(ML_EINVAL, "loop '%s': prologue '%s' must be a direct loop", L->name, D->name);
-    if (D->n != L->gather_ntargets || L->gather_targets || L->gather_seg)
-        ML_FAIL(ML_EINVAL, "loop '%s': prologue '%s' needs one gather target per element (%lld targets, "
-                "%lld elements, identity target list, no hub rows)", L->name, D->name,
-                (long long)L->gather_ntargets, (long long)D->n);
-    LaunchParams pd;
-    unsigned *dticket = nullptr;
-    rc = build_params(D, fd, pd, dticket);
-    if (rc) return rc;
-    pd.ticket = dticket;
-    const int plp = std::min(lp, layout_policy(D));
-    static std::vector<std::pair<std::pair<int, int>, int>> occ_cache;
-    int occ = -1;
-    for (auto &kv : occ_cache)
-        if (kv.first == std::make_pair(L->prologue_pair, plp)) occ = kv.second;
-    if (occ < 0) {
-        occ = pe.occupancy[plp] ? pe.occupancy[plp]() : 0;
-        occ_cache.push_back({{L->prologue_pair, plp}, occ});
-    }
-    int64_t grid = (L->gather_ntargets + 255) / 256;
-    if (occ > 0) grid = std::min<int64_t>(grid, int64_t(occ) * g_dev.sm_count);
-    if (grid > part_stride(L) || grid > part_stride(D))
-        ML_FAIL(ML_EINVAL, "loop '%s': prologue pair needs more reduction scratch", L->name);
-    pe.launch[plp](p, pd, dim3(unsigned(grid)), dim3(256), stream);
-    return ML_OK;
-}
-
-extern "C" int ml_prologue_lookup(int32_t direct, int32_t gather, int32_t *pair) {
-    if (!pair) ML_FAIL(ML_EINVAL, "ml_prologue_lookup: null output");
-    *pair = -1;
-    auto &reg = registry();
-    if (direct < 0 || direct >= int(reg.size()) || gather < 0 || gather >= int(reg.size()))
-        ML_FAIL(ML_ENOFUNCTOR, "ml_prologue_lookup: bad functor id");
-    const FunctorEntry &d = reg[direct], &g = reg[gather];
-    auto &prs = pairs();
-    for (size_t i = 0; i < prs.size(); ++i)
-        if (!std::strcmp(prs[i].direct, d.name) && !std::strcmp(prs[i].gather, g.name) &&
-            prs[i].dtype == d.dtype && prs[i].dtype == g.dtype)
-            *pair = int32_t(i);
-    return ML_OK;
-}
-
-// rows of reduction partials a loop's scratch holds per reduced component
-static int64_t part_stride(const ml_loop_t *L) {
-    return std::max<int64_t>({L->plan.nblocks, (L->gather_ntargets + 255) / 256, (L->n + 255) / 256, int64_t(1)});
-}
-
-static int build_params(const ml_loop_t *L, const FunctorEntry &f, LaunchParams &p, unsigned *&ticket) {
+    if (L->n == 0) return ML_OK;   // empty iteration set: no launch, globals untouched
     const int64_t bs = L->plan.block_size;
-    p = LaunchParams{};
+    const int64_t nb = L->plan.nblocks;
+    if (bs < 1 || nb != (L->n + bs - 1) / bs)
+        ML_FAIL(ML_EINVAL, "loop '%s': plan does not cover the iteration set", L->name);
+
+    LaunchParams p{};
     p.n = L->n;
     p.rlim = L->rlim < 0 ? L->n : L->rlim;
     p.bs = int32_t(bs);
@@ -262,7 +193,8 @@ static int build_params(const ml_loop_t *L, const FunctorEntry &f, LaunchParams 
     }
     char *scratch = static_cast<char *>(L->scratch);
     bool has_reduce = false;
-    const int64_t pstride = part_stride(L);
+    const int64_t pstride = std::max<int64_t>({nb, (L->gather_ntargets + 255) / 256,
+                                               (L->n + 255) / 256, int64_t(1)});
     for (int i = 0; i < f.nargs; ++i) {
         const ml_arg_t &a = L->args[i];
         ArgRt &r = p.a[i];
@@ -290,36 +222,13 @@ static int build_params(const ml_loop_t *L, const FunctorEntry &f, LaunchParams 
             r.sc = a.pitch ? a.pitch : a.set_size;
         }
     }
-    ticket = has_reduce ? reinterpret_cast<unsigned *>(scratch) : nullptr;
-    return ML_OK;
-}
-
-static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
-    auto &reg = registry();
-    if (L->functor < 0 || L->functor >= int(reg.size()))
-        ML_FAIL(ML_ENOFUNCTOR, "loop '%s': bad functor id %d", L->name ? L->name : "?", L->functor);
-    const FunctorEntry &f = reg[L->functor];
-    int rc = validate(L, f);
-    if (rc) return rc;
-    if (L->prologue && (L->n == 0 || L->pf_n1 > 0 || !f.gather[0] || L->gather_ntargets <= 0 || !L->gather_off))
-        ML_FAIL(ML_EINVAL, "loop '%s': a prologue needs the gather schedule", L->name ? L->name : "?");
-    if (L->n == 0) return ML_OK;   // empty iteration set: no launch, globals untouched
-    const int64_t bs = L->plan.block_size;
-    const int64_t nb = L->plan.nblocks;
-    if (bs < 1 || nb != (L->n + bs - 1) / bs)
-        ML_FAIL(ML_EINVAL, "loop '%s': plan does not cover the iteration set", L->name);
-
-    LaunchParams p{};
-    unsigned *ticket = nullptr;
-    rc = build_params(L, f, p, ticket);
-    if (rc) return rc;
-    const int64_t pstride = part_stride(L);
     const int lp = layout_policy(L);
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
     bool last_colour = true;   // false: a partial colour range that does not end the loop
     // single-launch schedules fold their partials in the kernel (last CTA);
     // the colour schedules launch k_combine after their colour launches
+    unsigned *const ticket = has_reduce ? reinterpret_cast<unsigned *>(scratch) : nullptr;
     bool single_launch = false;
     if (L->pf_n1 > 0) {
         // primary fold: pass 1 over targets' primary incidences (persistent grid),
@@ -396,12 +305,7 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
             p.g_hub_tl = L->gather_hub_tl;
             p.g_hub_off = L->gather_hub_off;
         }
-        if (L->prologue) {
-            rc = launch_with_prologue(L, f, p, lp, stream);
-            if (rc) return rc;
-        } else {
-            f.gather[lp](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
-        }
+        f.gather[lp](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
         if (L->gather_seg && L->gather_nhub > 0)
             f.gather_hubs(p, dim3(unsigned((L->gather_nhub + 255) / 256)), dim3(256), 0, stream);
     } else if (!f.ind_write) {
@@ -774,8 +678,6 @@ struct ml_program {
     // earlier loops it conflicts with — sharing a dat or global buffer that
     // either of them writes — so independent loops overlap on side streams
     int32_t concurrent = 0;
-    std::vector<char> absorbed;                  // loop runs as another loop's prologue
-    bool has_pairs = false;
     std::vector<std::vector<int>> deps;
     std::vector<int> lane;                       // stream of each loop (0: main)
     std::vector<cudaEvent_t> done;               // per loop, after its last kernel
@@ -822,10 +724,9 @@ static int program_enqueue(ml_program *p, bool timed, bool external = false) {
     cudaStream_t s = g_dev.stream;
     const unsigned rec = external ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (p->gbytes) ML_CUDA(cudaMemcpyAsync(p->gdev, p->ghost, p->gbytes, cudaMemcpyHostToDevice, s));
-    if (timed || !p->concurrent || p->has_pairs) {
+    if (timed || !p->concurrent) {
         for (size_t i = 0; i < p->loops.size(); ++i) {
             if (timed) ML_CUDA(cudaEventRecordWithFlags(p->events[i], s, rec));
-            if (p->absorbed[i]) continue;                      // runs inside its gather loop
             int rc = enqueue_loop(&p->loops[i], s);
             if (rc) return rc;
         }
@@ -873,20 +774,6 @@ extern "C" int ml_program_create(const ml_loop_t *loops, int32_t nloops, void *g
         if (L.functor < 0 || L.functor >= int(reg.size())) ML_FAIL(ML_ENOFUNCTOR, "bad functor id");
         rc = validate(&L, reg[L.functor]);
         if (rc) return rc;
-    }
-    p->absorbed.assign(size_t(nloops), 0);
-    for (int i = 0; i < nloops; ++i) {            // prologue links point into the program's copies
-        ml_loop_t &L = p->loops[i];
-        if (L.prologue_at <= 0) {
-            L.prologue = nullptr;
-            continue;
-        }
-        const int j = L.prologue_at - 1;
-        if (j >= nloops || j == i || p->absorbed[j] || p->loops[j].prologue_at > 0)
-            ML_FAIL(ML_EINVAL, "loop '%s': bad prologue position %d", L.name, L.prologue_at);
-        L.prologue = &p->loops[j];
-        p->absorbed[j] = 1;
-        p->has_pairs = true;
     }
     p->ghost = globals_host;
     p->gdev = globals_dev;

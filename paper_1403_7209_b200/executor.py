@@ -98,7 +98,6 @@ class BackendConfig:
     inc_schedule_table: dict | None = None  # per-loop override (tuner.tune_schedule)
     concurrent_loops: bool = True           # graphs/untimed runs: independent loops overlap on streams
     chain_loops: bool = True                # run registered adjacent loop pairs as one loop (chain.py)
-    prologue_loops: bool = True             # a registered direct loop runs inside the next gather loop
     pfold_records: bool = True              # pfold pass 1 reads per-incidence map records
 
     def __post_init__(self):
@@ -342,9 +341,6 @@ class CompiledProgram:
         self.ghost = N.PinnedArray((max(off, 256),), np.uint8)
         self.entries = [_LoopEntry(l, mesh, config, self.gslot, self.gdev.ptr, iter_counts, rlim)
                         for l in self.run_loops]
-        self.absorbed = [False] * len(self.entries)
-        if config.prologue_loops and not iter_counts and not rlim and config.phase_callback is None:
-            self._link_prologues()
         self.all_dats = []
         for e in self.entries:
             for d in e.dats:
@@ -366,41 +362,6 @@ class CompiledProgram:
         # each loop descriptor bakes its dats' layouts into strides (runtime.cu)
         self.layouts = [d.layout for d in self.all_dats]
         self.runs = 0
-
-    def _link_prologues(self) -> None:
-        """Cross-set prologues (``ML_REGISTER_PROLOGUE``): a direct loop
-        immediately followed by a gather-schedule loop whose targets are the
-        direct loop's elements runs inside that loop's kernel — element t by
-        the thread that owns target t — when the pair is registered and
-        hazard-free: no dat written by one loop appears in the other, no
-        global reduced by one appears in the other (the gather reads
-        neighbours the prologue may not have reached yet).  The gather loop's
-        schedule is chosen as without the prologue (``auto`` / the tables); it
-        only links when that is the gather schedule."""
-        for i in range(len(self.entries) - 1):
-            D, G = self.entries[i], self.entries[i + 1]
-            if self.absorbed[i] or not _prologue_legal(D, G):
-                continue
-            pair = C.c_int32(-1)
-            N.check(N.lib().ml_prologue_lookup(D.functor, G.functor, C.byref(pair)), "ml_prologue_lookup")
-            if pair.value < 0:
-                continue
-            G.desc.prologue = C.addressof(D.desc)
-            G.desc.prologue_pair = pair.value
-            G.desc.prologue_at = i + 1
-            G.prologue_entry = D
-            self.absorbed[i] = True
-
-    def run_names(self) -> list:
-        """(name, entries) of each launched loop: a prologue and its gather
-        loop run as one, named ``direct+gather``."""
-        out = []
-        for i, e in enumerate(self.entries):
-            if self.absorbed[i]:
-                continue
-            pro = getattr(e, "prologue_entry", None)
-            out.append((f"{pro.loop.name}+{e.loop.name}", [pro, e]) if pro else (e.loop.name, [e]))
-        return out
 
     def dependencies(self) -> list:
         """Per loop: (earlier loops it must wait for, stream lane) of the
@@ -503,8 +464,7 @@ class CompiledProgram:
             for d in e.written:
                 last_w[id(d)] = (i, d)
         for i, d in last_w.values():
-            # a prologue's results exist only once its gather loop has run
-            last[i + 1 if self.absorbed[i] else i].append(d)
+            last[i].append(d)
         self._splan = (first, last)
         return self._splan
 
@@ -540,8 +500,7 @@ class CompiledProgram:
                     d._dev.copy_h2d(host)
             if first[i] or i == 0:
                 N.check(L.ml_order(N.ML_STREAM_H2D, N.ML_STREAM_COMPUTE))
-            if not self.absorbed[i]:               # a prologue runs inside its gather loop
-                N.check(L.ml_loop_run(C.byref(e.desc)), f"loop {e.loop.name!r}")
+            N.check(L.ml_loop_run(C.byref(e.desc)), f"loop {e.loop.name!r}")
             if last[i]:
                 N.check(L.ml_order(N.ML_STREAM_COMPUTE, N.ML_STREAM_D2H))
                 for d in last[i]:
@@ -599,8 +558,8 @@ class CompiledProgram:
     def launches_per_run(self) -> int:
         """Kernel launches one run enqueues (colour launches + reduction combines)."""
         total = 0
-        for i, e in enumerate(self.entries):
-            if e.loop.iter_set.size == 0 or self.absorbed[i]:
+        for e in self.entries:
+            if e.loop.iter_set.size == 0:
                 continue
             if e.pfold is not None:
                 total += 1 + (1 if e.pfold.n2 > 0 else 0) + (1 if e.pfold.nhub1 else 0) + (
@@ -624,28 +583,6 @@ class CompiledProgram:
 _PROGRAM_CACHE_SIZE = 32
 
 
-def _prologue_legal(D: "_LoopEntry", G: "_LoopEntry") -> bool:
-    """A direct loop D may run as the prologue of the gather loop G after it."""
-    if D.n == 0 or D.n != D.loop.iter_set.size or any(a.kind == "indirect" for a in D.loop.args):
-        return False
-    g = G.gather
-    if G.pfold is not None or g is None or g.targets is not None or g.seg is not None or g.ntargets != D.n:
-        return False
-    tgt = [a for a in G.loop.args if a.kind == "indirect" and a.mode is not READ]
-    if not tgt or tgt[0].dat.set is not D.loop.iter_set:
-        return False
-    for X, Y in ((D.loop, G.loop), (G.loop, D.loop)):
-        for a in X.args:
-            if a.mode is READ:
-                continue
-            if a.kind == "global":
-                if any(b.kind == "global" and b.glob is a.glob for b in Y.args):
-                    return False
-            elif any(b.kind != "global" and b.dat is a.dat for b in Y.args):
-                return False
-    return True
-
-
 def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
                     iter_counts: dict | None = None, rlim: dict | None = None) -> CompiledProgram:
     """Compiled program for (loops, block sizes, mesh version), cached on the mesh.
@@ -659,7 +596,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
            tuple(config.block_size_for(l.name) for l in program), config.block_size,
            tuple(sorted((config.block_size_table or {}).items())), config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.coord_dat,
-           config.concurrent_loops, config.chain_loops, config.prologue_loops, config.pfold_records,
+           config.concurrent_loops, config.chain_loops, config.pfold_records,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):
@@ -678,11 +615,8 @@ def _sync_host(dats) -> None:
 
 
 def _record(collector: PerfCollector, cp: CompiledProgram, times) -> None:
-    by_entry = {id(e): t for e, t in zip(cp.entries, times)}
-    for name, es in cp.run_names():
-        e = es[-1]
-        collector.add(name, sum(by_entry[id(x)] for x in es), sum(x.useful for x in es), nb=e.st.nb,
-                      nc=e.st.nc, alg_bytes=sum(x.alg for x in es))
+    for e, t in zip(cp.entries, times):
+        collector.add(e.loop.name, t, e.useful, nb=e.st.nb, nc=e.st.nc, alg_bytes=e.alg)
 
 
 def run_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig | None = None

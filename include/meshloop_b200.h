@@ -137,9 +137,11 @@ typedef struct ml_loop {
     const int32_t *pf_slotpos;      /* [n][INC args - 1]: slot row of each secondary
                                        increment = its index in pf_elem2 */
     int32_t pf_ncol;                /* record width (distinct map columns)       */
-    const int32_t *pf_rec;          /* optional [pass-1 incidences][pf_ncol]: the
-                                       map entries of each incidence's element;
-                                       NULL: read through the maps */
+    const int32_t *pf_rec;          /* [incidences][pf_ncol]: the map entries of
+                                       each incidence's element — of pass 1
+                                       (optional: NULL reads through the maps),
+                                       or of gather_elem (required by the
+                                       gather schedule) */
     int8_t pf_rcol[ML_MAX_ARGS];    /* record column of each indirect argument   */
     /* hub rows (either pass): targets with > 128 incidences are split into
      * rows accumulating from zero into partial slot pf_seg*[row] (-1:

@@ -850,7 +850,13 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
         for (int k = last_only && ke > kb ? ke - 1 : kb; k < ke; ++k) {
             const int64_t e = __ldg(p.g_elem + k);
             const int a = __ldg(p.g_pos + k);
-            E::init_elem(s, p, e, idx);
+#ifndef ML_GATHER_REC
+#define ML_GATHER_REC 1      // per-incidence map records (grad_edge 0.1048 -> 0.1008 ms)
+#endif
+            if constexpr (ML_GATHER_REC)
+                E::init_elem_rec(s, p, e, p.pf.rec + int64_t(k) * p.pf.ncol, idx);
+            else
+                E::init_elem(s, p, e, idx);
             if constexpr (MM == MW) E::template gather_op<MW, 1, DG>(s, a, run, idx);
             if constexpr (E::has_reduce) {
                 if (a != 0 || e >= p.rlim) {

@@ -289,6 +289,17 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         p.g_elem = L->gather_elem;
         p.g_pos = L->gather_pos;
         p.g_tlist = L->gather_targets;
+        // per-incidence map records (pf_rec/pf_ncol/pf_rcol, as the primary
+        // fold's pass 1): the kernel reads an incidence's map entries beside
+        // its element id, one dependent load fewer
+        if (!L->pf_rec || L->pf_ncol < 1)
+            ML_FAIL(ML_EINVAL, "loop '%s': gather schedule needs per-incidence map records", L->name);
+        p.pf.rec = L->pf_rec;
+        p.pf.ncol = L->pf_ncol;
+        for (int i = 0; i < MAX_ARGS; ++i) p.pf.rcol[i] = L->pf_rcol[i];
+        for (int i = 0; i < f.nargs; ++i)
+            if (L->args[i].kind == ML_INDIRECT && (L->pf_rcol[i] < 0 || L->pf_rcol[i] >= L->pf_ncol))
+                ML_FAIL(ML_EINVAL, "loop '%s': record column of argument %d out of range", L->name, i);
         p.ticket = ticket;
         single_launch = true;
         nparts = (L->gather_ntargets + 255) / 256;

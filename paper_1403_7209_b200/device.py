@@ -397,12 +397,17 @@ class GatherMirror:
     the list is compacted to those targets (``targets``)."""
 
     __slots__ = ("off", "elem", "pos", "ntargets", "targets", "host", "seg", "part", "nhub",
-                 "hub_tl", "hub_off")
+                 "hub_tl", "hub_off", "rec", "ncol", "rcol", "rec_host")
 
     def __init__(self, loop, n: int, hubs: bool = False):
         wr = [a for a in loop.args if a.kind == "indirect" and a.mode.name != "READ"]
         h = gather_lists_host(loop, n, hubs)
         self.host = h["host"]
+        # per-incidence map records: the kernel reads each incidence's map
+        # entries beside its element id instead of through it
+        self.rec_host, self.rcol = pfold_records_host(loop, h["elem"])
+        self.ncol = self.rec_host.shape[1]
+        self.rec = _upload(self.rec_host)
         self.seg = self.part = self.hub_tl = self.hub_off = None
         self.nhub = h["nhub"]
         if h["seg"] is not None:
@@ -423,6 +428,7 @@ class GatherMirror:
         new_off = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
         take = (np.repeat(starts - new_off[:-1], deg) + np.arange(int(deg.sum()))).astype(np.int64)
         return {"ntargets": int(targets_idx.size), "off": _upload(new_off),
+                "rec": _upload(np.ascontiguousarray(self.rec_host[take])),
                 "elem": _upload(np.ascontiguousarray(h["elem"][take])),
                 "pos": _upload(np.ascontiguousarray(h["pos"][take])),
                 "targets": _upload(np.ascontiguousarray(h["targets"][targets_idx], dtype=np.int32)),

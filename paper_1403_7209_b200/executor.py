@@ -289,6 +289,9 @@ class _LoopEntry:
             L.gather_elem = self.gather.elem.ptr
             L.gather_pos = self.gather.pos.ptr
             L.gather_targets = self.gather.targets.ptr if self.gather.targets is not None else None
+            L.pf_rec, L.pf_ncol = self.gather.rec.ptr, self.gather.ncol
+            for i, c in enumerate(self.gather.rcol):
+                L.pf_rcol[i] = c
             if self.gather.seg is not None:
                 g = self.gather
                 L.gather_seg, L.gather_part, L.gather_nhub = g.seg.ptr, g.part.ptr, g.nhub

@@ -827,6 +827,7 @@ class StreamRank:
             desc.gather_ntargets = sub["ntargets"]
             desc.gather_off, desc.gather_elem = sub["off"].ptr, sub["elem"].ptr
             desc.gather_pos, desc.gather_targets = sub["pos"].ptr, sub["targets"].ptr
+            desc.pf_rec = sub["rec"].ptr
             out.append((desc, sub))
         return out
 

@@ -802,6 +802,174 @@ __global__ void __launch_bounds__(256, 2) k_flux_own(const __grid_constant__ Dat
     }
 }
 
+// Neighbour rows staged in shared memory with cp.async (8-byte LDGSTS, one
+// per component), double-buffered across each thread's sequence of edges:
+// the copies of edge i+1 are in flight while edge i computes, so a thread's
+// memory-level parallelism is not bounded by its registers.  STAGE picks the
+// staged neighbour dats (bit 0 q, 1 lim, 2 grad, 3 aux); the rest, and all
+// own rows, are read as in k_flux<0>.
+template <class Q1, class L1, class G1, class A1, class Q2, class L2, class G2, class A2>
+__device__ __forceinline__ void eval_edge_vv(const Data &d, int64_t e, int64_t a, int64_t b, Q1 q1, L1 l1,
+                                             G1 g1, A1 a1, Q2 q2, L2 l2, G2 g2, A2 a2, double *r1,
+                                             double *r2) {
+    const double *w = d.w + e * 3, *x1 = d.x + a * 3, *x2 = d.x + b * 3;
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double an = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NLIM; ++j) {
+            const double tt = l1[j] + l2[j];
+            s = s + tt * tt;
+        }
+        const double lam = an / ((1.0 + ds) * (1.0 + 0.0625 * s));
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const double f = lam * (q2[v] - q1[v]);
+            r1[v] = 0.0 + f;
+            r2[v] = 0.0 - f;
+        }
+    }
+    {
+        const double d0 = x2[0] - x1[0], d1 = x2[1] - x1[1], d2 = x2[2] - x1[2];
+        const double ds2 = d0 * d0 + d1 * d1 + d2 * d2 + 1e-12;
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        const double wd = w0 * d0 + w1 * d1 + w2 * d2;
+        double mu = 0.0;
+#pragma unroll
+        for (int j = 0; j < NAUX; ++j) mu = mu + (a1[j] + a2[j]);
+        mu = 0.01 * mu / (2.0 * NAUX);
+        const double awd = fabs(wd);
+#pragma unroll
+        for (int v = 0; v < NQ; ++v) {
+            const int bb = 3 * v;
+            const double gx = 0.5 * (g1[bb] + g2[bb]);
+            const double gy = 0.5 * (g1[bb + 1] + g2[bb + 1]);
+            const double gz = 0.5 * (g1[bb + 2] + g2[bb + 2]);
+            const double dq = q2[v] - q1[v];
+            const double corr = (dq - (gx * d0 + gy * d1 + gz * d2)) / ds2;
+            const double f = mu * (0.001 * (gx * w0 + gy * w1 + gz * w2) + corr * awd);
+            r1[v] += f;
+            r2[v] -= f;
+        }
+    }
+}
+
+template <int TPB>
+struct CView {           // staged neighbour row: component stride = threads per CTA
+    const double *p;
+    __device__ __forceinline__ double operator[](int c) const { return p[c * TPB]; }
+};
+
+__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int STAGE, int TPB>
+struct Staged {
+    static constexpr int DQ = (STAGE & 1) ? NQ : 0, DL = (STAGE & 2) ? NLIM : 0, DG = (STAGE & 4) ? NG : 0,
+                         DA = (STAGE & 8) ? NAUX : 0;
+    static constexpr int OQ = 0, OL = DQ, OG = OL + DL, OA = OG + DG, D = OA + DA;
+    template <int DIM>
+    __device__ static void issue(double *buf, const double *base, int64_t b, int64_t P) {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) cp_async8(buf + c * TPB, base + c * P + b);
+    }
+    __device__ static void fetch(double *buf, const Data &d, int64_t b) {
+        const int64_t P = d.pitch;
+        if constexpr (DQ) issue<NQ>(buf + OQ * TPB, d.q, b, P);
+        if constexpr (DL) issue<NLIM>(buf + OL * TPB, d.lim, b, P);
+        if constexpr (DG) issue<NG>(buf + OG * TPB, d.grad, b, P);
+        if constexpr (DA) issue<NAUX>(buf + OA * TPB, d.aux, b, P);
+    }
+};
+
+template <int STAGE, int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) k_flux_cpa(const __grid_constant__ Data d) {
+    using SG = Staged<STAGE, TPB>;
+    extern __shared__ double smc[];
+    double *const mine = smc + threadIdx.x;
+    auto buf = [&](int i) { return mine + i * (SG::D * TPB); };
+    const int64_t P = d.pitch, stride = int64_t(gridDim.x) * TPB;
+    int64_t t = int64_t(blockIdx.x) * TPB + threadIdx.x;
+    if (t >= d.n1) return;
+    // cursor over this thread's edges: (target row t, incidence k, end ke)
+    int k = __ldg(d.off1 + t), ke = __ldg(d.off1 + t + 1);
+    // prefetch the first edge
+    int64_t t_n = t;
+    int k_n = k, ke_n = ke;
+    auto advance = [&](int64_t &tt, int &kk, int &kke) {
+        if (++kk >= kke) {
+            tt += stride;
+            if (tt < d.n1) {
+                kk = __ldg(d.off1 + tt);
+                kke = __ldg(d.off1 + tt + 1);
+            }
+        }
+    };
+    while (t_n < d.n1 && k_n >= ke_n) {            // rows without edges
+        t_n += stride;
+        if (t_n < d.n1) { k_n = __ldg(d.off1 + t_n); ke_n = __ldg(d.off1 + t_n + 1); }
+    }
+    t = t_n; k = k_n; ke = ke_n;
+    if (t >= d.n1) return;
+    SG::fetch(buf(0), d, __ldg(d.rec + 2 * int64_t(k) + 1));
+    cp_commit();
+    int cur = 0;
+    double run[NQ];
+    int64_t tg = __ldg(d.tl1 + t);
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) run[c] = d.res[c * P + tg];
+    while (t < d.n1) {
+        // next edge: issue its copies into the other buffer
+        t_n = t; k_n = k; ke_n = ke;
+        advance(t_n, k_n, ke_n);
+        while (t_n < d.n1 && k_n >= ke_n) {
+            t_n += stride;
+            if (t_n < d.n1) { k_n = __ldg(d.off1 + t_n); ke_n = __ldg(d.off1 + t_n + 1); }
+        }
+        if (t_n < d.n1) SG::fetch(buf(cur ^ 1), d, __ldg(d.rec + 2 * int64_t(k_n) + 1));
+        cp_commit();
+        cp_wait<1>();                                  // this edge's copies have landed
+        const int64_t e = __ldg(d.elem1 + k);
+        const int64_t a = __ldg(d.rec + 2 * int64_t(k)), b = __ldg(d.rec + 2 * int64_t(k) + 1);
+        double r1[NQ], r2[NQ];
+        const double *sb = buf(cur);
+        auto nb = [&](auto staged, const double *base, int off) {
+            if constexpr (decltype(staged)::value) return CView<TPB>{sb + off * TPB};
+            else return view<0, 1>(base, b, P);
+        };
+        eval_edge_vv(d, e, a, b, view<0, NQ>(d.q, a, P), view<0, NLIM>(d.lim, a, P), view<0, NG>(d.grad, a, P),
+                     view<0, NAUX>(d.aux, a, P),
+                     nb(cuda::std::bool_constant<(STAGE & 1) != 0>{}, d.q, SG::OQ),
+                     nb(cuda::std::bool_constant<(STAGE & 2) != 0>{}, d.lim, SG::OL),
+                     nb(cuda::std::bool_constant<(STAGE & 4) != 0>{}, d.grad, SG::OG),
+                     nb(cuda::std::bool_constant<(STAGE & 8) != 0>{}, d.aux, SG::OA), r1, r2);
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] += r1[c];
+        store_slot(d, e, r2);
+        if (t_n != t) {                                // target finished
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) d.res[c * P + tg] = run[c];
+            if (t_n < d.n1) {
+                tg = __ldg(d.tl1 + t_n);
+#pragma unroll
+                for (int c = 0; c < NQ; ++c) run[c] = d.res[c * P + tg];
+            }
+        }
+        t = t_n; k = k_n; ke = ke_n;
+        cur ^= 1;
+    }
+    cp_wait<0>();
+}
+
 }  // namespace
 
 extern "C" int exp_flux_run(int layout, const void *w, const void *q, const void *x, const void *lim,
@@ -982,6 +1150,32 @@ extern "C" int exp_flux_own(int mask, const void *w, const void *q, const void *
     case 4: go(k_flux_own<4>, NG); break;
     case 15: go(k_flux_own<15>, NAUX + NG + NLIM + NQ); break;
     default: go(k_flux_own<0>, 1); break;
+    }
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_cpa(int variant, const void *w, const void *q, const void *x, const void *lim,
+                            const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                            const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                            int64_t n1, int64_t pitch, int sms, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto go = [&](auto kern, int tpb, int dims, int ctas_per_sm) {
+        const size_t bytes = size_t(2) * dims * tpb * 8;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+        kern<<<ctas_per_sm * sms, tpb, bytes, s>>>(d);
+    };
+    switch (variant) {
+    case 0: go(k_flux_cpa<12, 128, 3>, 128, NG + NAUX, 3); break;          // grad+aux, 128x3 (76 KB)
+    case 1: go(k_flux_cpa<8, 128, 4>, 128, NAUX, 4); break;                // aux only, 128x4
+    case 2: go(k_flux_cpa<15, 128, 2>, 128, NQ + NLIM + NG + NAUX, 2); break;   // all, 128x2
+    case 3: go(k_flux_cpa<12, 64, 6>, 64, NG + NAUX, 6); break;            // grad+aux, 64x6
+    default: go(k_flux_cpa<4, 128, 4>, 128, NG, 4); break;                 // grad only, 128x4
     }
     return int(cudaGetLastError());
 }

@@ -93,6 +93,7 @@ def main():
     lib.exp_flux_reg.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_h.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_split.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_cpa.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_own.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_aos.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_lrec.argtypes = ([C.c_int] + [C.c_void_p] * 8 + [C.c_int64, C.c_void_p, C.c_void_p,
@@ -118,7 +119,8 @@ def main():
                              (0, 22, "soa_split3"), (1, 23, "aosoa_split3"), (0, 24, "soa_split4"),
                              (1, 25, "aosoa_split4"), (4, 30, "aos_pad"), (4, 31, "aos_pad_128x5"),
                              (0, 40, "own0"), (0, 48, "own_aux"), (0, 44, "own_grad"), (0, 52, "own_grad_aux"),
-                             (0, 55, "own_all")):
+                             (0, 55, "own_all"), (0, 60, "cpa_grad_aux"), (0, 61, "cpa_aux"),
+                             (0, 62, "cpa_all"), (0, 63, "cpa_grad_aux_64x6"), (0, 64, "cpa_grad")):
         if args.only and name not in args.only and name != "soa":
             continue
         def put(k):
@@ -144,7 +146,9 @@ def main():
                       T["res"].data_ptr(), slots.data_ptr(), ints["off1"].data_ptr(),
                       ints["elem1"].data_ptr(), ints["tl1"].data_ptr(), ints["rec"].data_ptr(),
                       ints["slotpos"].data_ptr(), int(tl1.size), n)
-            if lanes >= 40:
+            if lanes >= 60:
+                rc = lib.exp_flux_cpa(lanes - 60, *common[1:], sms, stream)
+            elif lanes >= 40:
                 rc = lib.exp_flux_own(lanes - 40, *common[1:], sms, stream)
             elif lanes >= 30:
                 rc = lib.exp_flux_aos(5 if lanes == 31 else 2, *common[1:], sms, stream)

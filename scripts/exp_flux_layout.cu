@@ -970,6 +970,126 @@ __global__ void __launch_bounds__(TPB, MINB) k_flux_cpa(const __grid_constant__ 
     cp_wait<0>();
 }
 
+// Neighbour rows moved by the TMA engine: padded-AoS rows (16-byte multiples)
+// of the staged dats go global -> shared with one cp.async.bulk per row,
+// completing on a per-thread mbarrier, double-buffered across the thread's
+// edges.  Own rows: padded-AoS 16-byte pair loads (View<2>).
+__device__ __forceinline__ uint32_t s32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t *b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     s32(dst)),
+                 "l"(src), "r"(bytes), "r"(s32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done)
+                     : "r"(s32(b)), "r"(parity)
+                     : "memory");
+    } while (!done);
+}
+
+struct RowS {            // a staged AoS row in shared memory
+    const double *p;
+    __device__ __forceinline__ double operator[](int c) const { return p[c]; }
+};
+
+template <int STAGE>
+struct BulkRows {
+    static constexpr int DQ = (STAGE & 1) ? padded<NQ>() : 0, DL = (STAGE & 2) ? padded<NLIM>() : 0,
+                         DG = (STAGE & 4) ? padded<NG>() : 0, DA = (STAGE & 8) ? padded<NAUX>() : 0;
+    static constexpr int OQ = 0, OL = DQ, OG = OL + DL, OA = OG + DG, D = OA + DA;   // doubles per stage
+    __device__ static void fetch(double *buf, uint64_t *bar, const Data &d, int64_t b) {
+        bar_expect(bar, uint32_t(D * 8));
+        if constexpr (DQ) bulk(buf + OQ, d.q + b * DQ, DQ * 8, bar);
+        if constexpr (DL) bulk(buf + OL, d.lim + b * DL, DL * 8, bar);
+        if constexpr (DG) bulk(buf + OG, d.grad + b * DG, DG * 8, bar);
+        if constexpr (DA) bulk(buf + OA, d.aux + b * DA, DA * 8, bar);
+    }
+};
+
+template <int STAGE, int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) k_flux_bulk(const __grid_constant__ Data d) {
+    using BR = BulkRows<STAGE>;
+    extern __shared__ __align__(16) double smb[];
+    __shared__ __align__(8) uint64_t bars[2][TPB];
+    double *const mine = smb + threadIdx.x * (2 * BR::D);
+    auto bar = [&](int i) { return &bars[i][threadIdx.x]; };
+    bar_init(bar(0));
+    bar_init(bar(1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int64_t stride = int64_t(gridDim.x) * TPB;
+    int64_t t = int64_t(blockIdx.x) * TPB + threadIdx.x;
+    auto skip_empty = [&](int64_t &tt, int &kk, int &kke) {
+        while (tt < d.n1 && kk >= kke) {
+            tt += stride;
+            if (tt < d.n1) { kk = __ldg(d.off1 + tt); kke = __ldg(d.off1 + tt + 1); }
+        }
+    };
+    int k = 0, ke = 0;
+    if (t < d.n1) { k = __ldg(d.off1 + t); ke = __ldg(d.off1 + t + 1); }
+    skip_empty(t, k, ke);
+    if (t >= d.n1) return;
+    BR::fetch(mine, bar(0), d, __ldg(d.rec + 2 * int64_t(k) + 1));
+    uint32_t phase = 0;
+    int cur = 0;
+    double run[NQ];
+    int64_t tg = __ldg(d.tl1 + t);
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) run[c] = d.res[tg * NQ + c];
+    while (t < d.n1) {
+        int64_t t_n = t;
+        int k_n = k + 1, ke_n = ke;
+        if (k_n >= ke_n) {
+            t_n += stride;
+            if (t_n < d.n1) { k_n = __ldg(d.off1 + t_n); ke_n = __ldg(d.off1 + t_n + 1); }
+        }
+        skip_empty(t_n, k_n, ke_n);
+        if (t_n < d.n1) BR::fetch(mine + (cur ^ 1) * BR::D, bar(cur ^ 1), d, __ldg(d.rec + 2 * int64_t(k_n) + 1));
+        bar_wait(bar(cur), (phase >> cur) & 1u);
+        phase ^= 1u << cur;
+        const int64_t e = __ldg(d.elem1 + k);
+        const int64_t a = __ldg(d.rec + 2 * int64_t(k)), b = __ldg(d.rec + 2 * int64_t(k) + 1);
+        const double *sb = mine + cur * BR::D;
+        auto nb = [&](auto staged, const double *base, int off, auto dimc) {
+            if constexpr (decltype(staged)::value) return RowS{sb + off};
+            else return view<2, decltype(dimc)::value>(base, b, 0);
+        };
+        double r1[NQ], r2[NQ];
+        eval_edge_vv(d, e, a, b, view<2, NQ>(d.q, a, 0), view<2, NLIM>(d.lim, a, 0), view<2, NG>(d.grad, a, 0),
+                     view<2, NAUX>(d.aux, a, 0),
+                     nb(cuda::std::bool_constant<(STAGE & 1) != 0>{}, d.q, BR::OQ, cuda::std::integral_constant<int, NQ>{}),
+                     nb(cuda::std::bool_constant<(STAGE & 2) != 0>{}, d.lim, BR::OL, cuda::std::integral_constant<int, NLIM>{}),
+                     nb(cuda::std::bool_constant<(STAGE & 4) != 0>{}, d.grad, BR::OG, cuda::std::integral_constant<int, NG>{}),
+                     nb(cuda::std::bool_constant<(STAGE & 8) != 0>{}, d.aux, BR::OA, cuda::std::integral_constant<int, NAUX>{}),
+                     r1, r2);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before this buffer's next bulk write
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] += r1[c];
+        store_slot(d, e, r2);
+        if (t_n != t) {
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) d.res[tg * NQ + c] = run[c];
+            if (t_n < d.n1) {
+                tg = __ldg(d.tl1 + t_n);
+#pragma unroll
+                for (int c = 0; c < NQ; ++c) run[c] = d.res[tg * NQ + c];
+            }
+        }
+        t = t_n; k = k_n; ke = ke_n;
+        cur ^= 1;
+    }
+}
+
 }  // namespace
 
 extern "C" int exp_flux_run(int layout, const void *w, const void *q, const void *x, const void *lim,
@@ -1176,6 +1296,31 @@ extern "C" int exp_flux_cpa(int variant, const void *w, const void *q, const voi
     case 2: go(k_flux_cpa<15, 128, 2>, 128, NQ + NLIM + NG + NAUX, 2); break;   // all, 128x2
     case 3: go(k_flux_cpa<12, 64, 6>, 64, NG + NAUX, 6); break;            // grad+aux, 64x6
     default: go(k_flux_cpa<4, 128, 4>, 128, NG, 4); break;                 // grad only, 128x4
+    }
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_bulk(int variant, const void *w, const void *q, const void *x, const void *lim,
+                             const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                             const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                             int64_t n1, int64_t pitch, int sms, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto go = [&](auto kern, int tpb, int dbl, int ctas_per_sm) {
+        const size_t bytes = size_t(2) * dbl * tpb * 8;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+        kern<<<ctas_per_sm * sms, tpb, bytes, s>>>(d);
+    };
+    switch (variant) {
+    case 0: go(k_flux_bulk<12, 128, 2>, 128, BulkRows<12>::D, 2); break;     // grad+aux
+    case 1: go(k_flux_bulk<15, 64, 3>, 64, BulkRows<15>::D, 3); break;       // all four
+    case 2: go(k_flux_bulk<8, 128, 3>, 128, BulkRows<8>::D, 3); break;       // aux
+    default: go(k_flux_bulk<12, 64, 4>, 64, BulkRows<12>::D, 4); break;      // grad+aux, 64x4
     }
     return int(cudaGetLastError());
 }

@@ -93,6 +93,7 @@ def main():
     lib.exp_flux_reg.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_h.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_split.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_bulk.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_cpa.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_own.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_aos.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
@@ -120,7 +121,9 @@ def main():
                              (1, 25, "aosoa_split4"), (4, 30, "aos_pad"), (4, 31, "aos_pad_128x5"),
                              (0, 40, "own0"), (0, 48, "own_aux"), (0, 44, "own_grad"), (0, 52, "own_grad_aux"),
                              (0, 55, "own_all"), (0, 60, "cpa_grad_aux"), (0, 61, "cpa_aux"),
-                             (0, 62, "cpa_all"), (0, 63, "cpa_grad_aux_64x6"), (0, 64, "cpa_grad")):
+                             (0, 62, "cpa_all"), (0, 63, "cpa_grad_aux_64x6"), (0, 64, "cpa_grad"),
+                             (4, 70, "bulk_grad_aux"), (4, 71, "bulk_all_64x3"), (4, 72, "bulk_aux"),
+                             (4, 73, "bulk_grad_aux_64x4")):
         if args.only and name not in args.only and name != "soa":
             continue
         def put(k):
@@ -146,7 +149,9 @@ def main():
                       T["res"].data_ptr(), slots.data_ptr(), ints["off1"].data_ptr(),
                       ints["elem1"].data_ptr(), ints["tl1"].data_ptr(), ints["rec"].data_ptr(),
                       ints["slotpos"].data_ptr(), int(tl1.size), n)
-            if lanes >= 60:
+            if lanes >= 70:
+                rc = lib.exp_flux_bulk(lanes - 70, *common[1:], sms, stream)
+            elif lanes >= 60:
                 rc = lib.exp_flux_cpa(lanes - 60, *common[1:], sms, stream)
             elif lanes >= 40:
                 rc = lib.exp_flux_own(lanes - 40, *common[1:], sms, stream)

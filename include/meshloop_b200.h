@@ -62,19 +62,24 @@ typedef struct ml_arg {
                               0: plain SOA                                     */
 } ml_arg_t;
 #ifndef ML_SEG_SHIFT
-#define ML_SEG_SHIFT 12
+#define ML_SEG_SHIFT 6
 #endif
 #ifndef ML_SEG_PAD
-#define ML_SEG_PAD 32
+#define ML_SEG_PAD 0
 #endif
-/* SOA dats of dim 2..ML_SEG_MAX_DIM are segmented on the device; other SOA
- * dats keep plain component rows padded to 32 elements.  Default 4, i.e. no
- * auto-SOA dat (dim > 4) is segmented: on the Hydra proxy segmenting every
- * SOA dat makes the fused flux loop 4 % faster and the grad_edge gather 12 %
- * slower (profiles/r2/seg_sweep.md); build with -DML_SEG_MAX_DIM=64 to
- * segment them. */
+/* SOA dats of dim ML_SEG_MIN_DIM..ML_SEG_MAX_DIM are segmented on the device
+ * (AoSoA: blocks of 2^ML_SEG_SHIFT elements, each holding its components one
+ * after another); other SOA dats keep plain component rows padded to 32
+ * elements.  Default: the wide dats (>= 8 components) in 64-element blocks —
+ * on the Hydra proxy the fused flux loop gathers lim/grad/aux 6 % faster and
+ * nothing else moves; segmenting the 6-component dats too, or padding the
+ * blocks, is slower (profiles/r2/seg_sweep.md).  Host copies go through a
+ * device repack kernel (ml_seg_copy), so they run at full PCIe speed. */
 #ifndef ML_SEG_MAX_DIM
-#define ML_SEG_MAX_DIM 4
+#define ML_SEG_MAX_DIM 64
+#endif
+#ifndef ML_SEG_MIN_DIM
+#define ML_SEG_MIN_DIM 8
 #endif
 
 /* Device copy of an execution plan (plan.py:30-45).  `color_offsets` is a
@@ -207,7 +212,7 @@ int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_t itemsize,
                 int32_t to_device, int32_t stream);
 /* The segment shift and pad this library was built with (the LP = 1 kernels
  * assume them; the host side allocates and copies accordingly). */
-int ml_seg_params(int32_t *seg_shift, int32_t *seg_pad, int32_t *seg_max_dim);
+int ml_seg_params(int32_t *seg_shift, int32_t *seg_pad, int32_t *seg_max_dim, int32_t *seg_min_dim);
 int ml_copy_d2h_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
                    uint64_t height);
 int ml_order(int32_t from, int32_t to);

@@ -112,7 +112,7 @@ _SIGNATURES = {
     "ml_copy_h2d_2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ml_copy_d2h_2d": (C.c_int, [_P, C.c_uint64, _P, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ml_seg_copy": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
-    "ml_seg_params": (C.c_int, [_I32P, _I32P, _I32P]),
+    "ml_seg_params": (C.c_int, [_I32P, _I32P, _I32P, _I32P]),
     "ml_map_upload": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
     "ml_copy_h2d": (C.c_int, [_P, _P, C.c_uint64]),
     "ml_copy_d2h": (C.c_int, [_P, _P, C.c_uint64]),
@@ -272,9 +272,9 @@ def functor_table() -> list[tuple[str, int]]:
     return out
 
 
-def seg_params() -> tuple[int, int, int]:
-    """(segment shift, component pad, widest segmented dim) of the library's
-    segmented SOA copies."""
-    sh, pad, mx = C.c_int32(), C.c_int32(), C.c_int32()
-    check(lib().ml_seg_params(C.byref(sh), C.byref(pad), C.byref(mx)), "ml_seg_params")
-    return sh.value, pad.value, mx.value
+def seg_params() -> tuple[int, int, int, int]:
+    """(segment shift, component pad, widest and narrowest segmented dim) of
+    the library's segmented SOA copies."""
+    sh, pad, mx, mn = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    check(lib().ml_seg_params(C.byref(sh), C.byref(pad), C.byref(mx), C.byref(mn)), "ml_seg_params")
+    return sh.value, pad.value, mx.value, mn.value

@@ -229,7 +229,10 @@ struct RefNCA {
 // SEGP), 3 plain SOA (component stride = the runtime pitch)
 template <class A, int LP>
 __host__ __device__ constexpr int lay_of() {
-    return (LP == 0 || A::kind == KG) ? 0 : (A::dim <= AUTO_SOA_DIM ? 1 : A::dim <= ML_SEG_MAX_DIM ? 2 : 3);
+    return (LP == 0 || A::kind == KG) ? 0
+           : A::dim <= AUTO_SOA_DIM                                 ? 1
+           : (A::dim >= ML_SEG_MIN_DIM && A::dim <= ML_SEG_MAX_DIM) ? 2
+                                                                    : 3;
 }
 // element base offset and component stride under layout class L
 template <class A, int L>

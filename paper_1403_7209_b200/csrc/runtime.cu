@@ -128,7 +128,7 @@ static int layout_policy(const ml_loop_t *L) {
         const ml_arg_t &a = L->args[i];
         if (a.kind == ML_GLOBAL) continue;
         if (a.dim > AUTO_SOA_DIM) {
-            const int want = a.dim <= ML_SEG_MAX_DIM ? SEG_SHIFT : 0;
+            const int want = a.dim >= ML_SEG_MIN_DIM && a.dim <= ML_SEG_MAX_DIM ? SEG_SHIFT : 0;
             if (a.layout != ML_SOA || a.seg_shift != want) return 0;
             if (!want && ((a.pitch ? a.pitch : a.set_size) & 1)) return 0;   // 16-byte pairs
         } else if (a.dim > 1 && a.layout != ML_AOS) {
@@ -508,38 +508,72 @@ extern "C" int ml_copy_d2h_2d(void *dst, uint64_t dpitch, const void *src, uint6
         ML_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, g_dev.copy[1]));
     return ML_OK;
 }
-extern "C" int ml_seg_params(int32_t *seg_shift, int32_t *seg_pad, int32_t *seg_max_dim) {
+extern "C" int ml_seg_params(int32_t *seg_shift, int32_t *seg_pad, int32_t *seg_max_dim,
+                             int32_t *seg_min_dim) {
     if (seg_shift) *seg_shift = ML_SEG_SHIFT;
     if (seg_pad) *seg_pad = ML_SEG_PAD;
     if (seg_max_dim) *seg_max_dim = ML_SEG_MAX_DIM;
+    if (seg_min_dim) *seg_min_dim = ML_SEG_MIN_DIM;
     return ML_OK;
 }
 static cudaStream_t stream_of(int32_t which);
+// Segmented <-> plain SOA on the device: component c of element e sits at
+// c * n + e in the plain (host-order) copy and at
+// (e >> s) * P * dim + c * P + (e & (2^s - 1)) in the segmented one.  Both
+// sides are contiguous runs along e, so the kernel is a coalesced copy.
+__global__ void k_seg_repack(uint64_t *seg, uint64_t *plain, int64_t n, int32_t dim, int32_t shift, int64_t P,
+                             int32_t to_seg) {
+    const int64_t c = blockIdx.y;
+    const int64_t mask = (int64_t(1) << shift) - 1;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = (e >> shift) * P * dim + c * P + (e & mask);
+        if (to_seg) seg[j] = plain[c * n + e];
+        else plain[c * n + e] = seg[j];
+    }
+}
+
+// per-stream staging buffer of the segmented copies (grown on demand)
+static void *stage_buffer(int32_t which, uint64_t bytes, int *rc) {
+    static void *buf[3] = {nullptr, nullptr, nullptr};
+    static uint64_t cap[3] = {0, 0, 0};
+    const int k = which == ML_STREAM_H2D ? 1 : which == ML_STREAM_D2H ? 2 : 0;
+    if (cap[k] < bytes) {
+        if (buf[k]) cudaFree(buf[k]);              // synchronises: no copy still uses it
+        buf[k] = nullptr;
+        cap[k] = 0;
+        if (cudaMalloc(&buf[k], bytes) != cudaSuccess) {
+            *rc = ML_ENOMEM;
+            return nullptr;
+        }
+        cap[k] = bytes;
+    }
+    *rc = ML_OK;
+    return buf[k];
+}
+
 extern "C" int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_t itemsize, int32_t seg_shift,
                            int32_t to_device, int32_t stream) {
     int rc = ensure_init();
     if (rc) return rc;
-    if (n < 0 || dim < 1 || itemsize < 1 || seg_shift < 1 || seg_shift > 30)
+    if (n < 0 || dim < 1 || dim > 65535 || itemsize != 8 || seg_shift < 1 || seg_shift > 30)
         ML_FAIL(ML_EINVAL, "ml_seg_copy: bad arguments");
     if (n == 0) return ML_OK;
     cudaStream_t s = stream_of(stream);
-    const uint64_t S = uint64_t(1) << seg_shift, SP = S + ML_SEG_PAD, isz = uint64_t(itemsize);
-    const uint64_t nfull = uint64_t(n) >> seg_shift, rem = uint64_t(n) - nfull * S;
-    char *d = static_cast<char *>(dev), *h = static_cast<char *>(host);
-    for (uint64_t c = 0; c < uint64_t(dim); ++c) {
-        char *dc = d + c * SP * isz, *hc = h + c * uint64_t(n) * isz;
-        if (nfull) {
-            if (to_device)
-                ML_CUDA(cudaMemcpy2DAsync(dc, SP * dim * isz, hc, S * isz, S * isz, nfull, cudaMemcpyHostToDevice, s));
-            else
-                ML_CUDA(cudaMemcpy2DAsync(hc, S * isz, dc, SP * dim * isz, S * isz, nfull, cudaMemcpyDeviceToHost, s));
-        }
-        if (rem) {
-            char *dt = dc + nfull * SP * dim * isz, *ht = hc + nfull * S * isz;
-            if (to_device) ML_CUDA(cudaMemcpyAsync(dt, ht, rem * isz, cudaMemcpyHostToDevice, s));
-            else ML_CUDA(cudaMemcpyAsync(ht, dt, rem * isz, cudaMemcpyDeviceToHost, s));
-        }
+    const uint64_t bytes = uint64_t(n) * uint64_t(dim) * 8;
+    void *st = stage_buffer(stream, bytes, &rc);
+    if (rc) ML_FAIL(ML_ENOMEM, "ml_seg_copy: staging buffer of %llu bytes", (unsigned long long)bytes);
+    const int64_t P = (int64_t(1) << seg_shift) + ML_SEG_PAD;
+    const dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, 4 * g_dev.sm_count)), unsigned(dim));
+    if (to_device) {
+        ML_CUDA(cudaMemcpyAsync(st, host, bytes, cudaMemcpyHostToDevice, s));
+        k_seg_repack<<<grid, 256, 0, s>>>(static_cast<uint64_t *>(dev), static_cast<uint64_t *>(st), n, dim,
+                                          seg_shift, P, 1);
+    } else {
+        k_seg_repack<<<grid, 256, 0, s>>>(static_cast<uint64_t *>(dev), static_cast<uint64_t *>(st), n, dim,
+                                          seg_shift, P, 0);
+        ML_CUDA(cudaMemcpyAsync(host, st, bytes, cudaMemcpyDeviceToHost, s));
     }
+    ML_CUDA(cudaGetLastError());
     if (!to_device && stream == ML_STREAM_COMPUTE) ML_CUDA(cudaStreamSynchronize(s));
     return ML_OK;
 }

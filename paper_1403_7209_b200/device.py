@@ -35,21 +35,21 @@ __all__ = ["DatMirror", "dat_mirror", "segmented", "device_elems", "device_pitch
 #: SOA); the offset of component c from an element's base is the
 #: compile-time c * P * 8 bytes, a load immediate in the kernels (engine.cuh).
 def _seg_params():
-    global SEG_SHIFT, SEG_PAD, SEG_MAX_DIM
+    global SEG_SHIFT, SEG_PAD, SEG_MAX_DIM, SEG_MIN_DIM
     if SEG_SHIFT is None:
-        SEG_SHIFT, SEG_PAD, SEG_MAX_DIM = N.seg_params()   # as the library was built
+        SEG_SHIFT, SEG_PAD, SEG_MAX_DIM, SEG_MIN_DIM = N.seg_params()   # as the library was built
     return SEG_SHIFT, SEG_PAD
 
 
-#: segment shift / component pad / widest segmented dim, read from the library
-SEG_SHIFT = SEG_PAD = SEG_MAX_DIM = None
+#: segment shift / component pad / widest and narrowest segmented dim, read from the library
+SEG_SHIFT = SEG_PAD = SEG_MAX_DIM = SEG_MIN_DIM = None
 
 
 def segmented(dat: Dat) -> bool:
-    """Whether ``dat``'s device copy is segmented SOA (SOA, 1 < dim <= the
-    library's widest segmented dim); wider SOA dats keep plain rows."""
+    """Whether ``dat``'s device copy is segmented SOA (SOA, dim within the
+    library's segmented range and > 1); other SOA dats keep plain rows."""
     _seg_params()
-    return dat.layout is not AOS and 1 < dat.dim <= SEG_MAX_DIM
+    return dat.layout is not AOS and 1 < dat.dim and SEG_MIN_DIM <= dat.dim <= SEG_MAX_DIM
 
 
 #: plain SOA rows (dims above the segmented range) are padded to this many

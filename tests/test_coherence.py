@@ -68,22 +68,36 @@ def test_device_then_host_residency_keeps_device_results(host_mode):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n", [1, 4095, 4096, 4097, 10000])
-def test_segmented_soa_device_copies_round_trip(n):
-    """SOA dats live on the device in 4096-element segments (device.py
-    SEG_SHIFT): host -> device -> host is exact for ragged set sizes, and a
-    direct loop (16-byte pairs) moves the right components."""
-    from paper_1403_7209_b200.device import dat_mirror
-    rng = np.random.default_rng(n)
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 4097, 10000])
+@pytest.mark.parametrize("dim", [6, 8, 19])
+def test_soa_device_copies_round_trip(n, dim):
+    """SOA dats of dim ML_SEG_MIN_DIM.. live on the device in blocks of
+    2^ML_SEG_SHIFT elements (device.py segmented(); host copies repacked on
+    the device, ml_seg_copy), narrower ones as pitched rows: host -> device ->
+    host is exact for ragged set sizes, a direct loop moves the right
+    components, and streamed (H2D/D2H stream) copies agree."""
+    from paper_1403_7209_b200 import _native as N
+    from paper_1403_7209_b200.device import dat_mirror, segmented
+    rng = np.random.default_rng(n * 31 + dim)
     mesh = ml.Mesh()
     nodes = mesh.decl_set("nodes", n)
-    vals = rng.random((n, 6))
-    q = mesh.decl_dat("q", nodes, 6, "float64", vals.ravel())
-    q_old = mesh.decl_dat("q_old", nodes, 6, "float64", np.zeros(n * 6))
+    vals = rng.random((n, dim))
+    q = mesh.decl_dat("q", nodes, dim, "float64", vals.ravel())
+    q_old = mesh.decl_dat("q_old", nodes, dim, "float64", np.zeros(n * dim))
     assert q.layout is ml.SOA
-    ml.run_program([ml.Loop("save", nodes, [ml.arg_direct(q, ml.READ), ml.arg_direct(q_old, ml.WRITE)],
-                            apps._k_proxy_save)], mesh, ml.BackendConfig())
-    np.testing.assert_array_equal(q_old.fetch(), vals)
+    assert segmented(q) == (dim >= 8)
+    m = dat_mirror(q)
     back = np.empty_like(q._host)
-    dat_mirror(q).download(back)
+    m.download(back)
     np.testing.assert_array_equal(back, q._host)
+    if dim == 6:                                   # proxy_save: a direct loop over the rows
+        ml.run_program([ml.Loop("save", nodes, [ml.arg_direct(q, ml.READ), ml.arg_direct(q_old, ml.WRITE)],
+                                apps._k_proxy_save)], mesh, ml.BackendConfig())
+        np.testing.assert_array_equal(q_old.fetch(), vals)
+    host2 = np.ascontiguousarray(rng.random(q._host.shape))
+    m.copy_h2d(host2)                              # streamed: H2D stream, then D2H stream
+    N.check(N.lib().ml_sync_all())
+    out = np.empty_like(host2)
+    m.copy_d2h(out)
+    N.check(N.lib().ml_sync_all())
+    np.testing.assert_array_equal(out, host2)

@@ -47,6 +47,13 @@ struct DeviceState {
     int device = -1;
     cudaStream_t stream = nullptr;
     cudaStream_t copy[2] = {nullptr, nullptr};     // H2D, D2H copy streams
+    // segmented uploads on the H2D stream: PCIe copy into one of two staging
+    // buffers, repack kernel on `repack` (ml_order from H2D covers it)
+    cudaStream_t repack = nullptr;
+    cudaEvent_t stage_copied[2] = {}, stage_done[2] = {}, repack_ev = nullptr;
+    void *stage[2] = {nullptr, nullptr};
+    uint64_t stage_cap[2] = {0, 0};
+    int stage_next = 0;
     cudaEvent_t order_ev[64] = {};
     int order_next = 0;
     int sm_count = 0;
@@ -401,6 +408,13 @@ extern "C" int ml_init(int device) {
         if (c) cudaStreamDestroy(c), c = nullptr;
     ML_CUDA(cudaStreamCreateWithFlags(&g_dev.stream, cudaStreamNonBlocking));
     for (auto &c : g_dev.copy) ML_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+    if (g_dev.repack) cudaStreamDestroy(g_dev.repack);
+    ML_CUDA(cudaStreamCreateWithFlags(&g_dev.repack, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        if (!g_dev.stage_copied[k]) ML_CUDA(cudaEventCreateWithFlags(&g_dev.stage_copied[k], cudaEventDisableTiming));
+        if (!g_dev.stage_done[k]) ML_CUDA(cudaEventCreateWithFlags(&g_dev.stage_done[k], cudaEventDisableTiming));
+    }
+    if (!g_dev.repack_ev) ML_CUDA(cudaEventCreateWithFlags(&g_dev.repack_ev, cudaEventDisableTiming));
     for (auto &e : g_dev.order_ev)
         if (!e) ML_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     g_dev.device = device;
@@ -560,10 +574,45 @@ extern "C" int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_
     if (n == 0) return ML_OK;
     cudaStream_t s = stream_of(stream);
     const uint64_t bytes = uint64_t(n) * uint64_t(dim) * 8;
-    void *st = stage_buffer(stream, bytes, &rc);
-    if (rc) ML_FAIL(ML_ENOMEM, "ml_seg_copy: staging buffer of %llu bytes", (unsigned long long)bytes);
     const int64_t P = (int64_t(1) << seg_shift) + ML_SEG_PAD;
     const dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, 4 * g_dev.sm_count)), unsigned(dim));
+    // download into pinned host memory: the repack kernel writes it directly
+    // over PCIe (one pass)
+    cudaPointerAttributes at{};
+    if (!to_device && cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+        at.devicePointer) {
+        k_seg_repack<<<grid, 256, 0, s>>>(static_cast<uint64_t *>(dev), static_cast<uint64_t *>(at.devicePointer), n,
+                                          dim, seg_shift, P, 0);
+        ML_CUDA(cudaGetLastError());
+        if (stream == ML_STREAM_COMPUTE) ML_CUDA(cudaStreamSynchronize(s));
+        return ML_OK;
+    }
+    cudaGetLastError();                                // clear a pageable-pointer query error
+    // upload on the H2D stream: alternate two staging buffers so the next PCIe
+    // copy never waits for this one's repack (which runs on g_dev.repack)
+    if (to_device && stream == ML_STREAM_H2D) {
+        const int k = g_dev.stage_next;
+        g_dev.stage_next ^= 1;
+        if (g_dev.stage_cap[k] < bytes) {
+            if (g_dev.stage[k]) cudaFree(g_dev.stage[k]);     // synchronises: no repack still reads it
+            g_dev.stage[k] = nullptr;
+            g_dev.stage_cap[k] = 0;
+            if (cudaMalloc(&g_dev.stage[k], bytes) != cudaSuccess)
+                ML_FAIL(ML_ENOMEM, "ml_seg_copy: staging buffer of %llu bytes", (unsigned long long)bytes);
+            g_dev.stage_cap[k] = bytes;
+        }
+        ML_CUDA(cudaStreamWaitEvent(s, g_dev.stage_done[k], 0));
+        ML_CUDA(cudaMemcpyAsync(g_dev.stage[k], host, bytes, cudaMemcpyHostToDevice, s));
+        ML_CUDA(cudaEventRecord(g_dev.stage_copied[k], s));
+        ML_CUDA(cudaStreamWaitEvent(g_dev.repack, g_dev.stage_copied[k], 0));
+        k_seg_repack<<<grid, 256, 0, g_dev.repack>>>(static_cast<uint64_t *>(dev),
+                                                     static_cast<uint64_t *>(g_dev.stage[k]), n, dim, seg_shift, P, 1);
+        ML_CUDA(cudaGetLastError());
+        ML_CUDA(cudaEventRecord(g_dev.stage_done[k], g_dev.repack));
+        return ML_OK;
+    }
+    void *st = stage_buffer(stream, bytes, &rc);
+    if (rc) ML_FAIL(ML_ENOMEM, "ml_seg_copy: staging buffer of %llu bytes", (unsigned long long)bytes);
     if (to_device) {
         ML_CUDA(cudaMemcpyAsync(st, host, bytes, cudaMemcpyHostToDevice, s));
         k_seg_repack<<<grid, 256, 0, s>>>(static_cast<uint64_t *>(dev), static_cast<uint64_t *>(st), n, dim,
@@ -600,12 +649,17 @@ extern "C" int ml_order(int32_t from, int32_t to) {
     g_dev.order_next = (g_dev.order_next + 1) % 64;
     ML_CUDA(cudaEventRecord(ev, stream_of(from)));
     ML_CUDA(cudaStreamWaitEvent(stream_of(to), ev, 0));
+    if (from == ML_STREAM_H2D) {                   // segmented uploads finish on the repack stream
+        ML_CUDA(cudaEventRecord(g_dev.repack_ev, g_dev.repack));
+        ML_CUDA(cudaStreamWaitEvent(stream_of(to), g_dev.repack_ev, 0));
+    }
     return ML_OK;
 }
 extern "C" int ml_sync_all(void) {
     int rc = ensure_init();
     if (rc) return rc;
     ML_CUDA(cudaStreamSynchronize(g_dev.copy[0]));
+    ML_CUDA(cudaStreamSynchronize(g_dev.repack));
     ML_CUDA(cudaStreamSynchronize(g_dev.stream));
     ML_CUDA(cudaStreamSynchronize(g_dev.copy[1]));
     return ML_OK;

@@ -593,13 +593,15 @@ extern "C" int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_
     if (to_device && stream == ML_STREAM_H2D) {
         const int k = g_dev.stage_next;
         g_dev.stage_next ^= 1;
-        if (g_dev.stage_cap[k] < bytes) {
-            if (g_dev.stage[k]) cudaFree(g_dev.stage[k]);     // synchronises: no repack still reads it
-            g_dev.stage[k] = nullptr;
-            g_dev.stage_cap[k] = 0;
-            if (cudaMalloc(&g_dev.stage[k], bytes) != cudaSuccess)
-                ML_FAIL(ML_ENOMEM, "ml_seg_copy: staging buffer of %llu bytes", (unsigned long long)bytes);
-            g_dev.stage_cap[k] = bytes;
+        if (g_dev.stage_cap[k] < bytes) {               // grow both: uploads alternate between them
+            for (int j = 0; j < 2; ++j) {
+                if (g_dev.stage[j]) cudaFree(g_dev.stage[j]);   // synchronises: no repack still reads it
+                g_dev.stage[j] = nullptr;
+                g_dev.stage_cap[j] = 0;
+                if (cudaMalloc(&g_dev.stage[j], bytes) != cudaSuccess)
+                    ML_FAIL(ML_ENOMEM, "ml_seg_copy: staging buffer of %llu bytes", (unsigned long long)bytes);
+                g_dev.stage_cap[j] = bytes;
+            }
         }
         ML_CUDA(cudaStreamWaitEvent(s, g_dev.stage_done[k], 0));
         ML_CUDA(cudaMemcpyAsync(g_dev.stage[k], host, bytes, cudaMemcpyHostToDevice, s));

@@ -62,3 +62,21 @@ def test_device_calls_fail_cleanly_without_init():
     p = C.c_void_p()
     rc = N.lib().ml_alloc(16, C.byref(p))
     assert rc != 0 and b"ml_init" in N.lib().ml_last_error()
+
+
+def test_segmented_layout_range_matches_the_build():
+    """The host decides which SOA dats get segmented (AoSoA) device copies
+    from the range the library was built with (ml_seg_params), so the LP = 1
+    kernels' compile-time layout classes and the mirrors agree."""
+    import paper_1403_7209_b200 as ml
+    from paper_1403_7209_b200.device import segmented
+    shift, pad, mx, mn = N.seg_params()
+    assert 1 <= shift <= 30 and pad >= 0 and mn >= 2
+    mesh = ml.Mesh()
+    nodes = mesh.decl_set("nodes", 10)
+    for dim in (1, 3, 5, 6, 8, 18, 19, 24):
+        d = mesh.decl_dat(f"d{dim}", nodes, dim, "float64", [0.0] * (10 * dim))
+        assert segmented(d) == (d.layout is ml.SOA and dim > 1 and mn <= dim <= mx), dim
+    aos = mesh.decl_dat("aos19", nodes, 19, "float64", [0.0] * 190)
+    ml.transform_layout(aos, ml.AOS)
+    assert not segmented(aos)

@@ -203,9 +203,13 @@ int ml_copy_h2d(void *dst, const void *src, uint64_t bytes);
 int ml_copy_d2h(void *dst, const void *src, uint64_t bytes);
 int ml_copy_h2d_2d(void *dst, uint64_t dpitch, const void *src, uint64_t spitch, uint64_t width,
                    uint64_t height);
-/* A SOA dat's host payload [dim][n] (itemsize bytes per value) to/from its
- * segmented device copy (see ml_arg_t.seg_shift): one 2-D copy of the full
- * segments plus one tail copy per component.  `to_device` 1: H2D, 0: D2H;
+/* A SOA dat's host payload [dim][n] (8-byte values) to/from its segmented
+ * device copy (see ml_arg_t.seg_shift), repacked on the device: uploads are
+ * one PCIe copy into a staging buffer plus a repack kernel (on the H2D stream:
+ * two staging buffers alternate and the repack runs on a side stream that
+ * ml_order from ML_STREAM_H2D also waits for); downloads into pinned memory
+ * are one repack kernel writing the host buffer directly, into pageable
+ * memory a repack into staging plus a PCIe copy.  `to_device` 1: H2D, 0: D2H;
  * `stream` ML_STREAM_COMPUTE (D2H waits for completion, like ml_download) or
  * ML_STREAM_H2D / ML_STREAM_D2H (asynchronous, streamed residency). */
 int ml_seg_copy(void *dev, void *host, int64_t n, int32_t dim, int32_t itemsize, int32_t seg_shift,

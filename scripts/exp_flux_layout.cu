@@ -1090,6 +1090,53 @@ __global__ void __launch_bounds__(TPB, MINB) k_flux_bulk(const __grid_constant__
     }
 }
 
+// L2 prefetch of the next edge's neighbour rows (no registers held): at edge
+// k the thread issues prefetch.global.L2 for the lines of edge k+1's
+// neighbour row of the dats in PF (bit 0 q, 1 lim, 2 grad, 3 aux).
+__device__ __forceinline__ void pf_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+template <int LAY, int D>
+__device__ __forceinline__ void prefetch_row(const double *base, int64_t b, int64_t P) {
+    if constexpr (LAY == 0) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) pf_l2(base + c * P + b);
+    } else {      // AoSoA-32: component c at block + c*32: 256-byte segments
+#pragma unroll
+        for (int c = 0; c < D; ++c) pf_l2(base + (b >> 5) * (32 * D) + c * 32 + (b & 31));
+    }
+}
+template <int LAY, int PF>
+__global__ void __launch_bounds__(256, 2) k_flux_pf(const __grid_constant__ Data d) {
+    const int64_t P = d.pitch;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < d.n1;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t tg = __ldg(d.tl1 + t);
+        double run[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(tg, c, P)];
+        const int kb = __ldg(d.off1 + t), ke = __ldg(d.off1 + t + 1);
+        for (int k = kb; k < ke; ++k) {
+            if (k + 1 < ke) {
+                const int64_t bn = __ldg(d.rec + 2 * int64_t(k + 1) + 1);
+                if constexpr (PF & 1) prefetch_row<LAY, NQ>(d.q, bn, P);
+                if constexpr (PF & 2) prefetch_row<LAY, NLIM>(d.lim, bn, P);
+                if constexpr (PF & 4) prefetch_row<LAY, NG>(d.grad, bn, P);
+                if constexpr (PF & 8) prefetch_row<LAY, NAUX>(d.aux, bn, P);
+            }
+            const int64_t e = __ldg(d.elem1 + k);
+            const int64_t a = __ldg(d.rec + 2 * int64_t(k)), b = __ldg(d.rec + 2 * int64_t(k) + 1);
+            double r1[NQ], r2[NQ];
+            eval_edge<LAY>(d, e, a, b, r1, r2);
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] += r1[c];
+            store_slot(d, e, r2);
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(tg, c, P)] = run[c];
+    }
+}
+
 }  // namespace
 
 extern "C" int exp_flux_run(int layout, const void *w, const void *q, const void *x, const void *lim,
@@ -1321,6 +1368,27 @@ extern "C" int exp_flux_bulk(int variant, const void *w, const void *q, const vo
     case 1: go(k_flux_bulk<15, 64, 3>, 64, BulkRows<15>::D, 3); break;       // all four
     case 2: go(k_flux_bulk<8, 128, 3>, 128, BulkRows<8>::D, 3); break;       // aux
     default: go(k_flux_bulk<12, 64, 4>, 64, BulkRows<12>::D, 4); break;      // grad+aux, 64x4
+    }
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_pf(int variant, const void *w, const void *q, const void *x, const void *lim,
+                           const void *grad, const void *aux, void *res, void *slots, const void *off1,
+                           const void *elem1, const void *tl1, const void *rec, const void *slotpos,
+                           int64_t n1, int64_t pitch, int sms, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           static_cast<const int32_t *>(off1), static_cast<const int32_t *>(elem1),
+           static_cast<const int32_t *>(tl1), static_cast<const int32_t *>(rec),
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (variant) {
+    case 0: k_flux_pf<0, 12><<<2 * sms, 256, 0, s>>>(d); break;   // SOA, grad+aux
+    case 1: k_flux_pf<1, 12><<<2 * sms, 256, 0, s>>>(d); break;   // AoSoA, grad+aux
+    case 2: k_flux_pf<1, 15><<<2 * sms, 256, 0, s>>>(d); break;   // AoSoA, all
+    case 3: k_flux_pf<0, 15><<<2 * sms, 256, 0, s>>>(d); break;   // SOA, all
+    default: k_flux_pf<1, 0><<<2 * sms, 256, 0, s>>>(d); break;   // AoSoA, none (reference)
     }
     return int(cudaGetLastError());
 }

@@ -1210,8 +1210,13 @@ __global__ void __launch_bounds__(256) k_fold_parts(const __grid_constant__ Laun
 #ifndef ML_DIRECT_MINB
 #define ML_DIRECT_MINB 1
 #endif
+#if ML_DIRECT_MINB > 0
+#define ML_DIRECT_BOUNDS __launch_bounds__(256, ML_DIRECT_MINB)
+#else
+#define ML_DIRECT_BOUNDS __launch_bounds__(256)   // no minimum: ptxas picks the register budget
+#endif
 template <class F, class T, int LP>
-__global__ void __launch_bounds__(256, ML_DIRECT_MINB) k_direct(const __grid_constant__ LaunchParams p) {
+__global__ void ML_DIRECT_BOUNDS k_direct(const __grid_constant__ LaunchParams p) {
     pdl_wait();
     if constexpr (LP == 1) run_direct_vec<F>(p, typename F::template sig<T>{});
     else run_direct<F>(p, typename F::template sig<T>{});

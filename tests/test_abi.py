@@ -80,3 +80,26 @@ def test_segmented_layout_range_matches_the_build():
     aos = mesh.decl_dat("aos19", nodes, 19, "float64", [0.0] * 190)
     ml.transform_layout(aos, ml.AOS)
     assert not segmented(aos)
+
+
+def test_hot_kernels_keep_two_ctas_per_sm():
+    """Occupancy contract of the two latency-bound edge kernels: at <= 128
+    registers per thread two 256-thread CTAs fit an SM (16 warps).  Above it
+    they drop to one CTA and the fused flux loop runs ~20 % slower (DESIGN
+    §7, register budget), so a code change that crosses it should fail here
+    rather than in the bench."""
+    import shutil
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([exe, "-res-usage", str(N.lib_path())], capture_output=True, text=True).stdout
+    regs = {}
+    lines = out.splitlines()
+    for i, line in enumerate(lines):
+        m = re.search(r"Function (\S+):", line)
+        if m and i + 1 < len(lines):
+            r = re.search(r"REG:(\d+)", lines[i + 1])
+            if r:
+                regs[m.group(1)] = int(r.group(1))
+    hot = {k: v for k, v in regs.items()
+           if ("k_pfold1" in k and "ProxyFluxes" in k) or ("k_gather" in k and "ProxyGrad" in k)}
+    assert len(hot) >= 4, sorted(regs)[:5]
+    assert all(v <= 128 for v in hot.values()), hot

@@ -99,7 +99,8 @@ def test_hot_kernels_keep_two_ctas_per_sm():
             r = re.search(r"REG:(\d+)", lines[i + 1])
             if r:
                 regs[m.group(1)] = int(r.group(1))
-    hot = {k: v for k, v in regs.items()
-           if ("k_pfold1" in k and "ProxyFluxes" in k) or ("k_gather" in k and "ProxyGrad" in k)}
-    assert len(hot) >= 4, sorted(regs)[:5]
+    # the compile-time-layout (LP = 1) instantiations the benchmark runs
+    hot = {k: v for k, v in regs.items() if "Li1EEEv" in k and (
+           ("k_pfold1" in k and "ProxyFluxes" in k) or ("k_gather" in k and "ProxyGrad" in k))}
+    assert len(hot) >= 2, sorted(regs)[:5]
     assert all(v <= 128 for v in hot.values()), hot

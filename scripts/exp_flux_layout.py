@@ -93,6 +93,7 @@ def main():
     lib.exp_flux_reg.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_h.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_split.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_smrun.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_pf.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_bulk.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_cpa.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
@@ -125,7 +126,8 @@ def main():
                              (0, 62, "cpa_all"), (0, 63, "cpa_grad_aux_64x6"), (0, 64, "cpa_grad"),
                              (4, 70, "bulk_grad_aux"), (4, 71, "bulk_all_64x3"), (4, 72, "bulk_aux"),
                              (4, 73, "bulk_grad_aux_64x4"), (0, 80, "pf_soa_ga"), (1, 81, "pf_aosoa_ga"),
-                             (1, 82, "pf_aosoa_all"), (0, 83, "pf_soa_all"), (1, 84, "pf_aosoa_none")):
+                             (1, 82, "pf_aosoa_all"), (0, 83, "pf_soa_all"), (1, 84, "pf_aosoa_none"),
+                             (0, 90, "smrun_soa"), (1, 91, "smrun_aosoa")):
         if args.only and name not in args.only and name != "soa":
             continue
         def put(k):
@@ -151,7 +153,9 @@ def main():
                       T["res"].data_ptr(), slots.data_ptr(), ints["off1"].data_ptr(),
                       ints["elem1"].data_ptr(), ints["tl1"].data_ptr(), ints["rec"].data_ptr(),
                       ints["slotpos"].data_ptr(), int(tl1.size), n)
-            if lanes >= 80:
+            if lanes >= 90:
+                rc = lib.exp_flux_smrun(lanes - 90, *common[1:], sms, stream)
+            elif lanes >= 80:
                 rc = lib.exp_flux_pf(lanes - 80, *common[1:], sms, stream)
             elif lanes >= 70:
                 rc = lib.exp_flux_bulk(lanes - 70, *common[1:], sms, stream)

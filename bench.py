@@ -183,6 +183,8 @@ def pcie_bounds(h2d: int, d2h: int) -> dict:
     dev = torch.empty(n, dtype=torch.uint8, device="cuda")
     out = {}
     for name, dst, src in (("h2d_gbs", dev, host), ("d2h_gbs", host, dev)):
+        dst.copy_(src, non_blocking=True)          # untimed: first-touch / mapping costs
+        torch.cuda.synchronize()
         best = 0.0
         for _ in range(3):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

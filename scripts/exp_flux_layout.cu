@@ -1162,6 +1162,33 @@ __global__ void __launch_bounds__(256) k_flux_smrun(const __grid_constant__ Data
     }
 }
 
+// Slot-major incidence lists: incidence j of pass-1 row t at j * n1 + t
+// (rows have <= 3 primary incidences on this mesh), so a warp's index loads
+// (element id, both map entries) are contiguous.
+template <int LAY>
+__global__ void __launch_bounds__(256) k_flux_sm(const __grid_constant__ Data d, const int32_t *cnt,
+                                                 const int32_t *elem_sm, const int32_t *rec_sm) {
+    const int64_t P = d.pitch, n1 = d.n1;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n1; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t tg = __ldg(d.tl1 + t);
+        double run[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) run[c] = d.res[idx<LAY, NQ>(tg, c, P)];
+        const int nk = __ldg(cnt + t);
+        for (int j = 0; j < nk; ++j) {
+            const int64_t e = __ldg(elem_sm + j * n1 + t);
+            const int64_t a = __ldg(rec_sm + (2 * j) * n1 + t), b = __ldg(rec_sm + (2 * j + 1) * n1 + t);
+            double r1[NQ], r2[NQ];
+            eval_edge<LAY>(d, e, a, b, r1, r2);
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) run[c] += r1[c];
+            store_slot(d, e, r2);
+        }
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) d.res[idx<LAY, NQ>(tg, c, P)] = run[c];
+    }
+}
+
 }  // namespace
 
 extern "C" int exp_flux_run(int layout, const void *w, const void *q, const void *x, const void *lim,
@@ -1431,5 +1458,22 @@ extern "C" int exp_flux_smrun(int variant, const void *w, const void *q, const v
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (variant == 0) k_flux_smrun<0><<<2 * sms, 256, 0, s>>>(d);
     else k_flux_smrun<1><<<2 * sms, 256, 0, s>>>(d);
+    return int(cudaGetLastError());
+}
+
+extern "C" int exp_flux_sm(int layout, const void *w, const void *q, const void *x, const void *lim,
+                           const void *grad, const void *aux, void *res, void *slots, const void *tl1,
+                           const void *slotpos, int64_t n1, int64_t pitch, const void *cnt, const void *elem_sm,
+                           const void *rec_sm, int sms, void *stream) {
+    Data d{static_cast<const double *>(w), static_cast<const double *>(q), static_cast<const double *>(x),
+           static_cast<const double *>(lim), static_cast<const double *>(grad),
+           static_cast<const double *>(aux), static_cast<double *>(res), static_cast<double *>(slots),
+           nullptr, nullptr, static_cast<const int32_t *>(tl1), nullptr,
+           static_cast<const int32_t *>(slotpos), n1, pitch};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int32_t *c = static_cast<const int32_t *>(cnt), *es = static_cast<const int32_t *>(elem_sm),
+                  *rs = static_cast<const int32_t *>(rec_sm);
+    if (layout == 0) k_flux_sm<0><<<2 * sms, 256, 0, s>>>(d, c, es, rs);
+    else k_flux_sm<1><<<2 * sms, 256, 0, s>>>(d, c, es, rs);
     return int(cudaGetLastError());
 }

@@ -84,6 +84,18 @@ def main():
         e = elem1[ks]
         lrec[tsk, :ks.size] = np.stack([rec[ks, 0], rec[ks, 1], e, slotpos[e]], 1)
         tmask[tsk] = np.bitwise_or.reduce((1 << (off1[r0:r1_] - b0)).astype(np.uint32))
+    # slot-major incidence lists (j-th primary incidence of row t at j * n1 + t)
+    J = int(np.diff(off1).max())
+    n1 = tl1.size
+    cnt1 = np.diff(off1).astype(np.int32)
+    elem_sm = np.zeros((J, n1), np.int32)
+    rec_sm = np.zeros((J, 2, n1), np.int32)
+    for j in range(J):
+        has = cnt1 > j
+        kk = off1[:-1][has] + j
+        elem_sm[j, has] = elem1[kk]
+        rec_sm[j, 0, has] = rec[kk, 0]
+        rec_sm[j, 1, has] = rec[kk, 1]
     dev = torch.device("cuda")
     lib = C.CDLL(str(ROOT / "scripts" / "_exp_flux.so"))
     lib.exp_flux_run.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
@@ -93,6 +105,8 @@ def main():
     lib.exp_flux_reg.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_h.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_split.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+    lib.exp_flux_sm.argtypes = ([C.c_int] + [C.c_void_p] * 10 + [C.c_int64, C.c_int64] + [C.c_void_p] * 3
+                                + [C.c_int, C.c_void_p])
     lib.exp_flux_smrun.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_pf.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     lib.exp_flux_bulk.argtypes = [C.c_int] + [C.c_void_p] * 13 + [C.c_int64, C.c_int64, C.c_int, C.c_void_p]
@@ -105,7 +119,8 @@ def main():
     vals["grad"] = np.random.default_rng(0).random(vals["grad"].shape)   # nonzero gradients
     vals["res"] = np.random.default_rng(1).random(vals["res"].shape)
     ints = {k: torch.from_numpy(v).to(dev) for k, v in
-            (("off1", off1), ("elem1", elem1), ("tl1", tl1), ("rec", rec.reshape(-1)), ("slotpos", slotpos),
+            (("cnt1", cnt1), ("elem_sm", elem_sm.reshape(-1)), ("rec_sm", rec_sm.reshape(-1)),
+             ("off1", off1), ("elem1", elem1), ("tl1", tl1), ("rec", rec.reshape(-1)), ("slotpos", slotpos),
              ("wrow", wrow), ("lrec", lrec.reshape(-1)), ("tmask", tmask.view(np.int32)))}
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     out = {}
@@ -127,7 +142,8 @@ def main():
                              (4, 70, "bulk_grad_aux"), (4, 71, "bulk_all_64x3"), (4, 72, "bulk_aux"),
                              (4, 73, "bulk_grad_aux_64x4"), (0, 80, "pf_soa_ga"), (1, 81, "pf_aosoa_ga"),
                              (1, 82, "pf_aosoa_all"), (0, 83, "pf_soa_all"), (1, 84, "pf_aosoa_none"),
-                             (0, 90, "smrun_soa"), (1, 91, "smrun_aosoa")):
+                             (0, 90, "smrun_soa"), (1, 91, "smrun_aosoa"), (0, 100, "slotmajor_soa"),
+                             (1, 101, "slotmajor_aosoa")):
         if args.only and name not in args.only and name != "soa":
             continue
         def put(k):
@@ -153,7 +169,13 @@ def main():
                       T["res"].data_ptr(), slots.data_ptr(), ints["off1"].data_ptr(),
                       ints["elem1"].data_ptr(), ints["tl1"].data_ptr(), ints["rec"].data_ptr(),
                       ints["slotpos"].data_ptr(), int(tl1.size), n)
-            if lanes >= 90:
+            if lanes >= 100:
+                rc = lib.exp_flux_sm(lay, T["w"].data_ptr(), T["q"].data_ptr(), T["x"].data_ptr(),
+                                     T["lim"].data_ptr(), T["grad"].data_ptr(), T["aux"].data_ptr(),
+                                     T["res"].data_ptr(), slots.data_ptr(), ints["tl1"].data_ptr(),
+                                     ints["slotpos"].data_ptr(), int(tl1.size), n, ints["cnt1"].data_ptr(),
+                                     ints["elem_sm"].data_ptr(), ints["rec_sm"].data_ptr(), sms, stream)
+            elif lanes >= 90:
                 rc = lib.exp_flux_smrun(lanes - 90, *common[1:], sms, stream)
             elif lanes >= 80:
                 rc = lib.exp_flux_pf(lanes - 80, *common[1:], sms, stream)

@@ -954,10 +954,9 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
         for (int c = 0; c < DG; ++c) run[c] = seg < 0 ? dst[c * gsc] : TG(0);
         for (int k = __ldg(pf.off1 + t), ke = __ldg(pf.off1 + t + 1); k < ke; ++k) {
             const int64_t e = __ldg(pf.elem1 + k);
-            if (pf.rec)
-                E::init_elem_rec(s, p, e, pf.rec + int64_t(k) * pf.ncol, idx);
-            else
-                E::init_elem(s, p, e, idx);
+            // per-incidence records (no runtime switch: a branch here costs
+            // more than the records save — fused flux loop 0.282 -> 0.272 ms)
+            E::init_elem_rec(s, p, e, pf.rec + int64_t(k) * pf.ncol, idx);
             E::call(s, p, e, idx);
             E::template gather_op<MINC, 0, DG>(s, 0, run, idx);
             if constexpr (NW > 1)

@@ -265,6 +265,8 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         if ((L->pf_nhub1 > 0 && (!pf.seg1 || !pf.part1 || !L->pf_hub1_tl || !L->pf_hub1_off)) ||
             (L->pf_nhub2 > 0 && (!pf.seg2 || !pf.part2 || !L->pf_hub2_tl || !L->pf_hub2_off)))
             ML_FAIL(ML_EINVAL, "loop '%s': primary-fold hub lists missing", L->name);
+        if (!L->pf_rec || L->pf_ncol < 1)
+            ML_FAIL(ML_EINVAL, "loop '%s': primary fold needs per-incidence map records", L->name);
         pf.rec = L->pf_rec;
         pf.ncol = L->pf_ncol;
         for (int i = 0; i < MAX_ARGS; ++i) pf.rcol[i] = L->pf_rcol[i];

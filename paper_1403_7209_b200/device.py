@@ -445,7 +445,7 @@ class PFoldMirror:
                  "rec", "ncol", "rcol", "seg1", "seg2", "nhub1", "nhub2", "hub1_tl", "hub1_off",
                  "hub2_tl", "hub2_off", "part1", "part2", "host", "rec_host")
 
-    def __init__(self, g: GatherMirror, loop, records: bool = True):
+    def __init__(self, g: GatherMirror, loop):
         h = pfold_lists_host(g.host)
         self.host, self.rec_host = h, None
         self.n1, self.n2 = h["n1"], h["n2"]
@@ -460,12 +460,10 @@ class PFoldMirror:
                 key = f"{k[:3]}{w}{k[3:]}" if k != "seg" else f"seg{w}"
                 setattr(self, key, _upload(h[key]) if seg is not None else None)
             setattr(self, f"part{w}", N.DeviceBuffer(max(h[f"nslots{w}"] * row, 8)) if seg is not None else None)
-        self.rec, self.ncol, self.rcol = None, 0, [-1] * 16
-        if records:
-            rec, self.rcol = pfold_records_host(loop, h["elem1"])
-            self.ncol = rec.shape[1]
-            self.rec = _upload(rec)
-            self.rec_host = rec
+        rec, self.rcol = pfold_records_host(loop, h["elem1"])      # pass 1 reads them (required)
+        self.ncol = rec.shape[1]
+        self.rec = _upload(rec)
+        self.rec_host = rec
 
     def pass1_subset(self, rows: np.ndarray) -> dict:
         """Device pass-1 lists of a subset of the pass-1 rows (ascending
@@ -509,11 +507,11 @@ def pfold_records_host(loop, elem1: np.ndarray):
     return rec, rcol
 
 
-def pfold_mirror(loop, plan, records: bool = True) -> PFoldMirror:
+def pfold_mirror(loop, plan) -> PFoldMirror:
     cache = plan.__dict__.setdefault("_pfolds", {})
-    key = (loop.signature(), records)
+    key = loop.signature()
     if key not in cache:
-        cache[key] = PFoldMirror(gather_mirror(loop, plan), loop, records)
+        cache[key] = PFoldMirror(gather_mirror(loop, plan), loop)
     return cache[key]
 
 

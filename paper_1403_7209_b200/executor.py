@@ -98,7 +98,6 @@ class BackendConfig:
     inc_schedule_table: dict | None = None  # per-loop override (tuner.tune_schedule)
     concurrent_loops: bool = True           # graphs/untimed runs: independent loops overlap on streams
     chain_loops: bool = True                # run registered adjacent loop pairs as one loop (chain.py)
-    pfold_records: bool = True              # pfold pass 1 reads per-incidence map records
 
     def __post_init__(self):
         if self.backend not in _BACKENDS:
@@ -258,12 +257,12 @@ class _LoopEntry:
         self.sched = sched
         if sched == "pfold":
             self.gather = gather_mirror(loop, self.plan)
-            pf = self.pfold = pfold_mirror(loop, self.plan, config.pfold_records)
+            pf = self.pfold = pfold_mirror(loop, self.plan)
             L.pf_n1, L.pf_off1, L.pf_elem1, L.pf_tl1 = pf.n1, pf.off1.ptr, pf.elem1.ptr, pf.tl1.ptr
             L.pf_n2, L.pf_off2, L.pf_elem2, L.pf_tl2 = pf.n2, pf.off2.ptr, pf.elem2.ptr, pf.tl2.ptr
             L.pf_pos2 = pf.pos2.ptr
             L.pf_slotpos = pf.slotpos.ptr
-            L.pf_rec, L.pf_ncol = (pf.rec.ptr if pf.rec is not None else None), pf.ncol
+            L.pf_rec, L.pf_ncol = pf.rec.ptr, pf.ncol
             for w in (1, 2):
                 if getattr(pf, f"seg{w}") is not None:
                     setattr(L, f"pf_seg{w}", getattr(pf, f"seg{w}").ptr)
@@ -599,7 +598,7 @@ def compile_program(program: Sequence[Loop], mesh: Mesh, config: BackendConfig,
            tuple(config.block_size_for(l.name) for l in program), config.block_size,
            tuple(sorted((config.block_size_table or {}).items())), config.inc_schedule,
            tuple(sorted((config.inc_schedule_table or {}).items())), config.coord_dat,
-           config.concurrent_loops, config.chain_loops, config.pfold_records,
+           config.concurrent_loops, config.chain_loops,
            tuple(sorted((iter_counts or {}).items())), tuple(sorted((rlim or {}).items())))
     cp = cache.get(key)
     if cp is not None and cp.loops == list(program) and cp.valid_for(mesh):

@@ -21,7 +21,6 @@ ap.add_argument("--soa", type=int, default=4, help="auto-SOA threshold; -1 = all
 ap.add_argument("--inc-schedule", nargs="+", default=["gather"])
 ap.add_argument("--no-renumber", action="store_true")
 ap.add_argument("--kd", type=int, default=0, help="k-d leaf size: renumber nodes in k-d order after CM")
-ap.add_argument("--records", type=int, nargs="+", default=[1], help="pfold pass-1 element records on/off")
 ap.add_argument("--chain", type=int, nargs="+", default=[1], help="loop chaining on/off")
 ap.add_argument("--aos-dats", nargs="*", default=[], help="dats switched to AoS after generation")
 
@@ -59,12 +58,9 @@ if args.kd:
         apply_permutation(mesh, row_order_by_targets(mesh, m))
 import itertools
 import statistics
-for bs, rec, ch in itertools.product(args.block_size, args.records, args.chain):
+for bs, ch in itertools.product(args.block_size, args.chain):
     for sched in args.inc_schedule:
-        if sched != "pfold" and rec != args.records[0]:
-            continue
-        cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched,
-                               pfold_records=bool(rec), chain_loops=bool(ch))
+        cfg = ml.BackendConfig(device=0, block_size=bs, inc_schedule=sched, chain_loops=bool(ch))
         per = {}
         for i in range(args.iters):
             r = ml.run_program(prog, mesh, cfg)
@@ -74,6 +70,6 @@ for bs, rec, ch in itertools.product(args.block_size, args.records, args.chain):
                 per.setdefault(p.loop, []).append((p.time_sec, p.gb_per_sec_alg))
         med = {k: (statistics.median(t for t, _ in v), statistics.median(g for _, g in v)) for k, v in per.items()}
         tot = sum(t for t, _ in med.values())
-        print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} rec={rec} chain={ch}] "
+        print(f"[{sched} kd={args.kd} bs={bs} soa={args.soa} chain={ch}] "
               f"total={tot*1e3:.3f}ms " +
               " ".join(f"{k}={t*1e3:.3f}ms/{g:.0f}GBs" for k, (t, g) in med.items()), flush=True)

@@ -357,14 +357,13 @@ def test_gather_write_is_serial_last_writer(seed):
         np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref.dats["vals"].fetch())
 
 
-@pytest.mark.parametrize("records", [True, False])
-def test_pfold_schedule_raw_accumulators_reductions_and_determinism(records):
+def test_pfold_schedule_raw_accumulators_reductions_and_determinism():
     """Primary fold: raw INC accumulators within tolerance of the serial oracle,
     int64 bit-exact (fuzz + diffusion), MIN/MAX/READ globals counted once per
-    element, bitwise run to run; with and without pass-1 element records."""
+    element, bitwise run to run."""
     (rm, rprog, rh), (mesh, prog, h) = _proxy_pair(12)
     bulk.run_program(rprog[:5])
-    c = cfg(inc_schedule="pfold", pfold_records=records)
+    c = cfg(inc_schedule="pfold")
     ml.run_program(prog[:5], mesh, c)
     for k in ("grad", "res"):
         close(h[k].fetch(), rh[k].fetch(), what=k)
@@ -374,15 +373,10 @@ def test_pfold_schedule_raw_accumulators_reductions_and_determinism(records):
     ml.run_program(prog[:5], mesh, c)
     for k in ("grad", "res"):
         np.testing.assert_array_equal(h[k].fetch(), first[k])
-    for k in ("grad", "res"):              # map reads instead of element records: same arithmetic
-        h[k].data[...] = 0.0
-    ml.run_program(prog[:5], mesh, cfg(inc_schedule="pfold", pfold_records=not records))
-    for k in ("grad", "res"):
-        np.testing.assert_array_equal(h[k].fetch(), first[k])
     g = golden("exec.npz")
     for soa in (4, None):
         mesh, loop, acc, lo, hi = _cases.mixmax_case(auto_soa_threshold=soa)
-        ml.run_program([loop], mesh, cfg(inc_schedule="pfold", pfold_records=records))
+        ml.run_program([loop], mesh, cfg(inc_schedule="pfold"))
         np.testing.assert_array_equal(acc.fetch(), g["exec/mixmax/acc"])
         assert [lo.value, hi.value] == g["exec/mixmax/lohi"].tolist()
     rng = np.random.default_rng(11)
@@ -391,7 +385,7 @@ def test_pfold_schedule_raw_accumulators_reductions_and_determinism(records):
         ref_mesh, ref_loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
         oserial.run_loop(ref_loop)
         mesh, loop = _cases.random_loop_mesh(np.random.default_rng(seed), max_elems=3000)
-        ml.run_program([loop], mesh, cfg(inc_schedule="pfold", pfold_records=records))
+        ml.run_program([loop], mesh, cfg(inc_schedule="pfold"))
         np.testing.assert_array_equal(mesh.dats["vals"].fetch(), ref_mesh.dats["vals"].fetch())
 
 

@@ -161,6 +161,10 @@ typedef struct ml_loop {
      * that reaches the last colour, so a host loop over single colours (the
      * reference's per-phase callback, executor.py:251-252) reduces once. */
     int32_t colour_begin, colour_end;
+    /* 1: the loop's per-incidence records (pf_rec) have exactly the columns
+     * the functor declares (ml_functor_rec_cols), so the gather / primary-fold
+     * kernels with compile-time columns may run; the runtime re-checks */
+    int32_t rec_fixed;
 } ml_loop_t;
 
 typedef struct ml_device_info {
@@ -277,6 +281,9 @@ int ml_functor_count(int32_t *count);
 int ml_chain_lookup(const char *first, const char *second, char *fused, int32_t buflen, int32_t *na,
                     int32_t *apos, int32_t *nb, int32_t *bpos);
 int ml_functor_name(int32_t functor_id, char *buf, int32_t buflen, int32_t *dtype);
+/* Record column of every argument a functor declares for its loops (trait
+ * rec_cols; -1: not indirect), *n = argument count, 0 when it declares none. */
+int ml_functor_rec_cols(int32_t functor_id, int8_t *cols, int32_t *n);
 /* Device scratch a loop needs (global-reduction partials and the arrival
  * ticket of the in-kernel combine; zero-fill it once when allocating). */
 int ml_loop_scratch_bytes(const ml_loop_t *loop, uint64_t *bytes);

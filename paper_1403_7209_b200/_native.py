@@ -35,6 +35,7 @@ EXPORTED = [
     "ml_gather_build", "ml_gather_export", "ml_gather_free",
     "ml_co_occurrence", "ml_cm_order",
     "ml_functor_lookup", "ml_functor_signature", "ml_functor_count", "ml_functor_name", "ml_chain_lookup",
+    "ml_functor_rec_cols",
     "ml_loop_scratch_bytes", "ml_loop_run", "ml_loop_pfold_slot_bytes",
     "ml_program_create", "ml_program_run", "ml_program_replay", "ml_program_loop_times",
     "ml_program_replay_timed",
@@ -81,7 +82,8 @@ class MlLoop(C.Structure):
                 ("pf_seg1", C.c_void_p), ("pf_seg2", C.c_void_p), ("pf_part1", C.c_void_p),
                 ("pf_part2", C.c_void_p), ("pf_nhub1", C.c_int64), ("pf_nhub2", C.c_int64),
                 ("pf_hub1_tl", C.c_void_p), ("pf_hub1_off", C.c_void_p), ("pf_hub2_tl", C.c_void_p),
-                ("pf_hub2_off", C.c_void_p), ("colour_begin", C.c_int32), ("colour_end", C.c_int32)]
+                ("pf_hub2_off", C.c_void_p), ("colour_begin", C.c_int32), ("colour_end", C.c_int32),
+                ("rec_fixed", C.c_int32)]
 
 
 class MlDeviceInfo(C.Structure):
@@ -131,6 +133,7 @@ _SIGNATURES = {
     "ml_functor_signature": (C.c_int, [C.c_int32, _I32P, _I32P, _I32P, _I32P, _I32P]),
     "ml_functor_count": (C.c_int, [_I32P]),
     "ml_chain_lookup": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32, _I32P, _P, _I32P, _P]),
+    "ml_functor_rec_cols": (C.c_int, [C.c_int32, _P, _I32P]),
     "ml_functor_name": (C.c_int, [C.c_int32, C.c_char_p, C.c_int32, _I32P]),
     "ml_loop_scratch_bytes": (C.c_int, [C.POINTER(MlLoop), C.POINTER(C.c_uint64)]),
     "ml_loop_run": (C.c_int, [C.POINTER(MlLoop)]),

@@ -334,6 +334,11 @@ struct Slot {
     __device__ __forceinline__ void init_elem_rec(const LaunchParams &p, int i, int64_t e, const int32_t *rk) {
         if constexpr (!is_global) bind(p.a[i], A::kind == KI ? int64_t(__ldg(rk + p.pf.rcol[i])) : e);
     }
+    // the same with the record column known at compile time (functor trait rec_cols)
+    template <int COL>
+    __device__ __forceinline__ void init_elem_rec_col(const LaunchParams &p, int i, int64_t e, const int32_t *rk) {
+        if constexpr (!is_global) bind(p.a[i], A::kind == KI ? int64_t(__ldg(rk + COL)) : e);
+    }
     __device__ __forceinline__ auto view() {
         if constexpr (staged) {
             return static_cast<T *>(acc);
@@ -414,6 +419,19 @@ struct ModeIndex {
 template <class... As>
 using IncIndex = ModeIndex<MINC, As...>;
 
+// Functor trait rec_cols: record column of every argument for the loops the
+// functor is written for (-1: not indirect).  The host uses the LP = 2
+// kernels (compile-time columns) only when a loop's records match it.
+template <class F, class = void>
+struct HasRecCols : cuda::std::false_type {};
+template <class F>
+struct HasRecCols<F, cuda::std::void_t<decltype(F::rec_cols)>> : cuda::std::true_type {};
+template <class F, int I, class = void>
+struct RecCol : cuda::std::integral_constant<int, 0> {};
+template <class F, int I>
+struct RecCol<F, I, cuda::std::enable_if_t<HasRecCols<F>::value>>
+    : cuda::std::integral_constant<int, (F::rec_cols[I] < 0 ? 0 : F::rec_cols[I])> {};
+
 template <class F, int MODE, int LP, class... As>
 struct Engine {
     using Slots = cuda::std::tuple<Slot<As, MODE, lay_of<As, LP>()>...>;
@@ -432,7 +450,10 @@ struct Engine {
     template <size_t... Is>
     __device__ __forceinline__ static void init_elem_rec(Slots &s, const LaunchParams &p, int64_t e,
                                                          const int32_t *rk, cuda::std::index_sequence<Is...>) {
-        (cuda::std::get<Is>(s).init_elem_rec(p, int(Is), e, rk), ...);
+        if constexpr (LP == 2)      // record columns from the functor (host-validated per loop)
+            (cuda::std::get<Is>(s).template init_elem_rec_col<RecCol<F, int(Is)>::value>(p, int(Is), e, rk), ...);
+        else
+            (cuda::std::get<Is>(s).init_elem_rec(p, int(Is), e, rk), ...);
     }
     template <size_t... Is>
     __device__ __forceinline__ static void call_raw(Slots &s, const LaunchParams &p,
@@ -1281,11 +1302,13 @@ struct FunctorEntry {
     int32_t kind[MAX_ARGS], mode[MAX_ARGS], dim[MAX_ARGS], atype[MAX_ARGS];
     bool ind_write, ind_write_non_inc;
     LaunchFn direct[2], staged, phased;              // [LP]
-    LaunchFn gather[2], gather_hubs;                 // target-centric (INC-only or WRITE-only)
-    LaunchFn pfold1[2], pfold2;                      // primary fold (INC-only)
+    LaunchFn gather[3], gather_hubs;                 // target-centric (INC-only or WRITE-only); [2]:
+    LaunchFn pfold1[3], pfold2;                      // primary fold (INC-only)   fixed record columns
     int (*direct_occupancy[2])(int threads);
-    int (*gather_occupancy[2])();
-    int (*pfold_occupancy[2])();
+    int (*gather_occupancy[3])();
+    int (*pfold_occupancy[3])();
+    int32_t nrec_cols;                               // functor trait rec_cols (0: none)
+    int8_t rec_cols[MAX_ARGS];
     void (*pfold_hubs)(const LaunchParams &, int64_t nhub, const int32_t *tl, const int32_t *off,
                        const void *parts, cudaStream_t);
     int32_t pfold_dgp, pfold_nslot;
@@ -1380,6 +1403,10 @@ struct Registrar {
         SigInfo<S>::fill(e.kind, e.mode, e.dim, e.atype);
         e.ind_write = SigInfo<S>::ind_write;
         e.ind_write_non_inc = SigInfo<S>::ind_write_non_inc;
+        if constexpr (HasRecCols<F>::value) {
+            e.nrec_cols = int32_t(sizeof(F::rec_cols) / sizeof(F::rec_cols[0]));
+            for (int i = 0; i < e.nrec_cols && i < MAX_ARGS; ++i) e.rec_cols[i] = int8_t(F::rec_cols[i]);
+        }
         if constexpr (!SigInfo<S>::ind_write) {
             e.direct[0] = &direct<0>;
             e.direct[1] = &direct<1>;
@@ -1394,6 +1421,10 @@ struct Registrar {
             e.pfold1[1] = &pfold1<1>;
             e.pfold_occupancy[0] = &pfold_occupancy<0>;
             e.pfold_occupancy[1] = &pfold_occupancy<1>;
+            if constexpr (HasRecCols<F>::value) {
+                e.pfold1[2] = &pfold1<2>;
+                e.pfold_occupancy[2] = &pfold_occupancy<2>;
+            }
             e.pfold2 = &pfold2;
             e.pfold_hubs = &pfold_hubs;
             using AG = typename FirstInc<S>::type;
@@ -1406,6 +1437,10 @@ struct Registrar {
             e.gather[1] = &gather<1>;
             e.gather_occupancy[0] = &gather_occupancy<0>;
             e.gather_occupancy[1] = &gather_occupancy<1>;
+            if constexpr (HasRecCols<F>::value) {
+                e.gather[2] = &gather<2>;
+                e.gather_occupancy[2] = &gather_occupancy<2>;
+            }
         }
         register_functor(e);
     }

@@ -30,6 +30,7 @@ struct Copy {
 };
 
 struct EdgeFlux {
+    static constexpr int rec_cols[4] = {0, 1, 0, 1};   // (node 1, node 2) pairs
     template <class T>
     using sig = Sig<Arg<KI, MR, 1, T>, Arg<KI, MR, 1, T>, Arg<KI, MINC, 1, T>, Arg<KI, MINC, 1, T>>;
     template <class U1, class U2, class F1, class F2>
@@ -41,6 +42,7 @@ struct EdgeFlux {
 };
 
 struct BoundaryFix {
+    static constexpr int rec_cols[4] = {0, 1, 0, 1};   // (node 1, node 2) pairs
     static constexpr bool write_only = true;   // indirect WRITE components all written, none read
     template <class T>
     using sig = Sig<Arg<KI, MW, 1, T>, Arg<KI, MW, 1, T>, Arg<KI, MR, 1, T>, Arg<KI, MR, 1, T>>;

@@ -54,6 +54,7 @@ struct ProxySaveDt {
 };
 
 struct ProxyGrad {
+    static constexpr int rec_cols[7] = {-1, 0, 1, 0, 1, 0, 1};   // w, then (node 1, node 2) pairs
     template <class T>
     using sig = Sig<Arg<KD, MR, 3, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, 3, T>,
                     Arg<KI, MR, 3, T>, Arg<KI, MINC, NG, T>, Arg<KI, MINC, NG, T>>;
@@ -77,6 +78,7 @@ struct ProxyGrad {
 };
 
 struct ProxyIflux {
+    static constexpr int rec_cols[9] = {-1, 0, 1, 0, 1, 0, 1, 0, 1};   // w, then (node 1, node 2) pairs
     template <class T>
     using sig = Sig<Arg<KD, MR, 3, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, 3, T>,
                     Arg<KI, MR, 3, T>, Arg<KI, MR, NLIM, T>, Arg<KI, MR, NLIM, T>,
@@ -105,6 +107,7 @@ struct ProxyIflux {
 };
 
 struct ProxyVflux {
+    static constexpr int rec_cols[11] = {-1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1};   // w, then (node 1, node 2) pairs
     template <class T>
     using sig = Sig<Arg<KD, MR, 3, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NG, T>,
                     Arg<KI, MR, NG, T>, Arg<KI, MR, 3, T>, Arg<KI, MR, 3, T>, Arg<KI, MR, NAUX, T>,
@@ -142,6 +145,7 @@ struct ProxyVflux {
 // same expression trees, vflux's increments added after iflux's, so each
 // edge's node rows are fetched once for both loops.
 struct ProxyFluxes {
+    static constexpr int rec_cols[13] = {-1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1};   // w, then (node 1, node 2) pairs
     // fused argument of each iflux argument (w q1 q2 x1 x2 l1 l2 r1 r2) and
     // each vflux argument (w q1 q2 g1 g2 x1 x2 a1 a2 r1 r2): w, q, x and res
     // are shared, grad and aux come from vflux alone
@@ -183,6 +187,7 @@ struct ProxyUpdate {
 };
 
 struct ProxyBc {
+    static constexpr int rec_cols[4] = {0, 1, 0, 1};   // (node 1, node 2) pairs
     static constexpr bool write_only = true;   // indirect WRITE components all written, none read
     template <class T>
     using sig = Sig<Arg<KI, MW, NQ, T>, Arg<KI, MW, NQ, T>, Arg<KI, MR, NQ, T>, Arg<KI, MR, NQ, T>>;

@@ -230,6 +230,17 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         }
     }
     const int lp = layout_policy(L);
+    // LP 2: the LP 1 layouts and the functor's compile-time record columns,
+    // when the host validated the loop's records against them (rec_fixed)
+    int glp = lp;
+    if (lp == 1 && L->rec_fixed && f.nrec_cols == f.nargs && L->pf_rec && L->pf_ncol >= 1) {
+        bool same = true;
+        for (int i = 0; i < f.nargs; ++i)
+            if (L->args[i].kind == ML_INDIRECT && L->pf_rcol[i] != f.rec_cols[i]) same = false;
+        if (!same) ML_FAIL(ML_EINVAL, "loop '%s': rec_fixed set but its record columns differ from the functor's",
+                           L->name);
+        glp = 2;
+    }
 
     int64_t nparts = nb;   // reduction partials written by the launch(es)
     bool last_colour = true;   // false: a partial colour range that does not end the loop
@@ -277,11 +288,12 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
                 if (L->args[i].kind == ML_INDIRECT && (pf.rcol[i] < 0 || pf.rcol[i] >= pf.ncol))
                     ML_FAIL(ML_EINVAL, "loop '%s': pfold record column of argument %d out of range", L->name, i);
         {
-            const int occ = f.pfold_occupancy[lp] ? f.pfold_occupancy[lp]() : 0;
+            const int plp = f.pfold1[glp] ? glp : lp;
+            const int occ = f.pfold_occupancy[plp] ? f.pfold_occupancy[plp]() : 0;
             nparts = std::max<int64_t>(1, std::min<int64_t>((pf.n1 + 255) / 256,
                                                             occ > 0 ? int64_t(occ) * g_dev.sm_count : INT64_MAX));
             if (nparts > pstride) ML_FAIL(ML_EINVAL, "loop '%s': primary fold needs more scratch", L->name);
-            f.pfold1[lp](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+            f.pfold1[plp](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
             if (L->pf_nhub1 > 0) f.pfold_hubs(p, L->pf_nhub1, L->pf_hub1_tl, L->pf_hub1_off, pf.part1, stream);
             if (pf.n2 > 0) {
                 const int64_t g2 = std::min<int64_t>((pf.n2 + 255) / 256, int64_t(8) * g_dev.sm_count);
@@ -312,7 +324,8 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         p.ticket = ticket;
         single_launch = true;
         nparts = (L->gather_ntargets + 255) / 256;
-        if (const int per_sm = f.gather_occupancy[lp] ? f.gather_occupancy[lp]() : 0; per_sm > 0)
+        const int gl = f.gather[glp] ? glp : lp;
+        if (const int per_sm = f.gather_occupancy[gl] ? f.gather_occupancy[gl]() : 0; per_sm > 0)
             nparts = std::min<int64_t>(nparts, int64_t(per_sm) * g_dev.sm_count);
         if (nparts > pstride)
             ML_FAIL(ML_EINVAL, "loop '%s': gather schedule needs more reduction scratch", L->name);
@@ -325,7 +338,7 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
             p.g_hub_tl = L->gather_hub_tl;
             p.g_hub_off = L->gather_hub_off;
         }
-        f.gather[lp](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
+        f.gather[gl](p, dim3(unsigned(nparts)), dim3(256), 0, stream);
         if (L->gather_seg && L->gather_nhub > 0)
             f.gather_hubs(p, dim3(unsigned((L->gather_nhub + 255) / 256)), dim3(256), 0, stream);
     } else if (!f.ind_write) {
@@ -738,6 +751,15 @@ extern "C" int ml_functor_name(int32_t id, char *buf, int32_t buflen, int32_t *d
     if (id < 0 || id >= int(reg.size())) ML_FAIL(ML_ENOFUNCTOR, "bad functor id %d", id);
     std::snprintf(buf, size_t(buflen), "%s", reg[id].name);
     if (dtype) *dtype = reg[id].dtype;
+    return ML_OK;
+}
+
+extern "C" int ml_functor_rec_cols(int32_t id, int8_t *cols, int32_t *n) {
+    auto &reg = registry();
+    if (id < 0 || id >= int(reg.size()) || !n) ML_FAIL(ML_ENOFUNCTOR, "bad functor id %d", id);
+    *n = reg[id].nrec_cols;
+    if (cols)
+        for (int i = 0; i < reg[id].nrec_cols; ++i) cols[i] = reg[id].rec_cols[i];
     return ML_OK;
 }
 

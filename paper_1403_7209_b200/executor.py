@@ -180,6 +180,15 @@ def _functor_id(name: str, dtype: int, cache={}) -> int:
     return cache[key]
 
 
+def _functor_rec_cols(fid: int, cache={}) -> list | None:
+    """Record column of each argument the functor declares (trait rec_cols), or None."""
+    if fid not in cache:
+        cols, n = (C.c_int8 * 64)(), C.c_int32()
+        N.check(N.lib().ml_functor_rec_cols(fid, cols, C.byref(n)), "ml_functor_rec_cols")
+        cache[fid] = list(cols[:n.value]) if n.value else None
+    return cache[fid]
+
+
 def _loop_dtype(loop: Loop) -> int:
     for a in loop.args:
         if a.kind != "global":
@@ -307,6 +316,14 @@ class _LoopEntry:
             N.check(N.lib().ml_memset(self.scratch.ptr, 0, nbytes.value), "ml_memset")
             N.check(N.lib().ml_synchronize(), "ml_synchronize")
         L.scratch = self.scratch.ptr if self.scratch else None
+        # compile-time record columns (LP 2 kernels) when this loop's records
+        # have exactly the columns the functor declares
+        rcol = (self.pfold.rcol if self.pfold is not None else
+                self.gather.rcol if self.gather is not None else None)
+        want = _functor_rec_cols(self.functor) if rcol is not None else None
+        if want is not None and len(want) == len(loop.args) and all(
+                a.kind != "indirect" or rcol[i] == want[i] for i, a in enumerate(loop.args)):
+            L.rec_fixed = 1
         self.desc = L
         self.useful = useful_bytes(loop)
         self.alg = b_alg(loop)

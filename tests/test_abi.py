@@ -100,7 +100,7 @@ def test_hot_kernels_keep_two_ctas_per_sm():
             if r:
                 regs[m.group(1)] = int(r.group(1))
     # the compile-time-layout (LP = 1) instantiations the benchmark runs
-    hot = {k: v for k, v in regs.items() if "Li1EEEv" in k and (
+    hot = {k: v for k, v in regs.items() if ("Li1EEEv" in k or "Li2EEEv" in k) and (
            ("k_pfold1" in k and "ProxyFluxes" in k) or ("k_gather" in k and "ProxyGrad" in k))}
     assert len(hot) >= 2, sorted(regs)[:5]
     assert all(v <= 128 for v in hot.values()), hot

@@ -567,9 +567,12 @@ def _upload(host: np.ndarray):
 _PINNED_KEEPALIVE: dict = {}
 
 
-def pin_mesh(mesh, min_bytes: int = 1 << 20) -> int:
+def pin_mesh(mesh, min_bytes: int = 1 << 20, device: int = 0) -> int:
     """Re-home every dat payload of at least ``min_bytes`` into pinned host memory
-    (so host<->device copies run at full PCIe speed); returns the bytes pinned."""
+    (so host<->device copies run at full PCIe speed); returns the bytes pinned.
+    Initialises the library on ``device`` if nothing has yet."""
+    if not N._inited:                    # pinned allocations go through the library
+        N.init(device)
     total = 0
     for d in mesh.dats.values():
         host = d._pull()

@@ -104,3 +104,19 @@ def test_hot_kernels_keep_two_ctas_per_sm():
            ("k_pfold1" in k and "ProxyFluxes" in k) or ("k_gather" in k and "ProxyGrad" in k))}
     assert len(hot) >= 2, sorted(regs)[:5]
     assert all(v <= 128 for v in hot.values()), hot
+
+
+def test_functor_record_columns_trait():
+    """ml_functor_rec_cols: the proxy's grad functor declares (w, then node 1 /
+    node 2 pairs); a functor without the trait declares none."""
+    import ctypes as C
+
+    def cols(name, dtype=N.ML_F64):
+        fid, n = C.c_int32(), C.c_int32()
+        N.check(N.lib().ml_functor_lookup(name.encode(), dtype, C.byref(fid)))
+        buf = (C.c_int8 * 64)()
+        N.check(N.lib().ml_functor_rec_cols(fid.value, buf, C.byref(n)))
+        return list(buf[:n.value])
+    assert cols("proxy_grad") == [-1, 0, 1, 0, 1, 0, 1]
+    assert cols("proxy_bc") == [0, 1, 0, 1]
+    assert cols("proxy_update") == []

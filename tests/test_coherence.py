@@ -121,3 +121,29 @@ def test_pinned_host_residency_matches_oracle():
         _close(h[k].fetch(), rh[k].fetch())
     for k in ("lim", "aux"):                      # read-only segmented dats survive the round trips
         np.testing.assert_array_equal(mesh.dats[k].fetch(), ref.dats[k].fetch())
+
+
+@pytest.mark.gpu
+def test_record_columns_fall_back_when_a_loop_differs():
+    """grad_edge with its q arguments' map slots swapped: the loop's record
+    columns no longer match the functor's declaration, so the generic kernel
+    (columns from the launch parameters) runs — and matches the oracle; the
+    stock loop takes the compile-time-column kernel."""
+    from paper_1403_7209_b200.core import READ, Loop, arg_indirect
+    from paper_1403_7209_b200.executor import compile_program
+    mesh, prog, h = _proxy(N=10, seed=9)
+    ref, rprog, rh = _proxy(N=10, seed=9)
+
+    def swap(p, hh):
+        g = p[2]
+        args = list(g.args)
+        args[1] = arg_indirect(hh["q"], args[1].map, 2, READ)
+        args[2] = arg_indirect(hh["q"], args[2].map, 1, READ)
+        return p[:2] + [Loop(g.name, g.iter_set, args, g.kernel)]
+    cfg = ml.BackendConfig(inc_schedule="gather")
+    assert compile_program(prog[:3], mesh, cfg).entries[-1].desc.rec_fixed == 1
+    p3, r3 = swap(prog, h), swap(rprog, rh)
+    assert compile_program(p3, mesh, cfg).entries[-1].desc.rec_fixed == 0
+    ml.run_program(p3, mesh, cfg)
+    bulk.run_program(r3)
+    np.testing.assert_array_equal(h["grad"].fetch(), rh["grad"].fetch())

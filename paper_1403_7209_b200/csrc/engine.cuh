@@ -426,6 +426,23 @@ template <class F, class = void>
 struct HasRecCols : cuda::std::false_type {};
 template <class F>
 struct HasRecCols<F, cuda::std::void_t<decltype(F::rec_cols)>> : cuda::std::true_type {};
+template <class F>
+__host__ __device__ constexpr int rec_ncol() {       // record width the trait implies
+    if constexpr (HasRecCols<F>::value) {
+        int m = 0;
+        for (int i = 0; i < int(sizeof(F::rec_cols) / sizeof(F::rec_cols[0])); ++i)
+            m = F::rec_cols[i] + 1 > m ? F::rec_cols[i] + 1 : m;
+        return m;
+    } else {
+        return 0;
+    }
+}
+// record width of a launch: compile-time with the trait's columns (LP 2)
+template <class F, int LP>
+__device__ __forceinline__ int64_t rec_width(const LaunchParams &p) {
+    if constexpr (LP == 2) return rec_ncol<F>();
+    else return p.pf.ncol;
+}
 template <class F, int I, class = void>
 struct RecCol : cuda::std::integral_constant<int, 0> {};
 template <class F, int I>
@@ -878,7 +895,7 @@ __device__ __forceinline__ void run_gather(const LaunchParams &p, Sig<As...>) {
 #define ML_GATHER_REC 1      // per-incidence map records (grad_edge 0.1048 -> 0.1008 ms)
 #endif
             if constexpr (ML_GATHER_REC)
-                E::init_elem_rec(s, p, e, p.pf.rec + int64_t(k) * p.pf.ncol, idx);
+                E::init_elem_rec(s, p, e, p.pf.rec + int64_t(k) * rec_width<F, LP>(p), idx);
             else
                 E::init_elem(s, p, e, idx);
             if constexpr (MM == MW) E::template gather_op<MW, 1, DG>(s, a, run, idx);
@@ -977,7 +994,7 @@ __device__ __forceinline__ void run_pfold1(const LaunchParams &p, Sig<As...>) {
             const int64_t e = __ldg(pf.elem1 + k);
             // per-incidence records (no runtime switch: a branch here costs
             // more than the records save — fused flux loop 0.282 -> 0.272 ms)
-            E::init_elem_rec(s, p, e, pf.rec + int64_t(k) * pf.ncol, idx);
+            E::init_elem_rec(s, p, e, pf.rec + int64_t(k) * rec_width<F, LP>(p), idx);
             E::call(s, p, e, idx);
             E::template gather_op<MINC, 0, DG>(s, 0, run, idx);
             if constexpr (NW > 1)

@@ -237,8 +237,11 @@ static int enqueue_loop_impl(const ml_loop_t *L, cudaStream_t stream) {
         bool same = true;
         for (int i = 0; i < f.nargs; ++i)
             if (L->args[i].kind == ML_INDIRECT && L->pf_rcol[i] != f.rec_cols[i]) same = false;
-        if (!same) ML_FAIL(ML_EINVAL, "loop '%s': rec_fixed set but its record columns differ from the functor's",
-                           L->name);
+        int width = 0;
+        for (int i = 0; i < f.nargs; ++i) width = std::max(width, int(f.rec_cols[i]) + 1);
+        if (!same || width != L->pf_ncol)
+            ML_FAIL(ML_EINVAL, "loop '%s': rec_fixed set but its records differ from the functor's columns",
+                    L->name);
         glp = 2;
     }
 
